@@ -1,0 +1,130 @@
+/*
+ * w2l_criterion.h -- C-ABI of the B200-native sequence-criterion library
+ * (libw2l_criterion.so): batched ASG and CTC loss+gradient and ASG/CTC
+ * Viterbi alignment on sm_100a.
+ *
+ * The reference (asrkit, /root/reference/pkg) has no FFI: its boundary for
+ * this path is the Python criterion protocol in
+ * pkg/src/asrkit/criterion.py.  Each entry point below names the reference
+ * function it replaces; the Python host layer
+ * (paper_1812_07625_b200/criterion.py) binds these symbols with ctypes and
+ * re-exports the reference's names, signatures and exception types.
+ *
+ * Conventions (all entry points):
+ *   - every array pointer is a DEVICE pointer owned by the caller; inputs are
+ *     read-only, outputs are fully overwritten (zeros in padding);
+ *   - layouts are row-major; emissions are [B][Tmax][N], targets are
+ *     int64 [B][Lmax] padded with -1 (data.py:91-99), em_len / tgt_len are
+ *     int32 [B];
+ *   - transitions are A[to][from] (criterion.py:170-171);
+ *   - scratch comes from a caller-provided workspace of *_workspace_bytes();
+ *     there are no hidden allocations and no global mutable state, so calls
+ *     on different streams are reentrant;
+ *   - work is enqueued asynchronously on `stream`; the return value reports
+ *     host-side contract violations and launch failures only.  Per-utterance
+ *     data errors land in the device array `status[B]` (codes below); call
+ *     w2l_status_first_error() to synchronise and fetch the first one.
+ */
+#ifndef W2L_CRITERION_H
+#define W2L_CRITERION_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *w2l_stream_t; /* == cudaStream_t */
+
+#if defined(__GNUC__)
+#define W2L_API __attribute__((visibility("default")))
+#else
+#define W2L_API
+#endif
+
+/* Status codes; they map 1:1 onto the reference exception classes
+ * (pkg/src/asrkit/errors.py:12-54). */
+enum {
+  W2L_OK = 0,
+  W2L_ERR_CONTRACT = 1,   /* ContractError         */
+  W2L_ERR_NUMERIC = 2,    /* NumericError          */
+  W2L_ERR_TARGET = 3,     /* TargetError           */
+  W2L_ERR_INFEASIBLE = 4, /* InfeasibleTargetError */
+  W2L_ERR_CUDA = 5,       /* launch / runtime failure */
+  W2L_ERR_COMM = 6        /* collective failure (multi-GPU layer) */
+};
+
+/* Library limits of the sm_100a kernels. */
+#define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */
+#define W2L_MAX_ASG_LABELS 1024  /* Lmax for ASG (32 lanes x 32 states)        */
+#define W2L_MAX_CTC_LABELS 511   /* Lmax for CTC (2L+1 <= 1024 lattice states) */
+
+/* ------------------------------------------------------------------ ASG --
+ * Replaces asg_loss_grad (criterion.py:167-247), batched.
+ *   loss[B]            f64  per-utterance loss  (fcc score - fac score)
+ *   grad_em[B,Tmax,N]  f32  d loss_b / d emissions_b
+ *   grad_trans[N,N]    f32  sum over utterances of d loss_b / d A
+ *                           (trainer.py:417-418; the /B stays with the caller)
+ *   grad_trans_utt     f32  [B,N,N] per-utterance d loss_b / d A, or NULL
+ * fp32 arithmetic (scaled linear domain, exact power-of-two rescaling) with a
+ * per-utterance self-consistency guard; utterances that fail the guard are
+ * recomputed by the float64 log-domain kernel inside the same call. */
+W2L_API size_t w2l_asg_workspace_bytes(int B, int Tmax, int N, int Lmax);
+W2L_API int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
+                      int Lmax, double *loss, float *grad_em, float *grad_trans,
+                      float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                      w2l_stream_t stream);
+/* float64-input variant computed entirely by the float64 log-domain kernel:
+ * the reference's own numerics ("float64 internals", criterion.py:1-7). */
+W2L_API size_t w2l_asg_workspace_bytes_f64(int B, int Tmax, int N, int Lmax);
+W2L_API int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, const double *trans, int B, int Tmax,
+                          int N, int Lmax, double *loss, float *grad_em, float *grad_trans,
+                          float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                          w2l_stream_t stream);
+
+/* ------------------------------------------------------------------ CTC --
+ * Replaces ctc_loss_grad (criterion.py:84-162), batched.  Emissions are
+ * log-probabilities; rows must satisfy |logsumexp| <= 1e-2. */
+W2L_API size_t w2l_ctc_workspace_bytes(int B, int Tmax, int N, int Lmax);
+W2L_API int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
+                      double *loss, float *grad_em, int32_t *status, void *ws,
+                      size_t ws_bytes, w2l_stream_t stream);
+W2L_API size_t w2l_ctc_workspace_bytes_f64(int B, int Tmax, int N, int Lmax);
+W2L_API int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, int blank, int B, int Tmax, int N,
+                          int Lmax, double *loss, float *grad_em, int32_t *status, void *ws,
+                          size_t ws_bytes, w2l_stream_t stream);
+
+/* -------------------------------------------------------------- Viterbi --
+ * Replaces viterbi (criterion.py:259-284), batched.  float64 max-plus in the
+ * reference's operation order (bit-exact paths and scores); ties go to the
+ * lowest id.  trans may be NULL (zeros, the CTC viterbi_path at :334-336).
+ *   path[B,Tmax] int64 (zero padded), score[B] f64. */
+W2L_API size_t w2l_viterbi_workspace_bytes(int B, int Tmax, int N);
+W2L_API int w2l_viterbi(const float *em, const int32_t *em_len, const float *trans, int B, int Tmax,
+                int N, int64_t *path, double *score, int32_t *status, void *ws,
+                size_t ws_bytes, w2l_stream_t stream);
+W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const double *trans, int B,
+                    int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
+                    size_t ws_bytes, w2l_stream_t stream);
+
+/* ------------------------------------------------------------ utilities -- */
+/* Synchronises `stream`, copies status[B] to the host and returns the first
+ * non-zero code (W2L_OK if none); *bad_index receives its utterance or -1. */
+W2L_API int w2l_status_first_error(const int32_t *status, int B, int32_t *bad_index,
+                           w2l_stream_t stream);
+W2L_API const char *w2l_status_string(int code);
+/* Library build identifier (kernel generation), for provenance in benches. */
+W2L_API const char *w2l_version(void);
+/* Microbenchmarks used for the roofline denominators (MUFU ex2 ops/s and
+ * FP64 add ops/s), measured on the current device. */
+W2L_API int w2l_probe_peaks(double *mufu_ops_per_s, double *dadd_ops_per_s, double *ffma_ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* W2L_CRITERION_H */

@@ -1,0 +1,686 @@
+// fp32 batched ASG loss + gradient (replaces criterion.py:167-247 for the
+// batched hot path).
+//
+// Algorithm: the four ASG recursions are run in the SCALED LINEAR domain,
+// the standard exact reformulation of log-space forward-backward
+//     alpha_t = Et (.) (M alpha_{t-1}) * 2^-k_t ,   M = exp(A - max A),
+//     Et[i]   = exp(e[t][i] - max_i e[t][i]),
+// with exact power-of-two rescaling (only integer exponents accumulate, no
+// rounding in the scale factors).  The fcc (fully connected, N x N) graph is
+// a 32-lane mat-vec per frame with the previous vector broadcast through
+// shared memory; the fac (forced alignment, L-state chain) graph keeps SPL
+// states per lane in registers with a per-lane power-of-two exponent
+// (block floating point) and a single shuffle per frame to the neighbour.
+// No transcendental sits on the recursion's critical path.
+//
+// Kernels (one stream, in order):
+//   asg_csr      per utterance: states grouped by token (for the emissions
+//                gradient scatter), written to the workspace.
+//   asg_chain    grid (B, 4): fcc-alpha, fcc-beta, fac-alpha, fac-beta; one
+//                warp each; rows of alpha/beta and exponents to workspace.
+//   asg_grad     grid (frame blocks, B): 8 warps, one frame per warp at a time:
+//                posteriors (per-frame normaliser Z_t), grad_e, partial
+//                transition gradients, and the consistency guard G_t.
+//   asg_final    per utterance: loss, grad_A_b, guard verdict -> either OK or
+//                kNeedsExact (then the float64 kernel recomputes it).
+// Reference correspondence: fac alpha/beta = criterion.py:193-212, fac
+// posteriors = :214-224, fcc = :227-241, combine = :243-247.
+
+#include "chunk.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace w2l {
+namespace {
+
+constexpr int kGradFramesPerBlock = 64;
+constexpr int kGradWarps = 8;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float trans_max(const float *trans, int N) {
+  float m = -CUDART_INF_F;
+  for (int p = threadIdx.x & 31; p < N * N; p += 32) m = fmaxf(m, trans[p]);
+  return warp_max(m);
+}
+
+// ------------------------------------------------------------ token CSR --
+// perm lists the chain states grouped by token (ascending state order inside
+// a token), tok_start[k]..tok_start[k+1] its range.  state_mul/off map a
+// target position l to its chain state (ASG: l; CTC: 2l+1).
+__global__ void token_csr_kernel(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
+                                 int state_mul, int state_off, int *perm, int *tok_start,
+                                 const int32_t *status) {
+  const int b = blockIdx.x;
+  __shared__ int cnt[33];
+  if (status[b] != W2L_OK) return;
+  const int L = tgt_len[b];
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[(int)y[l]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k <= d.N; ++k) {
+      const int c = k < d.N ? cnt[k] : 0;
+      tok_start[b * 33 + k] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    const int tk = (int)y[l];
+    int before = 0;
+    for (int q = 0; q < l; ++q) before += (y[q] == tk);
+    perm[(size_t)b * lpad + tok_start[b * 33 + tk] + before] = l * state_mul + state_off;
+  }
+}
+
+// ---------------------------------------------------------- chain kernel --
+template <int SPL>
+__global__ void __launch_bounds__(32)
+    asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                     const float *__restrict__ trans, Dims d, AsgFastWs w,
+                     const int32_t *__restrict__ status) {
+  __shared__ __align__(16) float chunk[2 * kChunk * 33];
+  __shared__ __align__(16) float vec[2][32];
+  const int b = blockIdx.x, role = blockIdx.y, lane = threadIdx.x;
+  if (status[b] != W2L_OK) return;
+  const int T = em_len[b], N = d.N;
+  const float amax = trans_max(trans, N);
+  const bool fwd = (role == 0 || role == 2);
+  EmissionPipe pipe;
+  pipe.init(chunk, em + (size_t)b * d.Tmax * N, T, N, fwd);
+  const size_t row0 = (size_t)b * d.Tmax;
+
+  if (role == 0) {
+    // ---- fcc alpha: lane i, row i of M in registers
+    float mr[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      mr[j] = (lane < N && j < N) ? expf(trans[lane * N + j] - amax) : 0.f;
+    float a = lane < N ? pipe.row(0)[lane] : 0.f;
+    int K = 0;
+    vec[0][lane] = a;
+    w.fcc_a[row0 * 32 + lane] = a;
+    if (lane == 0) w.fcc_ka[row0] = 0;
+    for (int t = 1; t < T; ++t) {
+      const float et = lane < N ? pipe.row(t)[lane] : 0.f;
+      __syncwarp();
+      const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
+      float acc[8], sm[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = pv[q];
+        acc[q] = mr[4 * q] * x.x;
+        acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
+        acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
+        acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
+        sm[q] = (x.x + x.y) + (x.z + x.w);
+      }
+      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+      const int k = max(-126, min(126, exponent_of(tot)));
+      K += k;
+      a = et * (s * pow2f(-k));
+      vec[t & 1][lane] = a;
+      w.fcc_a[(row0 + t) * 32 + lane] = a;
+      if (lane == 0) w.fcc_ka[row0 + t] = K;
+    }
+    const float z = warp_sum(a);
+    if (lane == 0) w.scal[b * 4 + 0] = log((double)z) + (double)K * 0.6931471805599453;
+  } else if (role == 1) {
+    // ---- fcc beta' (excludes frame t's emission): lane j, column j of M
+    float mc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      mc[i] = (lane < N && i < N) ? expf(trans[i * N + lane] - amax) : 0.f;
+    float bb = lane < N ? 1.f : 0.f;
+    int K = 0;
+    w.fcc_b[(row0 + T - 1) * 32 + lane] = bb;
+    if (lane == 0) w.fcc_kb[row0 + T - 1] = 0;
+    for (int u = T - 1; u >= 1; --u) {
+      const float eu = lane < N ? pipe.row(u)[lane] : 0.f;
+      vec[u & 1][lane] = eu * bb;
+      __syncwarp();
+      const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
+      float acc[8], sm[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = pv[q];
+        acc[q] = mc[4 * q] * x.x;
+        acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
+        acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
+        acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
+        sm[q] = (x.x + x.y) + (x.z + x.w);
+      }
+      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+      const int k = max(-126, min(126, exponent_of(tot)));
+      K += k;
+      bb = s * pow2f(-k);
+      w.fcc_b[(row0 + u - 1) * 32 + lane] = bb;
+      if (lane == 0) w.fcc_kb[row0 + u - 1] = K;
+    }
+    const float e0 = lane < N ? pipe.row(0)[lane] : 0.f;
+    const float z = warp_sum(e0 * bb);
+    if (lane == 0) w.scal[b * 4 + 1] = log((double)z) + (double)K * 0.6931471805599453;
+  } else {
+    // ---- fac chains: state l = lane*SPL + k, per-lane power-of-two exponent
+    const int L = tgt_len[b];
+    const int64_t *y = tgt + (size_t)b * d.Lmax;
+    int tok[SPL];
+    float S[SPL], P[SPL];
+    const bool is_alpha = (role == 2);
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const int l = lane * SPL + k;
+      if (l < L) {
+        const int yl = (int)y[l];
+        tok[k] = yl;
+        S[k] = expf(trans[yl * N + yl] - amax);
+        if (is_alpha) {
+          P[k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
+        } else {  // beta uses the step weight INTO the next state
+          P[k] = l + 1 < L ? expf(trans[(int)y[l + 1] * N + yl] - amax) : 0.f;
+        }
+      } else {
+        tok[k] = N;  // zero column
+        S[k] = 0.f;
+        P[k] = 0.f;
+      }
+    }
+    float v[SPL];
+    int ex = 0;
+    float *out = is_alpha ? w.fac_a : w.fac_b;
+    int *oute = is_alpha ? w.fac_ea : w.fac_eb;
+    const int lp = w.lpad;
+    
+    
+    if (is_alpha) {
+      // t = 0: only the first target state is reachable (:194)
+      const float *r0 = pipe.row(0);
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) v[k] = 0.f;
+      ex = 0;
+      if (lane == 0) v[0] = r0[tok[0]];
+      lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, 0);
+      for (int t = 1; t < T; ++t) {
+        const float *r = pipe.row(t);
+        float E[SPL];
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) E[k] = r[tok[k]];
+        float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
+        int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
+        if (lane == 0) {
+          nb = 0.f;
+          nbe = kNegExp;
+        }
+        int dd = nbe - ex;
+        if (dd > 64) {  // neighbour dominates: rebase this lane to its exponent
+          const float sc = pow2f(-dd);
+#pragma unroll
+          for (int k = 0; k < SPL; ++k) v[k] *= sc;
+          ex = nbe;
+          dd = 0;
+        }
+        const float nbs = nb * pow2f(dd);
+#pragma unroll
+        for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
+        v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
+        lane_renorm<SPL>(v, ex);
+        lane_store<SPL>(v, ex, out, oute, row0, lp, lane, t);
+      }
+      // fac score = alpha_{T-1}[L-1] (:203)
+      const int lastl = L - 1;
+      if (lane == lastl / SPL) {
+        float vl = 0.f;
+#pragma unroll
+        for (int k = 0; k < SPL; ++k)
+          if (k == lastl % SPL) vl = v[k];
+        w.scal[b * 4 + 2] = log((double)vl) + (double)ex * 0.6931471805599453;
+      }
+    } else {
+      // beta'_{T-1} = 1 on the last target state, 0 elsewhere
+      const int lastl = L - 1;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
+      ex = (lane == lastl / SPL) ? 0 : kNegExp;
+      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, T - 1);
+      for (int u = T - 1; u >= 1; --u) {
+        const float *r = pipe.row(u);
+        float wv[SPL];
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) wv[k] = r[tok[k]] * v[k];
+        float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
+        int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
+        if (lane == 31) {
+          nb = 0.f;
+          nbe = kNegExp;
+        }
+        int dd = nbe - ex;
+        if (dd > 64) {
+          const float sc = pow2f(-dd);
+#pragma unroll
+          for (int k = 0; k < SPL; ++k) wv[k] *= sc;
+          ex = nbe;
+          dd = 0;
+        }
+        const float nbs = nb * pow2f(dd);
+#pragma unroll
+        for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
+        v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
+        lane_renorm<SPL>(v, ex);
+        lane_store<SPL>(v, ex, out, oute, row0, lp, lane, u - 1);
+      }
+      const float *r0 = pipe.row(0);
+      if (lane == 0) {
+        const float z = r0[tok[0]] * v[0];
+        w.scal[b * 4 + 3] = log((double)z) + (double)ex * 0.6931471805599453;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- grad kernel --
+template <int SPL>
+__global__ void __launch_bounds__(kGradWarps * 32)
+    asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                    const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                    const float *__restrict__ trans, Dims d, AsgFastWs w,
+                    float *__restrict__ grad_em, const int32_t *__restrict__ status) {
+  constexpr int LP = SPL * 32;
+  extern __shared__ __align__(16) float gsm[];
+  float *red = gsm;                              // [kGradWarps][32*32] fullA partials
+  float *redE = red + kGradWarps * 1024;         // [kGradWarps][2][LP] edge partials
+  float *prow = redE + kGradWarps * 2 * LP;      // [kGradWarps][LP] posterior row
+  float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
+  float *vrow = erow + kGradWarps * 64;          // [kGradWarps][32] alpha_{t-1} fcc row
+  float *gwarp = vrow + kGradWarps * 32;         // [kGradWarps][4] guard
+
+  const int b = blockIdx.y, blk = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = d.N;
+  const int T = em_len[b];
+  const int t0 = blk * kGradFramesPerBlock;
+  const bool ok = status[b] == W2L_OK;
+  float *ge = grad_em + (size_t)b * d.Tmax * N;
+  const int fpw = kGradFramesPerBlock / kGradWarps;
+  const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
+
+  // rows outside the utterance (or a failed utterance) get zero gradient
+  for (int t = ta; t < tb; ++t)
+    if (!ok || t >= T)
+      if (lane < N) ge[(size_t)t * N + lane] = 0.f;
+  if (!ok) return;
+  if (t0 >= T) {
+    // keep the partial buffers well-defined for the final reduction
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+      w.part_fullA[((size_t)b * w.nblk + blk) * 1024 + i] = 0.f;
+    for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x)
+      w.part_edge[((size_t)b * w.nblk + blk) * 2 * LP + i] = 0.f;
+    if (threadIdx.x < 4)
+      w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] =
+          (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
+    return;
+  }
+
+  const int L = tgt_len[b];
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  const float amax = trans_max(trans, N);
+  int tok[SPL];
+  float S[SPL], P[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    const int l = lane * SPL + k;
+    if (l < L) {
+      const int yl = (int)y[l];
+      tok[k] = yl;
+      S[k] = expf(trans[yl * N + yl] - amax);
+      P[k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
+    } else {
+      tok[k] = N;
+      S[k] = 0.f;
+      P[k] = 0.f;
+    }
+  }
+  const int *perm = w.perm + (size_t)b * w.lpad;
+  const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
+  const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
+
+  float accA[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) accA[j] = 0.f;
+  float accS[SPL], accP[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) accS[k] = accP[k] = 0.f;
+  // guard: deviation (log2 units) of every frame's normaliser from the
+  // forward totals the chain kernel produced
+  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
+  const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
+  float gminF = CUDART_INF_F, gmaxF = -CUDART_INF_F, gminC = CUDART_INF_F,
+        gmaxC = -CUDART_INF_F;
+
+  float *myp = prow + warp * LP;
+  float *mye = erow + warp * 64;
+  float *myv = vrow + warp * 32;
+  const size_t row0 = (size_t)b * d.Tmax;
+  const int tend = min(tb, T);
+
+  // fac alpha at t-1 (values and lane exponent) carried across frames
+  float pa[SPL];
+  int pea = kNegExp;
+  float pfa = 0.f;  // fcc alpha_{t-1}[lane]
+  int pka = 0;
+  if (ta >= 1 && ta < tend) {
+    const float *o = w.fac_a + (row0 + ta - 1) * LP;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) pa[k] = o[k * 32 + lane];
+    pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
+    pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
+    pka = w.fcc_ka[row0 + ta - 1];
+  }
+
+  for (int t = ta; t < tend; ++t) {
+    // ---- emissions of frame t, shifted and exponentiated (same as the chain)
+    const float et = shifted_prob(em + (row0 + t) * N, N, lane, nullptr);
+    mye[lane] = et;
+    if (lane == 0) mye[32] = 0.f;  // token id N == zero column only if N == 32
+    mye[N] = 0.f;
+    // ---- fcc node posteriors (:238)
+    const float fa = w.fcc_a[(row0 + t) * 32 + lane];
+    const float fb = w.fcc_b[(row0 + t) * 32 + lane];
+    const int ka = w.fcc_ka[row0 + t];
+    const int kb = w.fcc_kb[row0 + t];
+    const float gam = fa * fb;
+    const float zf = warp_sum(gam);
+    const float inv_zf = 1.f / zf;
+    const float gF = (float)((double)__log2f(zf) + (double)(ka + kb) - refF);
+    gminF = fminf(gminF, gF);
+    gmaxF = fmaxf(gmaxF, gF);
+    const float full_e = gam * inv_zf;
+    // ---- fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j], times M later
+    if (t >= 1) {
+      myv[lane] = pfa;
+      __syncwarp();
+      const float u = et * fb * pow2f(pka - ka) * inv_zf;
+      const float4 *pv = reinterpret_cast<const float4 *>(myv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = pv[q];
+        accA[4 * q] = fmaf(u, x.x, accA[4 * q]);
+        accA[4 * q + 1] = fmaf(u, x.y, accA[4 * q + 1]);
+        accA[4 * q + 2] = fmaf(u, x.z, accA[4 * q + 2]);
+        accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
+      }
+    }
+    // ---- fac node posteriors (:214-217)
+    float va[SPL], vb[SPL];
+    const float *oa = w.fac_a + (row0 + t) * LP;
+    const float *ob = w.fac_b + (row0 + t) * LP;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      va[k] = oa[k * 32 + lane];
+      vb[k] = ob[k * 32 + lane];
+    }
+    const int ea = w.fac_ea[(row0 + t) * 32 + lane];
+    const int eb = w.fac_eb[(row0 + t) * 32 + lane];
+    const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
+    const int es = alive ? ea + eb : kNegExp;
+    const int estar = warp_max(es);
+    const float sc = alive ? pow2f(es - estar) : 0.f;
+    float zl = 0.f;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const float p = va[k] * vb[k] * sc;
+      myp[lane * SPL + k] = p;
+      zl += p;
+    }
+    const float zc = warp_sum(zl);
+    const float inv_zc = 1.f / zc;
+    const float gC = (float)((double)__log2f(zc) + (double)estar - refC);
+    gminC = fminf(gminC, gC);
+    gmaxC = fmaxf(gmaxC, gC);
+    __syncwarp();
+    // token gather: lane k sums the posteriors of the states labelled k
+    float con = 0.f;
+    for (int q = ts0; q < ts1; ++q) con += myp[perm[q]];
+    if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
+    // ---- fac edge posteriors (:218-224)
+    if (t >= 1) {
+      const float nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
+      const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
+      const float base = pow2f(pea + eb - estar) * inv_zc;
+      const float nbase = (lane > 0) ? pow2f(nbe + eb - estar) * inv_zc : 0.f;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        const float ev = mye[tok[k]] * vb[k];
+        accS[k] = fmaf(pa[k] * S[k], ev * base, accS[k]);
+        const float prev = k > 0 ? pa[k - 1] * base : nbv * nbase;
+        accP[k] = fmaf(prev * P[k], ev, accP[k]);
+      }
+    }
+    // carry alpha_t as alpha_{t-1} for the next frame
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) pa[k] = va[k];
+    pea = ea;
+    pfa = fa;
+    pka = ka;
+    __syncwarp();
+  }
+
+  // ---- block reduction of the partials in fixed warp order (deterministic)
+  float *rA = red + warp * 1024;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) rA[lane * 32 + j] = accA[j];
+  float *rE = redE + warp * 2 * LP;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    rE[lane * SPL + k] = accS[k];
+    rE[LP + lane * SPL + k] = accP[k];
+  }
+  if (lane == 0) {
+    gwarp[warp * 4 + 0] = gminF;
+    gwarp[warp * 4 + 1] = gmaxF;
+    gwarp[warp * 4 + 2] = gminC;
+    gwarp[warp * 4 + 3] = gmaxC;
+  }
+  __syncthreads();
+  float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < kGradWarps; ++q) s += red[q * 1024 + i];
+    dstA[i] = s;
+  }
+  float *dstE = w.part_edge + ((size_t)b * w.nblk + blk) * 2 * LP;
+  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < kGradWarps; ++q) s += redE[q * 2 * LP + i];
+    dstE[i] = s;
+  }
+  if (threadIdx.x < 4) {
+    float g = (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
+    for (int q = 0; q < kGradWarps; ++q) {
+      const float v = gwarp[q * 4 + threadIdx.x];
+      g = (threadIdx.x & 1) ? fmaxf(g, v) : fminf(g, v);
+    }
+    w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
+  }
+}
+
+// ---------------------------------------------------------- final kernel --
+__global__ void asg_final_kernel(const int64_t *__restrict__ tgt,
+                                 const int32_t *__restrict__ tgt_len,
+                                 const int32_t *__restrict__ em_len,
+                                 const float *__restrict__ trans, Dims d, AsgFastWs w,
+                                 double *loss, float *ga_utt, int32_t *status) {
+  const int b = blockIdx.x;
+  __shared__ float sEdge[2 * 1024];
+  __shared__ int sy[1024];
+  __shared__ int s_bad;
+  if (status[b] != W2L_OK) {
+    for (int p = threadIdx.x; p < d.N * d.N; p += blockDim.x) ga_utt[(size_t)b * d.N * d.N + p] = 0.f;
+    return;
+  }
+  const int N = d.N, L = tgt_len[b], T = em_len[b], LP = w.lpad;
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  float amax = -CUDART_INF_F;
+  for (int p = 0; p < N * N; ++p) amax = fmaxf(amax, trans[p]);
+  for (int l = threadIdx.x; l < L; l += blockDim.x) sy[l] = (int)y[l];
+  // per-state edge sums over frame blocks (fixed order)
+  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < w.nblk; ++q) s += w.part_edge[((size_t)b * w.nblk + q) * 2 * LP + i];
+    sEdge[i] = s;
+  }
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < N * N; p += blockDim.x) {
+    const int i = p / N, j = p % N;
+    float s = 0.f;
+    for (int q = 0; q < w.nblk; ++q) s += w.part_fullA[((size_t)b * w.nblk + q) * 1024 + i * 32 + j];
+    const float full = s * expf(trans[p] - amax);
+    float con = 0.f;
+    for (int l = 0; l < L; ++l) {
+      if (sy[l] == i && sy[l] == j) con += sEdge[l];
+      if (l > 0 && sy[l] == i && sy[l - 1] == j) con += sEdge[LP + l];
+    }
+    ga_utt[(size_t)b * N * N + p] = full - con;
+  }
+  // guard: every frame's normaliser must reproduce the forward total
+  const double ln2 = 0.6931471805599453;
+  const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
+  const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
+  const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
+  int bad = !(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb));
+  bad |= fabs(zF - zFb) > tol || fabs(zC - zCb) > tol;
+  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
+  for (int q = threadIdx.x; q < nb_used; q += blockDim.x) {
+    const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 4;
+    bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
+    bad |= !(fabs((double)g[2]) * ln2 <= tol && fabs((double)g[3]) * ln2 <= tol);
+  }
+  if (bad) atomicOr(&s_bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    loss[b] = zF - zC;
+    if (s_bad) status[b] = kNeedsExact;
+  }
+}
+
+template <int SPL>
+cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
+                       const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
+                       float *grad_em, const int32_t *status, cudaStream_t s) {
+  asg_chain_kernel<SPL><<<dim3(d.B, 4), 32, 0, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
+                                                     status);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  constexpr int LP = SPL * 32;
+  const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4));
+  auto k = asg_grad_kernel<SPL>;
+  err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  k<<<dim3(w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
+                                                      grad_em, status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int asg_fast_spl(int Lmax) {
+  static const int opts[] = {2, 4, 8, 10, 12, 16, 20, 24, 32};
+  for (int o : opts)
+    if (32 * o >= Lmax) return o;
+  return 0;
+}
+
+cudaError_t launch_token_csr(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
+                             int state_mul, int state_off, int *perm, int *tok_start,
+                             const int32_t *status, cudaStream_t s) {
+  token_csr_kernel<<<d.B, 256, 0, s>>>(tgt, tgt_len, d, lpad, state_mul, state_off, perm,
+                                       tok_start, status);
+  return cudaGetLastError();
+}
+
+static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
+  const int spl = asg_fast_spl(d.Lmax);
+  const int lpad = spl * 32;
+  const int nblk = (d.Tmax + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
+  const size_t BT = (size_t)d.B * d.Tmax;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return base ? (void *)((char *)base + o) : nullptr;
+  };
+  AsgFastWs t;
+  t.fcc_a = (float *)take(BT * 32 * 4);
+  t.fcc_b = (float *)take(BT * 32 * 4);
+  t.fcc_ka = (int *)take(BT * 4);
+  t.fcc_kb = (int *)take(BT * 4);
+  t.fac_a = (float *)take(BT * lpad * 4);
+  t.fac_b = (float *)take(BT * lpad * 4);
+  t.fac_ea = (int *)take(BT * 32 * 4);
+  t.fac_eb = (int *)take(BT * 32 * 4);
+  t.scal = (double *)take((size_t)d.B * 4 * 8);
+  t.part_fullA = (float *)take((size_t)d.B * nblk * 1024 * 4);
+  t.part_edge = (float *)take((size_t)d.B * nblk * 2 * lpad * 4);
+  t.part_guard = (float *)take((size_t)d.B * nblk * 4 * 4);
+  t.perm = (int *)take((size_t)d.B * lpad * 4);
+  t.tok_start = (int *)take((size_t)d.B * 33 * 4);
+  t.spl = spl;
+  t.lpad = lpad;
+  t.nblk = nblk;
+  if (w) *w = t;
+  return off;
+}
+
+size_t asg_fast_ws_bytes(Dims d) { return asg_ws_layout(d, nullptr, nullptr); }
+void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w) { asg_ws_layout(d, ws, w); }
+
+cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, const float *trans, Dims d,
+                            const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
+                            int32_t *status, cudaStream_t s) {
+  cudaError_t err =
+      launch_token_csr(tgt, tgt_len, d, w.lpad, 1, 0, w.perm, w.tok_start, status, s);
+  if (err != cudaSuccess) return err;
+  switch (w.spl) {
+    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (err != cudaSuccess) return err;
+  asg_final_kernel<<<d.B, 256, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------- batch reduction of dA --
+__global__ void reduce_grad_trans_kernel(const float *ga_utt, const int32_t *status, Dims d,
+                                         float *grad_trans) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= d.N * d.N) return;
+  double s = 0.0;  // trainer.py:442-447 sums in float64
+  for (int b = 0; b < d.B; ++b)
+    if (status[b] == W2L_OK) s += (double)ga_utt[(size_t)b * d.N * d.N + p];
+  grad_trans[p] = (float)s;
+}
+
+cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
+                                     float *grad_trans, cudaStream_t s) {
+  const int n = d.N * d.N;
+  reduce_grad_trans_kernel<<<(n + 127) / 128, 128, 0, s>>>(ga_utt, status, d, grad_trans);
+  return cudaGetLastError();
+}
+
+}  // namespace w2l

@@ -1,0 +1,278 @@
+// The C-ABI (include/w2l_criterion.h): host-side contract checks, workspace
+// carving and the launch sequence of each entry point.  No allocations, no
+// global state; everything is enqueued on the caller's stream.
+
+#include <string.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace w2l;
+
+namespace {
+
+constexpr int kMaxExactSlotsFallback = 8;
+constexpr int kMaxExactSlotsF64 = 32;
+
+inline int from_cuda(cudaError_t e) { return e == cudaSuccess ? W2L_OK : W2L_ERR_CUDA; }
+
+bool dims_ok(int B, int Tmax, int N, int Lmax, int max_l) {
+  return B >= 0 && Tmax >= 1 && N >= 1 && N <= W2L_MAX_TOKENS && Lmax >= 0 && Lmax <= max_l;
+}
+
+struct Carver {
+  char *base;
+  size_t off = 0;
+  void *take(size_t bytes) {
+    void *p = base ? base + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return p;
+  }
+};
+
+int asg_slots(int B) { return B < kMaxExactSlotsFallback ? B : kMaxExactSlotsFallback; }
+int asg_slots_f64(int B) { return B < kMaxExactSlotsF64 ? B : kMaxExactSlotsF64; }
+
+}  // namespace
+
+extern "C" {
+
+const char *w2l_version(void) { return "w2l-criterion sm_100a r1 (scaled-linear fp32 + f64 exact)"; }
+
+const char *w2l_status_string(int code) {
+  switch (code) {
+    case W2L_OK: return "ok";
+    case W2L_ERR_CONTRACT: return "contract violation";
+    case W2L_ERR_NUMERIC: return "non-finite values";
+    case W2L_ERR_TARGET: return "invalid target";
+    case W2L_ERR_INFEASIBLE: return "infeasible target";
+    case W2L_ERR_CUDA: return "CUDA error";
+    case W2L_ERR_COMM: return "communication error";
+    default: return "unknown";
+  }
+}
+
+int w2l_status_first_error(const int32_t *status, int B, int32_t *bad_index,
+                           w2l_stream_t stream) {
+  if (bad_index) *bad_index = -1;
+  if (B <= 0) return W2L_OK;
+  if (!status) return W2L_ERR_CONTRACT;
+  int32_t small[256];
+  int32_t *host = B <= 256 ? small : (int32_t *)malloc(sizeof(int32_t) * B);
+  if (!host) return W2L_ERR_CUDA;
+  cudaError_t err = cudaMemcpyAsync(host, status, sizeof(int32_t) * B, cudaMemcpyDeviceToHost,
+                                    (cudaStream_t)stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize((cudaStream_t)stream);
+  int code = W2L_OK;
+  if (err != cudaSuccess) {
+    code = W2L_ERR_CUDA;
+  } else {
+    for (int b = 0; b < B; ++b) {
+      if (host[b] != W2L_OK) {
+        code = host[b] == kNeedsExact ? W2L_ERR_NUMERIC : host[b];
+        if (bad_index) *bad_index = b;
+        break;
+      }
+    }
+  }
+  if (host != small) free(host);
+  return code;
+}
+
+// ------------------------------------------------------------------ ASG --
+static size_t asg_ws(int B, int Tmax, int N, int Lmax, void *base, AsgFastWs *w,
+                     float **ga_utt, void **slots) {
+  Dims d{B, Tmax, N, Lmax};
+  Carver c{(char *)base};
+  void *fast = c.take(asg_fast_ws_bytes(d));
+  float *ga = (float *)c.take((size_t)B * N * N * sizeof(float));
+  void *sl = c.take(asg_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots(B));
+  if (base) {
+    asg_fast_ws_carve(d, fast, w);
+    *ga_utt = ga;
+    *slots = sl;
+  }
+  return c.off;
+}
+
+size_t w2l_asg_workspace_bytes(int B, int Tmax, int N, int Lmax) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return 0;
+  return asg_ws(B, Tmax, N, Lmax, nullptr, nullptr, nullptr, nullptr);
+}
+
+int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
+                      int Lmax, double *loss, float *grad_em, float *grad_trans,
+                      float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                      w2l_stream_t stream) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
+      !status || !ws)
+    return W2L_ERR_CONTRACT;
+  if (ws_bytes < w2l_asg_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, Lmax};
+  AsgFastWs w;
+  float *ga_ws;
+  void *slots;
+  asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
+  float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
+  int rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, status, s));
+  if (rc) return rc;
+  rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
+                                 status, s));
+  if (rc) return rc;
+  rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
+                                         slots, loss, grad_em, ga, status, s));
+  if (rc) return rc;
+  return from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
+}
+
+size_t w2l_asg_workspace_bytes_f64(int B, int Tmax, int N, int Lmax) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return 0;
+  Carver c{nullptr};
+  c.take((size_t)B * N * N * sizeof(float));
+  c.take(asg_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots_f64(B));
+  return c.off;
+}
+
+int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, const double *trans, int B, int Tmax,
+                          int N, int Lmax, double *loss, float *grad_em, float *grad_trans,
+                          float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                          w2l_stream_t stream) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
+      !status || !ws)
+    return W2L_ERR_CONTRACT;
+  if (ws_bytes < w2l_asg_workspace_bytes_f64(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, Lmax};
+  Carver c{(char *)ws};
+  float *ga_ws = (float *)c.take((size_t)B * N * N * sizeof(float));
+  void *slots = c.take(asg_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots_f64(B));
+  float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
+  int rc = from_cuda(launch_asg_validate<double>(em, em_len, tgt, tgt_len, trans, d, status, s));
+  if (rc) return rc;
+  // zero outputs of utterances that fail validation (the exact kernel skips them)
+  rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+  if (rc) return rc;
+  rc = from_cuda(cudaMemsetAsync(ga, 0, sizeof(float) * (size_t)B * N * N, s));
+  if (rc) return rc;
+  rc = from_cuda(launch_asg_exact<double>(em, em_len, tgt, tgt_len, trans, d, 0,
+                                          asg_slots_f64(B), slots, loss, grad_em, ga, status,
+                                          s));
+  if (rc) return rc;
+  return from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
+}
+
+// ------------------------------------------------------------------ CTC --
+static size_t ctc_ws(int B, int Tmax, int N, int Lmax, void *base, CtcFastWs *w, void **slots) {
+  Dims d{B, Tmax, N, Lmax};
+  Carver c{(char *)base};
+  void *fast = c.take(ctc_fast_ws_bytes(d));
+  void *sl = c.take(ctc_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots(B));
+  if (base) {
+    ctc_fast_ws_carve(d, fast, w);
+    *slots = sl;
+  }
+  return c.off;
+}
+
+size_t w2l_ctc_workspace_bytes(int B, int Tmax, int N, int Lmax) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return 0;
+  return ctc_ws(B, Tmax, N, Lmax, nullptr, nullptr, nullptr);
+}
+
+int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
+                      double *loss, float *grad_em, int32_t *status, void *ws,
+                      size_t ws_bytes, w2l_stream_t stream) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
+    return W2L_ERR_CONTRACT;
+  if (ws_bytes < w2l_ctc_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, Lmax};
+  CtcFastWs w;
+  void *slots;
+  ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
+  int rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, status, s));
+  if (rc) return rc;
+  rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s));
+  if (rc) return rc;
+  return from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
+                                           asg_slots(B), slots, loss, grad_em, status, s));
+}
+
+size_t w2l_ctc_workspace_bytes_f64(int B, int Tmax, int N, int Lmax) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return 0;
+  return align_up(ctc_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots_f64(B), 256);
+}
+
+int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, int blank, int B, int Tmax, int N,
+                          int Lmax, double *loss, float *grad_em, int32_t *status, void *ws,
+                          size_t ws_bytes, w2l_stream_t stream) {
+  if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
+    return W2L_ERR_CONTRACT;
+  if (ws_bytes < w2l_ctc_workspace_bytes_f64(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, Lmax};
+  int rc =
+      from_cuda(launch_ctc_validate<double>(logp, em_len, tgt, tgt_len, blank, d, status, s));
+  if (rc) return rc;
+  rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+  if (rc) return rc;
+  return from_cuda(launch_ctc_exact<double>(logp, em_len, tgt, tgt_len, blank, d, 0,
+                                            asg_slots_f64(B), ws, loss, grad_em, status, s));
+}
+
+// -------------------------------------------------------------- Viterbi --
+size_t w2l_viterbi_workspace_bytes(int B, int Tmax, int N) {
+  if (B < 0 || Tmax < 1 || N < 1 || N > W2L_MAX_TOKENS) return 0;
+  const size_t n = viterbi_ws_bytes(B, Tmax, N);
+  return n ? n : 256;
+}
+
+int w2l_viterbi(const float *em, const int32_t *em_len, const float *trans, int B, int Tmax,
+                int N, int64_t *path, double *score, int32_t *status, void *ws,
+                size_t ws_bytes, w2l_stream_t stream) {
+  if (B < 0 || Tmax < 1 || N < 1 || N > W2L_MAX_TOKENS) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!em || !em_len || !path || !score || !status) return W2L_ERR_CONTRACT;
+  if (viterbi_ws_bytes(B, Tmax, N) && (!ws || ws_bytes < viterbi_ws_bytes(B, Tmax, N)))
+    return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, 0};
+  int rc = from_cuda(launch_viterbi_validate<float>(em, em_len, d, status, s));
+  if (rc) return rc;
+  return from_cuda(launch_viterbi<float, float>(em, em_len, trans, d, path, score, status, ws, s));
+}
+
+int w2l_viterbi_f64(const double *em, const int32_t *em_len, const double *trans, int B,
+                    int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
+                    size_t ws_bytes, w2l_stream_t stream) {
+  if (B < 0 || Tmax < 1 || N < 1 || N > W2L_MAX_TOKENS) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!em || !em_len || !path || !score || !status) return W2L_ERR_CONTRACT;
+  if (viterbi_ws_bytes(B, Tmax, N) && (!ws || ws_bytes < viterbi_ws_bytes(B, Tmax, N)))
+    return W2L_ERR_CONTRACT;
+  cudaStream_t s = (cudaStream_t)stream;
+  Dims d{B, Tmax, N, 0};
+  int rc = from_cuda(launch_viterbi_validate<double>(em, em_len, d, status, s));
+  if (rc) return rc;
+  return from_cuda(
+      launch_viterbi<double, double>(em, em_len, trans, d, path, score, status, ws, s));
+}
+
+int w2l_probe_peaks(double *mufu_ops_per_s, double *dadd_ops_per_s, double *ffma_ops_per_s) {
+  return probe_peaks(mufu_ops_per_s, dadd_ops_per_s, ffma_ops_per_s);
+}
+
+}  // extern "C"

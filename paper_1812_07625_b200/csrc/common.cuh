@@ -1,0 +1,106 @@
+// Shared device helpers for the sm_100a sequence-criterion kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/w2l_criterion.h"
+
+namespace w2l {
+
+// Internal per-utterance status: the fp32 guard asks for the float64 kernel.
+constexpr int kNeedsExact = 100;
+
+constexpr int kWarp = 32;
+constexpr int kChunk = 32;            // frames per staged emission chunk
+constexpr int kNegExp = -(1 << 24);   // exponent of an all-zero lane block
+
+__host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline size_t align_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+// padded row stride of a staged emission row: odd (bank-conflict free for
+// row-per-lane access) and > N so column N can hold an explicit 0.
+__host__ __device__ inline int em_stride(int n) { return (n + 1) | 1; }
+
+// ------------------------------------------------------------ pow2 math --
+// Exact power-of-two rescaling keeps the scaled linear-domain recursions
+// free of rounding in the scale factors: only integer exponents accumulate.
+
+// 2^k as a float for k in [-149, 127]; 0 below, +inf never produced (clamped).
+__device__ __forceinline__ float pow2f(int k) {
+  if (k >= -126) {
+    k = min(k, 127);
+    return __int_as_float((k + 127) << 23);
+  }
+  if (k >= -149) return __int_as_float(1 << (k + 149));
+  return 0.0f;
+}
+
+// floor(log2(x)) for a positive normal float; subnormals map to -127.
+__device__ __forceinline__ int exponent_of(float x) {
+  return ((__float_as_int(x) >> 23) & 0xff) - 127;
+}
+
+__device__ __forceinline__ double pow2d(int k) {
+  if (k < -1022) return ldexp(1.0, k);
+  k = min(k, 1023);
+  return __longlong_as_double((long long)(k + 1023) << 52);
+}
+
+// ------------------------------------------------------------ log-space --
+// logaddexp on doubles with -inf handled explicitly.
+__device__ __forceinline__ double logadd(double a, double b) {
+  if (a == -CUDART_INF) return b;
+  if (b == -CUDART_INF) return a;
+  double m = fmax(a, b);
+  return m + log1p(exp(-fabs(a - b)));
+}
+
+// ------------------------------------------------------------- reduction --
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ----------------------------------------------------------- cp.async --
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// read-only, evict-first streaming load of an emission value
+__device__ __forceinline__ float ldg_stream(const float *p) { return __ldcs(p); }
+
+}  // namespace w2l

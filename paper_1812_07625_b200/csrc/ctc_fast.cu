@@ -1,0 +1,349 @@
+// fp32 batched CTC loss + gradient (replaces criterion.py:84-162 for the
+// batched hot path).
+//
+// The 2L+1-state blank-augmented lattice (criterion.py:113-120) runs in the
+// scaled linear domain, SPL states per lane with a per-lane power-of-two
+// exponent, exactly like the ASG fac chain:
+//   alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])
+//   beta'_t[s] = w[s] + w[s+1] + skip_{s+2} w[s+2],  w = Et+1[lab] beta'_{t+1}
+// with Et = exp(logp - max_i logp) and the per-frame shifts summed in f64 for
+// the loss.  The gradient kernel forms per-frame posteriors with their own
+// normaliser Z_t, gathers them by token (blank = even states, labels through
+// a token CSR) and checks the per-frame consistency guard; failing utterances
+// are recomputed by the float64 log-domain kernel.
+
+#include "chunk.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace w2l {
+namespace {
+
+constexpr int kGradFramesPerBlock = 64;
+constexpr int kGradWarps = 8;
+
+template <int SPL>
+__device__ __forceinline__ void ctc_lattice_lane(const int64_t *y, int L, int blank, int N,
+                                                 int lane, int *lab, float *sk, float *sk2) {
+  const int S = 2 * L + 1;
+  auto skip_of = [&](int s) -> bool {
+    return (s & 1) && s >= 3 && s < S && y[s >> 1] != y[(s >> 1) - 1];
+  };
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    const int s = lane * SPL + k;
+    lab[k] = s < S ? ((s & 1) ? (int)y[s >> 1] : blank) : N;
+    sk[k] = skip_of(s) ? 1.f : 0.f;
+    sk2[k] = skip_of(s + 2) ? 1.f : 0.f;
+  }
+}
+
+template <int SPL>
+__global__ void __launch_bounds__(32)
+    ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                     int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
+  __shared__ __align__(16) float chunk[2 * kChunk * 33];
+  const int b = blockIdx.x, role = blockIdx.y, lane = threadIdx.x;
+  if (status[b] != W2L_OK) return;
+  const int T = em_len[b], N = d.N, L = tgt_len[b], S = 2 * L + 1;
+  const bool fwd = role == 0;
+  EmissionPipe pipe;
+  pipe.init(chunk, em + (size_t)b * d.Tmax * N, T, N, fwd);
+  const size_t row0 = (size_t)b * d.Tmax;
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  int lab[SPL];
+  float sk[SPL], sk2[SPL];
+  ctc_lattice_lane<SPL>(y, L, blank, N, lane, lab, sk, sk2);
+
+  float v[SPL];
+  int ex = 0;
+  float *out = fwd ? w.a : w.b;
+  int *oute = fwd ? w.ea : w.eb;
+  const int lp = w.lpad;
+  
+  
+  const double ln2 = 0.6931471805599453;
+
+  if (fwd) {
+    const float *r0 = pipe.row(0);
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) v[k] = 0.f;
+    ex = 0;
+    if (lane == 0) {               // criterion.py:123-125
+      v[0] = r0[lab[0]];
+      if (S > 1) v[1] = r0[lab[1]];
+    }
+    lane_renorm<SPL>(v, ex);
+    lane_store<SPL>(v, ex, out, oute, row0, lp, lane, 0);
+    for (int t = 1; t < T; ++t) {
+      const float *r = pipe.row(t);
+      float E[SPL];
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) E[k] = r[lab[k]];
+      float nb1 = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
+      float nb2 = __shfl_up_sync(0xffffffffu, v[SPL - 2], 1);
+      int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
+      if (lane == 0) {
+        nb1 = nb2 = 0.f;
+        nbe = kNegExp;
+      }
+      int dd = nbe - ex;
+      if (dd > 64) {
+        const float sc = pow2f(-dd);
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) v[k] *= sc;
+        ex = nbe;
+        dd = 0;
+      }
+      const float scn = pow2f(dd);
+      const float n1 = nb1 * scn, n2 = nb2 * scn;
+#pragma unroll
+      for (int k = SPL - 1; k >= 2; --k) v[k] = E[k] * fmaf(sk[k], v[k - 2], v[k] + v[k - 1]);
+      const float v1 = E[1] * fmaf(sk[1], n1, v[1] + v[0]);
+      v[0] = E[0] * fmaf(sk[0], n2, v[0] + n1);
+      v[1] = v1;
+      lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, t);
+    }
+    // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
+    float part = 0.f;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const int s = lane * SPL + k;
+      if (s == S - 1 || s == S - 2) part += v[k];
+    }
+    const double lp_ = part > 0.f ? log((double)part) + (double)ex * ln2 : -CUDART_INF;
+    const double m = warp_max(lp_);
+    const double sum = warp_sum(lp_ > -CUDART_INF ? exp(lp_ - m) : 0.0);
+    const double shifts = warp_sum(pipe.shift_sum);
+    if (lane == 0) {
+      w.scal[b * 4 + 0] = isfinite(m) ? m + log(sum) : -CUDART_INF;
+      w.scal[b * 4 + 2] = shifts;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const int s = lane * SPL + k;
+      v[k] = (s == S - 1 || s == S - 2) ? 1.f : 0.f;
+    }
+    ex = 0;
+    lane_renorm<SPL>(v, ex);
+    lane_store<SPL>(v, ex, out, oute, row0, lp, lane, T - 1);
+    for (int u = T - 1; u >= 1; --u) {
+      const float *r = pipe.row(u);
+      float wv[SPL];
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) wv[k] = r[lab[k]] * v[k];
+      float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+      float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
+      int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
+      if (lane == 31) {
+        nb1 = nb2 = 0.f;
+        nbe = kNegExp;
+      }
+      int dd = nbe - ex;
+      if (dd > 64) {
+        const float sc = pow2f(-dd);
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) wv[k] *= sc;
+        ex = nbe;
+        dd = 0;
+      }
+      const float scn = pow2f(dd);
+      const float n1 = nb1 * scn, n2 = nb2 * scn;
+#pragma unroll
+      for (int k = 0; k < SPL - 2; ++k) v[k] = fmaf(sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
+      v[SPL - 2] = fmaf(sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
+      v[SPL - 1] = fmaf(sk2[SPL - 1], n2, wv[SPL - 1] + n1);
+      lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, u - 1);
+    }
+    const float *r0 = pipe.row(0);
+    if (lane == 0) {
+      float z = r0[lab[0]] * v[0];
+      if (S > 1) z += r0[lab[1]] * v[1];
+      w.scal[b * 4 + 1] = log((double)z) + (double)ex * ln2;
+    }
+  }
+}
+
+template <int SPL>
+__global__ void __launch_bounds__(kGradWarps * 32)
+    ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                    const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                    int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
+                    const int32_t *__restrict__ status) {
+  constexpr int LP = SPL * 32;
+  __shared__ float prow[kGradWarps][LP];
+  __shared__ float gw[kGradWarps][2];
+  const int b = blockIdx.y, blk = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = d.N, T = em_len[b];
+  const int t0 = blk * kGradFramesPerBlock;
+  const bool ok = status[b] == W2L_OK;
+  float *ge = grad_em + (size_t)b * d.Tmax * N;
+  const int fpw = kGradFramesPerBlock / kGradWarps;
+  const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
+  for (int t = ta; t < tb; ++t)
+    if (!ok || t >= T)
+      if (lane < N) ge[(size_t)t * N + lane] = 0.f;
+  if (!ok) return;
+  const int L = tgt_len[b], S = 2 * L + 1;
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  int lab[SPL];
+  float sk[SPL], sk2[SPL];
+  ctc_lattice_lane<SPL>(y, L, blank, N, lane, lab, sk, sk2);
+  (void)S;
+  const int *perm = w.perm + (size_t)b * w.lpad;
+  const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
+  const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
+  const double ref = w.scal[b * 4 + 0] * 1.4426950408889634;
+  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
+  const size_t row0 = (size_t)b * d.Tmax;
+  float *myp = prow[warp];
+  const int tend = min(tb, T);
+  for (int t = ta; t < tend; ++t) {
+    float va[SPL], vb[SPL];
+    const float *oa = w.a + (row0 + t) * LP;
+    const float *ob = w.b + (row0 + t) * LP;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      va[k] = oa[k * 32 + lane];
+      vb[k] = ob[k * 32 + lane];
+    }
+    const int ea = w.ea[(row0 + t) * 32 + lane];
+    const int eb = w.eb[(row0 + t) * 32 + lane];
+    const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
+    const int es = alive ? ea + eb : kNegExp;
+    const int estar = warp_max(es);
+    const float sc = alive ? pow2f(es - estar) : 0.f;
+    float zl = 0.f, zb = 0.f;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      const float p = va[k] * vb[k] * sc;
+      myp[lane * SPL + k] = p;
+      zl += p;
+      if (((lane * SPL + k) & 1) == 0) zb += p;   // blank states
+    }
+    const float z = warp_sum(zl);
+    const float zblank = warp_sum(zb);
+    const float inv = 1.f / z;
+    const float g = (float)((double)__log2f(z) + (double)estar - ref);
+    gmin = fminf(gmin, g);
+    gmax = fmaxf(gmax, g);
+    __syncwarp();
+    float acc = lane == blank ? zblank : 0.f;
+    for (int q = ts0; q < ts1; ++q) acc += myp[perm[q]];
+    if (lane < N) ge[(size_t)t * N + lane] = -acc * inv;   // criterion.py:159-161
+    __syncwarp();
+  }
+  if (lane == 0) {
+    gw[warp][0] = gmin;
+    gw[warp][1] = gmax;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    for (int q = 0; q < kGradWarps; ++q)
+      g = threadIdx.x ? fmaxf(g, gw[q][1]) : fminf(g, gw[q][0]);
+    w.part_guard[((size_t)b * w.nblk + blk) * 2 + threadIdx.x] = g;
+  }
+}
+
+__global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
+                                 double *loss, int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B || status[b] != W2L_OK) return;
+  const int T = em_len[b];
+  const double ln2 = 0.6931471805599453;
+  const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
+  const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
+  bool bad = !(isfinite(zA) && isfinite(zB)) || fabs(zA - zB) > tol;
+  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
+  for (int q = 0; q < nb_used && !bad; ++q) {
+    const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 2;
+    bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
+  }
+  loss[b] = -(zA + shifts);                                  // criterion.py:162
+  if (bad) status[b] = kNeedsExact;
+}
+
+template <int SPL>
+cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
+                       const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
+                       float *grad_em, const int32_t *status, cudaStream_t s) {
+  ctc_chain_kernel<SPL><<<dim3(d.B, 2), 32, 0, s>>>(em, em_len, tgt, tgt_len, blank, d, w,
+                                                     status);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  ctc_grad_kernel<SPL><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
+                                                                      blank, d, w, grad_em,
+                                                                      status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int ctc_fast_spl(int Lmax) {
+  static const int opts[] = {2, 4, 8, 10, 12, 16, 20, 24, 32};
+  const int S = 2 * Lmax + 1;
+  for (int o : opts)
+    if (32 * o >= S) return o;
+  return 0;
+}
+
+static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
+  const int spl = ctc_fast_spl(d.Lmax);
+  const int lpad = spl * 32;
+  const int nblk = (d.Tmax + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
+  const size_t BT = (size_t)d.B * d.Tmax;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return base ? (void *)((char *)base + o) : nullptr;
+  };
+  CtcFastWs t;
+  t.a = (float *)take(BT * lpad * 4);
+  t.b = (float *)take(BT * lpad * 4);
+  t.ea = (int *)take(BT * 32 * 4);
+  t.eb = (int *)take(BT * 32 * 4);
+  t.scal = (double *)take((size_t)d.B * 4 * 8);
+  t.part_guard = (float *)take((size_t)d.B * nblk * 2 * 4);
+  t.perm = (int *)take((size_t)d.B * lpad * 4);
+  t.tok_start = (int *)take((size_t)d.B * 33 * 4);
+  t.spl = spl;
+  t.lpad = lpad;
+  t.nblk = nblk;
+  if (w) *w = t;
+  return off;
+}
+
+size_t ctc_fast_ws_bytes(Dims d) { return ctc_ws_layout(d, nullptr, nullptr); }
+void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w); }
+
+cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
+                            double *loss, float *grad_em, int32_t *status, cudaStream_t s) {
+  cudaError_t err =
+      launch_token_csr(tgt, tgt_len, d, w.lpad, 2, 1, w.perm, w.tok_start, status, s);
+  if (err != cudaSuccess) return err;
+  switch (w.spl) {
+    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (err != cudaSuccess) return err;
+  ctc_final_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
+  return cudaGetLastError();
+}
+
+}  // namespace w2l

@@ -1,0 +1,99 @@
+// Host-side launchers for the sm_100a kernels (one translation unit each).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace w2l {
+
+struct Dims {
+  int B, Tmax, N, Lmax;
+};
+
+// ---- validation (reference check order; criterion.py:23-41,92-111,174-190)
+template <class TE>
+cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
+                                const int32_t *tgt_len, const TE *trans, Dims d,
+                                int32_t *status, cudaStream_t s);
+template <class TE>
+cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
+                                const int32_t *tgt_len, int blank, Dims d, int32_t *status,
+                                cudaStream_t s);
+template <class TE>
+cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
+                                    int32_t *status, cudaStream_t s);
+
+// ---- float64 log-domain kernels (exact path + fallback for the fp32 guard)
+size_t asg_exact_ws_bytes_per_slot(int Tmax, int N, int Lmax);
+size_t ctc_exact_ws_bytes_per_slot(int Tmax, int N, int Lmax);
+// only_flagged: process utterances whose status is kNeedsExact (fallback);
+// otherwise every utterance with status OK.
+template <class TE>
+cudaError_t launch_asg_exact(const TE *em, const int32_t *em_len, const int64_t *tgt,
+                             const int32_t *tgt_len, const TE *trans, Dims d, int only_flagged,
+                             int nslots, void *slot_ws, double *loss, float *grad_em,
+                             float *ga_utt, int32_t *status, cudaStream_t s);
+template <class TE>
+cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t *tgt,
+                             const int32_t *tgt_len, int blank, Dims d, int only_flagged,
+                             int nslots, void *slot_ws, double *loss, float *grad_em,
+                             int32_t *status, cudaStream_t s);
+
+// ---- fp32 fast path
+struct AsgFastWs {
+  float *fcc_a, *fcc_b;      // [B][Tmax][32]
+  int *fcc_ka, *fcc_kb;      // [B][Tmax] cumulative exponents
+  float *fac_a, *fac_b;      // [B][Tmax][SPL*32] slot-major
+  int *fac_ea, *fac_eb;      // [B][Tmax][32] per-lane exponents
+  double *scal;              // [B][4]: lnZ fcc fwd, fcc bwd, fac fwd, fac bwd
+  float *part_fullA;         // [B][nblk][32][32]
+  float *part_edge;          // [B][nblk][2][Lpad]
+  float *part_guard;         // [B][nblk][4]
+  int *perm;                 // [B][Lpad] states sorted by token
+  int *tok_start;            // [B][33]
+  int spl, lpad, nblk;
+};
+int asg_fast_spl(int Lmax);  // 0 if unsupported
+size_t asg_fast_ws_bytes(Dims d);
+void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w);
+cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, const float *trans, Dims d,
+                            const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
+                            int32_t *status, cudaStream_t s);
+
+struct CtcFastWs {
+  float *a, *b;              // [B][Tmax][SPL*32]
+  int *ea, *eb;              // [B][Tmax][32]
+  double *scal;              // [B][4]: lnZ fwd, lnZ bwd, sum of frame shifts, spare
+  float *part_guard;         // [B][nblk][2]
+  int *perm;                 // [B][Lpad] label positions sorted by token
+  int *tok_start;            // [B][33]
+  int spl, lpad, nblk;
+};
+int ctc_fast_spl(int Lmax);
+size_t ctc_fast_ws_bytes(Dims d);
+void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w);
+cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
+                            double *loss, float *grad_em, int32_t *status, cudaStream_t s);
+
+// token-grouped chain states (perm, tok_start) for the emissions-gradient gather
+cudaError_t launch_token_csr(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
+                             int state_mul, int state_off, int *perm, int *tok_start,
+                             const int32_t *status, cudaStream_t s);
+
+// ---- reductions
+cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
+                                     float *grad_trans, cudaStream_t s);
+
+// ---- Viterbi (float64 max-plus, bit-exact)
+size_t viterbi_ws_bytes(int B, int Tmax, int N);
+template <class TE, class TA>
+cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans, Dims d,
+                           int64_t *path, double *score, const int32_t *status, void *ws,
+                           cudaStream_t s);
+
+// ---- microbenchmarks
+int probe_peaks(double *mufu, double *dadd, double *ffma);
+
+}  // namespace w2l

@@ -1,0 +1,126 @@
+// Batched Viterbi best path (replaces criterion.py:259-284).
+//
+// One warp per utterance, lane i owns destination token i and keeps row i of
+// the transition matrix in registers (A[to][from], criterion.py:276).  The
+// max-plus recursion runs in float64 in the reference's operation order
+//     cand_j = dp[j] + A[i][j];  back = first argmax_j;  dp'[i] = e[t][i] + cand_back
+// so paths and scores are bit-identical to the numpy reference (ties go to
+// the lowest id, np.argmax semantics, NaN treated as the maximum).  The
+// previous frame's dp vector is broadcast through shared memory (double
+// buffered, one __syncwarp per frame); backpointers are uint8 in shared
+// memory when T*N fits, else in the workspace; lane 0 traces back.
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace w2l {
+namespace {
+
+constexpr int kSmemBackMax = 160 * 1024;
+
+template <class TE, class TA, bool kSmemBack>
+__global__ void __launch_bounds__(32) viterbi_kernel(const TE *__restrict__ em,
+                                                     const int32_t *__restrict__ em_len,
+                                                     const TA *__restrict__ trans, Dims d,
+                                                     int64_t *__restrict__ path,
+                                                     double *__restrict__ score,
+                                                     const int32_t *__restrict__ status,
+                                                     uint8_t *__restrict__ back_ws) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ __align__(16) double dp_buf[2][32];
+  const int b = blockIdx.x, lane = threadIdx.x, N = d.N;
+  int64_t *pb = path + (size_t)b * d.Tmax;
+  if (status[b] != W2L_OK) {
+    for (int t = lane; t < d.Tmax; t += 32) pb[t] = 0;
+    if (lane == 0) score[b] = 0.0;
+    return;
+  }
+  const int T = em_len[b];
+  uint8_t *back = kSmemBack ? smem : back_ws + (size_t)b * d.Tmax * N;
+  const TE *e = em + (size_t)b * d.Tmax * N;
+
+  double arow[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    arow[j] = (trans != nullptr && lane < N && j < N) ? (double)trans[lane * N + j] : 0.0;
+
+  double dp = lane < N ? (double)e[lane] : -CUDART_INF;
+  dp_buf[0][lane] = dp;
+  for (int t = 1; t < T; ++t) {
+    __syncwarp();
+    const double *prev = dp_buf[(t - 1) & 1];
+    const double et = lane < N ? (double)e[(size_t)t * N + lane] : 0.0;
+    double best = prev[0] + arow[0];
+    int arg = 0;
+#pragma unroll
+    for (int j = 1; j < 32; ++j) {
+      if (j < N) {
+        const double c = prev[j] + arow[j];
+        // first maximum wins; a NaN becomes (and stays) the maximum
+        if (!isnan(best) && (c > best || isnan(c))) {
+          best = c;
+          arg = j;
+        }
+      }
+    }
+    dp = et + best;
+    if (lane < N) back[(size_t)t * N + lane] = (uint8_t)arg;
+    dp_buf[t & 1][lane] = lane < N ? dp : -CUDART_INF;
+  }
+  __syncwarp();
+  // final argmax (first maximum): gather dp to lane 0 through shared memory
+  const double *fin = dp_buf[(T - 1) & 1];
+  if (lane == 0) {
+    int best_i = 0;
+    double bv = fin[0];
+    for (int i = 1; i < N; ++i) {
+      const double v = fin[i];
+      if (!isnan(bv) && (v > bv || isnan(v))) {
+        bv = v;
+        best_i = i;
+      }
+    }
+    score[b] = bv;
+    int cur = best_i;
+    pb[T - 1] = cur;
+    for (int t = T - 1; t > 0; --t) {
+      cur = back[(size_t)t * N + cur];
+      pb[t - 1] = cur;
+    }
+  }
+  for (int t = T + lane; t < d.Tmax; t += 32) pb[t] = 0;
+}
+
+}  // namespace
+
+size_t viterbi_ws_bytes(int B, int Tmax, int N) {
+  if ((size_t)Tmax * N <= (size_t)kSmemBackMax) return 0;
+  return align_up((size_t)B * Tmax * N, 256);
+}
+
+template <class TE, class TA>
+cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans, Dims d,
+                           int64_t *path, double *score, const int32_t *status, void *ws,
+                           cudaStream_t s) {
+  const size_t back_bytes = (size_t)d.Tmax * d.N;
+  if (back_bytes <= (size_t)kSmemBackMax) {
+    auto k = viterbi_kernel<TE, TA, true>;
+    cudaError_t err =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBackMax);
+    if (err != cudaSuccess) return err;
+    k<<<d.B, 32, back_bytes, s>>>(em, em_len, trans, d, path, score, status, nullptr);
+  } else {
+    viterbi_kernel<TE, TA, false><<<d.B, 32, 0, s>>>(em, em_len, trans, d, path, score, status,
+                                                     (uint8_t *)ws);
+  }
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_viterbi<float, float>(const float *, const int32_t *, const float *,
+                                                  Dims, int64_t *, double *, const int32_t *,
+                                                  void *, cudaStream_t);
+template cudaError_t launch_viterbi<double, double>(const double *, const int32_t *,
+                                                    const double *, Dims, int64_t *, double *,
+                                                    const int32_t *, void *, cudaStream_t);
+
+}  // namespace w2l

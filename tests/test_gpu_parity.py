@@ -1,0 +1,320 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the CPU oracle
+and the reference's golden fixtures.
+
+Tolerances: per-utterance float64 API -- the reference's own test bounds
+(|loss - enum| < 1e-5, FD rel 1e-3, Viterbi score abs 1e-9) and <= 1e-6
+against the reference outputs; batched fp32 API -- loss and gradients within
+1e-4 relative (norm-relative for gradients, oracles.rel_err), Viterbi paths
+and scores bit-exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_kat, load_npz
+from oracle import criterion_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+C = pytest.importorskip("paper_1812_07625_b200.criterion")
+from paper_1812_07625_b200.errors import (ContractError, InfeasibleTargetError,  # noqa: E402
+                                          NumericError, TargetError)
+from paper_1812_07625_b200.tokens import TokenTable  # noqa: E402
+
+REL = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _norm_rows(x):
+    return orc.log_softmax_rows(x)
+
+
+# ------------------------------------------- per-utterance (float64) API --
+
+def test_hand_values():
+    out = C.ctc_loss_grad(np.full((1, 2), math.log(0.5)), np.array([0]), blank_id=1)
+    assert out.loss == pytest.approx(math.log(2.0), abs=1e-12)
+    assert out.grad_emissions[0].tolist() == pytest.approx([-1.0, 0.0], abs=1e-6)
+    out = C.asg_loss_grad(np.zeros((2, 2)), np.array([0]), np.zeros((2, 2), np.float32))
+    assert out.loss == pytest.approx(math.log(4.0), abs=1e-12)
+    e = np.array([[0.3, -1.2, 2.0]])
+    out = C.asg_loss_grad(e, [1], np.zeros((3, 3), np.float32))
+    assert out.loss == pytest.approx(orc.lse(e[0]) - e[0, 1], abs=1e-12)
+    path, score = C.viterbi(np.zeros((4, 3)))
+    assert path.tolist() == [0, 0, 0, 0] and score == pytest.approx(0.0)
+
+
+def test_ctc_kat_and_enumeration():
+    for c in load_kat()["ctc"]:
+        out = C.ctc_loss_grad(np.asarray(c["e"]), np.asarray(c["y"]), c["blank"])
+        assert abs(out.loss - c["enum"]) < 1e-5
+        assert abs(out.loss - c["loss"]) < 1e-9
+        assert np.abs(out.grad_emissions - np.asarray(c["grad"])).max() < 1e-6
+        assert out.grad_emissions.dtype == np.float32 and isinstance(out.loss, float)
+
+
+def test_asg_kat_and_enumeration():
+    for c in load_kat()["asg"]:
+        out = C.asg_loss_grad(np.asarray(c["e"]), np.asarray(c["y"]),
+                              np.asarray(c["a"], np.float32))
+        assert abs(out.loss - c["enum"]) < 1e-5
+        assert abs(out.loss - c["loss"]) < 1e-9
+        assert np.abs(out.grad_emissions - np.asarray(c["grad_e"])).max() < 1e-6
+        assert np.abs(out.grad_transitions - np.asarray(c["grad_a"])).max() < 1e-6
+
+
+def test_viterbi_kat_bit_exact():
+    for c in load_kat()["viterbi"]:
+        a = None if c["a"] is None else np.asarray(c["a"])
+        path, score = C.viterbi(np.asarray(c["e"]), a)
+        assert path.tolist() == c["path"]
+        assert score == c["score"]
+        assert abs(score - c["enum"]) < 1e-9
+
+
+def test_gradients_match_finite_differences():
+    # test_criterion.py:121-147 with the shim inside the finite differences
+    rng = np.random.default_rng(500)
+    for _ in range(6):
+        n = int(rng.integers(2, 5))
+        t = int(rng.integers(1, 6))
+        length = int(rng.integers(1, 4))
+        y = [int(rng.integers(0, n))]
+        while len(y) < length:
+            v = int(rng.integers(0, n))
+            if v != y[-1]:
+                y.append(v)
+        t = max(t, len(y))
+        e = rng.normal(size=(t, n)) * 2.0
+        a = rng.normal(size=(n, n)).astype(np.float32)
+        out = C.asg_loss_grad(e, y, a)
+        fd_e = orc.finite_difference(lambda z: C.asg_loss_grad(z, y, a).loss, e, 1e-3)
+        fd_a = orc.finite_difference(lambda z: C.asg_loss_grad(e, y, z.astype(np.float32)).loss,
+                                     a.astype(np.float64), 1e-3)
+        assert orc.rel_err(out.grad_emissions, fd_e) < 1e-3
+        assert orc.rel_err(out.grad_transitions, fd_a) < 1e-3
+    rng = np.random.default_rng(400)
+    for _ in range(6):
+        n = int(rng.integers(3, 5))
+        e = _norm_rows(rng.normal(size=(5, n)) * 2.0)
+        y = [int(rng.integers(0, n - 1)), int(rng.integers(0, n - 1))]
+        out = C.ctc_loss_grad(e, y, n - 1)
+        fd = orc.finite_difference(lambda z: C.ctc_loss_grad(z, y, n - 1).loss, e, 1e-3)
+        assert orc.rel_err(out.grad_emissions, fd) < 1e-3
+
+
+def test_row_sums_and_invariances():
+    rng = np.random.default_rng(600)
+    e = _norm_rows(rng.normal(size=(6, 4)) * 2)
+    g = C.ctc_loss_grad(e, [0, 2, 1], 3).grad_emissions
+    assert np.allclose(g.sum(axis=1), -1.0, atol=1e-5)
+    e2 = rng.normal(size=(7, 3)) * 2
+    g = C.asg_loss_grad(e2, [0, 1], rng.normal(size=(3, 3)).astype(np.float32)).grad_emissions
+    assert np.allclose(g.sum(axis=1), 0.0, atol=1e-5)
+    # CTC label-permutation invariance (test_criterion.py:167-176)
+    e = _norm_rows(np.random.default_rng(700).normal(size=(5, 4)) * 2)
+    base = C.ctc_loss_grad(e, np.array([0, 2, 1]), blank_id=3).loss
+    perm = np.array([2, 0, 1, 3])
+    e_p = np.empty_like(e)
+    e_p[:, perm] = e
+    assert C.ctc_loss_grad(e_p, perm[[0, 2, 1]], blank_id=3).loss == pytest.approx(base, abs=1e-10)
+
+
+def test_scale_stability_matches_reference():
+    kat = load_kat()
+    c = kat["asg_scale"]
+    out = C.asg_loss_grad(np.asarray(c["e"]), c["y"], np.asarray(c["a"], np.float32))
+    assert out.loss == pytest.approx(c["loss"], rel=1e-12)
+    assert np.abs(out.grad_emissions - np.asarray(c["grad_e"])).max() < 1e-6
+    assert np.abs(out.grad_transitions - np.asarray(c["grad_a"])).max() < 1e-6
+    c = kat["ctc_scale"]
+    out = C.ctc_loss_grad(np.asarray(c["e"]), c["y"], c["blank"])
+    assert out.loss == pytest.approx(c["loss"], rel=1e-12)
+    assert np.isfinite(out.grad_emissions).all()
+
+
+def test_error_contracts():
+    with pytest.raises(ContractError):
+        C.ctc_loss_grad(np.zeros((3, 4)), np.array([0]), blank_id=3)      # unnormalised
+    e = _norm_rows(np.zeros((3, 3)))
+    with pytest.raises(TargetError):
+        C.ctc_loss_grad(e, np.array([2]), blank_id=2)                     # blank in target
+    with pytest.raises(TargetError):
+        C.ctc_loss_grad(e, np.array([7]), blank_id=2)                     # id out of range
+    e = _norm_rows(np.random.default_rng(0).normal(size=(2, 3)))
+    with pytest.raises(InfeasibleTargetError):
+        C.ctc_loss_grad(e, np.array([0, 0]), blank_id=2)
+    with pytest.raises(InfeasibleTargetError):
+        C.asg_loss_grad(np.zeros((1, 3)), np.array([0, 1]), np.zeros((3, 3), np.float32))
+    with pytest.raises(ContractError):
+        C.asg_loss_grad(np.zeros((3, 3)), np.array([1, 1]), np.zeros((3, 3), np.float32))
+    with pytest.raises(TargetError):
+        C.asg_loss_grad(np.zeros((2, 2)), np.array([], dtype=np.int64), np.zeros((2, 2)))
+    with pytest.raises(NumericError):
+        C.asg_loss_grad(np.array([[0.0, np.nan]]), [0], np.zeros((2, 2)))
+    with pytest.raises(NumericError):
+        C.asg_loss_grad(np.zeros((2, 2)), [0], np.array([[0.0, np.inf], [0, 0]]))
+    with pytest.raises(ContractError):
+        C.asg_loss_grad(np.zeros((2, 2)), [0], np.zeros((3, 3)))
+    with pytest.raises(ContractError):
+        C.asg_loss_grad(np.zeros((0, 2)), [0], np.zeros((2, 2)))
+    with pytest.raises(NumericError):
+        C.viterbi(np.array([[np.inf, 0.0]]))
+
+
+def test_criterion_adapters():
+    table = TokenTable(["a", "b", "<2>"])
+    crit = C.make_criterion("asg", table)
+    assert crit.n_outputs == 3 and set(crit.params()) == {"criterion.transitions"}
+    target = crit.prepare_target([0, 0, 1])
+    assert target == [0, table.rep_id, 1]
+    out = crit.loss_grad(np.random.default_rng(2).normal(size=(5, 3)), np.asarray(target))
+    assert out.grad_transitions is not None and out.grad_transitions.shape == (3, 3)
+    ctc = C.make_criterion("ctc", TokenTable(["a", "b", "|"]))
+    assert ctc.blank_id == 3 and ctc.n_outputs == 4 and ctc.params() == {}
+    e = _norm_rows(np.random.default_rng(1).normal(size=(4, 4)))
+    hyp = ctc.collapse(ctc.viterbi_path(e))
+    assert all(0 <= t < 3 for t in hyp)
+    with pytest.raises(ContractError):
+        C.make_criterion("transducer", TokenTable(["a"]))
+
+
+# ------------------------------------------------- batched fp32 hot path --
+
+def _asg_batch_check(g, rel=REL):
+    em = torch.from_numpy(g["em"]).cuda()
+    out = C.asg_loss_grad_batched(em, g["em_len"], g["targets"], g["tgt_len"], g["trans"],
+                                  per_utterance_grad_transitions=True)
+    loss = out.loss.cpu().numpy()
+    np.testing.assert_allclose(loss, g["loss"], rtol=rel, atol=rel)
+    ge = out.grad_emissions.cpu().numpy()
+    for b in range(ge.shape[0]):
+        assert orc.rel_err(ge[b], g["grad_e"][b]) < rel, b
+        assert orc.rel_err(out.grad_transitions_per_utt[b].cpu().numpy(),
+                           g["grad_a_per_utt"][b]) < rel, b
+    want = g["grad_a_per_utt"].astype(np.float64).sum(axis=0)
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), want) < rel
+    # padding frames are zero
+    for b in range(ge.shape[0]):
+        assert not ge[b, int(g["em_len"][b]):].any()
+    return out
+
+
+@pytest.mark.parametrize("name", ["asg_c1", "asg_ragged", "asg_c3_one"])
+def test_asg_batched_matches_reference(name):
+    _asg_batch_check(load_npz(name))
+
+
+@pytest.mark.parametrize("name", ["ctc_c2_one", "ctc_ragged"])
+def test_ctc_batched_matches_reference(name):
+    g = load_npz(name)
+    out = C.ctc_loss_grad_batched(torch.from_numpy(g["em"]).cuda(), g["em_len"], g["targets"],
+                                  g["tgt_len"], int(g["blank"]))
+    np.testing.assert_allclose(out.loss.cpu().numpy(), g["loss"], rtol=REL, atol=REL)
+    ge = out.grad_emissions.cpu().numpy()
+    for b in range(ge.shape[0]):
+        assert orc.rel_err(ge[b], g["grad_e"][b]) < REL, b
+        assert not ge[b, int(g["em_len"][b]):].any()
+
+
+def test_viterbi_batched_bit_exact():
+    g = load_npz("viterbi_c4")
+    em = torch.from_numpy(g["em"]).cuda()
+    el = np.full(em.shape[0], em.shape[1], np.int32)
+    paths, scores = C.viterbi_batched(em, el, g["trans"])
+    assert np.array_equal(paths.cpu().numpy(), g["paths"].astype(np.int64))
+    assert np.array_equal(scores.cpu().numpy(), g["scores"])
+    paths, scores = C.viterbi_batched(em, el, None)
+    assert np.array_equal(paths.cpu().numpy(), g["paths_noa"].astype(np.int64))
+    assert np.array_equal(scores.cpu().numpy(), g["scores_noa"])
+
+
+def test_viterbi_batched_ragged_vs_oracle():
+    em, el, _, _, a = orc.synth_asg(77, 5, 300, 29, 1, ragged=True)
+    paths, scores = C.viterbi_batched(torch.from_numpy(em).cuda(), el, a)
+    for b in range(5):
+        p, s = orc.viterbi(em[b, :el[b]], a)
+        assert np.array_equal(paths[b, :el[b]].cpu().numpy(), p)
+        assert not paths[b, el[b]:].any()
+        assert scores[b].item() == s
+
+
+def test_asg_batched_c3_scale_vs_oracle():
+    # C3 shape (T=1600 N=30 L=300) on a subset the oracle finishes in seconds
+    em, el, tg, tl, a = orc.synth_asg(20260002, 8, 1600, 30, 300)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a)
+    loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
+
+
+def test_ctc_batched_c5_scale_vs_oracle():
+    em, el, tg, tl, blank = orc.synth_ctc(20260004, 6, 1600, 30, 300)
+    out = C.ctc_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, blank)
+    loss, ge = orc.ctc_batch(em, el, tg, tl, blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+
+
+def test_full_size_properties():
+    # B=64, T=1600, N=30, L=300: size-independent invariants of the gradients
+    em, el, tg, tl, a = orc.synth_asg(20260005, 64, 1600, 30, 300)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a,
+                                  per_utterance_grad_transitions=True)
+    ge = out.grad_emissions.double()
+    assert ge.sum(dim=2).abs().max().item() < 1e-4          # ASG rows sum to 0
+    assert (out.loss >= -1e-6).all()
+    # both posterior sets sum to T-1 edges -> sum of dA is 0 per utterance
+    assert out.grad_transitions_per_utt.double().sum(dim=(1, 2)).abs().max().item() < 1e-2
+    emc, elc, tgc, tlc, blank = orc.synth_ctc(20260006, 64, 1600, 30, 300)
+    outc = C.ctc_loss_grad_batched(torch.from_numpy(emc).cuda(), elc, tgc, tlc, blank)
+    assert (outc.grad_emissions.double().sum(dim=2) + 1).abs().max().item() < 1e-4
+
+
+def test_batched_guard_fallback_extreme_scale():
+    # +-1e3 scaled inputs break the fp32 scaled domain -> float64 recompute
+    rng = np.random.default_rng(800)
+    em = (rng.normal(size=(3, 5, 3)) * 1e3).astype(np.float32)
+    a = (rng.normal(size=(3, 3)) * 1e3).astype(np.float32)
+    tg = np.array([[0, 1], [1, 2], [2, -1]], dtype=np.int64)
+    tl = np.array([2, 2, 1], dtype=np.int32)
+    el = np.full(3, 5, np.int32)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a)
+    loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=1e-6)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < 1e-5
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < 1e-5
+
+
+def test_batched_errors_name_the_utterance():
+    em, el, tg, tl, a = orc.synth_asg(5, 3, 20, 5, 4)
+    tg[1, 1] = tg[1, 0]                       # consecutive duplicate in utterance 1
+    with pytest.raises(ContractError, match="utterance 1"):
+        C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a)
+    em, el, tg, tl, blank = orc.synth_ctc(6, 3, 20, 5, 4)
+    em[2, 3, 0] = np.nan
+    with pytest.raises(NumericError, match="utterance 2"):
+        C.ctc_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, blank)
+
+
+def test_autograd_functions():
+    em, el, tg, tl, a = orc.synth_asg(9, 3, 40, 6, 8)
+    x = torch.from_numpy(em).cuda().requires_grad_(True)
+    A = torch.from_numpy(a).cuda().requires_grad_(True)
+    w = torch.tensor([0.5, 1.0, 2.0], device="cuda")
+    (C.asg_loss(x, A, el, tg, tl) * w).sum().backward()
+    for b in range(3):
+        _, g1, g2 = orc.asg(em[b], tg[b, :tl[b]], a)
+        assert orc.rel_err(x.grad[b].cpu().numpy(), w[b].item() * g1) < REL
+    want = sum(w[b].item() * orc.asg(em[b], tg[b, :tl[b]], a)[2].astype(np.float64)
+               for b in range(3))
+    assert orc.rel_err(A.grad.cpu().numpy(), want) < REL
