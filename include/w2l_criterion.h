@@ -52,8 +52,12 @@ enum {
   W2L_ERR_TARGET = 3,     /* TargetError           */
   W2L_ERR_INFEASIBLE = 4, /* InfeasibleTargetError */
   W2L_ERR_CUDA = 5,       /* launch / runtime failure */
-  W2L_ERR_COMM = 6        /* collective failure (multi-GPU layer) */
+  W2L_ERR_COMM = 6,       /* collective failure (multi-GPU layer) */
+  W2L_ERR_PRECISION = 7   /* fp32 guard failed and W2L_FLAG_NO_FALLBACK was set */
 };
+
+/* flags for the fp32 batched entry points */
+#define W2L_FLAG_NO_FALLBACK 1u  /* report guard failures instead of recomputing in f64 */
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */
@@ -75,7 +79,7 @@ W2L_API int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int6
                       const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
                       int Lmax, double *loss, float *grad_em, float *grad_trans,
                       float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
-                      w2l_stream_t stream);
+                      unsigned flags, w2l_stream_t stream);
 /* float64-input variant computed entirely by the float64 log-domain kernel:
  * the reference's own numerics ("float64 internals", criterion.py:1-7). */
 W2L_API size_t w2l_asg_workspace_bytes_f64(int B, int Tmax, int N, int Lmax);
@@ -92,7 +96,7 @@ W2L_API size_t w2l_ctc_workspace_bytes(int B, int Tmax, int N, int Lmax);
 W2L_API int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
                       const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
                       double *loss, float *grad_em, int32_t *status, void *ws,
-                      size_t ws_bytes, w2l_stream_t stream);
+                      size_t ws_bytes, unsigned flags, w2l_stream_t stream);
 W2L_API size_t w2l_ctc_workspace_bytes_f64(int B, int Tmax, int N, int Lmax);
 W2L_API int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64_t *tgt,
                           const int32_t *tgt_len, int blank, int B, int Tmax, int N,
@@ -118,6 +122,8 @@ W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const doubl
 W2L_API int w2l_status_first_error(const int32_t *status, int B, int32_t *bad_index,
                            w2l_stream_t stream);
 W2L_API const char *w2l_status_string(int code);
+/* Text of the last CUDA error seen by this thread's calls (then cleared). */
+W2L_API const char *w2l_last_cuda_error(void);
 /* Library build identifier (kernel generation), for provenance in benches. */
 W2L_API const char *w2l_version(void);
 /* Microbenchmarks used for the roofline denominators (MUFU ex2 ops/s and

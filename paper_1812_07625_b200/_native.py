@@ -27,13 +27,13 @@ c_i32_p = ctypes.POINTER(ctypes.c_int32)
 SIGNATURES = {
     "w2l_asg_workspace_bytes": (c_sz, [c_i, c_i, c_i, c_i]),
     "w2l_asg_loss_grad": (c_i, [c_p, c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_p, c_p, c_p, c_p,
-                                c_p, c_p, c_sz, c_p]),
+                                c_p, c_p, c_sz, ctypes.c_uint, c_p]),
     "w2l_asg_workspace_bytes_f64": (c_sz, [c_i, c_i, c_i, c_i]),
     "w2l_asg_loss_grad_f64": (c_i, [c_p, c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_p, c_p, c_p,
                                     c_p, c_p, c_p, c_sz, c_p]),
     "w2l_ctc_workspace_bytes": (c_sz, [c_i, c_i, c_i, c_i]),
     "w2l_ctc_loss_grad": (c_i, [c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_i, c_p, c_p, c_p, c_p,
-                                c_sz, c_p]),
+                                c_sz, ctypes.c_uint, c_p]),
     "w2l_ctc_workspace_bytes_f64": (c_sz, [c_i, c_i, c_i, c_i]),
     "w2l_ctc_loss_grad_f64": (c_i, [c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_i, c_p, c_p, c_p,
                                     c_p, c_sz, c_p]),
@@ -43,11 +43,14 @@ SIGNATURES = {
     "w2l_status_first_error": (c_i, [c_p, c_i, c_i32_p, c_p]),
     "w2l_status_string": (ctypes.c_char_p, [c_i]),
     "w2l_version": (ctypes.c_char_p, []),
+    "w2l_last_cuda_error": (ctypes.c_char_p, []),
     "w2l_probe_peaks": (c_i, [c_d_p, c_d_p, c_d_p]),
 }
 
 # C-ABI status codes (include/w2l_criterion.h)
-OK, ERR_CONTRACT, ERR_NUMERIC, ERR_TARGET, ERR_INFEASIBLE, ERR_CUDA, ERR_COMM = range(7)
+OK, ERR_CONTRACT, ERR_NUMERIC, ERR_TARGET, ERR_INFEASIBLE, ERR_CUDA, ERR_COMM, ERR_PRECISION = \
+    range(8)
+FLAG_NO_FALLBACK = 1
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

@@ -94,7 +94,10 @@ def _workspace(nbytes: int, dev, ws: Optional[torch.Tensor] = None) -> torch.Ten
 
 def _check_call(rc: int, what: str) -> None:
     if rc != nat.OK:
-        raise_for_status(rc, f"{what}: {nat.lib().w2l_status_string(rc).decode()}")
+        detail = nat.lib().w2l_status_string(rc).decode()
+        if rc == nat.ERR_CUDA:
+            detail += f" ({nat.lib().w2l_last_cuda_error().decode()})"
+        raise_for_status(rc, f"{what}: {detail}")
 
 
 def _first_error(status: torch.Tensor):
@@ -347,13 +350,16 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
 def _raise_batch(status: torch.Tensor, what: str) -> None:
     code, bad = _first_error(status)
     if code != nat.OK:
-        raise_for_status(code, f"{what}: utterance {bad}: "
-                               f"{nat.lib().w2l_status_string(code).decode()}")
+        detail = nat.lib().w2l_status_string(code).decode()
+        if code == nat.ERR_CUDA:
+            detail += f" ({nat.lib().w2l_last_cuda_error().decode()})"
+        raise_for_status(code, f"{what}: utterance {bad}: {detail}")
 
 
 def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, check=True,
                           per_utterance_grad_transitions=False, workspace=None,
-                          out: Optional[BatchLossOutput] = None) -> BatchLossOutput:
+                          out: Optional[BatchLossOutput] = None,
+                          fallback: bool = True) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -361,7 +367,9 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     tgt_len int [B]; transitions f32 [N,N] (A[to][from]).  Returns loss f64 [B],
     grad_emissions f32 [B,Tmax,N], grad_transitions f32 [N,N] summed over the
     batch and (optionally) per utterance.  check=True synchronises and raises
-    the reference exception for the first failing utterance."""
+    the reference exception for the first failing utterance.  fallback=False
+    disables the float64 recompute of utterances failing the fp32 guard (they
+    report W2L_ERR_PRECISION instead) -- a diagnostic for the fast path."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -384,7 +392,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     rc = lib.w2l_asg_loss_grad(_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax,
                                _p(out.loss), _p(out.grad_emissions), _p(out.grad_transitions),
                                _p(out.grad_transitions_per_utt), _p(out.status), _p(ws),
-                               ws.numel(), _stream())
+                               ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
     _check_call(rc, "w2l_asg_loss_grad")
     if check:
         _raise_batch(out.status, "asg_loss_grad_batched")
@@ -392,8 +400,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
 
 
 def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *, check=True,
-                          workspace=None, out: Optional[BatchLossOutput] = None
-                          ) -> BatchLossOutput:
+                          workspace=None, out: Optional[BatchLossOutput] = None,
+                          fallback: bool = True) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
     log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2."""
     dev = _device()
@@ -411,7 +419,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     rc = lib.w2l_ctc_loss_grad(_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax,
                                _p(out.loss), _p(out.grad_emissions), _p(out.status), _p(ws),
-                               ws.numel(), _stream())
+                               ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
     _check_call(rc, "w2l_ctc_loss_grad")
     if check:
         _raise_batch(out.status, "ctc_loss_grad_batched")

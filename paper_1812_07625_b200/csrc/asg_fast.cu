@@ -77,6 +77,215 @@ __global__ void token_csr_kernel(const int64_t *tgt, const int32_t *tgt_len, Dim
 }
 
 // ---------------------------------------------------------- chain kernel --
+// Each role is its own non-inlined device function so that its register
+// arrays are allocated independently; row pointers are formed once per
+// utterance and indexed with 32-bit offsets.
+
+struct ChainCtx {
+  const float *trans;
+  int N, T, lane;
+  float amax;
+};
+
+// fcc alpha: lane i owns token i and row i of M (criterion.py:227-231)
+__device__ __noinline__ void fcc_alpha(const ChainCtx c, EmissionPipe &pipe, float (*vec)[32],
+                                       float *out, int *outk, double *lnz) {
+  const int lane = c.lane, N = c.N;
+  float mr[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    mr[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax) : 0.f;
+  float a = lane < N ? pipe.row(0)[lane] : 0.f;
+  int K = 0;
+  vec[0][lane] = a;
+  out[lane] = a;
+  if (lane == 0) outk[0] = 0;
+  for (int t = 1; t < c.T; ++t) {
+    const float et = lane < N ? pipe.row(t)[lane] : 0.f;
+    __syncwarp();
+    const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
+    float acc[8], sm[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 x = pv[q];
+      acc[q] = mr[4 * q] * x.x;
+      acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
+      acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
+      acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
+      sm[q] = (x.x + x.y) + (x.z + x.w);
+    }
+    const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+    const int k = max(-126, min(126, exponent_of(tot)));
+    K += k;
+    a = et * (s * pow2f(-k));
+    vec[t & 1][lane] = a;
+    out[t * 32 + lane] = a;
+    if (lane == 0) outk[t] = K;
+  }
+  const float z = warp_sum(a);
+  if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
+}
+
+// fcc beta' (excludes frame t's emission): lane j owns column j of M (:233-236)
+__device__ __noinline__ void fcc_beta(const ChainCtx c, EmissionPipe &pipe, float (*vec)[32],
+                                      float *out, int *outk, double *lnz) {
+  const int lane = c.lane, N = c.N, T = c.T;
+  float mc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    mc[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax) : 0.f;
+  float bb = lane < N ? 1.f : 0.f;
+  int K = 0;
+  out[(T - 1) * 32 + lane] = bb;
+  if (lane == 0) outk[T - 1] = 0;
+  for (int u = T - 1; u >= 1; --u) {
+    const float eu = lane < N ? pipe.row(u)[lane] : 0.f;
+    vec[u & 1][lane] = eu * bb;
+    __syncwarp();
+    const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
+    float acc[8], sm[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 x = pv[q];
+      acc[q] = mc[4 * q] * x.x;
+      acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
+      acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
+      acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
+      sm[q] = (x.x + x.y) + (x.z + x.w);
+    }
+    const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+    const int k = max(-126, min(126, exponent_of(tot)));
+    K += k;
+    bb = s * pow2f(-k);
+    out[(u - 1) * 32 + lane] = bb;
+    if (lane == 0) outk[u - 1] = K;
+  }
+  const float e0 = lane < N ? pipe.row(0)[lane] : 0.f;
+  const float z = warp_sum(e0 * bb);
+  if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
+}
+
+// fac chain weights for this lane's states l = lane*SPL + k: token, stay
+// weight M[y_l][y_l] and the step weight (alpha: INTO l from l-1; beta: from
+// l INTO l+1).  Padding states read the zero emission column N.
+template <int SPL>
+__device__ __forceinline__ void fac_weights(const ChainCtx c, const int64_t *y, int L,
+                                            bool is_alpha, int (&tok)[SPL], float (&S)[SPL],
+                                            float (&P)[SPL]) {
+  const int N = c.N;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    const int l = c.lane * SPL + k;
+    if (l < L) {
+      const int yl = (int)y[l];
+      tok[k] = yl;
+      S[k] = expf(c.trans[yl * N + yl] - c.amax);
+      if (is_alpha)
+        P[k] = l > 0 ? expf(c.trans[yl * N + (int)y[l - 1]] - c.amax) : 0.f;
+      else
+        P[k] = l + 1 < L ? expf(c.trans[(int)y[l + 1] * N + yl] - c.amax) : 0.f;
+    } else {
+      tok[k] = N;
+      S[k] = 0.f;
+      P[k] = 0.f;
+    }
+  }
+}
+
+// fac alpha (criterion.py:193-203) in block floating point
+template <int SPL>
+__device__ __noinline__ void fac_alpha(const ChainCtx c, EmissionPipe &pipe, const int64_t *y,
+                                       int L, float *out, int *oute, int lp, double *lnz) {
+  const int lane = c.lane, T = c.T;
+  int tok[SPL];
+  float S[SPL], P[SPL], v[SPL];
+  fac_weights<SPL>(c, y, L, true, tok, S, P);
+  const float *r0 = pipe.row(0);
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) v[k] = 0.f;
+  int ex = 0;
+  if (lane == 0) v[0] = r0[tok[0]];          // only the first target state at t = 0 (:194)
+  lane_renorm<SPL>(v, ex);
+  lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
+  for (int t = 1; t < T; ++t) {
+    const float *r = pipe.row(t);
+    float E[SPL];
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) E[k] = r[tok[k]];
+    float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
+    int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
+    if (lane == 0) {
+      nb = 0.f;
+      nbe = kNegExp;
+    }
+    int dd = nbe - ex;
+    if (dd > 64) {  // the neighbour dominates: rebase this lane to its exponent
+      const float sc = pow2f(-dd);
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) v[k] *= sc;
+      ex = nbe;
+      dd = 0;
+    }
+    const float nbs = nb * pow2f(dd);
+#pragma unroll
+    for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
+    v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
+    lane_renorm<SPL>(v, ex);
+    lane_store<SPL>(v, ex, out, oute, lp, lane, t);
+  }
+  // fac score = alpha_{T-1}[L-1] (:203)
+  const int lastl = L - 1;
+  float vl = 0.f;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) vl = (lane * SPL + k == lastl) ? v[k] : vl;
+  if (lane == lastl / SPL) *lnz = log((double)vl) + (double)ex * 0.6931471805599453;
+}
+
+// fac beta' (criterion.py:205-212, without frame t's emission)
+template <int SPL>
+__device__ __noinline__ void fac_beta(const ChainCtx c, EmissionPipe &pipe, const int64_t *y,
+                                      int L, float *out, int *oute, int lp, double *lnz) {
+  const int lane = c.lane, T = c.T;
+  int tok[SPL];
+  float S[SPL], P[SPL], v[SPL];
+  fac_weights<SPL>(c, y, L, false, tok, S, P);
+  const int lastl = L - 1;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
+  int ex = (lane == lastl / SPL) ? 0 : kNegExp;
+  lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
+  for (int u = T - 1; u >= 1; --u) {
+    const float *r = pipe.row(u);
+    float wv[SPL];
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) wv[k] = r[tok[k]] * v[k];
+    float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
+    int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
+    if (lane == 31) {
+      nb = 0.f;
+      nbe = kNegExp;
+    }
+    int dd = nbe - ex;
+    if (dd > 64) {
+      const float sc = pow2f(-dd);
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) wv[k] *= sc;
+      ex = nbe;
+      dd = 0;
+    }
+    const float nbs = nb * pow2f(dd);
+#pragma unroll
+    for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
+    v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
+    lane_renorm<SPL>(v, ex);
+    lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
+  }
+  const float *r0 = pipe.row(0);
+  if (lane == 0) *lnz = log((double)(r0[tok[0]] * v[0])) + (double)ex * 0.6931471805599453;
+}
+
 template <int SPL>
 __global__ void __launch_bounds__(32)
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
@@ -85,202 +294,29 @@ __global__ void __launch_bounds__(32)
                      const int32_t *__restrict__ status) {
   __shared__ __align__(16) float chunk[2 * kChunk * 33];
   __shared__ __align__(16) float vec[2][32];
-  const int b = blockIdx.x, role = blockIdx.y, lane = threadIdx.x;
+  const int b = blockIdx.x, role = blockIdx.y;
   if (status[b] != W2L_OK) return;
-  const int T = em_len[b], N = d.N;
-  const float amax = trans_max(trans, N);
-  const bool fwd = (role == 0 || role == 2);
+  ChainCtx c;
+  c.trans = trans;
+  c.N = d.N;
+  c.T = em_len[b];
+  c.lane = threadIdx.x;
+  c.amax = trans_max(trans, d.N);
   EmissionPipe pipe;
-  pipe.init(chunk, em + (size_t)b * d.Tmax * N, T, N, fwd);
+  pipe.init(chunk, em + (size_t)b * d.Tmax * d.N, c.T, d.N, role == 0 || role == 2);
   const size_t row0 = (size_t)b * d.Tmax;
-
-  if (role == 0) {
-    // ---- fcc alpha: lane i, row i of M in registers
-    float mr[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      mr[j] = (lane < N && j < N) ? expf(trans[lane * N + j] - amax) : 0.f;
-    float a = lane < N ? pipe.row(0)[lane] : 0.f;
-    int K = 0;
-    vec[0][lane] = a;
-    w.fcc_a[row0 * 32 + lane] = a;
-    if (lane == 0) w.fcc_ka[row0] = 0;
-    for (int t = 1; t < T; ++t) {
-      const float et = lane < N ? pipe.row(t)[lane] : 0.f;
-      __syncwarp();
-      const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
-      float acc[8], sm[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 x = pv[q];
-        acc[q] = mr[4 * q] * x.x;
-        acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
-        acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
-        acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
-        sm[q] = (x.x + x.y) + (x.z + x.w);
-      }
-      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-      const int k = max(-126, min(126, exponent_of(tot)));
-      K += k;
-      a = et * (s * pow2f(-k));
-      vec[t & 1][lane] = a;
-      w.fcc_a[(row0 + t) * 32 + lane] = a;
-      if (lane == 0) w.fcc_ka[row0 + t] = K;
-    }
-    const float z = warp_sum(a);
-    if (lane == 0) w.scal[b * 4 + 0] = log((double)z) + (double)K * 0.6931471805599453;
-  } else if (role == 1) {
-    // ---- fcc beta' (excludes frame t's emission): lane j, column j of M
-    float mc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      mc[i] = (lane < N && i < N) ? expf(trans[i * N + lane] - amax) : 0.f;
-    float bb = lane < N ? 1.f : 0.f;
-    int K = 0;
-    w.fcc_b[(row0 + T - 1) * 32 + lane] = bb;
-    if (lane == 0) w.fcc_kb[row0 + T - 1] = 0;
-    for (int u = T - 1; u >= 1; --u) {
-      const float eu = lane < N ? pipe.row(u)[lane] : 0.f;
-      vec[u & 1][lane] = eu * bb;
-      __syncwarp();
-      const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
-      float acc[8], sm[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 x = pv[q];
-        acc[q] = mc[4 * q] * x.x;
-        acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
-        acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
-        acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
-        sm[q] = (x.x + x.y) + (x.z + x.w);
-      }
-      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-      const int k = max(-126, min(126, exponent_of(tot)));
-      K += k;
-      bb = s * pow2f(-k);
-      w.fcc_b[(row0 + u - 1) * 32 + lane] = bb;
-      if (lane == 0) w.fcc_kb[row0 + u - 1] = K;
-    }
-    const float e0 = lane < N ? pipe.row(0)[lane] : 0.f;
-    const float z = warp_sum(e0 * bb);
-    if (lane == 0) w.scal[b * 4 + 1] = log((double)z) + (double)K * 0.6931471805599453;
-  } else {
-    // ---- fac chains: state l = lane*SPL + k, per-lane power-of-two exponent
-    const int L = tgt_len[b];
-    const int64_t *y = tgt + (size_t)b * d.Lmax;
-    int tok[SPL];
-    float S[SPL], P[SPL];
-    const bool is_alpha = (role == 2);
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      const int l = lane * SPL + k;
-      if (l < L) {
-        const int yl = (int)y[l];
-        tok[k] = yl;
-        S[k] = expf(trans[yl * N + yl] - amax);
-        if (is_alpha) {
-          P[k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
-        } else {  // beta uses the step weight INTO the next state
-          P[k] = l + 1 < L ? expf(trans[(int)y[l + 1] * N + yl] - amax) : 0.f;
-        }
-      } else {
-        tok[k] = N;  // zero column
-        S[k] = 0.f;
-        P[k] = 0.f;
-      }
-    }
-    float v[SPL];
-    int ex = 0;
-    float *out = is_alpha ? w.fac_a : w.fac_b;
-    int *oute = is_alpha ? w.fac_ea : w.fac_eb;
-    const int lp = w.lpad;
-    
-    
-    if (is_alpha) {
-      // t = 0: only the first target state is reachable (:194)
-      const float *r0 = pipe.row(0);
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) v[k] = 0.f;
-      ex = 0;
-      if (lane == 0) v[0] = r0[tok[0]];
-      lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, 0);
-      for (int t = 1; t < T; ++t) {
-        const float *r = pipe.row(t);
-        float E[SPL];
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) E[k] = r[tok[k]];
-        float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
-        int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
-        if (lane == 0) {
-          nb = 0.f;
-          nbe = kNegExp;
-        }
-        int dd = nbe - ex;
-        if (dd > 64) {  // neighbour dominates: rebase this lane to its exponent
-          const float sc = pow2f(-dd);
-#pragma unroll
-          for (int k = 0; k < SPL; ++k) v[k] *= sc;
-          ex = nbe;
-          dd = 0;
-        }
-        const float nbs = nb * pow2f(dd);
-#pragma unroll
-        for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
-        v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
-        lane_renorm<SPL>(v, ex);
-        lane_store<SPL>(v, ex, out, oute, row0, lp, lane, t);
-      }
-      // fac score = alpha_{T-1}[L-1] (:203)
-      const int lastl = L - 1;
-      if (lane == lastl / SPL) {
-        float vl = 0.f;
-#pragma unroll
-        for (int k = 0; k < SPL; ++k)
-          if (k == lastl % SPL) vl = v[k];
-        w.scal[b * 4 + 2] = log((double)vl) + (double)ex * 0.6931471805599453;
-      }
-    } else {
-      // beta'_{T-1} = 1 on the last target state, 0 elsewhere
-      const int lastl = L - 1;
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
-      ex = (lane == lastl / SPL) ? 0 : kNegExp;
-      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, T - 1);
-      for (int u = T - 1; u >= 1; --u) {
-        const float *r = pipe.row(u);
-        float wv[SPL];
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) wv[k] = r[tok[k]] * v[k];
-        float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
-        int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
-        if (lane == 31) {
-          nb = 0.f;
-          nbe = kNegExp;
-        }
-        int dd = nbe - ex;
-        if (dd > 64) {
-          const float sc = pow2f(-dd);
-#pragma unroll
-          for (int k = 0; k < SPL; ++k) wv[k] *= sc;
-          ex = nbe;
-          dd = 0;
-        }
-        const float nbs = nb * pow2f(dd);
-#pragma unroll
-        for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
-        v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
-        lane_renorm<SPL>(v, ex);
-        lane_store<SPL>(v, ex, out, oute, row0, lp, lane, u - 1);
-      }
-      const float *r0 = pipe.row(0);
-      if (lane == 0) {
-        const float z = r0[tok[0]] * v[0];
-        w.scal[b * 4 + 3] = log((double)z) + (double)ex * 0.6931471805599453;
-      }
-    }
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  switch (role) {
+    case 0: fcc_alpha(c, pipe, vec, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0); break;
+    case 1: fcc_beta(c, pipe, vec, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1); break;
+    case 2:
+      fac_alpha<SPL>(c, pipe, y, tgt_len[b], w.fac_a + row0 * w.lpad, w.fac_ea + row0 * 32,
+                     w.lpad, w.scal + b * 4 + 2);
+      break;
+    default:
+      fac_beta<SPL>(c, pipe, y, tgt_len[b], w.fac_b + row0 * w.lpad, w.fac_eb + row0 * 32,
+                    w.lpad, w.scal + b * 4 + 3);
+      break;
   }
 }
 

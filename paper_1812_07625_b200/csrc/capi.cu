@@ -14,7 +14,13 @@ namespace {
 constexpr int kMaxExactSlotsFallback = 8;
 constexpr int kMaxExactSlotsF64 = 32;
 
-inline int from_cuda(cudaError_t e) { return e == cudaSuccess ? W2L_OK : W2L_ERR_CUDA; }
+thread_local cudaError_t g_last_cuda = cudaSuccess;  // per calling thread, like cudaGetLastError
+
+inline int from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return W2L_OK;
+  g_last_cuda = e;
+  return W2L_ERR_CUDA;
+}
 
 bool dims_ok(int B, int Tmax, int N, int Lmax, int max_l) {
   return B >= 0 && Tmax >= 1 && N >= 1 && N <= W2L_MAX_TOKENS && Lmax >= 0 && Lmax <= max_l;
@@ -39,6 +45,12 @@ extern "C" {
 
 const char *w2l_version(void) { return "w2l-criterion sm_100a r1 (scaled-linear fp32 + f64 exact)"; }
 
+const char *w2l_last_cuda_error(void) {
+  const cudaError_t e = g_last_cuda;
+  g_last_cuda = cudaSuccess;
+  return cudaGetErrorString(e);
+}
+
 const char *w2l_status_string(int code) {
   switch (code) {
     case W2L_OK: return "ok";
@@ -48,6 +60,7 @@ const char *w2l_status_string(int code) {
     case W2L_ERR_INFEASIBLE: return "infeasible target";
     case W2L_ERR_CUDA: return "CUDA error";
     case W2L_ERR_COMM: return "communication error";
+    case W2L_ERR_PRECISION: return "fp32 consistency guard failed";
     default: return "unknown";
   }
 }
@@ -65,11 +78,11 @@ int w2l_status_first_error(const int32_t *status, int B, int32_t *bad_index,
   if (err == cudaSuccess) err = cudaStreamSynchronize((cudaStream_t)stream);
   int code = W2L_OK;
   if (err != cudaSuccess) {
-    code = W2L_ERR_CUDA;
+    code = from_cuda(err);
   } else {
     for (int b = 0; b < B; ++b) {
       if (host[b] != W2L_OK) {
-        code = host[b] == kNeedsExact ? W2L_ERR_NUMERIC : host[b];
+        code = host[b] == kNeedsExact ? W2L_ERR_PRECISION : host[b];
         if (bad_index) *bad_index = b;
         break;
       }
@@ -104,13 +117,14 @@ int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt
                       const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
                       int Lmax, double *loss, float *grad_em, float *grad_trans,
                       float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
-                      w2l_stream_t stream) {
+                      unsigned flags, w2l_stream_t stream) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
       !status || !ws)
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_asg_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
+  const bool fallback = !(flags & W2L_FLAG_NO_FALLBACK);
   cudaStream_t s = (cudaStream_t)stream;
   Dims d{B, Tmax, N, Lmax};
   AsgFastWs w;
@@ -123,9 +137,11 @@ int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
                                  status, s));
   if (rc) return rc;
-  rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
-                                         slots, loss, grad_em, ga, status, s));
-  if (rc) return rc;
+  if (fallback) {
+    rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
+                                           slots, loss, grad_em, ga, status, s));
+    if (rc) return rc;
+  }
   return from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
 }
 
@@ -189,7 +205,7 @@ size_t w2l_ctc_workspace_bytes(int B, int Tmax, int N, int Lmax) {
 int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
                       const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
                       double *loss, float *grad_em, int32_t *status, void *ws,
-                      size_t ws_bytes, w2l_stream_t stream) {
+                      size_t ws_bytes, unsigned flags, w2l_stream_t stream) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
@@ -204,6 +220,7 @@ int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *t
   if (rc) return rc;
   rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s));
   if (rc) return rc;
+  if (flags & W2L_FLAG_NO_FALLBACK) return W2L_OK;
   return from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
                                            asg_slots(B), slots, loss, grad_em, status, s));
 }

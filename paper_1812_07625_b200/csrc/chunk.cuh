@@ -107,11 +107,11 @@ __device__ __forceinline__ void lane_renorm(float (&v)[SPL], int &ex) {
 // one frame's chain row, slot-major ([k][lane]) so every store is coalesced
 template <int SPL>
 __device__ __forceinline__ void lane_store(const float (&v)[SPL], int ex, float *out, int *oute,
-                                           size_t row0, int lp, int lane, int t) {
-  float *o = out + (row0 + t) * lp;
+                                           int lp, int lane, int t) {
+  float *o = out + t * lp + lane;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) o[k * 32 + lane] = v[k];
-  oute[(row0 + t) * 32 + lane] = ex;
+  for (int k = 0; k < SPL; ++k) o[k * 32] = v[k];
+  oute[t * 32 + lane] = ex;
 }
 
 }  // namespace w2l

@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(32)
 
   float v[SPL];
   int ex = 0;
-  float *out = fwd ? w.a : w.b;
-  int *oute = fwd ? w.ea : w.eb;
+  float *out = (fwd ? w.a : w.b) + row0 * w.lpad;
+  int *oute = (fwd ? w.ea : w.eb) + row0 * 32;
   const int lp = w.lpad;
   
   
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(32)
       if (S > 1) v[1] = r0[lab[1]];
     }
     lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, row0, lp, lane, 0);
+    lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
     for (int t = 1; t < T; ++t) {
       const float *r = pipe.row(t);
       float E[SPL];
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32)
       v[0] = E[0] * fmaf(sk[0], n2, v[0] + n1);
       v[1] = v1;
       lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, t);
+      lane_store<SPL>(v, ex, out, oute, lp, lane, t);
     }
     // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
     float part = 0.f;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(32)
     }
     ex = 0;
     lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, row0, lp, lane, T - 1);
+    lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
     for (int u = T - 1; u >= 1; --u) {
       const float *r = pipe.row(u);
       float wv[SPL];
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(32)
       v[SPL - 2] = fmaf(sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
       v[SPL - 1] = fmaf(sk2[SPL - 1], n2, wv[SPL - 1] + n1);
       lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, row0, lp, lane, u - 1);
+      lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
     }
     const float *r0 = pipe.row(0);
     if (lane == 0) {

@@ -42,6 +42,7 @@ STATUS_CLASSES = {
     4: InfeasibleTargetError,
     5: DeviceError,
     6: DeviceError,
+    7: NumericError,
 }
 
 

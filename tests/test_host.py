@@ -41,7 +41,7 @@ def test_workspace_sizes_and_contract_codes():
     assert lib.w2l_viterbi_workspace_bytes(4, 1600, 30) > 0
     # host-side contract violations return W2L_ERR_CONTRACT without touching the GPU
     rc = lib.w2l_asg_loss_grad(None, None, None, None, None, 1, 10, 40, 3, None, None, None,
-                               None, None, None, 0, None)
+                               None, None, None, 0, 0, None)
     assert rc == nat.ERR_CONTRACT
     assert lib.w2l_status_string(4).decode() == "infeasible target"
     bad = ctypes.c_int32(7)
