@@ -95,13 +95,15 @@ __device__ __noinline__ void fcc_alpha(const ChainCtx c, EmissionPipe &pipe, flo
 #pragma unroll
   for (int j = 0; j < 32; ++j)
     mr[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax) : 0.f;
-  float a = lane < N ? pipe.row(0)[lane] : 0.f;
+  const float *r0 = pipe.row(0);  // every lane walks the pipe (it syncs the warp)
+  float a = lane < N ? r0[lane] : 0.f;
   int K = 0;
   vec[0][lane] = a;
   out[lane] = a;
   if (lane == 0) outk[0] = 0;
   for (int t = 1; t < c.T; ++t) {
-    const float et = lane < N ? pipe.row(t)[lane] : 0.f;
+    const float *rt = pipe.row(t);
+    const float et = lane < N ? rt[lane] : 0.f;
     __syncwarp();
     const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
     float acc[8], sm[8];
@@ -140,7 +142,8 @@ __device__ __noinline__ void fcc_beta(const ChainCtx c, EmissionPipe &pipe, floa
   out[(T - 1) * 32 + lane] = bb;
   if (lane == 0) outk[T - 1] = 0;
   for (int u = T - 1; u >= 1; --u) {
-    const float eu = lane < N ? pipe.row(u)[lane] : 0.f;
+    const float *ru = pipe.row(u);
+    const float eu = lane < N ? ru[lane] : 0.f;
     vec[u & 1][lane] = eu * bb;
     __syncwarp();
     const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
@@ -162,7 +165,8 @@ __device__ __noinline__ void fcc_beta(const ChainCtx c, EmissionPipe &pipe, floa
     out[(u - 1) * 32 + lane] = bb;
     if (lane == 0) outk[u - 1] = K;
   }
-  const float e0 = lane < N ? pipe.row(0)[lane] : 0.f;
+  const float *r0 = pipe.row(0);
+  const float e0 = lane < N ? r0[lane] : 0.f;
   const float z = warp_sum(e0 * bb);
   if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
 }
