@@ -35,7 +35,6 @@ namespace {
 
 constexpr int kGradFramesPerBlock = 64;
 constexpr int kGradWarps = 8;
-constexpr float kLn2 = 0.6931471805599453f;
 
 __device__ __forceinline__ float trans_max(const float *trans, int N) {
   float m = -CUDART_INF_F;
@@ -43,130 +42,142 @@ __device__ __forceinline__ float trans_max(const float *trans, int N) {
   return warp_max(m);
 }
 
-// ------------------------------------------------------------ token CSR --
-// perm lists the chain states grouped by token (ascending state order inside
-// a token), tok_start[k]..tok_start[k+1] its range.  state_mul/off map a
-// target position l to its chain state (ASG: l; CTC: 2l+1).
-__global__ void token_csr_kernel(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
-                                 int state_mul, int state_off, int *perm, int *tok_start,
-                                 const int32_t *status) {
-  const int b = blockIdx.x;
-  __shared__ int cnt[33];
-  if (status[b] != W2L_OK) return;
-  const int L = tgt_len[b];
-  const int64_t *y = tgt + (size_t)b * d.Lmax;
-  if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[(int)y[l]], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k <= d.N; ++k) {
-      const int c = k < d.N ? cnt[k] : 0;
-      tok_start[b * 33 + k] = acc;
-      acc += c;
-    }
-  }
-  __syncthreads();
-  for (int l = threadIdx.x; l < L; l += blockDim.x) {
-    const int tk = (int)y[l];
-    int before = 0;
-    for (int q = 0; q < l; ++q) before += (y[q] == tk);
-    perm[(size_t)b * lpad + tok_start[b * 33 + tk] + before] = l * state_mul + state_off;
-  }
-}
-
 // ---------------------------------------------------------- chain kernel --
-// Each role is its own non-inlined device function so that its register
-// arrays are allocated independently; row pointers are formed once per
-// utterance and indexed with 32-bit offsets.
+// One warp per (utterance, role).  Loops are chunk-major: a chunk of kChunk
+// frames is staged (cp.async, one chunk in flight) and converted to Et once,
+// then the inner loop walks its rows with a plain shared-memory row pointer.
+// Rescaling is lazy:
+//   fcc: the normaliser of step t is the exponent of sum(alpha_{t-2}), which
+//        a spare lane (row of ones in M) produces as a by-product of step t-1's
+//        mat-vec and a shuffle delivers one step later -- off the critical
+//        path (for N = 32 every lane sums the vector instead);
+//   fac: each lane renormalises its block every kRenorm frames.
+// Both are exact (powers of two); growth between rescales is bounded by
+// 30^2 (fcc) and 2^kRenorm (fac), shrinkage by exp(-2 range(A)) resp. the
+// emissions -- anything the bounds cannot cover trips the guard.
 
-struct ChainCtx {
-  const float *trans;
-  int N, T, lane;
-  float amax;
-};
-
-// fcc alpha: lane i owns token i and row i of M (criterion.py:227-231)
-__device__ __noinline__ void fcc_alpha(const ChainCtx c, EmissionPipe &pipe, float (*vec)[32],
-                                       float *out, int *outk, double *lnz) {
-  const int lane = c.lane, N = c.N;
+// fcc alpha (criterion.py:227-231): lane i owns token i and row i of M
+__device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * 33],
+                                          float (*vec)[32], float *out, int *outk,
+                                          double *lnz) {
+  const int lane = c.lane, N = c.N, T = c.T;
+  const bool spare = N < 32;  // lane N sums the vector (row of ones)
   float mr[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j)
-    mr[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax) : 0.f;
-  const float *r0 = pipe.row(0);  // every lane walks the pipe (it syncs the warp)
-  float a = lane < N ? r0[lane] : 0.f;
-  int K = 0;
-  vec[0][lane] = a;
-  out[lane] = a;
-  if (lane == 0) outk[0] = 0;
-  for (int t = 1; t < c.T; ++t) {
-    const float *rt = pipe.row(t);
-    const float et = lane < N ? rt[lane] : 0.f;
-    __syncwarp();
-    const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
-    float acc[8], sm[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 x = pv[q];
-      acc[q] = mr[4 * q] * x.x;
-      acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
-      acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
-      acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
-      sm[q] = (x.x + x.y) + (x.z + x.w);
+    mr[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax)
+                                : ((spare && lane == N && j < N) ? 1.f : 0.f);
+  const int nch = (T + kChunk - 1) / kChunk;
+  stage_issue(chunk[0], c, 0);
+  float a = 0.f;
+  int K = 0, kpend = 0;  // exponent measured one step ago, applied now
+  for (int ch = 0; ch < nch; ++ch) {
+    float *buf = chunk[ch & 1];
+    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+    stage_convert(buf, c, rows);
+    if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
+    int r = 0;
+    if (ch == 0) {
+      a = lane < N ? buf[lane] : 0.f;
+      vec[0][lane] = lane < N ? a : 0.f;
+      out[lane] = lane < N ? a : 0.f;
+      if (lane == 0) outk[0] = 0;
+      r = 1;
     }
-    const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-    const int k = max(-126, min(126, exponent_of(tot)));
-    K += k;
-    a = et * (s * pow2f(-k));
-    vec[t & 1][lane] = a;
-    out[t * 32 + lane] = a;
-    if (lane == 0) outk[t] = K;
+    for (; r < rows; ++r) {
+      const int t = t0 + r;
+      const float et = buf[r * c.stride + (lane < N ? lane : N)];
+      __syncwarp();
+      const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = pv[q];
+        acc[q] = mr[4 * q] * x.x;
+        acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
+        acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
+        acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
+      }
+      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      int knew;
+      if (spare) {
+        knew = exponent_of(__shfl_sync(0xffffffffu, s, N));  // sum(alpha_{t-1})
+      } else {
+        float tot = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
+        knew = exponent_of(tot);
+      }
+      const int k = kpend;
+      kpend = max(-126, min(126, knew));
+      K += k;
+      a = et * (s * pow2f(-k));
+      vec[t & 1][lane] = lane < N ? a : 0.f;
+      if (lane < N) out[t * 32 + lane] = a;
+      if (lane == 0) outk[t] = K;
+    }
   }
-  const float z = warp_sum(a);
+  const float z = warp_sum(lane < N ? a : 0.f);
   if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
 }
 
-// fcc beta' (excludes frame t's emission): lane j owns column j of M (:233-236)
-__device__ __noinline__ void fcc_beta(const ChainCtx c, EmissionPipe &pipe, float (*vec)[32],
-                                      float *out, int *outk, double *lnz) {
+// fcc beta' (excludes frame t's emission; :233-236): lane j owns column j
+__device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChunk * 33],
+                                         float (*vec)[32], float *out, int *outk,
+                                         double *lnz) {
   const int lane = c.lane, N = c.N, T = c.T;
+  const bool spare = N < 32;
   float mc[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i)
-    mc[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax) : 0.f;
+    mc[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax)
+                                : ((spare && lane == N && i < N) ? 1.f : 0.f);
+  const int nch = (T + kChunk - 1) / kChunk;
+  stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
   float bb = lane < N ? 1.f : 0.f;
-  int K = 0;
+  int K = 0, kpend = 0;
   out[(T - 1) * 32 + lane] = bb;
   if (lane == 0) outk[T - 1] = 0;
-  for (int u = T - 1; u >= 1; --u) {
-    const float *ru = pipe.row(u);
-    const float eu = lane < N ? ru[lane] : 0.f;
-    vec[u & 1][lane] = eu * bb;
-    __syncwarp();
-    const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
-    float acc[8], sm[8];
+  float e0 = 0.f;
+  for (int ch = nch - 1; ch >= 0; --ch) {
+    float *buf = chunk[ch & 1];
+    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+    stage_convert(buf, c, rows);
+    if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
+    for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+      const int u = t0 + r;  // consumes frame u, produces beta'_{u-1}
+      const float eu = buf[r * c.stride + (lane < N ? lane : N)];
+      vec[u & 1][lane] = lane < N ? eu * bb : 0.f;
+      __syncwarp();
+      const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
+      float acc[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 x = pv[q];
-      acc[q] = mc[4 * q] * x.x;
-      acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
-      acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
-      acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
-      sm[q] = (x.x + x.y) + (x.z + x.w);
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = pv[q];
+        acc[q] = mc[4 * q] * x.x;
+        acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
+        acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
+        acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
+      }
+      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      int knew;
+      if (spare) {
+        knew = exponent_of(__shfl_sync(0xffffffffu, s, N));
+      } else {
+        float tot = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
+        knew = exponent_of(tot);
+      }
+      const int k = kpend;
+      kpend = max(-126, min(126, knew));
+      K += k;
+      bb = lane < N ? s * pow2f(-k) : 0.f;
+      if (lane < N) out[(u - 1) * 32 + lane] = bb;
+      if (lane == 0) outk[u - 1] = K;
     }
-    const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    const float tot = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-    const int k = max(-126, min(126, exponent_of(tot)));
-    K += k;
-    bb = s * pow2f(-k);
-    out[(u - 1) * 32 + lane] = bb;
-    if (lane == 0) outk[u - 1] = K;
+    if (ch == 0) e0 = lane < N ? buf[lane] : 0.f;
   }
-  const float *r0 = pipe.row(0);
-  const float e0 = lane < N ? r0[lane] : 0.f;
   const float z = warp_sum(e0 * bb);
   if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
 }
@@ -175,7 +186,7 @@ __device__ __noinline__ void fcc_beta(const ChainCtx c, EmissionPipe &pipe, floa
 // weight M[y_l][y_l] and the step weight (alpha: INTO l from l-1; beta: from
 // l INTO l+1).  Padding states read the zero emission column N.
 template <int SPL>
-__device__ __forceinline__ void fac_weights(const ChainCtx c, const int64_t *y, int L,
+__device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y, int L,
                                             bool is_alpha, int (&tok)[SPL], float (&S)[SPL],
                                             float (&P)[SPL]) {
   const int N = c.N;
@@ -200,44 +211,49 @@ __device__ __forceinline__ void fac_weights(const ChainCtx c, const int64_t *y, 
 
 // fac alpha (criterion.py:193-203) in block floating point
 template <int SPL>
-__device__ __noinline__ void fac_alpha(const ChainCtx c, EmissionPipe &pipe, const int64_t *y,
-                                       int L, float *out, int *oute, int lp, double *lnz) {
+__device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * 33],
+                                          const int64_t *y, int L, float *out, int *oute,
+                                          int lp, double *lnz) {
   const int lane = c.lane, T = c.T;
   int tok[SPL];
   float S[SPL], P[SPL], v[SPL];
   fac_weights<SPL>(c, y, L, true, tok, S, P);
-  const float *r0 = pipe.row(0);
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) v[k] = 0.f;
   int ex = 0;
-  if (lane == 0) v[0] = r0[tok[0]];          // only the first target state at t = 0 (:194)
-  lane_renorm<SPL>(v, ex);
-  lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
-  for (int t = 1; t < T; ++t) {
-    const float *r = pipe.row(t);
-    float E[SPL];
+  const int nch = (T + kChunk - 1) / kChunk;
+  stage_issue(chunk[0], c, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    float *buf = chunk[ch & 1];
+    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+    stage_convert(buf, c, rows);
+    if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
+    int r = 0;
+    if (ch == 0) {  // t = 0: only the first target state is reachable (:194)
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) E[k] = r[tok[k]];
-    float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
-    int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
-    if (lane == 0) {
-      nb = 0.f;
-      nbe = kNegExp;
+      for (int k = 0; k < SPL; ++k) v[k] = 0.f;
+      if (lane == 0) v[0] = buf[tok[0]];
+      lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
+      r = 1;
     }
-    int dd = nbe - ex;
-    if (dd > 64) {  // the neighbour dominates: rebase this lane to its exponent
-      const float sc = pow2f(-dd);
+    for (; r < rows; ++r) {
+      const int t = t0 + r;
+      const float *row = buf + r * c.stride;
+      float E[SPL];
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) v[k] *= sc;
-      ex = nbe;
-      dd = 0;
+      for (int k = 0; k < SPL; ++k) E[k] = row[tok[k]];
+      float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
+      int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
+      if (lane == 0) {
+        nb = 0.f;
+        nbe = kNegExp;
+      }
+      const float nbs = align_neighbour<SPL>(nb, nbe, v, ex);
+#pragma unroll
+      for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
+      v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
+      if ((t & (kRenorm - 1)) == 0 || t == T - 1) lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, lp, lane, t);
     }
-    const float nbs = nb * pow2f(dd);
-#pragma unroll
-    for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
-    v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
-    lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, lp, lane, t);
   }
   // fac score = alpha_{T-1}[L-1] (:203)
   const int lastl = L - 1;
@@ -249,8 +265,9 @@ __device__ __noinline__ void fac_alpha(const ChainCtx c, EmissionPipe &pipe, con
 
 // fac beta' (criterion.py:205-212, without frame t's emission)
 template <int SPL>
-__device__ __noinline__ void fac_beta(const ChainCtx c, EmissionPipe &pipe, const int64_t *y,
-                                      int L, float *out, int *oute, int lp, double *lnz) {
+__device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * 33],
+                                         const int64_t *y, int L, float *out, int *oute,
+                                         int lp, double *lnz) {
   const int lane = c.lane, T = c.T;
   int tok[SPL];
   float S[SPL], P[SPL], v[SPL];
@@ -260,34 +277,36 @@ __device__ __noinline__ void fac_beta(const ChainCtx c, EmissionPipe &pipe, cons
   for (int k = 0; k < SPL; ++k) v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
   int ex = (lane == lastl / SPL) ? 0 : kNegExp;
   lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
-  for (int u = T - 1; u >= 1; --u) {
-    const float *r = pipe.row(u);
-    float wv[SPL];
+  const int nch = (T + kChunk - 1) / kChunk;
+  stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
+  float e0 = 0.f;
+  for (int ch = nch - 1; ch >= 0; --ch) {
+    float *buf = chunk[ch & 1];
+    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+    stage_convert(buf, c, rows);
+    if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
+    for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+      const int u = t0 + r;
+      const float *row = buf + r * c.stride;
+      float wv[SPL];
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) wv[k] = r[tok[k]] * v[k];
-    float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
-    int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
-    if (lane == 31) {
-      nb = 0.f;
-      nbe = kNegExp;
+      for (int k = 0; k < SPL; ++k) wv[k] = row[tok[k]] * v[k];
+      float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
+      int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
+      if (lane == 31) {
+        nb = 0.f;
+        nbe = kNegExp;
+      }
+      const float nbs = align_neighbour<SPL>(nb, nbe, wv, ex);
+#pragma unroll
+      for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
+      v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
+      if (((u - 1) & (kRenorm - 1)) == 0 || u == 1) lane_renorm<SPL>(v, ex);
+      lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
     }
-    int dd = nbe - ex;
-    if (dd > 64) {
-      const float sc = pow2f(-dd);
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) wv[k] *= sc;
-      ex = nbe;
-      dd = 0;
-    }
-    const float nbs = nb * pow2f(dd);
-#pragma unroll
-    for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
-    v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
-    lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
+    if (ch == 0) e0 = buf[tok[0]];
   }
-  const float *r0 = pipe.row(0);
-  if (lane == 0) *lnz = log((double)(r0[tok[0]] * v[0])) + (double)ex * 0.6931471805599453;
+  if (lane == 0) *lnz = log((double)(e0 * v[0])) + (double)ex * 0.6931471805599453;
 }
 
 template <int SPL>
@@ -296,31 +315,30 @@ __global__ void __launch_bounds__(32)
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2 * kChunk * 33];
+  __shared__ __align__(16) float chunk[2][kChunk * 33];
   __shared__ __align__(16) float vec[2][32];
   const int b = blockIdx.x, role = blockIdx.y;
   if (status[b] != W2L_OK) return;
   ChainCtx c;
   c.trans = trans;
+  c.e = em + (size_t)b * d.Tmax * d.N;
   c.N = d.N;
   c.T = em_len[b];
   c.lane = threadIdx.x;
+  c.stride = em_stride(d.N);
   c.amax = trans_max(trans, d.N);
-  EmissionPipe pipe;
-  pipe.init(chunk, em + (size_t)b * d.Tmax * d.N, c.T, d.N, role == 0 || role == 2);
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  switch (role) {
-    case 0: fcc_alpha(c, pipe, vec, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0); break;
-    case 1: fcc_beta(c, pipe, vec, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1); break;
-    case 2:
-      fac_alpha<SPL>(c, pipe, y, tgt_len[b], w.fac_a + row0 * w.lpad, w.fac_ea + row0 * 32,
-                     w.lpad, w.scal + b * 4 + 2);
-      break;
-    default:
-      fac_beta<SPL>(c, pipe, y, tgt_len[b], w.fac_b + row0 * w.lpad, w.fac_eb + row0 * 32,
-                    w.lpad, w.scal + b * 4 + 3);
-      break;
+  if (role == 0) {
+    fcc_alpha(c, chunk, vec, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
+  } else if (role == 1) {
+    fcc_beta(c, chunk, vec, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
+  } else if (role == 2) {
+    fac_alpha<SPL>(c, chunk, y, tgt_len[b], w.fac_a + row0 * w.lpad, w.fac_ea + row0 * 32,
+                   w.lpad, w.scal + b * 4 + 2);
+  } else {
+    fac_beta<SPL>(c, chunk, y, tgt_len[b], w.fac_b + row0 * w.lpad, w.fac_eb + row0 * 32,
+                  w.lpad, w.scal + b * 4 + 3);
   }
 }
 
@@ -415,9 +433,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float pfa = 0.f;  // fcc alpha_{t-1}[lane]
   int pka = 0;
   if (ta >= 1 && ta < tend) {
-    const float *o = w.fac_a + (row0 + ta - 1) * LP;
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) pa[k] = o[k * 32 + lane];
+    lane_load<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
     pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
     pka = w.fcc_ka[row0 + ta - 1];
@@ -458,13 +474,8 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     }
     // ---- fac node posteriors (:214-217)
     float va[SPL], vb[SPL];
-    const float *oa = w.fac_a + (row0 + t) * LP;
-    const float *ob = w.fac_b + (row0 + t) * LP;
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      va[k] = oa[k * 32 + lane];
-      vb[k] = ob[k * 32 + lane];
-    }
+    lane_load<SPL>(va, w.fac_a + (row0 + t) * LP, lane);
+    lane_load<SPL>(vb, w.fac_b + (row0 + t) * LP, lane);
     const int ea = w.fac_ea[(row0 + t) * 32 + lane];
     const int eb = w.fac_eb[(row0 + t) * 32 + lane];
     const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
@@ -551,57 +562,66 @@ __global__ void __launch_bounds__(kGradWarps * 32)
 }
 
 // ---------------------------------------------------------- final kernel --
-__global__ void asg_final_kernel(const int64_t *__restrict__ tgt,
-                                 const int32_t *__restrict__ tgt_len,
-                                 const int32_t *__restrict__ em_len,
-                                 const float *__restrict__ trans, Dims d, AsgFastWs w,
-                                 double *loss, float *ga_utt, int32_t *status) {
+// per utterance: dA_b = M (.) sum_blocks(fullA partials) - scatter(fac edge
+// sums) (criterion.py:239-246), the loss (:244) and the guard verdict.
+__global__ void __launch_bounds__(256)
+    asg_final_kernel(const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                     const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
+                     AsgFastWs w, double *loss, float *ga_utt, int32_t *status) {
   const int b = blockIdx.x;
   __shared__ float sEdge[2 * 1024];
-  __shared__ int sy[1024];
+  __shared__ float s_red[8];
   __shared__ int s_bad;
+  const int N = d.N, NN = N * N;
   if (status[b] != W2L_OK) {
-    for (int p = threadIdx.x; p < d.N * d.N; p += blockDim.x) ga_utt[(size_t)b * d.N * d.N + p] = 0.f;
+    for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
     return;
   }
-  const int N = d.N, L = tgt_len[b], T = em_len[b], LP = w.lpad;
+  const int L = tgt_len[b], T = em_len[b], LP = w.lpad;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  float amax = -CUDART_INF_F;
-  for (int p = 0; p < N * N; ++p) amax = fmaxf(amax, trans[p]);
-  for (int l = threadIdx.x; l < L; l += blockDim.x) sy[l] = (int)y[l];
-  // per-state edge sums over frame blocks (fixed order)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float am = -CUDART_INF_F;
+  for (int p = threadIdx.x; p < NN; p += blockDim.x) am = fmaxf(am, trans[p]);
+  am = warp_max(am);
+  if (lane == 0) s_red[warp] = am;
+  if (threadIdx.x == 0) s_bad = 0;
+  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
   for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
     float s = 0.f;
-    for (int q = 0; q < w.nblk; ++q) s += w.part_edge[((size_t)b * w.nblk + q) * 2 * LP + i];
+    for (int q = 0; q < nb_used; ++q) s += w.part_edge[((size_t)b * w.nblk + q) * 2 * LP + i];
     sEdge[i] = s;
   }
-  if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
-  for (int p = threadIdx.x; p < N * N; p += blockDim.x) {
+  float amax = s_red[0];
+  for (int q = 1; q < (int)(blockDim.x >> 5); ++q) amax = fmaxf(amax, s_red[q]);
+  const int *perm = w.perm + (size_t)b * w.lpad;
+  const int *ts = w.tok_start + b * 33;
+  for (int p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = p / N, j = p % N;
     float s = 0.f;
-    for (int q = 0; q < w.nblk; ++q) s += w.part_fullA[((size_t)b * w.nblk + q) * 1024 + i * 32 + j];
+    for (int q = 0; q < nb_used; ++q) s += w.part_fullA[((size_t)b * w.nblk + q) * 1024 + i * 32 + j];
     const float full = s * expf(trans[p] - amax);
-    float con = 0.f;
-    for (int l = 0; l < L; ++l) {
-      if (sy[l] == i && sy[l] == j) con += sEdge[l];
-      if (l > 0 && sy[l] == i && sy[l - 1] == j) con += sEdge[LP + l];
+    float con = 0.f;  // states labelled i: stay edges (i,i), step edges (i, y_{l-1})
+    for (int q = ts[i]; q < ts[i + 1]; ++q) {
+      const int l = perm[q];
+      if (i == j) con += sEdge[l];
+      if (l > 0 && (int)y[l - 1] == j) con += sEdge[LP + l];
     }
-    ga_utt[(size_t)b * N * N + p] = full - con;
+    ga_utt[(size_t)b * NN + p] = full - con;
   }
-  // guard: every frame's normaliser must reproduce the forward total
+  // guard: every frame's normaliser must reproduce the forward totals
   const double ln2 = 0.6931471805599453;
   const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
   const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
   int bad = !(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb));
   bad |= fabs(zF - zFb) > tol || fabs(zC - zCb) > tol;
-  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
   for (int q = threadIdx.x; q < nb_used; q += blockDim.x) {
     const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 4;
     bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
     bad |= !(fabs((double)g[2]) * ln2 <= tol && fabs((double)g[3]) * ln2 <= tol);
   }
+  (void)L;
   if (bad) atomicOr(&s_bad, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -635,14 +655,6 @@ int asg_fast_spl(int Lmax) {
   for (int o : opts)
     if (32 * o >= Lmax) return o;
   return 0;
-}
-
-cudaError_t launch_token_csr(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
-                             int state_mul, int state_off, int *perm, int *tok_start,
-                             const int32_t *status, cudaStream_t s) {
-  token_csr_kernel<<<d.B, 256, 0, s>>>(tgt, tgt_len, d, lpad, state_mul, state_off, perm,
-                                       tok_start, status);
-  return cudaGetLastError();
 }
 
 static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
@@ -685,9 +697,7 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
                             int32_t *status, cudaStream_t s) {
-  cudaError_t err =
-      launch_token_csr(tgt, tgt_len, d, w.lpad, 1, 0, w.perm, w.tok_start, status, s);
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
   switch (w.spl) {
     case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
     case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
@@ -706,20 +716,24 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
 }
 
 // --------------------------------------------------- batch reduction of dA --
+// one warp per transition pair: fixed-order float64 sum over utterances
+// (trainer.py:442-447 sums in float64), deterministic run to run
 __global__ void reduce_grad_trans_kernel(const float *ga_utt, const int32_t *status, Dims d,
                                          float *grad_trans) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (p >= d.N * d.N) return;
-  double s = 0.0;  // trainer.py:442-447 sums in float64
-  for (int b = 0; b < d.B; ++b)
+  double s = 0.0;
+  for (int b = lane; b < d.B; b += 32)
     if (status[b] == W2L_OK) s += (double)ga_utt[(size_t)b * d.N * d.N + p];
-  grad_trans[p] = (float)s;
+  s = warp_sum(s);
+  if (lane == 0) grad_trans[p] = (float)s;
 }
 
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
                                      float *grad_trans, cudaStream_t s) {
   const int n = d.N * d.N;
-  reduce_grad_trans_kernel<<<(n + 127) / 128, 128, 0, s>>>(ga_utt, status, d, grad_trans);
+  reduce_grad_trans_kernel<<<(n + 7) / 8, 256, 0, s>>>(ga_utt, status, d, grad_trans);
   return cudaGetLastError();
 }
 

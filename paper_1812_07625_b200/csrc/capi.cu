@@ -132,7 +132,8 @@ int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt
   void *slots;
   asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
-  int rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, status, s));
+  int rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad,
+                                                w.perm, w.tok_start, status, s));
   if (rc) return rc;
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
                                  status, s));
@@ -170,7 +171,8 @@ int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t
   float *ga_ws = (float *)c.take((size_t)B * N * N * sizeof(float));
   void *slots = c.take(asg_exact_ws_bytes_per_slot(Tmax, N, Lmax) * asg_slots_f64(B));
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
-  int rc = from_cuda(launch_asg_validate<double>(em, em_len, tgt, tgt_len, trans, d, status, s));
+  int rc = from_cuda(launch_asg_validate<double>(em, em_len, tgt, tgt_len, trans, d, 0, nullptr,
+                                                 nullptr, status, s));
   if (rc) return rc;
   // zero outputs of utterances that fail validation (the exact kernel skips them)
   rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
@@ -216,7 +218,8 @@ int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *t
   CtcFastWs w;
   void *slots;
   ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
-  int rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, status, s));
+  int rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
+                                                w.perm, w.tok_start, status, s));
   if (rc) return rc;
   rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s));
   if (rc) return rc;
@@ -242,7 +245,8 @@ int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64
   cudaStream_t s = (cudaStream_t)stream;
   Dims d{B, Tmax, N, Lmax};
   int rc =
-      from_cuda(launch_ctc_validate<double>(logp, em_len, tgt, tgt_len, blank, d, status, s));
+      from_cuda(launch_ctc_validate<double>(logp, em_len, tgt, tgt_len, blank, d, 0, nullptr,
+                                            nullptr, status, s));
   if (rc) return rc;
   rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
   if (rc) return rc;

@@ -1,4 +1,5 @@
-// Warp-private emission staging for the serial recursions.
+// Warp-private emission staging and block-floating-point helpers for the
+// serial recursions.
 //
 // A chain warp walks an utterance frame by frame (forward or backward).  Its
 // emissions are staged kChunk frames at a time into shared memory with
@@ -14,65 +15,39 @@
 
 namespace w2l {
 
-struct EmissionPipe {
-  float *buf;        // [2][kChunk][stride] shared memory
-  const float *e;    // &em[b][0][0]
-  int T, N, stride, lane;
-  bool fwd;
-  int cur;           // chunk resident in buf[cur & 1], -1 before the first
-  double shift_sum;  // sum of this lane's row maxima (CTC loss offset)
+constexpr int kRenorm = 4;  // frames between lane renormalisations
 
-  __device__ void init(float *smem, const float *e_, int T_, int N_, bool fwd_) {
-    buf = smem;
-    e = e_;
-    T = T_;
-    N = N_;
-    stride = em_stride(N_);
-    lane = threadIdx.x & 31;
-    fwd = fwd_;
-    cur = -1;
-    shift_sum = 0.0;
-    issue(fwd ? 0 : (T - 1) / kChunk);
-  }
-
-  __device__ void issue(int c) {
-    const int t0 = c * kChunk;
-    const int rows = min(kChunk, T - t0);
-    float *dst = buf + (c & 1) * kChunk * stride;
-    if (lane < N)
-      for (int r = 0; r < rows; ++r)
-        cp_async4(dst + r * stride + lane, e + (size_t)(t0 + r) * N + lane);
-    cp_async_commit();
-  }
-
-  // make chunk c (the next one in walk order) resident and converted
-  __device__ void advance(int c) {
-    cp_async_wait<0>();
-    __syncwarp();
-    const int t0 = c * kChunk;
-    const int rows = min(kChunk, T - t0);
-    float *rb = buf + (c & 1) * kChunk * stride;
-    if (lane < rows) {
-      float *r = rb + lane * stride;
-      float m = -CUDART_INF_F;
-      for (int i = 0; i < N; ++i) m = fmaxf(m, r[i]);
-      for (int i = 0; i < N; ++i) r[i] = expf(r[i] - m);
-      r[N] = 0.f;
-      shift_sum += (double)m;
-    }
-    __syncwarp();
-    const int nxt = fwd ? c + 1 : c - 1;
-    if (nxt >= 0 && nxt * kChunk < T) issue(nxt);
-    cur = c;
-  }
-
-  // shared-memory row of Et for frame t (frames must be requested in walk order)
-  __device__ __forceinline__ const float *row(int t) {
-    const int c = t / kChunk;
-    if (c != cur) advance(c);
-    return buf + (c & 1) * kChunk * stride + (t - c * kChunk) * stride;
-  }
+struct ChainCtx {
+  const float *trans;
+  const float *e;  // &em[b][0][0]
+  int N, T, lane, stride;
+  float amax;
 };
+
+__device__ __forceinline__ void stage_issue(float *dst, const ChainCtx &c, int t0) {
+  const int rows = min(kChunk, c.T - t0);
+  if (c.lane < c.N)
+    for (int r = 0; r < rows; ++r)
+      cp_async4(dst + r * c.stride + c.lane, c.e + (size_t)(t0 + r) * c.N + c.lane);
+  cp_async_commit();
+}
+
+// wait for the staged chunk, convert it to Et in place (lane r owns row r);
+// the row maxima are summed into *shift_sum (the CTC loss offset) if given
+__device__ __forceinline__ void stage_convert(float *buf, const ChainCtx &c, int rows,
+                                              double *shift_sum = nullptr) {
+  cp_async_wait<0>();
+  __syncwarp();
+  if (c.lane < rows) {
+    float *r = buf + c.lane * c.stride;
+    float m = -CUDART_INF_F;
+    for (int i = 0; i < c.N; ++i) m = fmaxf(m, r[i]);
+    for (int i = 0; i < c.N; ++i) r[i] = expf(r[i] - m);
+    r[c.N] = 0.f;
+    if (shift_sum) *shift_sum += (double)m;
+  }
+  __syncwarp();
+}
 
 // The same per-frame shift and conversion, computed by a whole warp for one
 // frame (lane i < N holds token i): used by the gradient kernels.
@@ -104,14 +79,42 @@ __device__ __forceinline__ void lane_renorm(float (&v)[SPL], int &ex) {
   }
 }
 
-// one frame's chain row, slot-major ([k][lane]) so every store is coalesced
+// one frame's chain row, lane-major ([lane][k]): SPL is even, so a lane's
+// states go out as SPL/2 8-byte stores
 template <int SPL>
 __device__ __forceinline__ void lane_store(const float (&v)[SPL], int ex, float *out, int *oute,
                                            int lp, int lane, int t) {
-  float *o = out + t * lp + lane;
+  static_assert(SPL % 2 == 0, "SPL must be even");
+  float2 *o = reinterpret_cast<float2 *>(out + t * lp + lane * SPL);
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) o[k * 32] = v[k];
+  for (int k = 0; k < SPL / 2; ++k) o[k] = make_float2(v[2 * k], v[2 * k + 1]);
   oute[t * 32 + lane] = ex;
+}
+
+template <int SPL>
+__device__ __forceinline__ void lane_load(float (&v)[SPL], const float *row, int lane) {
+  const float2 *o = reinterpret_cast<const float2 *>(row + lane * SPL);
+#pragma unroll
+  for (int k = 0; k < SPL / 2; ++k) {
+    const float2 x = o[k];
+    v[2 * k] = x.x;
+    v[2 * k + 1] = x.y;
+  }
+}
+
+// align the neighbour lane's value to this lane's exponent; if the
+// neighbour dominates by more than 2^64, rebase this lane onto it first
+template <int SPL>
+__device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[SPL], int &ex) {
+  int dd = nbe - ex;
+  if (dd > 64) {
+    const float sc = pow2f(-dd);
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) v[k] *= sc;
+    ex = nbe;
+    dd = 0;
+  }
+  return nb * pow2f(dd);
 }
 
 }  // namespace w2l

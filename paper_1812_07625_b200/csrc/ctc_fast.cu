@@ -43,68 +43,75 @@ __global__ void __launch_bounds__(32)
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2 * kChunk * 33];
-  const int b = blockIdx.x, role = blockIdx.y, lane = threadIdx.x;
+  __shared__ __align__(16) float chunk[2][kChunk * 33];
+  const int b = blockIdx.x, lane = threadIdx.x;
   if (status[b] != W2L_OK) return;
-  const int T = em_len[b], N = d.N, L = tgt_len[b], S = 2 * L + 1;
-  const bool fwd = role == 0;
-  EmissionPipe pipe;
-  pipe.init(chunk, em + (size_t)b * d.Tmax * N, T, N, fwd);
+  ChainCtx c;
+  c.trans = nullptr;
+  c.e = em + (size_t)b * d.Tmax * d.N;
+  c.N = d.N;
+  c.T = em_len[b];
+  c.lane = lane;
+  c.stride = em_stride(d.N);
+  c.amax = 0.f;
+  const int T = c.T, L = tgt_len[b], S = 2 * L + 1;
+  const bool fwd = blockIdx.y == 0;
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   int lab[SPL];
   float sk[SPL], sk2[SPL];
-  ctc_lattice_lane<SPL>(y, L, blank, N, lane, lab, sk, sk2);
-
-  float v[SPL];
-  int ex = 0;
+  ctc_lattice_lane<SPL>(y, L, blank, d.N, lane, lab, sk, sk2);
   float *out = (fwd ? w.a : w.b) + row0 * w.lpad;
   int *oute = (fwd ? w.ea : w.eb) + row0 * 32;
   const int lp = w.lpad;
-  
-  
   const double ln2 = 0.6931471805599453;
+  const int nch = (T + kChunk - 1) / kChunk;
+  float v[SPL];
+  int ex = 0;
 
   if (fwd) {
-    const float *r0 = pipe.row(0);
+    double shifts = 0.0;
+    stage_issue(chunk[0], c, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      float *buf = chunk[ch & 1];
+      const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+      stage_convert(buf, c, rows, &shifts);
+      if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
+      int r = 0;
+      if (ch == 0) {  // criterion.py:123-125
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) v[k] = 0.f;
-    ex = 0;
-    if (lane == 0) {               // criterion.py:123-125
-      v[0] = r0[lab[0]];
-      if (S > 1) v[1] = r0[lab[1]];
-    }
-    lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
-    for (int t = 1; t < T; ++t) {
-      const float *r = pipe.row(t);
-      float E[SPL];
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) E[k] = r[lab[k]];
-      float nb1 = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
-      float nb2 = __shfl_up_sync(0xffffffffu, v[SPL - 2], 1);
-      int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
-      if (lane == 0) {
-        nb1 = nb2 = 0.f;
-        nbe = kNegExp;
+        for (int k = 0; k < SPL; ++k) v[k] = 0.f;
+        if (lane == 0) {
+          v[0] = buf[lab[0]];
+          if (S > 1) v[1] = buf[lab[1]];
+        }
+        lane_renorm<SPL>(v, ex);
+        lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
+        r = 1;
       }
-      int dd = nbe - ex;
-      if (dd > 64) {
-        const float sc = pow2f(-dd);
+      for (; r < rows; ++r) {
+        const int t = t0 + r;
+        const float *row = buf + r * c.stride;
+        float E[SPL];
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) v[k] *= sc;
-        ex = nbe;
-        dd = 0;
+        for (int k = 0; k < SPL; ++k) E[k] = row[lab[k]];
+        float nb1 = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
+        float nb2 = __shfl_up_sync(0xffffffffu, v[SPL - 2], 1);
+        int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
+        if (lane == 0) {
+          nb1 = nb2 = 0.f;
+          nbe = kNegExp;
+        }
+        const float n1 = align_neighbour<SPL>(nb1, nbe, v, ex);
+        const float n2 = nb2 * pow2f(nbe - ex);
+#pragma unroll
+        for (int k = SPL - 1; k >= 2; --k) v[k] = E[k] * fmaf(sk[k], v[k - 2], v[k] + v[k - 1]);
+        const float v1 = E[1] * fmaf(sk[1], n1, v[1] + v[0]);
+        v[0] = E[0] * fmaf(sk[0], n2, v[0] + n1);
+        v[1] = v1;
+        if ((t & (kRenorm - 1)) == 0 || t == T - 1) lane_renorm<SPL>(v, ex);
+        lane_store<SPL>(v, ex, out, oute, lp, lane, t);
       }
-      const float scn = pow2f(dd);
-      const float n1 = nb1 * scn, n2 = nb2 * scn;
-#pragma unroll
-      for (int k = SPL - 1; k >= 2; --k) v[k] = E[k] * fmaf(sk[k], v[k - 2], v[k] + v[k - 1]);
-      const float v1 = E[1] * fmaf(sk[1], n1, v[1] + v[0]);
-      v[0] = E[0] * fmaf(sk[0], n2, v[0] + n1);
-      v[1] = v1;
-      lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, lp, lane, t);
     }
     // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
     float part = 0.f;
@@ -116,7 +123,7 @@ __global__ void __launch_bounds__(32)
     const double lp_ = part > 0.f ? log((double)part) + (double)ex * ln2 : -CUDART_INF;
     const double m = warp_max(lp_);
     const double sum = warp_sum(lp_ > -CUDART_INF ? exp(lp_ - m) : 0.0);
-    const double shifts = warp_sum(pipe.shift_sum);
+    shifts = warp_sum(shifts);
     if (lane == 0) {
       w.scal[b * 4 + 0] = isfinite(m) ? m + log(sum) : -CUDART_INF;
       w.scal[b * 4 + 2] = shifts;
@@ -127,44 +134,43 @@ __global__ void __launch_bounds__(32)
       const int s = lane * SPL + k;
       v[k] = (s == S - 1 || s == S - 2) ? 1.f : 0.f;
     }
-    ex = 0;
     lane_renorm<SPL>(v, ex);
     lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
-    for (int u = T - 1; u >= 1; --u) {
-      const float *r = pipe.row(u);
-      float wv[SPL];
+    stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
+    float z0 = 0.f;
+    for (int ch = nch - 1; ch >= 0; --ch) {
+      float *buf = chunk[ch & 1];
+      const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
+      stage_convert(buf, c, rows);
+      if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
+      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+        const int u = t0 + r;
+        const float *row = buf + r * c.stride;
+        float wv[SPL];
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) wv[k] = r[lab[k]] * v[k];
-      float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-      float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
-      int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
-      if (lane == 31) {
-        nb1 = nb2 = 0.f;
-        nbe = kNegExp;
+        for (int k = 0; k < SPL; ++k) wv[k] = row[lab[k]] * v[k];
+        float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+        float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
+        int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
+        if (lane == 31) {
+          nb1 = nb2 = 0.f;
+          nbe = kNegExp;
+        }
+        const float n1 = align_neighbour<SPL>(nb1, nbe, wv, ex);
+        const float n2 = nb2 * pow2f(nbe - ex);
+#pragma unroll
+        for (int k = 0; k < SPL - 2; ++k) v[k] = fmaf(sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
+        v[SPL - 2] = fmaf(sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
+        v[SPL - 1] = fmaf(sk2[SPL - 1], n2, wv[SPL - 1] + n1);
+        if (((u - 1) & (kRenorm - 1)) == 0 || u == 1) lane_renorm<SPL>(v, ex);
+        lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
       }
-      int dd = nbe - ex;
-      if (dd > 64) {
-        const float sc = pow2f(-dd);
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) wv[k] *= sc;
-        ex = nbe;
-        dd = 0;
+      if (ch == 0 && lane == 0) {
+        z0 = buf[lab[0]] * v[0];
+        if (S > 1) z0 += buf[lab[1]] * v[1];
       }
-      const float scn = pow2f(dd);
-      const float n1 = nb1 * scn, n2 = nb2 * scn;
-#pragma unroll
-      for (int k = 0; k < SPL - 2; ++k) v[k] = fmaf(sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
-      v[SPL - 2] = fmaf(sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
-      v[SPL - 1] = fmaf(sk2[SPL - 1], n2, wv[SPL - 1] + n1);
-      lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
     }
-    const float *r0 = pipe.row(0);
-    if (lane == 0) {
-      float z = r0[lab[0]] * v[0];
-      if (S > 1) z += r0[lab[1]] * v[1];
-      w.scal[b * 4 + 1] = log((double)z) + (double)ex * ln2;
-    }
+    if (lane == 0) w.scal[b * 4 + 1] = log((double)z0) + (double)ex * ln2;
   }
 }
 
@@ -205,13 +211,8 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const int tend = min(tb, T);
   for (int t = ta; t < tend; ++t) {
     float va[SPL], vb[SPL];
-    const float *oa = w.a + (row0 + t) * LP;
-    const float *ob = w.b + (row0 + t) * LP;
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      va[k] = oa[k * 32 + lane];
-      vb[k] = ob[k * 32 + lane];
-    }
+    lane_load<SPL>(va, w.a + (row0 + t) * LP, lane);
+    lane_load<SPL>(vb, w.b + (row0 + t) * LP, lane);
     const int ea = w.ea[(row0 + t) * 32 + lane];
     const int eb = w.eb[(row0 + t) * 32 + lane];
     const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
@@ -326,9 +327,7 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w)
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s) {
-  cudaError_t err =
-      launch_token_csr(tgt, tgt_len, d, w.lpad, 2, 1, w.perm, w.tok_start, status, s);
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
   switch (w.spl) {
     case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
     case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;

@@ -11,14 +11,15 @@ struct Dims {
 };
 
 // ---- validation (reference check order; criterion.py:23-41,92-111,174-190)
+// perm/tok_start (nullable): token CSR of valid utterances for the fast path
 template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                const int32_t *tgt_len, const TE *trans, Dims d,
-                                int32_t *status, cudaStream_t s);
+                                const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
+                                int *perm, int *tok_start, int32_t *status, cudaStream_t s);
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                const int32_t *tgt_len, int blank, Dims d, int32_t *status,
-                                cudaStream_t s);
+                                const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
+                                int *tok_start, int32_t *status, cudaStream_t s);
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s);
@@ -76,11 +77,6 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w);
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s);
-
-// token-grouped chain states (perm, tok_start) for the emissions-gradient gather
-cudaError_t launch_token_csr(const int64_t *tgt, const int32_t *tgt_len, Dims d, int lpad,
-                             int state_mul, int state_off, int *perm, int *tok_start,
-                             const int32_t *status, cudaStream_t s);
 
 // ---- reductions
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,

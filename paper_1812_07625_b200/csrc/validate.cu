@@ -1,10 +1,18 @@
-// Device-side input validation in the reference's check order.
+// Device-side input validation in the reference's check order, plus the
+// per-utterance target preparation the fast kernels need.
 //
 // The reference validates before computing, so a failing utterance never
 // produces partial outputs (criterion.py:23-41 _check_emissions/_check_target,
-// :92-111 CTC, :174-190 ASG).  Each block validates one utterance and writes
-// the FIRST failing check's code to status[b]; compute kernels skip
-// utterances whose status is non-zero.
+// :92-111 CTC, :174-190 ASG).  Two launches:
+//   em_check  -- one thread per frame row, the whole batch in parallel:
+//                non-finite values (bit 1) and, for CTC, rows whose
+//                logsumexp is off by more than 1e-2 (bit 2) are OR-ed into
+//                status[b] (zeroed beforehand);
+//   prep      -- one block per utterance: folds those bits and the target /
+//                transition checks into the FIRST failing check's code, and
+//                for valid utterances builds the token CSR (chain states
+//                grouped by token) used by the emissions-gradient gather.
+// Compute kernels skip utterances whose status is non-zero.
 
 #include "common.cuh"
 #include "kernels.h"
@@ -12,148 +20,207 @@
 namespace w2l {
 namespace {
 
-template <class TE>
-__device__ bool block_any_nonfinite(const TE *p, long long n) {
-  int bad = 0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite((double)p[i]);
-  return __syncthreads_or(bad);
-}
-
-// target ids in [0, n_tok) over the first L entries (_check_target, :32-41)
-__device__ bool block_target_out_of_range(const int64_t *y, int L, int n_tok) {
-  int bad = 0;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) bad |= (y[i] < 0 || y[i] >= n_tok);
-  return __syncthreads_or(bad);
-}
+constexpr int kBitNonFinite = 1 << 8;
+constexpr int kBitRowLse = 1 << 9;
 
 template <class TE>
-__global__ void asg_validate_kernel(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                    const int32_t *tgt_len, const TE *trans, Dims d,
-                                    int32_t *status) {
+__global__ void em_check_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len,
+                                Dims d, int check_lse, int32_t *status) {
+  const int b = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = min(max(em_len[b], 0), d.Tmax);
+  if (t >= T) return;
+  const TE *r = em + ((size_t)b * d.Tmax + t) * d.N;
+  int bits = 0;
+  double m = -CUDART_INF;
+  for (int i = 0; i < d.N; ++i) {
+    const double v = (double)r[i];
+    if (!isfinite(v)) bits = kBitNonFinite;
+    m = fmax(m, v);
+  }
+  if (check_lse && !bits) {
+    // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101)
+    double s = 0.0;
+    for (int i = 0; i < d.N; ++i) s += exp((double)r[i] - m);
+    if (fabs(log(s) + m) > 1e-2) bits |= kBitRowLse;
+  }
+  if (bits) atomicOr(&status[b], bits);
+}
+
+__device__ bool block_any(int v) { return __syncthreads_or(v); }
+
+// grouped-by-token chain states: perm[tok_start[k] .. tok_start[k+1]) lists
+// the states (ASG: l, CTC: 2l+1) whose label is k, in ascending order
+__device__ void build_token_csr(const int64_t *y, int L, int N, int state_mul, int state_off,
+                                int *perm, int *tok_start) {
+  __shared__ int cnt[33];
+  if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[(int)y[l]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k <= N; ++k) {
+      const int c = k < N ? cnt[k] : 0;
+      tok_start[k] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    const int tk = (int)y[l];
+    int before = 0;
+    for (int q = 0; q < l; ++q) before += (y[q] == tk);
+    perm[tok_start[tk] + before] = l * state_mul + state_off;
+  }
+}
+
+template <class TE>
+__global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
+                                const int64_t *__restrict__ tgt,
+                                const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans,
+                                Dims d, int lpad, int *perm, int *tok_start, int32_t *status) {
   const int b = blockIdx.x;
   const int T = em_len[b], L = tgt_len[b];
+  const int bits = status[b];
+  __syncthreads();
   int code = W2L_OK;
   if (T < 1 || T > d.Tmax) {
     code = W2L_ERR_CONTRACT;                        // criterion.py:25-26
-  } else if (block_any_nonfinite(em + (size_t)b * d.Tmax * d.N, (long long)T * d.N)) {
+  } else if (bits & kBitNonFinite) {
     code = W2L_ERR_NUMERIC;                         // :27-28
-  } else if (block_any_nonfinite(trans, (long long)d.N * d.N)) {
-    code = W2L_ERR_NUMERIC;                         // :179-180
-  } else if (L < 0 || L > d.Lmax) {
-    code = W2L_ERR_CONTRACT;
   } else {
-    const int64_t *y = tgt + (size_t)b * d.Lmax;
-    if (block_target_out_of_range(y, L, d.N)) {
-      code = W2L_ERR_TARGET;                        // :36-40
-    } else if (L == 0) {
-      code = W2L_ERR_TARGET;                        // :183-184
-    } else {
-      int dup = 0;
-      for (int i = threadIdx.x + 1; i < L; i += blockDim.x) dup |= (y[i] == y[i - 1]);
-      if (__syncthreads_or(dup)) code = W2L_ERR_CONTRACT;   // :185-186
-      else if (T < L) code = W2L_ERR_INFEASIBLE;            // :187-190
-    }
-  }
-  if (threadIdx.x == 0) status[b] = code;
-}
-
-template <class TE>
-__global__ void ctc_validate_kernel(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                    const int32_t *tgt_len, int blank, Dims d,
-                                    int32_t *status) {
-  const int b = blockIdx.x;
-  const int T = em_len[b], L = tgt_len[b];
-  const TE *e = em + (size_t)b * d.Tmax * d.N;
-  int code = W2L_OK;
-  if (T < 1 || T > d.Tmax) {
-    code = W2L_ERR_CONTRACT;
-  } else if (block_any_nonfinite(e, (long long)T * d.N)) {
-    code = W2L_ERR_NUMERIC;
-  } else if (blank < 0 || blank >= d.N) {
-    code = W2L_ERR_CONTRACT;                        // :94-95
-  } else {
-    // rows must be log-normalised: |logsumexp| <= 1e-2 (:96-101)
     int bad = 0;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-      const TE *r = e + (size_t)t * d.N;
-      double m = -CUDART_INF;
-      for (int i = 0; i < d.N; ++i) m = fmax(m, (double)r[i]);
-      double s = 0.0;
-      for (int i = 0; i < d.N; ++i) s += exp((double)r[i] - m);
-      bad |= fabs(log(s) + m) > 1e-2;
-    }
-    if (__syncthreads_or(bad)) {
-      code = W2L_ERR_CONTRACT;
+    for (int i = threadIdx.x; i < d.N * d.N; i += blockDim.x) bad |= !isfinite((double)trans[i]);
+    if (block_any(bad)) {
+      code = W2L_ERR_NUMERIC;                       // :179-180
     } else if (L < 0 || L > d.Lmax) {
       code = W2L_ERR_CONTRACT;
     } else {
       const int64_t *y = tgt + (size_t)b * d.Lmax;
-      if (block_target_out_of_range(y, L, d.N)) {
-        code = W2L_ERR_TARGET;                      // :102
-      } else {
-        int has_blank = 0, reps = 0;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) {
-          has_blank |= (y[i] == blank);
-          reps += (i > 0 && y[i] == y[i - 1]);
-        }
-        has_blank = __syncthreads_or(has_blank);
-        // block sum of repeats
-        __shared__ int s_reps;
-        if (threadIdx.x == 0) s_reps = 0;
-        __syncthreads();
-        atomicAdd(&s_reps, reps);
-        __syncthreads();
-        if (has_blank) code = W2L_ERR_TARGET;                   // :103-104
-        else if (T < L + s_reps) code = W2L_ERR_INFEASIBLE;     // :105-111
+      int oor = 0, dup = 0;
+      for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        oor |= (y[i] < 0 || y[i] >= d.N);
+        dup |= (i > 0 && y[i] == y[i - 1]);
       }
+      oor = block_any(oor);
+      dup = block_any(dup);
+      if (oor) code = W2L_ERR_TARGET;               // :36-40
+      else if (L == 0) code = W2L_ERR_TARGET;       // :183-184
+      else if (dup) code = W2L_ERR_CONTRACT;        // :185-186
+      else if (T < L) code = W2L_ERR_INFEASIBLE;    // :187-190
+      if (code == W2L_OK && perm)
+        build_token_csr(y, L, d.N, 1, 0, perm + (size_t)b * lpad, tok_start + b * 33);
     }
   }
+  __syncthreads();
   if (threadIdx.x == 0) status[b] = code;
 }
 
-template <class TE>
-__global__ void viterbi_validate_kernel(const TE *em, const int32_t *em_len, Dims d,
-                                        int32_t *status) {
+__global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
+                                const int64_t *__restrict__ tgt,
+                                const int32_t *__restrict__ tgt_len, int blank, Dims d,
+                                int lpad, int *perm, int *tok_start, int32_t *status) {
   const int b = blockIdx.x;
+  const int T = em_len[b], L = tgt_len[b];
+  const int bits = status[b];
+  __syncthreads();
+  int code = W2L_OK;
+  if (T < 1 || T > d.Tmax) {
+    code = W2L_ERR_CONTRACT;
+  } else if (bits & kBitNonFinite) {
+    code = W2L_ERR_NUMERIC;
+  } else if (blank < 0 || blank >= d.N) {
+    code = W2L_ERR_CONTRACT;                        // :94-95
+  } else if (bits & kBitRowLse) {
+    code = W2L_ERR_CONTRACT;                        // :96-101
+  } else if (L < 0 || L > d.Lmax) {
+    code = W2L_ERR_CONTRACT;
+  } else {
+    const int64_t *y = tgt + (size_t)b * d.Lmax;
+    int oor = 0, has_blank = 0, reps = 0;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      oor |= (y[i] < 0 || y[i] >= d.N);
+      has_blank |= (y[i] == blank);
+      reps += (i > 0 && y[i] == y[i - 1]);
+    }
+    oor = block_any(oor);
+    has_blank = block_any(has_blank);
+    __shared__ int s_reps;
+    if (threadIdx.x == 0) s_reps = 0;
+    __syncthreads();
+    atomicAdd(&s_reps, reps);
+    __syncthreads();
+    if (oor) code = W2L_ERR_TARGET;                           // :102
+    else if (has_blank) code = W2L_ERR_TARGET;                // :103-104
+    else if (T < L + s_reps) code = W2L_ERR_INFEASIBLE;       // :105-111
+    if (code == W2L_OK && perm)
+      build_token_csr(y, L, d.N, 2, 1, perm + (size_t)b * lpad, tok_start + b * 33);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) status[b] = code;
+}
+
+__global__ void viterbi_prep_kernel(const int32_t *__restrict__ em_len, Dims d,
+                                    int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B) return;
   const int T = em_len[b];
   int code = W2L_OK;
   if (T < 1 || T > d.Tmax) code = W2L_ERR_CONTRACT;
-  else if (block_any_nonfinite(em + (size_t)b * d.Tmax * d.N, (long long)T * d.N))
-    code = W2L_ERR_NUMERIC;                          // _check_emissions (:265)
-  if (threadIdx.x == 0) status[b] = code;
+  else if (status[b] & kBitNonFinite) code = W2L_ERR_NUMERIC;   // _check_emissions (:265)
+  status[b] = code;
+}
+
+template <class TE>
+cudaError_t em_check(const TE *em, const int32_t *em_len, Dims d, int check_lse,
+                     int32_t *status, cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(status, 0, sizeof(int32_t) * d.B, s);
+  if (err != cudaSuccess) return err;
+  dim3 grid((d.Tmax + 127) / 128, d.B);
+  em_check_kernel<TE><<<grid, 128, 0, s>>>(em, em_len, d, check_lse, status);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                const int32_t *tgt_len, const TE *trans, Dims d,
-                                int32_t *status, cudaStream_t s) {
-  asg_validate_kernel<TE><<<d.B, 256, 0, s>>>(em, em_len, tgt, tgt_len, trans, d, status);
+                                const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
+                                int *perm, int *tok_start, int32_t *status, cudaStream_t s) {
+  cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s);
+  if (err != cudaSuccess) return err;
+  asg_prep_kernel<TE><<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, trans, d, lpad, perm,
+                                          tok_start, status);
   return cudaGetLastError();
 }
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
-                                const int32_t *tgt_len, int blank, Dims d, int32_t *status,
-                                cudaStream_t s) {
-  ctc_validate_kernel<TE><<<d.B, 256, 0, s>>>(em, em_len, tgt, tgt_len, blank, d, status);
+                                const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
+                                int *tok_start, int32_t *status, cudaStream_t s) {
+  cudaError_t err = em_check<TE>(em, em_len, d, 1, status, s);
+  if (err != cudaSuccess) return err;
+  ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
+                                      status);
   return cudaGetLastError();
 }
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s) {
-  viterbi_validate_kernel<TE><<<d.B, 256, 0, s>>>(em, em_len, d, status);
+  cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s);
+  if (err != cudaSuccess) return err;
+  viterbi_prep_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, status);
   return cudaGetLastError();
 }
 
-#define INST(TE)                                                                          \
-  template cudaError_t launch_asg_validate<TE>(const TE *, const int32_t *, const int64_t *, \
-                                               const int32_t *, const TE *, Dims, int32_t *, \
-                                               cudaStream_t);                              \
-  template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *, \
-                                               const int32_t *, int, Dims, int32_t *,       \
-                                               cudaStream_t);                              \
-  template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,        \
+#define INST(TE)                                                                           \
+  template cudaError_t launch_asg_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
+                                               const int32_t *, const TE *, Dims, int, int *, \
+                                               int *, int32_t *, cudaStream_t);               \
+  template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
+                                               const int32_t *, int, Dims, int, int *, int *, \
+                                               int32_t *, cudaStream_t);                      \
+  template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,         \
                                                    int32_t *, cudaStream_t);
 INST(float)
 INST(double)

@@ -6,6 +6,8 @@
 //     cand_j = dp[j] + A[i][j];  back = first argmax_j;  dp'[i] = e[t][i] + cand_back
 // so paths and scores are bit-identical to the numpy reference (ties go to
 // the lowest id, np.argmax semantics, NaN treated as the maximum).  The
+// argmax is a 5-level tournament over index-ordered pairs (depth 5 instead of
+// a 30-long compare chain); emissions are prefetched 8 frames ahead; the
 // previous frame's dp vector is broadcast through shared memory (double
 // buffered, one __syncwarp per frame); backpointers are uint8 in shared
 // memory when T*N fits, else in the workspace; lane 0 traces back.
@@ -17,6 +19,89 @@ namespace w2l {
 namespace {
 
 constexpr int kSmemBackMax = 160 * 1024;
+
+template <bool kNanAware>
+__device__ __forceinline__ bool vit_take(double a, double b) {
+  // does candidate b (higher index) replace a?  np.argmax: first maximum wins,
+  // a NaN is the maximum and the first NaN wins
+  if (kNanAware) return !isnan(a) && (b > a || isnan(b));
+  return b > a;
+}
+
+// one frame of the max-plus recursion for destination token `lane`;
+// returns the new dp value and writes the backpointer
+template <bool kNanAware>
+__device__ __forceinline__ double vit_step(const double *prev, const double (&arow)[32], int N,
+                                           double et, int &arg_out) {
+  double c[32];
+  int idx[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    c[j] = j < N ? prev[j] + arow[j] : -CUDART_INF;   // cand_j = dp[j] + A[i][j]
+    idx[j] = j;
+  }
+  // pairwise tournament over index-ordered halves keeps first-max semantics
+#pragma unroll
+  for (int w = 1; w < 32; w <<= 1) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2 * w) {
+      if (vit_take<kNanAware>(c[j], c[j + w])) {
+        c[j] = c[j + w];
+        idx[j] = idx[j + w];
+      }
+    }
+  }
+  arg_out = idx[0];
+  return et + c[0];                                   // dp'[i] = e[t][i] + cand_back
+}
+
+template <class TE, class TA, bool kSmemBack, bool kNanAware>
+__device__ __forceinline__ void viterbi_body(const TE *__restrict__ e, int T, int N, int lane,
+                                             const double (&arow)[32], double (*dp_buf)[32],
+                                             uint8_t *back, double *score_out,
+                                             int64_t *path_out) {
+  constexpr int kPre = 8;   // emission prefetch distance (frames)
+  double pre[kPre];
+#pragma unroll
+  for (int q = 0; q < kPre; ++q)
+    pre[q] = (lane < N && 1 + q < T) ? (double)e[(size_t)(1 + q) * N + lane] : 0.0;
+  double dp = lane < N ? (double)e[lane] : -CUDART_INF;
+  dp_buf[0][lane] = dp;
+  for (int t0 = 1; t0 < T; t0 += kPre) {
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+      const int t = t0 + q;
+      if (t < T) {
+        const double et = pre[q];
+        const int tn = t + kPre;
+        pre[q] = (lane < N && tn < T) ? (double)e[(size_t)tn * N + lane] : 0.0;
+        __syncwarp();
+        int arg;
+        dp = vit_step<kNanAware>(dp_buf[(t - 1) & 1], arow, N, et, arg);
+        if (lane < N) back[(size_t)t * N + lane] = (uint8_t)arg;
+        dp_buf[t & 1][lane] = lane < N ? dp : -CUDART_INF;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const double *fin = dp_buf[(T - 1) & 1];
+    int best_i = 0;
+    double bv = fin[0];
+    for (int i = 1; i < N; ++i)
+      if (vit_take<true>(bv, fin[i])) {
+        bv = fin[i];
+        best_i = i;
+      }
+    *score_out = bv;
+    int cur = best_i;
+    path_out[T - 1] = cur;
+    for (int t = T - 1; t > 0; --t) {
+      cur = back[(size_t)t * N + cur];
+      path_out[t - 1] = cur;
+    }
+  }
+}
 
 template <class TE, class TA, bool kSmemBack>
 __global__ void __launch_bounds__(32) viterbi_kernel(const TE *__restrict__ em,
@@ -38,56 +123,19 @@ __global__ void __launch_bounds__(32) viterbi_kernel(const TE *__restrict__ em,
   const int T = em_len[b];
   uint8_t *back = kSmemBack ? smem : back_ws + (size_t)b * d.Tmax * N;
   const TE *e = em + (size_t)b * d.Tmax * N;
-
   double arow[32];
+  bool finite = true;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
+  for (int j = 0; j < 32; ++j) {
     arow[j] = (trans != nullptr && lane < N && j < N) ? (double)trans[lane * N + j] : 0.0;
-
-  double dp = lane < N ? (double)e[lane] : -CUDART_INF;
-  dp_buf[0][lane] = dp;
-  for (int t = 1; t < T; ++t) {
-    __syncwarp();
-    const double *prev = dp_buf[(t - 1) & 1];
-    const double et = lane < N ? (double)e[(size_t)t * N + lane] : 0.0;
-    double best = prev[0] + arow[0];
-    int arg = 0;
-#pragma unroll
-    for (int j = 1; j < 32; ++j) {
-      if (j < N) {
-        const double c = prev[j] + arow[j];
-        // first maximum wins; a NaN becomes (and stays) the maximum
-        if (!isnan(best) && (c > best || isnan(c))) {
-          best = c;
-          arg = j;
-        }
-      }
-    }
-    dp = et + best;
-    if (lane < N) back[(size_t)t * N + lane] = (uint8_t)arg;
-    dp_buf[t & 1][lane] = lane < N ? dp : -CUDART_INF;
+    finite &= isfinite(arow[j]);
   }
-  __syncwarp();
-  // final argmax (first maximum): gather dp to lane 0 through shared memory
-  const double *fin = dp_buf[(T - 1) & 1];
-  if (lane == 0) {
-    int best_i = 0;
-    double bv = fin[0];
-    for (int i = 1; i < N; ++i) {
-      const double v = fin[i];
-      if (!isnan(bv) && (v > bv || isnan(v))) {
-        bv = v;
-        best_i = i;
-      }
-    }
-    score[b] = bv;
-    int cur = best_i;
-    pb[T - 1] = cur;
-    for (int t = T - 1; t > 0; --t) {
-      cur = back[(size_t)t * N + cur];
-      pb[t - 1] = cur;
-    }
-  }
+  // A may hold inf/NaN (the reference does not validate it, :270-272): only
+  // then is the NaN-aware comparison needed
+  if (__all_sync(0xffffffffu, finite))
+    viterbi_body<TE, TA, kSmemBack, false>(e, T, N, lane, arow, dp_buf, back, score + b, pb);
+  else
+    viterbi_body<TE, TA, kSmemBack, true>(e, T, N, lane, arow, dp_buf, back, score + b, pb);
   for (int t = T + lane; t < d.Tmax; t += 32) pb[t] = 0;
 }
 
