@@ -56,6 +56,36 @@ __device__ __forceinline__ float trans_max(const float *trans, int N) {
 // 30^2 (fcc) and 2^kRenorm (fac), shrinkage by exp(-2 range(A)) resp. the
 // emissions -- anything the bounds cannot cover trips the guard.
 
+// Power-of-two scale for a recursion whose vector sum is only known one
+// step late.  At step t the exponent e_{t-1} of the vector consumed by step t
+// (scaled by 2^-K_{t-1}) becomes available after step t's own scale k_t is
+// chosen, so k_t is predicted from the true (unscaled) log-masses
+// X_s = e_s + K_s:  K_t = X_{t-2} + (X_{t-2} - X_{t-3}).  Then the scaled
+// log-mass is x_t = (X_t - X_{t-2}) - (X_{t-2} - X_{t-3}), bounded by the
+// per-step growth of the recursion -- unlike using k_t = e_{t-2} directly,
+// whose x_t = g + x_{t-1} - x_{t-2} is only marginally stable and drifts.
+struct LaggedScale {
+  int K1 = 0;                    // cumulative exponent of the newest vector
+  int X2 = 0, X3 = 0, seen = 0;  // log-masses of the last two observed vectors
+  int pending_K = 0;             // K of the vector whose exponent arrives next
+  // exponent for the vector being produced now (the one read this step has K1)
+  __device__ __forceinline__ int next() {
+    int Kt = K1;
+    if (seen >= 2) Kt = X2 + (X2 - X3);
+    else if (seen == 1) Kt = X2;
+    const int k = max(-120, min(120, Kt - K1));
+    pending_K = K1;
+    K1 += k;
+    return k;
+  }
+  // e = floor(log2(sum)) of the vector read this step (scaled by pending_K)
+  __device__ __forceinline__ void observe(int e) {
+    X3 = X2;
+    X2 = e + pending_K;
+    ++seen;
+  }
+};
+
 // fcc alpha (criterion.py:227-231): lane i owns token i and row i of M
 __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * 33],
                                           float (*vec)[32], float *out, int *outk,
@@ -70,7 +100,8 @@ __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChu
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[0], c, 0);
   float a = 0.f;
-  int K = 0, kpend = 0;  // exponent measured one step ago, applied now
+  int K = 0;
+  LaggedScale sc;
   for (int ch = 0; ch < nch; ++ch) {
     float *buf = chunk[ch & 1];
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
@@ -99,19 +130,19 @@ __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChu
         acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
       }
       const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      int knew;
+      int e1;  // floor(log2(sum(alpha_{t-1}))): the vector this step read
       if (spare) {
-        knew = exponent_of(__shfl_sync(0xffffffffu, s, N));  // sum(alpha_{t-1})
+        e1 = exponent_of(__shfl_sync(0xffffffffu, s, N));
       } else {
         float tot = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-        knew = exponent_of(tot);
+        e1 = exponent_of(tot);
       }
-      const int k = kpend;
-      kpend = max(-126, min(126, knew));
+      const int k = sc.next();
       K += k;
       a = et * (s * pow2f(-k));
+      sc.observe(e1);
       vec[t & 1][lane] = lane < N ? a : 0.f;
       if (lane < N) out[t * 32 + lane] = a;
       if (lane == 0) outk[t] = K;
@@ -135,7 +166,8 @@ __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChun
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
   float bb = lane < N ? 1.f : 0.f;
-  int K = 0, kpend = 0;
+  int K = 0;
+  LaggedScale sc;
   out[(T - 1) * 32 + lane] = bb;
   if (lane == 0) outk[T - 1] = 0;
   float e0 = 0.f;
@@ -160,19 +192,19 @@ __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChun
         acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
       }
       const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      int knew;
+      int e1;  // floor(log2(sum(w_u))): the vector this step read
       if (spare) {
-        knew = exponent_of(__shfl_sync(0xffffffffu, s, N));
+        e1 = exponent_of(__shfl_sync(0xffffffffu, s, N));
       } else {
         float tot = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-        knew = exponent_of(tot);
+        e1 = exponent_of(tot);
       }
-      const int k = kpend;
-      kpend = max(-126, min(126, knew));
+      const int k = sc.next();
       K += k;
       bb = lane < N ? s * pow2f(-k) : 0.f;
+      sc.observe(e1);
       if (lane < N) out[(u - 1) * 32 + lane] = bb;
       if (lane == 0) outk[u - 1] = K;
     }
@@ -478,10 +510,11 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     lane_load<SPL>(vb, w.fac_b + (row0 + t) * LP, lane);
     const int ea = w.fac_ea[(row0 + t) * 32 + lane];
     const int eb = w.fac_eb[(row0 + t) * 32 + lane];
-    const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
-    const int es = alive ? ea + eb : kNegExp;
+    // frame reference exponent from the actual magnitudes (the chains
+    // renormalise lazily, so a lane exponent alone can overstate its block)
+    const int es = lane_pair_exponent<SPL>(va, vb, ea, eb);
     const int estar = warp_max(es);
-    const float sc = alive ? pow2f(es - estar) : 0.f;
+    const float sc = es > kNegExp / 2 ? pow2f(ea + eb - estar) : 0.f;
     float zl = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
@@ -499,18 +532,20 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     float con = 0.f;
     for (int q = ts0; q < ts1; ++q) con += myp[perm[q]];
     if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
-    // ---- fac edge posteriors (:218-224)
+    // ---- fac edge posteriors (:218-224); the power of two is applied with
+    // ldexpf to the finished mantissa product so no intermediate can overflow
     if (t >= 1) {
       const float nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
       const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
-      const float base = pow2f(pea + eb - estar) * inv_zc;
-      const float nbase = (lane > 0) ? pow2f(nbe + eb - estar) * inv_zc : 0.f;
+      const int d_own = max(pea + eb - estar, -1000);
+      const int d_nb = lane > 0 ? max(nbe + eb - estar, -1000) : -1000;
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
         const float ev = mye[tok[k]] * vb[k];
-        accS[k] = fmaf(pa[k] * S[k], ev * base, accS[k]);
-        const float prev = k > 0 ? pa[k - 1] * base : nbv * nbase;
-        accP[k] = fmaf(prev * P[k], ev, accP[k]);
+        accS[k] = fmaf(ldexpf(pa[k] * S[k] * ev, d_own), inv_zc, accS[k]);
+        const float prev = k > 0 ? ldexpf(pa[k - 1] * P[k] * ev, d_own)
+                                 : ldexpf(nbv * P[k] * ev, d_nb);
+        accP[k] = fmaf(prev, inv_zc, accP[k]);
       }
     }
     // carry alpha_t as alpha_{t-1} for the next frame
@@ -608,6 +643,7 @@ __global__ void __launch_bounds__(256)
       if (l > 0 && (int)y[l - 1] == j) con += sEdge[LP + l];
     }
     ga_utt[(size_t)b * NN + p] = full - con;
+    if (!isfinite(full - con)) atomicOr(&s_bad, 1);
   }
   // guard: every frame's normaliser must reproduce the forward totals
   const double ln2 = 0.6931471805599453;

@@ -117,4 +117,16 @@ __device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[S
   return nb * pow2f(dd);
 }
 
+// floor(log2(max_k a[k] b[k])) + ea + eb, a bound on this lane's largest
+// alpha*beta product (kNegExp if either side is dead or all-zero)
+template <int SPL>
+__device__ __forceinline__ int lane_pair_exponent(const float (&a)[SPL], const float (&b)[SPL],
+                                                  int ea, int eb) {
+  float m = 0.f;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) m = fmaxf(m, a[k] * b[k]);
+  if (!(m > 0.f) || ea <= kNegExp / 2 || eb <= kNegExp / 2) return kNegExp;
+  return ea + eb + exponent_of(m);
+}
+
 }  // namespace w2l

@@ -215,10 +215,9 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     lane_load<SPL>(vb, w.b + (row0 + t) * LP, lane);
     const int ea = w.ea[(row0 + t) * 32 + lane];
     const int eb = w.eb[(row0 + t) * 32 + lane];
-    const bool alive = ea > kNegExp / 2 && eb > kNegExp / 2;
-    const int es = alive ? ea + eb : kNegExp;
+    const int es = lane_pair_exponent<SPL>(va, vb, ea, eb);
     const int estar = warp_max(es);
-    const float sc = alive ? pow2f(es - estar) : 0.f;
+    const float sc = es > kNegExp / 2 ? pow2f(ea + eb - estar) : 0.f;
     float zl = 0.f, zb = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {

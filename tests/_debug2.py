@@ -4,9 +4,9 @@ from conftest import load_npz
 from paper_1812_07625_b200 import criterion as C, _native as nat
 from oracle import criterion_oracle as orc
 def al(x): return (x + 255)//256*256
-g = load_npz("asg_c1")
+name = sys.argv[1] if len(sys.argv) > 1 else "asg_c1"; g = load_npz(name)
 B, T, N = g["em"].shape; L = g["targets"].shape[1]
-spl = 2 if 64 >= L else 4; lpad = spl*32; nblk = (T+63)//64; BT = B*T
+spl = next(o for o in [2,4,8,10,12,16,20,24,32] if 32*o >= L); lpad = spl*32; nblk = (T+63)//64; BT = B*T
 ws = torch.zeros(nat.lib().w2l_asg_workspace_bytes(B, T, N, L), dtype=torch.uint8, device="cuda")
 out = C.asg_loss_grad_batched(torch.from_numpy(g["em"]).cuda(), g["em_len"], g["targets"], g["tgt_len"], g["trans"], check=False, fallback=False, workspace=ws)
 torch.cuda.synchronize()
@@ -24,3 +24,18 @@ fb = get("fcc_b", torch.float32).reshape(B, T, 32); kb = get("fcc_kb", torch.int
 print("fcc_b rows", fb[0, -3:, :6], kb[0, -5:])
 for b in range(B):
     print(b, "grad rel", orc.rel_err(out.grad_emissions[b].cpu().numpy(), g["grad_e"][b]), "gA", orc.rel_err(out.grad_transitions.cpu().numpy(), g["grad_a_per_utt"].sum(0)))
+import math
+print("fcc_a nan rows", np.where(~np.isfinite(fa[0]).all(axis=1))[0][:10], "ka range", ka[0].min(), ka[0].max())
+print("fcc_b nan rows", np.where(~np.isfinite(fb[0]).all(axis=1))[0][:10], "kb range", kb[0].min(), kb[0].max())
+print("fcc_a row sums log2 (first 12)", np.log2(fa[0,:12].sum(1)))
+print("fcc_b row sums log2 (last 12)", np.log2(fb[0,-12:].sum(1)))
+fac = get("fac_a", torch.float32).reshape(B, T, lpad); ea = get("fac_ea", torch.int32).reshape(B, T, 32)
+print("fac_a nan rows", np.where(~np.isfinite(fac[0]).all(axis=1))[0][:10])
+ge = out.grad_emissions[0].cpu().numpy(); print("grad nan rows", np.where(~np.isfinite(ge).all(axis=1))[0][:10])
+pA = get("pA", torch.float32).reshape(B, nblk, 32, 32); pE = get("pE", torch.float32).reshape(B, nblk, 2, lpad)
+print("pA nonfinite blocks", np.where(~np.isfinite(pA[0]).all(axis=(1,2)))[0])
+print("pE nonfinite blocks", np.where(~np.isfinite(pE[0]).all(axis=(1,2)))[0])
+bad = np.where(~np.isfinite(pE[0]))
+print("pE bad idx", list(zip(*[x[:10] for x in bad])))
+ebv = get("fac_eb", torch.int32).reshape(B, T, 32)
+print("ea/eb rows 60..66 lanes 0..12:\n", ea[0, 60:67, :12], "\n", ebv[0, 60:67, :12])
