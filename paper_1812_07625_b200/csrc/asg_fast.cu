@@ -44,31 +44,33 @@ __device__ __forceinline__ float trans_max(const float *trans, int N) {
 
 // ---------------------------------------------------------- chain kernel --
 // One warp per (utterance, role).  Loops are chunk-major: a chunk of kChunk
-// frames is staged (cp.async, one chunk in flight) and converted to Et once,
-// then the inner loop walks its rows with a plain shared-memory row pointer.
-// Rescaling is lazy:
-//   fcc: the normaliser of step t is the exponent of sum(alpha_{t-2}), which
-//        a spare lane (row of ones in M) produces as a by-product of step t-1's
-//        mat-vec and a shuffle delivers one step later -- off the critical
-//        path (for N = 32 every lane sums the vector instead);
+// frames is staged (cp.async, one chunk in flight) and converted to Et once;
+// full chunks are then walked in fully unrolled blocks of kUnroll frames, so
+// every shared-memory row offset, store offset, buffer parity and
+// renormalisation decision is a compile-time constant (no per-frame address
+// arithmetic or branches on the critical path).  The first/last partial
+// chunks take a generic per-frame path.
+// Rescaling is lazy and exact (powers of two):
+//   fcc: the exponent of sum(vector read this step) arrives through a spare
+//        lane (row of ones in M) after the step's own scale is chosen; the
+//        scale is predicted from the last two observed log-masses
+//        (LaggedScale) -- off the critical path (for N = 32 every lane sums);
 //   fac: each lane renormalises its block every kRenorm frames.
-// Both are exact (powers of two); growth between rescales is bounded by
-// 30^2 (fcc) and 2^kRenorm (fac), shrinkage by exp(-2 range(A)) resp. the
-// emissions -- anything the bounds cannot cover trips the guard.
+// Growth between rescales is bounded; whatever the bounds cannot cover (huge
+// transition ranges, emissions that underflow) trips the guard.
 
 // Power-of-two scale for a recursion whose vector sum is only known one
 // step late.  At step t the exponent e_{t-1} of the vector consumed by step t
-// (scaled by 2^-K_{t-1}) becomes available after step t's own scale k_t is
-// chosen, so k_t is predicted from the true (unscaled) log-masses
-// X_s = e_s + K_s:  K_t = X_{t-2} + (X_{t-2} - X_{t-3}).  Then the scaled
-// log-mass is x_t = (X_t - X_{t-2}) - (X_{t-2} - X_{t-3}), bounded by the
-// per-step growth of the recursion -- unlike using k_t = e_{t-2} directly,
-// whose x_t = g + x_{t-1} - x_{t-2} is only marginally stable and drifts.
+// becomes available after step t's own scale k_t is chosen, so k_t is
+// predicted from the true (unscaled) log-masses X_s = e_s + K_s:
+// K_t = X_{t-2} + (X_{t-2} - X_{t-3}).  The scaled log-mass is then
+// x_t = (X_t - X_{t-2}) - (X_{t-2} - X_{t-3}), bounded by the per-step growth
+// of the recursion -- unlike k_t = e_{t-2} directly, whose
+// x_t = g + x_{t-1} - x_{t-2} is only marginally stable and drifts.
 struct LaggedScale {
   int K1 = 0;                    // cumulative exponent of the newest vector
   int X2 = 0, X3 = 0, seen = 0;  // log-masses of the last two observed vectors
   int pending_K = 0;             // K of the vector whose exponent arrives next
-  // exponent for the vector being produced now (the one read this step has K1)
   __device__ __forceinline__ int next() {
     int Kt = K1;
     if (seen >= 2) Kt = X2 + (X2 - X3);
@@ -78,7 +80,6 @@ struct LaggedScale {
     K1 += k;
     return k;
   }
-  // e = floor(log2(sum)) of the vector read this step (scaled by pending_K)
   __device__ __forceinline__ void observe(int e) {
     X3 = X2;
     X2 = e + pending_K;
@@ -86,132 +87,161 @@ struct LaggedScale {
   }
 };
 
-// fcc alpha (criterion.py:227-231): lane i owns token i and row i of M
-__device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * 33],
+// ---- fcc: one frame of the 32-lane mat-vec recursion.  `vin` is the vector
+// of the previous step (alpha_{t-1}, or w_u = Et_u * beta'_u), m the lane's
+// row (alpha) or column (beta) of M; returns the unscaled product.
+__device__ __forceinline__ float fcc_matvec(const float (&m)[32], const float *vin, bool spare,
+                                            int N, int &e_sum) {
+  const float4 *pv = reinterpret_cast<const float4 *>(vin);
+  float acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 x = pv[q];
+    acc[q] = m[4 * q] * x.x;
+    acc[q] = fmaf(m[4 * q + 1], x.y, acc[q]);
+    acc[q] = fmaf(m[4 * q + 2], x.z, acc[q]);
+    acc[q] = fmaf(m[4 * q + 3], x.w, acc[q]);
+  }
+  const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  if (spare) {
+    e_sum = exponent_of(__shfl_sync(0xffffffffu, s, N));   // lane N: row of ones
+  } else {
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
+    e_sum = exponent_of(tot);
+  }
+  return s;
+}
+
+struct FccState {
+  float m[32];
+  float v;       // this lane's current alpha_t / beta'_t
+  int K;
+  LaggedScale sc;
+  bool spare;
+};
+
+// fcc alpha step t (criterion.py:230): alpha_t = Et (.) (M alpha_{t-1}) 2^-k
+__device__ __forceinline__ void fcc_alpha_step(FccState &f, const float *row, float (*vec)[32],
+                                               int par, float *out_row, int *outk_t, int lane,
+                                               int N) {
+  const float et = row[lane];
+  __syncwarp();
+  int e1;
+  const float s = fcc_matvec(f.m, vec[par ^ 1], f.spare, N, e1);
+  const int k = f.sc.next();
+  f.K += k;
+  f.v = et * (s * pow2f(-k));
+  f.sc.observe(e1);
+  vec[par][lane] = f.v;
+  out_row[lane] = f.v;
+  if (lane == 0) *outk_t = f.K;
+}
+
+// fcc beta' step consuming frame u (criterion.py:236): beta'_{u-1} = M^T (Et_u beta'_u) 2^-k
+__device__ __forceinline__ void fcc_beta_step(FccState &f, const float *row, float (*vec)[32],
+                                              int par, float *out_row, int *outk_t, int lane,
+                                              int N) {
+  vec[par][lane] = row[lane] * f.v;
+  __syncwarp();
+  int e1;
+  const float s = fcc_matvec(f.m, vec[par], f.spare, N, e1);
+  const int k = f.sc.next();
+  f.K += k;
+  f.v = lane < N ? s * pow2f(-k) : 0.f;
+  f.sc.observe(e1);
+  out_row[lane] = f.v;
+  if (lane == 0) *outk_t = f.K;
+}
+
+__device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
                                           float (*vec)[32], float *out, int *outk,
                                           double *lnz) {
   const int lane = c.lane, N = c.N, T = c.T;
-  const bool spare = N < 32;  // lane N sums the vector (row of ones)
-  float mr[32];
+  FccState f;
+  f.spare = N < 32;
 #pragma unroll
   for (int j = 0; j < 32; ++j)
-    mr[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax)
-                                : ((spare && lane == N && j < N) ? 1.f : 0.f);
+    f.m[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax)
+                                 : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
+  f.K = 0;
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[0], c, 0);
-  float a = 0.f;
-  int K = 0;
-  LaggedScale sc;
   for (int ch = 0; ch < nch; ++ch) {
     float *buf = chunk[ch & 1];
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
     stage_convert(buf, c, rows);
     if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
-    int r = 0;
-    if (ch == 0) {
-      a = lane < N ? buf[lane] : 0.f;
-      vec[0][lane] = lane < N ? a : 0.f;
-      out[lane] = lane < N ? a : 0.f;
-      if (lane == 0) outk[0] = 0;
-      r = 1;
-    }
-    for (; r < rows; ++r) {
-      const int t = t0 + r;
-      const float et = buf[r * c.stride + (lane < N ? lane : N)];
-      __syncwarp();
-      const float4 *pv = reinterpret_cast<const float4 *>(vec[(t - 1) & 1]);
-      float acc[8];
+    if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+      for (int g = 0; g < kChunk; g += kUnroll) {
+        const int tb = t0 + g;   // multiple of kUnroll: parities are static
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 x = pv[q];
-        acc[q] = mr[4 * q] * x.x;
-        acc[q] = fmaf(mr[4 * q + 1], x.y, acc[q]);
-        acc[q] = fmaf(mr[4 * q + 2], x.z, acc[q]);
-        acc[q] = fmaf(mr[4 * q + 3], x.w, acc[q]);
+        for (int q = 0; q < kUnroll; ++q)
+          fcc_alpha_step(f, buf + (g + q) * kStride, vec, q & 1, out + (tb + q) * 32,
+                         outk + tb + q, lane, N);
       }
-      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      int e1;  // floor(log2(sum(alpha_{t-1}))): the vector this step read
-      if (spare) {
-        e1 = exponent_of(__shfl_sync(0xffffffffu, s, N));
-      } else {
-        float tot = 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-        e1 = exponent_of(tot);
+    } else {
+      int r = 0;
+      if (ch == 0) {
+        f.v = buf[lane];               // alpha_0 = Et_0 (criterion.py:228)
+        vec[0][lane] = f.v;
+        out[lane] = f.v;
+        if (lane == 0) outk[0] = 0;
+        r = 1;
       }
-      const int k = sc.next();
-      K += k;
-      a = et * (s * pow2f(-k));
-      sc.observe(e1);
-      vec[t & 1][lane] = lane < N ? a : 0.f;
-      if (lane < N) out[t * 32 + lane] = a;
-      if (lane == 0) outk[t] = K;
+      for (; r < rows; ++r) {
+        const int t = t0 + r;
+        fcc_alpha_step(f, buf + r * kStride, vec, t & 1, out + t * 32, outk + t, lane, N);
+      }
     }
   }
-  const float z = warp_sum(lane < N ? a : 0.f);
-  if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
+  const float z = warp_sum(lane < N ? f.v : 0.f);
+  if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
-// fcc beta' (excludes frame t's emission; :233-236): lane j owns column j
-__device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChunk * 33],
-                                         float (*vec)[32], float *out, int *outk,
-                                         double *lnz) {
+__device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
+                                         float (*vec)[32], float *out, int *outk, double *lnz) {
   const int lane = c.lane, N = c.N, T = c.T;
-  const bool spare = N < 32;
-  float mc[32];
+  FccState f;
+  f.spare = N < 32;
 #pragma unroll
   for (int i = 0; i < 32; ++i)
-    mc[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax)
-                                : ((spare && lane == N && i < N) ? 1.f : 0.f);
+    f.m[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax)
+                                 : ((f.spare && lane == N && i < N) ? 1.f : 0.f);
+  f.K = 0;
+  f.v = lane < N ? 1.f : 0.f;
+  out[(T - 1) * 32 + lane] = f.v;
+  if (lane == 0) outk[T - 1] = 0;
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
-  float bb = lane < N ? 1.f : 0.f;
-  int K = 0;
-  LaggedScale sc;
-  out[(T - 1) * 32 + lane] = bb;
-  if (lane == 0) outk[T - 1] = 0;
   float e0 = 0.f;
   for (int ch = nch - 1; ch >= 0; --ch) {
     float *buf = chunk[ch & 1];
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
     stage_convert(buf, c, rows);
     if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
-    for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
-      const int u = t0 + r;  // consumes frame u, produces beta'_{u-1}
-      const float eu = buf[r * c.stride + (lane < N ? lane : N)];
-      vec[u & 1][lane] = lane < N ? eu * bb : 0.f;
-      __syncwarp();
-      const float4 *pv = reinterpret_cast<const float4 *>(vec[u & 1]);
-      float acc[8];
+    if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+        const int ub = t0 + g;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 x = pv[q];
-        acc[q] = mc[4 * q] * x.x;
-        acc[q] = fmaf(mc[4 * q + 1], x.y, acc[q]);
-        acc[q] = fmaf(mc[4 * q + 2], x.z, acc[q]);
-        acc[q] = fmaf(mc[4 * q + 3], x.w, acc[q]);
+        for (int q = kUnroll - 1; q >= 0; --q)
+          fcc_beta_step(f, buf + (g + q) * kStride, vec, q & 1, out + (ub + q - 1) * 32,
+                        outk + ub + q - 1, lane, N);
       }
-      const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      int e1;  // floor(log2(sum(w_u))): the vector this step read
-      if (spare) {
-        e1 = exponent_of(__shfl_sync(0xffffffffu, s, N));
-      } else {
-        float tot = 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-        e1 = exponent_of(tot);
+    } else {
+      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+        const int u = t0 + r;   // consumes frame u, produces beta'_{u-1}
+        fcc_beta_step(f, buf + r * kStride, vec, u & 1, out + (u - 1) * 32, outk + u - 1,
+                      lane, N);
       }
-      const int k = sc.next();
-      K += k;
-      bb = lane < N ? s * pow2f(-k) : 0.f;
-      sc.observe(e1);
-      if (lane < N) out[(u - 1) * 32 + lane] = bb;
-      if (lane == 0) outk[u - 1] = K;
     }
-    if (ch == 0) e0 = lane < N ? buf[lane] : 0.f;
+    if (ch == 0) e0 = buf[lane];
   }
-  const float z = warp_sum(e0 * bb);
-  if (lane == 0) *lnz = log((double)z) + (double)K * 0.6931471805599453;
+  const float z = warp_sum(e0 * f.v);
+  if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
 // fac chain weights for this lane's states l = lane*SPL + k: token, stay
@@ -241,16 +271,63 @@ __device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y,
   }
 }
 
-// fac alpha (criterion.py:193-203) in block floating point
 template <int SPL>
-__device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * 33],
-                                          const int64_t *y, int L, float *out, int *oute,
-                                          int lp, double *lnz) {
-  const int lane = c.lane, T = c.T;
+struct FacState {
   int tok[SPL];
   float S[SPL], P[SPL], v[SPL];
-  fac_weights<SPL>(c, y, L, true, tok, S, P);
-  int ex = 0;
+  int ex;
+};
+
+// fac alpha step t (criterion.py:197-202) in block floating point
+template <int SPL>
+__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *row, bool renorm,
+                                               float *out, int *oute, int lane, int t) {
+  float E[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) E[k] = row[f.tok[k]];
+  float nb = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
+  int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
+  if (lane == 0) {
+    nb = 0.f;
+    nbe = kNegExp;
+  }
+  const float nbs = align_neighbour<SPL>(nb, nbe, f.v, f.ex);
+#pragma unroll
+  for (int k = SPL - 1; k >= 1; --k) f.v[k] = E[k] * fmaf(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
+  f.v[0] = E[0] * fmaf(f.S[0], f.v[0], f.P[0] * nbs);
+  if (renorm) lane_renorm<SPL>(f.v, f.ex);
+  lane_store<SPL>(f.v, f.ex, out, oute, lane, t);
+}
+
+// fac beta' step consuming frame u (criterion.py:207-212)
+template <int SPL>
+__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row, bool renorm,
+                                              float *out, int *oute, int lane, int t_out) {
+  float wv[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) wv[k] = row[f.tok[k]] * f.v[k];
+  float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
+  int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
+  if (lane == 31) {
+    nb = 0.f;
+    nbe = kNegExp;
+  }
+  const float nbs = align_neighbour<SPL>(nb, nbe, wv, f.ex);
+#pragma unroll
+  for (int k = 0; k < SPL - 1; ++k) f.v[k] = fmaf(f.S[k], wv[k], f.P[k] * wv[k + 1]);
+  f.v[SPL - 1] = fmaf(f.S[SPL - 1], wv[SPL - 1], f.P[SPL - 1] * nbs);
+  if (renorm) lane_renorm<SPL>(f.v, f.ex);
+  lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
+}
+
+template <int SPL>
+__device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
+                                          const int64_t *y, int L, float *out, int *oute,
+                                          double *lnz) {
+  const int lane = c.lane, T = c.T;
+  FacState<SPL> f;
+  fac_weights<SPL>(c, y, L, true, f.tok, f.S, f.P);
+  f.ex = 0;
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[0], c, 0);
   for (int ch = 0; ch < nch; ++ch) {
@@ -258,57 +335,53 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
     stage_convert(buf, c, rows);
     if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
-    int r = 0;
-    if (ch == 0) {  // t = 0: only the first target state is reachable (:194)
+    if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+      for (int g = 0; g < kChunk; g += kUnroll) {
+        const int tb = t0 + g;
+        float *ob = out + (size_t)tb * (SPL * 32);
+        int *oeb = oute + tb * 32;
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) v[k] = 0.f;
-      if (lane == 0) v[0] = buf[tok[0]];
-      lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
-      r = 1;
-    }
-    for (; r < rows; ++r) {
-      const int t = t0 + r;
-      const float *row = buf + r * c.stride;
-      float E[SPL];
-#pragma unroll
-      for (int k = 0; k < SPL; ++k) E[k] = row[tok[k]];
-      float nb = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
-      int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
-      if (lane == 0) {
-        nb = 0.f;
-        nbe = kNegExp;
+        for (int q = 0; q < kUnroll; ++q)
+          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, ob, oeb, lane, q);
       }
-      const float nbs = align_neighbour<SPL>(nb, nbe, v, ex);
+    } else {
+      int r = 0;
+      if (ch == 0) {   // t = 0: only the first target state is reachable (:194)
 #pragma unroll
-      for (int k = SPL - 1; k >= 1; --k) v[k] = E[k] * fmaf(S[k], v[k], P[k] * v[k - 1]);
-      v[0] = E[0] * fmaf(S[0], v[0], P[0] * nbs);
-      if ((t & (kRenorm - 1)) == 0 || t == T - 1) lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, lp, lane, t);
+        for (int k = 0; k < SPL; ++k) f.v[k] = 0.f;
+        if (lane == 0) f.v[0] = buf[f.tok[0]];
+        lane_renorm<SPL>(f.v, f.ex);
+        lane_store<SPL>(f.v, f.ex, out, oute, lane, 0);
+        r = 1;
+      }
+      for (; r < rows; ++r) {
+        const int t = t0 + r;
+        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, out, oute,
+                            lane, t);
+      }
     }
   }
   // fac score = alpha_{T-1}[L-1] (:203)
   const int lastl = L - 1;
   float vl = 0.f;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) vl = (lane * SPL + k == lastl) ? v[k] : vl;
-  if (lane == lastl / SPL) *lnz = log((double)vl) + (double)ex * 0.6931471805599453;
+  for (int k = 0; k < SPL; ++k) vl = (lane * SPL + k == lastl) ? f.v[k] : vl;
+  if (lane == lastl / SPL) *lnz = log((double)vl) + (double)f.ex * 0.6931471805599453;
 }
 
-// fac beta' (criterion.py:205-212, without frame t's emission)
 template <int SPL>
-__device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * 33],
+__device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
                                          const int64_t *y, int L, float *out, int *oute,
-                                         int lp, double *lnz) {
+                                         double *lnz) {
   const int lane = c.lane, T = c.T;
-  int tok[SPL];
-  float S[SPL], P[SPL], v[SPL];
-  fac_weights<SPL>(c, y, L, false, tok, S, P);
+  FacState<SPL> f;
+  fac_weights<SPL>(c, y, L, false, f.tok, f.S, f.P);
   const int lastl = L - 1;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
-  int ex = (lane == lastl / SPL) ? 0 : kNegExp;
-  lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
+  for (int k = 0; k < SPL; ++k) f.v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
+  f.ex = (lane == lastl / SPL) ? 0 : kNegExp;
+  lane_store<SPL>(f.v, f.ex, out, oute, lane, T - 1);
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
   float e0 = 0.f;
@@ -317,28 +390,27 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
     stage_convert(buf, c, rows);
     if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
-    for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
-      const int u = t0 + r;
-      const float *row = buf + r * c.stride;
-      float wv[SPL];
+    if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+        const int ub = t0 + g;   // frames ub .. ub+7 produce beta' at ub-1 .. ub+6
+        float *ob = out + (size_t)(ub - 1) * (SPL * 32);
+        int *oeb = oute + (ub - 1) * 32;
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) wv[k] = row[tok[k]] * v[k];
-      float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
-      int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
-      if (lane == 31) {
-        nb = 0.f;
-        nbe = kNegExp;
+        for (int q = kUnroll - 1; q >= 0; --q)
+          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
+                             ob, oeb, lane, q);
       }
-      const float nbs = align_neighbour<SPL>(nb, nbe, wv, ex);
-#pragma unroll
-      for (int k = 0; k < SPL - 1; ++k) v[k] = fmaf(S[k], wv[k], P[k] * wv[k + 1]);
-      v[SPL - 1] = fmaf(S[SPL - 1], wv[SPL - 1], P[SPL - 1] * nbs);
-      if (((u - 1) & (kRenorm - 1)) == 0 || u == 1) lane_renorm<SPL>(v, ex);
-      lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
+    } else {
+      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+        const int u = t0 + r;
+        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, out, oute,
+                           lane, u - 1);
+      }
     }
-    if (ch == 0) e0 = buf[tok[0]];
+    if (ch == 0) e0 = buf[f.tok[0]];
   }
-  if (lane == 0) *lnz = log((double)(e0 * v[0])) + (double)ex * 0.6931471805599453;
+  if (lane == 0) *lnz = log((double)(e0 * f.v[0])) + (double)f.ex * 0.6931471805599453;
 }
 
 template <int SPL>
@@ -347,7 +419,7 @@ __global__ void __launch_bounds__(32)
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2][kChunk * 33];
+  __shared__ __align__(16) float chunk[2][kChunk * kStride];
   __shared__ __align__(16) float vec[2][32];
   const int b = blockIdx.x, role = blockIdx.y;
   if (status[b] != W2L_OK) return;
@@ -357,7 +429,6 @@ __global__ void __launch_bounds__(32)
   c.N = d.N;
   c.T = em_len[b];
   c.lane = threadIdx.x;
-  c.stride = em_stride(d.N);
   c.amax = trans_max(trans, d.N);
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
@@ -366,11 +437,11 @@ __global__ void __launch_bounds__(32)
   } else if (role == 1) {
     fcc_beta(c, chunk, vec, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
   } else if (role == 2) {
-    fac_alpha<SPL>(c, chunk, y, tgt_len[b], w.fac_a + row0 * w.lpad, w.fac_ea + row0 * 32,
-                   w.lpad, w.scal + b * 4 + 2);
+    fac_alpha<SPL>(c, chunk, y, tgt_len[b], w.fac_a + row0 * (SPL * 32), w.fac_ea + row0 * 32,
+                   w.scal + b * 4 + 2);
   } else {
-    fac_beta<SPL>(c, chunk, y, tgt_len[b], w.fac_b + row0 * w.lpad, w.fac_eb + row0 * 32,
-                  w.lpad, w.scal + b * 4 + 3);
+    fac_beta<SPL>(c, chunk, y, tgt_len[b], w.fac_b + row0 * (SPL * 32), w.fac_eb + row0 * 32,
+                  w.scal + b * 4 + 3);
   }
 }
 

@@ -15,12 +15,14 @@
 
 namespace w2l {
 
-constexpr int kRenorm = 4;  // frames between lane renormalisations
+constexpr int kRenorm = 4;   // frames between lane renormalisations
+constexpr int kStride = 33;  // staged row pitch: odd (conflict-free per-lane rows), > 32
+constexpr int kUnroll = 8;   // frames per fully unrolled block (immediate smem offsets)
 
 struct ChainCtx {
   const float *trans;
   const float *e;  // &em[b][0][0]
-  int N, T, lane, stride;
+  int N, T, lane;
   float amax;
 };
 
@@ -28,22 +30,23 @@ __device__ __forceinline__ void stage_issue(float *dst, const ChainCtx &c, int t
   const int rows = min(kChunk, c.T - t0);
   if (c.lane < c.N)
     for (int r = 0; r < rows; ++r)
-      cp_async4(dst + r * c.stride + c.lane, c.e + (size_t)(t0 + r) * c.N + c.lane);
+      cp_async4(dst + r * kStride + c.lane, c.e + (size_t)(t0 + r) * c.N + c.lane);
   cp_async_commit();
 }
 
-// wait for the staged chunk, convert it to Et in place (lane r owns row r);
-// the row maxima are summed into *shift_sum (the CTC loss offset) if given
+// wait for the staged chunk, convert it to Et in place (lane r owns row r)
+// and zero columns N..32 (padding states and idle lanes read 0); the row
+// maxima are summed into *shift_sum (the CTC loss offset) if given
 __device__ __forceinline__ void stage_convert(float *buf, const ChainCtx &c, int rows,
                                               double *shift_sum = nullptr) {
   cp_async_wait<0>();
   __syncwarp();
   if (c.lane < rows) {
-    float *r = buf + c.lane * c.stride;
+    float *r = buf + c.lane * kStride;
     float m = -CUDART_INF_F;
     for (int i = 0; i < c.N; ++i) m = fmaxf(m, r[i]);
     for (int i = 0; i < c.N; ++i) r[i] = expf(r[i] - m);
-    r[c.N] = 0.f;
+    for (int i = c.N; i < kStride; ++i) r[i] = 0.f;
     if (shift_sum) *shift_sum += (double)m;
   }
   __syncwarp();
@@ -83,8 +86,9 @@ __device__ __forceinline__ void lane_renorm(float (&v)[SPL], int &ex) {
 // states go out as SPL/2 8-byte stores
 template <int SPL>
 __device__ __forceinline__ void lane_store(const float (&v)[SPL], int ex, float *out, int *oute,
-                                           int lp, int lane, int t) {
+                                           int lane, int t) {
   static_assert(SPL % 2 == 0, "SPL must be even");
+  constexpr int lp = SPL * 32;
   float2 *o = reinterpret_cast<float2 *>(out + t * lp + lane * SPL);
 #pragma unroll
   for (int k = 0; k < SPL / 2; ++k) o[k] = make_float2(v[2 * k], v[2 * k + 1]);

@@ -39,11 +39,68 @@ __device__ __forceinline__ void ctc_lattice_lane(const int64_t *y, int L, int bl
 }
 
 template <int SPL>
+struct CtcState {
+  int lab[SPL];
+  float sk[SPL], sk2[SPL], v[SPL];
+  int ex;
+};
+
+// alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])  (:126-134)
+template <int SPL>
+__device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *row, bool renorm,
+                                               float *out, int *oute, int lane, int t) {
+  float E[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) E[k] = row[f.lab[k]];
+  float nb1 = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
+  float nb2 = __shfl_up_sync(0xffffffffu, f.v[SPL - 2], 1);
+  int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
+  if (lane == 0) {
+    nb1 = nb2 = 0.f;
+    nbe = kNegExp;
+  }
+  const float n1 = align_neighbour<SPL>(nb1, nbe, f.v, f.ex);
+  const float n2 = nb2 * pow2f(nbe - f.ex);
+#pragma unroll
+  for (int k = SPL - 1; k >= 2; --k)
+    f.v[k] = E[k] * fmaf(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1]);
+  const float v1 = E[1] * fmaf(f.sk[1], n1, f.v[1] + f.v[0]);
+  f.v[0] = E[0] * fmaf(f.sk[0], n2, f.v[0] + n1);
+  f.v[1] = v1;
+  if (renorm) lane_renorm<SPL>(f.v, f.ex);
+  lane_store<SPL>(f.v, f.ex, out, oute, lane, t);
+}
+
+// beta'_{u-1}[s] = w[s] + w[s+1] + skip_{s+2} w[s+2],  w = Et_u[lab] beta'_u  (:147-155)
+template <int SPL>
+__device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row, bool renorm,
+                                              float *out, int *oute, int lane, int t_out) {
+  float wv[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) wv[k] = row[f.lab[k]] * f.v[k];
+  float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+  float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
+  int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
+  if (lane == 31) {
+    nb1 = nb2 = 0.f;
+    nbe = kNegExp;
+  }
+  const float n1 = align_neighbour<SPL>(nb1, nbe, wv, f.ex);
+  const float n2 = nb2 * pow2f(nbe - f.ex);
+#pragma unroll
+  for (int k = 0; k < SPL - 2; ++k) f.v[k] = fmaf(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
+  f.v[SPL - 2] = fmaf(f.sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
+  f.v[SPL - 1] = fmaf(f.sk2[SPL - 1], n2, wv[SPL - 1] + n1);
+  if (renorm) lane_renorm<SPL>(f.v, f.ex);
+  lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
+}
+
+template <int SPL>
 __global__ void __launch_bounds__(32)
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2][kChunk * 33];
+  __shared__ __align__(16) float chunk[2][kChunk * kStride];
   const int b = blockIdx.x, lane = threadIdx.x;
   if (status[b] != W2L_OK) return;
   ChainCtx c;
@@ -52,22 +109,18 @@ __global__ void __launch_bounds__(32)
   c.N = d.N;
   c.T = em_len[b];
   c.lane = lane;
-  c.stride = em_stride(d.N);
   c.amax = 0.f;
   const int T = c.T, L = tgt_len[b], S = 2 * L + 1;
   const bool fwd = blockIdx.y == 0;
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  int lab[SPL];
-  float sk[SPL], sk2[SPL];
-  ctc_lattice_lane<SPL>(y, L, blank, d.N, lane, lab, sk, sk2);
-  float *out = (fwd ? w.a : w.b) + row0 * w.lpad;
+  CtcState<SPL> f;
+  ctc_lattice_lane<SPL>(y, L, blank, d.N, lane, f.lab, f.sk, f.sk2);
+  float *out = (fwd ? w.a : w.b) + row0 * (SPL * 32);
   int *oute = (fwd ? w.ea : w.eb) + row0 * 32;
-  const int lp = w.lpad;
   const double ln2 = 0.6931471805599453;
   const int nch = (T + kChunk - 1) / kChunk;
-  float v[SPL];
-  int ex = 0;
+  f.ex = 0;
 
   if (fwd) {
     double shifts = 0.0;
@@ -77,40 +130,34 @@ __global__ void __launch_bounds__(32)
       const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
       stage_convert(buf, c, rows, &shifts);
       if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
-      int r = 0;
-      if (ch == 0) {  // criterion.py:123-125
+      if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+        for (int g = 0; g < kChunk; g += kUnroll) {
+          const int tb = t0 + g;
+          float *ob = out + (size_t)tb * (SPL * 32);
+          int *oeb = oute + tb * 32;
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) v[k] = 0.f;
-        if (lane == 0) {
-          v[0] = buf[lab[0]];
-          if (S > 1) v[1] = buf[lab[1]];
+          for (int q = 0; q < kUnroll; ++q)
+            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, ob, oeb, lane, q);
         }
-        lane_renorm<SPL>(v, ex);
-        lane_store<SPL>(v, ex, out, oute, lp, lane, 0);
-        r = 1;
-      }
-      for (; r < rows; ++r) {
-        const int t = t0 + r;
-        const float *row = buf + r * c.stride;
-        float E[SPL];
+      } else {
+        int r = 0;
+        if (ch == 0) {  // criterion.py:123-125
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) E[k] = row[lab[k]];
-        float nb1 = __shfl_up_sync(0xffffffffu, v[SPL - 1], 1);
-        float nb2 = __shfl_up_sync(0xffffffffu, v[SPL - 2], 1);
-        int nbe = __shfl_up_sync(0xffffffffu, ex, 1);
-        if (lane == 0) {
-          nb1 = nb2 = 0.f;
-          nbe = kNegExp;
+          for (int k = 0; k < SPL; ++k) f.v[k] = 0.f;
+          if (lane == 0) {
+            f.v[0] = buf[f.lab[0]];
+            if (S > 1) f.v[1] = buf[f.lab[1]];
+          }
+          lane_renorm<SPL>(f.v, f.ex);
+          lane_store<SPL>(f.v, f.ex, out, oute, lane, 0);
+          r = 1;
         }
-        const float n1 = align_neighbour<SPL>(nb1, nbe, v, ex);
-        const float n2 = nb2 * pow2f(nbe - ex);
-#pragma unroll
-        for (int k = SPL - 1; k >= 2; --k) v[k] = E[k] * fmaf(sk[k], v[k - 2], v[k] + v[k - 1]);
-        const float v1 = E[1] * fmaf(sk[1], n1, v[1] + v[0]);
-        v[0] = E[0] * fmaf(sk[0], n2, v[0] + n1);
-        v[1] = v1;
-        if ((t & (kRenorm - 1)) == 0 || t == T - 1) lane_renorm<SPL>(v, ex);
-        lane_store<SPL>(v, ex, out, oute, lp, lane, t);
+        for (; r < rows; ++r) {
+          const int t = t0 + r;
+          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, out, oute,
+                              lane, t);
+        }
       }
     }
     // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
@@ -118,9 +165,9 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
       const int s = lane * SPL + k;
-      if (s == S - 1 || s == S - 2) part += v[k];
+      if (s == S - 1 || s == S - 2) part += f.v[k];
     }
-    const double lp_ = part > 0.f ? log((double)part) + (double)ex * ln2 : -CUDART_INF;
+    const double lp_ = part > 0.f ? log((double)part) + (double)f.ex * ln2 : -CUDART_INF;
     const double m = warp_max(lp_);
     const double sum = warp_sum(lp_ > -CUDART_INF ? exp(lp_ - m) : 0.0);
     shifts = warp_sum(shifts);
@@ -132,10 +179,10 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
       const int s = lane * SPL + k;
-      v[k] = (s == S - 1 || s == S - 2) ? 1.f : 0.f;
+      f.v[k] = (s == S - 1 || s == S - 2) ? 1.f : 0.f;
     }
-    lane_renorm<SPL>(v, ex);
-    lane_store<SPL>(v, ex, out, oute, lp, lane, T - 1);
+    lane_renorm<SPL>(f.v, f.ex);
+    lane_store<SPL>(f.v, f.ex, out, oute, lane, T - 1);
     stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
     float z0 = 0.f;
     for (int ch = nch - 1; ch >= 0; --ch) {
@@ -143,34 +190,30 @@ __global__ void __launch_bounds__(32)
       const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
       stage_convert(buf, c, rows);
       if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
-      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
-        const int u = t0 + r;
-        const float *row = buf + r * c.stride;
-        float wv[SPL];
+      if (ch > 0 && rows == kChunk) {
+#pragma unroll 1
+        for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+          const int ub = t0 + g;
+          float *ob = out + (size_t)(ub - 1) * (SPL * 32);
+          int *oeb = oute + (ub - 1) * 32;
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) wv[k] = row[lab[k]] * v[k];
-        float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-        float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
-        int nbe = __shfl_down_sync(0xffffffffu, ex, 1);
-        if (lane == 31) {
-          nb1 = nb2 = 0.f;
-          nbe = kNegExp;
+          for (int q = kUnroll - 1; q >= 0; --q)
+            ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
+                               ob, oeb, lane, q);
         }
-        const float n1 = align_neighbour<SPL>(nb1, nbe, wv, ex);
-        const float n2 = nb2 * pow2f(nbe - ex);
-#pragma unroll
-        for (int k = 0; k < SPL - 2; ++k) v[k] = fmaf(sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
-        v[SPL - 2] = fmaf(sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
-        v[SPL - 1] = fmaf(sk2[SPL - 1], n2, wv[SPL - 1] + n1);
-        if (((u - 1) & (kRenorm - 1)) == 0 || u == 1) lane_renorm<SPL>(v, ex);
-        lane_store<SPL>(v, ex, out, oute, lp, lane, u - 1);
+      } else {
+        for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
+          const int u = t0 + r;
+          ctc_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, out,
+                             oute, lane, u - 1);
+        }
       }
       if (ch == 0 && lane == 0) {
-        z0 = buf[lab[0]] * v[0];
-        if (S > 1) z0 += buf[lab[1]] * v[1];
+        z0 = buf[f.lab[0]] * f.v[0];
+        if (S > 1) z0 += buf[f.lab[1]] * f.v[1];
       }
     }
-    if (lane == 0) w.scal[b * 4 + 1] = log((double)z0) + (double)ex * ln2;
+    if (lane == 0) w.scal[b * 4 + 1] = log((double)z0) + (double)f.ex * ln2;
   }
 }
 

@@ -29,30 +29,44 @@ __device__ __forceinline__ bool vit_take(double a, double b) {
 }
 
 // one frame of the max-plus recursion for destination token `lane`;
-// returns the new dp value and writes the backpointer
+// returns the new dp value and writes the backpointer.  Sources j >= N hold
+// dp = -inf (and A = 0), so they never win and need no bounds test.
 template <bool kNanAware>
-__device__ __forceinline__ double vit_step(const double *prev, const double (&arow)[32], int N,
+__device__ __forceinline__ double vit_step(const double *prev, const double (&arow)[32],
                                            double et, int &arg_out) {
-  double c[32];
-  int idx[32];
+  double c16[16];
+  int i16[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    c[j] = j < N ? prev[j] + arow[j] : -CUDART_INF;   // cand_j = dp[j] + A[i][j]
-    idx[j] = j;
+  for (int j = 0; j < 16; ++j) {   // level 1 of the tournament fused with cand_j = dp[j] + A[i][j]
+    const double a = prev[2 * j] + arow[2 * j];
+    const double b = prev[2 * j + 1] + arow[2 * j + 1];
+    const bool tb = vit_take<kNanAware>(a, b);
+    c16[j] = tb ? b : a;
+    i16[j] = tb ? 2 * j + 1 : 2 * j;
   }
-  // pairwise tournament over index-ordered halves keeps first-max semantics
+  double c8[8];
+  int i8[8];
 #pragma unroll
-  for (int w = 1; w < 32; w <<= 1) {
-#pragma unroll
-    for (int j = 0; j < 32; j += 2 * w) {
-      if (vit_take<kNanAware>(c[j], c[j + w])) {
-        c[j] = c[j + w];
-        idx[j] = idx[j + w];
-      }
-    }
+  for (int j = 0; j < 8; ++j) {
+    const bool tb = vit_take<kNanAware>(c16[2 * j], c16[2 * j + 1]);
+    c8[j] = tb ? c16[2 * j + 1] : c16[2 * j];
+    i8[j] = tb ? i16[2 * j + 1] : i16[2 * j];
   }
-  arg_out = idx[0];
-  return et + c[0];                                   // dp'[i] = e[t][i] + cand_back
+  double c4[4];
+  int i4[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool tb = vit_take<kNanAware>(c8[2 * j], c8[2 * j + 1]);
+    c4[j] = tb ? c8[2 * j + 1] : c8[2 * j];
+    i4[j] = tb ? i8[2 * j + 1] : i8[2 * j];
+  }
+  const bool t0 = vit_take<kNanAware>(c4[0], c4[1]);
+  const bool t1 = vit_take<kNanAware>(c4[2], c4[3]);
+  const double c2a = t0 ? c4[1] : c4[0], c2b = t1 ? c4[3] : c4[2];
+  const int i2a = t0 ? i4[1] : i4[0], i2b = t1 ? i4[3] : i4[2];
+  const bool tf = vit_take<kNanAware>(c2a, c2b);
+  arg_out = tf ? i2b : i2a;
+  return et + (tf ? c2b : c2a);                       // dp'[i] = e[t][i] + cand_back
 }
 
 template <class TE, class TA, bool kSmemBack, bool kNanAware>
@@ -61,10 +75,10 @@ __device__ __forceinline__ void viterbi_body(const TE *__restrict__ e, int T, in
                                              uint8_t *back, double *score_out,
                                              int64_t *path_out) {
   constexpr int kPre = 8;   // emission prefetch distance (frames)
-  double pre[kPre];
+  TE pre[kPre];   // raw emissions, converted at use so the load latency stays hidden
 #pragma unroll
   for (int q = 0; q < kPre; ++q)
-    pre[q] = (lane < N && 1 + q < T) ? (double)e[(size_t)(1 + q) * N + lane] : 0.0;
+    pre[q] = (lane < N && 1 + q < T) ? e[(size_t)(1 + q) * N + lane] : TE(0);
   double dp = lane < N ? (double)e[lane] : -CUDART_INF;
   dp_buf[0][lane] = dp;
   for (int t0 = 1; t0 < T; t0 += kPre) {
@@ -72,12 +86,12 @@ __device__ __forceinline__ void viterbi_body(const TE *__restrict__ e, int T, in
     for (int q = 0; q < kPre; ++q) {
       const int t = t0 + q;
       if (t < T) {
-        const double et = pre[q];
+        const double et = (double)pre[q];
         const int tn = t + kPre;
-        pre[q] = (lane < N && tn < T) ? (double)e[(size_t)tn * N + lane] : 0.0;
+        pre[q] = (lane < N && tn < T) ? e[(size_t)tn * N + lane] : TE(0);
         __syncwarp();
         int arg;
-        dp = vit_step<kNanAware>(dp_buf[(t - 1) & 1], arow, N, et, arg);
+        dp = vit_step<kNanAware>(dp_buf[(t - 1) & 1], arow, et, arg);
         if (lane < N) back[(size_t)t * N + lane] = (uint8_t)arg;
         dp_buf[t & 1][lane] = lane < N ? dp : -CUDART_INF;
       }
