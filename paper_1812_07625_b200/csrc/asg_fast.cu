@@ -413,29 +413,32 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
   if (lane == 0) *lnz = log((double)(e0 * f.v[0])) + (double)f.ex * 0.6931471805599453;
 }
 
+// One CTA per utterance with one warp per recursion: warp w runs role w on
+// SM sub-partition w, so the four serial chains never share an issue port.
 template <int SPL>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(128)
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2][kChunk * kStride];
-  __shared__ __align__(16) float vec[2][32];
-  const int b = blockIdx.x, role = blockIdx.y;
+  __shared__ __align__(16) float chunk_all[4][2][kChunk * kStride];
+  __shared__ __align__(16) float vec_all[2][2][32];
+  const int b = blockIdx.x, role = threadIdx.x >> 5;
   if (status[b] != W2L_OK) return;
+  float (*chunk)[kChunk * kStride] = chunk_all[role];
   ChainCtx c;
   c.trans = trans;
   c.e = em + (size_t)b * d.Tmax * d.N;
   c.N = d.N;
   c.T = em_len[b];
-  c.lane = threadIdx.x;
+  c.lane = threadIdx.x & 31;
   c.amax = trans_max(trans, d.N);
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (role == 0) {
-    fcc_alpha(c, chunk, vec, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
+    fcc_alpha(c, chunk, vec_all[0], w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
   } else if (role == 1) {
-    fcc_beta(c, chunk, vec, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
+    fcc_beta(c, chunk, vec_all[1], w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
   } else if (role == 2) {
     fac_alpha<SPL>(c, chunk, y, tgt_len[b], w.fac_a + row0 * (SPL * 32), w.fac_ea + row0 * 32,
                    w.scal + b * 4 + 2);
@@ -741,8 +744,7 @@ template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                        float *grad_em, const int32_t *status, cudaStream_t s) {
-  asg_chain_kernel<SPL><<<dim3(d.B, 4), 32, 0, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
-                                                     status);
+  asg_chain_kernel<SPL><<<d.B, 128, 0, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   constexpr int LP = SPL * 32;

@@ -66,11 +66,22 @@ __device__ __forceinline__ float shifted_prob(const float *erow, int N, int lane
 // Block floating point for a lane's SPL consecutive chain states: scale them
 // so the largest lies in [1, 2) and fold the power of two into the lane
 // exponent (an all-zero lane is marked dead with kNegExp).
+// max over a register array as a balanced tree (depth log2 SPL, not SPL)
+template <int SPL>
+__device__ __forceinline__ float tree_max(const float (&v)[SPL]) {
+  float m[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) m[k] = v[k];
+#pragma unroll
+  for (int w = 1; w < SPL; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < SPL; k += 2 * w) m[k] = fmaxf(m[k], m[k + w]);
+  return fmaxf(m[0], 0.f);
+}
+
 template <int SPL>
 __device__ __forceinline__ void lane_renorm(float (&v)[SPL], int &ex) {
-  float mx = 0.f;
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) mx = fmaxf(mx, v[k]);
+  const float mx = tree_max<SPL>(v);
   if (mx > 0.f) {
     const int kx = exponent_of(mx);
     const float sc = pow2f(-kx);
@@ -126,9 +137,10 @@ __device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[S
 template <int SPL>
 __device__ __forceinline__ int lane_pair_exponent(const float (&a)[SPL], const float (&b)[SPL],
                                                   int ea, int eb) {
-  float m = 0.f;
+  float p[SPL];
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) m = fmaxf(m, a[k] * b[k]);
+  for (int k = 0; k < SPL; ++k) p[k] = a[k] * b[k];
+  const float m = tree_max<SPL>(p);
   if (!(m > 0.f) || ea <= kNegExp / 2 || eb <= kNegExp / 2) return kNegExp;
   return ea + eb + exponent_of(m);
 }

@@ -95,13 +95,15 @@ __device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row
   lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
 }
 
+// One CTA per utterance: warp 0 runs alpha, warp 1 beta (separate SMSPs).
 template <int SPL>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(64)
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2][kChunk * kStride];
-  const int b = blockIdx.x, lane = threadIdx.x;
+  __shared__ __align__(16) float chunk_all[2][2][kChunk * kStride];
+  const int b = blockIdx.x, lane = threadIdx.x & 31;
+  float (*chunk)[kChunk * kStride] = chunk_all[threadIdx.x >> 5];
   if (status[b] != W2L_OK) return;
   ChainCtx c;
   c.trans = nullptr;
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(32)
   c.lane = lane;
   c.amax = 0.f;
   const int T = c.T, L = tgt_len[b], S = 2 * L + 1;
-  const bool fwd = blockIdx.y == 0;
+  const bool fwd = (threadIdx.x >> 5) == 0;
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   CtcState<SPL> f;
@@ -316,8 +318,7 @@ template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                        float *grad_em, const int32_t *status, cudaStream_t s) {
-  ctc_chain_kernel<SPL><<<dim3(d.B, 2), 32, 0, s>>>(em, em_len, tgt, tgt_len, blank, d, w,
-                                                     status);
+  ctc_chain_kernel<SPL><<<d.B, 64, 0, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   ctc_grad_kernel<SPL><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
