@@ -156,8 +156,9 @@ __device__ __forceinline__ void fcc_beta_step(FccState &f, const float *row, flo
 }
 
 __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                          float (*vec)[32], float *out, int *outk,
-                                          double *lnz) {
+                                          float (*vec)[32], RowStage<32, 1> &st, float *out,
+                                          int *outk, double *lnz) {
+  int gi = 0;
   const int lane = c.lane, N = c.N, T = c.T;
   FccState f;
   f.spare = N < 32;
@@ -175,12 +176,15 @@ __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChu
     if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-      for (int g = 0; g < kChunk; g += kUnroll) {
+      for (int g = 0; g < kChunk; g += kUnroll, ++gi) {
         const int tb = t0 + g;   // multiple of kUnroll: parities are static
+        const int slot = gi & 1;
+        stage_acquire(gi, lane);
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-          fcc_alpha_step(f, buf + (g + q) * kStride, vec, q & 1, out + (tb + q) * 32,
-                         outk + tb + q, lane, N);
+          fcc_alpha_step(f, buf + (g + q) * kStride, vec, q & 1, st.v[slot] + q * 32,
+                         st.e[slot] + q, lane, N);
+        stage_release(st, slot, out + tb * 32, outk + tb, lane);
       }
     } else {
       int r = 0;
@@ -197,12 +201,15 @@ __device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChu
       }
     }
   }
+  stage_drain(lane);
   const float z = warp_sum(lane < N ? f.v : 0.f);
   if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
 __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                         float (*vec)[32], float *out, int *outk, double *lnz) {
+                                         float (*vec)[32], RowStage<32, 1> &st, float *out,
+                                         int *outk, double *lnz) {
+  int gi = 0;
   const int lane = c.lane, N = c.N, T = c.T;
   FccState f;
   f.spare = N < 32;
@@ -224,12 +231,15 @@ __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChun
     if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll, ++gi) {
         const int ub = t0 + g;
+        const int slot = gi & 1;
+        stage_acquire(gi, lane);
 #pragma unroll
         for (int q = kUnroll - 1; q >= 0; --q)
-          fcc_beta_step(f, buf + (g + q) * kStride, vec, q & 1, out + (ub + q - 1) * 32,
-                        outk + ub + q - 1, lane, N);
+          fcc_beta_step(f, buf + (g + q) * kStride, vec, q & 1, st.v[slot] + q * 32,
+                        st.e[slot] + q, lane, N);
+        stage_release(st, slot, out + (ub - 1) * 32, outk + ub - 1, lane);
       }
     } else {
       for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
@@ -240,6 +250,7 @@ __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChun
     }
     if (ch == 0) e0 = buf[lane];
   }
+  stage_drain(lane);
   const float z = warp_sum(e0 * f.v);
   if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
@@ -322,8 +333,9 @@ __device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row
 
 template <int SPL>
 __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                          const int64_t *y, int L, float *out, int *oute,
-                                          double *lnz) {
+                                          RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
+                                          float *out, int *oute, double *lnz) {
+  int gi = 0;
   const int lane = c.lane, T = c.T;
   FacState<SPL> f;
   fac_weights<SPL>(c, y, L, true, f.tok, f.S, f.P);
@@ -337,13 +349,15 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
     if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-      for (int g = 0; g < kChunk; g += kUnroll) {
+      for (int g = 0; g < kChunk; g += kUnroll, ++gi) {
         const int tb = t0 + g;
-        float *ob = out + (size_t)tb * (SPL * 32);
-        int *oeb = oute + tb * 32;
+        const int slot = gi & 1;
+        stage_acquire(gi, lane);
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, ob, oeb, lane, q);
+          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, st.v[slot],
+                              st.e[slot], lane, q);
+        stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
       }
     } else {
       int r = 0;
@@ -362,6 +376,7 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
       }
     }
   }
+  stage_drain(lane);
   // fac score = alpha_{T-1}[L-1] (:203)
   const int lastl = L - 1;
   float vl = 0.f;
@@ -372,8 +387,9 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
 
 template <int SPL>
 __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                         const int64_t *y, int L, float *out, int *oute,
-                                         double *lnz) {
+                                         RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
+                                         float *out, int *oute, double *lnz) {
+  int gi = 0;
   const int lane = c.lane, T = c.T;
   FacState<SPL> f;
   fac_weights<SPL>(c, y, L, false, f.tok, f.S, f.P);
@@ -392,14 +408,15 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
     if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll, ++gi) {
         const int ub = t0 + g;   // frames ub .. ub+7 produce beta' at ub-1 .. ub+6
-        float *ob = out + (size_t)(ub - 1) * (SPL * 32);
-        int *oeb = oute + (ub - 1) * 32;
+        const int slot = gi & 1;
+        stage_acquire(gi, lane);
 #pragma unroll
         for (int q = kUnroll - 1; q >= 0; --q)
           fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
-                             ob, oeb, lane, q);
+                             st.v[slot], st.e[slot], lane, q);
+        stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32, lane);
       }
     } else {
       for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
@@ -410,22 +427,29 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
     }
     if (ch == 0) e0 = buf[f.tok[0]];
   }
+  stage_drain(lane);
   if (lane == 0) *lnz = log((double)(e0 * f.v[0])) + (double)f.ex * 0.6931471805599453;
 }
 
-// One CTA per utterance with one warp per recursion: warp w runs role w on
-// SM sub-partition w, so the four serial chains never share an issue port.
+// One warp per CTA, grid (B, 4 roles): the CTA scheduler spreads the
+// serial recursions over the SMs (measured faster than packing several
+// recursions per SM, which contend for the load/store path).
 template <int SPL>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32)
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk_all[4][2][kChunk * kStride];
-  __shared__ __align__(16) float vec_all[2][2][32];
-  const int b = blockIdx.x, role = threadIdx.x >> 5;
+  __shared__ __align__(16) float chunk[2][kChunk * kStride];
+  __shared__ __align__(16) float vec[2][32];
+  extern __shared__ __align__(128) unsigned char dsm[];  // row staging (dynamic)
+  union Stage {
+    RowStage<32, 1> fcc;
+    RowStage<SPL * 32, 32> fac;
+  };
+  Stage &st = *reinterpret_cast<Stage *>(dsm);
+  const int b = blockIdx.x, role = blockIdx.y;
   if (status[b] != W2L_OK) return;
-  float (*chunk)[kChunk * kStride] = chunk_all[role];
   ChainCtx c;
   c.trans = trans;
   c.e = em + (size_t)b * d.Tmax * d.N;
@@ -436,15 +460,15 @@ __global__ void __launch_bounds__(128)
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (role == 0) {
-    fcc_alpha(c, chunk, vec_all[0], w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
+    fcc_alpha(c, chunk, vec, st.fcc, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
   } else if (role == 1) {
-    fcc_beta(c, chunk, vec_all[1], w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
+    fcc_beta(c, chunk, vec, st.fcc, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
   } else if (role == 2) {
-    fac_alpha<SPL>(c, chunk, y, tgt_len[b], w.fac_a + row0 * (SPL * 32), w.fac_ea + row0 * 32,
-                   w.scal + b * 4 + 2);
+    fac_alpha<SPL>(c, chunk, st.fac, y, tgt_len[b], w.fac_a + row0 * (SPL * 32),
+                   w.fac_ea + row0 * 32, w.scal + b * 4 + 2);
   } else {
-    fac_beta<SPL>(c, chunk, y, tgt_len[b], w.fac_b + row0 * (SPL * 32), w.fac_eb + row0 * 32,
-                  w.scal + b * 4 + 3);
+    fac_beta<SPL>(c, chunk, st.fac, y, tgt_len[b], w.fac_b + row0 * (SPL * 32),
+                  w.fac_eb + row0 * 32, w.scal + b * 4 + 3);
   }
 }
 
@@ -744,7 +768,12 @@ template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                        float *grad_em, const int32_t *status, cudaStream_t s) {
-  asg_chain_kernel<SPL><<<d.B, 128, 0, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status);
+  const size_t stage_bytes = sizeof(RowStage<SPL * 32, 32>);
+  auto kc = asg_chain_kernel<SPL>;
+  cudaError_t err0 =
+      cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_bytes);
+  if (err0 != cudaSuccess) return err0;
+  kc<<<dim3(d.B, 4), 32, stage_bytes, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   constexpr int LP = SPL * 32;

@@ -145,4 +145,61 @@ __device__ __forceinline__ int lane_pair_exponent(const float (&a)[SPL], const f
   return ea + eb + exponent_of(m);
 }
 
+// ---- TMA bulk stores of staged chain rows (smem -> global, async proxy).
+// Chain warps write each block of kUnroll frame rows into a shared-memory
+// staging slot and one lane hands the contiguous block to the bulk-copy
+// engine, so the serial recursion never waits on the LSU store path.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_fence() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// double-buffered staging for kUnroll rows of kRowFloats values + kRowInts ints
+template <int kRowFloats, int kRowInts>
+struct RowStage {
+  float v[2][kUnroll * kRowFloats];
+  int e[2][kUnroll * kRowInts];
+};
+
+// before writing slot (gi & 1): its previous bulk copy must have read it
+__device__ __forceinline__ void stage_acquire(int gi, int lane) {
+  if (gi >= 2 && lane == 0) bulk_wait_read1();
+  __syncwarp();
+}
+
+// hand the finished slot to the bulk engine
+template <int kRowFloats, int kRowInts>
+__device__ __forceinline__ void stage_release(RowStage<kRowFloats, kRowInts> &st, int slot,
+                                              float *gv, int *ge, int lane) {
+  static_assert((kUnroll * kRowInts * sizeof(int)) % 16 == 0, "bulk copies move 16B multiples");
+  bulk_fence();
+  __syncwarp();
+  if (lane == 0) {
+    bulk_store(gv, st.v[slot], kUnroll * kRowFloats * sizeof(float));
+    bulk_store(ge, st.e[slot], kUnroll * kRowInts * sizeof(int));
+    bulk_commit();
+  }
+}
+
+__device__ __forceinline__ void stage_drain(int lane) {
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
 }  // namespace w2l

@@ -95,16 +95,18 @@ __device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row
   lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
 }
 
-// One CTA per utterance: warp 0 runs alpha, warp 1 beta (separate SMSPs).
+// One warp per CTA, grid (B, 2): blockIdx.y 0 = alpha, 1 = beta.
 template <int SPL>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32)
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk_all[2][2][kChunk * kStride];
-  const int b = blockIdx.x, lane = threadIdx.x & 31;
-  float (*chunk)[kChunk * kStride] = chunk_all[threadIdx.x >> 5];
+  __shared__ __align__(16) float chunk[2][kChunk * kStride];
+  extern __shared__ __align__(128) unsigned char dsm[];  // row staging (dynamic)
+  RowStage<SPL * 32, 32> &st = *reinterpret_cast<RowStage<SPL * 32, 32> *>(dsm);
+  const int b = blockIdx.x, lane = threadIdx.x;
   if (status[b] != W2L_OK) return;
+  int gi = 0;
   ChainCtx c;
   c.trans = nullptr;
   c.e = em + (size_t)b * d.Tmax * d.N;
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(64)
   c.lane = lane;
   c.amax = 0.f;
   const int T = c.T, L = tgt_len[b], S = 2 * L + 1;
-  const bool fwd = (threadIdx.x >> 5) == 0;
+  const bool fwd = blockIdx.y == 0;
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   CtcState<SPL> f;
@@ -134,13 +136,15 @@ __global__ void __launch_bounds__(64)
       if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
       if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-        for (int g = 0; g < kChunk; g += kUnroll) {
+        for (int g = 0; g < kChunk; g += kUnroll, ++gi) {
           const int tb = t0 + g;
-          float *ob = out + (size_t)tb * (SPL * 32);
-          int *oeb = oute + tb * 32;
+          const int slot = gi & 1;
+          stage_acquire(gi, lane);
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
-            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, ob, oeb, lane, q);
+            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, st.v[slot],
+                                st.e[slot], lane, q);
+          stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
         }
       } else {
         int r = 0;
@@ -162,6 +166,7 @@ __global__ void __launch_bounds__(64)
         }
       }
     }
+    stage_drain(lane);
     // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
     float part = 0.f;
 #pragma unroll
@@ -194,14 +199,16 @@ __global__ void __launch_bounds__(64)
       if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
       if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
-        for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+        for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll, ++gi) {
           const int ub = t0 + g;
-          float *ob = out + (size_t)(ub - 1) * (SPL * 32);
-          int *oeb = oute + (ub - 1) * 32;
+          const int slot = gi & 1;
+          stage_acquire(gi, lane);
 #pragma unroll
           for (int q = kUnroll - 1; q >= 0; --q)
             ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
-                               ob, oeb, lane, q);
+                               st.v[slot], st.e[slot], lane, q);
+          stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32,
+                        lane);
         }
       } else {
         for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
@@ -215,6 +222,7 @@ __global__ void __launch_bounds__(64)
         if (S > 1) z0 += buf[f.lab[1]] * f.v[1];
       }
     }
+    stage_drain(lane);
     if (lane == 0) w.scal[b * 4 + 1] = log((double)z0) + (double)f.ex * ln2;
   }
 }
@@ -318,7 +326,12 @@ template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                        float *grad_em, const int32_t *status, cudaStream_t s) {
-  ctc_chain_kernel<SPL><<<d.B, 64, 0, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status);
+  const size_t stage_bytes = sizeof(RowStage<SPL * 32, 32>);
+  auto kc = ctc_chain_kernel<SPL>;
+  cudaError_t err0 =
+      cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_bytes);
+  if (err0 != cudaSuccess) return err0;
+  kc<<<dim3(d.B, 2), 32, stage_bytes, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   ctc_grad_kernel<SPL><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
