@@ -460,9 +460,11 @@ __global__ void __launch_bounds__(32)
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (role == 0) {
-    fcc_alpha(c, chunk, vec, st.fcc, w.fcc_a + row0 * 32, w.fcc_ka + row0, w.scal + b * 4 + 0);
+    fcc_alpha(c, chunk, vec, st.fcc, w.fcc_a + row0 * 32, w.fcc_ka + (size_t)b * w.tpad,
+              w.scal + b * 4 + 0);
   } else if (role == 1) {
-    fcc_beta(c, chunk, vec, st.fcc, w.fcc_b + row0 * 32, w.fcc_kb + row0, w.scal + b * 4 + 1);
+    fcc_beta(c, chunk, vec, st.fcc, w.fcc_b + row0 * 32, w.fcc_kb + (size_t)b * w.tpad + 1,
+             w.scal + b * 4 + 1);
   } else if (role == 2) {
     fac_alpha<SPL>(c, chunk, st.fac, y, tgt_len[b], w.fac_a + row0 * (SPL * 32),
                    w.fac_ea + row0 * 32, w.scal + b * 4 + 2);
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     lane_load<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
     pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
-    pka = w.fcc_ka[row0 + ta - 1];
+    pka = w.fcc_ka[(size_t)b * w.tpad + ta - 1];
   }
 
   for (int t = ta; t < tend; ++t) {
@@ -578,8 +580,8 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     // ---- fcc node posteriors (:238)
     const float fa = w.fcc_a[(row0 + t) * 32 + lane];
     const float fb = w.fcc_b[(row0 + t) * 32 + lane];
-    const int ka = w.fcc_ka[row0 + t];
-    const int kb = w.fcc_kb[row0 + t];
+    const int ka = w.fcc_ka[(size_t)b * w.tpad + t];
+    const int kb = w.fcc_kb[(size_t)b * w.tpad + t + 1];
     const float gam = fa * fb;
     const float zf = warp_sum(gam);
     const float inv_zf = 1.f / zf;
@@ -809,8 +811,9 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   AsgFastWs t;
   t.fcc_a = (float *)take(BT * 32 * 4);
   t.fcc_b = (float *)take(BT * 32 * 4);
-  t.fcc_ka = (int *)take(BT * 4);
-  t.fcc_kb = (int *)take(BT * 4);
+  const int tpad = round_up(d.Tmax + 1, 8);
+  t.fcc_ka = (int *)take((size_t)d.B * tpad * 4);
+  t.fcc_kb = (int *)take((size_t)d.B * tpad * 4);
   t.fac_a = (float *)take(BT * lpad * 4);
   t.fac_b = (float *)take(BT * lpad * 4);
   t.fac_ea = (int *)take(BT * 32 * 4);
@@ -824,6 +827,7 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   t.spl = spl;
   t.lpad = lpad;
   t.nblk = nblk;
+  t.tpad = tpad;
   if (w) *w = t;
   return off;
 }

@@ -43,7 +43,7 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
 // ---- fp32 fast path
 struct AsgFastWs {
   float *fcc_a, *fcc_b;      // [B][Tmax][32]
-  int *fcc_ka, *fcc_kb;      // [B][Tmax] cumulative exponents
+  int *fcc_ka, *fcc_kb;      // [B][tpad] cumulative exponents (kb stored at t+1)
   float *fac_a, *fac_b;      // [B][Tmax][SPL*32] slot-major
   int *fac_ea, *fac_eb;      // [B][Tmax][32] per-lane exponents
   double *scal;              // [B][4]: lnZ fcc fwd, fcc bwd, fac fwd, fac bwd
@@ -52,7 +52,7 @@ struct AsgFastWs {
   float *part_guard;         // [B][nblk][4]
   int *perm;                 // [B][Lpad] states sorted by token
   int *tok_start;            // [B][33]
-  int spl, lpad, nblk;
+  int spl, lpad, nblk, tpad;  // tpad = round_up(Tmax + 1, 8): 16B-aligned bulk blocks
 };
 int asg_fast_spl(int Lmax);  // 0 if unsupported
 size_t asg_fast_ws_bytes(Dims d);
