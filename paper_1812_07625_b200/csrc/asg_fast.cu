@@ -291,7 +291,7 @@ struct FacState {
 
 // fac alpha step t (criterion.py:197-202) in block floating point
 template <int SPL>
-__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *row, bool renorm,
+__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *row, bool renorm, bool check,
                                                float *out, int *oute, int lane, int t) {
   float E[SPL];
 #pragma unroll
@@ -302,7 +302,7 @@ __device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *ro
     nb = 0.f;
     nbe = kNegExp;
   }
-  const float nbs = align_neighbour<SPL>(nb, nbe, f.v, f.ex);
+  const float nbs = align_neighbour<SPL>(nb, nbe, f.v, f.ex, check);
 #pragma unroll
   for (int k = SPL - 1; k >= 1; --k) f.v[k] = E[k] * fmaf(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
   f.v[0] = E[0] * fmaf(f.S[0], f.v[0], f.P[0] * nbs);
@@ -312,7 +312,7 @@ __device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *ro
 
 // fac beta' step consuming frame u (criterion.py:207-212)
 template <int SPL>
-__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row, bool renorm,
+__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row, bool renorm, bool check,
                                               float *out, int *oute, int lane, int t_out) {
   float wv[SPL];
 #pragma unroll
@@ -323,7 +323,7 @@ __device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row
     nb = 0.f;
     nbe = kNegExp;
   }
-  const float nbs = align_neighbour<SPL>(nb, nbe, wv, f.ex);
+  const float nbs = align_neighbour<SPL>(nb, nbe, wv, f.ex, check);
 #pragma unroll
   for (int k = 0; k < SPL - 1; ++k) f.v[k] = fmaf(f.S[k], wv[k], f.P[k] * wv[k + 1]);
   f.v[SPL - 1] = fmaf(f.S[SPL - 1], wv[SPL - 1], f.P[SPL - 1] * nbs);
@@ -355,7 +355,7 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
         stage_acquire(gi, lane);
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, st.v[slot],
+          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, (q % kRenorm) == 1, st.v[slot],
                               st.e[slot], lane, q);
         stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
       }
@@ -371,7 +371,7 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
       }
       for (; r < rows; ++r) {
         const int t = t0 + r;
-        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, out, oute,
+        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, true, out, oute,
                             lane, t);
       }
     }
@@ -414,14 +414,14 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
         stage_acquire(gi, lane);
 #pragma unroll
         for (int q = kUnroll - 1; q >= 0; --q)
-          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
+          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0, (q % kRenorm) == 0,
                              st.v[slot], st.e[slot], lane, q);
         stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32, lane);
       }
     } else {
       for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
         const int u = t0 + r;
-        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, out, oute,
+        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, true, out, oute,
                            lane, u - 1);
       }
     }

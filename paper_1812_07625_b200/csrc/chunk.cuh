@@ -82,15 +82,12 @@ __device__ __forceinline__ float tree_max(const float (&v)[SPL]) {
 template <int SPL>
 __device__ __forceinline__ void lane_renorm(float (&v)[SPL], int &ex) {
   const float mx = tree_max<SPL>(v);
-  if (mx > 0.f) {
-    const int kx = exponent_of(mx);
-    const float sc = pow2f(-kx);
+  // branch-free: an all-zero block keeps zeros and is marked dead
+  const int kx = exponent_of(mx);           // -127 for mx == 0
+  const float sc = pow2f_fast(-kx);
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) v[k] *= sc;
-    ex += kx;
-  } else {
-    ex = kNegExp;
-  }
+  for (int k = 0; k < SPL; ++k) v[k] *= sc;
+  ex = mx > 0.f ? ex + kx : kNegExp;
 }
 
 // one frame's chain row, lane-major ([lane][k]): SPL is even, so a lane's
@@ -117,19 +114,28 @@ __device__ __forceinline__ void lane_load(float (&v)[SPL], const float *row, int
   }
 }
 
-// align the neighbour lane's value to this lane's exponent; if the
-// neighbour dominates by more than 2^64, rebase this lane onto it first
+// align the neighbour lane's value to this lane's exponent.  kCheck: the
+// full version -- if the neighbour dominates by more than 2^64, rebase this
+// lane onto it first (a branch).  Lane exponents only move at
+// renormalisation steps, so the unrolled blocks run the full version on the
+// step after each renormalisation and the branch-free one elsewhere (a dead
+// lane adopts the neighbour's exponent; the shift is clamped to 2^126).
 template <int SPL>
-__device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[SPL], int &ex) {
-  int dd = nbe - ex;
-  if (dd > 64) {
-    const float sc = pow2f(-dd);
+__device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[SPL], int &ex,
+                                                 bool check) {
+  if (check) {
+    int dd = nbe - ex;
+    if (dd > 64) {
+      const float sc = pow2f(-dd);
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) v[k] *= sc;
-    ex = nbe;
-    dd = 0;
+      for (int k = 0; k < SPL; ++k) v[k] *= sc;
+      ex = nbe;
+      dd = 0;
+    }
+    return nb * pow2f(dd);
   }
-  return nb * pow2f(dd);
+  ex = ex == kNegExp ? nbe : ex;
+  return nb * pow2f_fast(min(nbe - ex, 126));
 }
 
 // floor(log2(max_k a[k] b[k])) + ea + eb, a bound on this lane's largest

@@ -37,6 +37,12 @@ __device__ __forceinline__ float pow2f(int k) {
   return 0.0f;
 }
 
+// 2^k without branches for k <= 127; k <= -127 gives 0 (no subnormals).
+__device__ __forceinline__ float pow2f_fast(int k) {
+  k = max(min(k, 127), -127);
+  return __int_as_float((k + 127) << 23);
+}
+
 // floor(log2(x)) for a positive normal float; subnormals map to -127.
 __device__ __forceinline__ int exponent_of(float x) {
   return ((__float_as_int(x) >> 23) & 0xff) - 127;

@@ -47,7 +47,7 @@ struct CtcState {
 
 // alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])  (:126-134)
 template <int SPL>
-__device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *row, bool renorm,
+__device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *row, bool renorm, bool check,
                                                float *out, int *oute, int lane, int t) {
   float E[SPL];
 #pragma unroll
@@ -59,8 +59,8 @@ __device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *ro
     nb1 = nb2 = 0.f;
     nbe = kNegExp;
   }
-  const float n1 = align_neighbour<SPL>(nb1, nbe, f.v, f.ex);
-  const float n2 = nb2 * pow2f(nbe - f.ex);
+  const float n1 = align_neighbour<SPL>(nb1, nbe, f.v, f.ex, check);
+  const float n2 = nb2 * (check ? pow2f(nbe - f.ex) : pow2f_fast(min(nbe - f.ex, 126)));
 #pragma unroll
   for (int k = SPL - 1; k >= 2; --k)
     f.v[k] = E[k] * fmaf(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1]);
@@ -73,7 +73,7 @@ __device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *ro
 
 // beta'_{u-1}[s] = w[s] + w[s+1] + skip_{s+2} w[s+2],  w = Et_u[lab] beta'_u  (:147-155)
 template <int SPL>
-__device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row, bool renorm,
+__device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row, bool renorm, bool check,
                                               float *out, int *oute, int lane, int t_out) {
   float wv[SPL];
 #pragma unroll
@@ -85,8 +85,8 @@ __device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row
     nb1 = nb2 = 0.f;
     nbe = kNegExp;
   }
-  const float n1 = align_neighbour<SPL>(nb1, nbe, wv, f.ex);
-  const float n2 = nb2 * pow2f(nbe - f.ex);
+  const float n1 = align_neighbour<SPL>(nb1, nbe, wv, f.ex, check);
+  const float n2 = nb2 * (check ? pow2f(nbe - f.ex) : pow2f_fast(min(nbe - f.ex, 126)));
 #pragma unroll
   for (int k = 0; k < SPL - 2; ++k) f.v[k] = fmaf(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
   f.v[SPL - 2] = fmaf(f.sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(32)
           stage_acquire(gi, lane);
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
-            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, st.v[slot],
+            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, (q % kRenorm) == 1, st.v[slot],
                                 st.e[slot], lane, q);
           stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
         }
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(32)
         }
         for (; r < rows; ++r) {
           const int t = t0 + r;
-          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, out, oute,
+          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, true, out, oute,
                               lane, t);
         }
       }
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(32)
           stage_acquire(gi, lane);
 #pragma unroll
           for (int q = kUnroll - 1; q >= 0; --q)
-            ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0,
+            ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0, (q % kRenorm) == 0,
                                st.v[slot], st.e[slot], lane, q);
           stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32,
                         lane);
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(32)
       } else {
         for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
           const int u = t0 + r;
-          ctc_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, out,
+          ctc_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, true, out,
                              oute, lane, u - 1);
         }
       }
