@@ -536,7 +536,11 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       P[k] = 0.f;
     }
   }
-  const int *perm = w.perm + (size_t)b * w.lpad;
+  // token CSR of this utterance, staged once per block (the gather reads it
+  // every frame)
+  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 4);
+  for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
+  __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
 
@@ -557,7 +561,26 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float *mye = erow + warp * 64;
   float *myv = vrow + warp * 32;
   const size_t row0 = (size_t)b * d.Tmax;
+  const int *ka_row = w.fcc_ka + (size_t)b * w.tpad;
+  const int *kb_row = w.fcc_kb + (size_t)b * w.tpad + 1;
   const int tend = min(tb, T);
+
+  // one frame's inputs; the next frame's are loaded while this one is used
+  struct Frame {
+    float e, fa, fb, va[SPL], vb[SPL];
+    int ka, kb, ea, eb;
+  };
+  auto load = [&](Frame &f, int t) {
+    f.e = lane < N ? em[(row0 + t) * N + lane] : -CUDART_INF_F;
+    f.fa = w.fcc_a[(row0 + t) * 32 + lane];
+    f.fb = w.fcc_b[(row0 + t) * 32 + lane];
+    f.ka = ka_row[t];
+    f.kb = kb_row[t];
+    lane_load<SPL>(f.va, w.fac_a + (row0 + t) * LP, lane);
+    lane_load<SPL>(f.vb, w.fac_b + (row0 + t) * LP, lane);
+    f.ea = w.fac_ea[(row0 + t) * 32 + lane];
+    f.eb = w.fac_eb[(row0 + t) * 32 + lane];
+  };
 
   // fac alpha at t-1 (values and lane exponent) carried across frames
   float pa[SPL];
@@ -568,24 +591,23 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     lane_load<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
     pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
-    pka = w.fcc_ka[(size_t)b * w.tpad + ta - 1];
+    pka = ka_row[ta - 1];
   }
+  Frame cur, nxt;
+  if (ta < tend) load(cur, ta);
 
   for (int t = ta; t < tend; ++t) {
+    if (t + 1 < tend) load(nxt, t + 1);
     // ---- emissions of frame t, shifted and exponentiated (same as the chain)
-    const float et = shifted_prob(em + (row0 + t) * N, N, lane, nullptr);
+    const float m = warp_max(cur.e);
+    const float et = lane < N ? expf(cur.e - m) : 0.f;
     mye[lane] = et;
-    if (lane == 0) mye[32] = 0.f;  // token id N == zero column only if N == 32
-    mye[N] = 0.f;
+    if (lane == 0) mye[32] = 0.f;
     // ---- fcc node posteriors (:238)
-    const float fa = w.fcc_a[(row0 + t) * 32 + lane];
-    const float fb = w.fcc_b[(row0 + t) * 32 + lane];
-    const int ka = w.fcc_ka[(size_t)b * w.tpad + t];
-    const int kb = w.fcc_kb[(size_t)b * w.tpad + t + 1];
-    const float gam = fa * fb;
+    const float gam = cur.fa * cur.fb;
     const float zf = warp_sum(gam);
     const float inv_zf = 1.f / zf;
-    const float gF = (float)((double)__log2f(zf) + (double)(ka + kb) - refF);
+    const float gF = (float)((double)__log2f(zf) + (double)(cur.ka + cur.kb) - refF);
     gminF = fminf(gminF, gF);
     gmaxF = fmaxf(gmaxF, gF);
     const float full_e = gam * inv_zf;
@@ -593,7 +615,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     if (t >= 1) {
       myv[lane] = pfa;
       __syncwarp();
-      const float u = et * fb * pow2f(pka - ka) * inv_zf;
+      const float u = et * cur.fb * pow2f(pka - cur.ka) * inv_zf;
       const float4 *pv = reinterpret_cast<const float4 *>(myv);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -604,21 +626,15 @@ __global__ void __launch_bounds__(kGradWarps * 32)
         accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
       }
     }
-    // ---- fac node posteriors (:214-217)
-    float va[SPL], vb[SPL];
-    lane_load<SPL>(va, w.fac_a + (row0 + t) * LP, lane);
-    lane_load<SPL>(vb, w.fac_b + (row0 + t) * LP, lane);
-    const int ea = w.fac_ea[(row0 + t) * 32 + lane];
-    const int eb = w.fac_eb[(row0 + t) * 32 + lane];
-    // frame reference exponent from the actual magnitudes (the chains
-    // renormalise lazily, so a lane exponent alone can overstate its block)
-    const int es = lane_pair_exponent<SPL>(va, vb, ea, eb);
+    // ---- fac node posteriors (:214-217); the frame reference exponent comes
+    // from the actual magnitudes (the chains renormalise lazily)
+    const int es = lane_pair_exponent<SPL>(cur.va, cur.vb, cur.ea, cur.eb);
     const int estar = warp_max(es);
-    const float sc = es > kNegExp / 2 ? pow2f(ea + eb - estar) : 0.f;
+    const float sc = es > kNegExp / 2 ? pow2f(cur.ea + cur.eb - estar) : 0.f;
     float zl = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      const float p = va[k] * vb[k] * sc;
+      const float p = cur.va[k] * cur.vb[k] * sc;
       myp[lane * SPL + k] = p;
       zl += p;
     }
@@ -629,31 +645,40 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     gmaxC = fmaxf(gmaxC, gC);
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
-    float con = 0.f;
-    for (int q = ts0; q < ts1; ++q) con += myp[perm[q]];
-    if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
-    // ---- fac edge posteriors (:218-224); the power of two is applied with
-    // ldexpf to the finished mantissa product so no intermediate can overflow
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+    int q = ts0;
+    for (; q + 4 <= ts1; q += 4) {
+      c0 += myp[sperm[q]];
+      c1 += myp[sperm[q + 1]];
+      c2 += myp[sperm[q + 2]];
+      c3 += myp[sperm[q + 3]];
+    }
+    for (; q < ts1; ++q) c0 += myp[sperm[q]];
+    const float con = (c0 + c1) + (c2 + c3);
+    if (lane < N) ge[(row0 + t) * N + lane] = full_e - con * inv_zc;
+    // ---- fac edge posteriors (:218-224).  The lane scale 2^d is bounded by
+    // 2^127 and the mantissa products are tiny whenever d is large (a
+    // posterior is <= 1), so x * 2^d * (1/Z) cannot overflow.
     if (t >= 1) {
       const float nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
       const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
-      const int d_own = max(pea + eb - estar, -1000);
-      const int d_nb = lane > 0 ? max(nbe + eb - estar, -1000) : -1000;
+      const float s_own = pow2f_fast(pea + cur.eb - estar);
+      const float s_nb = lane > 0 ? pow2f_fast(nbe + cur.eb - estar) : 0.f;
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
-        const float ev = mye[tok[k]] * vb[k];
-        accS[k] = fmaf(ldexpf(pa[k] * S[k] * ev, d_own), inv_zc, accS[k]);
-        const float prev = k > 0 ? ldexpf(pa[k - 1] * P[k] * ev, d_own)
-                                 : ldexpf(nbv * P[k] * ev, d_nb);
+        const float ev = mye[tok[k]] * cur.vb[k];   // mantissas first, then the scale
+        accS[k] = fmaf(((pa[k] * S[k]) * ev) * s_own, inv_zc, accS[k]);
+        const float prev = k > 0 ? ((pa[k - 1] * P[k]) * ev) * s_own : ((nbv * P[k]) * ev) * s_nb;
         accP[k] = fmaf(prev, inv_zc, accP[k]);
       }
     }
     // carry alpha_t as alpha_{t-1} for the next frame
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) pa[k] = va[k];
-    pea = ea;
-    pfa = fa;
-    pka = ka;
+    for (int k = 0; k < SPL; ++k) pa[k] = cur.va[k];
+    pea = cur.ea;
+    pfa = cur.fa;
+    pka = cur.ka;
+    cur = nxt;
     __syncwarp();
   }
 
@@ -779,7 +804,7 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   constexpr int LP = SPL * 32;
-  const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4));
+  const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4) + LP);
   auto k = asg_grad_kernel<SPL>;
   err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
