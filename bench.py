@@ -1,0 +1,482 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 sequence-criterion hot path (BASELINE.json metric:
+"ASG/CTC loss+grad frames/sec (B x T) at 1/2/4/8 B200; % of HBM/SFU roofline").
+
+One step = batched ASG loss+grad (fcc - fac, grads w.r.t. emissions and
+transitions, transition-gradient all-reduce across ranks) AND batched CTC
+loss+grad on the same log-softmaxed emissions, for a
+per-GPU shard of B=64 utterances, T=1600 frames, N=30 tokens, L=300 labels
+(the C3 shape; at 8 GPUs the global batch is C5's B=512 -> weak scaling).
+ASG and CTC run concurrently on two streams.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: launched by torchrun, one process per GPU; timing is the max over
+ranks.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ASG/CTC loss+grad frames/sec (B×T) at 1/2/4/8 B200; % of HBM/SFU roofline"
+B_PER_GPU, T_FR, N_TOK, L_LAB = 64, 1600, 30, 300
+SEED = 20260004  # 20260000 + config index (C5)
+
+
+# ---------------------------------------------------------------- inputs --
+
+def make_inputs(rank: int, b=B_PER_GPU, t=T_FR, n=N_TOK, l=L_LAB):
+    """Seeded synthetic shard for `rank`: emissions log_softmax(2 N(0,1))
+    (f64 -> f32; valid CTC input, used for ASG too), ASG targets without
+    consecutive duplicates, CTC targets over the N-1 non-blank ids,
+    N(0,1) transitions (identical on every rank)."""
+    rng = np.random.default_rng(SEED + 1000 * rank)
+    x = 2.0 * rng.standard_normal((b, t, n))
+    x -= x.max(axis=2, keepdims=True)
+    em = (x - np.log(np.exp(x).sum(axis=2, keepdims=True))).astype(np.float32)
+    asg_t = np.empty((b, l), np.int64)
+    for i in range(b):
+        row = rng.integers(0, n - 1, size=l)
+        for k in range(1, l):                       # no consecutive duplicates
+            if row[k] == row[k - 1]:
+                row[k] = (row[k] + 1) % n
+        asg_t[i] = row
+    ctc_t = rng.integers(0, n - 1, size=(b, l)).astype(np.int64)
+    trans = np.random.default_rng(SEED).standard_normal((n, n)).astype(np.float32)
+    em_len = np.full(b, t, np.int32)
+    tgt_len = np.full(b, l, np.int32)
+    return em, em_len, asg_t, ctc_t, tgt_len, trans, n - 1
+
+
+# ----------------------------------------------------------- CPU baseline --
+
+def _cpu_worker(args):
+    from oracle import criterion_oracle as orc
+    e, ya, yc, a, blank = args
+    orc.asg(e, ya, a)
+    orc.ctc(e, yc, blank)
+    return e.shape[0]
+
+
+def _pool(cores):
+    import concurrent.futures as cf
+    import multiprocessing as mpc
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    return cf.ProcessPoolExecutor(max_workers=cores, mp_context=mpc.get_context("fork"))
+
+
+def cpu_sample(pool, em, asg_t, ctc_t, trans, blank, n_utts):
+    """Oracle port (the reference algorithm, float64 numpy) over n_utts
+    utterances, one per task; returns frames/s (wall clock)."""
+    tasks = [(em[i % len(em)], asg_t[i % len(em)], ctc_t[i % len(em)], trans, blank)
+             for i in range(n_utts)]
+    t0 = time.perf_counter()
+    frames = sum(pool.map(_cpu_worker, tasks))
+    return frames / (time.perf_counter() - t0)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during timing."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- roofline --
+
+def algorithmic_work(n=N_TOK, l=L_LAB, ctc_targets=None):
+    """Per-frame algorithmic work of the reference algorithm:
+    log-semiring transcendental ops (the SFU bound of the log-space
+    recursions) and HBM bytes (emissions in, gradient out)."""
+    s = 2 * l + 1
+    if ctc_targets is not None:
+        k = float(np.mean(np.sum(ctc_targets[:, 1:] != ctc_targets[:, :-1], axis=1)))
+    else:
+        k = (l - 1) * (n - 2) / (n - 1)
+    asg_chain = 2 * (n * n + n) + 4 * (l - 1)          # fcc alpha/beta + fac alpha/beta
+    asg_grad = (n * n + n) + (l + 2 * l - 1)           # full node+edge, con node+edges
+    ctc_chain = 4 * (s - 1 + k)                        # alpha/beta, 2 per logadd edge
+    ctc_grad = s + n + 1                               # posteriors + row check
+    return {"asg_chain": asg_chain, "asg_grad": asg_grad, "ctc_chain": ctc_chain,
+            "ctc_grad": ctc_grad, "bytes_asg": 8 * n, "bytes_ctc": 8 * n}
+
+
+# ------------------------------------------------------------------- main --
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip per-criterion sub-benchmarks")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    # CPU baseline pool forked before CUDA initialises (rank 0, single GPU)
+    pool = None
+    if world == 1 and not args.no_cpu_baseline:
+        pool = _pool(cpu_cores())
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1812_07625_b200 import _native, criterion as C
+    from paper_1812_07625_b200.distributed import allreduce_grad_transitions
+
+    em, em_len, asg_t, ctc_t, tgt_len, trans, blank = make_inputs(rank)
+    B, T, N = em.shape
+    em_d = torch.from_numpy(em).to(dev)
+    el_d = torch.from_numpy(em_len).to(dev)
+    ta_d = torch.from_numpy(asg_t).to(dev)
+    tc_d = torch.from_numpy(ctc_t).to(dev)
+    tl_d = torch.from_numpy(tgt_len).to(dev)
+    A_d = torch.from_numpy(trans).to(dev)
+    lib = _native.lib()
+    ws_a = torch.empty(lib.w2l_asg_workspace_bytes(B, T, N, L_LAB), dtype=torch.uint8, device=dev)
+    ws_c = torch.empty(lib.w2l_ctc_workspace_bytes(B, T, N, L_LAB), dtype=torch.uint8, device=dev)
+    out_a = C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=True, workspace=ws_a)
+    out_c = C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=True, workspace=ws_c)
+    # the fp32 path must not have needed the float64 fallback on this data
+    chk_a = C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a,
+                                    fallback=False)
+    chk_c = C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False, workspace=ws_c,
+                                    fallback=False)
+    fallbacks = int((chk_a.status != 0).sum().item() + (chk_c.status != 0).sum().item())
+
+    side = torch.cuda.Stream(device=dev)
+    main_s = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        side.wait_stream(main_s)
+        with torch.cuda.stream(side):
+            C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False, workspace=ws_c,
+                                    out=out_c)
+        C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a,
+                                out=out_a)
+        allreduce_grad_transitions(out_a.grad_transitions)
+        main_s.wait_stream(side)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()                      # evict L2 between timed steps
+            starts[i].record(main_s)
+            step()
+            ends[i].record(main_s)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(total_ms.item())
+    frames_step = world * B * T
+    value = frames_step * args.steps / (total_ms / 1e3)
+
+    # ---- end to end through the public API: pinned host inputs -> device ->
+    # both criteria -> losses back to the host, every step
+    em_h = torch.from_numpy(em).pin_memory()
+    ta_h = torch.from_numpy(asg_t).pin_memory()
+    tc_h = torch.from_numpy(ctc_t).pin_memory()
+    el_h = torch.from_numpy(em_len).pin_memory()
+    tl_h = torch.from_numpy(tgt_len).pin_memory()
+    loss_a_h = torch.empty(B, dtype=torch.float64).pin_memory()
+    loss_c_h = torch.empty(B, dtype=torch.float64).pin_memory()
+    em_in = torch.empty_like(em_d)
+    ta_in, tc_in = torch.empty_like(ta_d), torch.empty_like(tc_d)
+    el_in, tl_in = torch.empty_like(el_d), torch.empty_like(tl_d)
+
+    def e2e_step():
+        em_in.copy_(em_h, non_blocking=True)
+        ta_in.copy_(ta_h, non_blocking=True)
+        tc_in.copy_(tc_h, non_blocking=True)
+        el_in.copy_(el_h, non_blocking=True)
+        tl_in.copy_(tl_h, non_blocking=True)
+        side.wait_stream(main_s)
+        with torch.cuda.stream(side):
+            oc = C.ctc_loss_grad_batched(em_in, el_in, tc_in, tl_in, blank, check=False,
+                                         workspace=ws_c, out=out_c)
+        oa = C.asg_loss_grad_batched(em_in, el_in, ta_in, tl_in, A_d, check=False,
+                                     workspace=ws_a, out=out_a)
+        allreduce_grad_transitions(oa.grad_transitions)
+        main_s.wait_stream(side)
+        loss_a_h.copy_(oa.loss, non_blocking=True)
+        loss_c_h.copy_(oc.loss, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        e_s.record(main_s)
+        e2e_step()
+        e_e.record(main_s)
+        e_e.synchronize()
+        e2e_ms += e_s.elapsed_time(e_e)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = frames_step * args.steps / (float(e2e_t.item()) / 1e3)
+    h2d = em.nbytes + asg_t.nbytes + ctc_t.nbytes + em_len.nbytes + tgt_len.nbytes
+    d2h = 2 * B * 8
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- per-stage device times (traced calls) and the roofline of the
+    # dominant kernel; sub-benchmarks per criterion and Viterbi
+    torch.cuda.synchronize(dev)
+    ta_run = C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a,
+                                     trace=True)
+    tc_run = C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False,
+                                     workspace=ws_c, trace=True)
+    peaks = _native.probe_peaks()
+    work = algorithmic_work(ctc_targets=ctc_t)
+    frames = B * T
+    stages = {("asg", k): v for k, v in ta_run.stage_ms.items()}
+    stages.update({("ctc", k): v for k, v in tc_run.stage_ms.items()})
+    (crit, stage), dom_ms = max(stages.items(), key=lambda kv: kv[1])
+    ops_key = f"{crit}_{stage}" if f"{crit}_{stage}" in work else None
+    sfu_ops = work[ops_key] * frames if ops_key else None
+    roof = {
+        "kernel": f"{crit}_{stage}",
+        "bound": "sfu",
+        "achieved": (sfu_ops / (dom_ms / 1e3) / 1e9) if sfu_ops else None,
+        "peak": peaks["mufu_ex2_per_s"] / 1e9,
+        "unit": "Gop/s (log-semiring transcendental ops, SURVEY §8d)",
+        "frac": (sfu_ops / (dom_ms / 1e3) / peaks["mufu_ex2_per_s"]) if sfu_ops else None,
+        "traffic": None,
+        "kernel_ms": dom_ms,
+        "peak_source": "w2l_probe_peaks: MUFU ex2 throughput measured on this GPU",
+    }
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak, hbm_src = float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    step_s = total_ms / args.steps / 1e3
+    step_bytes = (work["bytes_asg"] + work["bytes_ctc"]) * frames
+    step_ops = (work["asg_chain"] + work["asg_grad"] + work["ctc_chain"] + work["ctc_grad"]) * frames
+    roof["step"] = {
+        "sfu_ops_per_step": step_ops,
+        "sfu_achieved_gops": step_ops / step_s / 1e9,
+        "sfu_frac": step_ops / step_s / peaks["mufu_ex2_per_s"],
+        "hbm_bytes_per_step": step_bytes,
+        "hbm_achieved_gbs": step_bytes / step_s / 1e9,
+        "hbm_peak_gbs": hbm_peak,
+        "hbm_peak_source": hbm_src,
+        "hbm_frac": step_bytes / step_s / 1e9 / hbm_peak,
+    }
+
+    sub = {"asg_stage_ms": ta_run.stage_ms, "ctc_stage_ms": tc_run.stage_ms,
+           "peaks": peaks, "fp32_guard_fallbacks": fallbacks}
+    if not args.no_sub:
+        def timeit(fn, reps=5):
+            fn()
+            torch.cuda.synchronize(dev)
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot = 0.0
+            for _ in range(reps):
+                flush.zero_()
+                s_.record()
+                fn()
+                e_.record()
+                e_.synchronize()
+                tot += s_.elapsed_time(e_)
+            return tot / reps
+        ms_a = timeit(lambda: C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False,
+                                                      workspace=ws_a, out=out_a))
+        ms_c = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
+                                                      check=False, workspace=ws_c, out=out_c))
+        ms_v = timeit(lambda: C.viterbi_batched(em_d, el_d, A_d, check=False))
+        sub.update({"asg_only_frames_per_s": frames / (ms_a / 1e3), "asg_only_ms": ms_a,
+                    "ctc_only_frames_per_s": frames / (ms_c / 1e3), "ctc_only_ms": ms_c,
+                    "viterbi_frames_per_s": frames / (ms_v / 1e3), "viterbi_ms": ms_v})
+
+    cpu = None
+    if pool is not None:
+        cores = cpu_cores()
+        n_utts = max(16, min(cores, 64))
+        with pool:
+            list(pool.map(_cpu_worker, [(em[0][:8], asg_t[0][:4], ctc_t[0][:4], trans, blank)] * cores))
+            fps = cpu_sample(pool, em, asg_t, ctc_t, trans, blank, n_utts)
+        cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
+               "cpu": cpu_model(),
+               "sample": f"{n_utts} utterances (T={T}, N={N}, L={L_LAB}) ASG+CTC loss+grad, "
+                         f"oracle port (float64 numpy), one utterance per task, process pool "
+                         f"of {cores}"}
+
+    launches_per_step = 7 + 6  # ASG: em_check, prep, chain, grad, final, exact, reduce; CTC: 6
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic seeded: log_softmax(2*N(0,1)) emissions, N(0,1) transitions, "
+                "uniform targets",
+        "config": {"workload": f"ASG+CTC loss+grad, B={B}/GPU T={T} N={N} L={L_LAB} "
+                               "(C3 shape per GPU; C5 B=512 at 8 GPUs)",
+                   "global_batch": world * B, "frames_per_step": frames_step,
+                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between steps"},
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "sub": sub,
+        "library": lib.w2l_version().decode(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank):
+    """The reference algorithm (oracle port, float64 numpy, one utterance per
+    task on all host cores) on this arm's config and metric; rank 0 only."""
+    if rank != 0:
+        return
+    em, em_len, asg_t, ctc_t, tgt_len, trans, blank = make_inputs(0)
+    cores = cpu_cores()
+    n_utts = max(16, min(cores, 64))
+    total = 0.0
+    with _pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_sample(pool, em, asg_t, ctc_t, trans, blank, cores)
+        frames = 0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            tasks = [(em[i % len(em)], asg_t[i % len(em)], ctc_t[i % len(em)], trans, blank)
+                     for i in range(n_utts)]
+            frames += sum(pool.map(_cpu_worker, tasks))
+        total = time.perf_counter() - t0
+    value = frames / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic seeded (same generator as the GPU arm)",
+        "config": {"workload": f"ASG+CTC loss+grad, T={T_FR} N={N_TOK} L={L_LAB}; each step a "
+                               f"{n_utts}-utterance sample of the B={B_PER_GPU} shard",
+                   "global_batch": n_utts, "parallelism": f"process pool x{cores}"},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+                         "cpu": cpu_model(),
+                         "sample": f"{n_utts} utterances per step, one per task"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

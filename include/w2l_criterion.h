@@ -116,6 +116,25 @@ W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const doubl
                     int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
                     size_t ws_bytes, w2l_stream_t stream);
 
+/* ------------------------------------------------------------- tracing --
+ * Same computation as w2l_asg_loss_grad / w2l_ctc_loss_grad, with a CUDA
+ * event after every stage; synchronises `stream` and writes the per-stage
+ * device times (ms) to stage_ms[*n_stages] (names: w2l_stage_name; kind 0 =
+ * ASG: validate, chain, grad, final, exact_fallback, reduce; kind 1 = CTC:
+ * validate, chain, grad, final, exact_fallback).  stage_ms needs 16 slots. */
+W2L_API int w2l_asg_loss_grad_traced(const float *em, const int32_t *em_len, const int64_t *tgt,
+                                     const int32_t *tgt_len, const float *trans, int B, int Tmax,
+                                     int N, int Lmax, double *loss, float *grad_em,
+                                     float *grad_trans, float *grad_trans_utt, int32_t *status,
+                                     void *ws, size_t ws_bytes, unsigned flags,
+                                     w2l_stream_t stream, float *stage_ms, int *n_stages);
+W2L_API int w2l_ctc_loss_grad_traced(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                                     const int32_t *tgt_len, int blank, int B, int Tmax, int N,
+                                     int Lmax, double *loss, float *grad_em, int32_t *status,
+                                     void *ws, size_t ws_bytes, unsigned flags,
+                                     w2l_stream_t stream, float *stage_ms, int *n_stages);
+W2L_API const char *w2l_stage_name(int kind, int i);
+
 /* ------------------------------------------------------------ utilities -- */
 /* Synchronises `stream`, copies status[B] to the host and returns the first
  * non-zero code (W2L_OK if none); *bad_index receives its utterance or -1. */

@@ -40,6 +40,11 @@ SIGNATURES = {
     "w2l_viterbi_workspace_bytes": (c_sz, [c_i, c_i, c_i]),
     "w2l_viterbi": (c_i, [c_p, c_p, c_p, c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "w2l_viterbi_f64": (c_i, [c_p, c_p, c_p, c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_sz, c_p]),
+    "w2l_asg_loss_grad_traced": (c_i, [c_p, c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_p, c_p,
+                                       c_p, c_p, c_p, c_p, c_sz, ctypes.c_uint, c_p, c_p, c_p]),
+    "w2l_ctc_loss_grad_traced": (c_i, [c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_i, c_p, c_p,
+                                       c_p, c_p, c_sz, ctypes.c_uint, c_p, c_p, c_p]),
+    "w2l_stage_name": (ctypes.c_char_p, [c_i, c_i]),
     "w2l_status_first_error": (c_i, [c_p, c_i, c_i32_p, c_p]),
     "w2l_status_string": (ctypes.c_char_p, [c_i]),
     "w2l_version": (ctypes.c_char_p, []),

@@ -60,6 +60,7 @@ class BatchLossOutput:
     grad_transitions: Optional[torch.Tensor] = None        # f32 [N, N], sum over B
     grad_transitions_per_utt: Optional[torch.Tensor] = None  # f32 [B, N, N]
     status: Optional[torch.Tensor] = None    # int32 [B]
+    stage_ms: Optional[dict] = None          # per-stage device times (trace=True)
 
 
 # ------------------------------------------------------------------ plumbing --
@@ -98,6 +99,11 @@ def _check_call(rc: int, what: str) -> None:
         if rc == nat.ERR_CUDA:
             detail += f" ({nat.lib().w2l_last_cuda_error().decode()})"
         raise_for_status(rc, f"{what}: {detail}")
+
+
+def _stage_times(kind: int, ms, n) -> dict:
+    lib = nat.lib()
+    return {lib.w2l_stage_name(kind, i).decode(): float(ms[i]) for i in range(n.value)}
 
 
 def _first_error(status: torch.Tensor):
@@ -359,7 +365,7 @@ def _raise_batch(status: torch.Tensor, what: str) -> None:
 def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, check=True,
                           per_utterance_grad_transitions=False, workspace=None,
                           out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True) -> BatchLossOutput:
+                          fallback: bool = True, trace: bool = False) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -389,10 +395,16 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
             grad_transitions_per_utt=(torch.empty((b, n, n), dtype=torch.float32, device=dev)
                                       if per_utterance_grad_transitions else None),
             status=torch.empty(b, dtype=torch.int32, device=dev))
-    rc = lib.w2l_asg_loss_grad(_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax,
-                               _p(out.loss), _p(out.grad_emissions), _p(out.grad_transitions),
-                               _p(out.grad_transitions_per_utt), _p(out.status), _p(ws),
-                               ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
+    args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
+            _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
+            _p(out.status), _p(ws), ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK,
+            _stream())
+    if trace:
+        ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
+        rc = lib.w2l_asg_loss_grad_traced(*args, ms, ctypes.byref(cnt))
+        out.stage_ms = _stage_times(0, ms, cnt)
+    else:
+        rc = lib.w2l_asg_loss_grad(*args)
     _check_call(rc, "w2l_asg_loss_grad")
     if check:
         _raise_batch(out.status, "asg_loss_grad_batched")
@@ -401,7 +413,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
 
 def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *, check=True,
                           workspace=None, out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True) -> BatchLossOutput:
+                          fallback: bool = True, trace: bool = False) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
     log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2."""
     dev = _device()
@@ -417,9 +429,15 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             loss=torch.empty(b, dtype=torch.float64, device=dev),
             grad_emissions=torch.empty((b, t_max, n), dtype=torch.float32, device=dev),
             status=torch.empty(b, dtype=torch.int32, device=dev))
-    rc = lib.w2l_ctc_loss_grad(_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax,
-                               _p(out.loss), _p(out.grad_emissions), _p(out.status), _p(ws),
-                               ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
+    args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
+            _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
+            0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
+    if trace:
+        ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
+        rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))
+        out.stage_ms = _stage_times(1, ms, cnt)
+    else:
+        rc = lib.w2l_ctc_loss_grad(*args)
     _check_call(rc, "w2l_ctc_loss_grad")
     if check:
         _raise_batch(out.status, "ctc_loss_grad_batched")

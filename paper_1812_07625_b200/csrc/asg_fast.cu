@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(256)
 template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
-                       float *grad_em, const int32_t *status, cudaStream_t s) {
+                       float *grad_em, const int32_t *status, cudaStream_t s, Tracer *tr) {
   const size_t stage_bytes = sizeof(RowStage<SPL * 32, 32>);
   auto kc = asg_chain_kernel<SPL>;
   cudaError_t err0 =
@@ -803,6 +803,7 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
   kc<<<dim3(d.B, 4), 32, stage_bytes, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
+  trace(tr, s);  // chain
   constexpr int LP = SPL * 32;
   const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4) + LP);
   auto k = asg_grad_kernel<SPL>;
@@ -863,23 +864,26 @@ void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w) { asg_ws_layout(d, ws, w)
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
-                            int32_t *status, cudaStream_t s) {
+                            int32_t *status, cudaStream_t s, Tracer *tr) {
   cudaError_t err = cudaSuccess;
   switch (w.spl) {
-    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
     default: return cudaErrorInvalidValue;
   }
   if (err != cudaSuccess) return err;
+  trace(tr, s);  // grad
   asg_final_kernel<<<d.B, 256, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status);
-  return cudaGetLastError();
+  err = cudaGetLastError();
+  trace(tr, s);  // final
+  return err;
 }
 
 // --------------------------------------------------- batch reduction of dA --

@@ -45,6 +45,14 @@ extern "C" {
 
 const char *w2l_version(void) { return "w2l-criterion sm_100a r1 (scaled-linear fp32 + f64 exact)"; }
 
+const char *w2l_stage_name(int kind, int i) {
+  static const char *asg[] = {"validate", "chain", "grad", "final", "exact_fallback", "reduce"};
+  static const char *ctc[] = {"validate", "chain", "grad", "final", "exact_fallback"};
+  if (kind == 0 && i >= 0 && i < 6) return asg[i];
+  if (kind == 1 && i >= 0 && i < 5) return ctc[i];
+  return "";
+}
+
 const char *w2l_last_cuda_error(void) {
   const cudaError_t e = g_last_cuda;
   g_last_cuda = cudaSuccess;
@@ -113,11 +121,11 @@ size_t w2l_asg_workspace_bytes(int B, int Tmax, int N, int Lmax) {
   return asg_ws(B, Tmax, N, Lmax, nullptr, nullptr, nullptr, nullptr);
 }
 
-int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt,
-                      const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
-                      int Lmax, double *loss, float *grad_em, float *grad_trans,
-                      float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
-                      unsigned flags, w2l_stream_t stream) {
+static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
+                   const int32_t *tgt_len, const float *trans, int B, int Tmax, int N, int Lmax,
+                   double *loss, float *grad_em, float *grad_trans, float *grad_trans_utt,
+                   int32_t *status, void *ws, size_t ws_bytes, unsigned flags,
+                   cudaStream_t s, Tracer *tr) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
@@ -125,25 +133,70 @@ int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_asg_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
   const bool fallback = !(flags & W2L_FLAG_NO_FALLBACK);
-  cudaStream_t s = (cudaStream_t)stream;
   Dims d{B, Tmax, N, Lmax};
   AsgFastWs w;
   float *ga_ws;
   void *slots;
   asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
+  trace(tr, s);
   int rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad,
                                                 w.perm, w.tok_start, status, s));
   if (rc) return rc;
+  trace(tr, s);  // validate
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
-                                 status, s));
+                                 status, s, tr));
   if (rc) return rc;
   if (fallback) {
     rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
                                            slots, loss, grad_em, ga, status, s));
     if (rc) return rc;
   }
-  return from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
+  trace(tr, s);  // exact fallback
+  rc = from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
+  trace(tr, s);  // reduce
+  return rc;
+}
+
+int w2l_asg_loss_grad(const float *em, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
+                      int Lmax, double *loss, float *grad_em, float *grad_trans,
+                      float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                      unsigned flags, w2l_stream_t stream) {
+  return asg_run(em, em_len, tgt, tgt_len, trans, B, Tmax, N, Lmax, loss, grad_em, grad_trans,
+                 grad_trans_utt, status, ws, ws_bytes, flags, (cudaStream_t)stream, nullptr);
+}
+
+}  // extern "C"
+
+// run a traced launch sequence and turn its events into per-stage times
+template <class F>
+static int traced(F run, cudaStream_t s, float *stage_ms, int *n_stages) {
+  Tracer tr;
+  for (int i = 0; i < Tracer::kMax; ++i) cudaEventCreate(&tr.ev[i]);
+  int rc = run(&tr);
+  if (rc == W2L_OK) rc = from_cuda(cudaStreamSynchronize(s));
+  int n = 0;
+  if (rc == W2L_OK)
+    for (int i = 1; i < tr.n; ++i) cudaEventElapsedTime(&stage_ms[n++], tr.ev[i - 1], tr.ev[i]);
+  if (n_stages) *n_stages = n;
+  for (int i = 0; i < Tracer::kMax; ++i) cudaEventDestroy(tr.ev[i]);
+  return rc;
+}
+
+extern "C" {
+
+int w2l_asg_loss_grad_traced(const float *em, const int32_t *em_len, const int64_t *tgt,
+                             const int32_t *tgt_len, const float *trans, int B, int Tmax, int N,
+                             int Lmax, double *loss, float *grad_em, float *grad_trans,
+                             float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
+                             unsigned flags, w2l_stream_t stream, float *stage_ms,
+                             int *n_stages) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return traced([&](Tracer *tr) {
+    return asg_run(em, em_len, tgt, tgt_len, trans, B, Tmax, N, Lmax, loss, grad_em, grad_trans,
+                   grad_trans_utt, status, ws, ws_bytes, flags, s, tr);
+  }, s, stage_ms, n_stages);
 }
 
 size_t w2l_asg_workspace_bytes_f64(int B, int Tmax, int N, int Lmax) {
@@ -204,28 +257,52 @@ size_t w2l_ctc_workspace_bytes(int B, int Tmax, int N, int Lmax) {
   return ctc_ws(B, Tmax, N, Lmax, nullptr, nullptr, nullptr);
 }
 
-int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
-                      const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
-                      double *loss, float *grad_em, int32_t *status, void *ws,
-                      size_t ws_bytes, unsigned flags, w2l_stream_t stream) {
+static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                   const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
+                   double *loss, float *grad_em, int32_t *status, void *ws, size_t ws_bytes,
+                   unsigned flags, cudaStream_t s, Tracer *tr) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_ctc_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
-  cudaStream_t s = (cudaStream_t)stream;
   Dims d{B, Tmax, N, Lmax};
   CtcFastWs w;
   void *slots;
   ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
+  trace(tr, s);
   int rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
                                                 w.perm, w.tok_start, status, s));
   if (rc) return rc;
-  rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s));
+  trace(tr, s);  // validate
+  rc = from_cuda(
+      launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s, tr));
   if (rc) return rc;
-  if (flags & W2L_FLAG_NO_FALLBACK) return W2L_OK;
-  return from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
+  if (!(flags & W2L_FLAG_NO_FALLBACK))
+    rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
                                            asg_slots(B), slots, loss, grad_em, status, s));
+  trace(tr, s);  // exact fallback
+  return rc;
+}
+
+int w2l_ctc_loss_grad(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                      const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
+                      double *loss, float *grad_em, int32_t *status, void *ws,
+                      size_t ws_bytes, unsigned flags, w2l_stream_t stream) {
+  return ctc_run(logp, em_len, tgt, tgt_len, blank, B, Tmax, N, Lmax, loss, grad_em, status, ws,
+                 ws_bytes, flags, (cudaStream_t)stream, nullptr);
+}
+
+int w2l_ctc_loss_grad_traced(const float *logp, const int32_t *em_len, const int64_t *tgt,
+                             const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
+                             double *loss, float *grad_em, int32_t *status, void *ws,
+                             size_t ws_bytes, unsigned flags, w2l_stream_t stream,
+                             float *stage_ms, int *n_stages) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return traced([&](Tracer *tr) {
+    return ctc_run(logp, em_len, tgt, tgt_len, blank, B, Tmax, N, Lmax, loss, grad_em, status,
+                   ws, ws_bytes, flags, s, tr);
+  }, s, stage_ms, n_stages);
 }
 
 size_t w2l_ctc_workspace_bytes_f64(int B, int Tmax, int N, int Lmax) {

@@ -325,7 +325,7 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
 template <int SPL>
 cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
                        const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
-                       float *grad_em, const int32_t *status, cudaStream_t s) {
+                       float *grad_em, const int32_t *status, cudaStream_t s, Tracer *tr) {
   const size_t stage_bytes = sizeof(RowStage<SPL * 32, 32>);
   auto kc = ctc_chain_kernel<SPL>;
   cudaError_t err0 =
@@ -334,6 +334,7 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
   kc<<<dim3(d.B, 2), 32, stage_bytes, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
+  trace(tr, s);  // chain
   ctc_grad_kernel<SPL><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
                                                                       blank, d, w, grad_em,
                                                                       status);
@@ -382,23 +383,27 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w)
 
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
-                            double *loss, float *grad_em, int32_t *status, cudaStream_t s) {
+                            double *loss, float *grad_em, int32_t *status, cudaStream_t s,
+                            Tracer *tr) {
   cudaError_t err = cudaSuccess;
   switch (w.spl) {
-    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
+    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s, tr); break;
     default: return cudaErrorInvalidValue;
   }
   if (err != cudaSuccess) return err;
+  trace(tr, s);  // grad
   ctc_final_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
-  return cudaGetLastError();
+  err = cudaGetLastError();
+  trace(tr, s);  // final
+  return err;
 }
 
 }  // namespace w2l

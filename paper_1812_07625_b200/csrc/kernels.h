@@ -10,6 +10,20 @@ struct Dims {
   int B, Tmax, N, Lmax;
 };
 
+// Optional per-stage event trace (profiling entry points only): mark()
+// records an event on the stream after each stage of a launch sequence.
+struct Tracer {
+  static constexpr int kMax = 16;
+  cudaEvent_t ev[kMax];
+  int n = 0;
+  void mark(cudaStream_t s) {
+    if (n < kMax) cudaEventRecord(ev[n++], s);
+  }
+};
+inline void trace(Tracer *t, cudaStream_t s) {
+  if (t) t->mark(s);
+}
+
 // ---- validation (reference check order; criterion.py:23-41,92-111,174-190)
 // perm/tok_start (nullable): token CSR of valid utterances for the fast path
 template <class TE>
@@ -60,7 +74,7 @@ void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w);
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
-                            int32_t *status, cudaStream_t s);
+                            int32_t *status, cudaStream_t s, Tracer *tr = nullptr);
 
 struct CtcFastWs {
   float *a, *b;              // [B][Tmax][SPL*32]
@@ -76,7 +90,8 @@ size_t ctc_fast_ws_bytes(Dims d);
 void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w);
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
-                            double *loss, float *grad_em, int32_t *status, cudaStream_t s);
+                            double *loss, float *grad_em, int32_t *status, cudaStream_t s,
+                            Tracer *tr = nullptr);
 
 // ---- reductions
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
