@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     }
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
     const float con = (c0 + c1) + (c2 + c3);
-    if (lane < N) ge[(row0 + t) * N + lane] = full_e - con * inv_zc;
+    if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
     // ---- fac edge posteriors (:218-224).  The lane scale 2^d is bounded by
     // 2^127 and the mantissa products are tiny whenever d is large (a
     // posterior is <= 1), so x * 2^d * (1/Z) cannot overflow.
