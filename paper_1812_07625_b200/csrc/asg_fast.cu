@@ -27,6 +27,7 @@
 // posteriors = :214-224, fcc = :227-241, combine = :243-247.
 
 #include "chunk.cuh"
+#include "lane64.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -260,8 +261,8 @@ __device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChun
 // l INTO l+1).  Padding states read the zero emission column N.
 template <int SPL>
 __device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y, int L,
-                                            bool is_alpha, int (&tok)[SPL], float (&S)[SPL],
-                                            float (&P)[SPL]) {
+                                            bool is_alpha, int (&tok)[SPL], double (&S)[SPL],
+                                            double (&P)[SPL]) {
   const int N = c.N;
 #pragma unroll
   for (int k = 0; k < SPL; ++k) {
@@ -269,15 +270,15 @@ __device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y,
     if (l < L) {
       const int yl = (int)y[l];
       tok[k] = yl;
-      S[k] = expf(c.trans[yl * N + yl] - c.amax);
+      S[k] = (double)expf(c.trans[yl * N + yl] - c.amax);
       if (is_alpha)
-        P[k] = l > 0 ? expf(c.trans[yl * N + (int)y[l - 1]] - c.amax) : 0.f;
+        P[k] = l > 0 ? (double)expf(c.trans[yl * N + (int)y[l - 1]] - c.amax) : 0.0;
       else
-        P[k] = l + 1 < L ? expf(c.trans[(int)y[l + 1] * N + yl] - c.amax) : 0.f;
+        P[k] = l + 1 < L ? (double)expf(c.trans[(int)y[l + 1] * N + yl] - c.amax) : 0.0;
     } else {
       tok[k] = N;
-      S[k] = 0.f;
-      P[k] = 0.f;
+      S[k] = 0.0;
+      P[k] = 0.0;
     }
   }
 }
@@ -285,54 +286,57 @@ __device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y,
 template <int SPL>
 struct FacState {
   int tok[SPL];
-  float S[SPL], P[SPL], v[SPL];
+  double S[SPL], P[SPL], v[SPL];
   int ex;
 };
 
-// fac alpha step t (criterion.py:197-202) in block floating point
+// fac alpha step t (criterion.py:197-202), fp64 lane block
 template <int SPL>
-__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const float *row, bool renorm, bool check,
-                                               float *out, int *oute, int lane, int t) {
-  float E[SPL];
+__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const double *row, bool renorm,
+                                               bool check, float *out, int *oute, int lane,
+                                               int t) {
+  double E[SPL];
 #pragma unroll
   for (int k = 0; k < SPL; ++k) E[k] = row[f.tok[k]];
-  float nb = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
+  double nb = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
   int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
   if (lane == 0) {
-    nb = 0.f;
+    nb = 0.0;
     nbe = kNegExp;
   }
-  const float nbs = align_neighbour<SPL>(nb, nbe, f.v, f.ex, check);
+  const double nbs = align_neighbour_d<SPL>(nb, nbe, f.v, f.ex, check);
 #pragma unroll
-  for (int k = SPL - 1; k >= 1; --k) f.v[k] = E[k] * fmaf(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
-  f.v[0] = E[0] * fmaf(f.S[0], f.v[0], f.P[0] * nbs);
-  if (renorm) lane_renorm<SPL>(f.v, f.ex);
-  lane_store<SPL>(f.v, f.ex, out, oute, lane, t);
+  for (int k = SPL - 1; k >= 1; --k) f.v[k] = E[k] * fma(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
+  f.v[0] = E[0] * fma(f.S[0], f.v[0], f.P[0] * nbs);
+  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
+  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t);
 }
 
 // fac beta' step consuming frame u (criterion.py:207-212)
 template <int SPL>
-__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const float *row, bool renorm, bool check,
-                                              float *out, int *oute, int lane, int t_out) {
-  float wv[SPL];
+__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const double *row, bool renorm,
+                                              bool check, float *out, int *oute, int lane,
+                                              int t_out) {
+  double wv[SPL];
 #pragma unroll
   for (int k = 0; k < SPL; ++k) wv[k] = row[f.tok[k]] * f.v[k];
-  float nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
+  double nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
   int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
   if (lane == 31) {
-    nb = 0.f;
+    nb = 0.0;
     nbe = kNegExp;
   }
-  const float nbs = align_neighbour<SPL>(nb, nbe, wv, f.ex, check);
+  const double nbs = align_neighbour_d<SPL>(nb, nbe, wv, f.ex, check);
 #pragma unroll
-  for (int k = 0; k < SPL - 1; ++k) f.v[k] = fmaf(f.S[k], wv[k], f.P[k] * wv[k + 1]);
-  f.v[SPL - 1] = fmaf(f.S[SPL - 1], wv[SPL - 1], f.P[SPL - 1] * nbs);
-  if (renorm) lane_renorm<SPL>(f.v, f.ex);
-  lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
+  for (int k = 0; k < SPL - 1; ++k) f.v[k] = fma(f.S[k], wv[k], f.P[k] * wv[k + 1]);
+  f.v[SPL - 1] = fma(f.S[SPL - 1], wv[SPL - 1], f.P[SPL - 1] * nbs);
+  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
+  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t_out);
 }
 
 template <int SPL>
 __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
+                                          double (*dchunk)[kChunk * kStride],
                                           RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
                                           float *out, int *oute, double *lnz) {
   int gi = 0;
@@ -343,9 +347,9 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[0], c, 0);
   for (int ch = 0; ch < nch; ++ch) {
-    float *buf = chunk[ch & 1];
+    const double *buf = dchunk[ch & 1];
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert(buf, c, rows);
+    stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows);
     if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
@@ -355,38 +359,39 @@ __device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChu
         stage_acquire(gi, lane);
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, (q % kRenorm) == 1, st.v[slot],
-                              st.e[slot], lane, q);
+          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenormD) == 0,
+                              (q % kRenormD) == 1, st.v[slot], st.e[slot], lane, q);
         stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
       }
     } else {
       int r = 0;
       if (ch == 0) {   // t = 0: only the first target state is reachable (:194)
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) f.v[k] = 0.f;
+        for (int k = 0; k < SPL; ++k) f.v[k] = 0.0;
         if (lane == 0) f.v[0] = buf[f.tok[0]];
-        lane_renorm<SPL>(f.v, f.ex);
-        lane_store<SPL>(f.v, f.ex, out, oute, lane, 0);
+        lane_renorm_d<SPL>(f.v, f.ex);
+        lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, 0);
         r = 1;
       }
       for (; r < rows; ++r) {
         const int t = t0 + r;
-        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, true, out, oute,
-                            lane, t);
+        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenormD) == 0 || t == T - 1, true, out,
+                            oute, lane, t);
       }
     }
   }
   stage_drain(lane);
   // fac score = alpha_{T-1}[L-1] (:203)
   const int lastl = L - 1;
-  float vl = 0.f;
+  double vl = 0.0;
 #pragma unroll
   for (int k = 0; k < SPL; ++k) vl = (lane * SPL + k == lastl) ? f.v[k] : vl;
-  if (lane == lastl / SPL) *lnz = log((double)vl) + (double)f.ex * 0.6931471805599453;
+  if (lane == lastl / SPL) *lnz = log(vl) + (double)f.ex * 0.6931471805599453;
 }
 
 template <int SPL>
 __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
+                                         double (*dchunk)[kChunk * kStride],
                                          RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
                                          float *out, int *oute, double *lnz) {
   int gi = 0;
@@ -395,16 +400,16 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
   fac_weights<SPL>(c, y, L, false, f.tok, f.S, f.P);
   const int lastl = L - 1;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) f.v[k] = (lane * SPL + k == lastl) ? 1.f : 0.f;
+  for (int k = 0; k < SPL; ++k) f.v[k] = (lane * SPL + k == lastl) ? 1.0 : 0.0;
   f.ex = (lane == lastl / SPL) ? 0 : kNegExp;
-  lane_store<SPL>(f.v, f.ex, out, oute, lane, T - 1);
+  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, T - 1);
   const int nch = (T + kChunk - 1) / kChunk;
   stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
-  float e0 = 0.f;
+  double e0 = 0.0;
   for (int ch = nch - 1; ch >= 0; --ch) {
-    float *buf = chunk[ch & 1];
+    const double *buf = dchunk[ch & 1];
     const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert(buf, c, rows);
+    stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows);
     if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
     if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
@@ -414,21 +419,21 @@ __device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChun
         stage_acquire(gi, lane);
 #pragma unroll
         for (int q = kUnroll - 1; q >= 0; --q)
-          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0, (q % kRenorm) == 0,
-                             st.v[slot], st.e[slot], lane, q);
+          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenormD) == 0,
+                             (q % kRenormD) == 0, st.v[slot], st.e[slot], lane, q);
         stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32, lane);
       }
     } else {
       for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
         const int u = t0 + r;
-        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, true, out, oute,
-                           lane, u - 1);
+        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenormD) == 0 || u == 1, true,
+                           out, oute, lane, u - 1);
       }
     }
     if (ch == 0) e0 = buf[f.tok[0]];
   }
   stage_drain(lane);
-  if (lane == 0) *lnz = log((double)(e0 * f.v[0])) + (double)f.ex * 0.6931471805599453;
+  if (lane == 0) *lnz = log(e0 * f.v[0]) + (double)f.ex * 0.6931471805599453;
 }
 
 // One warp per CTA, grid (B, 4 roles): the CTA scheduler spreads the
@@ -441,6 +446,7 @@ __global__ void __launch_bounds__(32)
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
   __shared__ __align__(16) float chunk[2][kChunk * kStride];
+  __shared__ __align__(16) double dchunk[2][kChunk * kStride];
   __shared__ __align__(16) float vec[2][32];
   extern __shared__ __align__(128) unsigned char dsm[];  // row staging (dynamic)
   union Stage {
@@ -466,10 +472,10 @@ __global__ void __launch_bounds__(32)
     fcc_beta(c, chunk, vec, st.fcc, w.fcc_b + row0 * 32, w.fcc_kb + (size_t)b * w.tpad + 1,
              w.scal + b * 4 + 1);
   } else if (role == 2) {
-    fac_alpha<SPL>(c, chunk, st.fac, y, tgt_len[b], w.fac_a + row0 * (SPL * 32),
+    fac_alpha<SPL>(c, chunk, dchunk, st.fac, y, tgt_len[b], w.fac_a + row0 * (SPL * 32),
                    w.fac_ea + row0 * 32, w.scal + b * 4 + 2);
   } else {
-    fac_beta<SPL>(c, chunk, st.fac, y, tgt_len[b], w.fac_b + row0 * (SPL * 32),
+    fac_beta<SPL>(c, chunk, dchunk, st.fac, y, tgt_len[b], w.fac_b + row0 * (SPL * 32),
                   w.fac_eb + row0 * 32, w.scal + b * 4 + 3);
   }
 }
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const int tend = min(tb, T);
 
   // one frame's inputs; the next frame's are loaded while this one is used
-  struct Frame {
+  struct Frame {   // fac rows hold the high words of fp64 values (lane64.cuh)
     float e, fa, fb, va[SPL], vb[SPL];
     int ka, kb, ea, eb;
   };
@@ -583,12 +589,12 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   };
 
   // fac alpha at t-1 (values and lane exponent) carried across frames
-  float pa[SPL];
+  double pa[SPL];
   int pea = kNegExp;
   float pfa = 0.f;  // fcc alpha_{t-1}[lane]
   int pka = 0;
   if (ta >= 1 && ta < tend) {
-    lane_load<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
+    lane_load_hi<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
     pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
     pka = ka_row[ta - 1];
@@ -626,15 +632,21 @@ __global__ void __launch_bounds__(kGradWarps * 32)
         accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
       }
     }
-    // ---- fac node posteriors (:214-217); the frame reference exponent comes
-    // from the actual magnitudes (the chains renormalise lazily)
-    const int es = lane_pair_exponent<SPL>(cur.va, cur.vb, cur.ea, cur.eb);
+    // ---- fac node posteriors (:214-217) in fp64 (lane64.cuh); the frame
+    // reference exponent comes from the actual magnitudes (lazy renorm)
+    double va[SPL], vb[SPL];
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      va[k] = from_hi(__float_as_int(cur.va[k]));
+      vb[k] = from_hi(__float_as_int(cur.vb[k]));
+    }
+    const int es = lane_pair_exponent_d<SPL>(va, vb, cur.ea, cur.eb);
     const int estar = warp_max(es);
-    const float sc = es > kNegExp / 2 ? pow2f(cur.ea + cur.eb - estar) : 0.f;
+    const double sc = es > kNegExp / 2 ? pow2d_fast(cur.ea + cur.eb - estar) : 0.0;
     float zl = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      const float p = cur.va[k] * cur.vb[k] * sc;
+      const float p = (float)(va[k] * vb[k] * sc);
       myp[lane * SPL + k] = p;
       zl += p;
     }
@@ -660,21 +672,21 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     // 2^127 and the mantissa products are tiny whenever d is large (a
     // posterior is <= 1), so x * 2^d * (1/Z) cannot overflow.
     if (t >= 1) {
-      const float nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
+      const double nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
       const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
-      const float s_own = pow2f_fast(pea + cur.eb - estar);
-      const float s_nb = lane > 0 ? pow2f_fast(nbe + cur.eb - estar) : 0.f;
+      const double s_own = pow2d_fast(max(pea + cur.eb - estar, -1100));
+      const double s_nb = lane > 0 ? pow2d_fast(max(nbe + cur.eb - estar, -1100)) : 0.0;
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
-        const float ev = mye[tok[k]] * cur.vb[k];   // mantissas first, then the scale
-        accS[k] = fmaf(((pa[k] * S[k]) * ev) * s_own, inv_zc, accS[k]);
-        const float prev = k > 0 ? ((pa[k - 1] * P[k]) * ev) * s_own : ((nbv * P[k]) * ev) * s_nb;
-        accP[k] = fmaf(prev, inv_zc, accP[k]);
+        const double ev = (double)mye[tok[k]] * vb[k];
+        accS[k] = fmaf((float)(pa[k] * (double)S[k] * ev * s_own), inv_zc, accS[k]);
+        const double prev = k > 0 ? pa[k - 1] * s_own : nbv * s_nb;
+        accP[k] = fmaf((float)(prev * (double)P[k] * ev), inv_zc, accP[k]);
       }
     }
     // carry alpha_t as alpha_{t-1} for the next frame
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) pa[k] = cur.va[k];
+    for (int k = 0; k < SPL; ++k) pa[k] = va[k];
     pea = cur.ea;
     pfa = cur.fa;
     pka = cur.ka;

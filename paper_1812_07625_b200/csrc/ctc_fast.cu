@@ -13,6 +13,7 @@
 // are recomputed by the float64 log-domain kernel.
 
 #include "chunk.cuh"
+#include "lane64.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -22,9 +23,9 @@ namespace {
 constexpr int kGradFramesPerBlock = 64;
 constexpr int kGradWarps = 8;
 
-template <int SPL>
+template <int SPL, class R>
 __device__ __forceinline__ void ctc_lattice_lane(const int64_t *y, int L, int blank, int N,
-                                                 int lane, int *lab, float *sk, float *sk2) {
+                                                 int lane, int *lab, R *sk, R *sk2) {
   const int S = 2 * L + 1;
   auto skip_of = [&](int s) -> bool {
     return (s & 1) && s >= 3 && s < S && y[s >> 1] != y[(s >> 1) - 1];
@@ -33,66 +34,68 @@ __device__ __forceinline__ void ctc_lattice_lane(const int64_t *y, int L, int bl
   for (int k = 0; k < SPL; ++k) {
     const int s = lane * SPL + k;
     lab[k] = s < S ? ((s & 1) ? (int)y[s >> 1] : blank) : N;
-    sk[k] = skip_of(s) ? 1.f : 0.f;
-    sk2[k] = skip_of(s + 2) ? 1.f : 0.f;
+    sk[k] = skip_of(s) ? R(1) : R(0);
+    sk2[k] = skip_of(s + 2) ? R(1) : R(0);
   }
 }
 
 template <int SPL>
 struct CtcState {
   int lab[SPL];
-  float sk[SPL], sk2[SPL], v[SPL];
+  double sk[SPL], sk2[SPL], v[SPL];
   int ex;
 };
 
-// alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])  (:126-134)
+// alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])  (:126-134), fp64 lanes
 template <int SPL>
-__device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const float *row, bool renorm, bool check,
-                                               float *out, int *oute, int lane, int t) {
-  float E[SPL];
+__device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const double *row, bool renorm,
+                                               bool check, float *out, int *oute, int lane,
+                                               int t) {
+  double E[SPL];
 #pragma unroll
   for (int k = 0; k < SPL; ++k) E[k] = row[f.lab[k]];
-  float nb1 = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
-  float nb2 = __shfl_up_sync(0xffffffffu, f.v[SPL - 2], 1);
+  double nb1 = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
+  double nb2 = __shfl_up_sync(0xffffffffu, f.v[SPL - 2], 1);
   int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
   if (lane == 0) {
-    nb1 = nb2 = 0.f;
+    nb1 = nb2 = 0.0;
     nbe = kNegExp;
   }
-  const float n1 = align_neighbour<SPL>(nb1, nbe, f.v, f.ex, check);
-  const float n2 = nb2 * (check ? pow2f(nbe - f.ex) : pow2f_fast(min(nbe - f.ex, 126)));
+  const double n1 = align_neighbour_d<SPL>(nb1, nbe, f.v, f.ex, check);
+  const double n2 = nb2 * pow2d_fast(min(nbe - f.ex, 1000));
 #pragma unroll
   for (int k = SPL - 1; k >= 2; --k)
-    f.v[k] = E[k] * fmaf(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1]);
-  const float v1 = E[1] * fmaf(f.sk[1], n1, f.v[1] + f.v[0]);
-  f.v[0] = E[0] * fmaf(f.sk[0], n2, f.v[0] + n1);
+    f.v[k] = E[k] * fma(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1]);
+  const double v1 = E[1] * fma(f.sk[1], n1, f.v[1] + f.v[0]);
+  f.v[0] = E[0] * fma(f.sk[0], n2, f.v[0] + n1);
   f.v[1] = v1;
-  if (renorm) lane_renorm<SPL>(f.v, f.ex);
-  lane_store<SPL>(f.v, f.ex, out, oute, lane, t);
+  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
+  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t);
 }
 
 // beta'_{u-1}[s] = w[s] + w[s+1] + skip_{s+2} w[s+2],  w = Et_u[lab] beta'_u  (:147-155)
 template <int SPL>
-__device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const float *row, bool renorm, bool check,
-                                              float *out, int *oute, int lane, int t_out) {
-  float wv[SPL];
+__device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const double *row, bool renorm,
+                                              bool check, float *out, int *oute, int lane,
+                                              int t_out) {
+  double wv[SPL];
 #pragma unroll
   for (int k = 0; k < SPL; ++k) wv[k] = row[f.lab[k]] * f.v[k];
-  float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-  float nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
+  double nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+  double nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
   int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
   if (lane == 31) {
-    nb1 = nb2 = 0.f;
+    nb1 = nb2 = 0.0;
     nbe = kNegExp;
   }
-  const float n1 = align_neighbour<SPL>(nb1, nbe, wv, f.ex, check);
-  const float n2 = nb2 * (check ? pow2f(nbe - f.ex) : pow2f_fast(min(nbe - f.ex, 126)));
+  const double n1 = align_neighbour_d<SPL>(nb1, nbe, wv, f.ex, check);
+  const double n2 = nb2 * pow2d_fast(min(nbe - f.ex, 1000));
 #pragma unroll
-  for (int k = 0; k < SPL - 2; ++k) f.v[k] = fmaf(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
-  f.v[SPL - 2] = fmaf(f.sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
-  f.v[SPL - 1] = fmaf(f.sk2[SPL - 1], n2, wv[SPL - 1] + n1);
-  if (renorm) lane_renorm<SPL>(f.v, f.ex);
-  lane_store<SPL>(f.v, f.ex, out, oute, lane, t_out);
+  for (int k = 0; k < SPL - 2; ++k) f.v[k] = fma(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
+  f.v[SPL - 2] = fma(f.sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
+  f.v[SPL - 1] = fma(f.sk2[SPL - 1], n2, wv[SPL - 1] + n1);
+  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
+  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t_out);
 }
 
 // One warp per CTA, grid (B, 2): blockIdx.y 0 = alpha, 1 = beta.
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(32)
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
   __shared__ __align__(16) float chunk[2][kChunk * kStride];
+  __shared__ __align__(16) double dchunk[2][kChunk * kStride];
   extern __shared__ __align__(128) unsigned char dsm[];  // row staging (dynamic)
   RowStage<SPL * 32, 32> &st = *reinterpret_cast<RowStage<SPL * 32, 32> *>(dsm);
   const int b = blockIdx.x, lane = threadIdx.x;
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(32)
   const size_t row0 = (size_t)b * d.Tmax;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   CtcState<SPL> f;
-  ctc_lattice_lane<SPL>(y, L, blank, d.N, lane, f.lab, f.sk, f.sk2);
+  ctc_lattice_lane<SPL, double>(y, L, blank, d.N, lane, f.lab, f.sk, f.sk2);
   float *out = (fwd ? w.a : w.b) + row0 * (SPL * 32);
   int *oute = (fwd ? w.ea : w.eb) + row0 * 32;
   const double ln2 = 0.6931471805599453;
@@ -130,9 +134,9 @@ __global__ void __launch_bounds__(32)
     double shifts = 0.0;
     stage_issue(chunk[0], c, 0);
     for (int ch = 0; ch < nch; ++ch) {
-      float *buf = chunk[ch & 1];
+      const double *buf = dchunk[ch & 1];
       const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-      stage_convert(buf, c, rows, &shifts);
+      stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows, &shifts);
       if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
       if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
@@ -142,39 +146,39 @@ __global__ void __launch_bounds__(32)
           stage_acquire(gi, lane);
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
-            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenorm) == 0, (q % kRenorm) == 1, st.v[slot],
-                                st.e[slot], lane, q);
+            ctc_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenormD) == 0,
+                                (q % kRenormD) == 1, st.v[slot], st.e[slot], lane, q);
           stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
         }
       } else {
         int r = 0;
         if (ch == 0) {  // criterion.py:123-125
 #pragma unroll
-          for (int k = 0; k < SPL; ++k) f.v[k] = 0.f;
+          for (int k = 0; k < SPL; ++k) f.v[k] = 0.0;
           if (lane == 0) {
             f.v[0] = buf[f.lab[0]];
             if (S > 1) f.v[1] = buf[f.lab[1]];
           }
-          lane_renorm<SPL>(f.v, f.ex);
-          lane_store<SPL>(f.v, f.ex, out, oute, lane, 0);
+          lane_renorm_d<SPL>(f.v, f.ex);
+          lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, 0);
           r = 1;
         }
         for (; r < rows; ++r) {
           const int t = t0 + r;
-          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenorm) == 0 || t == T - 1, true, out, oute,
-                              lane, t);
+          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenormD) == 0 || t == T - 1, true,
+                              out, oute, lane, t);
         }
       }
     }
     stage_drain(lane);
     // log Z = logadd(alpha[S-1], alpha[S-2]) (criterion.py:136-139), in f64
-    float part = 0.f;
+    double part = 0.0;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
       const int s = lane * SPL + k;
       if (s == S - 1 || s == S - 2) part += f.v[k];
     }
-    const double lp_ = part > 0.f ? log((double)part) + (double)f.ex * ln2 : -CUDART_INF;
+    const double lp_ = part > 0.0 ? log(part) + (double)f.ex * ln2 : -CUDART_INF;
     const double m = warp_max(lp_);
     const double sum = warp_sum(lp_ > -CUDART_INF ? exp(lp_ - m) : 0.0);
     shifts = warp_sum(shifts);
@@ -186,16 +190,16 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
       const int s = lane * SPL + k;
-      f.v[k] = (s == S - 1 || s == S - 2) ? 1.f : 0.f;
+      f.v[k] = (s == S - 1 || s == S - 2) ? 1.0 : 0.0;
     }
-    lane_renorm<SPL>(f.v, f.ex);
-    lane_store<SPL>(f.v, f.ex, out, oute, lane, T - 1);
+    lane_renorm_d<SPL>(f.v, f.ex);
+    lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, T - 1);
     stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
-    float z0 = 0.f;
+    double z0 = 0.0;
     for (int ch = nch - 1; ch >= 0; --ch) {
-      float *buf = chunk[ch & 1];
+      const double *buf = dchunk[ch & 1];
       const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-      stage_convert(buf, c, rows);
+      stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows);
       if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
       if (ch > 0 && rows == kChunk) {
 #pragma unroll 1
@@ -205,16 +209,16 @@ __global__ void __launch_bounds__(32)
           stage_acquire(gi, lane);
 #pragma unroll
           for (int q = kUnroll - 1; q >= 0; --q)
-            ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenorm) == 0, (q % kRenorm) == 0,
-                               st.v[slot], st.e[slot], lane, q);
+            ctc_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenormD) == 0,
+                               (q % kRenormD) == 0, st.v[slot], st.e[slot], lane, q);
           stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32,
                         lane);
         }
       } else {
         for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
           const int u = t0 + r;
-          ctc_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenorm) == 0 || u == 1, true, out,
-                             oute, lane, u - 1);
+          ctc_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenormD) == 0 || u == 1, true,
+                             out, oute, lane, u - 1);
         }
       }
       if (ch == 0 && lane == 0) {
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(32)
       }
     }
     stage_drain(lane);
-    if (lane == 0) w.scal[b * 4 + 1] = log((double)z0) + (double)f.ex * ln2;
+    if (lane == 0) w.scal[b * 4 + 1] = log(z0) + (double)f.ex * ln2;
   }
 }
 
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   int lab[SPL];
   float sk[SPL], sk2[SPL];
-  ctc_lattice_lane<SPL>(y, L, blank, N, lane, lab, sk, sk2);
+  ctc_lattice_lane<SPL, float>(y, L, blank, N, lane, lab, sk, sk2);
   (void)S;
   const int *perm = w.perm + (size_t)b * w.lpad;
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
@@ -263,18 +267,18 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float *myp = prow[warp];
   const int tend = min(tb, T);
   for (int t = ta; t < tend; ++t) {
-    float va[SPL], vb[SPL];
-    lane_load<SPL>(va, w.a + (row0 + t) * LP, lane);
-    lane_load<SPL>(vb, w.b + (row0 + t) * LP, lane);
+    double va[SPL], vb[SPL];   // high words of fp64 lane values (lane64.cuh)
+    lane_load_hi<SPL>(va, w.a + (row0 + t) * LP, lane);
+    lane_load_hi<SPL>(vb, w.b + (row0 + t) * LP, lane);
     const int ea = w.ea[(row0 + t) * 32 + lane];
     const int eb = w.eb[(row0 + t) * 32 + lane];
-    const int es = lane_pair_exponent<SPL>(va, vb, ea, eb);
+    const int es = lane_pair_exponent_d<SPL>(va, vb, ea, eb);
     const int estar = warp_max(es);
-    const float sc = es > kNegExp / 2 ? pow2f(ea + eb - estar) : 0.f;
+    const double sc = es > kNegExp / 2 ? pow2d_fast(ea + eb - estar) : 0.0;
     float zl = 0.f, zb = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      const float p = va[k] * vb[k] * sc;
+      const float p = (float)(va[k] * vb[k] * sc);
       myp[lane * SPL + k] = p;
       zl += p;
       if (((lane * SPL + k) & 1) == 0) zb += p;   // blank states

@@ -318,3 +318,19 @@ def test_autograd_functions():
     want = sum(w[b].item() * orc.asg(em[b], tg[b, :tl[b]], a)[2].astype(np.float64)
                for b in range(3))
     assert orc.rel_err(A.grad.cpu().numpy(), want) < REL
+
+
+def test_fast_path_holds_on_peaky_emissions():
+    # log_softmax(2 N(0,1)) emissions (the bench data): the fp32 path must pass
+    # its own guard (no float64 fallback) and match the oracle
+    import bench
+    em, el, ta, tc, tl, a, blank = bench.make_inputs(0, b=6)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, ta, tl, a, fallback=False)
+    loss, ge, ga = orc.asg_batch(em, el, ta, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
+    outc = C.ctc_loss_grad_batched(torch.from_numpy(em).cuda(), el, tc, tl, blank, fallback=False)
+    loss, ge = orc.ctc_batch(em, el, tc, tl, blank)
+    np.testing.assert_allclose(outc.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(outc.grad_emissions.cpu().numpy(), ge) < REL
