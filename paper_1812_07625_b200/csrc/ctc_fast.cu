@@ -706,6 +706,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
         bad |= !(fabs(sm.gmin[q] * ln2 - zA) <= tol && fabs(sm.gmax[q] * ln2 - zA) <= tol);
     }
     loss[b] = -(zA + sm.shifts);                                 // criterion.py:162
+#ifdef W2L_DEBUG_FUSED
+    if (b < 2)
+      printf("b=%d T=%d S=%d zA=%f zB=%f shifts=%f g0=[%f %f] g1=[%f %f] g2=[%f %f] g3=[%f %f]\n", b, T, S, zA, zB, sm.shifts,
+             sm.gmin[0], sm.gmax[0], sm.gmin[1], sm.gmax[1], sm.gmin[2], sm.gmax[2], sm.gmin[3], sm.gmax[3]);
+#endif
     if (bad) status[b] = kNeedsExact;
   }
 }
@@ -718,7 +723,7 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
   const size_t smem = sizeof(CtcSmem<SPL>);
   auto k = ctc_fused_kernel<SPL>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return err;
+  if (err != cudaSuccess) return err;
   k<<<d.B, kFusedWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, blank, d, w, loss, grad_em,
                                         status);
   err = cudaGetLastError();
@@ -785,11 +790,6 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
     case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s, tr); break;
     default: return cudaErrorInvalidValue;
   }
-  return err;
-  trace(tr, s);  // grad
-  ctc_final_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
-  err = cudaGetLastError();
-  trace(tr, s);  // final
   return err;
 }
 
