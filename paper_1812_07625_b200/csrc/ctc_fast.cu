@@ -328,42 +328,68 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
 
 // ------------------------------------------------------------- fused kernel --
 // One CTA per utterance: warp 0 = alpha chain, warp 1 = beta chain, then
-// kHelpers helper warps for alpha and kHelpers for beta.  Meet in the middle
-// at row S (a multiple of 32, ~T/2):
+// H helper warps for alpha and H for beta.  Meet in the middle at row S (a
+// multiple of 32, ~T/2):
 //   phase 1  alpha computes rows [0, S), beta rows [S, T); each stores its rows
 //            with TMA bulk stores out of a shared-memory ring;
 //   barrier  bulk writes complete and published (named barrier, all warps);
 //   phase 2  alpha computes rows [S, T), beta rows [0, S); each hands its rows
-//            through the same ring (mbarrier full/empty per slot) to its
-//            helper warps, which read the partner's stored row of the same
-//            frame and emit that frame's posteriors, gradient row and guard.
+//            through the same ring to its helper warps (mbarrier "full" per
+//            slot, per-helper "consumed" counters back), which bulk-prefetch the
+//            partner's stored rows (TMA, mbarrier complete_tx) and emit every
+//            frame's posteriors, gradient row and guard value.
 // Every row is stored once, every posterior is computed once, and the
 // gradient work overlaps the serial recursions (no separate gradient pass).
-constexpr int kSlot = 4;      // rows per ring slot
-constexpr int kRing = 4;      // slots per chain
-constexpr int kHelpers = 2;   // helper warps per chain
-constexpr int kFusedWarps = 2 + 2 * kHelpers;
+template <int SPL>
+struct CtcCfg {
+  static constexpr int kSlot = 2;                     // rows per ring slot
+  static constexpr int kRing = 4;                     // slots per chain
+  static constexpr int kHelpers = SPL <= 24 ? 3 : 2;  // helper warps per chain
+  static constexpr int kWarps = 2 + 2 * kHelpers;
+};
 
 template <int SPL>
 struct CtcSmem {
-  float raw[2][2][kChunk * kStride];     // [chain][buffer] raw emission chunks
-  double dch[2][2][kChunk * kStride];    // converted Et (fp64)
-  int rv[2][kRing][kSlot * SPL * 32];    // ring rows (fp64 high words), row r at r % kSlot
-  int re[2][kRing][kSlot * 32];          // ring lane exponents
-  uint64_t full[2][kRing], empty[2][kRing];
-  float prow[2 * kHelpers][SPL * 32];    // helper posterior rows
-  double gmin[2 * kHelpers], gmax[2 * kHelpers];
-  int perm[SPL * 16];                    // label states grouped by token (<= L entries)
+  using C = CtcCfg<SPL>;
+  static constexpr int kRowI = SPL * 32;
+  float raw[2][2][kChunk * kStride];                  // [chain][buffer] raw emission chunks
+  double dch[2][2][kChunk * kStride];                 // converted Et (fp64)
+  int rv[2][C::kRing][C::kSlot * kRowI];              // ring rows (fp64 high words)
+  int re[2][C::kRing][C::kSlot * 32];                 // ring lane exponents
+  int pf[2 * C::kHelpers][2][C::kSlot * kRowI];       // partner rows (TMA prefetch)
+  int pfe[2 * C::kHelpers][2][C::kSlot * 32];
+  uint64_t full[2][C::kRing];                         // chain -> helper
+  uint64_t pfbar[2 * C::kHelpers][2];                 // prefetch completion
+  volatile int consumed[2 * C::kHelpers];             // helper -> chain (slots released)
+  float prow[2 * C::kHelpers][kRowI];                 // helper posterior rows
+  double gmin[2 * C::kHelpers], gmax[2 * C::kHelpers];
+  int perm[SPL * 16];                                 // label states grouped by token
   double lnz[2], shifts;
 };
 
 __device__ __forceinline__ int split_row(int T) { return (T / 64) * 32; }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // A chain's row sink: phase 1 -> bulk stores to its global rows, phase 2 ->
 // the helpers.  Slots are aligned to kSlot in row space; a slot holds the rows
-// of one phase only.
+// of one phase only.  Phase-2 slot q goes to helper q % H.
 template <int SPL>
 struct Emitter {
+  using C = CtcCfg<SPL>;
   CtcSmem<SPL> *sm;
   int chain;       // 0 alpha (rows ascending), 1 beta (descending)
   float *grow;     // this chain's rows in the workspace (utterance base)
@@ -371,8 +397,9 @@ struct Emitter {
   int S, T;
   bool phase2, met;
   int seq1, seq2;  // slots issued in phase 1 / phase 2
+  int seen[C::kHelpers];  // cached consumed counters
 
-  __device__ __forceinline__ int ring() const { return (phase2 ? seq2 : seq1) % kRing; }
+  __device__ __forceinline__ int ring() const { return (phase2 ? seq2 : seq1) % C::kRing; }
   __device__ __forceinline__ float *rows() {
     return reinterpret_cast<float *>(sm->rv[chain][ring()]);
   }
@@ -384,7 +411,7 @@ struct Emitter {
     if (!met) {
       if (lane == 0) bulk_publish();
       __syncwarp();
-      named_barrier(1, kFusedWarps * 32);
+      named_barrier(1, C::kWarps * 32);
       met = true;
     }
   }
@@ -394,9 +421,17 @@ struct Emitter {
   }
   __device__ __forceinline__ void acquire(int lane) {
     if (!phase2) {
-      if (seq1 >= kRing && lane == 0) bulk_wait_read_n<kRing - 1>();
-    } else if (seq2 >= kRing) {
-      mbar_wait(&sm->empty[chain][seq2 % kRing], ((seq2 / kRing) - 1) & 1);
+      if (seq1 >= C::kRing && lane == 0) bulk_wait_read_n<C::kRing - 1>();
+    } else if (seq2 >= C::kRing) {
+      // slot seq2 - kRing (same ring position) must have been released by its helper
+      const int prev = seq2 - C::kRing;
+      const int hh = prev % C::kHelpers, need = prev / C::kHelpers + 1;
+#pragma unroll
+      for (int x = 0; x < C::kHelpers; ++x)
+        if (x == hh) {
+          while (seen[x] < need) seen[x] = sm->consumed[chain * C::kHelpers + x];
+        }
+      __threadfence_block();
     }
     __syncwarp();
   }
@@ -407,27 +442,29 @@ struct Emitter {
       __syncwarp();
       if (lane == 0) {
         constexpr int LP = SPL * 32;
-        bulk_store(grow + (size_t)lo * LP, rows() + (lo % kSlot) * LP, n * LP * sizeof(int));
-        bulk_store(gexp + lo * 32, exps() + (lo % kSlot) * 32, n * 32 * sizeof(int));
+        bulk_store(grow + (size_t)lo * LP, rows() + (lo % C::kSlot) * LP,
+                   n * LP * sizeof(int));
+        bulk_store(gexp + lo * 32, exps() + (lo % C::kSlot) * 32, n * 32 * sizeof(int));
         bulk_commit();
       }
       ++seq1;
     } else {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm->full[chain][seq2 % kRing]);
+      if (lane == 0) mbar_arrive(&sm->full[chain][seq2 % C::kRing]);
       ++seq2;
     }
   }
   // generic per-row protocol around the step that produces row r
   __device__ __forceinline__ void begin(int r, int lane) {
     if (!phase2 && (chain == 0 ? r >= S : r < S)) enter_phase2(lane);
-    const int k = r / kSlot;
-    const int first = chain == 0 ? max(k * kSlot, lo_phase()) : min(k * kSlot + kSlot, hi_phase()) - 1;
+    const int k = r / C::kSlot;
+    const int first = chain == 0 ? max(k * C::kSlot, lo_phase())
+                                 : min(k * C::kSlot + C::kSlot, hi_phase()) - 1;
     if (r == first) acquire(lane);
   }
   __device__ __forceinline__ void end(int r, int lane) {
-    const int k = r / kSlot;
-    const int lo = max(k * kSlot, lo_phase()), hi = min(k * kSlot + kSlot, hi_phase());
+    const int k = r / C::kSlot;
+    const int lo = max(k * C::kSlot, lo_phase()), hi = min(k * C::kSlot + C::kSlot, hi_phase());
     const int last = chain == 0 ? hi - 1 : lo;
     if (r == last) release(lo, hi - lo, lane);
   }
@@ -437,6 +474,7 @@ struct Emitter {
 template <int SPL>
 __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL> &f,
                                 Emitter<SPL> &o, int S_len) {
+  constexpr int SLOT = CtcCfg<SPL>::kSlot;
   const int lane = c.lane, T = c.T, S = o.S;
   const int nch = (T + kChunk - 1) / kChunk;
   double shifts = 0.0;
@@ -450,19 +488,19 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
     if (ch > 0 && rows == kChunk) {
       if (!o.phase2 && t0 >= S) o.enter_phase2(lane);
 #pragma unroll 1
-      for (int g = 0; g < kChunk; g += 2 * kSlot) {
+      for (int g = 0; g < kChunk; g += kUnroll) {
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int sl = 0; sl < kUnroll / SLOT; ++sl) {
           o.acquire(lane);
           float *rw = o.rows();
           int *re = o.exps();
 #pragma unroll
-          for (int q = 0; q < kSlot; ++q) {
-            const int qq = half * kSlot + q;   // position in the 8-row block
+          for (int q = 0; q < SLOT; ++q) {
+            const int qq = sl * SLOT + q;   // position in the 8-row block
             ctc_alpha_step<SPL>(f, buf + (g + qq) * kStride, (qq % kRenormD) == 0,
                                 (qq % kRenormD) == 1, rw, re, lane, q);
           }
-          o.release(t0 + g + half * kSlot, kSlot, lane);
+          o.release(t0 + g + sl * SLOT, SLOT, lane);
         }
       }
     } else {
@@ -477,10 +515,10 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
             if (S_len > 1) f.v[1] = buf[f.lab[1]];
           }
           lane_renorm_d<SPL>(f.v, f.ex);
-          lane_store_hi<SPL>(f.v, f.ex, o.rows(), o.exps(), lane, t % kSlot);
+          lane_store_hi<SPL>(f.v, f.ex, o.rows(), o.exps(), lane, t % SLOT);
         } else {
           ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenormD) == 0 || t == T - 1, true,
-                              o.rows(), o.exps(), lane, t % kSlot);
+                              o.rows(), o.exps(), lane, t % SLOT);
         }
         o.end(t, lane);
       }
@@ -510,20 +548,20 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
 template <int SPL>
 __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL> &f,
                                Emitter<SPL> &o, int S_len) {
+  constexpr int SLOT = CtcCfg<SPL>::kSlot;
   const int lane = c.lane, T = c.T;
   ChainCtx cf = c;
   cf.e = c.e + c.N;   // frame r+1 for row r
   cf.T = T - 1;       // rows 0 .. T-2 have a step
-  // row T-1: beta' = 1 on the last two states
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) {
+  for (int k = 0; k < SPL; ++k) {   // row T-1: beta' = 1 on the last two states
     const int s = lane * SPL + k;
     f.v[k] = (s == S_len - 1 || s == S_len - 2) ? 1.0 : 0.0;
   }
   f.ex = 0;
   lane_renorm_d<SPL>(f.v, f.ex);
   o.begin(T - 1, lane);
-  lane_store_hi<SPL>(f.v, f.ex, o.rows(), o.exps(), lane, (T - 1) % kSlot);
+  lane_store_hi<SPL>(f.v, f.ex, o.rows(), o.exps(), lane, (T - 1) % SLOT);
   o.end(T - 1, lane);
   const int nch = (T - 1 + kChunk - 1) / kChunk;   // row chunks with a step
   if (nch > 0) stage_issue(sm.raw[1][(nch - 1) & 1], cf, (nch - 1) * kChunk);
@@ -532,25 +570,25 @@ __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL
     const double *buf = sm.dch[1][ch & 1];
     stage_convert_d(sm.raw[1][ch & 1], sm.dch[1][ch & 1], cf, rows);
     if (ch > 0) stage_issue(sm.raw[1][(ch - 1) & 1], cf, r0 - kChunk);
-    // full chunk, phase uniform (S is a multiple of kChunk), slots complete
-    const bool uniform = rows == kChunk && (r0 + kChunk <= o.S || r0 >= o.S) &&
-                         (r0 + kChunk) % kSlot == 0 && r0 + kChunk <= T - 1;
+    // full chunk below the top, inside one phase (S is a multiple of kChunk)
+    const bool uniform = rows == kChunk && r0 + kChunk <= T - 1 &&
+                         (r0 + kChunk <= o.S || r0 >= o.S);
     if (uniform) {
       if (!o.phase2 && r0 + kChunk <= o.S) o.enter_phase2(lane);
 #pragma unroll 1
-      for (int g = kChunk - 2 * kSlot; g >= 0; g -= 2 * kSlot) {
+      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
 #pragma unroll
-        for (int half = 1; half >= 0; --half) {
+        for (int sl = kUnroll / SLOT - 1; sl >= 0; --sl) {
           o.acquire(lane);
           float *rw = o.rows();
           int *re = o.exps();
 #pragma unroll
-          for (int q = kSlot - 1; q >= 0; --q) {
-            const int qq = half * kSlot + q;   // row offset in the 8-row block
+          for (int q = SLOT - 1; q >= 0; --q) {
+            const int qq = sl * SLOT + q;   // row offset in the 8-row block
             ctc_beta_step<SPL>(f, buf + (g + qq) * kStride, (qq % kRenormD) == 0,
                                (qq % kRenormD) == kRenormD - 1, rw, re, lane, q);
           }
-          o.release(r0 + g + half * kSlot, kSlot, lane);
+          o.release(r0 + g + sl * SLOT, SLOT, lane);
         }
       }
     } else {
@@ -558,7 +596,7 @@ __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL
         const int r = r0 + j;   // produces beta'_r from frame r+1
         o.begin(r, lane);
         ctc_beta_step<SPL>(f, buf + j * kStride, (r % kRenormD) == 0, true, o.rows(), o.exps(),
-                           lane, r % kSlot);
+                           lane, r % SLOT);
         o.end(r, lane);
       }
     }
@@ -577,41 +615,77 @@ __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL
   }
 }
 
-// ---- helper: posteriors and gradient rows for the slots of one chain
+// ---- helper: posteriors and gradient rows for the phase-2 slots of a chain
 template <int SPL>
 __device__ void ctc_helper(CtcSmem<SPL> &sm, int chain, int h, int lane, const CtcFastWs &w,
-                           size_t row0, int T, int S, int N, int blank, const int *lab,
-                           const int *ts, float *ge, int L) {
-  constexpr int LP = SPL * 32;
-  const int hid = chain * kHelpers + h;
+                           size_t row0, int T, int S, int N, int blank, const int *ts,
+                           float *ge) {
+  using C = CtcCfg<SPL>;
+  constexpr int LP = SPL * 32, SLOT = C::kSlot, H = C::kHelpers;
+  const int hid = chain * H + h;
   float *myp = sm.prow[hid];
-  const float *prow_g = chain == 0 ? w.b : w.a;   // the partner's stored rows
+  const int *prow_g = reinterpret_cast<const int *>(chain == 0 ? w.b : w.a);   // partner rows
   const int *pexp_g = chain == 0 ? w.eb : w.ea;
   const int ts0 = lane < N ? ts[lane] : 0, ts1 = lane < N ? ts[lane + 1] : 0;
   double gmin = CUDART_INF, gmax = -CUDART_INF;
-  const int Q = chain == 0 ? (T - S + kSlot - 1) / kSlot : S / kSlot;
-  named_barrier(1, kFusedWarps * 32);   // phase 1 finished: partner rows are in memory
-  for (int q = h; q < Q; q += kHelpers) {
-    const int ring = q % kRing;
-    const int k = chain == 0 ? S / kSlot + q : S / kSlot - 1 - q;
-    const int lo = k * kSlot, hi = min(lo + kSlot, T);
-    mbar_wait(&sm.full[chain][ring], (q / kRing) & 1);
+  const int Q = chain == 0 ? (T - S + SLOT - 1) / SLOT : S / SLOT;
+  auto rows_of = [&](int q, int &lo, int &hi) {
+    const int k = chain == 0 ? S / SLOT + q : S / SLOT - 1 - q;
+    lo = k * SLOT;
+    hi = min(lo + SLOT, T);
+  };
+  auto prefetch = [&](int q, int buf) {
+    if (lane == 0 && q < Q) {
+      int lo, hi;
+      rows_of(q, lo, hi);
+      const uint32_t bv = (hi - lo) * LP * sizeof(int), be = (hi - lo) * 32 * sizeof(int);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_expect_tx(&sm.pfbar[hid][buf], bv + be);
+      bulk_load(sm.pf[hid][buf], prow_g + (row0 + lo) * LP, bv, &sm.pfbar[hid][buf]);
+      bulk_load(sm.pfe[hid][buf], pexp_g + (row0 + lo) * 32, be, &sm.pfbar[hid][buf]);
+    }
+  };
+  named_barrier(1, C::kWarps * 32);   // phase 1 finished: partner rows are in memory
+  prefetch(h, 0);
+  prefetch(h + H, 1);
+  int i = 0;
+  for (int q = h; q < Q; q += H, ++i) {
+    const int buf = i & 1, ring = q % C::kRing;
+    int lo, hi;
+    rows_of(q, lo, hi);
+    mbar_wait(&sm.pfbar[hid][buf], (i >> 1) & 1);
+    mbar_wait(&sm.full[chain][ring], (q / C::kRing) & 1);
     for (int r = lo; r < hi; ++r) {
-      double own[SPL], oth[SPL];
-      lane_load_hi<SPL>(own, reinterpret_cast<const float *>(sm.rv[chain][ring]) + (r % kSlot) * LP, lane);
-      lane_load_hi<SPL>(oth, prow_g + (row0 + r) * LP, lane);
-      const int eo = sm.re[chain][ring][(r % kSlot) * 32 + lane];
-      const int ep = pexp_g[(row0 + r) * 32 + lane];
-      const int es = lane_pair_exponent_d<SPL>(own, oth, eo, ep);
+      const int2 *own2 = reinterpret_cast<const int2 *>(sm.rv[chain][ring] + (r % SLOT) * LP + lane * SPL);
+      const int2 *oth2 = reinterpret_cast<const int2 *>(sm.pf[hid][buf] + (r - lo) * LP + lane * SPL);
+      int oh[SPL], ph[SPL];
+#pragma unroll
+      for (int k = 0; k < SPL / 2; ++k) {
+        const int2 a = own2[k], bq = oth2[k];
+        oh[2 * k] = a.x;
+        oh[2 * k + 1] = a.y;
+        ph[2 * k] = bq.x;
+        ph[2 * k + 1] = bq.y;
+      }
+      const int eo = sm.re[chain][ring][(r % SLOT) * 32 + lane];
+      const int ep = sm.pfe[hid][buf][(r - lo) * 32 + lane];
+      // largest product exponent of the lane from the stored high words
+      // (positive doubles: biased exponent = hi >> 20; zero -> excluded)
+      int pe = -(1 << 20);
+#pragma unroll
+      for (int k = 0; k < SPL; ++k)
+        pe = max(pe, (oh[k] && ph[k]) ? (oh[k] >> 20) + (ph[k] >> 20) : -(1 << 20));
+      const bool alive = pe > 0 && eo > kNegExp / 2 && ep > kNegExp / 2;
+      const int es = alive ? eo + ep + pe - 2046 : kNegExp;
       const int estar = warp_max(es);
-      const double sc = es > kNegExp / 2 ? pow2d_fast(eo + ep - estar) : 0.0;
+      const double sc = alive ? pow2d_fast(max(eo + ep - estar, -1100)) : 0.0;
       float zl = 0.f, zb = 0.f;
 #pragma unroll
-      for (int kk = 0; kk < SPL; ++kk) {
-        const float p = (float)(own[kk] * oth[kk] * sc);
-        myp[lane * SPL + kk] = p;
+      for (int k = 0; k < SPL; ++k) {
+        const float p = (float)(from_hi(oh[k]) * from_hi(ph[k]) * sc);
+        myp[lane * SPL + k] = p;
         zl += p;
-        if ((kk & 1) == 0) zb += p;   // even states are blanks (SPL is even)
+        if ((k & 1) == 0) zb += p;   // even states are blanks (SPL is even)
       }
       const float z = warp_sum(zl);
       const float zblank = warp_sum(zb);
@@ -625,22 +699,25 @@ __device__ void ctc_helper(CtcSmem<SPL> &sm, int chain, int h, int lane, const C
       __syncwarp();
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[chain][ring]);
+    if (lane == 0) {
+      __threadfence_block();
+      sm.consumed[hid] = i + 1;   // releases ring slot q back to the chain
+    }
+    prefetch(q + 2 * H, buf);
   }
   if (lane == 0) {
     sm.gmin[hid] = gmin;
     sm.gmax[hid] = gmax;
   }
-  (void)lab;
-  (void)L;
 }
 
 template <int SPL>
-__global__ void __launch_bounds__(kFusedWarps * 32)
+__global__ void __launch_bounds__(CtcCfg<SPL>::kWarps * 32)
     ctc_fused_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, CtcFastWs w, double *loss, float *grad_em,
                      int32_t *status) {
+  using C = CtcCfg<SPL>;
   extern __shared__ __align__(128) unsigned char dsm[];
   CtcSmem<SPL> &sm = *reinterpret_cast<CtcSmem<SPL> *>(dsm);
   const int b = blockIdx.x, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -656,12 +733,19 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
   const size_t row0 = (size_t)b * d.Tmax;
   const int S = split_row(T);
   for (int i = threadIdx.x; i < L; i += blockDim.x) sm.perm[i] = w.perm[(size_t)b * w.lpad + i];
+  if (threadIdx.x < 2 * C::kHelpers) {
+    sm.consumed[threadIdx.x] = 0;
+    sm.gmin[threadIdx.x] = CUDART_INF;
+    sm.gmax[threadIdx.x] = -CUDART_INF;
+  }
   if (threadIdx.x == 0) {
     for (int c2 = 0; c2 < 2; ++c2)
-      for (int r = 0; r < kRing; ++r) {
-        mbar_init(&sm.full[c2][r], 1);
-        mbar_init(&sm.empty[c2][r], 1);
-      }
+      for (int r = 0; r < C::kRing; ++r) mbar_init(&sm.full[c2][r], 1);
+    for (int hh = 0; hh < 2 * C::kHelpers; ++hh) {
+      mbar_init(&sm.pfbar[hh][0], 1);
+      mbar_init(&sm.pfbar[hh][1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (wid < 2) {
@@ -685,15 +769,15 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     o.met = false;
     o.seq1 = 0;
     o.seq2 = 0;
+#pragma unroll
+    for (int x = 0; x < C::kHelpers; ++x) o.seen[x] = 0;
     if (wid == 0) ctc_alpha_chain<SPL>(sm, c, f, o, S_len);
     else ctc_beta_chain<SPL>(sm, c, f, o, S_len);
     if (lane == 0) bulk_wait_all();
   } else {
     const int hw = wid - 2;
-    int lab[SPL];
-    (void)lab;
-    ctc_helper<SPL>(sm, hw / kHelpers, hw % kHelpers, lane, w, row0, T, S, N, blank, lab,
-                    w.tok_start + b * 33, ge, L);
+    ctc_helper<SPL>(sm, hw / C::kHelpers, hw % C::kHelpers, lane, w, row0, T, S, N, blank,
+                    w.tok_start + b * 33, ge);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -701,16 +785,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
     const double ln2 = 0.6931471805599453;
     bool bad = !(isfinite(zA) && isfinite(zB)) || fabs(zA - zB) > tol;
-    for (int q = 0; q < 2 * kHelpers; ++q) {
+    for (int q = 0; q < 2 * C::kHelpers; ++q) {
       if (sm.gmin[q] <= sm.gmax[q])   // helpers that saw frames
         bad |= !(fabs(sm.gmin[q] * ln2 - zA) <= tol && fabs(sm.gmax[q] * ln2 - zA) <= tol);
     }
     loss[b] = -(zA + sm.shifts);                                 // criterion.py:162
-#ifdef W2L_DEBUG_FUSED
-    if (b < 2)
-      printf("b=%d T=%d S=%d zA=%f zB=%f shifts=%f g0=[%f %f] g1=[%f %f] g2=[%f %f] g3=[%f %f]\n", b, T, S, zA, zB, sm.shifts,
-             sm.gmin[0], sm.gmax[0], sm.gmin[1], sm.gmax[1], sm.gmin[2], sm.gmax[2], sm.gmin[3], sm.gmax[3]);
-#endif
     if (bad) status[b] = kNeedsExact;
   }
 }
@@ -724,8 +803,8 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
   auto k = ctc_fused_kernel<SPL>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<d.B, kFusedWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, blank, d, w, loss, grad_em,
-                                        status);
+  k<<<d.B, CtcCfg<SPL>::kWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, blank, d, w, loss,
+                                                 grad_em, status);
   err = cudaGetLastError();
   trace(tr, s);  // chain (fused chains + gradient)
   trace(tr, s);  // grad (inside the fused kernel)
