@@ -43,7 +43,7 @@ template <int SPL>
 struct CtcState {
   int lab[SPL];
   double sk[SPL], sk2[SPL], v[SPL];
-  int ex;
+  int ex, blank;
 };
 
 // alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])  (:126-134), fp64 lanes
@@ -51,9 +51,11 @@ template <int SPL>
 __device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const double *row, bool renorm,
                                                bool check, float *out, int *oute, int lane,
                                                int t) {
+  // even states are blanks (SPL is even): one shared emission, no skip edge
   double E[SPL];
+  const double Eb = row[f.blank];
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) E[k] = row[f.lab[k]];
+  for (int k = 1; k < SPL; k += 2) E[k] = row[f.lab[k]];
   double nb1 = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
   double nb2 = __shfl_up_sync(0xffffffffu, f.v[SPL - 2], 1);
   int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
@@ -65,10 +67,12 @@ __device__ __forceinline__ void ctc_alpha_step(CtcState<SPL> &f, const double *r
   const double n2 = nb2 * pow2d_fast(min(nbe - f.ex, 1000));
 #pragma unroll
   for (int k = SPL - 1; k >= 2; --k)
-    f.v[k] = E[k] * fma(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1]);
+    f.v[k] = (k & 1) ? E[k] * fma(f.sk[k], f.v[k - 2], f.v[k] + f.v[k - 1])
+                     : Eb * (f.v[k] + f.v[k - 1]);
   const double v1 = E[1] * fma(f.sk[1], n1, f.v[1] + f.v[0]);
-  f.v[0] = E[0] * fma(f.sk[0], n2, f.v[0] + n1);
+  f.v[0] = Eb * (f.v[0] + n1);
   f.v[1] = v1;
+  (void)n2;
   if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
   lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t);
 }
@@ -79,8 +83,9 @@ __device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const double *ro
                                               bool check, float *out, int *oute, int lane,
                                               int t_out) {
   double wv[SPL];
+  const double Eb = row[f.blank];
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) wv[k] = row[f.lab[k]] * f.v[k];
+  for (int k = 0; k < SPL; ++k) wv[k] = ((k & 1) ? row[f.lab[k]] : Eb) * f.v[k];
   double nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
   double nb2 = __shfl_down_sync(0xffffffffu, wv[1], 1);
   int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
@@ -91,8 +96,9 @@ __device__ __forceinline__ void ctc_beta_step(CtcState<SPL> &f, const double *ro
   const double n1 = align_neighbour_d<SPL>(nb1, nbe, wv, f.ex, check);
   const double n2 = nb2 * pow2d_fast(min(nbe - f.ex, 1000));
 #pragma unroll
-  for (int k = 0; k < SPL - 2; ++k) f.v[k] = fma(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]);
-  f.v[SPL - 2] = fma(f.sk2[SPL - 2], n1, wv[SPL - 2] + wv[SPL - 1]);
+  for (int k = 0; k < SPL - 2; ++k)
+    f.v[k] = (k & 1) ? fma(f.sk2[k], wv[k + 2], wv[k] + wv[k + 1]) : wv[k] + wv[k + 1];
+  f.v[SPL - 2] = wv[SPL - 2] + wv[SPL - 1];
   f.v[SPL - 1] = fma(f.sk2[SPL - 1], n2, wv[SPL - 1] + n1);
   if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
   lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t_out);
@@ -342,6 +348,8 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
 // gradient work overlaps the serial recursions (no separate gradient pass).
 template <int SPL>
 struct CtcCfg {
+  static constexpr int kUnroll = 4;                   // rows per unrolled block (I-cache)
+  static constexpr int kRenorm = 4;                   // rows between lane renormalisations
   static constexpr int kSlot = 2;                     // rows per ring slot
   static constexpr int kRing = 4;                     // slots per chain
   static constexpr int kHelpers = SPL <= 24 ? 3 : 2;  // helper warps per chain
@@ -474,7 +482,7 @@ struct Emitter {
 template <int SPL>
 __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL> &f,
                                 Emitter<SPL> &o, int S_len) {
-  constexpr int SLOT = CtcCfg<SPL>::kSlot;
+  constexpr int SLOT = CtcCfg<SPL>::kSlot, UNR = CtcCfg<SPL>::kUnroll, RN = CtcCfg<SPL>::kRenorm;
   const int lane = c.lane, T = c.T, S = o.S;
   const int nch = (T + kChunk - 1) / kChunk;
   double shifts = 0.0;
@@ -488,17 +496,17 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
     if (ch > 0 && rows == kChunk) {
       if (!o.phase2 && t0 >= S) o.enter_phase2(lane);
 #pragma unroll 1
-      for (int g = 0; g < kChunk; g += kUnroll) {
+      for (int g = 0; g < kChunk; g += UNR) {
 #pragma unroll
-        for (int sl = 0; sl < kUnroll / SLOT; ++sl) {
+        for (int sl = 0; sl < UNR / SLOT; ++sl) {
           o.acquire(lane);
           float *rw = o.rows();
           int *re = o.exps();
 #pragma unroll
           for (int q = 0; q < SLOT; ++q) {
-            const int qq = sl * SLOT + q;   // position in the 8-row block
-            ctc_alpha_step<SPL>(f, buf + (g + qq) * kStride, (qq % kRenormD) == 0,
-                                (qq % kRenormD) == 1, rw, re, lane, q);
+            const int qq = sl * SLOT + q;   // position in the unrolled block
+            ctc_alpha_step<SPL>(f, buf + (g + qq) * kStride, (qq % RN) == 0, (qq % RN) == 1, rw,
+                                re, lane, q);
           }
           o.release(t0 + g + sl * SLOT, SLOT, lane);
         }
@@ -517,7 +525,7 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
           lane_renorm_d<SPL>(f.v, f.ex);
           lane_store_hi<SPL>(f.v, f.ex, o.rows(), o.exps(), lane, t % SLOT);
         } else {
-          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % kRenormD) == 0 || t == T - 1, true,
+          ctc_alpha_step<SPL>(f, buf + r * kStride, (t % RN) == 0 || t == T - 1, true,
                               o.rows(), o.exps(), lane, t % SLOT);
         }
         o.end(t, lane);
@@ -548,7 +556,7 @@ __device__ void ctc_alpha_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SP
 template <int SPL>
 __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL> &f,
                                Emitter<SPL> &o, int S_len) {
-  constexpr int SLOT = CtcCfg<SPL>::kSlot;
+  constexpr int SLOT = CtcCfg<SPL>::kSlot, UNR = CtcCfg<SPL>::kUnroll, RN = CtcCfg<SPL>::kRenorm;
   const int lane = c.lane, T = c.T;
   ChainCtx cf = c;
   cf.e = c.e + c.N;   // frame r+1 for row r
@@ -576,17 +584,17 @@ __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL
     if (uniform) {
       if (!o.phase2 && r0 + kChunk <= o.S) o.enter_phase2(lane);
 #pragma unroll 1
-      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll) {
+      for (int g = kChunk - UNR; g >= 0; g -= UNR) {
 #pragma unroll
-        for (int sl = kUnroll / SLOT - 1; sl >= 0; --sl) {
+        for (int sl = UNR / SLOT - 1; sl >= 0; --sl) {
           o.acquire(lane);
           float *rw = o.rows();
           int *re = o.exps();
 #pragma unroll
           for (int q = SLOT - 1; q >= 0; --q) {
-            const int qq = sl * SLOT + q;   // row offset in the 8-row block
-            ctc_beta_step<SPL>(f, buf + (g + qq) * kStride, (qq % kRenormD) == 0,
-                               (qq % kRenormD) == kRenormD - 1, rw, re, lane, q);
+            const int qq = sl * SLOT + q;   // row offset in the unrolled block
+            ctc_beta_step<SPL>(f, buf + (g + qq) * kStride, (qq % RN) == 0, (qq % RN) == RN - 1,
+                               rw, re, lane, q);
           }
           o.release(r0 + g + sl * SLOT, SLOT, lane);
         }
@@ -595,7 +603,7 @@ __device__ void ctc_beta_chain(CtcSmem<SPL> &sm, const ChainCtx &c, CtcState<SPL
       for (int j = rows - 1; j >= 0; --j) {
         const int r = r0 + j;   // produces beta'_r from frame r+1
         o.begin(r, lane);
-        ctc_beta_step<SPL>(f, buf + j * kStride, (r % kRenormD) == 0, true, o.rows(), o.exps(),
+        ctc_beta_step<SPL>(f, buf + j * kStride, (r % RN) == 0, true, o.rows(), o.exps(),
                            lane, r % SLOT);
         o.end(r, lane);
       }
@@ -758,6 +766,7 @@ __global__ void __launch_bounds__(CtcCfg<SPL>::kWarps * 32)
     c.amax = 0.f;
     CtcState<SPL> f;
     ctc_lattice_lane<SPL, double>(y, L, blank, N, lane, f.lab, f.sk, f.sk2);
+    f.blank = blank;
     Emitter<SPL> o;
     o.sm = &sm;
     o.chain = wid;

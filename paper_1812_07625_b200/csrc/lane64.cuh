@@ -38,14 +38,23 @@ __device__ __forceinline__ double tree_max_d(const double (&v)[SPL]) {
   return fmax(m[0], 0.0);
 }
 
+// renormalise a lane block: scale so the largest value lies in [1, 2).  The
+// maximum is taken over the high words as integers (for non-negative doubles
+// the bit pattern is monotonic), which is much cheaper than fp64 compares.
 template <int SPL>
 __device__ __forceinline__ void lane_renorm_d(double (&v)[SPL], int &ex) {
-  const double mx = tree_max_d<SPL>(v);
-  const int kx = exponent_of_d(mx);  // -1023 for mx == 0
+  int m[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) m[k] = __double2hiint(v[k]);
+#pragma unroll
+  for (int w = 1; w < SPL; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < SPL; k += 2 * w) m[k] = max(m[k], m[k + w]);
+  const int kx = ((m[0] >> 20) & 0x7ff) - 1023;   // -1023 for an all-zero block
   const double sc = pow2d_fast(-kx);
 #pragma unroll
   for (int k = 0; k < SPL; ++k) v[k] *= sc;
-  ex = mx > 0.0 ? ex + kx : kNegExp;
+  ex = m[0] > 0 ? ex + kx : kNegExp;
 }
 
 // store the high words of a lane's doubles (lane-major, SPL/2 8-byte stores)
