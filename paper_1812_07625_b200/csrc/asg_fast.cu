@@ -588,13 +588,13 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     f.eb = w.fac_eb[(row0 + t) * 32 + lane];
   };
 
-  // fac alpha at t-1 (values and lane exponent) carried across frames
-  double pa[SPL];
+  // fac alpha at t-1 (high words and lane exponent) carried across frames
+  int pa[SPL];
   int pea = kNegExp;
   float pfa = 0.f;  // fcc alpha_{t-1}[lane]
   int pka = 0;
   if (ta >= 1 && ta < tend) {
-    lane_load_hi<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
+    lane_load_int<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
     pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
     pka = ka_row[ta - 1];
@@ -632,21 +632,22 @@ __global__ void __launch_bounds__(kGradWarps * 32)
         accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
       }
     }
-    // ---- fac node posteriors (:214-217) in fp64 (lane64.cuh); the frame
-    // reference exponent comes from the actual magnitudes (lazy renorm)
-    double va[SPL], vb[SPL];
+    // ---- fac node posteriors (:214-217) from the fp64 high words (lane64.cuh);
+    // the frame reference exponent comes from the actual magnitudes
+    int vah[SPL], vbh[SPL];
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      va[k] = from_hi(__float_as_int(cur.va[k]));
-      vb[k] = from_hi(__float_as_int(cur.vb[k]));
+      vah[k] = __float_as_int(cur.va[k]);
+      vbh[k] = __float_as_int(cur.vb[k]);
     }
-    const int es = lane_pair_exponent_d<SPL>(va, vb, cur.ea, cur.eb);
+    double pd[SPL];
+    const int es = lane_products<SPL>(vah, vbh, cur.ea, cur.eb, pd);
     const int estar = warp_max(es);
-    const double sc = es > kNegExp / 2 ? pow2d_fast(cur.ea + cur.eb - estar) : 0.0;
+    const double sc = pow2d_fast(max(cur.ea + cur.eb - estar, -1100));
     float zl = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      const float p = (float)(va[k] * vb[k] * sc);
+      const float p = (float)(pd[k] * sc);
       myp[lane * SPL + k] = p;
       zl += p;
     }
@@ -672,21 +673,26 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     // 2^127 and the mantissa products are tiny whenever d is large (a
     // posterior is <= 1), so x * 2^d * (1/Z) cannot overflow.
     if (t >= 1) {
-      const double nbv = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
+      // stay/step edge posteriors: (alpha_{t-1} beta'_t) products in fp64 scaled
+      // to the frame reference, then the float weights S|P * Et
+      const int nbh = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
       const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
       const double s_own = pow2d_fast(max(pea + cur.eb - estar, -1100));
       const double s_nb = lane > 0 ? pow2d_fast(max(nbe + cur.eb - estar, -1100)) : 0.0;
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
-        const double ev = (double)mye[tok[k]] * vb[k];
-        accS[k] = fmaf((float)(pa[k] * (double)S[k] * ev * s_own), inv_zc, accS[k]);
-        const double prev = k > 0 ? pa[k - 1] * s_own : nbv * s_nb;
-        accP[k] = fmaf((float)(prev * (double)P[k] * ev), inv_zc, accP[k]);
+        const double bk = hi_to_d(vbh[k]);
+        const float ek = mye[tok[k]] * inv_zc;
+        const float stay = (float)(hi_to_d(pa[k]) * bk * s_own);
+        const float prev = k > 0 ? (float)(hi_to_d(pa[k - 1]) * bk * s_own)
+                                 : (float)(hi_to_d(nbh) * bk * s_nb);
+        accS[k] = fmaf(stay * S[k], ek, accS[k]);
+        accP[k] = fmaf(prev * P[k], ek, accP[k]);
       }
     }
     // carry alpha_t as alpha_{t-1} for the next frame
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) pa[k] = va[k];
+    for (int k = 0; k < SPL; ++k) pa[k] = vah[k];
     pea = cur.ea;
     pfa = cur.fa;
     pka = cur.ka;
@@ -736,13 +742,14 @@ __global__ void __launch_bounds__(kGradWarps * 32)
 // ---------------------------------------------------------- final kernel --
 // per utterance: dA_b = M (.) sum_blocks(fullA partials) - scatter(fac edge
 // sums) (criterion.py:239-246), the loss (:244) and the guard verdict.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     asg_final_kernel(const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
                      AsgFastWs w, double *loss, float *ga_utt, int32_t *status) {
   const int b = blockIdx.x;
   __shared__ float sEdge[2 * 1024];
-  __shared__ float s_red[8];
+  __shared__ float sA[1024];
+  __shared__ float s_red[32];
   __shared__ int s_bad;
   const int N = d.N, NN = N * N;
   if (status[b] != W2L_OK) {
@@ -757,12 +764,25 @@ __global__ void __launch_bounds__(256)
   am = warp_max(am);
   if (lane == 0) s_red[warp] = am;
   if (threadIdx.x == 0) s_bad = 0;
+  // fixed-order sums of the per-frame-block partials; 4 independent
+  // accumulators keep several loads in flight per thread
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
-  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < nb_used; ++q) s += w.part_edge[((size_t)b * w.nblk + q) * 2 * LP + i];
-    sEdge[i] = s;
-  }
+  auto sum_parts = [&](const float *base, size_t stride) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int q = 0;
+    for (; q + 4 <= nb_used; q += 4) {
+      a0 += base[(size_t)q * stride];
+      a1 += base[(size_t)(q + 1) * stride];
+      a2 += base[(size_t)(q + 2) * stride];
+      a3 += base[(size_t)(q + 3) * stride];
+    }
+    for (; q < nb_used; ++q) a0 += base[(size_t)q * stride];
+    return (a0 + a1) + (a2 + a3);
+  };
+  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x)
+    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * 2 * LP + i, 2 * LP);
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+    sA[i] = sum_parts(w.part_fullA + (size_t)b * w.nblk * 1024 + i, 1024);
   __syncthreads();
   float amax = s_red[0];
   for (int q = 1; q < (int)(blockDim.x >> 5); ++q) amax = fmaxf(amax, s_red[q]);
@@ -770,9 +790,7 @@ __global__ void __launch_bounds__(256)
   const int *ts = w.tok_start + b * 33;
   for (int p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = p / N, j = p % N;
-    float s = 0.f;
-    for (int q = 0; q < nb_used; ++q) s += w.part_fullA[((size_t)b * w.nblk + q) * 1024 + i * 32 + j];
-    const float full = s * expf(trans[p] - amax);
+    const float full = sA[i * 32 + j] * expf(trans[p] - amax);
     float con = 0.f;  // states labelled i: stay edges (i,i), step edges (i, y_{l-1})
     for (int q = ts[i]; q < ts[i + 1]; ++q) {
       const int l = perm[q];
@@ -892,7 +910,7 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
   }
   if (err != cudaSuccess) return err;
   trace(tr, s);  // grad
-  asg_final_kernel<<<d.B, 256, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status);
+  asg_final_kernel<<<d.B, 1024, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status);
   err = cudaGetLastError();
   trace(tr, s);  // final
   return err;

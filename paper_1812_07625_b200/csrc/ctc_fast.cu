@@ -274,21 +274,22 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float *myp = prow[warp];
   const int tend = min(tb, T);
   for (int t = ta; t < tend; ++t) {
-    double va[SPL], vb[SPL];   // high words of fp64 lane values (lane64.cuh)
-    lane_load_hi<SPL>(va, w.a + (row0 + t) * LP, lane);
-    lane_load_hi<SPL>(vb, w.b + (row0 + t) * LP, lane);
+    int va[SPL], vb[SPL];   // high words of fp64 lane values (lane64.cuh)
+    lane_load_int<SPL>(va, w.a + (row0 + t) * LP, lane);
+    lane_load_int<SPL>(vb, w.b + (row0 + t) * LP, lane);
     const int ea = w.ea[(row0 + t) * 32 + lane];
     const int eb = w.eb[(row0 + t) * 32 + lane];
-    const int es = lane_pair_exponent_d<SPL>(va, vb, ea, eb);
+    double pd[SPL];
+    const int es = lane_products<SPL>(va, vb, ea, eb, pd);
     const int estar = warp_max(es);
-    const double sc = es > kNegExp / 2 ? pow2d_fast(ea + eb - estar) : 0.0;
+    const double sc = pow2d_fast(max(ea + eb - estar, -1100));
     float zl = 0.f, zb = 0.f;
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
-      const float p = (float)(va[k] * vb[k] * sc);
+      const float p = (float)(pd[k] * sc);
       myp[lane * SPL + k] = p;
       zl += p;
-      if (((lane * SPL + k) & 1) == 0) zb += p;   // blank states
+      if ((k & 1) == 0) zb += p;   // blank states (SPL is even)
     }
     const float z = warp_sum(zl);
     const float zblank = warp_sum(zb);

@@ -117,6 +117,37 @@ __device__ __forceinline__ int lane_pair_exponent_d(const double (&a)[SPL],
   return ea + eb + exponent_of_d(m);
 }
 
+// raw high words of a stored row (lane-major)
+template <int SPL>
+__device__ __forceinline__ void lane_load_int(int (&v)[SPL], const float *row, int lane) {
+  const int2 *o = reinterpret_cast<const int2 *>(row + lane * SPL);
+#pragma unroll
+  for (int k = 0; k < SPL / 2; ++k) {
+    const int2 x = o[k];
+    v[2 * k] = x.x;
+    v[2 * k + 1] = x.y;
+  }
+}
+
+__device__ __forceinline__ double hi_to_d(int hi) { return __hiloint2double(hi, 0); }
+
+// alpha*beta products of a lane's states from stored high words (truncated,
+// relative error < 2^-19) and the exponent of the lane's largest product plus
+// the lane exponents (kNegExp if either side is dead or all-zero); the
+// largest product is found on the products' high words as integers
+template <int SPL>
+__device__ __forceinline__ int lane_products(const int (&ah)[SPL], const int (&bh)[SPL], int ea,
+                                             int eb, double (&p)[SPL]) {
+  int m = 0;
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    p[k] = hi_to_d(ah[k]) * hi_to_d(bh[k]);
+    m = max(m, __double2hiint(p[k]));
+  }
+  return (m > 0 && ea > kNegExp / 2 && eb > kNegExp / 2) ? ea + eb + ((m >> 20) & 0x7ff) - 1023
+                                                          : kNegExp;
+}
+
 // chunk conversion to double Et rows (the float staging holds raw emissions;
 // values are the float Et of stage_convert, widened exactly)
 __device__ __forceinline__ void stage_convert_d(const float *raw, double *dbuf, const ChainCtx &c,
