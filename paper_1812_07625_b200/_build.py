@@ -23,6 +23,8 @@ LIB = os.path.join(LIBDIR, "libw2l_criterion.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
+# debug-only extra flags (e.g. -DW2L_PROF for the chain cycle profile)
+FLAGS += os.environ.get("W2L_EXTRA_NVCC_FLAGS", "").split()
 SOURCES = ["validate.cu", "viterbi.cu", "exact.cu", "asg_fast.cu", "ctc_fast.cu", "probe.cu",
            "capi.cu"]
 

@@ -8,16 +8,15 @@
 // with exact power-of-two rescaling (only integer exponents accumulate, no
 // rounding in the scale factors).  The fcc (fully connected, N x N) graph is
 // a 32-lane mat-vec per frame with the previous vector broadcast through
-// shared memory; the fac (forced alignment, L-state chain) graph keeps SPL
-// states per lane in registers with a per-lane power-of-two exponent
-// (block floating point) and a single shuffle per frame to the neighbour.
-// No transcendental sits on the recursion's critical path.
+// shared memory; the fac (forced alignment, L-state chain) graph is a
+// multi-warp wavefront lattice (lattice.cuh): 4 states per lane in fp64 with
+// one power-of-two exponent per lane.  No transcendental sits on the
+// recursion's critical path.
 //
 // Kernels (one stream, in order):
-//   asg_csr      per utterance: states grouped by token (for the emissions
-//                gradient scatter), written to the workspace.
-//   asg_chain    grid (B, 4): fcc-alpha, fcc-beta, fac-alpha, fac-beta; one
-//                warp each; rows of alpha/beta and exponents to workspace.
+//   asg_chain    grid (B, 2 directions), one CTA per (utterance, direction):
+//                producer warp (Et ring), fcc warp, W fac lattice warps;
+//                rows of alpha/beta and exponents to the workspace.
 //   asg_grad     grid (frame blocks, B): 8 warps, one frame per warp at a time:
 //                posteriors (per-frame normaliser Z_t), grad_e, partial
 //                transition gradients, and the consistency guard G_t.
@@ -27,7 +26,7 @@
 // posteriors = :214-224, fcc = :227-241, combine = :243-247.
 
 #include "chunk.cuh"
-#include "lane64.cuh"
+#include "lattice.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -43,23 +42,7 @@ __device__ __forceinline__ float trans_max(const float *trans, int N) {
   return warp_max(m);
 }
 
-// ---------------------------------------------------------- chain kernel --
-// One warp per (utterance, role).  Loops are chunk-major: a chunk of kChunk
-// frames is staged (cp.async, one chunk in flight) and converted to Et once;
-// full chunks are then walked in fully unrolled blocks of kUnroll frames, so
-// every shared-memory row offset, store offset, buffer parity and
-// renormalisation decision is a compile-time constant (no per-frame address
-// arithmetic or branches on the critical path).  The first/last partial
-// chunks take a generic per-frame path.
-// Rescaling is lazy and exact (powers of two):
-//   fcc: the exponent of sum(vector read this step) arrives through a spare
-//        lane (row of ones in M) after the step's own scale is chosen; the
-//        scale is predicted from the last two observed log-masses
-//        (LaggedScale) -- off the critical path (for N = 32 every lane sums);
-//   fac: each lane renormalises its block every kRenorm frames.
-// Growth between rescales is bounded; whatever the bounds cannot cover (huge
-// transition ranges, emissions that underflow) trips the guard.
-
+// ---------------------------------------------------------- fcc steps --
 // Power-of-two scale for a recursion whose vector sum is only known one
 // step late.  At step t the exponent e_{t-1} of the vector consumed by step t
 // becomes available after step t's own scale k_t is chosen, so k_t is
@@ -73,9 +56,7 @@ struct LaggedScale {
   int X2 = 0, X3 = 0, seen = 0;  // log-masses of the last two observed vectors
   int pending_K = 0;             // K of the vector whose exponent arrives next
   __device__ __forceinline__ int next() {
-    int Kt = K1;
-    if (seen >= 2) Kt = X2 + (X2 - X3);
-    else if (seen == 1) Kt = X2;
+    const int Kt = seen >= 2 ? X2 + (X2 - X3) : (seen == 1 ? X2 : K1);
     const int k = max(-120, min(120, Kt - K1));
     pending_K = K1;
     K1 += k;
@@ -124,16 +105,16 @@ struct FccState {
 };
 
 // fcc alpha step t (criterion.py:230): alpha_t = Et (.) (M alpha_{t-1}) 2^-k
-__device__ __forceinline__ void fcc_alpha_step(FccState &f, const float *row, float (*vec)[32],
+__device__ __forceinline__ void fcc_alpha_step(FccState &f, float et, float (*vec)[32],
                                                int par, float *out_row, int *outk_t, int lane,
                                                int N) {
-  const float et = row[lane];
   __syncwarp();
   int e1;
-  const float s = fcc_matvec(f.m, vec[par ^ 1], f.spare, N, e1);
   const int k = f.sc.next();
+  const float sc = et * pow2f_fast(-k);   // |k| <= 120: exact
+  const float s = fcc_matvec(f.m, vec[par ^ 1], f.spare, N, e1);
   f.K += k;
-  f.v = et * (s * pow2f(-k));
+  f.v = s * sc;
   f.sc.observe(e1);
   vec[par][lane] = f.v;
   out_row[lane] = f.v;
@@ -141,353 +122,191 @@ __device__ __forceinline__ void fcc_alpha_step(FccState &f, const float *row, fl
 }
 
 // fcc beta' step consuming frame u (criterion.py:236): beta'_{u-1} = M^T (Et_u beta'_u) 2^-k
-__device__ __forceinline__ void fcc_beta_step(FccState &f, const float *row, float (*vec)[32],
+__device__ __forceinline__ void fcc_beta_step(FccState &f, float et, float (*vec)[32],
                                               int par, float *out_row, int *outk_t, int lane,
                                               int N) {
-  vec[par][lane] = row[lane] * f.v;
+  vec[par][lane] = et * f.v;
   __syncwarp();
   int e1;
-  const float s = fcc_matvec(f.m, vec[par], f.spare, N, e1);
   const int k = f.sc.next();
+  const float sc = lane < N ? pow2f_fast(-k) : 0.f;
+  const float s = fcc_matvec(f.m, vec[par], f.spare, N, e1);
   f.K += k;
-  f.v = lane < N ? s * pow2f(-k) : 0.f;
+  f.v = s * sc;
   f.sc.observe(e1);
   out_row[lane] = f.v;
   if (lane == 0) *outk_t = f.K;
 }
 
-__device__ __forceinline__ void fcc_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                          float (*vec)[32], RowStage<32, 1> &st, float *out,
-                                          int *outk, double *lnz) {
-  int gi = 0;
-  const int lane = c.lane, N = c.N, T = c.T;
-  FccState f;
-  f.spare = N < 32;
-#pragma unroll
-  for (int j = 0; j < 32; ++j)
-    f.m[j] = (lane < N && j < N) ? expf(c.trans[lane * N + j] - c.amax)
-                                 : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
-  f.K = 0;
-  const int nch = (T + kChunk - 1) / kChunk;
-  stage_issue(chunk[0], c, 0);
-  for (int ch = 0; ch < nch; ++ch) {
-    float *buf = chunk[ch & 1];
-    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert(buf, c, rows);
-    if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
-    if (ch > 0 && rows == kChunk) {
-#pragma unroll 1
-      for (int g = 0; g < kChunk; g += kUnroll, ++gi) {
-        const int tb = t0 + g;   // multiple of kUnroll: parities are static
-        const int slot = gi & 1;
-        stage_acquire(gi, lane);
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q)
-          fcc_alpha_step(f, buf + (g + q) * kStride, vec, q & 1, st.v[slot] + q * 32,
-                         st.e[slot] + q, lane, N);
-        stage_release(st, slot, out + tb * 32, outk + tb, lane);
-      }
-    } else {
-      int r = 0;
-      if (ch == 0) {
-        f.v = buf[lane];               // alpha_0 = Et_0 (criterion.py:228)
-        vec[0][lane] = f.v;
-        out[lane] = f.v;
-        if (lane == 0) outk[0] = 0;
-        r = 1;
-      }
-      for (; r < rows; ++r) {
-        const int t = t0 + r;
-        fcc_alpha_step(f, buf + r * kStride, vec, t & 1, out + t * 32, outk + t, lane, N);
-      }
-    }
-  }
-  stage_drain(lane);
-  const float z = warp_sum(lane < N ? f.v : 0.f);
-  if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
-}
-
-__device__ __forceinline__ void fcc_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                         float (*vec)[32], RowStage<32, 1> &st, float *out,
-                                         int *outk, double *lnz) {
-  int gi = 0;
-  const int lane = c.lane, N = c.N, T = c.T;
-  FccState f;
-  f.spare = N < 32;
-#pragma unroll
-  for (int i = 0; i < 32; ++i)
-    f.m[i] = (lane < N && i < N) ? expf(c.trans[i * N + lane] - c.amax)
-                                 : ((f.spare && lane == N && i < N) ? 1.f : 0.f);
-  f.K = 0;
-  f.v = lane < N ? 1.f : 0.f;
-  out[(T - 1) * 32 + lane] = f.v;
-  if (lane == 0) outk[T - 1] = 0;
-  const int nch = (T + kChunk - 1) / kChunk;
-  stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
-  float e0 = 0.f;
-  for (int ch = nch - 1; ch >= 0; --ch) {
-    float *buf = chunk[ch & 1];
-    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert(buf, c, rows);
-    if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
-    if (ch > 0 && rows == kChunk) {
-#pragma unroll 1
-      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll, ++gi) {
-        const int ub = t0 + g;
-        const int slot = gi & 1;
-        stage_acquire(gi, lane);
-#pragma unroll
-        for (int q = kUnroll - 1; q >= 0; --q)
-          fcc_beta_step(f, buf + (g + q) * kStride, vec, q & 1, st.v[slot] + q * 32,
-                        st.e[slot] + q, lane, N);
-        stage_release(st, slot, out + (ub - 1) * 32, outk + ub - 1, lane);
-      }
-    } else {
-      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
-        const int u = t0 + r;   // consumes frame u, produces beta'_{u-1}
-        fcc_beta_step(f, buf + r * kStride, vec, u & 1, out + (u - 1) * 32, outk + u - 1,
-                      lane, N);
-      }
-    }
-    if (ch == 0) e0 = buf[lane];
-  }
-  stage_drain(lane);
-  const float z = warp_sum(e0 * f.v);
-  if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
-}
-
-// fac chain weights for this lane's states l = lane*SPL + k: token, stay
-// weight M[y_l][y_l] and the step weight (alpha: INTO l from l-1; beta: from
-// l INTO l+1).  Padding states read the zero emission column N.
-template <int SPL>
-__device__ __forceinline__ void fac_weights(const ChainCtx &c, const int64_t *y, int L,
-                                            bool is_alpha, int (&tok)[SPL], double (&S)[SPL],
-                                            double (&P)[SPL]) {
-  const int N = c.N;
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) {
-    const int l = c.lane * SPL + k;
-    if (l < L) {
-      const int yl = (int)y[l];
-      tok[k] = yl;
-      S[k] = (double)expf(c.trans[yl * N + yl] - c.amax);
-      if (is_alpha)
-        P[k] = l > 0 ? (double)expf(c.trans[yl * N + (int)y[l - 1]] - c.amax) : 0.0;
-      else
-        P[k] = l + 1 < L ? (double)expf(c.trans[(int)y[l + 1] * N + yl] - c.amax) : 0.0;
-    } else {
-      tok[k] = N;
-      S[k] = 0.0;
-      P[k] = 0.0;
-    }
-  }
-}
-
-template <int SPL>
-struct FacState {
-  int tok[SPL];
-  double S[SPL], P[SPL], v[SPL];
-  int ex;
+struct FccCtx {
+  const float *trans;
+  float amax;
+  int N, T, lane, cons_idx;
+  float *rows;  // [Tmax][32] this utterance
+  int *ks;      // cumulative exponents, indexed by frame
 };
 
-// fac alpha step t (criterion.py:197-202), fp64 lane block
-template <int SPL>
-__device__ __forceinline__ void fac_alpha_step(FacState<SPL> &f, const double *row, bool renorm,
-                                               bool check, float *out, int *oute, int lane,
-                                               int t) {
-  double E[SPL];
+// fcc recursion over the shared Et ring (criterion.py:227-236); the same
+// step schedule as the lattice warps (lattice.cuh)
+template <bool FWD>
+__device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
+  PROF_T0();
+  const int lane = c.lane, N = c.N, T = c.T;
+  FccState f;
+  f.spare = N < 32;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) E[k] = row[f.tok[k]];
-  double nb = __shfl_up_sync(0xffffffffu, f.v[SPL - 1], 1);
-  int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
-  if (lane == 0) {
-    nb = 0.0;
-    nbe = kNegExp;
+  for (int j = 0; j < 32; ++j) {
+    // forward: row `lane` of M; backward: column `lane`; lane N of a spare
+    // lane is a row of ones (its product is the sum of the vector)
+    const int p = FWD ? lane * N + j : j * N + lane;
+    f.m[j] = (lane < N && j < N) ? expf(c.trans[p] - c.amax)
+                                 : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
   }
-  const double nbs = align_neighbour_d<SPL>(nb, nbe, f.v, f.ex, check);
-#pragma unroll
-  for (int k = SPL - 1; k >= 1; --k) f.v[k] = E[k] * fma(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
-  f.v[0] = E[0] * fma(f.S[0], f.v[0], f.P[0] * nbs);
-  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
-  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t);
-}
-
-// fac beta' step consuming frame u (criterion.py:207-212)
-template <int SPL>
-__device__ __forceinline__ void fac_beta_step(FacState<SPL> &f, const double *row, bool renorm,
-                                              bool check, float *out, int *oute, int lane,
-                                              int t_out) {
-  double wv[SPL];
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) wv[k] = row[f.tok[k]] * f.v[k];
-  double nb = __shfl_down_sync(0xffffffffu, wv[0], 1);
-  int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
-  if (lane == 31) {
-    nb = 0.0;
-    nbe = kNegExp;
+  f.K = 0;
+  int *mycons = &sm.cons[c.cons_idx];
+  if (FWD) {
+    wait_ge(&sm.prod, 1);
+    f.v = sm.ering[ring_slot(true, 0)][lane];   // alpha_0 = Et_0 (criterion.py:228)
+    sm.vec[0][lane] = f.v;
+    c.rows[lane] = f.v;
+    if (lane == 0) c.ks[0] = 0;
+  } else {
+    f.v = lane < N ? 1.f : 0.f;
+    c.rows[(size_t)(T - 1) * 32 + lane] = f.v;
+    if (lane == 0) c.ks[T - 1] = 0;
   }
-  const double nbs = align_neighbour_d<SPL>(nb, nbe, wv, f.ex, check);
-#pragma unroll
-  for (int k = 0; k < SPL - 1; ++k) f.v[k] = fma(f.S[k], wv[k], f.P[k] * wv[k + 1]);
-  f.v[SPL - 1] = fma(f.S[SPL - 1], wv[SPL - 1], f.P[SPL - 1] * nbs);
-  if (renorm) lane_renorm_d<SPL>(f.v, f.ex);
-  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, t_out);
-}
-
-template <int SPL>
-__device__ __forceinline__ void fac_alpha(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                          double (*dchunk)[kChunk * kStride],
-                                          RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
-                                          float *out, int *oute, double *lnz) {
-  int gi = 0;
-  const int lane = c.lane, T = c.T;
-  FacState<SPL> f;
-  fac_weights<SPL>(c, y, L, true, f.tok, f.S, f.P);
-  f.ex = 0;
-  const int nch = (T + kChunk - 1) / kChunk;
-  stage_issue(chunk[0], c, 0);
-  for (int ch = 0; ch < nch; ++ch) {
-    const double *buf = dchunk[ch & 1];
-    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows);
-    if (ch + 1 < nch) stage_issue(chunk[(ch + 1) & 1], c, t0 + kChunk);
-    if (ch > 0 && rows == kChunk) {
+  publish(mycons, 1, lane);
+  auto generic = [&](int j) {
+    wait_ge(&sm.prod, eidx_of(FWD, j) + 1);
+    const float et = sm.ering[j & (kRing - 1)][lane];
+    const int t = frame_of(FWD, T, j);
+    if (FWD)
+      fcc_alpha_step(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+    else
+      fcc_beta_step(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+    publish(mycons, j + 1, lane);
+  };
+  const int pro_end = min(T, kUnroll);
+  for (int j = 1; j < pro_end; ++j) generic(j);
+  const int nfull = T > kUnroll ? (T - kUnroll) / kUnroll : 0;
 #pragma unroll 1
-      for (int g = 0; g < kChunk; g += kUnroll, ++gi) {
-        const int tb = t0 + g;
-        const int slot = gi & 1;
-        stage_acquire(gi, lane);
+  for (int m = 1; m <= nfull; ++m) {
+    const int j0 = m * kUnroll;
+    PROF_STEADY(m >= 40 && m < 160);
+    PROF_WAIT(1, wait3(&sm.prod, eidx_of(FWD, j0 + kUnroll - 1) + 1, &sm.prod, 0, &sm.prod, 0));
+    const float *eb = sm.ering[j0 & (kRing - 1)];
+    const int tb = frame_of(FWD, T, j0);
+    float *sv = c.rows + (size_t)tb * 32;
+    float etq[kUnroll];
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q)
-          fac_alpha_step<SPL>(f, buf + (g + q) * kStride, (q % kRenormD) == 0,
-                              (q % kRenormD) == 1, st.v[slot], st.e[slot], lane, q);
-        stage_release(st, slot, out + (size_t)tb * (SPL * 32), oute + tb * 32, lane);
-      }
-    } else {
-      int r = 0;
-      if (ch == 0) {   // t = 0: only the first target state is reachable (:194)
+    for (int q = 0; q < kUnroll; ++q) etq[q] = eb[q * kStride + lane];
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) f.v[k] = 0.0;
-        if (lane == 0) f.v[0] = buf[f.tok[0]];
-        lane_renorm_d<SPL>(f.v, f.ex);
-        lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, 0);
-        r = 1;
-      }
-      for (; r < rows; ++r) {
-        const int t = t0 + r;
-        fac_alpha_step<SPL>(f, buf + r * kStride, (t % kRenormD) == 0 || t == T - 1, true, out,
-                            oute, lane, t);
-      }
+    for (int q = 0; q < kUnroll; ++q) {
+      const int dq = FWD ? q : -q;
+      if (FWD)
+        fcc_alpha_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+      else
+        fcc_beta_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
     }
+    publish(mycons, j0 + kUnroll, lane);
   }
-  stage_drain(lane);
-  // fac score = alpha_{T-1}[L-1] (:203)
-  const int lastl = L - 1;
-  double vl = 0.0;
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) vl = (lane * SPL + k == lastl) ? f.v[k] : vl;
-  if (lane == lastl / SPL) *lnz = log(vl) + (double)f.ex * 0.6931471805599453;
+  for (int j = max(pro_end, (nfull + 1) * kUnroll); j < T; ++j) generic(j);
+  publish(mycons, kDone, lane);
+  if (lane == 0) PROF_ADD(0, clock64() - _pt0);
+  float z;
+  if (FWD) {
+    z = warp_sum(lane < N ? f.v : 0.f);
+  } else {
+    const float e0 = sm.ering[ring_slot(false, T - 1)][lane];   // frame 0
+    z = warp_sum(e0 * f.v);
+  }
+  if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
-template <int SPL>
-__device__ __forceinline__ void fac_beta(const ChainCtx &c, float (*chunk)[kChunk * kStride],
-                                         double (*dchunk)[kChunk * kStride],
-                                         RowStage<SPL * 32, 32> &st, const int64_t *y, int L,
-                                         float *out, int *oute, double *lnz) {
-  int gi = 0;
-  const int lane = c.lane, T = c.T;
-  FacState<SPL> f;
-  fac_weights<SPL>(c, y, L, false, f.tok, f.S, f.P);
-  const int lastl = L - 1;
-#pragma unroll
-  for (int k = 0; k < SPL; ++k) f.v[k] = (lane * SPL + k == lastl) ? 1.0 : 0.0;
-  f.ex = (lane == lastl / SPL) ? 0 : kNegExp;
-  lane_store_hi<SPL>(f.v, f.ex, out, oute, lane, T - 1);
-  const int nch = (T + kChunk - 1) / kChunk;
-  stage_issue(chunk[(nch - 1) & 1], c, (nch - 1) * kChunk);
-  double e0 = 0.0;
-  for (int ch = nch - 1; ch >= 0; --ch) {
-    const double *buf = dchunk[ch & 1];
-    const int t0 = ch * kChunk, rows = min(kChunk, T - t0);
-    stage_convert_d(chunk[ch & 1], dchunk[ch & 1], c, rows);
-    if (ch > 0) stage_issue(chunk[(ch - 1) & 1], c, t0 - kChunk);
-    if (ch > 0 && rows == kChunk) {
-#pragma unroll 1
-      for (int g = kChunk - kUnroll; g >= 0; g -= kUnroll, ++gi) {
-        const int ub = t0 + g;   // frames ub .. ub+7 produce beta' at ub-1 .. ub+6
-        const int slot = gi & 1;
-        stage_acquire(gi, lane);
-#pragma unroll
-        for (int q = kUnroll - 1; q >= 0; --q)
-          fac_beta_step<SPL>(f, buf + (g + q) * kStride, ((q + kUnroll - 1) % kRenormD) == 0,
-                             (q % kRenormD) == 0, st.v[slot], st.e[slot], lane, q);
-        stage_release(st, slot, out + (size_t)(ub - 1) * (SPL * 32), oute + (ub - 1) * 32, lane);
-      }
-    } else {
-      for (int r = rows - 1; r >= (ch == 0 ? 1 : 0); --r) {
-        const int u = t0 + r;
-        fac_beta_step<SPL>(f, buf + r * kStride, ((u - 1) % kRenormD) == 0 || u == 1, true,
-                           out, oute, lane, u - 1);
-      }
-    }
-    if (ch == 0) e0 = buf[f.tok[0]];
+template <bool FWD>
+__device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, int W,
+                                               const float *em, int T, int L,
+                                               const int64_t *y, const float *trans, Dims d,
+                                               const AsgFastWs &w, int b) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float amax = trans_max(trans, d.N);
+  const int weff = lat_warps(L);
+  if (warp == 0) {
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W};
+    producer_run(sm, pc, lane, nullptr);
+  } else if (warp == 1) {
+    FccCtx fc;
+    fc.trans = trans;
+    fc.amax = amax;
+    fc.N = d.N;
+    fc.T = T;
+    fc.lane = lane;
+    fc.cons_idx = 0;
+    fc.rows = (FWD ? w.fcc_a : w.fcc_b) + (size_t)b * d.Tmax * 32;
+    fc.ks = FWD ? w.fcc_ka + (size_t)b * w.tpad : w.fcc_kb + (size_t)b * w.tpad + 1;
+    fcc_run<FWD>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
+  } else if (warp - 2 < weff) {
+    LatCtx c;
+    c.w = warp - 2;
+    c.W = weff;
+    c.lane = lane;
+    c.T = T;
+    c.N = d.N;
+    c.nstates = L;
+    c.cons_idx = 1;
+    c.Tmax = d.Tmax;
+    const size_t ub = (size_t)b * w.W * d.Tmax;
+    c.rows = (FWD ? w.fac_a : w.fac_b) + ub * kLatStates;
+    c.exps = (FWD ? w.fac_ea : w.fac_eb) + ub * 32;
+    LatState f;
+    lat_init_weights<kFac, FWD>(f, c, y, L, trans, amax, 0);
+    lattice_run<kFac, FWD>(sm, c, f);
   }
-  stage_drain(lane);
-  if (lane == 0) *lnz = log(e0 * f.v[0]) + (double)f.ex * 0.6931471805599453;
+  __syncthreads();
+  if (threadIdx.x == 0) w.scal[b * 4 + (FWD ? 2 : 3)] = lattice_total(sm, weff);
 }
 
-// One warp per CTA, grid (B, 4 roles): the CTA scheduler spreads the
-// serial recursions over the SMs (measured faster than packing several
-// recursions per SM, which contend for the load/store path).
-template <int SPL>
-__global__ void __launch_bounds__(32)
+// grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
+__global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
                      const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float chunk[2][kChunk * kStride];
-  __shared__ __align__(16) double dchunk[2][kChunk * kStride];
-  __shared__ __align__(16) float vec[2][32];
-  extern __shared__ __align__(128) unsigned char dsm[];  // row staging (dynamic)
-  union Stage {
-    RowStage<32, 1> fcc;
-    RowStage<SPL * 32, 32> fac;
-  };
-  Stage &st = *reinterpret_cast<Stage *>(dsm);
-  const int b = blockIdx.x, role = blockIdx.y;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const int W = w.W;
+  ChainSm &sm = *reinterpret_cast<ChainSm *>(
+      dsm);
+  const int b = blockIdx.x;
   if (status[b] != W2L_OK) return;
-  ChainCtx c;
-  c.trans = trans;
-  c.e = em + (size_t)b * d.Tmax * d.N;
-  c.N = d.N;
-  c.T = em_len[b];
-  c.lane = threadIdx.x & 31;
-  c.amax = trans_max(trans, d.N);
-  const size_t row0 = (size_t)b * d.Tmax;
+  const int T = em_len[b], L = tgt_len[b];
+  const int weff = lat_warps(L);
+  if (threadIdx.x == 0) sm.prod = 0;
+  // counters: 0 = fcc, 1 + w = lattice warp w (absent warps are done)
+  if (threadIdx.x < kCounters) sm.cons[threadIdx.x] = threadIdx.x <= weff ? 0 : kDone;
+  __syncthreads();
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  if (role == 0) {
-    fcc_alpha(c, chunk, vec, st.fcc, w.fcc_a + row0 * 32, w.fcc_ka + (size_t)b * w.tpad,
-              w.scal + b * 4 + 0);
-  } else if (role == 1) {
-    fcc_beta(c, chunk, vec, st.fcc, w.fcc_b + row0 * 32, w.fcc_kb + (size_t)b * w.tpad + 1,
-             w.scal + b * 4 + 1);
-  } else if (role == 2) {
-    fac_alpha<SPL>(c, chunk, dchunk, st.fac, y, tgt_len[b], w.fac_a + row0 * (SPL * 32),
-                   w.fac_ea + row0 * 32, w.scal + b * 4 + 2);
-  } else {
-    fac_beta<SPL>(c, chunk, dchunk, st.fac, y, tgt_len[b], w.fac_b + row0 * (SPL * 32),
-                  w.fac_eb + row0 * 32, w.scal + b * 4 + 3);
-  }
+  if (blockIdx.y == 0)
+    asg_chain_body<true>(sm, dsm, W, em, T, L, y, trans, d, w, b);
+  else
+    asg_chain_body<false>(sm, dsm, W, em, T, L, y, trans, d, w, b);
+}
+
+size_t asg_chain_smem(int W) {
+  (void)W;
+  return sizeof(ChainSm);
 }
 
 // ----------------------------------------------------------- grad kernel --
-template <int SPL>
+// W: fac lattice warps (segments of 128 states).  A warp handles one frame at
+// a time; lane i owns token i of the fcc graph and states
+// 128 w + 4 i + k (w < W, k < 4) of the fac lattice.
+template <int W>
 __global__ void __launch_bounds__(kGradWarps * 32)
     asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     const float *__restrict__ trans, Dims d, AsgFastWs w,
                     float *__restrict__ grad_em, const int32_t *__restrict__ status) {
-  constexpr int LP = SPL * 32;
+  constexpr int LP = W * kLatStates;
   extern __shared__ __align__(16) float gsm[];
   float *red = gsm;                              // [kGradWarps][32*32] fullA partials
   float *redE = red + kGradWarps * 1024;         // [kGradWarps][2][LP] edge partials
@@ -495,6 +314,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
   float *vrow = erow + kGradWarps * 64;          // [kGradWarps][32] alpha_{t-1} fcc row
   float *gwarp = vrow + kGradWarps * 32;         // [kGradWarps][4] guard
+  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 4);   // [LP]
 
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -524,27 +344,29 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   }
 
   const int L = tgt_len[b];
+  const int weff = min(lat_warps(L), W);
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   const float amax = trans_max(trans, N);
-  int tok[SPL];
-  float S[SPL], P[SPL];
+  int tok[W][kSpl];
+  float S[W][kSpl], P[W][kSpl];
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) {
-    const int l = lane * SPL + k;
-    if (l < L) {
-      const int yl = (int)y[l];
-      tok[k] = yl;
-      S[k] = expf(trans[yl * N + yl] - amax);
-      P[k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
-    } else {
-      tok[k] = N;
-      S[k] = 0.f;
-      P[k] = 0.f;
+  for (int sw = 0; sw < W; ++sw)
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) {
+      const int l = sw * kLatStates + lane * kSpl + k;
+      if (l < L) {
+        const int yl = (int)y[l];
+        tok[sw][k] = yl;
+        S[sw][k] = expf(trans[yl * N + yl] - amax);
+        P[sw][k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
+      } else {
+        tok[sw][k] = N;
+        S[sw][k] = 0.f;
+        P[sw][k] = 0.f;
+      }
     }
-  }
   // token CSR of this utterance, staged once per block (the gather reads it
   // every frame)
-  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 4);
   for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
   __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
@@ -553,13 +375,17 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float accA[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) accA[j] = 0.f;
-  float accS[SPL], accP[SPL];
+  float accS[W][kSpl], accP[W][kSpl];
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) accS[k] = accP[k] = 0.f;
-  // guard: deviation (log2 units) of every frame's normaliser from the
-  // forward totals the chain kernel produced
+  for (int sw = 0; sw < W; ++sw)
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) accS[sw][k] = accP[sw][k] = 0.f;
+  // Every frame's normaliser must reproduce the forward totals the chain
+  // kernel produced (the scaled alpha_t * beta_t mass is frame-invariant);
+  // deviations in log2 units feed the guard.
   const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
   const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
+  const int refCi = isfinite(refC) ? (int)floor(refC) : 0;
   float gminF = CUDART_INF_F, gmaxF = -CUDART_INF_F, gminC = CUDART_INF_F,
         gmaxC = -CUDART_INF_F;
 
@@ -567,53 +393,55 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   float *mye = erow + warp * 64;
   float *myv = vrow + warp * 32;
   const size_t row0 = (size_t)b * d.Tmax;
+  const size_t seg0 = (size_t)b * w.W * d.Tmax;   // warp-major lattice rows
   const int *ka_row = w.fcc_ka + (size_t)b * w.tpad;
   const int *kb_row = w.fcc_kb + (size_t)b * w.tpad + 1;
   const int tend = min(tb, T);
-
-  // one frame's inputs; the next frame's are loaded while this one is used
-  struct Frame {   // fac rows hold the high words of fp64 values (lane64.cuh)
-    float e, fa, fb, va[SPL], vb[SPL];
-    int ka, kb, ea, eb;
+  auto arow = [&](int sw, int t) {
+    return reinterpret_cast<const float4 *>(w.fac_a + ((seg0 + (size_t)sw * d.Tmax + t) * kLatStates)) + lane;
   };
-  auto load = [&](Frame &f, int t) {
-    f.e = lane < N ? em[(row0 + t) * N + lane] : -CUDART_INF_F;
-    f.fa = w.fcc_a[(row0 + t) * 32 + lane];
-    f.fb = w.fcc_b[(row0 + t) * 32 + lane];
-    f.ka = ka_row[t];
-    f.kb = kb_row[t];
-    lane_load<SPL>(f.va, w.fac_a + (row0 + t) * LP, lane);
-    lane_load<SPL>(f.vb, w.fac_b + (row0 + t) * LP, lane);
-    f.ea = w.fac_ea[(row0 + t) * 32 + lane];
-    f.eb = w.fac_eb[(row0 + t) * 32 + lane];
+  auto brow = [&](int sw, int t) {
+    return reinterpret_cast<const float4 *>(w.fac_b + ((seg0 + (size_t)sw * d.Tmax + t) * kLatStates)) + lane;
   };
+  auto aexp = [&](int sw, int t) { return w.fac_ea[(seg0 + (size_t)sw * d.Tmax + t) * 32 + lane]; };
+  auto bexp = [&](int sw, int t) { return w.fac_eb[(seg0 + (size_t)sw * d.Tmax + t) * 32 + lane]; };
 
-  // fac alpha at t-1 (high words and lane exponent) carried across frames
-  int pa[SPL];
-  int pea = kNegExp;
   float pfa = 0.f;  // fcc alpha_{t-1}[lane]
   int pka = 0;
   if (ta >= 1 && ta < tend) {
-    lane_load_int<SPL>(pa, w.fac_a + (row0 + ta - 1) * LP, lane);
-    pea = w.fac_ea[(row0 + ta - 1) * 32 + lane];
     pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
     pka = ka_row[ta - 1];
   }
-  Frame cur, nxt;
-  if (ta < tend) load(cur, ta);
 
   for (int t = ta; t < tend; ++t) {
-    if (t + 1 < tend) load(nxt, t + 1);
+    const float e = lane < N ? em[(row0 + t) * N + lane] : -CUDART_INF_F;
+    const float fa = w.fcc_a[(row0 + t) * 32 + lane];
+    const float fb = w.fcc_b[(row0 + t) * 32 + lane];
+    const int ka = ka_row[t], kb = kb_row[t];
+    float4 va[W], vb[W];
+    int ea[W], eb[W];
+#pragma unroll
+    for (int sw = 0; sw < W; ++sw) {
+      if (sw < weff) {
+        va[sw] = *arow(sw, t);
+        vb[sw] = *brow(sw, t);
+        ea[sw] = aexp(sw, t);
+        eb[sw] = bexp(sw, t);
+      } else {
+        va[sw] = vb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ea[sw] = eb[sw] = kNegExp;
+      }
+    }
     // ---- emissions of frame t, shifted and exponentiated (same as the chain)
-    const float m = warp_max(cur.e);
-    const float et = lane < N ? expf(cur.e - m) : 0.f;
+    const float m = warp_max(e);
+    const float et = lane < N ? et_of(e, m) : 0.f;
     mye[lane] = et;
     if (lane == 0) mye[32] = 0.f;
     // ---- fcc node posteriors (:238)
-    const float gam = cur.fa * cur.fb;
+    const float gam = fa * fb;
     const float zf = warp_sum(gam);
     const float inv_zf = 1.f / zf;
-    const float gF = (float)((double)__log2f(zf) + (double)(cur.ka + cur.kb) - refF);
+    const float gF = (float)((double)__log2f(zf) + (double)(ka + kb) - refF);
     gminF = fminf(gminF, gF);
     gmaxF = fmaxf(gmaxF, gF);
     const float full_e = gam * inv_zf;
@@ -621,7 +449,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     if (t >= 1) {
       myv[lane] = pfa;
       __syncwarp();
-      const float u = et * cur.fb * pow2f(pka - cur.ka) * inv_zf;
+      const float u = et * fb * pow2f(pka - ka) * inv_zf;
       const float4 *pv = reinterpret_cast<const float4 *>(myv);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -632,28 +460,23 @@ __global__ void __launch_bounds__(kGradWarps * 32)
         accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
       }
     }
-    // ---- fac node posteriors (:214-217) from the fp64 high words (lane64.cuh);
-    // the frame reference exponent comes from the actual magnitudes
-    int vah[SPL], vbh[SPL];
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      vah[k] = __float_as_int(cur.va[k]);
-      vbh[k] = __float_as_int(cur.vb[k]);
-    }
-    double pd[SPL];
-    const int es = lane_products<SPL>(vah, vbh, cur.ea, cur.eb, pd);
-    const int estar = warp_max(es);
-    const double sc = pow2d_fast(max(cur.ea + cur.eb - estar, -1100));
+    // ---- fac node posteriors (:214-217) from the fp64 high words, scaled
+    // by the lane exponents against the utterance reference
     float zl = 0.f;
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      const float p = (float)(pd[k] * sc);
-      myp[lane * SPL + k] = p;
-      zl += p;
+    for (int sw = 0; sw < W; ++sw) {
+      const PostScale sc = post_scale(ea[sw], eb[sw], refCi);
+      float4 p;
+      p.x = post_of(va[sw].x, vb[sw].x, sc);
+      p.y = post_of(va[sw].y, vb[sw].y, sc);
+      p.z = post_of(va[sw].z, vb[sw].z, sc);
+      p.w = post_of(va[sw].w, vb[sw].w, sc);
+      reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
+      zl += (p.x + p.y) + (p.z + p.w);
     }
     const float zc = warp_sum(zl);
     const float inv_zc = 1.f / zc;
-    const float gC = (float)((double)__log2f(zc) + (double)estar - refC);
+    const float gC = (float)((double)__log2f(zc) + (double)refCi - refC);
     gminC = fminf(gminC, gC);
     gmaxC = fmaxf(gmaxC, gC);
     __syncwarp();
@@ -669,34 +492,44 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
     const float con = (c0 + c1) + (c2 + c3);
     if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
-    // ---- fac edge posteriors (:218-224).  The lane scale 2^d is bounded by
-    // 2^127 and the mantissa products are tiny whenever d is large (a
-    // posterior is <= 1), so x * 2^d * (1/Z) cannot overflow.
+    // ---- fac edge posteriors (:218-224): alpha_{t-1} (stay from the same
+    // state, step from the previous one) times beta'_t, weights S|P * Et
     if (t >= 1) {
-      // stay/step edge posteriors: (alpha_{t-1} beta'_t) products in fp64 scaled
-      // to the frame reference, then the float weights S|P * Et
-      const int nbh = __shfl_up_sync(0xffffffffu, pa[SPL - 1], 1);
-      const int nbe = __shfl_up_sync(0xffffffffu, pea, 1);
-      const double s_own = pow2d_fast(max(pea + cur.eb - estar, -1100));
-      const double s_nb = lane > 0 ? pow2d_fast(max(nbe + cur.eb - estar, -1100)) : 0.0;
+      float carry_v = 0.f;                  // state 128 sw - 1 (previous segment)
+      int carry_e = kNegExp;
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) {
-        const double bk = hi_to_d(vbh[k]);
-        const float ek = mye[tok[k]] * inv_zc;
-        const float stay = (float)(hi_to_d(pa[k]) * bk * s_own);
-        const float prev = k > 0 ? (float)(hi_to_d(pa[k - 1]) * bk * s_own)
-                                 : (float)(hi_to_d(nbh) * bk * s_nb);
-        accS[k] = fmaf(stay * S[k], ek, accS[k]);
-        accP[k] = fmaf(prev * P[k], ek, accP[k]);
+      for (int sw = 0; sw < W; ++sw) {
+        if (sw < weff) {
+          const float4 pa = *arow(sw, t - 1);
+          const int pea = aexp(sw, t - 1);
+          float nbv = __shfl_sync(0xffffffffu, pa.w, (lane + 31) & 31);
+          int nbe = __shfl_sync(0xffffffffu, pea, (lane + 31) & 31);
+          const float cv = __shfl_sync(0xffffffffu, pa.w, 31);
+          const int ce = __shfl_sync(0xffffffffu, pea, 31);
+          if (lane == 0) {
+            nbv = carry_v;
+            nbe = carry_e;
+          }
+          carry_v = cv;
+          carry_e = ce;
+          const PostScale s_own = post_scale(pea, eb[sw], refCi);
+          const PostScale s_nb = post_scale(nbe, eb[sw], refCi);
+          const float pav[4] = {pa.x, pa.y, pa.z, pa.w};
+          const float vbv[4] = {vb[sw].x, vb[sw].y, vb[sw].z, vb[sw].w};
+#pragma unroll
+          for (int k = 0; k < kSpl; ++k) {
+            const float ek = mye[tok[sw][k]] * inv_zc;
+            const float stay = post_of(pav[k], vbv[k], s_own);
+            const float prev = k > 0 ? post_of(pav[k - 1], vbv[k], s_own)
+                                     : post_of(nbv, vbv[0], s_nb);
+            accS[sw][k] = fmaf(stay * S[sw][k], ek, accS[sw][k]);
+            accP[sw][k] = fmaf(prev * P[sw][k], ek, accP[sw][k]);
+          }
+        }
       }
     }
-    // carry alpha_t as alpha_{t-1} for the next frame
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) pa[k] = vah[k];
-    pea = cur.ea;
-    pfa = cur.fa;
-    pka = cur.ka;
-    cur = nxt;
+    pfa = fa;
+    pka = ka;
     __syncwarp();
   }
 
@@ -706,10 +539,12 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   for (int j = 0; j < 32; ++j) rA[lane * 32 + j] = accA[j];
   float *rE = redE + warp * 2 * LP;
 #pragma unroll
-  for (int k = 0; k < SPL; ++k) {
-    rE[lane * SPL + k] = accS[k];
-    rE[LP + lane * SPL + k] = accP[k];
-  }
+  for (int sw = 0; sw < W; ++sw)
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) {
+      rE[sw * kLatStates + lane * kSpl + k] = accS[sw][k];
+      rE[LP + sw * kLatStates + lane * kSpl + k] = accP[sw][k];
+    }
   if (lane == 0) {
     gwarp[warp * 4 + 0] = gminF;
     gwarp[warp * 4 + 1] = gmaxF;
@@ -821,23 +656,14 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-template <int SPL>
-cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tgt,
-                       const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
-                       float *grad_em, const int32_t *status, cudaStream_t s, Tracer *tr) {
-  const size_t stage_bytes = sizeof(RowStage<SPL * 32, 32>);
-  auto kc = asg_chain_kernel<SPL>;
-  cudaError_t err0 =
-      cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_bytes);
-  if (err0 != cudaSuccess) return err0;
-  kc<<<dim3(d.B, 4), 32, stage_bytes, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
-  trace(tr, s);  // chain
-  constexpr int LP = SPL * 32;
+template <int W>
+cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
+                          float *grad_em, const int32_t *status, cudaStream_t s) {
+  constexpr int LP = W * kLatStates;
   const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4) + LP);
-  auto k = asg_grad_kernel<SPL>;
-  err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto k = asg_grad_kernel<W>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   k<<<dim3(w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
                                                       grad_em, status);
@@ -846,16 +672,15 @@ cudaError_t launch_spl(const float *em, const int32_t *em_len, const int64_t *tg
 
 }  // namespace
 
-int asg_fast_spl(int Lmax) {
-  static const int opts[] = {2, 4, 8, 10, 12, 16, 20, 24, 32};
-  for (int o : opts)
-    if (32 * o >= Lmax) return o;
-  return 0;
-}
+#ifdef W2L_PROF
+W2L_PROF_READER(w2l_debug_prof_asg)
+#endif
+
+int asg_fast_spl(int Lmax) { return lat_warps(Lmax) <= kMaxLatWarps ? kSpl : 0; }
 
 static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
-  const int spl = asg_fast_spl(d.Lmax);
-  const int lpad = spl * 32;
+  const int W = lat_warps(d.Lmax);
+  const int lpad = W * kLatStates;
   const int nblk = (d.Tmax + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
   const size_t BT = (size_t)d.B * d.Tmax;
   size_t off = 0;
@@ -872,15 +697,16 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   t.fcc_kb = (int *)take((size_t)d.B * tpad * 4);
   t.fac_a = (float *)take(BT * lpad * 4);
   t.fac_b = (float *)take(BT * lpad * 4);
-  t.fac_ea = (int *)take(BT * 32 * 4);
-  t.fac_eb = (int *)take(BT * 32 * 4);
+  t.fac_ea = (int *)take(BT * W * 32 * 4);
+  t.fac_eb = (int *)take(BT * W * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
   t.part_fullA = (float *)take((size_t)d.B * nblk * 1024 * 4);
   t.part_edge = (float *)take((size_t)d.B * nblk * 2 * lpad * 4);
   t.part_guard = (float *)take((size_t)d.B * nblk * 4 * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
-  t.spl = spl;
+  t.spl = kSpl;
+  t.W = W;
   t.lpad = lpad;
   t.nblk = nblk;
   t.tpad = tpad;
@@ -895,17 +721,25 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
                             int32_t *status, cudaStream_t s, Tracer *tr) {
-  cudaError_t err = cudaSuccess;
-  switch (w.spl) {
-    case 2: err = launch_spl<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 4: err = launch_spl<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 8: err = launch_spl<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 10: err = launch_spl<10>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 12: err = launch_spl<12>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 16: err = launch_spl<16>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 20: err = launch_spl<20>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 24: err = launch_spl<24>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
-    case 32: err = launch_spl<32>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s, tr); break;
+  if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
+  const size_t smem = asg_chain_smem(w.W);
+  cudaError_t err =
+      cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d,
+                                                               w, status);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  trace(tr, s);  // chain
+  switch (w.W) {
+    case 1: err = launch_grad_w<1>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 2: err = launch_grad_w<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 3: err = launch_grad_w<3>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 4: err = launch_grad_w<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 5: err = launch_grad_w<5>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 6: err = launch_grad_w<6>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 7: err = launch_grad_w<7>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 8: err = launch_grad_w<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
     default: return cudaErrorInvalidValue;
   }
   if (err != cudaSuccess) return err;

@@ -132,10 +132,29 @@ __device__ __forceinline__ float align_neighbour(float nb, int nbe, float (&v)[S
       ex = nbe;
       dd = 0;
     }
-    return nb * pow2f(dd);
+    return nb * pow2f_fast(dd);
   }
   ex = ex == kNegExp ? nbe : ex;
   return nb * pow2f_fast(min(nbe - ex, 126));
+}
+
+// The same alignment, returning the power-of-two factor for the neighbour's
+// values (it stays valid until the next renormalisation or adoption).
+template <int SPL>
+__device__ __forceinline__ float align_factor(int nbe, float (&v)[SPL], int &ex, bool check) {
+  if (check) {
+    int dd = nbe - ex;
+    if (dd > 64) {
+      const float sc = pow2f_fast(max(-dd, -127));
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) v[k] *= sc;
+      ex = nbe;
+      dd = 0;
+    }
+    return pow2f_fast(dd);
+  }
+  ex = ex == kNegExp ? nbe : ex;
+  return pow2f_fast(min(nbe - ex, 126));
 }
 
 // floor(log2(max_k a[k] b[k])) + ea + eb, a bound on this lane's largest

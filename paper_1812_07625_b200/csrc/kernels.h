@@ -58,15 +58,15 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
 struct AsgFastWs {
   float *fcc_a, *fcc_b;      // [B][Tmax][32]
   int *fcc_ka, *fcc_kb;      // [B][tpad] cumulative exponents (kb stored at t+1)
-  float *fac_a, *fac_b;      // [B][Tmax][SPL*32] slot-major
-  int *fac_ea, *fac_eb;      // [B][Tmax][32] per-lane exponents
+  float *fac_a, *fac_b;      // [B][W][Tmax][128] warp-major lattice rows (fp64 high words)
+  int *fac_ea, *fac_eb;      // [B][W][Tmax][32] per-lane exponents
   double *scal;              // [B][4]: lnZ fcc fwd, fcc bwd, fac fwd, fac bwd
   float *part_fullA;         // [B][nblk][32][32]
   float *part_edge;          // [B][nblk][2][Lpad]
   float *part_guard;         // [B][nblk][4]
   int *perm;                 // [B][Lpad] states sorted by token
   int *tok_start;            // [B][33]
-  int spl, lpad, nblk, tpad;  // tpad = round_up(Tmax + 1, 8): 16B-aligned bulk blocks
+  int spl, W, lpad, nblk, tpad;  // W lattice warps; tpad = round_up(Tmax + 1, 8): 16B-aligned bulk blocks
 };
 int asg_fast_spl(int Lmax);  // 0 if unsupported
 size_t asg_fast_ws_bytes(Dims d);
@@ -77,13 +77,13 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
                             int32_t *status, cudaStream_t s, Tracer *tr = nullptr);
 
 struct CtcFastWs {
-  float *a, *b;              // [B][Tmax][SPL*32]
-  int *ea, *eb;              // [B][Tmax][32]
+  float *a, *b;              // [B][W][Tmax][128] warp-major lattice rows
+  int *ea, *eb;              // [B][W][Tmax][32]
   double *scal;              // [B][4]: lnZ fwd, lnZ bwd, sum of frame shifts, spare
   float *part_guard;         // [B][nblk][2]
   int *perm;                 // [B][Lpad] label positions sorted by token
   int *tok_start;            // [B][33]
-  int spl, lpad, nblk;
+  int spl, W, lpad, nblk;
 };
 int ctc_fast_spl(int Lmax);
 size_t ctc_fast_ws_bytes(Dims d);
