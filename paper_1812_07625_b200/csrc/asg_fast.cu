@@ -297,11 +297,29 @@ size_t asg_chain_smem(int W) {
 }
 
 // ----------------------------------------------------------- grad kernel --
+// packed fp32x2 FMA (FFMA2): d = a * b + c on two lanes of a 64-bit register
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_dup(float x) {
+  const unsigned u = __float_as_uint(x);
+  return ((unsigned long long)u << 32) | u;
+}
+// 2^x as a float for integer x clamped to [-127, 127] (0 below)
+__device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
+
 // W: fac lattice warps (segments of 128 states).  A warp handles one frame at
-// a time; lane i owns token i of the fcc graph and states
-// 128 w + 4 i + k (w < W, k < 4) of the fac lattice.
+// a time (consecutive frames, so alpha_{t-1} is carried in registers); lane i
+// owns token i of the fcc graph and states 128 w + 4 i + k (w < W, k < 4) of
+// the fac lattice.  Posteriors are normalised per frame by their own sums
+// (z_t), scaled into range by the lane exponents against the utterance's
+// reference exponent.  Edge sums are accumulated without their constant
+// transition weights (S, P, M), which are applied once in the epilogue.
 template <int W>
-__global__ void __launch_bounds__(kGradWarps * 32)
+__global__ void __launch_bounds__(kGradWarps * 32, 1)
     asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     const float *__restrict__ trans, Dims d, AsgFastWs w,
@@ -344,139 +362,125 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   }
 
   const int L = tgt_len[b];
-  const int weff = min(lat_warps(L), W);
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  const float amax = trans_max(trans, N);
   int tok[W][kSpl];
-  float S[W][kSpl], P[W][kSpl];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) {
       const int l = sw * kLatStates + lane * kSpl + k;
-      if (l < L) {
-        const int yl = (int)y[l];
-        tok[sw][k] = yl;
-        S[sw][k] = expf(trans[yl * N + yl] - amax);
-        P[sw][k] = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
-      } else {
-        tok[sw][k] = N;
-        S[sw][k] = 0.f;
-        P[sw][k] = 0.f;
-      }
+      tok[sw][k] = l < L ? (int)y[l] : N;
     }
   // token CSR of this utterance, staged once per block (the gather reads it
   // every frame)
   for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
+  float *myp = prow + warp * LP;
+  float *mye = erow + warp * 64;
+  float *myv = vrow + warp * 32;
+  mye[32 + lane] = 0.f;   // column N.. of the Et row: padding states read 0
   __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
 
-  float accA[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) accA[j] = 0.f;
-  float accS[W][kSpl], accP[W][kSpl];
-#pragma unroll
-  for (int sw = 0; sw < W; ++sw)
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) accS[sw][k] = accP[sw][k] = 0.f;
   // Every frame's normaliser must reproduce the forward totals the chain
   // kernel produced (the scaled alpha_t * beta_t mass is frame-invariant);
   // deviations in log2 units feed the guard.
   const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
   const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
+  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
   const int refCi = isfinite(refC) ? (int)floor(refC) : 0;
+  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
+  const float refCf = isfinite(refC) ? (float)(refC - refCi) : CUDART_NAN_F;
   float gminF = CUDART_INF_F, gmaxF = -CUDART_INF_F, gminC = CUDART_INF_F,
         gmaxC = -CUDART_INF_F;
 
-  float *myp = prow + warp * LP;
-  float *mye = erow + warp * 64;
-  float *myv = vrow + warp * 32;
-  const size_t row0 = (size_t)b * d.Tmax;
-  const size_t seg0 = (size_t)b * w.W * d.Tmax;   // warp-major lattice rows
-  const int *ka_row = w.fcc_ka + (size_t)b * w.tpad;
-  const int *kb_row = w.fcc_kb + (size_t)b * w.tpad + 1;
-  const int tend = min(tb, T);
-  auto arow = [&](int sw, int t) {
-    return reinterpret_cast<const float4 *>(w.fac_a + ((seg0 + (size_t)sw * d.Tmax + t) * kLatStates)) + lane;
-  };
-  auto brow = [&](int sw, int t) {
-    return reinterpret_cast<const float4 *>(w.fac_b + ((seg0 + (size_t)sw * d.Tmax + t) * kLatStates)) + lane;
-  };
-  auto aexp = [&](int sw, int t) { return w.fac_ea[(seg0 + (size_t)sw * d.Tmax + t) * 32 + lane]; };
-  auto bexp = [&](int sw, int t) { return w.fac_eb[(seg0 + (size_t)sw * d.Tmax + t) * 32 + lane]; };
+  // per-utterance bases, 32-bit offsets within the utterance
+  const float *emb = em + (size_t)b * d.Tmax * N;
+  const float *fa_r = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
+  const float *fb_r = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
+  const int *ka_r = w.fcc_ka + (size_t)b * w.tpad;
+  const int *kb_r = w.fcc_kb + (size_t)b * w.tpad + 1;
+  const size_t seg0 = (size_t)b * w.W * d.Tmax;
+  const float4 *A4 = reinterpret_cast<const float4 *>(w.fac_a + seg0 * kLatStates) + lane;
+  const float4 *B4 = reinterpret_cast<const float4 *>(w.fac_b + seg0 * kLatStates) + lane;
+  const int *EA = w.fac_ea + seg0 * 32 + lane;
+  const int *EB = w.fac_eb + seg0 * 32 + lane;
+  const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);   // float4 per segment
+  const unsigned sege = (unsigned)d.Tmax * 32;
 
-  float pfa = 0.f;  // fcc alpha_{t-1}[lane]
+  unsigned long long accA[16];   // accA[jj] = (row lane, columns 2jj, 2jj+1)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) accA[j] = 0ull;
+  float accS[W][kSpl], accP[W][kSpl];
+#pragma unroll
+  for (int sw = 0; sw < W; ++sw)
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) accS[sw][k] = accP[sw][k] = 0.f;
+
+  // alpha_{t-1} carried across frames (fcc value/exponent, fac lane blocks)
+  const int tend = min(tb, T);
+  float pfa = 0.f;
   int pka = 0;
+  float4 pa[W];
+  int pea[W];
+#pragma unroll
+  for (int sw = 0; sw < W; ++sw) {
+    pa[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+    pea[sw] = kNegExp;
+  }
   if (ta >= 1 && ta < tend) {
-    pfa = w.fcc_a[(row0 + ta - 1) * 32 + lane];
-    pka = ka_row[ta - 1];
+    pfa = fa_r[(unsigned)(ta - 1) * 32];
+    pka = ka_r[ta - 1];
+#pragma unroll
+    for (int sw = 0; sw < W; ++sw) {
+      pa[sw] = A4[sw * segq + (unsigned)(ta - 1) * 32];
+      pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
+    }
   }
 
   for (int t = ta; t < tend; ++t) {
-    const float e = lane < N ? em[(row0 + t) * N + lane] : -CUDART_INF_F;
-    const float fa = w.fcc_a[(row0 + t) * 32 + lane];
-    const float fb = w.fcc_b[(row0 + t) * 32 + lane];
-    const int ka = ka_row[t], kb = kb_row[t];
+    const unsigned tq = (unsigned)t * 32;
+    const float e = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
+    const float fa = fa_r[tq], fb = fb_r[tq];
+    const int ka = ka_r[t], kb = kb_r[t];
     float4 va[W], vb[W];
     int ea[W], eb[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      if (sw < weff) {
-        va[sw] = *arow(sw, t);
-        vb[sw] = *brow(sw, t);
-        ea[sw] = aexp(sw, t);
-        eb[sw] = bexp(sw, t);
-      } else {
-        va[sw] = vb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ea[sw] = eb[sw] = kNegExp;
-      }
+      va[sw] = A4[sw * segq + tq];
+      vb[sw] = B4[sw * segq + tq];
+      ea[sw] = EA[sw * sege + tq];
+      eb[sw] = EB[sw * sege + tq];
     }
     // ---- emissions of frame t, shifted and exponentiated (same as the chain)
     const float m = warp_max(e);
     const float et = lane < N ? et_of(e, m) : 0.f;
     mye[lane] = et;
-    if (lane == 0) mye[32] = 0.f;
+    myv[lane] = pfa;
     // ---- fcc node posteriors (:238)
     const float gam = fa * fb;
     const float zf = warp_sum(gam);
-    const float inv_zf = 1.f / zf;
-    const float gF = (float)((double)__log2f(zf) + (double)(ka + kb) - refF);
+    const float izf = 1.f / zf;
+    const float gF = __log2f(zf) + (float)(ka + kb - refFi) - refFf;
     gminF = fminf(gminF, gF);
     gmaxF = fmaxf(gmaxF, gF);
-    const float full_e = gam * inv_zf;
-    // ---- fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j], times M later
-    if (t >= 1) {
-      myv[lane] = pfa;
-      __syncwarp();
-      const float u = et * fb * pow2f(pka - ka) * inv_zf;
-      const float4 *pv = reinterpret_cast<const float4 *>(myv);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 x = pv[q];
-        accA[4 * q] = fmaf(u, x.x, accA[4 * q]);
-        accA[4 * q + 1] = fmaf(u, x.y, accA[4 * q + 1]);
-        accA[4 * q + 2] = fmaf(u, x.z, accA[4 * q + 2]);
-        accA[4 * q + 3] = fmaf(u, x.w, accA[4 * q + 3]);
-      }
-    }
-    // ---- fac node posteriors (:214-217) from the fp64 high words, scaled
-    // by the lane exponents against the utterance reference
+    const float full_e = gam * izf;
+    // ---- fac node posteriors (:214-217)
     float zl = 0.f;
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      const PostScale sc = post_scale(ea[sw], eb[sw], refCi);
+      const float sc = pow2_clamped(ea[sw] + eb[sw] - refCi);
       float4 p;
-      p.x = post_of(va[sw].x, vb[sw].x, sc);
-      p.y = post_of(va[sw].y, vb[sw].y, sc);
-      p.z = post_of(va[sw].z, vb[sw].z, sc);
-      p.w = post_of(va[sw].w, vb[sw].w, sc);
+      p.x = va[sw].x * vb[sw].x * sc;
+      p.y = va[sw].y * vb[sw].y * sc;
+      p.z = va[sw].z * vb[sw].z * sc;
+      p.w = va[sw].w * vb[sw].w * sc;
       reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
       zl += (p.x + p.y) + (p.z + p.w);
     }
     const float zc = warp_sum(zl);
-    const float inv_zc = 1.f / zc;
-    const float gC = (float)((double)__log2f(zc) + (double)refCi - refC);
+    const float izc = 1.f / zc;
+    const float gC = __log2f(zc) - refCf;
     gminC = fminf(gminC, gC);
     gmaxC = fmaxf(gmaxC, gC);
     __syncwarp();
@@ -491,59 +495,81 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     }
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
     const float con = (c0 + c1) + (c2 + c3);
-    if (lane < N) ge[(size_t)t * N + lane] = full_e - con * inv_zc;
-    // ---- fac edge posteriors (:218-224): alpha_{t-1} (stay from the same
-    // state, step from the previous one) times beta'_t, weights S|P * Et
+    if (lane < N) ge[(unsigned)t * N + lane] = full_e - con * izc;
     if (t >= 1) {
-      float carry_v = 0.f;                  // state 128 sw - 1 (previous segment)
+      // ---- fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
+      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(pka - ka) * izf);
+      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(myv);
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const ulonglong2 x = pv[qq];
+        accA[2 * qq] = ffma2(u2, x.x, accA[2 * qq]);
+        accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
+      }
+      // ---- fac edge posteriors (:218-224): alpha_{t-1} (stay: same state,
+      // step: previous state) times Et[y] beta'_t (times S|P later)
+      float carry_v = 0.f;   // state 128 sw - 1 (previous segment)
       int carry_e = kNegExp;
 #pragma unroll
       for (int sw = 0; sw < W; ++sw) {
-        if (sw < weff) {
-          const float4 pa = *arow(sw, t - 1);
-          const int pea = aexp(sw, t - 1);
-          float nbv = __shfl_sync(0xffffffffu, pa.w, (lane + 31) & 31);
-          int nbe = __shfl_sync(0xffffffffu, pea, (lane + 31) & 31);
-          const float cv = __shfl_sync(0xffffffffu, pa.w, 31);
-          const int ce = __shfl_sync(0xffffffffu, pea, 31);
-          if (lane == 0) {
-            nbv = carry_v;
-            nbe = carry_e;
-          }
-          carry_v = cv;
-          carry_e = ce;
-          const PostScale s_own = post_scale(pea, eb[sw], refCi);
-          const PostScale s_nb = post_scale(nbe, eb[sw], refCi);
-          const float pav[4] = {pa.x, pa.y, pa.z, pa.w};
-          const float vbv[4] = {vb[sw].x, vb[sw].y, vb[sw].z, vb[sw].w};
+        float nbv = __shfl_sync(0xffffffffu, pa[sw].w, (lane + 31) & 31);
+        int nbe = __shfl_sync(0xffffffffu, pea[sw], (lane + 31) & 31);
+        const float cv = __shfl_sync(0xffffffffu, pa[sw].w, 31);
+        const int ce = __shfl_sync(0xffffffffu, pea[sw], 31);
+        if (lane == 0) {
+          nbv = carry_v;
+          nbe = carry_e;
+        }
+        carry_v = cv;
+        carry_e = ce;
+        const float s_own = pow2_clamped(pea[sw] + eb[sw] - refCi) * izc;
+        const float s_nb = pow2_clamped(nbe + eb[sw] - refCi) * izc;
+        const float pav[4] = {pa[sw].x, pa[sw].y, pa[sw].z, pa[sw].w};
+        const float vbv[4] = {vb[sw].x, vb[sw].y, vb[sw].z, vb[sw].w};
 #pragma unroll
-          for (int k = 0; k < kSpl; ++k) {
-            const float ek = mye[tok[sw][k]] * inv_zc;
-            const float stay = post_of(pav[k], vbv[k], s_own);
-            const float prev = k > 0 ? post_of(pav[k - 1], vbv[k], s_own)
-                                     : post_of(nbv, vbv[0], s_nb);
-            accS[sw][k] = fmaf(stay * S[sw][k], ek, accS[sw][k]);
-            accP[sw][k] = fmaf(prev * P[sw][k], ek, accP[sw][k]);
-          }
+        for (int k = 0; k < kSpl; ++k) {
+          const float qk = vbv[k] * mye[tok[sw][k]];
+          const float qs = qk * s_own;
+          accS[sw][k] = fmaf(pav[k], qs, accS[sw][k]);
+          accP[sw][k] = k > 0 ? fmaf(pav[k - 1], qs, accP[sw][k])
+                              : fmaf(nbv, qk * s_nb, accP[sw][k]);
         }
       }
     }
+    // carry alpha_t as alpha_{t-1}
     pfa = fa;
     pka = ka;
+#pragma unroll
+    for (int sw = 0; sw < W; ++sw) {
+      pa[sw] = va[sw];
+      pea[sw] = ea[sw];
+    }
     __syncwarp();
   }
 
-  // ---- block reduction of the partials in fixed warp order (deterministic)
+  // ---- block reduction of the partials in fixed warp order (deterministic);
+  // the constant weights S (stay), P (step) are applied here
+  const float amax = trans_max(trans, N);
   float *rA = red + warp * 1024;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) rA[lane * 32 + j] = accA[j];
+  for (int j = 0; j < 16; ++j) {
+    rA[lane * 32 + 2 * j] = __uint_as_float((unsigned)(accA[j] & 0xffffffffu));
+    rA[lane * 32 + 2 * j + 1] = __uint_as_float((unsigned)(accA[j] >> 32));
+  }
   float *rE = redE + warp * 2 * LP;
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) {
-      rE[sw * kLatStates + lane * kSpl + k] = accS[sw][k];
-      rE[LP + sw * kLatStates + lane * kSpl + k] = accP[sw][k];
+      const int l = sw * kLatStates + lane * kSpl + k;
+      float S = 0.f, P = 0.f;
+      if (l < L) {
+        const int yl = (int)y[l];
+        S = expf(trans[yl * N + yl] - amax);
+        P = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
+      }
+      rE[l] = accS[sw][k] * S;
+      rE[LP + l] = accP[sw][k] * P;
     }
   if (lane == 0) {
     gwarp[warp * 4 + 0] = gminF;

@@ -79,17 +79,22 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
 
 size_t ctc_chain_smem(int W) { (void)W; return sizeof(ChainSm); }
 
+// 2^x as a float for integer x clamped to [-127, 127] (0 below)
+__device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
+
 // One warp per frame at a time; lane i owns states 128 w + 4 i + k of every
-// segment w and token i of the gradient row.
+// segment w and token i of the gradient row.  Posteriors are scaled into
+// range by the lane exponents against the utterance's reference exponent
+// and normalised by their own per-frame sum z_t.
+template <int W>
 __global__ void __launch_bounds__(kGradWarps * 32)
     ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
                     const int32_t *__restrict__ status) {
-  extern __shared__ __align__(16) float gsm2[];
-  const int LP = w.lpad;
-  float *prow = gsm2;                               // [kGradWarps][LP]
-  int *sperm = reinterpret_cast<int *>(prow + kGradWarps * LP);   // [LP]
+  constexpr int LP = W * kLatStates;
+  __shared__ __align__(16) float prow[kGradWarps][LP];
+  __shared__ int sperm[LP];
   __shared__ float gw[kGradWarps][2];
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,30 +116,40 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
   const double ref = w.scal[b * 4 + 0] * 1.4426950408889634;
   const int refi = isfinite(ref) ? (int)floor(ref) : 0;
+  const float reff = isfinite(ref) ? (float)(ref - refi) : CUDART_NAN_F;
   float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  float *myp = prow + warp * LP;
+  const float4 *A4 = reinterpret_cast<const float4 *>(w.a + seg0 * kLatStates) + lane;
+  const float4 *B4 = reinterpret_cast<const float4 *>(w.b + seg0 * kLatStates) + lane;
+  const int *EA = w.ea + seg0 * 32 + lane;
+  const int *EB = w.eb + seg0 * 32 + lane;
+  const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);
+  const unsigned sege = (unsigned)d.Tmax * 32;
+  float *myp = prow[warp];
   const int tend = min(tb, T);
   for (int t = ta; t < tend; ++t) {
+    const unsigned tq = (unsigned)t * 32;
     float zl = 0.f, zb = 0.f;
-    for (int sw = 0; sw < weff; ++sw) {
-      const size_t r = seg0 + (size_t)sw * d.Tmax + t;
-      const float4 va = reinterpret_cast<const float4 *>(w.a + r * kLatStates)[lane];
-      const float4 vb = reinterpret_cast<const float4 *>(w.b + r * kLatStates)[lane];
-      const PostScale sc = post_scale(w.ea[r * 32 + lane], w.eb[r * 32 + lane], refi);
-      float4 p;
-      p.x = post_of(va.x, vb.x, sc);
-      p.y = post_of(va.y, vb.y, sc);
-      p.z = post_of(va.z, vb.z, sc);
-      p.w = post_of(va.w, vb.w, sc);
-      reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
-      zl += (p.x + p.y) + (p.z + p.w);
-      zb += p.x + p.z;   // blank states are the even ones
+#pragma unroll
+    for (int sw = 0; sw < W; ++sw) {
+      if (sw < weff) {
+        const float4 va = A4[sw * segq + tq];
+        const float4 vb = B4[sw * segq + tq];
+        const float sc = pow2_clamped(EA[sw * sege + tq] + EB[sw * sege + tq] - refi);
+        float4 p;
+        p.x = va.x * vb.x * sc;
+        p.y = va.y * vb.y * sc;
+        p.z = va.z * vb.z * sc;
+        p.w = va.w * vb.w * sc;
+        reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
+        zl += (p.x + p.y) + (p.z + p.w);
+        zb += p.x + p.z;   // blank states are the even ones
+      }
     }
     const float z = warp_sum(zl);
     const float zblank = warp_sum(zb);
     const float inv = 1.f / z;
-    const float g = (float)((double)__log2f(z) + (double)refi - ref);
+    const float g = __log2f(z) - reff;
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
     __syncwarp();
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       c3 += myp[sperm[q + 3]];
     }
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
-    if (lane < N) ge[(size_t)t * N + lane] = -((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
+    if (lane < N) ge[(unsigned)t * N + lane] = -((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
     __syncwarp();
   }
   if (lane == 0) {
@@ -161,6 +176,15 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       g = threadIdx.x ? fmaxf(g, gw[q][1]) : fminf(g, gw[q][0]);
     w.part_guard[((size_t)b * w.nblk + blk) * 2 + threadIdx.x] = g;
   }
+}
+
+template <int W>
+cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
+                              const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
+                              float *grad_em, const int32_t *status, cudaStream_t s) {
+  ctc_grad_kernel<W><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
+                                                                   blank, d, w, grad_em, status);
+  return cudaGetLastError();
 }
 
 __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
@@ -234,12 +258,17 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   trace(tr, s);  // chain
-  const size_t gsmem = sizeof(float) * (size_t)(kGradWarps + 1) * w.lpad;
-  err = cudaFuncSetAttribute(ctc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
-  if (err != cudaSuccess) return err;
-  ctc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, gsmem, s>>>(em, em_len, tgt, tgt_len,
-                                                                    blank, d, w, grad_em, status);
-  err = cudaGetLastError();
+  switch (w.W) {
+    case 1: err = launch_ctc_grad_w<1>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 2: err = launch_ctc_grad_w<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 3: err = launch_ctc_grad_w<3>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 4: err = launch_ctc_grad_w<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 5: err = launch_ctc_grad_w<5>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 6: err = launch_ctc_grad_w<6>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 7: err = launch_ctc_grad_w<7>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    case 8: err = launch_ctc_grad_w<8>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
+    default: return cudaErrorInvalidValue;
+  }
   if (err != cudaSuccess) return err;
   trace(tr, s);  // grad
   ctc_final_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
