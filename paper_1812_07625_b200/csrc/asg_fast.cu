@@ -72,6 +72,30 @@ struct LaggedScale {
 // ---- fcc: one frame of the 32-lane mat-vec recursion.  `vin` is the vector
 // of the previous step (alpha_{t-1}, or w_u = Et_u * beta'_u), m the lane's
 // row (alpha) or column (beta) of M; returns the unscaled product.
+// packed fp32x2 arithmetic (FFMA2 / FADD2): two lanes of a 64-bit register
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ unsigned long long f2_dup(float x) { return f2_pack(x, x); }
+__device__ __forceinline__ float f2_lo(unsigned long long x) { return __uint_as_float((unsigned)x); }
+__device__ __forceinline__ float f2_hi(unsigned long long x) {
+  return __uint_as_float((unsigned)(x >> 32));
+}
+
+// m: the lane's row of M (alpha) or column (beta); vin: the 32-vector (16B
+// aligned); 8 independent accumulators of depth 4 (scalar FFMA measured
+// faster than FFMA2 on this latency-bound chain)
 __device__ __forceinline__ float fcc_matvec(const float (&m)[32], const float *vin, bool spare,
                                             int N, int &e_sum) {
   const float4 *pv = reinterpret_cast<const float4 *>(vin);
@@ -100,42 +124,49 @@ struct FccState {
   float m[32];
   float v;       // this lane's current alpha_t / beta'_t
   int K;
+  int knext;     // scale exponent of the next step (chosen one step ahead)
   LaggedScale sc;
   bool spare;
 };
+
+// The scale bookkeeping of a step (the sum's exponent arrives through a
+// shuffle) runs after the step's vector is stored, so the next step's
+// mat-vec does not wait behind it; the operation sequence is unchanged.
 
 // fcc alpha step t (criterion.py:230): alpha_t = Et (.) (M alpha_{t-1}) 2^-k
 __device__ __forceinline__ void fcc_alpha_step(FccState &f, float et, float (*vec)[32],
                                                int par, float *out_row, int *outk_t, int lane,
                                                int N) {
+  const int k = f.knext;
+  const float sc = et * pow2f_fast(-k);   // |k| <= 120: exact
   __syncwarp();
   int e1;
-  const int k = f.sc.next();
-  const float sc = et * pow2f_fast(-k);   // |k| <= 120: exact
   const float s = fcc_matvec(f.m, vec[par ^ 1], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
-  f.sc.observe(e1);
   vec[par][lane] = f.v;
   out_row[lane] = f.v;
   if (lane == 0) *outk_t = f.K;
+  f.sc.observe(e1);
+  f.knext = f.sc.next();
 }
 
 // fcc beta' step consuming frame u (criterion.py:236): beta'_{u-1} = M^T (Et_u beta'_u) 2^-k
 __device__ __forceinline__ void fcc_beta_step(FccState &f, float et, float (*vec)[32],
                                               int par, float *out_row, int *outk_t, int lane,
                                               int N) {
+  const int k = f.knext;
+  const float sc = lane < N ? pow2f_fast(-k) : 0.f;
   vec[par][lane] = et * f.v;
   __syncwarp();
   int e1;
-  const int k = f.sc.next();
-  const float sc = lane < N ? pow2f_fast(-k) : 0.f;
   const float s = fcc_matvec(f.m, vec[par], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
-  f.sc.observe(e1);
   out_row[lane] = f.v;
   if (lane == 0) *outk_t = f.K;
+  f.sc.observe(e1);
+  f.knext = f.sc.next();
 }
 
 struct FccCtx {
@@ -154,15 +185,19 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
   const int lane = c.lane, N = c.N, T = c.T;
   FccState f;
   f.spare = N < 32;
+  float mrow[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     // forward: row `lane` of M; backward: column `lane`; lane N of a spare
     // lane is a row of ones (its product is the sum of the vector)
     const int p = FWD ? lane * N + j : j * N + lane;
-    f.m[j] = (lane < N && j < N) ? expf(c.trans[p] - c.amax)
-                                 : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
+    mrow[j] = (lane < N && j < N) ? expf(c.trans[p] - c.amax)
+                                  : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
   }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f.m[j] = mrow[j];
   f.K = 0;
+  f.knext = f.sc.next();
   int *mycons = &sm.cons[c.cons_idx];
   if (FWD) {
     wait_ge(&sm.prod, 1);
@@ -297,17 +332,6 @@ size_t asg_chain_smem(int W) {
 }
 
 // ----------------------------------------------------------- grad kernel --
-// packed fp32x2 FMA (FFMA2): d = a * b + c on two lanes of a 64-bit register
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
-                                                    unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ unsigned long long f2_dup(float x) {
-  const unsigned u = __float_as_uint(x);
-  return ((unsigned long long)u << 32) | u;
-}
 // 2^x as a float for integer x clamped to [-127, 127] (0 below)
 __device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
 
