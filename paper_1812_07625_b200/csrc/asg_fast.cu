@@ -335,29 +335,25 @@ size_t asg_chain_smem(int W) {
 // 2^x as a float for integer x clamped to [-127, 127] (0 below)
 __device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
 
-// W: fac lattice warps (segments of 128 states).  A warp handles one frame at
-// a time (consecutive frames, so alpha_{t-1} is carried in registers); lane i
-// owns token i of the fcc graph and states 128 w + 4 i + k (w < W, k < 4) of
-// the fac lattice.  Posteriors are normalised per frame by their own sums
-// (z_t), scaled into range by the lane exponents against the utterance's
+// The gradient is split in two kernels with small register footprints (so
+// that enough warps are resident to hide the row loads):
+//   asg_fcc_grad  fcc node posteriors -> grad_e row (full part), fcc edge
+//                 outer products u_t alpha_{t-1}^T, fcc guard;
+//   asg_fac_grad  fac node posteriors gathered by token (subtracted from the
+//                 row), fac stay/step edge sums, fac guard.
+// A warp handles consecutive frames (alpha_{t-1} carried in registers).
+// Posteriors are normalised per frame by their own sums z_t; lattice values
+// are scaled into range by the lane exponents against the utterance's
 // reference exponent.  Edge sums are accumulated without their constant
-// transition weights (S, P, M), which are applied once in the epilogue.
-template <int W>
-__global__ void __launch_bounds__(kGradWarps * 32, 1)
-    asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
-                    const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
-                    const float *__restrict__ trans, Dims d, AsgFastWs w,
-                    float *__restrict__ grad_em, const int32_t *__restrict__ status) {
-  constexpr int LP = W * kLatStates;
-  extern __shared__ __align__(16) float gsm[];
-  float *red = gsm;                              // [kGradWarps][32*32] fullA partials
-  float *redE = red + kGradWarps * 1024;         // [kGradWarps][2][LP] edge partials
-  float *prow = redE + kGradWarps * 2 * LP;      // [kGradWarps][LP] posterior row
-  float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
-  float *vrow = erow + kGradWarps * 64;          // [kGradWarps][32] alpha_{t-1} fcc row
-  float *gwarp = vrow + kGradWarps * 32;         // [kGradWarps][4] guard
-  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 4);   // [LP]
+// transition weights (M, S, P), which are applied once in the epilogues.
 
+__global__ void __launch_bounds__(kGradWarps * 32, 2)
+    asg_fcc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                        Dims d, AsgFastWs w, float *__restrict__ grad_em,
+                        const int32_t *__restrict__ status) {
+  __shared__ __align__(16) float red[kGradWarps][1024];   // accA partials
+  __shared__ __align__(16) float vrow[kGradWarps][32];    // alpha_{t-1} fcc row
+  __shared__ float gwarp[kGradWarps][2];
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
@@ -367,12 +363,106 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
-
   // rows outside the utterance (or a failed utterance) get zero gradient
   for (int t = ta; t < tb; ++t)
     if (!ok || t >= T)
       if (lane < N) ge[(size_t)t * N + lane] = 0.f;
   if (!ok) return;
+  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
+  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
+  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
+  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
+  const float *emb = em + (size_t)b * d.Tmax * N;
+  const float *fa_r = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
+  const float *fb_r = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
+  const int *ka_r = w.fcc_ka + (size_t)b * w.tpad;
+  const int *kb_r = w.fcc_kb + (size_t)b * w.tpad + 1;
+  unsigned long long accA[16];   // accA[jj] = (row lane, columns 2jj, 2jj+1)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) accA[j] = 0ull;
+  float *myv = vrow[warp];
+  const int tend = min(tb, T);
+  float pfa = 0.f;
+  int pka = 0;
+  if (ta >= 1 && ta < tend) {
+    pfa = fa_r[(unsigned)(ta - 1) * 32];
+    pka = ka_r[ta - 1];
+  }
+  for (int t = ta; t < tend; ++t) {
+    const float e = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
+    const float fa = fa_r[(unsigned)t * 32], fb = fb_r[(unsigned)t * 32];
+    const int ka = ka_r[t], kb = kb_r[t];
+    const float m = warp_max(e);
+    const float et = lane < N ? et_of(e, m) : 0.f;
+    myv[lane] = pfa;
+    // fcc node posteriors (:238): the full part of the gradient row
+    const float gam = fa * fb;
+    const float zf = warp_sum(gam);
+    const float izf = 1.f / zf;
+    const float g = __log2f(zf) + (float)(ka + kb - refFi) - refFf;
+    gmin = fminf(gmin, g);
+    gmax = fmaxf(gmax, g);
+    if (lane < N) ge[(unsigned)t * N + lane] = gam * izf;
+    __syncwarp();
+    if (t >= 1) {
+      // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
+      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(pka - ka) * izf);
+      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(myv);
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const ulonglong2 x = pv[qq];
+        accA[2 * qq] = ffma2(u2, x.x, accA[2 * qq]);
+        accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
+      }
+    }
+    pfa = fa;
+    pka = ka;
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    red[warp][lane * 32 + 2 * j] = f2_lo(accA[j]);
+    red[warp][lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
+  }
+  if (lane == 0) {
+    gwarp[warp][0] = gmin;
+    gwarp[warp][1] = gmax;
+  }
+  __syncthreads();
+  float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < kGradWarps; ++q) s += red[q][i];
+    dstA[i] = s;
+  }
+  if (threadIdx.x < 2) {
+    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    for (int q = 0; q < kGradWarps; ++q)
+      g = threadIdx.x ? fmaxf(g, gwarp[q][1]) : fminf(g, gwarp[q][0]);
+    w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
+    asg_fac_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                        const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                        const float *__restrict__ trans, Dims d, AsgFastWs w,
+                        float *__restrict__ grad_em, const int32_t *__restrict__ status) {
+  constexpr int LP = W * kLatStates;
+  extern __shared__ __align__(16) float gsm[];
+  float *redE = gsm;                             // [kGradWarps][2][LP] edge partials
+  float *prow = redE + kGradWarps * 2 * LP;      // [kGradWarps][LP] posterior row
+  float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
+  float *gwarp = erow + kGradWarps * 64;         // [kGradWarps][2] guard
+  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 2);   // [LP]
+
+  const int b = blockIdx.y, blk = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = d.N;
+  const int T = em_len[b];
+  const int t0 = blk * kGradFramesPerBlock;
+  if (status[b] != W2L_OK) return;
   if (t0 >= T) {
     // keep the partial buffers well-defined for the final reduction
     for (int i = threadIdx.x; i < 1024; i += blockDim.x)
@@ -384,6 +474,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
           (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
     return;
   }
+  float *ge = grad_em + (size_t)b * d.Tmax * N;
+  const int fpw = kGradFramesPerBlock / kGradWarps;
+  const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
 
   const int L = tgt_len[b];
   const int64_t *y = tgt + (size_t)b * d.Lmax;
@@ -395,35 +488,19 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
       const int l = sw * kLatStates + lane * kSpl + k;
       tok[sw][k] = l < L ? (int)y[l] : N;
     }
-  // token CSR of this utterance, staged once per block (the gather reads it
-  // every frame)
   for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
   float *myp = prow + warp * LP;
   float *mye = erow + warp * 64;
-  float *myv = vrow + warp * 32;
-  mye[32 + lane] = 0.f;   // column N.. of the Et row: padding states read 0
+  mye[32 + lane] = 0.f;   // columns N.. of the Et row: padding states read 0
   __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
-
-  // Every frame's normaliser must reproduce the forward totals the chain
-  // kernel produced (the scaled alpha_t * beta_t mass is frame-invariant);
-  // deviations in log2 units feed the guard.
-  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
   const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
-  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
   const int refCi = isfinite(refC) ? (int)floor(refC) : 0;
-  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
   const float refCf = isfinite(refC) ? (float)(refC - refCi) : CUDART_NAN_F;
-  float gminF = CUDART_INF_F, gmaxF = -CUDART_INF_F, gminC = CUDART_INF_F,
-        gmaxC = -CUDART_INF_F;
+  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
 
-  // per-utterance bases, 32-bit offsets within the utterance
   const float *emb = em + (size_t)b * d.Tmax * N;
-  const float *fa_r = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
-  const float *fb_r = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
-  const int *ka_r = w.fcc_ka + (size_t)b * w.tpad;
-  const int *kb_r = w.fcc_kb + (size_t)b * w.tpad + 1;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
   const float4 *A4 = reinterpret_cast<const float4 *>(w.fac_a + seg0 * kLatStates) + lane;
   const float4 *B4 = reinterpret_cast<const float4 *>(w.fac_b + seg0 * kLatStates) + lane;
@@ -432,19 +509,12 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
   const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);   // float4 per segment
   const unsigned sege = (unsigned)d.Tmax * 32;
 
-  unsigned long long accA[16];   // accA[jj] = (row lane, columns 2jj, 2jj+1)
-#pragma unroll
-  for (int j = 0; j < 16; ++j) accA[j] = 0ull;
   float accS[W][kSpl], accP[W][kSpl];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) accS[sw][k] = accP[sw][k] = 0.f;
-
-  // alpha_{t-1} carried across frames (fcc value/exponent, fac lane blocks)
   const int tend = min(tb, T);
-  float pfa = 0.f;
-  int pka = 0;
   float4 pa[W];
   int pea[W];
 #pragma unroll
@@ -453,20 +523,15 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
     pea[sw] = kNegExp;
   }
   if (ta >= 1 && ta < tend) {
-    pfa = fa_r[(unsigned)(ta - 1) * 32];
-    pka = ka_r[ta - 1];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
       pa[sw] = A4[sw * segq + (unsigned)(ta - 1) * 32];
       pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
     }
   }
-
   for (int t = ta; t < tend; ++t) {
     const unsigned tq = (unsigned)t * 32;
     const float e = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
-    const float fa = fa_r[tq], fb = fb_r[tq];
-    const int ka = ka_r[t], kb = kb_r[t];
     float4 va[W], vb[W];
     int ea[W], eb[W];
 #pragma unroll
@@ -476,20 +541,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
       ea[sw] = EA[sw * sege + tq];
       eb[sw] = EB[sw * sege + tq];
     }
-    // ---- emissions of frame t, shifted and exponentiated (same as the chain)
     const float m = warp_max(e);
-    const float et = lane < N ? et_of(e, m) : 0.f;
-    mye[lane] = et;
-    myv[lane] = pfa;
-    // ---- fcc node posteriors (:238)
-    const float gam = fa * fb;
-    const float zf = warp_sum(gam);
-    const float izf = 1.f / zf;
-    const float gF = __log2f(zf) + (float)(ka + kb - refFi) - refFf;
-    gminF = fminf(gminF, gF);
-    gmaxF = fmaxf(gmaxF, gF);
-    const float full_e = gam * izf;
-    // ---- fac node posteriors (:214-217)
+    mye[lane] = lane < N ? et_of(e, m) : 0.f;
+    // fac node posteriors (:214-217)
     float zl = 0.f;
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
@@ -504,9 +558,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
     }
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
-    const float gC = __log2f(zc) - refCf;
-    gminC = fminf(gminC, gC);
-    gmaxC = fmaxf(gmaxC, gC);
+    const float g = __log2f(zc) - refCf;
+    gmin = fminf(gmin, g);
+    gmax = fmaxf(gmax, g);
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
     float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
@@ -518,20 +572,10 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
       c3 += myp[sperm[q + 3]];
     }
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
-    const float con = (c0 + c1) + (c2 + c3);
-    if (lane < N) ge[(unsigned)t * N + lane] = full_e - con * izc;
+    if (lane < N) ge[tq / 32 * N + lane] -= ((c0 + c1) + (c2 + c3)) * izc;
     if (t >= 1) {
-      // ---- fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
-      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(pka - ka) * izf);
-      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(myv);
-#pragma unroll
-      for (int qq = 0; qq < 8; ++qq) {
-        const ulonglong2 x = pv[qq];
-        accA[2 * qq] = ffma2(u2, x.x, accA[2 * qq]);
-        accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
-      }
-      // ---- fac edge posteriors (:218-224): alpha_{t-1} (stay: same state,
-      // step: previous state) times Et[y] beta'_t (times S|P later)
+      // fac edge posteriors (:218-224): alpha_{t-1} (stay: same state, step:
+      // previous state) times Et[y] beta'_t (times S|P later)
       float carry_v = 0.f;   // state 128 sw - 1 (previous segment)
       int carry_e = kNegExp;
 #pragma unroll
@@ -560,9 +604,6 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
         }
       }
     }
-    // carry alpha_t as alpha_{t-1}
-    pfa = fa;
-    pka = ka;
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
       pa[sw] = va[sw];
@@ -574,12 +615,6 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
   // ---- block reduction of the partials in fixed warp order (deterministic);
   // the constant weights S (stay), P (step) are applied here
   const float amax = trans_max(trans, N);
-  float *rA = red + warp * 1024;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    rA[lane * 32 + 2 * j] = __uint_as_float((unsigned)(accA[j] & 0xffffffffu));
-    rA[lane * 32 + 2 * j + 1] = __uint_as_float((unsigned)(accA[j] >> 32));
-  }
   float *rE = redE + warp * 2 * LP;
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
@@ -596,31 +631,23 @@ __global__ void __launch_bounds__(kGradWarps * 32, 1)
       rE[LP + l] = accP[sw][k] * P;
     }
   if (lane == 0) {
-    gwarp[warp * 4 + 0] = gminF;
-    gwarp[warp * 4 + 1] = gmaxF;
-    gwarp[warp * 4 + 2] = gminC;
-    gwarp[warp * 4 + 3] = gmaxC;
+    gwarp[warp * 2 + 0] = gmin;
+    gwarp[warp * 2 + 1] = gmax;
   }
   __syncthreads();
-  float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < kGradWarps; ++q) s += red[q * 1024 + i];
-    dstA[i] = s;
-  }
   float *dstE = w.part_edge + ((size_t)b * w.nblk + blk) * 2 * LP;
   for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
     float s = 0.f;
     for (int q = 0; q < kGradWarps; ++q) s += redE[q * 2 * LP + i];
     dstE[i] = s;
   }
-  if (threadIdx.x < 4) {
-    float g = (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
+  if (threadIdx.x < 2) {
+    float g2 = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
     for (int q = 0; q < kGradWarps; ++q) {
-      const float v = gwarp[q * 4 + threadIdx.x];
-      g = (threadIdx.x & 1) ? fmaxf(g, v) : fminf(g, v);
+      const float v = gwarp[q * 2 + threadIdx.x];
+      g2 = threadIdx.x ? fmaxf(g2, v) : fminf(g2, v);
     }
-    w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
+    w.part_guard[((size_t)b * w.nblk + blk) * 4 + 2 + threadIdx.x] = g2;
   }
 }
 
@@ -711,8 +738,8 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                           float *grad_em, const int32_t *status, cudaStream_t s) {
   constexpr int LP = W * kLatStates;
-  const size_t smem = sizeof(float) * (kGradWarps * (1024 + 2 * LP + LP + 64 + 32 + 4) + LP);
-  auto k = asg_grad_kernel<W>;
+  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2) + LP);
+  auto k = asg_fac_grad_kernel<W>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   k<<<dim3(w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
@@ -781,6 +808,10 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   trace(tr, s);  // chain
+  asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, d, w, grad_em,
+                                                                    status);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
   switch (w.W) {
     case 1: err = launch_grad_w<1>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
     case 2: err = launch_grad_w<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
