@@ -33,7 +33,7 @@
 namespace w2l {
 namespace {
 
-constexpr int kGradFramesPerBlock = 64;
+constexpr int kGradFramesPerBlock = 128;
 constexpr int kGradWarps = 8;
 
 __device__ __forceinline__ float trans_max(const float *trans, int N) {
@@ -663,6 +663,9 @@ __global__ void __launch_bounds__(1024)
   __shared__ float sA[1024];
   __shared__ float s_red[32];
   __shared__ int s_bad;
+  __shared__ int sy[W2L_MAX_ASG_LABELS];      // targets (int), staged once
+  __shared__ int sperm[W2L_MAX_ASG_LABELS];   // token CSR
+  __shared__ int sts[33];
   const int N = d.N, NN = N * N;
   if (status[b] != W2L_OK) {
     for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
@@ -676,6 +679,11 @@ __global__ void __launch_bounds__(1024)
   am = warp_max(am);
   if (lane == 0) s_red[warp] = am;
   if (threadIdx.x == 0) s_bad = 0;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    sy[l] = (int)y[l];
+    sperm[l] = w.perm[(size_t)b * w.lpad + l];
+  }
+  if (threadIdx.x < 33) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];
   // fixed-order sums of the per-frame-block partials; 4 independent
   // accumulators keep several loads in flight per thread
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
@@ -698,8 +706,8 @@ __global__ void __launch_bounds__(1024)
   __syncthreads();
   float amax = s_red[0];
   for (int q = 1; q < (int)(blockDim.x >> 5); ++q) amax = fmaxf(amax, s_red[q]);
-  const int *perm = w.perm + (size_t)b * w.lpad;
-  const int *ts = w.tok_start + b * 33;
+  const int *perm = sperm;
+  const int *ts = sts;
   for (int p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = p / N, j = p % N;
     const float full = sA[i * 32 + j] * expf(trans[p] - amax);
@@ -707,7 +715,7 @@ __global__ void __launch_bounds__(1024)
     for (int q = ts[i]; q < ts[i + 1]; ++q) {
       const int l = perm[q];
       if (i == j) con += sEdge[l];
-      if (l > 0 && (int)y[l - 1] == j) con += sEdge[LP + l];
+      if (l > 0 && sy[l - 1] == j) con += sEdge[LP + l];
     }
     ga_utt[(size_t)b * NN + p] = full - con;
     if (!isfinite(full - con)) atomicOr(&s_bad, 1);

@@ -20,7 +20,7 @@
 namespace w2l {
 namespace {
 
-constexpr int kGradFramesPerBlock = 64;
+constexpr int kGradFramesPerBlock = 128;
 constexpr int kGradWarps = 8;
 
 template <bool FWD>
@@ -187,22 +187,28 @@ cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int6
   return cudaGetLastError();
 }
 
+// one warp per utterance: loss and guard verdict (partials read in parallel)
 __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
                                  double *loss, int32_t *status) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (b >= d.B || status[b] != W2L_OK) return;
   const int T = em_len[b];
   const double ln2 = 0.6931471805599453;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
-  bool bad = !(isfinite(zA) && isfinite(zB)) || fabs(zA - zB) > tol;
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
-  for (int q = 0; q < nb_used && !bad; ++q) {
+  int bad = 0;
+  for (int q = lane; q < nb_used; q += 32) {
     const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 2;
     bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
   }
-  loss[b] = -(zA + shifts);                                  // criterion.py:162
-  if (bad) status[b] = kNeedsExact;
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    bad |= !(isfinite(zA) && isfinite(zB)) || fabs(zA - zB) > tol;
+    loss[b] = -(zA + shifts);                                  // criterion.py:162
+    if (bad) status[b] = kNeedsExact;
+  }
 }
 
 }  // namespace
@@ -271,7 +277,7 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
   }
   if (err != cudaSuccess) return err;
   trace(tr, s);  // grad
-  ctc_final_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
+  ctc_final_kernel<<<(d.B + 7) / 8, 256, 0, s>>>(em_len, d, w, loss, status);
   err = cudaGetLastError();
   trace(tr, s);  // final
   return err;

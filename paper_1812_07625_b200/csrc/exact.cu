@@ -64,6 +64,14 @@ __global__ void __launch_bounds__(kExactThreads)
   int *y = (int *)(edge + 2 * Lmax);    // [Lmax]
   __shared__ double s_fal, s_fcc;
 
+  // nothing to do for this slot (the common fallback case): leave after one
+  // parallel look at the statuses instead of walking them serially
+  {
+    int any = 0;
+    for (int b = blockIdx.x + nslots * (int)threadIdx.x; b < d.B; b += nslots * (int)blockDim.x)
+      any |= wants(status[b], only_flagged);
+    if (!__syncthreads_or(any)) return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) A[i] = (double)trans[i];
 
@@ -254,6 +262,14 @@ __global__ void __launch_bounds__(kExactThreads)
   int *lab = (int *)(rows + 4 * Smax);       // [Smax]
   int *skip = lab + Smax;                    // [Smax]
   __shared__ double s_logz;
+  // nothing to do for this slot (the common fallback case): leave after one
+  // parallel look at the statuses instead of walking them serially
+  {
+    int any = 0;
+    for (int b = blockIdx.x + nslots * (int)threadIdx.x; b < d.B; b += nslots * (int)blockDim.x)
+      any |= wants(status[b], only_flagged);
+    if (!__syncthreads_or(any)) return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *alpha = (double *)(slot_ws + ctc_slot_bytes(d.Tmax, d.Lmax) * blockIdx.x);
   double *beta = alpha + (size_t)d.Tmax * Smax;

@@ -23,56 +23,87 @@ namespace {
 constexpr int kBitNonFinite = 1 << 8;
 constexpr int kBitRowLse = 1 << 9;
 
+// One warp per 32 consecutive frame rows of one utterance: the rows are a
+// contiguous range, loaded coalesced into shared memory, then lane r checks
+// row r.  The CTC row normalisation is checked in fp32 and re-checked in
+// float64 (the reference's arithmetic) only near the 1e-2 threshold.
 template <class TE>
-__global__ void em_check_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len,
-                                Dims d, int check_lse, int32_t *status) {
+__global__ void __launch_bounds__(128)
+    em_check_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len, Dims d,
+                    int check_lse, int32_t *status) {
+  __shared__ TE rows[4][32 * 32];
   const int b = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = min(max(em_len[b], 0), d.Tmax);
-  if (t >= T) return;
-  const TE *r = em + ((size_t)b * d.Tmax + t) * d.N;
+  const int t0 = (blockIdx.x * 4 + warp) * 32;
+  if (t0 >= T) return;
+  const int nrows = min(32, T - t0), N = d.N;
+  const TE *src = em + ((size_t)b * d.Tmax + t0) * N;
+  TE *buf = rows[warp];
+  for (int e = lane; e < nrows * N; e += 32) buf[e] = src[e];
+  __syncwarp();
   int bits = 0;
-  double m = -CUDART_INF;
-  for (int i = 0; i < d.N; ++i) {
-    const double v = (double)r[i];
-    if (!isfinite(v)) bits = kBitNonFinite;
-    m = fmax(m, v);
+  if (lane < nrows) {
+    const TE *r = buf + lane * N;
+    float m = -CUDART_INF_F;
+    for (int i = 0; i < N; ++i) {
+      const double v = (double)r[i];
+      if (!isfinite(v)) bits = kBitNonFinite;
+      m = fmaxf(m, (float)v);
+    }
+    if (check_lse && !bits) {
+      // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101)
+      float sum = 0.f;
+      for (int i = 0; i < N; ++i) sum += __expf((float)r[i] - m);
+      const float dev = fabsf(__logf(sum) + m);
+      if (dev > 0.0099f) {
+        if (dev > 0.0101f) {
+          bits |= kBitRowLse;
+        } else {
+          double md = -CUDART_INF, sd = 0.0;
+          for (int i = 0; i < N; ++i) md = fmax(md, (double)r[i]);
+          for (int i = 0; i < N; ++i) sd += exp((double)r[i] - md);
+          if (fabs(log(sd) + md) > 1e-2) bits |= kBitRowLse;
+        }
+      }
+    }
   }
-  if (check_lse && !bits) {
-    // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101)
-    double s = 0.0;
-    for (int i = 0; i < d.N; ++i) s += exp((double)r[i] - m);
-    if (fabs(log(s) + m) > 1e-2) bits |= kBitRowLse;
-  }
-  if (bits) atomicOr(&status[b], bits);
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if (lane == 0 && bits) atomicOr(&status[b], bits);
 }
 
 __device__ bool block_any(int v) { return __syncthreads_or(v); }
 
 // grouped-by-token chain states: perm[tok_start[k] .. tok_start[k+1]) lists
-// the states (ASG: l, CTC: 2l+1) whose label is k, in ascending order
+// the states (ASG: l, CTC: 2l+1) whose label is k, in ascending order.  The
+// targets are staged in shared memory; thread k < N appends the positions of
+// token k in one ordered scan.
 __device__ void build_token_csr(const int64_t *y, int L, int N, int state_mul, int state_off,
                                 int *perm, int *tok_start) {
+  __shared__ unsigned char ys[W2L_MAX_ASG_LABELS];
   __shared__ int cnt[33];
+  for (int l = threadIdx.x; l < L; l += blockDim.x) ys[l] = (unsigned char)y[l];
   if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
   __syncthreads();
-  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[(int)y[l]], 1);
+  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[ys[l]], 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k <= N; ++k) {
       const int c = k < N ? cnt[k] : 0;
       tok_start[k] = acc;
+      cnt[k] = acc;
       acc += c;
     }
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < L; l += blockDim.x) {
-    const int tk = (int)y[l];
-    int before = 0;
-    for (int q = 0; q < l; ++q) before += (y[q] == tk);
-    perm[tok_start[tk] + before] = l * state_mul + state_off;
+  if (threadIdx.x < N) {
+    const int k = threadIdx.x;
+    int o = cnt[k];
+    for (int l = 0; l < L; ++l)
+      if (ys[l] == k) perm[o++] = l * state_mul + state_off;
   }
+  __syncthreads();
 }
 
 template <class TE>
