@@ -221,31 +221,31 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
       fcc_beta_step(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
     publish(mycons, j + 1, lane);
   };
-  const int pro_end = min(T, kUnroll);
+  const int pro_end = min(T, kBlk);
   for (int j = 1; j < pro_end; ++j) generic(j);
-  const int nfull = T > kUnroll ? (T - kUnroll) / kUnroll : 0;
+  const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
-    const int j0 = m * kUnroll;
+    const int j0 = m * kBlk;
     PROF_STEADY(m >= 40 && m < 160);
-    PROF_WAIT(1, wait3(&sm.prod, eidx_of(FWD, j0 + kUnroll - 1) + 1, &sm.prod, 0, &sm.prod, 0));
+    PROF_WAIT(1, wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, &sm.prod, 0, &sm.prod, 0));
     const float *eb = sm.ering[j0 & (kRing - 1)];
     const int tb = frame_of(FWD, T, j0);
     float *sv = c.rows + (size_t)tb * 32;
-    float etq[kUnroll];
+    float etq[kBlk];
 #pragma unroll
-    for (int q = 0; q < kUnroll; ++q) etq[q] = eb[q * kStride + lane];
+    for (int q = 0; q < kBlk; ++q) etq[q] = eb[q * kStride + lane];
 #pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
+    for (int q = 0; q < kBlk; ++q) {
       const int dq = FWD ? q : -q;
       if (FWD)
         fcc_alpha_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
       else
         fcc_beta_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
     }
-    publish(mycons, j0 + kUnroll, lane);
+    publish(mycons, j0 + kBlk, lane);
   }
-  for (int j = max(pro_end, (nfull + 1) * kUnroll); j < T; ++j) generic(j);
+  for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
   publish(mycons, kDone, lane);
   if (lane == 0) PROF_ADD(0, clock64() - _pt0);
   float z;

@@ -73,6 +73,7 @@ constexpr int kBndRing = 128;              // boundary ring (steps): decouples n
 constexpr int kCounters = kMaxLatWarps + 2;  // lattice warps + fcc warp (+ spare)
 constexpr int kDone = 1 << 30;             // progress of a finished consumer
 constexpr int kRenormF = 4;                // steps between fp32 lane renormalisations
+constexpr int kBlk = 8;                    // steps per unrolled block (one publish / wait per block)
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
 
 struct __align__(16) Bnd {
@@ -479,23 +480,23 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     lat_store_row(f.v, f.ex, row_of(t), exp_of(t), lane);
     publish(mycons, j + 1, lane);
   };
-  const int pro_end = min(T, kUnroll);
+  const int pro_end = min(T, kBlk);
   for (int j = 1; j < pro_end; ++j) generic(j);
 
-  // ---- full blocks of kUnroll steps at j0 = 8 m
-  const int nfull = T > kUnroll ? (T - kUnroll) / kUnroll : 0;
+  // ---- full blocks of kBlk steps at j0 = 8 m
+  const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
-    const int j0 = m * kUnroll;
+    const int j0 = m * kBlk;
     PROF_STEADY(m >= 40 && m < 160);
 #ifdef W2L_PROF
-    PROF_WAIT(1, while (ld_relaxed(&sm.prod) < eidx_of(FWD, j0 + kUnroll - 1) + 1) {});
-    PROF_WAIT(2, while (has_up && ld_relaxed(upcons) < j0 + kUnroll - 1) {});
-    PROF_WAIT(3, while (has_dn && ld_relaxed(dncons) < j0 + kUnroll + 1 - kBndRing) {});
+    PROF_WAIT(1, while (ld_relaxed(&sm.prod) < eidx_of(FWD, j0 + kBlk - 1) + 1) {});
+    PROF_WAIT(2, while (has_up && ld_relaxed(upcons) < j0 + kBlk - 1) {});
+    PROF_WAIT(3, while (has_dn && ld_relaxed(dncons) < j0 + kBlk + 1 - kBndRing) {});
 #endif
-    PROF_WAIT(6, wait3(&sm.prod, eidx_of(FWD, j0 + kUnroll - 1) + 1, upcons,
-                       has_up ? j0 + kUnroll - 1 : 0, dncons,
-                       has_dn ? j0 + kUnroll + 1 - kBndRing : -kDone));
+    PROF_WAIT(6, wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, upcons,
+                       has_up ? j0 + kBlk - 1 : 0, dncons,
+                       has_dn ? j0 + kBlk + 1 - kBndRing : -kDone));
     const float *eb = sm.ering[j0 & (kRing - 1)];
     const Bnd *ub0 = has_up ? &ubnd[(j0 - 1) & (kBndRing - 1)] : nullptr;
     const Bnd *ub1 = has_up ? &ubnd[j0 & (kBndRing - 1)] : nullptr;   // q >= 1: ub1[q-1]
@@ -504,9 +505,9 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     const int tb = frame_of(FWD, T, j0);
     float *sv = row_of(tb);
     int *se = exp_of(tb);
-    StepIn in[kUnroll];
+    StepIn in[kBlk];
 #pragma unroll
-    for (int q = 0; q < kUnroll; ++q)
+    for (int q = 0; q < kBlk; ++q)
       load_step_in<KIND, FWD>(in[q], f, eb + q * kStride,
                               q == 0 ? ub0 : (ub1 ? ub1 + (q - 1) : nullptr), lane);
     // every lane live (and the incoming boundary lane): exponents only move at
@@ -517,7 +518,7 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     auto run_block = [&](auto fast_tag) {
       constexpr bool FAST = decltype(fast_tag)::value;
 #pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
+      for (int q = 0; q < kBlk; ++q) {
         lat_step<KIND, FWD, FAST>(f, in[q], ob + q, lane, (q % kRenormF) == 0,
                                   (q % kRenormF) == 1);
         const int dq = FWD ? q : -q;
@@ -537,10 +538,10 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     if (lane == 0 && m == 100) PROF_ADD(4, 0), g_prof[(((blockIdx.x & 63) * 2 + blockIdx.y) * 16 + (threadIdx.x >> 5)) * 8 + 4] = clock64();
     if (lane == 0 && m == 159) PROF_ADD(5, -clock64());
 #endif
-    publish(mycons, j0 + kUnroll, lane);
+    publish(mycons, j0 + kBlk, lane);
   }
   // ---- tail steps
-  for (int j = max(pro_end, (nfull + 1) * kUnroll); j < T; ++j) generic(j);
+  for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
   publish(mycons, kDone, lane);
   if (lane == 0) { PROF_ADD(0, clock64() - _pt0); PROF_ADD(5, nfull); }
 

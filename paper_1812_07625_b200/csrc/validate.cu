@@ -97,11 +97,20 @@ __device__ void build_token_csr(const int64_t *y, int L, int N, int state_mul, i
     }
   }
   __syncthreads();
-  if (threadIdx.x < N) {
-    const int k = threadIdx.x;
-    int o = cnt[k];
-    for (int l = 0; l < L; ++l)
-      if (ys[l] == k) perm[o++] = l * state_mul + state_off;
+  // warp 0 walks the targets 32 at a time: lanes holding the same token
+  // find each other (match.any) and take consecutive slots in order
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int l0 = 0; l0 < L; l0 += 32) {
+      const int l = l0 + lane;
+      const int tk = l < L ? (int)ys[l] : 32 + lane;   // unique dummies past the end
+      const unsigned same = __match_any_sync(0xffffffffu, tk);
+      const int rank = __popc(same & ((1u << lane) - 1u));
+      if (l < L) perm[cnt[tk] + rank] = l * state_mul + state_off;
+      __syncwarp();
+      if (l < L && rank == 0) cnt[tk] += __popc(same);
+      __syncwarp();
+    }
   }
   __syncthreads();
 }
