@@ -58,6 +58,15 @@ enum {
 
 /* flags for the fp32 batched entry points */
 #define W2L_FLAG_NO_FALLBACK 1u  /* report guard failures instead of recomputing in f64 */
+/* Split-phase calls (both bits clear = the whole call).  PHASE_CHAIN runs the
+ * validation and the forward/backward recursions, leaving their rows in the
+ * workspace; PHASE_GRAD then runs the posterior/gradient kernels, the loss,
+ * the float64 fallback and the batch reduction from that workspace (same
+ * inputs, same stream order).  Lets a caller schedule the latency-bound
+ * recursions of several criteria together, ahead of their throughput-bound
+ * gradient phases. */
+#define W2L_FLAG_PHASE_CHAIN 2u
+#define W2L_FLAG_PHASE_GRAD 4u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

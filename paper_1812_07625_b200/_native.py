@@ -56,6 +56,8 @@ SIGNATURES = {
 OK, ERR_CONTRACT, ERR_NUMERIC, ERR_TARGET, ERR_INFEASIBLE, ERR_CUDA, ERR_COMM, ERR_PRECISION = \
     range(8)
 FLAG_NO_FALLBACK = 1
+FLAG_PHASE_CHAIN = 2
+FLAG_PHASE_GRAD = 4
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

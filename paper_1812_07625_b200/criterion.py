@@ -353,6 +353,17 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
     return em, el, tg, tl
 
 
+def _flags(fallback: bool, phase: str) -> int:
+    f = 0 if fallback else nat.FLAG_NO_FALLBACK
+    if phase == "chain":
+        f |= nat.FLAG_PHASE_CHAIN
+    elif phase == "grad":
+        f |= nat.FLAG_PHASE_GRAD
+    elif phase != "all":
+        raise ContractError(f"phase must be 'all', 'chain' or 'grad', got {phase!r}")
+    return f
+
+
 def _raise_batch(status: torch.Tensor, what: str) -> None:
     code, bad = _first_error(status)
     if code != nat.OK:
@@ -365,7 +376,8 @@ def _raise_batch(status: torch.Tensor, what: str) -> None:
 def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, check=True,
                           per_utterance_grad_transitions=False, workspace=None,
                           out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True, trace: bool = False) -> BatchLossOutput:
+                          fallback: bool = True, trace: bool = False,
+                          phase: str = "all") -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -375,7 +387,10 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     batch and (optionally) per utterance.  check=True synchronises and raises
     the reference exception for the first failing utterance.  fallback=False
     disables the float64 recompute of utterances failing the fp32 guard (they
-    report W2L_ERR_PRECISION instead) -- a diagnostic for the fast path."""
+    report W2L_ERR_PRECISION instead) -- a diagnostic for the fast path.
+    phase="chain" | "grad" splits the call (W2L_FLAG_PHASE_*): "chain" runs
+    the recursions into the workspace, a later "grad" call with the same
+    inputs, workspace and out on the same stream order finishes it."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -397,8 +412,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
-            _p(out.status), _p(ws), ws.numel(), 0 if fallback else nat.FLAG_NO_FALLBACK,
-            _stream())
+            _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_asg_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -413,9 +427,11 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
 
 def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *, check=True,
                           workspace=None, out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True, trace: bool = False) -> BatchLossOutput:
+                          fallback: bool = True, trace: bool = False,
+                          phase: str = "all") -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
-    log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2."""
+    log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase: as
+    for asg_loss_grad_batched."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -431,7 +447,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
-            0 if fallback else nat.FLAG_NO_FALLBACK, _stream())
+            _flags(fallback, phase), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))

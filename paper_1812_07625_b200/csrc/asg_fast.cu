@@ -805,17 +805,26 @@ void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w) { asg_ws_layout(d, ws, w)
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
-                            int32_t *status, cudaStream_t s, Tracer *tr) {
+                            int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
-  const size_t smem = asg_chain_smem(w.W);
-  cudaError_t err =
-      cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d,
-                                                               w, status);
-  err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
+  if (phases & 1u) {
+    const size_t smem = asg_chain_smem(w.W);
+    err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (err != cudaSuccess) return err;
+    // maximum shared-memory carveout: chain CTAs of different criteria (and
+    // several per SM) can then be co-resident on one SM configuration
+    err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (err != cudaSuccess) return err;
+    asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans,
+                                                                 d, w, status);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
   trace(tr, s);  // chain
+  if (!(phases & 2u)) return cudaSuccess;
   asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, d, w, grad_em,
                                                                     status);
   err = cudaGetLastError();

@@ -36,6 +36,12 @@ struct Carver {
   }
 };
 
+// W2L_FLAG_PHASE_* -> bit 0 chain, bit 1 gradient (neither flag: both)
+unsigned phase_mask(unsigned flags) {
+  unsigned m = ((flags & W2L_FLAG_PHASE_CHAIN) ? 1u : 0u) | ((flags & W2L_FLAG_PHASE_GRAD) ? 2u : 0u);
+  return m ? m : 3u;
+}
+
 int asg_slots(int B) { return B < kMaxExactSlotsFallback ? B : kMaxExactSlotsFallback; }
 int asg_slots_f64(int B) { return B < kMaxExactSlotsF64 ? B : kMaxExactSlotsF64; }
 
@@ -139,14 +145,19 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   void *slots;
   asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
+  const unsigned phases = phase_mask(flags);
   trace(tr, s);
-  int rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad,
-                                                w.perm, w.tok_start, status, s));
-  if (rc) return rc;
+  int rc = W2L_OK;
+  if (phases & 1u) {
+    rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
+                                              w.tok_start, status, s));
+    if (rc) return rc;
+  }
   trace(tr, s);  // validate
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
-                                 status, s, tr));
+                                 status, s, tr, phases));
   if (rc) return rc;
+  if (!(phases & 2u)) return W2L_OK;
   if (fallback) {
     rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
                                            slots, loss, grad_em, ga, status, s));
@@ -270,14 +281,19 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   CtcFastWs w;
   void *slots;
   ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
+  const unsigned phases = phase_mask(flags);
   trace(tr, s);
-  int rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
-                                                w.perm, w.tok_start, status, s));
-  if (rc) return rc;
+  int rc = W2L_OK;
+  if (phases & 1u) {
+    rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
+                                              w.perm, w.tok_start, status, s));
+    if (rc) return rc;
+  }
   trace(tr, s);  // validate
-  rc = from_cuda(
-      launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status, s, tr));
+  rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
+                                 s, tr, phases));
   if (rc) return rc;
+  if (!(phases & 2u)) return W2L_OK;
   if (!(flags & W2L_FLAG_NO_FALLBACK))
     rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
                                            asg_slots(B), slots, loss, grad_em, status, s));

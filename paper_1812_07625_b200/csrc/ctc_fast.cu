@@ -253,17 +253,26 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w)
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
-                            Tracer *tr) {
+                            Tracer *tr, unsigned phases) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
-  const size_t smem = ctc_chain_smem(w.W);
-  cudaError_t err =
-      cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  ctc_chain_kernel<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank, d,
-                                                               w, status);
-  err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
+  if (phases & 1u) {
+    const size_t smem = ctc_chain_smem(w.W);
+    err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (err != cudaSuccess) return err;
+    // maximum shared-memory carveout: chain CTAs of different criteria (and
+    // several per SM) can then be co-resident on one SM configuration
+    err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (err != cudaSuccess) return err;
+    ctc_chain_kernel<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank,
+                                                                 d, w, status);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
   trace(tr, s);  // chain
+  if (!(phases & 2u)) return cudaSuccess;
   switch (w.W) {
     case 1: err = launch_ctc_grad_w<1>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
     case 2: err = launch_ctc_grad_w<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;

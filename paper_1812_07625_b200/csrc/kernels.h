@@ -74,7 +74,8 @@ void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w);
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
-                            int32_t *status, cudaStream_t s, Tracer *tr = nullptr);
+                            int32_t *status, cudaStream_t s, Tracer *tr = nullptr,
+                            unsigned phases = 3u);   // bit 0: chain, bit 1: gradient
 
 struct CtcFastWs {
   float *a, *b;              // [B][W][Tmax][128] warp-major lattice rows
@@ -91,7 +92,7 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w);
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
-                            Tracer *tr = nullptr);
+                            Tracer *tr = nullptr, unsigned phases = 3u);
 
 // ---- reductions
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,

@@ -215,7 +215,11 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
     if (lane < rows) {
       float *dd = sm.ering[ring_slot(c.fwd, p0 + lane)];
 #pragma unroll
+#ifdef W2L_EXP_PRODFAST
+      for (int i = 0; i < 32; ++i) dd[i] = i < c.N ? x[i] : 0.f;
+#else
       for (int i = 0; i < 32; ++i) dd[i] = i < c.N ? et_of(x[i], m) : 0.f;
+#endif
       dd[32] = 0.f;
       shifts += (double)m;
     }
@@ -407,8 +411,14 @@ __device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo,
 
 __device__ __forceinline__ void lat_store_row(const float (&v)[kSpl], int ex, float *row,
                                               int *erow, int lane) {
+#ifdef W2L_EXP_NOSTORE
+  if (ex == 12345) {
+#endif
   reinterpret_cast<float4 *>(row)[lane] = make_float4(v[0], v[1], v[2], v[3]);
   erow[lane] = ex;
+#ifdef W2L_EXP_NOSTORE
+  }
+#endif
 }
 
 // Run a lattice warp over the whole utterance; its share of the recursion's

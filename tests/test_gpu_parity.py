@@ -334,3 +334,27 @@ def test_fast_path_holds_on_peaky_emissions():
     loss, ge = orc.ctc_batch(em, el, tc, tl, blank)
     np.testing.assert_allclose(outc.loss.cpu().numpy(), loss, rtol=REL)
     assert orc.rel_err(outc.grad_emissions.cpu().numpy(), ge) < REL
+
+
+def test_split_phase_calls_match_whole_calls():
+    # W2L_FLAG_PHASE_CHAIN then W2L_FLAG_PHASE_GRAD == one whole call
+    em, el, tg, tl, a = orc.synth_asg(31, 3, 120, 7, 12)
+    ws = torch.empty(C.nat.lib().w2l_asg_workspace_bytes(3, 120, 7, 12), dtype=torch.uint8,
+                     device="cuda")
+    x = torch.from_numpy(em).cuda()
+    whole = C.asg_loss_grad_batched(x, el, tg, tl, a)
+    part = C.asg_loss_grad_batched(x, el, tg, tl, a, workspace=ws, phase="chain")
+    part = C.asg_loss_grad_batched(x, el, tg, tl, a, workspace=ws, out=part, phase="grad")
+    assert torch.equal(whole.loss, part.loss)
+    assert torch.equal(whole.grad_emissions, part.grad_emissions)
+    assert torch.equal(whole.grad_transitions, part.grad_transitions)
+    emc, elc, tgc, tlc, blank = orc.synth_ctc(32, 3, 90, 6, 10)
+    xc = torch.from_numpy(emc).cuda()
+    wsc = torch.empty(C.nat.lib().w2l_ctc_workspace_bytes(3, 90, 6, 10), dtype=torch.uint8,
+                      device="cuda")
+    whole = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank)
+    part = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, workspace=wsc, phase="chain")
+    part = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, workspace=wsc, out=part,
+                                   phase="grad")
+    assert torch.equal(whole.loss, part.loss)
+    assert torch.equal(whole.grad_emissions, part.grad_emissions)
