@@ -332,6 +332,32 @@ size_t asg_chain_smem(int W) {
 }
 
 // ----------------------------------------------------------- grad kernel --
+// sum of the shared-memory floats at addresses addr[q0 .. q1) (4 independent
+// chains; addresses are absolute shared-window addresses)
+__device__ __forceinline__ float lds_f32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float gather_shared(const unsigned *addr, int q0, int q1) {
+  float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+  int q = q0;
+  for (; q + 4 <= q1; q += 4) {
+    const unsigned a0 = addr[q], a1 = addr[q + 1], a2 = addr[q + 2], a3 = addr[q + 3];
+    c0 += lds_f32(a0);
+    c1 += lds_f32(a1);
+    c2 += lds_f32(a2);
+    c3 += lds_f32(a3);
+  }
+  // tail of up to 3 (independent loads, predicated)
+  const int r = q1 - q;
+  const unsigned a0 = r > 0 ? addr[q] : 0u, a1 = r > 1 ? addr[q + 1] : 0u, a2 = r > 2 ? addr[q + 2] : 0u;
+  if (r > 0) c0 += lds_f32(a0);
+  if (r > 1) c1 += lds_f32(a1);
+  if (r > 2) c2 += lds_f32(a2);
+  return (c0 + c1) + (c2 + c3);
+}
+
 // 2^x as a float for integer x clamped to [-127, 127] (0 below)
 __device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
 
@@ -455,7 +481,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   float *prow = redE + kGradWarps * 2 * LP;      // [kGradWarps][LP] posterior row
   float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
   float *gwarp = erow + kGradWarps * 64;         // [kGradWarps][2] guard
-  int *sperm = reinterpret_cast<int *>(gwarp + kGradWarps * 2);   // [LP]
+  // per-warp token CSR as absolute shared addresses into that warp's
+  // posterior row (the gather is then load-address, load-value, add)
+  unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][LP]
 
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -488,9 +516,13 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
       const int l = sw * kLatStates + lane * kSpl + k;
       tok[sw][k] = l < L ? (int)y[l] : N;
     }
-  for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
   float *myp = prow + warp * LP;
   float *mye = erow + warp * 64;
+  unsigned *myaddr = saddr + warp * LP;
+  {
+    const unsigned base = (unsigned)__cvta_generic_to_shared(myp);
+    for (int i = lane; i < L; i += 32) myaddr[i] = base + 4u * (unsigned)w.perm[(size_t)b * w.lpad + i];
+  }
   mye[32 + lane] = 0.f;   // columns N.. of the Et row: padding states read 0
   __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
@@ -529,9 +561,15 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
       pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
     }
   }
+  // the emission and the gradient-row value (written by asg_fcc_grad) of the
+  // next frame are loaded one frame ahead
+  float e_nx = 0.f, g_nx = 0.f;
+  if (ta < tend && lane < N) {
+    e_nx = emb[(unsigned)ta * N + lane];
+    g_nx = ge[(unsigned)ta * N + lane];
+  }
   for (int t = ta; t < tend; ++t) {
     const unsigned tq = (unsigned)t * 32;
-    const float e = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
     float4 va[W], vb[W];
     int ea[W], eb[W];
 #pragma unroll
@@ -540,6 +578,12 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
       vb[sw] = B4[sw * segq + tq];
       ea[sw] = EA[sw * sege + tq];
       eb[sw] = EB[sw * sege + tq];
+    }
+    const float e = lane < N ? e_nx : -CUDART_INF_F;
+    const float g_old = g_nx;
+    if (t + 1 < tend && lane < N) {
+      e_nx = emb[(unsigned)(t + 1) * N + lane];
+      g_nx = ge[(unsigned)(t + 1) * N + lane];
     }
     const float m = warp_max(e);
     mye[lane] = lane < N ? et_of(e, m) : 0.f;
@@ -563,16 +607,8 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     gmax = fmaxf(gmax, g);
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-    int q = ts0;
-    for (; q + 4 <= ts1; q += 4) {
-      c0 += myp[sperm[q]];
-      c1 += myp[sperm[q + 1]];
-      c2 += myp[sperm[q + 2]];
-      c3 += myp[sperm[q + 3]];
-    }
-    for (; q < ts1; ++q) c0 += myp[sperm[q]];
-    if (lane < N) ge[tq / 32 * N + lane] -= ((c0 + c1) + (c2 + c3)) * izc;
+    const float con = gather_shared(myaddr, ts0, ts1);
+    if (lane < N) ge[tq / 32 * N + lane] = g_old - con * izc;
     if (t >= 1) {
       // fac edge posteriors (:218-224): alpha_{t-1} (stay: same state, step:
       // previous state) times Et[y] beta'_t (times S|P later)
@@ -746,7 +782,7 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                           float *grad_em, const int32_t *status, cudaStream_t s) {
   constexpr int LP = W * kLatStates;
-  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2) + LP);
+  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2 + LP));
   auto k = asg_fac_grad_kernel<W>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
