@@ -441,9 +441,20 @@ def main():
         ms_c = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
                                                       check=False, workspace=ws_c, out=out_c))
         ms_v = timeit(lambda: C.viterbi_batched(em_d, el_d, A_d, check=False))
+        # SURVEY f3 (evaluation: loss only) and f1 (CTC on logits, log_softmax fused)
+        ms_al = timeit(lambda: C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False,
+                                                       workspace=ws_a, out=out_a, loss_only=True))
+        ms_cl = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
+                                                       check=False, workspace=ws_c, out=out_c,
+                                                       loss_only=True))
+        ms_cx = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
+                                                       check=False, workspace=ws_c, out=out_c,
+                                                       logits=True))
         sub.update({"asg_only_frames_per_s": frames / (ms_a / 1e3), "asg_only_ms": ms_a,
                     "ctc_only_frames_per_s": frames / (ms_c / 1e3), "ctc_only_ms": ms_c,
-                    "viterbi_frames_per_s": frames / (ms_v / 1e3), "viterbi_ms": ms_v})
+                    "viterbi_frames_per_s": frames / (ms_v / 1e3), "viterbi_ms": ms_v,
+                    "asg_loss_only_ms": ms_al, "ctc_loss_only_ms": ms_cl,
+                    "ctc_logits_fused_ms": ms_cx})
 
     cpu = None
     if pool is not None:

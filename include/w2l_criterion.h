@@ -67,6 +67,14 @@ enum {
  * gradient phases. */
 #define W2L_FLAG_PHASE_CHAIN 2u
 #define W2L_FLAG_PHASE_GRAD 4u
+/* Loss only (evaluation): the forward recursion and the loss; no
+ * posterior/gradient kernels and no transition gradient (grad_em is written
+ * only for utterances recomputed by the float64 fallback). */
+#define W2L_FLAG_LOSS_ONLY 8u
+/* CTC on unnormalised logits with log-softmax fused in: the loss
+ * is that of log_softmax(x) (autodiff.py:394-411) and grad_em is the gradient
+ * with respect to x; the |row logsumexp| <= 1e-2 contract does not apply. */
+#define W2L_FLAG_CTC_LOGITS 16u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

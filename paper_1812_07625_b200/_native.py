@@ -58,6 +58,8 @@ OK, ERR_CONTRACT, ERR_NUMERIC, ERR_TARGET, ERR_INFEASIBLE, ERR_CUDA, ERR_COMM, E
 FLAG_NO_FALLBACK = 1
 FLAG_PHASE_CHAIN = 2
 FLAG_PHASE_GRAD = 4
+FLAG_LOSS_ONLY = 8
+FLAG_CTC_LOGITS = 16
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

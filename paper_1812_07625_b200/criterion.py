@@ -353,8 +353,12 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
     return em, el, tg, tl
 
 
-def _flags(fallback: bool, phase: str) -> int:
+def _flags(fallback: bool, phase: str, loss_only: bool = False, logits: bool = False) -> int:
     f = 0 if fallback else nat.FLAG_NO_FALLBACK
+    if loss_only:
+        f |= nat.FLAG_LOSS_ONLY
+    if logits:
+        f |= nat.FLAG_CTC_LOGITS
     if phase == "chain":
         f |= nat.FLAG_PHASE_CHAIN
     elif phase == "grad":
@@ -377,7 +381,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
                           per_utterance_grad_transitions=False, workspace=None,
                           out: Optional[BatchLossOutput] = None,
                           fallback: bool = True, trace: bool = False,
-                          phase: str = "all") -> BatchLossOutput:
+                          phase: str = "all", loss_only: bool = False) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -390,7 +394,10 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     report W2L_ERR_PRECISION instead) -- a diagnostic for the fast path.
     phase="chain" | "grad" splits the call (W2L_FLAG_PHASE_*): "chain" runs
     the recursions into the workspace, a later "grad" call with the same
-    inputs, workspace and out on the same stream order finishes it."""
+    inputs, workspace and out on the same stream order finishes it.
+    loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the forward
+    recursion and the loss only: grad_emissions / grad_transitions are not
+    computed."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -412,7 +419,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
-            _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase), _stream())
+            _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase, loss_only), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_asg_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -428,10 +435,15 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
 def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *, check=True,
                           workspace=None, out: Optional[BatchLossOutput] = None,
                           fallback: bool = True, trace: bool = False,
-                          phase: str = "all") -> BatchLossOutput:
+                          phase: str = "all", loss_only: bool = False,
+                          logits: bool = False) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
-    log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase: as
-    for asg_loss_grad_batched."""
+    log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase and
+    loss_only: as for asg_loss_grad_batched.  logits=True
+    (W2L_FLAG_CTC_LOGITS): emissions are unnormalised logits with
+    log_softmax fused in (autodiff.py:394-411); the loss is that of
+    log_softmax(emissions) and grad_emissions is the gradient with respect to
+    the logits (softmax - posterior)."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -447,7 +459,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
-            _flags(fallback, phase), _stream())
+            _flags(fallback, phase, loss_only, logits), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -504,15 +516,16 @@ class _AsgLossFn(torch.autograd.Function):
 
 class _CtcLossFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, logp, em_len, targets, tgt_len, blank_id):
-        out = ctc_loss_grad_batched(logp.detach(), em_len, targets, tgt_len, blank_id)
+    def forward(ctx, logp, em_len, targets, tgt_len, blank_id, logits=False):
+        out = ctc_loss_grad_batched(logp.detach(), em_len, targets, tgt_len, blank_id,
+                                    logits=logits)
         ctx.save_for_backward(out.grad_emissions)
         return out.loss.to(logp.dtype)
 
     @staticmethod
     def backward(ctx, g):
         (ge,) = ctx.saved_tensors
-        return (ge * g.to(torch.float32)[:, None, None], None, None, None, None)
+        return (ge * g.to(torch.float32)[:, None, None], None, None, None, None, None)
 
 
 def asg_loss(emissions, transitions, em_len, targets, tgt_len) -> torch.Tensor:
@@ -520,9 +533,10 @@ def asg_loss(emissions, transitions, em_len, targets, tgt_len) -> torch.Tensor:
     return _AsgLossFn.apply(emissions, transitions, em_len, targets, tgt_len)
 
 
-def ctc_loss(logp, em_len, targets, tgt_len, blank_id: int) -> torch.Tensor:
-    """Differentiable per-utterance CTC losses [B] on log-probabilities."""
-    return _CtcLossFn.apply(logp, em_len, targets, tgt_len, blank_id)
+def ctc_loss(logp, em_len, targets, tgt_len, blank_id: int, logits: bool = False) -> torch.Tensor:
+    """Differentiable per-utterance CTC losses [B] on log-probabilities, or on
+    unnormalised logits with log_softmax fused in (logits=True)."""
+    return _CtcLossFn.apply(logp, em_len, targets, tgt_len, blank_id, logits)
 
 
 # ------------------------------------------------------ trainer adapters --

@@ -267,7 +267,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, 
   const float amax = trans_max(trans, d.N);
   const int weff = lat_warps(L);
   if (warp == 0) {
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W};
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W, 0};
     producer_run(sm, pc, lane, nullptr);
   } else if (warp == 1) {
     FccCtx fc;
@@ -777,6 +777,15 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// loss only: fcc minus fac forward totals; non-finite -> float64
+__global__ void asg_loss_only_kernel(Dims d, AsgFastWs w, double *loss, int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B || status[b] != W2L_OK) return;
+  const double zF = w.scal[b * 4 + 0], zC = w.scal[b * 4 + 2];
+  loss[b] = zF - zC;                                         // criterion.py:244
+  if (!isfinite(zF - zC)) status[b] = kNeedsExact;
+}
+
 template <int W>
 cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
@@ -844,7 +853,7 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
                             int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
   cudaError_t err = cudaSuccess;
-  if (phases & 1u) {
+  if (phases & 5u) {
     const size_t smem = asg_chain_smem(w.W);
     err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
@@ -854,12 +863,17 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
     err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
-    asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans,
-                                                                 d, w, status);
+    // loss only: the forward CTA alone (blockIdx.y == 0)
+    asg_chain_kernel<<<dim3(d.B, (phases & 4u) ? 1 : 2), 32 * (2 + w.W), smem, s>>>(
+        em, em_len, tgt, tgt_len, trans, d, w, status);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
+  if (phases & 4u) {
+    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(d, w, loss, status);
+    return cudaGetLastError();
+  }
   if (!(phases & 2u)) return cudaSuccess;
   asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, d, w, grad_em,
                                                                     status);

@@ -145,7 +145,8 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   void *slots;
   asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
-  const unsigned phases = phase_mask(flags);
+  const bool loss_only = flags & W2L_FLAG_LOSS_ONLY;
+  const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
   trace(tr, s);
   int rc = W2L_OK;
   if (phases & 1u) {
@@ -157,6 +158,12 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
                                  status, s, tr, phases));
   if (rc) return rc;
+  if (loss_only) {
+    if (fallback)
+      rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
+                                             slots, loss, grad_em, ga, status, s));
+    return rc;
+  }
   if (!(phases & 2u)) return W2L_OK;
   if (fallback) {
     rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
@@ -281,22 +288,28 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   CtcFastWs w;
   void *slots;
   ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
-  const unsigned phases = phase_mask(flags);
+  const bool loss_only = flags & W2L_FLAG_LOSS_ONLY;
+  const int logits = (flags & W2L_FLAG_CTC_LOGITS) ? 1 : 0;
+  w.logits = logits;
+  const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
   trace(tr, s);
   int rc = W2L_OK;
   if (phases & 1u) {
+    // logits: the |row logsumexp| <= 1e-2 contract (criterion.py:96-101) does
+    // not apply to unnormalised inputs
     rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
-                                              w.perm, w.tok_start, status, s));
+                                              w.perm, w.tok_start, status, s, !logits));
     if (rc) return rc;
   }
   trace(tr, s);  // validate
   rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
                                  s, tr, phases));
   if (rc) return rc;
-  if (!(phases & 2u)) return W2L_OK;
+  if (!loss_only && !(phases & 2u)) return W2L_OK;
   if (!(flags & W2L_FLAG_NO_FALLBACK))
     rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
-                                           asg_slots(B), slots, loss, grad_em, status, s));
+                                           asg_slots(B), slots, loss, grad_em, status, s,
+                                           logits));
   trace(tr, s);  // exact fallback
   return rc;
 }

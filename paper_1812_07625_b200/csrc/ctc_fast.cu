@@ -32,7 +32,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm &sm, unsigned char *dsm, 
   const int S = 2 * L + 1;
   const int weff = lat_warps(S);
   if (warp == 0) {
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, W};
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, W, w.logits};
     producer_run(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
   } else if (warp - 1 < weff) {
     LatCtx c;
@@ -162,7 +162,14 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       c3 += myp[sperm[q + 3]];
     }
     for (; q < ts1; ++q) c0 += myp[sperm[q]];
-    if (lane < N) ge[(unsigned)t * N + lane] = -((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
+    float sm_k = 0.f;
+    if (w.logits) {   // gradient w.r.t. logits: softmax - posterior
+      const float x = lane < N ? em[((size_t)b * d.Tmax + t) * N + lane] : -CUDART_INF_F;
+      const float mx = warp_max(x);
+      const float ex = lane < N ? __expf(x - mx) : 0.f;
+      sm_k = ex / warp_sum(ex);
+    }
+    if (lane < N) ge[(unsigned)t * N + lane] = sm_k - ((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
     __syncwarp();
   }
   if (lane == 0) {
@@ -211,6 +218,15 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
   }
 }
 
+// loss only: forward total and shifts; non-finite -> float64
+__global__ void ctc_loss_only_kernel(Dims d, CtcFastWs w, double *loss, int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B || status[b] != W2L_OK) return;
+  const double zA = w.scal[b * 4 + 0], shifts = w.scal[b * 4 + 2];
+  loss[b] = -(zA + shifts);                                  // criterion.py:162
+  if (!isfinite(zA + shifts)) status[b] = kNeedsExact;
+}
+
 }  // namespace
 
 #ifdef W2L_PROF
@@ -243,6 +259,7 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
   t.W = W;
   t.lpad = lpad;
   t.nblk = nblk;
+  t.logits = 0;
   if (w) *w = t;
   return off;
 }
@@ -256,7 +273,7 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
                             Tracer *tr, unsigned phases) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
   cudaError_t err = cudaSuccess;
-  if (phases & 1u) {
+  if (phases & 5u) {
     const size_t smem = ctc_chain_smem(w.W);
     err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
@@ -266,12 +283,17 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
     err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
-    ctc_chain_kernel<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank,
-                                                                 d, w, status);
+    // loss only: the forward CTA alone (blockIdx.y == 0)
+    ctc_chain_kernel<<<dim3(d.B, (phases & 4u) ? 1 : 2), 32 * (1 + w.W), smem, s>>>(
+        em, em_len, tgt, tgt_len, blank, d, w, status);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
+  if (phases & 4u) {
+    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(d, w, loss, status);
+    return cudaGetLastError();
+  }
   if (!(phases & 2u)) return cudaSuccess;
   switch (w.W) {
     case 1: err = launch_ctc_grad_w<1>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;

@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(kExactThreads)
 // --------------------------------------------------------------- CTC -----
 __host__ __device__ inline size_t ctc_slot_bytes(int Tmax, int Lmax) {
   const int S = 2 * Lmax + 1;
-  return align_up((size_t)Tmax * S * 2 * sizeof(double), 256);
+  // alpha, beta [T][S] and the per-frame log-softmax normaliser (logits mode)
+  return align_up((size_t)Tmax * S * 2 * sizeof(double) + (size_t)Tmax * sizeof(double), 256);
 }
 
 template <class TE>
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kExactThreads)
     ctc_exact_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, int only_flagged, int nslots, uint8_t *slot_ws,
-                     double *loss, float *grad_em, int32_t *status) {
+                     double *loss, float *grad_em, int32_t *status, int logits) {
   extern __shared__ __align__(16) double sm[];
   const int N = d.N, Smax = 2 * d.Lmax + 1;
   double *rows = sm;                         // 2 chains x 2 buffers x Smax
@@ -273,12 +274,24 @@ __global__ void __launch_bounds__(kExactThreads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *alpha = (double *)(slot_ws + ctc_slot_bytes(d.Tmax, d.Lmax) * blockIdx.x);
   double *beta = alpha + (size_t)d.Tmax * Smax;
+  double *lse = beta + (size_t)d.Tmax * Smax;   // [Tmax] logits mode
 
   for (int b = blockIdx.x; b < d.B; b += nslots) {
     __syncthreads();
     if (!wants(status[b], only_flagged)) continue;
     const int T = em_len[b], L = tgt_len[b], S = 2 * L + 1;
     const TE *e = em + (size_t)b * d.Tmax * N;
+    // logits: log_softmax rows in float64 (autodiff.py:400-403): x - lse(x)
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      double m = -CUDART_INF, acc = 0.0;
+      if (logits) {
+        for (int i = 0; i < N; ++i) m = fmax(m, (double)e[(size_t)t * N + i]);
+        for (int i = 0; i < N; ++i) acc += exp((double)e[(size_t)t * N + i] - m);
+        lse[t] = m + log(acc);
+      } else {
+        lse[t] = 0.0;
+      }
+    }
     const int64_t *yb = tgt + (size_t)b * d.Lmax;
     // lattice (criterion.py:113-120)
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -286,7 +299,7 @@ __global__ void __launch_bounds__(kExactThreads)
       skip[s] = (s & 1) && s >= 3 && yb[s >> 1] != yb[(s >> 1) - 1];
     }
     __syncthreads();
-    auto EL = [&](int t, int s) { return (double)e[(size_t)t * N + lab[s]]; };
+    auto EL = [&](int t, int s) { return (double)e[(size_t)t * N + lab[s]] - lse[t]; };
 
     if (warp == 0) {                                                  // alpha (:122-141)
       double *buf = rows;
@@ -357,6 +370,8 @@ __global__ void __launch_bounds__(kExactThreads)
                                 EL(t, s) - logz);
         g[lab[s]] -= post;
       }
+      if (logits)   // d/dx of log_softmax: g - softmax * sum(g), sum(g) = -1
+        for (int i = 0; i < N; ++i) g[i] += exp((double)e[(size_t)t * N + i] - lse[t]);
       for (int i = 0; i < N; ++i) ge[(size_t)t * N + i] = (float)g[i];
     }
     if (threadIdx.x == 0) {
@@ -398,7 +413,7 @@ template <class TE>
 cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t *tgt,
                              const int32_t *tgt_len, int blank, Dims d, int only_flagged,
                              int nslots, void *slot_ws, double *loss, float *grad_em,
-                             int32_t *status, cudaStream_t s) {
+                             int32_t *status, cudaStream_t s, int logits) {
   const int Smax = 2 * d.Lmax + 1;
   const size_t smem = sizeof(double) * 4 * Smax + sizeof(int) * 2 * Smax;
   auto k = ctc_exact_kernel<TE>;
@@ -406,7 +421,8 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
                                          (int)smem);
   if (err != cudaSuccess) return err;
   k<<<nslots, kExactThreads, smem, s>>>(em, em_len, tgt, tgt_len, blank, d, only_flagged,
-                                         nslots, (uint8_t *)slot_ws, loss, grad_em, status);
+                                         nslots, (uint8_t *)slot_ws, loss, grad_em, status,
+                                         logits);
   return cudaGetLastError();
 }
 
@@ -417,7 +433,7 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
                                             cudaStream_t);                                  \
   template cudaError_t launch_ctc_exact<TE>(const TE *, const int32_t *, const int64_t *,   \
                                             const int32_t *, int, Dims, int, int, void *,   \
-                                            double *, float *, int32_t *, cudaStream_t);
+                                            double *, float *, int32_t *, cudaStream_t, int);
 INST(float)
 INST(double)
 #undef INST

@@ -33,7 +33,8 @@ cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
-                                int *tok_start, int32_t *status, cudaStream_t s);
+                                int *tok_start, int32_t *status, cudaStream_t s,
+                                int check_lse = 1);
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s);
@@ -52,7 +53,7 @@ template <class TE>
 cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t *tgt,
                              const int32_t *tgt_len, int blank, Dims d, int only_flagged,
                              int nslots, void *slot_ws, double *loss, float *grad_em,
-                             int32_t *status, cudaStream_t s);
+                             int32_t *status, cudaStream_t s, int logits = 0);
 
 // ---- fp32 fast path
 struct AsgFastWs {
@@ -85,6 +86,7 @@ struct CtcFastWs {
   int *perm;                 // [B][Lpad] label positions sorted by token
   int *tok_start;            // [B][33]
   int spl, W, lpad, nblk;
+  int logits;                // W2L_FLAG_CTC_LOGITS: log-softmax fused in
 };
 int ctc_fast_spl(int Lmax);
 size_t ctc_fast_ws_bytes(Dims d);
@@ -93,6 +95,7 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
                             Tracer *tr = nullptr, unsigned phases = 3u);
+// phases bit 2 (value 4): loss only -- forward recursion + loss, no gradients
 
 // ---- reductions
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,

@@ -125,18 +125,12 @@ __device__ __forceinline__ void wait3(const int *p0, int n0, const int *p1, int 
     const int a = ld_relaxed(p0), b = ld_relaxed(p1), c = ld_relaxed(p2);
     if (a >= n0 && b >= n1 && c >= n2) break;
   }
-#ifndef W2L_EXPERIMENT_RELAXED
   fence_acq_rel_cta();
-#endif
 }
 // all lanes' shared-memory writes are ordered before lane 0's release
 __device__ __forceinline__ void publish(int *p, int v, int lane) {
   __syncwarp();
-#ifdef W2L_EXPERIMENT_RELAXED
-  if (lane == 0) asm volatile("st.relaxed.cta.shared.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
-#else
   if (lane == 0) st_release(p, v);
-#endif
   __syncwarp();
 }
 
@@ -145,6 +139,7 @@ struct ProdCtx {
   int N, T;
   bool fwd;
   int nconsumers;  // counters cons[0 .. nconsumers) gate ring reuse
+  int logits;      // shift term: 0 = max_i e (log-probs), 1 = -log sum_i Et (logits)
 };
 
 // frame of processing index p
@@ -214,14 +209,17 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
     fence_acq_rel_cta();
     if (lane < rows) {
       float *dd = sm.ering[ring_slot(c.fwd, p0 + lane)];
+      float se = 0.f;
 #pragma unroll
-#ifdef W2L_EXP_PRODFAST
-      for (int i = 0; i < 32; ++i) dd[i] = i < c.N ? x[i] : 0.f;
-#else
-      for (int i = 0; i < 32; ++i) dd[i] = i < c.N ? et_of(x[i], m) : 0.f;
-#endif
+      for (int i = 0; i < 32; ++i) {
+        const float v = i < c.N ? et_of(x[i], m) : 0.f;
+        dd[i] = v;
+        se += v;
+      }
       dd[32] = 0.f;
-      shifts += (double)m;
+      // log-probs: the frame's shift is its max; logits (log-softmax fused):
+      // max logp = -log sum_i exp(x_i - max x)
+      shifts += c.logits ? -log((double)se) : (double)m;
     }
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
@@ -411,14 +409,8 @@ __device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo,
 
 __device__ __forceinline__ void lat_store_row(const float (&v)[kSpl], int ex, float *row,
                                               int *erow, int lane) {
-#ifdef W2L_EXP_NOSTORE
-  if (ex == 12345) {
-#endif
   reinterpret_cast<float4 *>(row)[lane] = make_float4(v[0], v[1], v[2], v[3]);
   erow[lane] = ex;
-#ifdef W2L_EXP_NOSTORE
-  }
-#endif
 }
 
 // Run a lattice warp over the whole utterance; its share of the recursion's

@@ -237,8 +237,8 @@ cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
-                                int *tok_start, int32_t *status, cudaStream_t s) {
-  cudaError_t err = em_check<TE>(em, em_len, d, 1, status, s);
+                                int *tok_start, int32_t *status, cudaStream_t s, int check_lse) {
+  cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s);
   if (err != cudaSuccess) return err;
   ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
                                       status);
@@ -259,7 +259,7 @@ cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                                int *, int32_t *, cudaStream_t);               \
   template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, int, Dims, int, int *, int *, \
-                                               int32_t *, cudaStream_t);                      \
+                                               int32_t *, cudaStream_t, int);                 \
   template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,         \
                                                    int32_t *, cudaStream_t);
 INST(float)

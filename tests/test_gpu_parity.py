@@ -358,3 +358,67 @@ def test_split_phase_calls_match_whole_calls():
                                    phase="grad")
     assert torch.equal(whole.loss, part.loss)
     assert torch.equal(whole.grad_emissions, part.grad_emissions)
+
+
+def _ctc_logits_oracle(x, el, tg, tl, blank):
+    # the reference composition: log_softmax (float32 out, autodiff.py:394-411),
+    # CTC on it, then the log_softmax backward g - softmax * sum(g)
+    logp = orc.log_softmax_rows(x).astype(np.float32)
+    loss, g = orc.ctc_batch(logp, el, tg, tl, blank)
+    sm = np.exp(logp.astype(np.float64))
+    gx = g - sm * g.sum(axis=-1, keepdims=True)
+    for b in range(x.shape[0]):
+        gx[b, el[b]:] = 0.0
+    return loss, gx
+
+
+def test_ctc_logits_fused_log_softmax():
+    # CTC on logits with log_softmax fused in, vs the reference
+    # composition; ragged batch, and the bench shape on a subset
+    rng = np.random.default_rng(41)
+    em, el, tg, tl, blank = orc.synth_ctc(41, 4, 160, 9, 20, ragged=True)
+    x = (3.0 * rng.standard_normal(em.shape)).astype(np.float32)
+    out = C.ctc_loss_grad_batched(torch.from_numpy(x).cuda(), el, tg, tl, blank, logits=True,
+                                  fallback=False)
+    loss, gx = _ctc_logits_oracle(x, el, tg, tl, blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), gx) < REL
+    em, el, tg, tl, blank = orc.synth_ctc(42, 3, 1600, 30, 300)
+    x = (2.0 * rng.standard_normal(em.shape)).astype(np.float32)
+    out = C.ctc_loss_grad_batched(torch.from_numpy(x).cuda(), el, tg, tl, blank, logits=True,
+                                  fallback=False)
+    loss, gx = _ctc_logits_oracle(x, el, tg, tl, blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), gx) < REL
+
+
+def test_ctc_logits_float64_fallback():
+    # extreme logits break the fp32 lattice; the float64 recompute (logits mode
+    # of the exact kernel) must still match the reference composition
+    rng = np.random.default_rng(43)
+    em, el, tg, tl, blank = orc.synth_ctc(43, 3, 12, 5, 3)
+    x = (400.0 * rng.standard_normal(em.shape)).astype(np.float32)
+    out = C.ctc_loss_grad_batched(torch.from_numpy(x).cuda(), el, tg, tl, blank, logits=True,
+                                  check=False)
+    loss, gx = _ctc_logits_oracle(x, el, tg, tl, blank)
+    ok = np.isfinite(loss)
+    np.testing.assert_allclose(out.loss.cpu().numpy()[ok], loss[ok], rtol=1e-5)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy()[ok], gx[ok]) < 1e-5
+
+
+def test_loss_only_mode_matches_full_call():
+    # forward recursion + loss only (evaluation)
+    em, el, tg, tl, a = orc.synth_asg(44, 5, 300, 12, 40, ragged=True)
+    x = torch.from_numpy(em).cuda()
+    full = C.asg_loss_grad_batched(x, el, tg, tl, a)
+    lo = C.asg_loss_grad_batched(x, el, tg, tl, a, loss_only=True)
+    assert torch.equal(full.loss, lo.loss)
+    emc, elc, tgc, tlc, blank = orc.synth_ctc(45, 5, 300, 12, 40, ragged=True)
+    xc = torch.from_numpy(emc).cuda()
+    full = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank)
+    lo = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, loss_only=True)
+    assert torch.equal(full.loss, lo.loss)
+    # logits + loss only
+    lo = C.ctc_loss_grad_batched(xc * 3.0, elc, tgc, tlc, blank, loss_only=True, logits=True)
+    loss, _ = _ctc_logits_oracle(emc * 3.0, elc, tgc, tlc, blank)
+    np.testing.assert_allclose(lo.loss.cpu().numpy(), loss, rtol=REL)
