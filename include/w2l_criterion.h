@@ -133,6 +133,17 @@ W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const doubl
                     int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
                     size_t ws_bytes, w2l_stream_t stream);
 
+/* ------------------------------------------------- transition update --
+ * the step after the transition-gradient all-reduce
+ * (trainer.py:442-449, autodiff.py:429-433) in one N x N kernel:
+ *   g = float32(grad_sum / batch_size); v = v * momentum + g; A = A - lr * v
+ * with the reference's float32 rounding (no fused multiply-add).
+ * trans, velocity: f32[N][N] device, updated in place; grad_sum: f32[N][N]
+ * (the batch sum, e.g. after the NCCL all-reduce). */
+W2L_API int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_sum, int N,
+                                     int batch_size, float lr, float momentum,
+                                     w2l_stream_t stream);
+
 /* ------------------------------------------------------------- tracing --
  * Same computation as w2l_asg_loss_grad / w2l_ctc_loss_grad, with a CUDA
  * event after every stage; synchronises `stream` and writes the per-stage

@@ -50,6 +50,8 @@ SIGNATURES = {
     "w2l_version": (ctypes.c_char_p, []),
     "w2l_last_cuda_error": (ctypes.c_char_p, []),
     "w2l_probe_peaks": (c_i, [c_d_p, c_d_p, c_d_p]),
+    "w2l_transitions_sgd_step": (c_i, [c_p, c_p, c_p, c_i, c_i, ctypes.c_float, ctypes.c_float,
+                                       c_p]),
 }
 
 # C-ABI status codes (include/w2l_criterion.h)

@@ -913,6 +913,26 @@ __global__ void reduce_grad_trans_kernel(const float *ga_utt, const int32_t *sta
   if (lane == 0) grad_trans[p] = (float)s;
 }
 
+// SGD with classical momentum on the transitions (autodiff.py:429-433) after
+// the /B of trainer.py:447; float32 arithmetic without contraction, as numpy
+__global__ void transitions_sgd_kernel(float *w, float *v, const float *gsum, int nn, double inv_b,
+                                       float lr, float momentum) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nn) return;
+  const float g = (float)((double)gsum[p] * inv_b);
+  const float vv = __fadd_rn(__fmul_rn(v[p], momentum), g);
+  v[p] = vv;
+  w[p] = __fsub_rn(w[p], __fmul_rn(lr, vv));
+}
+
+cudaError_t launch_transitions_sgd(float *w, float *v, const float *gsum, int N, int batch,
+                                   float lr, float momentum, cudaStream_t s) {
+  const int nn = N * N;
+  transitions_sgd_kernel<<<(nn + 255) / 256, 256, 0, s>>>(w, v, gsum, nn, 1.0 / batch, lr,
+                                                          momentum);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
                                      float *grad_trans, cudaStream_t s) {
   const int n = d.N * d.N;

@@ -398,6 +398,14 @@ int w2l_viterbi_f64(const double *em, const int32_t *em_len, const double *trans
       launch_viterbi<double, double>(em, em_len, trans, d, path, score, status, ws, s));
 }
 
+int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_sum, int N,
+                             int batch_size, float lr, float momentum, w2l_stream_t stream) {
+  if (N < 1 || N > W2L_MAX_TOKENS || batch_size < 1 || !trans || !velocity || !grad_sum)
+    return W2L_ERR_CONTRACT;
+  return from_cuda(launch_transitions_sgd(trans, velocity, grad_sum, N, batch_size, lr, momentum,
+                                          (cudaStream_t)stream));
+}
+
 int w2l_probe_peaks(double *mufu_ops_per_s, double *dadd_ops_per_s, double *ffma_ops_per_s) {
   return probe_peaks(mufu_ops_per_s, dadd_ops_per_s, ffma_ops_per_s);
 }

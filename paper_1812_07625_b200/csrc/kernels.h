@@ -101,6 +101,9 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
                                      float *grad_trans, cudaStream_t s);
 
+cudaError_t launch_transitions_sgd(float *w, float *v, const float *gsum, int N, int batch,
+                                   float lr, float momentum, cudaStream_t s);
+
 // ---- Viterbi (float64 max-plus, bit-exact)
 size_t viterbi_ws_bytes(int B, int Tmax, int N);
 template <class TE, class TA>

@@ -35,6 +35,25 @@ def allreduce_grad_transitions(grad: torch.Tensor, group=None) -> torch.Tensor:
     return grad
 
 
+def sgd_step_transitions(transitions: torch.Tensor, velocity: torch.Tensor,
+                         grad_sum: torch.Tensor, batch_size: int, lr: float,
+                         momentum: float) -> None:
+    """The step after the all-reduce (trainer.py:442-449 with the
+    optimizer of autodiff.py:429-433): g = grad_sum / B, v = momentum v + g,
+    A -= lr v, in one device kernel with the reference's float32 rounding.
+    transitions and velocity are updated in place."""
+    from . import _native as nat
+    from .criterion import _check_call, _stream
+    for t in (transitions, velocity, grad_sum):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("transitions, velocity and grad_sum must be contiguous CUDA f32")
+    n = transitions.shape[0]
+    rc = nat.lib().w2l_transitions_sgd_step(transitions.data_ptr(), velocity.data_ptr(),
+                                            grad_sum.data_ptr(), n, int(batch_size),
+                                            float(lr), float(momentum), _stream())
+    _check_call(rc, "w2l_transitions_sgd_step")
+
+
 def allreduce_loss_sum(loss: torch.Tensor, group=None) -> torch.Tensor:
     """Sum of per-utterance losses over all ranks (trainer.py:452 loss_sum)."""
     total = loss.sum().to(torch.float64).reshape(1)

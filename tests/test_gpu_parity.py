@@ -422,3 +422,22 @@ def test_loss_only_mode_matches_full_call():
     lo = C.ctc_loss_grad_batched(xc * 3.0, elc, tgc, tlc, blank, loss_only=True, logits=True)
     loss, _ = _ctc_logits_oracle(emc * 3.0, elc, tgc, tlc, blank)
     np.testing.assert_allclose(lo.loss.cpu().numpy(), loss, rtol=REL)
+
+
+def test_transitions_sgd_step_matches_reference_optimizer():
+    # /B + momentum + SGD (trainer.py:442-449, autodiff.py:429-433)
+    from paper_1812_07625_b200.distributed import sgd_step_transitions
+    rng = np.random.default_rng(46)
+    n, bsz, lr, mom = 30, 64, 0.05, 0.9
+    a = rng.standard_normal((n, n)).astype(np.float32)
+    v = rng.standard_normal((n, n)).astype(np.float32)
+    gsum = (rng.standard_normal((n, n)) * 7).astype(np.float32)
+    at, vt, gt = (torch.from_numpy(x.copy()).cuda() for x in (a, v, gsum))
+    for _ in range(3):
+        sgd_step_transitions(at, vt, gt, bsz, lr, mom)
+        g = (gsum.astype(np.float64) / bsz).astype(np.float32)
+        np.multiply(v, mom, out=v)
+        v += g
+        a = a - lr * v
+    assert np.array_equal(vt.cpu().numpy(), v)
+    assert np.array_equal(at.cpu().numpy(), a)
