@@ -30,6 +30,10 @@ class InfeasibleTargetError(TargetError):
     """No framewise alignment of the target exists for the given length (errors.py:53)."""
 
 
+class EmissionsFormatError(AsrkitError):
+    """Corrupt or incompatible emissions binary file (errors.py:78)."""
+
+
 class DeviceError(AsrkitError):
     """CUDA launch/runtime failure or collective failure in the native layer."""
 

@@ -441,3 +441,18 @@ def test_transitions_sgd_step_matches_reference_optimizer():
         a = a - lr * v
     assert np.array_equal(vt.cpu().numpy(), v)
     assert np.array_equal(at.cpu().numpy(), a)
+
+
+def test_w2le_batch_feeds_the_batched_criterion(tmp_path):
+    # W2LE files -> one pinned padded batch -> device -> ASG
+    from paper_1812_07625_b200 import emissions_io as eio
+    em, el, tg, tl, a = orc.synth_asg(47, 3, 50, 8, 9, ragged=True)
+    paths = []
+    for b in range(3):
+        paths.append(tmp_path / f"{b}.w2le")
+        eio.dump_emissions(em[b, :el[b]], paths[-1])
+    x, lens = eio.load_emissions_batch(paths, device=torch.device("cuda"))
+    out = C.asg_loss_grad_batched(x, lens, tg, tl, a)
+    loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy()[:, :x.shape[1]], ge[:, :x.shape[1]]) < REL
