@@ -1,3 +1,4 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV (second half of the launches)."""
 import csv, sys
 lines = open(sys.argv[1]).read().splitlines()
 start = [i for i,l in enumerate(lines) if l.startswith('"ID"')][0]

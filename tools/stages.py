@@ -1,4 +1,6 @@
-import sys,torch; sys.path.insert(0,".")
+"""Per-stage device times (traced calls) of one ASG and one CTC batched call at the bench shape."""
+import sys, torch
+sys.path.insert(0, ".")
 import bench
 from paper_1812_07625_b200 import criterion as C
 em, el, ta, tc, tl, A, blank = bench.make_inputs(0)
