@@ -507,6 +507,8 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
 
   const int L = tgt_len[b];
+  // segments the chain wrote for this utterance (the batch's W may be wider)
+  const int weff = min(lat_warps(L), W);
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   int tok[W][kSpl];
 #pragma unroll
@@ -556,10 +558,11 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   }
   if (ta >= 1 && ta < tend) {
 #pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-      pa[sw] = A4[sw * segq + (unsigned)(ta - 1) * 32];
-      pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
-    }
+    for (int sw = 0; sw < W; ++sw)
+      if (sw < weff) {
+        pa[sw] = A4[sw * segq + (unsigned)(ta - 1) * 32];
+        pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
+      }
   }
   // the emission and the gradient-row value (written by asg_fcc_grad) of the
   // next frame are loaded one frame ahead
@@ -574,10 +577,15 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     int ea[W], eb[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      va[sw] = A4[sw * segq + tq];
-      vb[sw] = B4[sw * segq + tq];
-      ea[sw] = EA[sw * sege + tq];
-      eb[sw] = EB[sw * sege + tq];
+      if (sw < weff) {
+        va[sw] = A4[sw * segq + tq];
+        vb[sw] = B4[sw * segq + tq];
+        ea[sw] = EA[sw * sege + tq];
+        eb[sw] = EB[sw * sege + tq];
+      } else {
+        va[sw] = vb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ea[sw] = eb[sw] = kNegExp;
+      }
     }
     const float e = lane < N ? e_nx : -CUDART_INF_F;
     const float g_old = g_nx;

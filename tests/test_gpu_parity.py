@@ -456,3 +456,47 @@ def test_w2le_batch_feeds_the_batched_criterion(tmp_path):
     loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
     np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
     assert orc.rel_err(out.grad_emissions.cpu().numpy()[:, :x.shape[1]], ge[:, :x.shape[1]]) < REL
+
+
+@pytest.mark.parametrize("t_max,n,l_max", [(1, 2, 1), (2, 2, 1), (5, 3, 2), (7, 4, 7), (9, 2, 5),
+                                           (17, 30, 8), (130, 32, 128), (260, 32, 257)])
+def test_asg_batched_edge_sizes(t_max, n, l_max):
+    # fp32 fast path at the edges of its schedule: T below one 8-step block,
+    # T = L (no slack), N = 2 and N = 32 (no spare fcc lane), lattices that
+    # end exactly on / just past a 128-state warp boundary; ragged lengths
+    em, el, tg, tl, a = orc.synth_asg(50 + t_max, 3, t_max, n, l_max, ragged=True)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a)
+    loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL, atol=1e-5)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
+
+
+@pytest.mark.parametrize("t_max,n,l_max", [(1, 2, 1), (3, 2, 0), (6, 3, 2), (9, 5, 4),
+                                           (200, 32, 63), (300, 32, 127)])
+def test_ctc_batched_edge_sizes(t_max, n, l_max):
+    # including the empty target (L = 0, CTC allows it) and T = 1
+    em, el, tg, tl, blank = orc.synth_ctc(60 + t_max, 3, t_max, n, max(l_max, 1), ragged=True)
+    if l_max == 0:
+        tg[:] = -1
+        tl[:] = 0
+    out = C.ctc_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, blank)
+    loss, ge = orc.ctc_batch(em, el, tg, tl, blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL, atol=1e-5)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+
+
+def test_maximum_lattices():
+    # the largest supported lattices: ASG L = 1024 (8 lattice warps) and CTC
+    # L = 511 (2L+1 = 1023 states, 8 warps), N = 32
+    em, el, tg, tl, a = orc.synth_asg(70, 2, 1100, 32, 1024)
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a)
+    loss, ge, ga = orc.asg_batch(em, el, tg, tl, a)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
+    emc, elc, tgc, tlc, blank = orc.synth_ctc(71, 2, 1100, 32, 511)
+    outc = C.ctc_loss_grad_batched(torch.from_numpy(emc).cuda(), elc, tgc, tlc, blank)
+    loss, ge = orc.ctc_batch(emc, elc, tgc, tlc, blank)
+    np.testing.assert_allclose(outc.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(outc.grad_emissions.cpu().numpy(), ge) < REL
