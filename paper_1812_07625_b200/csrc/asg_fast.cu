@@ -95,7 +95,9 @@ __device__ __forceinline__ float f2_hi(unsigned long long x) {
 
 // m: the lane's row of M (alpha) or column (beta); vin: the 32-vector (16B
 // aligned); 8 independent accumulators of depth 4 (scalar FFMA measured
-// faster than FFMA2 on this latency-bound chain)
+// faster than FFMA2 on this latency-bound chain).  SUM: also return the
+// exponent of the vector's sum (lane N's row of ones, or a direct sum).
+template <bool SUM>
 __device__ __forceinline__ float fcc_matvec(const float (&m)[32], const float *vin, bool spare,
                                             int N, int &e_sum) {
   const float4 *pv = reinterpret_cast<const float4 *>(vin);
@@ -109,13 +111,15 @@ __device__ __forceinline__ float fcc_matvec(const float (&m)[32], const float *v
     acc[q] = fmaf(m[4 * q + 3], x.w, acc[q]);
   }
   const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  if (spare) {
-    e_sum = exponent_of(__shfl_sync(0xffffffffu, s, N));   // lane N: row of ones
-  } else {
-    float tot = 0.f;
+  if (SUM) {
+    if (spare) {
+      e_sum = exponent_of(__shfl_sync(0xffffffffu, s, N));   // lane N: row of ones
+    } else {
+      float tot = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-    e_sum = exponent_of(tot);
+      for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
+      e_sum = exponent_of(tot);
+    }
   }
   return s;
 }
@@ -129,44 +133,53 @@ struct FccState {
   bool spare;
 };
 
-// The scale bookkeeping of a step (the sum's exponent arrives through a
-// shuffle) runs after the step's vector is stored, so the next step's
-// mat-vec does not wait behind it; the operation sequence is unchanged.
+// The power-of-two rescaling runs on every kFccRescale-th step only (RS):
+// between rescales the vector's magnitude moves by at most a few steps of
+// growth, far inside fp32's range.  The scale bookkeeping (the sum's exponent
+// arrives through a shuffle) runs after the step's vector is stored, so the
+// next step's mat-vec does not wait behind it.
+constexpr int kFccRescale = 4;
 
 // fcc alpha step t (criterion.py:230): alpha_t = Et (.) (M alpha_{t-1}) 2^-k
+template <bool RS>
 __device__ __forceinline__ void fcc_alpha_step(FccState &f, float et, float (*vec)[32],
                                                int par, float *out_row, int *outk_t, int lane,
                                                int N) {
-  const int k = f.knext;
-  const float sc = et * pow2f_fast(-k);   // |k| <= 120: exact
+  const int k = RS ? f.knext : 0;
+  const float sc = RS ? et * pow2f_fast(-k) : et;   // |k| <= 120: exact
   __syncwarp();
-  int e1;
-  const float s = fcc_matvec(f.m, vec[par ^ 1], f.spare, N, e1);
+  int e1 = 0;
+  const float s = fcc_matvec<RS>(f.m, vec[par ^ 1], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
   vec[par][lane] = f.v;
   out_row[lane] = f.v;
   if (lane == 0) *outk_t = f.K;
-  f.sc.observe(e1);
-  f.knext = f.sc.next();
+  if (RS) {
+    f.sc.observe(e1);
+    f.knext = f.sc.next();
+  }
 }
 
 // fcc beta' step consuming frame u (criterion.py:236): beta'_{u-1} = M^T (Et_u beta'_u) 2^-k
+template <bool RS>
 __device__ __forceinline__ void fcc_beta_step(FccState &f, float et, float (*vec)[32],
                                               int par, float *out_row, int *outk_t, int lane,
                                               int N) {
-  const int k = f.knext;
-  const float sc = lane < N ? pow2f_fast(-k) : 0.f;
+  const int k = RS ? f.knext : 0;
+  const float sc = lane < N ? (RS ? pow2f_fast(-k) : 1.f) : 0.f;
   vec[par][lane] = et * f.v;
   __syncwarp();
-  int e1;
-  const float s = fcc_matvec(f.m, vec[par], f.spare, N, e1);
+  int e1 = 0;
+  const float s = fcc_matvec<RS>(f.m, vec[par], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
   out_row[lane] = f.v;
   if (lane == 0) *outk_t = f.K;
-  f.sc.observe(e1);
-  f.knext = f.sc.next();
+  if (RS) {
+    f.sc.observe(e1);
+    f.knext = f.sc.next();
+  }
 }
 
 struct FccCtx {
@@ -216,9 +229,9 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
     const float et = sm.ering[j & (kRing - 1)][lane];
     const int t = frame_of(FWD, T, j);
     if (FWD)
-      fcc_alpha_step(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+      fcc_alpha_step<true>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
     else
-      fcc_beta_step(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+      fcc_beta_step<true>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
     publish(mycons, j + 1, lane);
   };
   const int pro_end = min(T, kBlk);
@@ -238,10 +251,17 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
 #pragma unroll
     for (int q = 0; q < kBlk; ++q) {
       const int dq = FWD ? q : -q;
-      if (FWD)
-        fcc_alpha_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
-      else
-        fcc_beta_step(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+      if ((q % kFccRescale) == kFccRescale - 1) {
+        if (FWD)
+          fcc_alpha_step<true>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+        else
+          fcc_beta_step<true>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+      } else {
+        if (FWD)
+          fcc_alpha_step<false>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+        else
+          fcc_beta_step<false>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+      }
     }
     publish(mycons, j0 + kBlk, lane);
   }
