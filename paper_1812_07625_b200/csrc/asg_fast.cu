@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   float *gwarp = erow + kGradWarps * 64;         // [kGradWarps][2] guard
   // per-warp token CSR as absolute shared addresses into that warp's
   // posterior row (the gather is then load-address, load-value, add)
-  unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][LP]
+  unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][2 LP]
 
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -540,15 +540,28 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     }
   float *myp = prow + warp * LP;
   float *mye = erow + warp * 64;
-  unsigned *myaddr = saddr + warp * LP;
-  {
-    const unsigned base = (unsigned)__cvta_generic_to_shared(myp);
-    for (int i = lane; i < L; i += 32) myaddr[i] = base + 4u * (unsigned)w.perm[(size_t)b * w.lpad + i];
-  }
+  unsigned *myaddr = saddr + warp * 2 * LP;
   mye[32 + lane] = 0.f;   // columns N.. of the Et row: padding states read 0
-  __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
+  // Token gather table: column `lane` lists the shared addresses (in this
+  // warp's posterior row) of the states labelled `lane`, padded with a zero
+  // cell to a uniform depth G4 -- every lane then runs the same unrolled loop
+  // (no divergence, no tail).  Falls back to the CSR walk if too deep.
+  const int g4 = (warp_max(ts1 - ts0) + 3) & ~3;
+  const bool uniform = g4 * 32 <= 2 * LP;
+  {
+    const unsigned base = (unsigned)__cvta_generic_to_shared(myp);
+    const unsigned zero = (unsigned)__cvta_generic_to_shared(mye + 40);
+    const int *perm = w.perm + (size_t)b * w.lpad;
+    if (uniform) {
+      for (int q = 0; q < g4; ++q)
+        myaddr[q * 32 + lane] = ts0 + q < ts1 ? base + 4u * (unsigned)perm[ts0 + q] : zero;
+    } else {
+      for (int i = lane; i < L; i += 32) myaddr[i] = base + 4u * (unsigned)perm[i];
+    }
+  }
+  __syncthreads();
   const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
   const int refCi = isfinite(refC) ? (int)floor(refC) : 0;
   const float refCf = isfinite(refC) ? (float)(refC - refCi) : CUDART_NAN_F;
@@ -635,7 +648,21 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     gmax = fmaxf(gmax, g);
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
-    const float con = gather_shared(myaddr, ts0, ts1);
+    float con;
+    if (uniform) {
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+      for (int q = 0; q < g4; q += 4) {
+        const unsigned a0 = myaddr[q * 32 + lane], a1 = myaddr[(q + 1) * 32 + lane];
+        const unsigned a2 = myaddr[(q + 2) * 32 + lane], a3 = myaddr[(q + 3) * 32 + lane];
+        c0 += lds_f32(a0);
+        c1 += lds_f32(a1);
+        c2 += lds_f32(a2);
+        c3 += lds_f32(a3);
+      }
+      con = (c0 + c1) + (c2 + c3);
+    } else {
+      con = gather_shared(myaddr, ts0, ts1);
+    }
     if (lane < N) ge[tq / 32 * N + lane] = g_old - con * izc;
     if (t >= 1) {
       // fac edge posteriors (:218-224): alpha_{t-1} (stay: same state, step:
@@ -819,7 +846,7 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                           float *grad_em, const int32_t *status, cudaStream_t s) {
   constexpr int LP = W * kLatStates;
-  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2 + LP));
+  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2 + 2 * LP));
   auto k = asg_fac_grad_kernel<W>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
