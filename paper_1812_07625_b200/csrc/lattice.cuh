@@ -312,8 +312,14 @@ struct StepIn {
 template <int KIND, bool FWD>
 __device__ __forceinline__ void load_step_in(StepIn &in, const LatState &f, const float *er,
                                              const Bnd *bi, int lane) {
+  if (KIND == kCtc) {   // even states are blanks: one shared Et
+    in.E[0] = in.E[2] = er[f.tok[0]];
+    in.E[1] = er[f.tok[1]];
+    in.E[3] = er[f.tok[3]];
+  } else {
 #pragma unroll
-  for (int k = 0; k < kSpl; ++k) in.E[k] = er[f.tok[k]];
+    for (int k = 0; k < kSpl; ++k) in.E[k] = er[f.tok[k]];
+  }
   if (!FWD) {
     in.En1 = er[f.nbtok1];
     in.En2 = KIND == kCtc ? er[f.nbtok2] : 0.f;
@@ -397,7 +403,7 @@ __device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo,
   }
   if (renorm) lane_renorm<kSpl>(f.v, f.ex);
   const bool edge = FWD ? lane == 31 : lane == 0;
-  if (edge) {
+  if (bo && edge) {
     Bnd o;
     o.v0 = FWD ? f.v[kSpl - 1] : f.v[0];
     o.v1 = FWD ? f.v[kSpl - 2] : f.v[1];
@@ -502,7 +508,7 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     const float *eb = sm.ering[j0 & (kRing - 1)];
     const Bnd *ub0 = has_up ? &ubnd[(j0 - 1) & (kBndRing - 1)] : nullptr;
     const Bnd *ub1 = has_up ? &ubnd[j0 & (kBndRing - 1)] : nullptr;   // q >= 1: ub1[q-1]
-    Bnd *ob = &mybnd[j0 & (kBndRing - 1)];
+    Bnd *ob = has_dn ? &mybnd[j0 & (kBndRing - 1)] : nullptr;   // no reader: no store
     // rows go straight to global memory (fire-and-forget vector stores)
     const int tb = frame_of(FWD, T, j0);
     float *sv = row_of(tb);
@@ -521,7 +527,7 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
       constexpr bool FAST = decltype(fast_tag)::value;
 #pragma unroll
       for (int q = 0; q < kBlk; ++q) {
-        lat_step<KIND, FWD, FAST>(f, in[q], ob + q, lane, (q % kRenormF) == 0,
+        lat_step<KIND, FWD, FAST>(f, in[q], ob ? ob + q : nullptr, lane, (q % kRenormF) == 0,
                                   (q % kRenormF) == 1);
         const int dq = FWD ? q : -q;
         lat_store_row(f.v, f.ex, sv + dq * kLatStates, se + dq * 32, lane);
