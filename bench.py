@@ -408,7 +408,10 @@ def main():
         "alg_bytes_per_launch": dom_alg_bytes,
         "kernel_ms": dom_ms,
         "peak_source": hbm_src,
-        "note": "serial T-step recursion: latency-bound; the SFU-equivalent view is in roofline_sfu",
+        "note": ("serial T-step recursion: latency-bound; the SFU-equivalent view is in "
+                 "roofline_sfu") if stage == "chain" else
+                ("posterior/gradient kernels: achieved counts only the algorithmic bytes "
+                 "(emissions in, gradient out); traffic adds the workspace rows they read"),
         "step": {
             "sfu_ops_per_step": step_ops,
             "sfu_achieved_gops": step_ops / step_s / 1e9,

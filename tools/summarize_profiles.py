@@ -81,5 +81,7 @@ for r in data:
                f"{inst:11.1f}{float(r[ix['sm__inst_executed.avg.per_cycle_active']]):6.2f}"
                f"{r[ix['launch__registers_per_thread']]:>6s}")
 open(os.path.join(dst, "ncu_full_summary.txt"), "w").write("\n".join(out) + "\n")
+if "asg_grad_fcc" in traffic and "asg_grad_fac" in traffic:   # the bench's "asg_grad" stage
+    traffic["asg_grad"] = traffic["asg_grad_fcc"] + traffic["asg_grad_fac"]
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
 print("\n".join(out))
