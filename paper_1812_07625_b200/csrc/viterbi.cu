@@ -1,16 +1,16 @@
 // Batched Viterbi best path (replaces criterion.py:259-284).
 //
-// One warp per utterance, lane i owns destination token i and keeps row i of
-// the transition matrix in registers (A[to][from], criterion.py:276).  The
-// max-plus recursion runs in float64 in the reference's operation order
+// One CTA of 4 warps per utterance (see viterbi4_body).  The max-plus
+// recursion runs in float64 in the reference's operation order
 //     cand_j = dp[j] + A[i][j];  back = first argmax_j;  dp'[i] = e[t][i] + cand_back
 // so paths and scores are bit-identical to the numpy reference (ties go to
 // the lowest id, np.argmax semantics, NaN treated as the maximum).  The
-// argmax is a 5-level tournament over index-ordered pairs (depth 5 instead of
-// a 30-long compare chain); emissions are prefetched 8 frames ahead; the
-// previous frame's dp vector is broadcast through shared memory (double
-// buffered, one __syncwarp per frame); backpointers are uint8 in shared
-// memory when T*N fits, else in the workspace; lane 0 traces back.
+// argmax is a 5-level tournament over index-ordered pairs (3 levels inside a
+// lane's 8 sources, 2 across lanes by shuffles); emissions are prefetched 8
+// frames ahead; the previous frame's dp vector is broadcast through shared
+// memory (double buffered, one CTA barrier per frame); backpointers are
+// uint8 in shared memory when T*N fits, else in the workspace; thread 0
+// traces back.
 
 #include "common.cuh"
 #include "kernels.h"
@@ -28,84 +28,95 @@ __device__ __forceinline__ bool vit_take(double a, double b) {
   return b > a;
 }
 
-// one frame of the max-plus recursion for destination token `lane`;
-// returns the new dp value and writes the backpointer.  Sources j >= N hold
-// dp = -inf (and A = 0), so they never win and need no bounds test.
+// ---- 4-warp variant: one CTA of 4 warps per utterance.  Warp w owns
+// destinations 8w .. 8w+7; lane = 4 d + q handles destination 8w + d over the
+// sources 8q .. 8q+7 (fp64 cand_j = dp[j] + A[i][j], first-max argmax in
+// ascending j), then the four quarter results are combined by shuffles in
+// ascending quarter order -- the same comparisons in the same order of
+// precedence as the single-lane tournament, so paths and scores stay
+// bit-identical.  The new dp row goes through shared memory (one CTA barrier
+// per frame).  About 4x less fp64 work per warp on the serial chain.
 template <bool kNanAware>
-__device__ __forceinline__ double vit_step(const double *prev, const double (&arow)[32],
-                                           double et, int &arg_out) {
-  double c16[16];
-  int i16[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {   // level 1 of the tournament fused with cand_j = dp[j] + A[i][j]
-    const double a = prev[2 * j] + arow[2 * j];
-    const double b = prev[2 * j + 1] + arow[2 * j + 1];
-    const bool tb = vit_take<kNanAware>(a, b);
-    c16[j] = tb ? b : a;
-    i16[j] = tb ? 2 * j + 1 : 2 * j;
-  }
-  double c8[8];
-  int i8[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const bool tb = vit_take<kNanAware>(c16[2 * j], c16[2 * j + 1]);
-    c8[j] = tb ? c16[2 * j + 1] : c16[2 * j];
-    i8[j] = tb ? i16[2 * j + 1] : i16[2 * j];
-  }
-  double c4[4];
-  int i4[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const bool tb = vit_take<kNanAware>(c8[2 * j], c8[2 * j + 1]);
-    c4[j] = tb ? c8[2 * j + 1] : c8[2 * j];
-    i4[j] = tb ? i8[2 * j + 1] : i8[2 * j];
-  }
-  const bool t0 = vit_take<kNanAware>(c4[0], c4[1]);
-  const bool t1 = vit_take<kNanAware>(c4[2], c4[3]);
-  const double c2a = t0 ? c4[1] : c4[0], c2b = t1 ? c4[3] : c4[2];
-  const int i2a = t0 ? i4[1] : i4[0], i2b = t1 ? i4[3] : i4[2];
-  const bool tf = vit_take<kNanAware>(c2a, c2b);
-  arg_out = tf ? i2b : i2a;
-  return et + (tf ? c2b : c2a);                       // dp'[i] = e[t][i] + cand_back
+__device__ __forceinline__ void vit_merge(double &v, int &i, double ov, int oi, bool other_is_higher) {
+  // (v, i) and (ov, oi) cover disjoint source ranges; the lower range wins ties
+  const double lo_v = other_is_higher ? v : ov, hi_v = other_is_higher ? ov : v;
+  const int lo_i = other_is_higher ? i : oi, hi_i = other_is_higher ? oi : i;
+  const bool th = vit_take<kNanAware>(lo_v, hi_v);
+  v = th ? hi_v : lo_v;
+  i = th ? hi_i : lo_i;
 }
 
-template <class TE, class TA, bool kSmemBack, bool kNanAware>
-__device__ __forceinline__ void viterbi_body(const TE *__restrict__ e, int T, int N, int lane,
-                                             const double (&arow)[32], double (*dp_buf)[32],
-                                             uint8_t *back, double *score_out,
-                                             int64_t *path_out) {
-  constexpr int kPre = 8;   // emission prefetch distance (frames)
-  TE pre[kPre];   // raw emissions, converted at use so the load latency stays hidden
+template <class TE, bool kSmemBack, bool kNanAware>
+__device__ __forceinline__ void viterbi4_body(const TE *__restrict__ e, int T, int N,
+                                              const double (&arow)[8], double (*dp_buf)[32],
+                                              uint8_t *back, double *score_out,
+                                              int64_t *path_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = warp * 8 + (lane >> 2), q = lane & 3;
+  const bool owner = q == 0 && d < N;   // writes dp'[d] and back[t][d]
+  constexpr int kPre = 8;
+  TE pre[kPre];
 #pragma unroll
-  for (int q = 0; q < kPre; ++q)
-    pre[q] = (lane < N && 1 + q < T) ? e[(size_t)(1 + q) * N + lane] : TE(0);
-  double dp = lane < N ? (double)e[lane] : -CUDART_INF;
-  dp_buf[0][lane] = dp;
+  for (int r = 0; r < kPre; ++r) pre[r] = (owner && 1 + r < T) ? e[(size_t)(1 + r) * N + d] : TE(0);
+  if (threadIdx.x < 32) dp_buf[0][threadIdx.x] = threadIdx.x < N ? (double)e[threadIdx.x] : -CUDART_INF;
+  __syncthreads();
   for (int t0 = 1; t0 < T; t0 += kPre) {
 #pragma unroll
-    for (int q = 0; q < kPre; ++q) {
-      const int t = t0 + q;
+    for (int r = 0; r < kPre; ++r) {
+      const int t = t0 + r;
       if (t < T) {
-        const double et = (double)pre[q];
+        const double et = (double)pre[r];
         const int tn = t + kPre;
-        pre[q] = (lane < N && tn < T) ? e[(size_t)tn * N + lane] : TE(0);
-        __syncwarp();
-        int arg;
-        dp = vit_step<kNanAware>(dp_buf[(t - 1) & 1], arow, et, arg);
-        if (lane < N) back[(size_t)t * N + lane] = (uint8_t)arg;
-        dp_buf[t & 1][lane] = lane < N ? dp : -CUDART_INF;
+        pre[r] = (owner && tn < T) ? e[(size_t)tn * N + d] : TE(0);
+        const double2 *pv = reinterpret_cast<const double2 *>(dp_buf[(t - 1) & 1] + 8 * q);
+        double c[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 x = pv[k];
+          c[2 * k] = x.x + arow[2 * k];          // cand_j = dp[j] + A[i][j] (:276)
+          c[2 * k + 1] = x.y + arow[2 * k + 1];
+        }
+        // first-max tournament over the 8 sources of this quarter
+        double c4[4];
+        int i4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool tb = vit_take<kNanAware>(c[2 * k], c[2 * k + 1]);
+          c4[k] = tb ? c[2 * k + 1] : c[2 * k];
+          i4[k] = tb ? 2 * k + 1 : 2 * k;
+        }
+        const bool t0b = vit_take<kNanAware>(c4[0], c4[1]);
+        const bool t1b = vit_take<kNanAware>(c4[2], c4[3]);
+        const double c2a = t0b ? c4[1] : c4[0], c2b = t1b ? c4[3] : c4[2];
+        const int i2a = t0b ? i4[1] : i4[0], i2b = t1b ? i4[3] : i4[2];
+        const bool tf = vit_take<kNanAware>(c2a, c2b);
+        double v = tf ? c2b : c2a;
+        int i = 8 * q + (tf ? i2b : i2a);
+        // combine quarters: (0,1) and (2,3), then (01, 23)
+#pragma unroll
+        for (int m = 1; m <= 2; m <<= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, m);
+          const int oi = __shfl_xor_sync(0xffffffffu, i, m);
+          vit_merge<kNanAware>(v, i, ov, oi, (q & m) == 0);
+        }
+        if (owner) {
+          back[(size_t)t * N + d] = (uint8_t)i;
+          dp_buf[t & 1][d] = et + v;             // dp'[i] = e[t][i] + cand_back
+        } else if (q == 0) {
+          dp_buf[t & 1][d] = -CUDART_INF;        // destinations >= N never win
+        }
+        __syncthreads();
       }
     }
   }
-  __syncwarp();
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     const double *fin = dp_buf[(T - 1) & 1];
     int best_i = 0;
     double bv = fin[0];
-    for (int i = 1; i < N; ++i)
-      if (vit_take<true>(bv, fin[i])) {
-        bv = fin[i];
-        best_i = i;
+    for (int k = 1; k < N; ++k)
+      if (vit_take<true>(bv, fin[k])) {
+        bv = fin[k];
+        best_i = k;
       }
     *score_out = bv;
     int cur = best_i;
@@ -118,39 +129,42 @@ __device__ __forceinline__ void viterbi_body(const TE *__restrict__ e, int T, in
 }
 
 template <class TE, class TA, bool kSmemBack>
-__global__ void __launch_bounds__(32) viterbi_kernel(const TE *__restrict__ em,
-                                                     const int32_t *__restrict__ em_len,
-                                                     const TA *__restrict__ trans, Dims d,
-                                                     int64_t *__restrict__ path,
-                                                     double *__restrict__ score,
-                                                     const int32_t *__restrict__ status,
-                                                     uint8_t *__restrict__ back_ws) {
+__global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em,
+                                                       const int32_t *__restrict__ em_len,
+                                                       const TA *__restrict__ trans, Dims d,
+                                                       int64_t *__restrict__ path,
+                                                       double *__restrict__ score,
+                                                       const int32_t *__restrict__ status,
+                                                       uint8_t *__restrict__ back_ws) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) double dp_buf[2][32];
-  const int b = blockIdx.x, lane = threadIdx.x, N = d.N;
+  const int b = blockIdx.x, N = d.N;
   int64_t *pb = path + (size_t)b * d.Tmax;
   if (status[b] != W2L_OK) {
-    for (int t = lane; t < d.Tmax; t += 32) pb[t] = 0;
-    if (lane == 0) score[b] = 0.0;
+    for (int t = threadIdx.x; t < d.Tmax; t += blockDim.x) pb[t] = 0;
+    if (threadIdx.x == 0) score[b] = 0.0;
     return;
   }
   const int T = em_len[b];
   uint8_t *back = kSmemBack ? smem : back_ws + (size_t)b * d.Tmax * N;
   const TE *e = em + (size_t)b * d.Tmax * N;
-  double arow[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dst = warp * 8 + (lane >> 2), q = lane & 3;
+  double arow[8];
   bool finite = true;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    arow[j] = (trans != nullptr && lane < N && j < N) ? (double)trans[lane * N + j] : 0.0;
-    finite &= isfinite(arow[j]);
+  for (int k = 0; k < 8; ++k) {
+    const int j = 8 * q + k;
+    arow[k] = (trans != nullptr && dst < N && j < N) ? (double)trans[dst * N + j] : 0.0;
+    finite &= isfinite(arow[k]);
   }
-  // A may hold inf/NaN (the reference does not validate it, :270-272): only
-  // then is the NaN-aware comparison needed
-  if (__all_sync(0xffffffffu, finite))
-    viterbi_body<TE, TA, kSmemBack, false>(e, T, N, lane, arow, dp_buf, back, score + b, pb);
+  // sources j >= N: dp = -inf makes them lose; A may hold inf/NaN (not
+  // validated by the reference, :270-272) -- only then the NaN-aware compare
+  if (__syncthreads_and(finite))
+    viterbi4_body<TE, kSmemBack, false>(e, T, N, arow, dp_buf, back, score + b, pb);
   else
-    viterbi_body<TE, TA, kSmemBack, true>(e, T, N, lane, arow, dp_buf, back, score + b, pb);
-  for (int t = T + lane; t < d.Tmax; t += 32) pb[t] = 0;
+    viterbi4_body<TE, kSmemBack, true>(e, T, N, arow, dp_buf, back, score + b, pb);
+  for (int t = T + threadIdx.x; t < d.Tmax; t += blockDim.x) pb[t] = 0;
 }
 
 }  // namespace
@@ -166,14 +180,14 @@ cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans,
                            cudaStream_t s) {
   const size_t back_bytes = (size_t)d.Tmax * d.N;
   if (back_bytes <= (size_t)kSmemBackMax) {
-    auto k = viterbi_kernel<TE, TA, true>;
+    auto k = viterbi4_kernel<TE, TA, true>;
     cudaError_t err =
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBackMax);
     if (err != cudaSuccess) return err;
-    k<<<d.B, 32, back_bytes, s>>>(em, em_len, trans, d, path, score, status, nullptr);
+    k<<<d.B, 128, back_bytes, s>>>(em, em_len, trans, d, path, score, status, nullptr);
   } else {
-    viterbi_kernel<TE, TA, false><<<d.B, 32, 0, s>>>(em, em_len, trans, d, path, score, status,
-                                                     (uint8_t *)ws);
+    viterbi4_kernel<TE, TA, false><<<d.B, 128, 0, s>>>(em, em_len, trans, d, path, score, status,
+                                                       (uint8_t *)ws);
   }
   return cudaGetLastError();
 }
