@@ -434,10 +434,22 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
     pfa = fa_r[(unsigned)(ta - 1) * 32];
     pka = ka_r[ta - 1];
   }
+  // the next frame's inputs are loaded while this frame is processed (each
+  // frame otherwise pays a full DRAM round trip)
+  float e_n = 0.f, fa_n = 0.f, fb_n = 0.f;
+  int ka_n = 0, kb_n = 0;
+  auto load_fcc = [&](int t) {
+    e_n = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
+    fa_n = fa_r[(unsigned)t * 32];
+    fb_n = fb_r[(unsigned)t * 32];
+    ka_n = ka_r[t];
+    kb_n = kb_r[t];
+  };
+  if (ta < tend) load_fcc(ta);
   for (int t = ta; t < tend; ++t) {
-    const float e = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
-    const float fa = fa_r[(unsigned)t * 32], fb = fb_r[(unsigned)t * 32];
-    const int ka = ka_r[t], kb = kb_r[t];
+    const float e = e_n, fa = fa_n, fb = fb_n;
+    const int ka = ka_n, kb = kb_n;
+    if (t + 1 < tend) load_fcc(t + 1);
     const float m = warp_max(e);
     const float et = lane < N ? et_of(e, m) : 0.f;
     myv[lane] = pfa;
