@@ -25,7 +25,7 @@
 // Reference correspondence: fac alpha/beta = criterion.py:193-212, fac
 // posteriors = :214-224, fcc = :227-241, combine = :243-247.
 
-#include "chunk.cuh"
+#include "laneblock.cuh"
 #include "lattice.cuh"
 #include "common.cuh"
 #include "kernels.h"

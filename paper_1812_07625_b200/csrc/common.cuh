@@ -19,23 +19,10 @@ constexpr int kNegExp = -(1 << 24);   // exponent of an all-zero lane block
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline size_t align_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
-// padded row stride of a staged emission row: odd (bank-conflict free for
-// row-per-lane access) and > N so column N can hold an explicit 0.
-__host__ __device__ inline int em_stride(int n) { return (n + 1) | 1; }
 
 // ------------------------------------------------------------ pow2 math --
 // Exact power-of-two rescaling keeps the scaled linear-domain recursions
 // free of rounding in the scale factors: only integer exponents accumulate.
-
-// 2^k as a float for k in [-149, 127]; 0 below, +inf never produced (clamped).
-__device__ __forceinline__ float pow2f(int k) {
-  if (k >= -126) {
-    k = min(k, 127);
-    return __int_as_float((k + 127) << 23);
-  }
-  if (k >= -149) return __int_as_float(1 << (k + 149));
-  return 0.0f;
-}
 
 // 2^k without branches for k <= 127; k <= -127 gives 0 (no subnormals).
 __device__ __forceinline__ float pow2f_fast(int k) {
@@ -46,12 +33,6 @@ __device__ __forceinline__ float pow2f_fast(int k) {
 // floor(log2(x)) for a positive normal float; subnormals map to -127.
 __device__ __forceinline__ int exponent_of(float x) {
   return ((__float_as_int(x) >> 23) & 0xff) - 127;
-}
-
-__device__ __forceinline__ double pow2d(int k) {
-  if (k < -1022) return ldexp(1.0, k);
-  k = min(k, 1023);
-  return __longlong_as_double((long long)(k + 1023) << 52);
 }
 
 // ------------------------------------------------------------ log-space --
@@ -105,8 +86,5 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
-
-// read-only, evict-first streaming load of an emission value
-__device__ __forceinline__ float ldg_stream(const float *p) { return __ldcs(p); }
 
 }  // namespace w2l

@@ -12,7 +12,7 @@
 // a token CSR) and checks the per-frame consistency guard; failing utterances
 // are recomputed by the float64 log-domain kernel.
 
-#include "chunk.cuh"
+#include "laneblock.cuh"
 #include "lattice.cuh"
 #include "common.cuh"
 #include "kernels.h"

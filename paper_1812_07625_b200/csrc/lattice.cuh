@@ -18,7 +18,7 @@
 // runs a few steps behind its upstream neighbour (w-1 forward, w+1 backward)
 // and reads the neighbour's boundary states of step j-1 from a small ring in
 // shared memory instead of a shuffle.  Progress is published every
-// kUnroll = 8 steps through release/acquire counters, so the warps never
+// kBlk = 8 steps through release/acquire counters, so the warps never
 // meet at a barrier.  Splitting the lattice over W warps cuts the
 // instructions each warp issues per frame by W, which is what bounds a
 // latency-bound serial recursion (one dependent step per frame).
@@ -39,7 +39,7 @@
 
 #include <type_traits>
 
-#include "chunk.cuh"
+#include "laneblock.cuh"
 
 namespace w2l {
 
@@ -92,8 +92,6 @@ struct ChainSm {
   int cons[kCounters];
 };
 
-using FccStage = RowStage<32, 1>;
-using LatStage = RowStage<kLatStates, 32>;
 
 // ---- release/acquire progress counters (CTA scope, shared memory)
 __device__ __forceinline__ int ld_acquire(const int *p) {
