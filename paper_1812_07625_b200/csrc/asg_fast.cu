@@ -509,10 +509,12 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
                         float *__restrict__ grad_em, const int32_t *__restrict__ status) {
   constexpr int LP = W * kLatStates;
   extern __shared__ __align__(16) float gsm[];
-  float *redE = gsm;                             // [kGradWarps][2][LP] edge partials
-  float *prow = redE + kGradWarps * 2 * LP;      // [kGradWarps][LP] posterior row
-  float *erow = prow + kGradWarps * LP;          // [kGradWarps][64] Et row (+ zero col)
-  float *gwarp = erow + kGradWarps * 64;         // [kGradWarps][2] guard
+  // [kGradWarps][LP] posterior row; after its frame loop each warp reuses
+  // its own row for the occupancy partials (redE)
+  float *prow = gsm;
+  float *redE = prow;
+  float *zcell = prow + kGradWarps * LP;         // [kGradWarps][2] zero cells
+  float *gwarp = zcell + kGradWarps * 2;         // [kGradWarps][2] guard
   // per-warp token CSR as absolute shared addresses into that warp's
   // posterior row (the gather is then load-address, load-value, add)
   unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][2 LP]
@@ -527,8 +529,8 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     // keep the partial buffers well-defined for the final reduction
     for (int i = threadIdx.x; i < 1024; i += blockDim.x)
       w.part_fullA[((size_t)b * w.nblk + blk) * 1024 + i] = 0.f;
-    for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x)
-      w.part_edge[((size_t)b * w.nblk + blk) * 2 * LP + i] = 0.f;
+    for (int i = threadIdx.x; i < LP; i += blockDim.x)
+      w.part_edge[((size_t)b * w.nblk + blk) * LP + i] = 0.f;
     if (threadIdx.x < 4)
       w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] =
           (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
@@ -541,19 +543,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   const int L = tgt_len[b];
   // segments the chain wrote for this utterance (the batch's W may be wider)
   const int weff = min(lat_warps(L), W);
-  const int64_t *y = tgt + (size_t)b * d.Lmax;
-  int tok[W][kSpl];
-#pragma unroll
-  for (int sw = 0; sw < W; ++sw)
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) {
-      const int l = sw * kLatStates + lane * kSpl + k;
-      tok[sw][k] = l < L ? (int)y[l] : N;
-    }
   float *myp = prow + warp * LP;
-  float *mye = erow + warp * 64;
   unsigned *myaddr = saddr + warp * 2 * LP;
-  mye[32 + lane] = 0.f;   // columns N.. of the Et row: padding states read 0
+  if (lane == 0) zcell[warp * 2] = 0.f;   // padding entries of the gather table
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
   const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
   // Token gather table: column `lane` lists the shared addresses (in this
@@ -564,7 +556,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   const bool uniform = g4 * 32 <= 2 * LP;
   {
     const unsigned base = (unsigned)__cvta_generic_to_shared(myp);
-    const unsigned zero = (unsigned)__cvta_generic_to_shared(mye + 40);
+    const unsigned zero = (unsigned)__cvta_generic_to_shared(zcell + warp * 2);
     const int *perm = w.perm + (size_t)b * w.lpad;
     if (uniform) {
       for (int q = 0; q < g4; ++q)
@@ -579,7 +571,6 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   const float refCf = isfinite(refC) ? (float)(refC - refCi) : CUDART_NAN_F;
   float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
 
-  const float *emb = em + (size_t)b * d.Tmax * N;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
   const float4 *A4 = reinterpret_cast<const float4 *>(w.fac_a + seg0 * kLatStates) + lane;
   const float4 *B4 = reinterpret_cast<const float4 *>(w.fac_b + seg0 * kLatStates) + lane;
@@ -588,33 +579,35 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);   // float4 per segment
   const unsigned sege = (unsigned)d.Tmax * 32;
 
-  float accS[W][kSpl], accP[W][kSpl];
+  // Fac edge sums need no edge products: a forced alignment enters every
+  // state l >= 1 exactly once and stays in state l (n_l - 1) times, n_l its
+  // frame count, so the summed posteriors of the stay and step edges
+  // (:218-224) are occ(l) - 1 and 1, occ(l) = sum_t of the node posterior.
+  // Only occ is accumulated here; asg_final applies the identity.
+  float accO[W][kSpl];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
 #pragma unroll
-    for (int k = 0; k < kSpl; ++k) accS[sw][k] = accP[sw][k] = 0.f;
+    for (int k = 0; k < kSpl; ++k) accO[sw][k] = 0.f;
   const int tend = min(tb, T);
-  float4 pa[W];
-  int pea[W];
+  // the gradient-row value (written by asg_fcc_grad) of the next frame is
+  // loaded one frame ahead
+  float g_nx = 0.f;
+  if (ta < tend && lane < N) g_nx = ge[(unsigned)ta * N + lane];
+  // the rows are loaded one frame ahead too (segments >= weff read zeros)
+  float4 na[W], nb[W];
+  int nea[W], neb[W];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw) {
-    pa[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
-    pea[sw] = kNegExp;
-  }
-  if (ta >= 1 && ta < tend) {
-#pragma unroll
-    for (int sw = 0; sw < W; ++sw)
-      if (sw < weff) {
-        pa[sw] = A4[sw * segq + (unsigned)(ta - 1) * 32];
-        pea[sw] = EA[sw * sege + (unsigned)(ta - 1) * 32];
-      }
-  }
-  // the emission and the gradient-row value (written by asg_fcc_grad) of the
-  // next frame are loaded one frame ahead
-  float e_nx = 0.f, g_nx = 0.f;
-  if (ta < tend && lane < N) {
-    e_nx = emb[(unsigned)ta * N + lane];
-    g_nx = ge[(unsigned)ta * N + lane];
+    na[sw] = nb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+    nea[sw] = neb[sw] = kNegExp;
+    if (sw < weff && ta < tend) {
+      const unsigned tq = (unsigned)ta * 32;
+      na[sw] = A4[sw * segq + tq];
+      nb[sw] = B4[sw * segq + tq];
+      nea[sw] = EA[sw * sege + tq];
+      neb[sw] = EB[sw * sege + tq];
+    }
   }
   for (int t = ta; t < tend; ++t) {
     const unsigned tq = (unsigned)t * 32;
@@ -622,42 +615,44 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     int ea[W], eb[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      if (sw < weff) {
-        va[sw] = A4[sw * segq + tq];
-        vb[sw] = B4[sw * segq + tq];
-        ea[sw] = EA[sw * sege + tq];
-        eb[sw] = EB[sw * sege + tq];
-      } else {
-        va[sw] = vb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ea[sw] = eb[sw] = kNegExp;
+      va[sw] = na[sw];
+      vb[sw] = nb[sw];
+      ea[sw] = nea[sw];
+      eb[sw] = neb[sw];
+      if (sw < weff && t + 1 < tend) {
+        na[sw] = A4[sw * segq + tq + 32];
+        nb[sw] = B4[sw * segq + tq + 32];
+        nea[sw] = EA[sw * sege + tq + 32];
+        neb[sw] = EB[sw * sege + tq + 32];
       }
     }
-    const float e = lane < N ? e_nx : -CUDART_INF_F;
     const float g_old = g_nx;
-    if (t + 1 < tend && lane < N) {
-      e_nx = emb[(unsigned)(t + 1) * N + lane];
-      g_nx = ge[(unsigned)(t + 1) * N + lane];
-    }
-    const float m = warp_max(e);
-    mye[lane] = lane < N ? et_of(e, m) : 0.f;
+    if (t + 1 < tend && lane < N) g_nx = ge[(unsigned)(t + 1) * N + lane];
     // fac node posteriors (:214-217)
     float zl = 0.f;
+    float4 p[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
       const float sc = pow2_clamped(ea[sw] + eb[sw] - refCi);
-      float4 p;
-      p.x = va[sw].x * vb[sw].x * sc;
-      p.y = va[sw].y * vb[sw].y * sc;
-      p.z = va[sw].z * vb[sw].z * sc;
-      p.w = va[sw].w * vb[sw].w * sc;
-      reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
-      zl += (p.x + p.y) + (p.z + p.w);
+      p[sw].x = va[sw].x * vb[sw].x * sc;
+      p[sw].y = va[sw].y * vb[sw].y * sc;
+      p[sw].z = va[sw].z * vb[sw].z * sc;
+      p[sw].w = va[sw].w * vb[sw].w * sc;
+      reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p[sw];
+      zl += (p[sw].x + p[sw].y) + (p[sw].z + p[sw].w);
     }
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
     const float g = __log2f(zc) - refCf;
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
+#pragma unroll
+    for (int sw = 0; sw < W; ++sw) {
+      accO[sw][0] = fmaf(p[sw].x, izc, accO[sw][0]);
+      accO[sw][1] = fmaf(p[sw].y, izc, accO[sw][1]);
+      accO[sw][2] = fmaf(p[sw].z, izc, accO[sw][2]);
+      accO[sw][3] = fmaf(p[sw].w, izc, accO[sw][3]);
+    }
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
     float con;
@@ -676,72 +671,25 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
       con = gather_shared(myaddr, ts0, ts1);
     }
     if (lane < N) ge[tq / 32 * N + lane] = g_old - con * izc;
-    if (t >= 1) {
-      // fac edge posteriors (:218-224): alpha_{t-1} (stay: same state, step:
-      // previous state) times Et[y] beta'_t (times S|P later)
-      float carry_v = 0.f;   // state 128 sw - 1 (previous segment)
-      int carry_e = kNegExp;
-#pragma unroll
-      for (int sw = 0; sw < W; ++sw) {
-        float nbv = __shfl_sync(0xffffffffu, pa[sw].w, (lane + 31) & 31);
-        int nbe = __shfl_sync(0xffffffffu, pea[sw], (lane + 31) & 31);
-        const float cv = __shfl_sync(0xffffffffu, pa[sw].w, 31);
-        const int ce = __shfl_sync(0xffffffffu, pea[sw], 31);
-        if (lane == 0) {
-          nbv = carry_v;
-          nbe = carry_e;
-        }
-        carry_v = cv;
-        carry_e = ce;
-        const float s_own = pow2_clamped(pea[sw] + eb[sw] - refCi) * izc;
-        const float s_nb = pow2_clamped(nbe + eb[sw] - refCi) * izc;
-        const float pav[4] = {pa[sw].x, pa[sw].y, pa[sw].z, pa[sw].w};
-        const float vbv[4] = {vb[sw].x, vb[sw].y, vb[sw].z, vb[sw].w};
-#pragma unroll
-        for (int k = 0; k < kSpl; ++k) {
-          const float qk = vbv[k] * mye[tok[sw][k]];
-          const float qs = qk * s_own;
-          accS[sw][k] = fmaf(pav[k], qs, accS[sw][k]);
-          accP[sw][k] = k > 0 ? fmaf(pav[k - 1], qs, accP[sw][k])
-                              : fmaf(nbv, qk * s_nb, accP[sw][k]);
-        }
-      }
-    }
-#pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-      pa[sw] = va[sw];
-      pea[sw] = ea[sw];
-    }
     __syncwarp();
   }
 
-  // ---- block reduction of the partials in fixed warp order (deterministic);
-  // the constant weights S (stay), P (step) are applied here
-  const float amax = trans_max(trans, N);
-  float *rE = redE + warp * 2 * LP;
+  // ---- block reduction of the occupancy partials in fixed warp order
+  // (deterministic)
+  float *rE = redE + warp * LP;
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
 #pragma unroll
-    for (int k = 0; k < kSpl; ++k) {
-      const int l = sw * kLatStates + lane * kSpl + k;
-      float S = 0.f, P = 0.f;
-      if (l < L) {
-        const int yl = (int)y[l];
-        S = expf(trans[yl * N + yl] - amax);
-        P = l > 0 ? expf(trans[yl * N + (int)y[l - 1]] - amax) : 0.f;
-      }
-      rE[l] = accS[sw][k] * S;
-      rE[LP + l] = accP[sw][k] * P;
-    }
+    for (int k = 0; k < kSpl; ++k) rE[sw * kLatStates + lane * kSpl + k] = accO[sw][k];
   if (lane == 0) {
     gwarp[warp * 2 + 0] = gmin;
     gwarp[warp * 2 + 1] = gmax;
   }
   __syncthreads();
-  float *dstE = w.part_edge + ((size_t)b * w.nblk + blk) * 2 * LP;
-  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x) {
+  float *dstE = w.part_edge + ((size_t)b * w.nblk + blk) * LP;
+  for (int i = threadIdx.x; i < LP; i += blockDim.x) {
     float s = 0.f;
-    for (int q = 0; q < kGradWarps; ++q) s += redE[q * 2 * LP + i];
+    for (int q = 0; q < kGradWarps; ++q) s += redE[q * LP + i];
     dstE[i] = s;
   }
   if (threadIdx.x < 2) {
@@ -762,7 +710,7 @@ __global__ void __launch_bounds__(1024)
                      const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
                      AsgFastWs w, double *loss, float *ga_utt, int32_t *status) {
   const int b = blockIdx.x;
-  __shared__ float sEdge[2 * 1024];
+  __shared__ float sEdge[1024];
   __shared__ float sA[1024];
   __shared__ float s_red[32];
   __shared__ int s_bad;
@@ -802,8 +750,8 @@ __global__ void __launch_bounds__(1024)
     for (; q < nb_used; ++q) a0 += base[(size_t)q * stride];
     return (a0 + a1) + (a2 + a3);
   };
-  for (int i = threadIdx.x; i < 2 * LP; i += blockDim.x)
-    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * 2 * LP + i, 2 * LP);
+  for (int i = threadIdx.x; i < LP; i += blockDim.x)
+    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * LP + i, LP);
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
     sA[i] = sum_parts(w.part_fullA + (size_t)b * w.nblk * 1024 + i, 1024);
   __syncthreads();
@@ -814,11 +762,13 @@ __global__ void __launch_bounds__(1024)
   for (int p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = p / N, j = p % N;
     const float full = sA[i * 32 + j] * expf(trans[p] - amax);
-    float con = 0.f;  // states labelled i: stay edges (i,i), step edges (i, y_{l-1})
+    // states labelled i: stay edges (i,i) sum to occ(l) - 1, step edges
+    // (i, y_{l-1}) to 1 (see asg_fac_grad_kernel)
+    float con = 0.f;
     for (int q = ts[i]; q < ts[i + 1]; ++q) {
       const int l = perm[q];
-      if (i == j) con += sEdge[l];
-      if (l > 0 && sy[l - 1] == j) con += sEdge[LP + l];
+      if (i == j) con += sEdge[l] - 1.f;
+      if (l > 0 && sy[l - 1] == j) con += 1.f;
     }
     ga_utt[(size_t)b * NN + p] = full - con;
     if (!isfinite(full - con)) atomicOr(&s_bad, 1);
@@ -858,7 +808,7 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                           float *grad_em, const int32_t *status, cudaStream_t s) {
   constexpr int LP = W * kLatStates;
-  const size_t smem = sizeof(float) * (kGradWarps * (2 * LP + LP + 64 + 2 + 2 * LP));
+  const size_t smem = sizeof(float) * (kGradWarps * (LP + 2 + 2 + 2 * LP));
   auto k = asg_fac_grad_kernel<W>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
@@ -898,7 +848,7 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   t.fac_eb = (int *)take(BT * W * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
   t.part_fullA = (float *)take((size_t)d.B * nblk * 1024 * 4);
-  t.part_edge = (float *)take((size_t)d.B * nblk * 2 * lpad * 4);
+  t.part_edge = (float *)take((size_t)d.B * nblk * lpad * 4);
   t.part_guard = (float *)take((size_t)d.B * nblk * 4 * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
