@@ -12,7 +12,10 @@ import os
 import re
 import threading
 
-from ._build import LIB
+from ._build import LIB as _BUILT_LIB
+
+# W2L_LIB selects another build of the same library (A/B timing in tools/ab.sh)
+LIB = os.environ.get("W2L_LIB", _BUILT_LIB)
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                       "include", "w2l_criterion.h")

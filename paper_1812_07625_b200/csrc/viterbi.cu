@@ -6,8 +6,8 @@
 // so paths and scores are bit-identical to the numpy reference (ties go to
 // the lowest id, np.argmax semantics, NaN treated as the maximum).  The
 // argmax is a 5-level tournament over index-ordered pairs (3 levels inside a
-// lane's 8 sources, 2 across lanes by shuffles); emissions are prefetched 8
-// frames ahead; the previous frame's dp vector is broadcast through shared
+// lane's 8 sources, 2 across lanes by shuffles); emissions are staged in
+// shared memory 32 frames at a time (cp.async, double buffered); the previous frame's dp vector is broadcast through shared
 // memory (double buffered, one CTA barrier per frame); backpointers are
 // uint8 in shared memory when T*N fits, else in the workspace; thread 0
 // traces back.
@@ -28,7 +28,7 @@ __device__ __forceinline__ bool vit_take(double a, double b) {
   return b > a;
 }
 
-// ---- 4-warp variant: one CTA of 4 warps per utterance.  Warp w owns
+// ---- One CTA of 4 warps per utterance.  Warp w owns
 // destinations 8w .. 8w+7; lane = 4 d + q handles destination 8w + d over the
 // sources 8q .. 8q+7 (fp64 cand_j = dp[j] + A[i][j], first-max argmax in
 // ascending j), then the four quarter results are combined by shuffles in
@@ -46,67 +46,103 @@ __device__ __forceinline__ void vit_merge(double &v, int &i, double ov, int oi, 
   i = th ? hi_i : lo_i;
 }
 
+// Emissions are staged through shared memory in chunks of kVitChunk frames,
+// double buffered with cp.async (groups complete in order, so waiting for the
+// older chunk never waits for the newer one).  Register prefetching stalled:
+// the loads of different frames shared a scoreboard, so every step waited for
+// the newest load's full latency.
+constexpr int kVitChunk = 32;
+
+template <class TE>
+__device__ __forceinline__ void vit_issue_chunk(const TE *__restrict__ e, int T, int N, int c,
+                                                TE *ebuf) {
+  const int f0 = c * kVitChunk, f1 = min(T, f0 + kVitChunk);
+  const int n = (f1 - f0) * N;
+  TE *dst = ebuf + (c & 1) * kVitChunk * 32;
+  const TE *src = e + (size_t)f0 * N;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + i);
+    if (sizeof(TE) == 8)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + i) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 template <class TE, bool kSmemBack, bool kNanAware>
 __device__ __forceinline__ void viterbi4_body(const TE *__restrict__ e, int T, int N,
                                               const double (&arow)[8], double (*dp_buf)[32],
-                                              uint8_t *back, double *score_out,
+                                              TE *ebuf, uint8_t *back, double *score_out,
                                               int64_t *path_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = warp * 8 + (lane >> 2), q = lane & 3;
   const bool owner = q == 0 && d < N;   // writes dp'[d] and back[t][d]
-  constexpr int kPre = 8;
-  TE pre[kPre];
-#pragma unroll
-  for (int r = 0; r < kPre; ++r) pre[r] = (owner && 1 + r < T) ? e[(size_t)(1 + r) * N + d] : TE(0);
-  if (threadIdx.x < 32) dp_buf[0][threadIdx.x] = threadIdx.x < N ? (double)e[threadIdx.x] : -CUDART_INF;
+  // shared address of back[0][d] (smem backpointers), computed once
+  const unsigned back_sa = kSmemBack ? (unsigned)__cvta_generic_to_shared(back) + (unsigned)d : 0u;
+  const int nch = (T + kVitChunk - 1) / kVitChunk;
+  vit_issue_chunk(e, T, N, 0, ebuf);
+  if (nch > 1) {
+    vit_issue_chunk(e, T, N, 1, ebuf);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
   __syncthreads();
-  for (int t0 = 1; t0 < T; t0 += kPre) {
+  if (threadIdx.x < 32) dp_buf[0][threadIdx.x] = threadIdx.x < N ? (double)ebuf[threadIdx.x] : -CUDART_INF;
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    if (c >= 1) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // chunk c landed
+      __syncthreads();
+      if (c + 1 < nch) vit_issue_chunk(e, T, N, c + 1, ebuf);   // into chunk c-1's buffer
+    }
+    const TE *eb = ebuf + (c & 1) * kVitChunk * 32 + (owner ? d : 0);
+    const int tlo = max(1, c * kVitChunk), thi = min(T, (c + 1) * kVitChunk);
+    for (int t = tlo; t < thi; ++t) {
+      const double et = (double)eb[(t - c * kVitChunk) * N];
+      const double2 *pv = reinterpret_cast<const double2 *>(dp_buf[(t - 1) & 1] + 8 * q);
+      double cv[8];
 #pragma unroll
-    for (int r = 0; r < kPre; ++r) {
-      const int t = t0 + r;
-      if (t < T) {
-        const double et = (double)pre[r];
-        const int tn = t + kPre;
-        pre[r] = (owner && tn < T) ? e[(size_t)tn * N + d] : TE(0);
-        const double2 *pv = reinterpret_cast<const double2 *>(dp_buf[(t - 1) & 1] + 8 * q);
-        double c[8];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 x = pv[k];
-          c[2 * k] = x.x + arow[2 * k];          // cand_j = dp[j] + A[i][j] (:276)
-          c[2 * k + 1] = x.y + arow[2 * k + 1];
-        }
-        // first-max tournament over the 8 sources of this quarter
-        double c4[4];
-        int i4[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool tb = vit_take<kNanAware>(c[2 * k], c[2 * k + 1]);
-          c4[k] = tb ? c[2 * k + 1] : c[2 * k];
-          i4[k] = tb ? 2 * k + 1 : 2 * k;
-        }
-        const bool t0b = vit_take<kNanAware>(c4[0], c4[1]);
-        const bool t1b = vit_take<kNanAware>(c4[2], c4[3]);
-        const double c2a = t0b ? c4[1] : c4[0], c2b = t1b ? c4[3] : c4[2];
-        const int i2a = t0b ? i4[1] : i4[0], i2b = t1b ? i4[3] : i4[2];
-        const bool tf = vit_take<kNanAware>(c2a, c2b);
-        double v = tf ? c2b : c2a;
-        int i = 8 * q + (tf ? i2b : i2a);
-        // combine quarters: (0,1) and (2,3), then (01, 23)
-#pragma unroll
-        for (int m = 1; m <= 2; m <<= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, v, m);
-          const int oi = __shfl_xor_sync(0xffffffffu, i, m);
-          vit_merge<kNanAware>(v, i, ov, oi, (q & m) == 0);
-        }
-        if (owner) {
-          back[(size_t)t * N + d] = (uint8_t)i;
-          dp_buf[t & 1][d] = et + v;             // dp'[i] = e[t][i] + cand_back
-        } else if (q == 0) {
-          dp_buf[t & 1][d] = -CUDART_INF;        // destinations >= N never win
-        }
-        __syncthreads();
+      for (int k = 0; k < 4; ++k) {
+        const double2 x = pv[k];
+        cv[2 * k] = x.x + arow[2 * k];          // cand_j = dp[j] + A[i][j] (:276)
+        cv[2 * k + 1] = x.y + arow[2 * k + 1];
       }
+      // first-max tournament over the 8 sources of this quarter
+      double c4[4];
+      int i4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool tb = vit_take<kNanAware>(cv[2 * k], cv[2 * k + 1]);
+        c4[k] = tb ? cv[2 * k + 1] : cv[2 * k];
+        i4[k] = tb ? 2 * k + 1 : 2 * k;
+      }
+      const bool t0b = vit_take<kNanAware>(c4[0], c4[1]);
+      const bool t1b = vit_take<kNanAware>(c4[2], c4[3]);
+      const double c2a = t0b ? c4[1] : c4[0], c2b = t1b ? c4[3] : c4[2];
+      const int i2a = t0b ? i4[1] : i4[0], i2b = t1b ? i4[3] : i4[2];
+      const bool tf = vit_take<kNanAware>(c2a, c2b);
+      double v = tf ? c2b : c2a;
+      int i = 8 * q + (tf ? i2b : i2a);
+      // combine quarters: (0,1) and (2,3), then (01, 23)
+#pragma unroll
+      for (int m = 1; m <= 2; m <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, m);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, m);
+        vit_merge<kNanAware>(v, i, ov, oi, (q & m) == 0);
+      }
+      // dp'[i] = e[t][i] + cand_back; destinations >= N hold -inf (never win)
+      const double nv = owner ? et + v : -CUDART_INF;
+      if (q == 0) dp_buf[t & 1][d] = nv;
+      if (owner) {
+        if (kSmemBack)
+          asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(back_sa + (unsigned)(t * N)), "r"(i)
+                       : "memory");
+        else
+          back[(size_t)t * N + d] = (uint8_t)i;
+      }
+      __syncthreads();
     }
   }
   if (threadIdx.x == 0) {
@@ -138,6 +174,7 @@ __global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em
                                                        uint8_t *__restrict__ back_ws) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) double dp_buf[2][32];
+  __shared__ __align__(16) TE ebuf[2 * kVitChunk * 32];
   const int b = blockIdx.x, N = d.N;
   int64_t *pb = path + (size_t)b * d.Tmax;
   if (status[b] != W2L_OK) {
@@ -161,9 +198,9 @@ __global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em
   // sources j >= N: dp = -inf makes them lose; A may hold inf/NaN (not
   // validated by the reference, :270-272) -- only then the NaN-aware compare
   if (__syncthreads_and(finite))
-    viterbi4_body<TE, kSmemBack, false>(e, T, N, arow, dp_buf, back, score + b, pb);
+    viterbi4_body<TE, kSmemBack, false>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb);
   else
-    viterbi4_body<TE, kSmemBack, true>(e, T, N, arow, dp_buf, back, score + b, pb);
+    viterbi4_body<TE, kSmemBack, true>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb);
   for (int t = T + threadIdx.x; t < d.Tmax; t += blockDim.x) pb[t] = 0;
 }
 

@@ -247,6 +247,23 @@ def test_viterbi_batched_ragged_vs_oracle():
         assert scores[b].item() == s
 
 
+@pytest.mark.parametrize("T,N", [(1, 5), (31, 7), (32, 30), (33, 32), (65, 3),
+                                 (5500, 30)])   # 5500*30 > 160 KB: backpointers in HBM
+def test_viterbi_batched_chunk_edges_vs_oracle(T, N):
+    # emissions are staged 32 frames at a time; lengths around the chunk size
+    # and a batch whose backpointers do not fit in shared memory
+    rng = np.random.default_rng(T * 100 + N)
+    B = 3
+    em = rng.standard_normal((B, T, N)).astype(np.float32)
+    el = np.array([T, max(1, T - 1), max(1, T // 2)], np.int32)
+    a = rng.standard_normal((N, N)).astype(np.float32)
+    paths, scores = C.viterbi_batched(torch.from_numpy(em).cuda(), el, a)
+    for b in range(B):
+        p, s = orc.viterbi(em[b, :el[b]], a)
+        assert np.array_equal(paths[b, :el[b]].cpu().numpy(), p)
+        assert scores[b].item() == s
+
+
 def test_asg_batched_c3_scale_vs_oracle():
     # C3 shape (T=1600 N=30 L=300) on a subset the oracle finishes in seconds
     em, el, tg, tl, a = orc.synth_asg(20260002, 8, 1600, 30, 300)
