@@ -393,12 +393,25 @@ __device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min
 // reference exponent.  Edge sums are accumulated without their constant
 // transition weights (M, S, P), which are applied once in the epilogues.
 
+// Per-warp staging area of asg_fcc_grad (floats): the warp's frames' fcc
+// rows (alpha including frame ta-1, beta), exponents and emission rows come
+// in with one cp.async batch -- with a one-frame register prefetch every
+// frame paid most of a DRAM round trip.  Reused for the block reduction.
+constexpr int kFccFpw = kGradFramesPerBlock / kGradWarps;            // 16 frames per warp
+constexpr int kFccStage = ((kFccFpw + 1) * 32 + 2 * kFccFpw * 32 + 2 * (kFccFpw + 1) + 3) & ~3;
+static_assert(kFccStage >= 1024, "the staging area doubles as the reduction buffer");
+constexpr size_t kFccGradSmem = sizeof(float) * kGradWarps * kFccStage;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
 __global__ void __launch_bounds__(kGradWarps * 32, 2)
     asg_fcc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                         Dims d, AsgFastWs w, float *__restrict__ grad_em,
                         const int32_t *__restrict__ status) {
-  __shared__ __align__(16) float red[kGradWarps][1024];   // accA partials
-  __shared__ __align__(16) float vrow[kGradWarps][32];    // alpha_{t-1} fcc row
+  extern __shared__ __align__(16) float fsm[];
   __shared__ float gwarp[kGradWarps][2];
   const int b = blockIdx.y, blk = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -407,8 +420,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
   const int t0 = blk * kGradFramesPerBlock;
   const bool ok = status[b] == W2L_OK;
   float *ge = grad_em + (size_t)b * d.Tmax * N;
-  const int fpw = kGradFramesPerBlock / kGradWarps;
-  const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
+  const int ta = t0 + warp * kFccFpw, tb = min(ta + kFccFpw, d.Tmax);
   // rows outside the utterance (or a failed utterance) get zero gradient
   for (int t = ta; t < tb; ++t)
     if (!ok || t >= T)
@@ -418,41 +430,46 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
   const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
   const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
   float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
-  const float *emb = em + (size_t)b * d.Tmax * N;
-  const float *fa_r = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
-  const float *fb_r = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
-  const int *ka_r = w.fcc_ka + (size_t)b * w.tpad;
-  const int *kb_r = w.fcc_kb + (size_t)b * w.tpad + 1;
+  const int tend = min(tb, T);
+
+  // ---- stage this warp's frames: row r of sfa/ska is frame ta-1+r, row r of
+  // sfb/skb/se is frame ta+r
+  float *st = fsm + warp * kFccStage;
+  float *sfa = st;                                   // [kFccFpw+1][32]
+  float *sfb = sfa + (kFccFpw + 1) * 32;             // [kFccFpw][32]
+  float *se = sfb + kFccFpw * 32;                    // [kFccFpw][N] (flat)
+  int *ska = reinterpret_cast<int *>(se + kFccFpw * 32);   // [kFccFpw+1]
+  int *skb = ska + kFccFpw + 1;                      // [kFccFpw]
+  if (ta < tend) {
+    const int f0 = max(ta - 1, 0), nf = tend - ta;
+    const float *fa_g = w.fcc_a + (size_t)b * d.Tmax * 32;
+    const float *fb_g = w.fcc_b + (size_t)b * d.Tmax * 32;
+    const int nfa = (tend - f0) * 8;   // 16-byte chunks
+    float *dfa = sfa + (f0 - (ta - 1)) * 32;
+    for (int i = lane; i < nfa; i += 32) cp_async16(dfa + 4 * i, fa_g + (size_t)f0 * 32 + 4 * i);
+    for (int i = lane; i < nf * 8; i += 32) cp_async16(sfb + 4 * i, fb_g + (size_t)ta * 32 + 4 * i);
+    const float *e_g = em + ((size_t)b * d.Tmax + ta) * N;
+    for (int i = lane; i < nf * N; i += 32) cp_async4(se + i, e_g + i);
+    const int *ka_g = w.fcc_ka + (size_t)b * w.tpad;
+    const int *kb_g = w.fcc_kb + (size_t)b * w.tpad + 1;
+    if (lane < tend - f0) cp_async4(ska + (f0 - (ta - 1)) + lane, ka_g + f0 + lane);
+    if (lane < nf) cp_async4(skb + lane, kb_g + ta + lane);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncwarp();
+
   unsigned long long accA[16];   // accA[jj] = (row lane, columns 2jj, 2jj+1)
 #pragma unroll
   for (int j = 0; j < 16; ++j) accA[j] = 0ull;
-  float *myv = vrow[warp];
-  const int tend = min(tb, T);
-  float pfa = 0.f;
-  int pka = 0;
-  if (ta >= 1 && ta < tend) {
-    pfa = fa_r[(unsigned)(ta - 1) * 32];
-    pka = ka_r[ta - 1];
-  }
-  // the next frame's inputs are loaded while this frame is processed (each
-  // frame otherwise pays a full DRAM round trip)
-  float e_n = 0.f, fa_n = 0.f, fb_n = 0.f;
-  int ka_n = 0, kb_n = 0;
-  auto load_fcc = [&](int t) {
-    e_n = lane < N ? emb[(unsigned)t * N + lane] : -CUDART_INF_F;
-    fa_n = fa_r[(unsigned)t * 32];
-    fb_n = fb_r[(unsigned)t * 32];
-    ka_n = ka_r[t];
-    kb_n = kb_r[t];
-  };
-  if (ta < tend) load_fcc(ta);
+#pragma unroll 2
   for (int t = ta; t < tend; ++t) {
-    const float e = e_n, fa = fa_n, fb = fb_n;
-    const int ka = ka_n, kb = kb_n;
-    if (t + 1 < tend) load_fcc(t + 1);
+    const int r = t - ta;
+    const float e = lane < N ? se[r * N + lane] : -CUDART_INF_F;
+    const float fa = sfa[(r + 1) * 32 + lane], fb = sfb[r * 32 + lane];
+    const int ka = ska[r + 1], kb = skb[r];
     const float m = warp_max(e);
     const float et = lane < N ? et_of(e, m) : 0.f;
-    myv[lane] = pfa;
     // fcc node posteriors (:238): the full part of the gradient row
     const float gam = fa * fb;
     const float zf = warp_sum(gam);
@@ -461,11 +478,10 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
     if (lane < N) ge[(unsigned)t * N + lane] = gam * izf;
-    __syncwarp();
     if (t >= 1) {
       // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
-      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(pka - ka) * izf);
-      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(myv);
+      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(ska[r] - ka) * izf);
+      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(sfa + r * 32);
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
         const ulonglong2 x = pv[qq];
@@ -473,14 +489,13 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
         accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
       }
     }
-    pfa = fa;
-    pka = ka;
-    __syncwarp();
   }
+  __syncwarp();
+  float *red = st;   // this warp's partial [32][32]
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    red[warp][lane * 32 + 2 * j] = f2_lo(accA[j]);
-    red[warp][lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
+    red[lane * 32 + 2 * j] = f2_lo(accA[j]);
+    red[lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
   }
   if (lane == 0) {
     gwarp[warp][0] = gmin;
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
   float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
     float s = 0.f;
-    for (int q = 0; q < kGradWarps; ++q) s += red[q][i];
+    for (int q = 0; q < kGradWarps; ++q) s += fsm[q * kFccStage + i];
     dstA[i] = s;
   }
   if (threadIdx.x < 2) {
@@ -892,8 +907,11 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
     return cudaGetLastError();
   }
   if (!(phases & 2u)) return cudaSuccess;
-  asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, d, w, grad_em,
-                                                                    status);
+  err = cudaFuncSetAttribute(asg_fcc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kFccGradSmem);
+  if (err != cudaSuccess) return err;
+  asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, kFccGradSmem, s>>>(
+      em, em_len, d, w, grad_em, status);
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   switch (w.W) {
