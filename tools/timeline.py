@@ -98,12 +98,41 @@ def main():
         t1.record(main_s)
         rec.append((t0, marks, t1))
 
-    for split in (False, True, "stagger"):
+    hi_s = torch.cuda.Stream(device=dev, priority=-5)   # clamped to the device's range
+
+    def prio(rec, asg_hi=True):
+        # ASG (the tail of the step) on a high-priority stream, CTC on a
+        # normal one (asg_hi=False: the other way round)
+        t0 = ev()
+        t0.record(main_s)
+        a_s, c_s = (hi_s, side) if asg_hi else (side, hi_s)
+        a_s.wait_stream(main_s)
+        c_s.wait_stream(main_s)
+        marks = {}
+        with torch.cuda.stream(c_s):
+            C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False,
+                                    workspace=ws_c, out=oc)
+            marks["ctc_end"] = ev()
+            marks["ctc_end"].record(c_s)
+        with torch.cuda.stream(a_s):
+            C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a,
+                                    out=oa)
+            marks["asg_end"] = ev()
+            marks["asg_end"].record(a_s)
+        main_s.wait_stream(a_s)
+        main_s.wait_stream(c_s)
+        t1 = ev()
+        t1.record(main_s)
+        rec.append((t0, marks, t1))
+
+    for split in (False, True, "stagger", "asg_hi", "ctc_hi", False):
         recs = []
         for i in range(25):
             flush.zero_()
             if split == "stagger":
                 stagger(recs if i >= 5 else [])
+            elif split in ("asg_hi", "ctc_hi"):
+                prio(recs if i >= 5 else [], split == "asg_hi")
             else:
                 step(split, recs if i >= 5 else [])
         torch.cuda.synchronize()
@@ -112,7 +141,8 @@ def main():
             for k, e in marks.items():
                 rows.setdefault(k, []).append(t0.elapsed_time(e))
             rows.setdefault("step", []).append(t0.elapsed_time(t1))
-        print({False: "whole", True: "split", "stagger": "stagger"}[split], {k: round(float(np.median(v)), 4)
+        print({False: "whole", True: "split", "stagger": "stagger", "asg_hi": "asg_hi",
+               "ctc_hi": "ctc_hi"}[split], {k: round(float(np.median(v)), 4)
                                              for k, v in rows.items()})
     # each criterion alone
     for name, fn in (("asg_alone", lambda: C.asg_loss_grad_batched(
