@@ -407,25 +407,21 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 
-__global__ void __launch_bounds__(kGradWarps * 32, 2)
-    asg_fcc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
-                        Dims d, AsgFastWs w, float *__restrict__ grad_em,
-                        const int32_t *__restrict__ status) {
+// fcc edge posteriors and the fcc guard (the fcc node posteriors are formed
+// by asg_fac_grad_body, which writes the whole gradient row)
+__device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
+                                                  const int32_t *__restrict__ em_len, Dims d,
+                                                  const AsgFastWs &w,
+                                                  const int32_t *__restrict__ status, int blk) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ float gwarp[kGradWarps][2];
-  const int b = blockIdx.y, blk = blockIdx.x;
+  const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
   const int T = em_len[b];
   const int t0 = blk * kGradFramesPerBlock;
-  const bool ok = status[b] == W2L_OK;
-  float *ge = grad_em + (size_t)b * d.Tmax * N;
+  if (status[b] != W2L_OK) return;
   const int ta = t0 + warp * kFccFpw, tb = min(ta + kFccFpw, d.Tmax);
-  // rows outside the utterance (or a failed utterance) get zero gradient
-  for (int t = ta; t < tb; ++t)
-    if (!ok || t >= T)
-      if (lane < N) ge[(size_t)t * N + lane] = 0.f;
-  if (!ok) return;
   const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
   const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
   const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
@@ -470,14 +466,13 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
     const int ka = ska[r + 1], kb = skb[r];
     const float m = warp_max(e);
     const float et = lane < N ? et_of(e, m) : 0.f;
-    // fcc node posteriors (:238): the full part of the gradient row
-    const float gam = fa * fb;
-    const float zf = warp_sum(gam);
+    // the frame's fcc normaliser (the node posteriors themselves, :238, are
+    // formed in asg_fac_grad_body)
+    const float zf = warp_sum(fa * fb);
     const float izf = 1.f / zf;
     const float g = __log2f(zf) + (float)(ka + kb - refFi) - refFf;
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
-    if (lane < N) ge[(unsigned)t * N + lane] = gam * izf;
     if (t >= 1) {
       // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
       const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(ska[r] - ka) * izf);
@@ -516,12 +511,13 @@ __global__ void __launch_bounds__(kGradWarps * 32, 2)
   }
 }
 
+// The whole gradient row: fcc node posteriors (full part, :238) minus the
+// fac node posteriors gathered by token (:214-217), plus the fac occupancy.
 template <int W>
-__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
-    asg_fac_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
-                        const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
-                        const float *__restrict__ trans, Dims d, AsgFastWs w,
-                        float *__restrict__ grad_em, const int32_t *__restrict__ status) {
+__device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em_len,
+                                                  const int32_t *__restrict__ tgt_len, Dims d,
+                                                  const AsgFastWs &w, float *__restrict__ grad_em,
+                                                  const int32_t *__restrict__ status, int blk) {
   constexpr int LP = W * kLatStates;
   extern __shared__ __align__(16) float gsm[];
   // [kGradWarps][LP] posterior row; after its frame loop each warp reuses
@@ -534,26 +530,29 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
   // posterior row (the gather is then load-address, load-value, add)
   unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][2 LP]
 
-  const int b = blockIdx.y, blk = blockIdx.x;
+  const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
   const int T = em_len[b];
   const int t0 = blk * kGradFramesPerBlock;
-  if (status[b] != W2L_OK) return;
-  if (t0 >= T) {
-    // keep the partial buffers well-defined for the final reduction
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x)
-      w.part_fullA[((size_t)b * w.nblk + blk) * 1024 + i] = 0.f;
-    for (int i = threadIdx.x; i < LP; i += blockDim.x)
-      w.part_edge[((size_t)b * w.nblk + blk) * LP + i] = 0.f;
-    if (threadIdx.x < 4)
-      w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] =
-          (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
-    return;
-  }
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
+  const bool ok = status[b] == W2L_OK;
+  // rows outside the utterance (or of a failed utterance) get zero gradient
+  for (int t = max(ta, ok ? T : 0); t < tb; ++t)
+    if (lane < N) ge[(size_t)t * N + lane] = 0.f;
+  if (!ok) return;
+  if (t0 >= T) {
+    // keep the partial buffers well-defined for the final reduction (the
+    // fcc part and its guard half come from asg_fcc_grad_body)
+    for (int i = threadIdx.x; i < LP; i += blockDim.x)
+      w.part_edge[((size_t)b * w.nblk + blk) * LP + i] = 0.f;
+    if (threadIdx.x < 2)
+      w.part_guard[((size_t)b * w.nblk + blk) * 4 + 2 + threadIdx.x] =
+          (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
+    return;
+  }
 
   const int L = tgt_len[b];
   // segments the chain wrote for this utterance (the batch's W may be wider)
@@ -605,10 +604,15 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) accO[sw][k] = 0.f;
   const int tend = min(tb, T);
-  // the gradient-row value (written by asg_fcc_grad) of the next frame is
-  // loaded one frame ahead
-  float g_nx = 0.f;
-  if (ta < tend && lane < N) g_nx = ge[(unsigned)ta * N + lane];
+  // the fcc rows of the next frame (full-part node posteriors) are loaded one
+  // frame ahead
+  const float *fca = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
+  const float *fcb = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
+  float ca_nx = 0.f, cb_nx = 0.f;
+  if (ta < tend) {
+    ca_nx = fca[(unsigned)ta * 32];
+    cb_nx = fcb[(unsigned)ta * 32];
+  }
   // the rows are loaded one frame ahead too (segments >= weff read zeros)
   float4 na[W], nb[W];
   int nea[W], neb[W];
@@ -641,8 +645,11 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
         neb[sw] = EB[sw * sege + tq + 32];
       }
     }
-    const float g_old = g_nx;
-    if (t + 1 < tend && lane < N) g_nx = ge[(unsigned)(t + 1) * N + lane];
+    const float gam = ca_nx * cb_nx;   // fcc node posterior, unnormalised
+    if (t + 1 < tend) {
+      ca_nx = fca[(unsigned)(t + 1) * 32];
+      cb_nx = fcb[(unsigned)(t + 1) * 32];
+    }
     // fac node posteriors (:214-217)
     float zl = 0.f;
     float4 p[W];
@@ -658,6 +665,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     }
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
+    const float izf = 1.f / warp_sum(gam);
     const float g = __log2f(zc) - refCf;
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     } else {
       con = gather_shared(myaddr, ts0, ts1);
     }
-    if (lane < N) ge[tq / 32 * N + lane] = g_old - con * izc;
+    if (lane < N) ge[tq / 32 * N + lane] = gam * izf - con * izc;
     __syncwarp();
   }
 
@@ -818,17 +826,33 @@ __global__ void asg_loss_only_kernel(Dims d, AsgFastWs w, double *loss, int32_t 
   if (!isfinite(zF - zC)) status[b] = kNeedsExact;
 }
 
+// One launch for both gradient kernels; they are independent, so their CTAs
+// run side by side.  The kinds alternate in x (even: fac + gradient row, odd:
+// fcc edges) so that both are dispatched from the start of the launch.
 template <int W>
-cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
-                          const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
-                          float *grad_em, const int32_t *status, cudaStream_t s) {
+__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
+    asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
+                    const int32_t *__restrict__ tgt_len, Dims d, AsgFastWs w,
+                    float *__restrict__ grad_em, const int32_t *__restrict__ status) {
+  const int blk = blockIdx.x >> 1;
+  if ((blockIdx.x & 1) == 0)
+    asg_fac_grad_body<W>(em_len, tgt_len, d, w, grad_em, status, blk);
+  else
+    asg_fcc_grad_body(em, em_len, d, w, status, blk);
+}
+
+template <int W>
+cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int32_t *tgt_len, Dims d,
+                          const AsgFastWs &w, float *grad_em, const int32_t *status,
+                          cudaStream_t s) {
   constexpr int LP = W * kLatStates;
-  const size_t smem = sizeof(float) * (kGradWarps * (LP + 2 + 2 + 2 * LP));
-  auto k = asg_fac_grad_kernel<W>;
+  const size_t smem = std::max(sizeof(float) * (kGradWarps * (LP + 2 + 2 + 2 * LP)),
+                               kFccGradSmem);
+  auto k = asg_grad_kernel<W>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
-                                                      grad_em, status);
+  k<<<dim3(2 * w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt_len, d, w, grad_em,
+                                                         status);
   return cudaGetLastError();
 }
 
@@ -907,22 +931,15 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
     return cudaGetLastError();
   }
   if (!(phases & 2u)) return cudaSuccess;
-  err = cudaFuncSetAttribute(asg_fcc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kFccGradSmem);
-  if (err != cudaSuccess) return err;
-  asg_fcc_grad_kernel<<<dim3(w.nblk, d.B), kGradWarps * 32, kFccGradSmem, s>>>(
-      em, em_len, d, w, grad_em, status);
-  err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
   switch (w.W) {
-    case 1: err = launch_grad_w<1>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 2: err = launch_grad_w<2>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 3: err = launch_grad_w<3>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 4: err = launch_grad_w<4>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 5: err = launch_grad_w<5>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 6: err = launch_grad_w<6>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 7: err = launch_grad_w<7>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
-    case 8: err = launch_grad_w<8>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, s); break;
+    case 1: err = launch_grad_w<1>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 2: err = launch_grad_w<2>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 3: err = launch_grad_w<3>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 4: err = launch_grad_w<4>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 5: err = launch_grad_w<5>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 6: err = launch_grad_w<6>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 7: err = launch_grad_w<7>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
+    case 8: err = launch_grad_w<8>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
     default: return cudaErrorInvalidValue;
   }
   if (err != cudaSuccess) return err;
