@@ -72,8 +72,9 @@ for r in data:
         dur /= 1e3
     rd = to_mb(r[ix["dram__bytes_read.sum"]], units[ix["dram__bytes_read.sum"]])
     wr = to_mb(r[ix["dram__bytes_write.sum"]], units[ix["dram__bytes_write.sum"]])
-    key = keymap.get(name, "asg_grad_fac" if name.startswith("asg_fac_grad") else
-                     ("ctc_grad" if name.startswith("ctc_grad") else name))
+    key = keymap.get(name, "asg_grad" if name.startswith("asg_grad") else
+                     ("asg_grad_fac" if name.startswith("asg_fac_grad") else
+                      ("ctc_grad" if name.startswith("ctc_grad") else name)))
     traffic[key] = int((rd + wr) * 1e6)
     inst = float(r[ix["smsp__inst_executed.sum"]].replace(",", "")) / 102400
     out.append(f"{name:30s}{dur:9.1f}{rd:11.1f}{wr:11.1f}"
