@@ -472,10 +472,10 @@ def main():
                          f"oracle port (float64 numpy), one utterance per task, process pool "
                          f"of {cores}"}
 
-    # our kernels per step: ASG em_check, prep, chain, fcc_grad, fac_grad, final,
-    # exact (fallback, early exit), reduce; CTC em_check, prep, chain, grad,
-    # final, exact
-    launches_per_step = 8 + 6
+    # our kernels per step: ASG em_check, prep, chain, grad (fac + fcc CTAs in
+    # one launch), final, exact (fallback, early exit), reduce; CTC em_check,
+    # prep, chain, grad, final, exact
+    launches_per_step = 7 + 6
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
