@@ -761,17 +761,21 @@ __global__ void __launch_bounds__(1024)
   // fixed-order sums of the per-frame-block partials; 4 independent
   // accumulators keep several loads in flight per thread
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
+  // (16 partials are loaded at once -- one memory latency per 16 blocks --
+  // then added in a fixed order)
   auto sum_parts = [&](const float *base, size_t stride) {
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    int q = 0;
-    for (; q + 4 <= nb_used; q += 4) {
-      a0 += base[(size_t)q * stride];
-      a1 += base[(size_t)(q + 1) * stride];
-      a2 += base[(size_t)(q + 2) * stride];
-      a3 += base[(size_t)(q + 3) * stride];
+    float acc = 0.f;
+    for (int q0 = 0; q0 < nb_used; q0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = q0 + k < nb_used ? base[(size_t)(q0 + k) * stride] : 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) v[k] += v[k + 1];
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) v[k] += v[k + 2];
+      acc += (v[0] + v[4]) + (v[8] + v[12]);
     }
-    for (; q < nb_used; ++q) a0 += base[(size_t)q * stride];
-    return (a0 + a1) + (a2 + a3);
+    return acc;
   };
   for (int i = threadIdx.x; i < LP; i += blockDim.x)
     sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * LP + i, LP);
