@@ -503,6 +503,42 @@ def test_ctc_batched_edge_sizes(t_max, n, l_max):
     assert orc.rel_err(out.grad_emissions.cpu().numpy(), ge) < REL
 
 
+def test_asg_batched_mixed_widths_and_block_edges():
+    # one batch whose utterances use 1..4 lattice warps (weff below the
+    # batch's W), lengths at the 16-frame warp and 128-frame block edges of
+    # the gradient kernels, and one utterance that fails validation (its rows
+    # must come back zero and the others must be unaffected)
+    rng = np.random.default_rng(81)
+    lens = [(16, 1), (140, 127), (128, 128), (129, 129), (255, 200), (256, 256), (300, 257),
+            (400, 384), (450, 385), (500, 450)]
+    b_sz, t_max, n = len(lens) + 1, 520, 30
+    em = rng.standard_normal((b_sz, t_max, n), dtype=np.float32)
+    a = rng.standard_normal((n, n)).astype(np.float32)
+    el = np.array([t for t, _ in lens] + [300], np.int32)
+    tl = np.array([l for _, l in lens] + [100], np.int32)
+    tg = np.full((b_sz, int(tl.max())), -1, np.int64)
+    for b in range(b_sz):
+        seq = [int(rng.integers(0, n))]
+        while len(seq) < tl[b]:
+            v = int(rng.integers(0, n))
+            if v != seq[-1]:
+                seq.append(v)
+        tg[b, :tl[b]] = seq
+        em[b, el[b]:] = 0.0
+    em[-1, 5, 3] = np.nan          # the failing utterance: non-finite emission
+    out = C.asg_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, a, check=False,
+                                  per_utterance_grad_transitions=True)
+    st = out.status.cpu().numpy()
+    assert st[-1] != 0 and (st[:-1] == 0).all()
+    ge_gpu = out.grad_emissions.cpu().numpy()
+    assert not ge_gpu[-1].any()
+    good = slice(0, b_sz - 1)
+    loss, ge, ga = orc.asg_batch(em[good], el[good], tg[good], tl[good], a)
+    np.testing.assert_allclose(out.loss.cpu().numpy()[good], loss, rtol=REL)
+    assert orc.rel_err(ge_gpu[good], ge) < REL
+    assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
+
+
 def test_maximum_lattices():
     # the largest supported lattices: ASG L = 1024 (8 lattice warps) and CTC
     # L = 511 (2L+1 = 1023 states, 8 warps), N = 32
