@@ -539,6 +539,34 @@ def test_asg_batched_mixed_widths_and_block_edges():
     assert orc.rel_err(out.grad_transitions.cpu().numpy(), ga) < REL
 
 
+def test_ctc_batched_mixed_widths_and_block_edges():
+    # CTC counterpart: lattices of 1..5 warps (S = 2L+1) in one batch, the
+    # empty target, lengths at the gradient kernel's block edges, and one
+    # utterance that fails validation (a row that is not log-normalised)
+    rng = np.random.default_rng(82)
+    lens = [(16, 0), (16, 3), (128, 63), (129, 64), (256, 127), (300, 128), (400, 191),
+            (450, 192), (500, 255), (520, 256)]
+    b_sz, t_max, n = len(lens) + 1, 600, 29
+    blank = n - 1
+    em = orc.log_softmax_rows(2.0 * rng.standard_normal((b_sz, t_max, n))).astype(np.float32)
+    el = np.array([t for t, _ in lens] + [300], np.int32)
+    tl = np.array([l for _, l in lens] + [50], np.int32)
+    tg = np.full((b_sz, int(tl.max())), -1, np.int64)
+    for b in range(b_sz):
+        tg[b, :tl[b]] = rng.integers(0, n - 1, size=tl[b])
+        em[b, el[b]:] = 0.0
+    em[-1, 7, :] += 1.0            # |logsumexp| = 1 > 1e-2: ContractError
+    out = C.ctc_loss_grad_batched(torch.from_numpy(em).cuda(), el, tg, tl, blank, check=False)
+    st = out.status.cpu().numpy()
+    assert st[-1] != 0 and (st[:-1] == 0).all()
+    ge_gpu = out.grad_emissions.cpu().numpy()
+    assert not ge_gpu[-1].any()
+    good = slice(0, b_sz - 1)
+    loss, ge = orc.ctc_batch(em[good], el[good], tg[good], tl[good], blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy()[good], loss, rtol=REL, atol=1e-5)
+    assert orc.rel_err(ge_gpu[good], ge) < REL
+
+
 def test_maximum_lattices():
     # the largest supported lattices: ASG L = 1024 (8 lattice warps) and CTC
     # L = 511 (2L+1 = 1023 states, 8 warps), N = 32
