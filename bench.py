@@ -250,7 +250,8 @@ def main():
     main_s = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def both(em_, el_, ta_, tc_, tl_):
+    def both(em_, el_, ta_, tc_, tl_, outs=None):
+        oa_, oc_ = outs if outs is not None else (out_a, out_c)
         # the two criteria run concurrently on two streams (chain CTAs of both
         # are co-resident: maximum shared-memory carveout).  The split-phase
         # schedule (all recursions, then all gradient phases; phase="chain" /
@@ -259,9 +260,9 @@ def main():
         side.wait_stream(main_s)
         with torch.cuda.stream(side):
             oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False, workspace=ws_c,
-                                         out=out_c)
+                                         out=oc_)
         oa = C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
-                                     out=out_a)
+                                     out=oa_)
         allreduce_grad_transitions(oa.grad_transitions)
         main_s.wait_stream(side)
         return oa, oc
@@ -309,8 +310,16 @@ def main():
     bufs = [dict(em=torch.empty_like(em_d), ta=torch.empty_like(ta_d), tc=torch.empty_like(tc_d),
                  el=torch.empty_like(el_d), tl=torch.empty_like(tl_d)) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
+    d2h_s = torch.cuda.Stream(device=dev)   # loss read-back off the compute stream
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
+    read_back = [torch.cuda.Event() for _ in range(2)]
+    # outputs double-buffered like the inputs: step i+2 reuses step i's
+    # outputs only after step i's losses reached the host
+    outs = [(out_a, out_c),
+            (C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a),
+             C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False,
+                                     workspace=ws_c))]
 
     def e2e_step(i):
         bi = bufs[i & 1]
@@ -324,10 +333,17 @@ def main():
             bi["tl"].copy_(tl_h, non_blocking=True)
             copied[i & 1].record(copy_s)
         main_s.wait_event(copied[i & 1])
-        oa, oc = both(bi["em"], bi["el"], bi["ta"], bi["tc"], bi["tl"])
+        if i >= 2:
+            main_s.wait_event(read_back[i & 1])       # outputs free again
+        oa, oc = both(bi["em"], bi["el"], bi["ta"], bi["tc"], bi["tl"], outs[i & 1])
         consumed[i & 1].record(main_s)
-        loss_a_h.copy_(oa.loss, non_blocking=True)
-        loss_c_h.copy_(oc.loss, non_blocking=True)
+        # the losses go back on their own stream, so the next step's kernels
+        # do not queue behind the copy
+        with torch.cuda.stream(d2h_s):
+            d2h_s.wait_event(consumed[i & 1])
+            loss_a_h.copy_(oa.loss, non_blocking=True)
+            loss_c_h.copy_(oc.loss, non_blocking=True)
+            read_back[i & 1].record(d2h_s)
 
     for i in range(args.warmup):
         e2e_step(i)
@@ -344,6 +360,7 @@ def main():
     copy_s.wait_stream(main_s)
     for i in range(args.steps):
         e2e_step(i)
+    main_s.wait_stream(d2h_s)                  # the last losses are on the host
     e_e.record(main_s)
     e_e.synchronize()
     e2e_ms = e_s.elapsed_time(e_e)
