@@ -102,6 +102,44 @@ __global__ void fcc_probe(float *out, long long *cyc, int steps) {
   if (lane == 0) *cyc = t1 - t0;
 }
 
+// two warps: warp w sums columns [16w, 16w+16) of row `lane`; partial sums
+// cross through shared memory behind a 64-thread named barrier; each warp
+// keeps its own copy of the new vector (no second barrier)
+__global__ void fcc_probe2(float *out, long long *cyc, int steps) {
+  __shared__ __align__(16) float vbuf[2][32];     // per-warp copy of v
+  __shared__ float part[2][2][32];                // [parity][warp][row]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float m[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) m[j] = 0.03f * ((lane * 7 + (16 * w + j) * 3) % 11);
+  float v = 1.f;
+  vbuf[w][lane] = v;
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int t = 1; t < steps; ++t) {
+    const float4 *pv = reinterpret_cast<const float4 *>(vbuf[w]) + 4 * w;
+    float acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 x = pv[q];
+      acc[q] = m[4 * q] * x.x;
+      acc[q] = fmaf(m[4 * q + 1], x.y, acc[q]);
+      acc[q] = fmaf(m[4 * q + 2], x.z, acc[q]);
+      acc[q] = fmaf(m[4 * q + 3], x.w, acc[q]);
+    }
+    const float sw = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    part[t & 1][w][lane] = sw;
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const float so = part[t & 1][w ^ 1][lane];
+    v = (w == 0 ? sw + so : so + sw) * 0.5f;       // same order in both warps
+    vbuf[w][lane] = v;
+    __syncwarp();
+  }
+  const long long t1 = clock64();
+  if (w == 0) out[lane] = v;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+
 int main() {
   float *out;
   long long *cyc, h;
@@ -125,5 +163,10 @@ int main() {
       cudaMemcpy(&h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
       if (rep) printf("%-34s %6.1f cycles/step\n", names[v], (double)h / (steps - 1));
     }
+  for (int rep = 0; rep < 2; ++rep) {
+    fcc_probe2<<<1, 64>>>(out, cyc, steps);
+    cudaMemcpy(&h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    if (rep) printf("%-34s %6.1f cycles/step\n", "two warps, named barrier", (double)h / (steps - 1));
+  }
   return 0;
 }
