@@ -440,6 +440,21 @@ def main():
         },
     }
 
+    # the HBM-bound gradient stages: their measured DRAM traffic per launch
+    # (committed ncu --set full capture, profiles/traffic.json) over the stage
+    # time measured here -- how close the workspace-row streaming runs to the
+    # HBM peak (the contract roofline above counts algorithmic bytes only)
+    roof_dram = {}
+    for crit_, stages_ in (("asg", ta_run.stage_ms), ("ctc", tc_run.stage_ms)):
+        traffic = _ncu_traffic(f"{crit_}_grad")
+        if traffic and stages_.get("grad"):
+            gbs = traffic / (stages_["grad"] / 1e3) / 1e9
+            roof_dram[f"{crit_}_grad"] = {"dram_bytes_per_launch": traffic,
+                                         "kernel_ms": stages_["grad"], "achieved_gbs": gbs,
+                                         "frac": gbs / hbm_peak}
+    roof_dram = {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "peak_source": hbm_src,
+                 "kernels": roof_dram} if roof_dram else None
+
     sub = {"asg_stage_ms": ta_run.stage_ms, "ctc_stage_ms": tc_run.stage_ms,
            "peaks": peaks, "fp32_guard_fallbacks": fallbacks}
     if not args.no_sub:
@@ -508,6 +523,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
         "roofline_sfu": roof_sfu,
+        "roofline_dram_grad": roof_dram,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "sub": sub,
