@@ -231,9 +231,12 @@ __global__ void __launch_bounds__(kExactThreads)
     for (int p = threadIdx.x; p < N * N; p += blockDim.x) {
       const int i = p / N, j = p % N;
       double con = 0.0;
+      int prev = -1;   // y[l-1], carried (a paired y[l-1], y[l] load ran past y's end)
       for (int l = 0; l < L; ++l) {
-        if (y[l] == i && y[l] == j) con += edge[l];
-        if (l > 0 && y[l] == i && y[l - 1] == j) con += edge[Lmax + l];
+        const int yl = y[l];
+        if (yl == i && yl == j) con += edge[l];
+        if (l > 0 && yl == i && prev == j) con += edge[Lmax + l];
+        prev = yl;
       }
       ga_utt[(size_t)b * N * N + p] = (float)(fullA[p] - con);          // :246
     }
