@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(1024)
     sy[l] = (int)y[l];
     sperm[l] = w.perm[(size_t)b * w.lpad + l];
   }
-  if (threadIdx.x < 33) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];
+  if (threadIdx.x <= N) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];   // N+1 written
   // fixed-order sums of the per-frame-block partials; 4 independent
   // accumulators keep several loads in flight per thread
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
