@@ -409,6 +409,29 @@ def test_ctc_logits_fused_log_softmax():
     assert orc.rel_err(out.grad_emissions.cpu().numpy(), gx) < REL
 
 
+def test_ctc_logits_mixed_widths():
+    # f1 on a batch mixing lattice widths (S = 2L+1 over 1..5 warps), the empty
+    # target and the gradient kernel's block edges, loss-only included
+    rng = np.random.default_rng(46)
+    lens = [(16, 0), (128, 63), (129, 64), (256, 127), (300, 191), (520, 256)]
+    b_sz, t_max, n = len(lens), 540, 29
+    blank = n - 1
+    x = (2.0 * rng.standard_normal((b_sz, t_max, n))).astype(np.float32)
+    el = np.array([t for t, _ in lens], np.int32)
+    tl = np.array([l for _, l in lens], np.int32)
+    tg = np.full((b_sz, int(tl.max())), -1, np.int64)
+    for b in range(b_sz):
+        tg[b, :tl[b]] = rng.integers(0, n - 1, size=tl[b])
+        x[b, el[b]:] = 0.0
+    xd = torch.from_numpy(x).cuda()
+    out = C.ctc_loss_grad_batched(xd, el, tg, tl, blank, logits=True)
+    loss, gx = _ctc_logits_oracle(x, el, tg, tl, blank)
+    np.testing.assert_allclose(out.loss.cpu().numpy(), loss, rtol=REL)
+    assert orc.rel_err(out.grad_emissions.cpu().numpy(), gx) < REL
+    lo = C.ctc_loss_grad_batched(xd, el, tg, tl, blank, logits=True, loss_only=True)
+    np.testing.assert_allclose(lo.loss.cpu().numpy(), loss, rtol=REL)
+
+
 def test_ctc_logits_float64_fallback():
     # extreme logits break the fp32 lattice; the float64 recompute (logits mode
     # of the exact kernel) must still match the reference composition
