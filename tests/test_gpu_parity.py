@@ -247,6 +247,28 @@ def test_viterbi_batched_ragged_vs_oracle():
         assert scores[b].item() == s
 
 
+def test_viterbi_batched_nonfinite_transitions_vs_oracle():
+    # A is not validated by the reference's viterbi (criterion.py:270-272):
+    # forbidden transitions (-inf) and a NaN entry take the NaN-aware
+    # tournament (np.argmax: the first NaN is the maximum)
+    rng = np.random.default_rng(83)
+    B, T, N = 3, 200, 12
+    em = rng.standard_normal((B, T, N)).astype(np.float32)
+    el = np.array([200, 150, 37], np.int32)
+    for a_mod in ("neginf", "nan"):
+        a = rng.standard_normal((N, N)).astype(np.float32)
+        a[rng.random((N, N)) < 0.3] = -np.inf
+        a[np.arange(N), np.arange(N)] = 0.0     # keep every token reachable
+        if a_mod == "nan":
+            a[3, 5] = np.nan
+        paths, scores = C.viterbi_batched(torch.from_numpy(em).cuda(), el, a)
+        for b in range(B):
+            p, sc = orc.viterbi(em[b, :el[b]], a)
+            assert np.array_equal(paths[b, :el[b]].cpu().numpy(), p)
+            got = scores[b].item()
+            assert (np.isnan(got) and np.isnan(sc)) or got == sc
+
+
 @pytest.mark.parametrize("T,N", [(1, 5), (31, 7), (32, 30), (33, 32), (65, 3),
                                  (5500, 30)])   # 5500*30 > 160 KB: backpointers in HBM
 def test_viterbi_batched_chunk_edges_vs_oracle(T, N):
