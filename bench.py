@@ -10,9 +10,14 @@ per-GPU shard of B=64 utterances, T=1600 frames, N=30 tokens, L=300 labels
 ASG and CTC run concurrently on two streams.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--global-batch G]   # strong scaling: G utterances split over N
 
-Multi-GPU: launched by torchrun, one process per GPU; timing is the max over
-ranks.  Prints ONE JSON line on rank 0.
+Multi-GPU: one process per GPU (torchrun; with --gpus N > 1 and no
+WORLD_SIZE in the environment the script re-launches itself under
+torch.distributed.run).  Contiguous batch shards (trainer.py:433), ONE
+all-reduce of the 3.6 KB transition gradient per step through the library's
+own NCCL entry (w2l_allreduce_grad_A) on the compute stream; timing is the
+max over ranks.  Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -20,6 +25,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,15 +39,16 @@ sys.path.insert(0, ROOT)
 METRIC = "ASG/CTC loss+grad frames/sec (B×T) at 1/2/4/8 B200; % of HBM/SFU roofline"
 B_PER_GPU, T_FR, N_TOK, L_LAB = 64, 1600, 30, 300
 SEED = 20260004  # 20260000 + config index (C5)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 # ---------------------------------------------------------------- inputs --
 
 def make_inputs(rank: int, b=B_PER_GPU, t=T_FR, n=N_TOK, l=L_LAB):
-    """Seeded synthetic shard for `rank`: emissions log_softmax(2 N(0,1))
-    (f64 -> f32; valid CTC input, used for ASG too), ASG targets without
-    consecutive duplicates, CTC targets over the N-1 non-blank ids,
-    N(0,1) transitions (identical on every rank)."""
+    """Seeded synthetic block `rank` of 64 utterances: emissions
+    log_softmax(2 N(0,1)) (f64 -> f32; valid CTC input, used for ASG too),
+    ASG targets without consecutive duplicates, CTC targets over the N-1
+    non-blank ids, N(0,1) transitions (identical on every rank)."""
     rng = np.random.default_rng(SEED + 1000 * rank)
     x = 2.0 * rng.standard_normal((b, t, n))
     x -= x.max(axis=2, keepdims=True)
@@ -60,13 +67,54 @@ def make_inputs(rank: int, b=B_PER_GPU, t=T_FR, n=N_TOK, l=L_LAB):
     return em, em_len, asg_t, ctc_t, tgt_len, trans, n - 1
 
 
+def shard_inputs(lo: int, hi: int):
+    """Utterances [lo, hi) of the global synthetic batch (utterance u lives in
+    block u // 64 of make_inputs), so every rank generates only its shard."""
+    parts = []
+    for blk in range(lo // B_PER_GPU, (hi - 1) // B_PER_GPU + 1):
+        em, el, ta, tc, tl, trans, blank = make_inputs(blk)
+        a, z = max(lo - blk * B_PER_GPU, 0), min(hi - blk * B_PER_GPU, B_PER_GPU)
+        parts.append((em[a:z], el[a:z], ta[a:z], tc[a:z], tl[a:z]))
+    cat = [np.concatenate([p[k] for p in parts]) for k in range(5)]
+    return (*cat, trans, blank)
+
+
+def peaky_inputs(scale: float, b=B_PER_GPU, t=T_FR, n=N_TOK, l=L_LAB):
+    """The bench shape with log_softmax(scale N(0,1)) emissions (trained
+    acoustic models are peaky); targets and transitions as make_inputs(0)."""
+    em, el, ta, tc, tl, trans, blank = make_inputs(0, b, t, n, l)
+    rng = np.random.default_rng(SEED + 7)
+    x = scale * rng.standard_normal((b, t, n))
+    x -= x.max(axis=2, keepdims=True)
+    em = (x - np.log(np.exp(x).sum(axis=2, keepdims=True))).astype(np.float32)
+    return em, el, ta, tc, tl, trans, blank
+
+
 # ----------------------------------------------------------- CPU baseline --
+# The reference's own functions (asrkit.criterion, installed unmodified into
+# baseline/_ref) when present -- kind "reference" -- else the oracle port
+# (oracle/criterion_oracle.py, the same algorithm restated) -- kind "port".
+
+def _ref_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "asrkit"))
+
+
+def _cpu_impl():
+    if _ref_available():
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from asrkit import criterion as rc
+        return (lambda e, y, a: rc.asg_loss_grad(e, y, a),
+                lambda e, y, blank: rc.ctc_loss_grad(e, y, blank), "reference")
+    from oracle import criterion_oracle as orc
+    return orc.asg, orc.ctc, "port"
+
 
 def _cpu_worker(args):
-    from oracle import criterion_oracle as orc
+    asg, ctc, _ = _cpu_impl()
     e, ya, yc, a, blank = args
-    orc.asg(e, ya, a)
-    orc.ctc(e, yc, blank)
+    asg(e, ya, a)
+    ctc(e, yc, blank)
     return e.shape[0]
 
 
@@ -75,17 +123,39 @@ def _pool(cores):
     import multiprocessing as mpc
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
-    return cf.ProcessPoolExecutor(max_workers=cores, mp_context=mpc.get_context("fork"))
+    pool = cf.ProcessPoolExecutor(max_workers=cores, mp_context=mpc.get_context("fork"))
+    pool.submit(os.getpid).result()   # fork every worker now, before CUDA initialises
+    return pool
 
 
-def cpu_sample(pool, em, asg_t, ctc_t, trans, blank, n_utts):
-    """Oracle port (the reference algorithm, float64 numpy) over n_utts
-    utterances, one per task; returns frames/s (wall clock)."""
-    tasks = [(em[i % len(em)], asg_t[i % len(em)], ctc_t[i % len(em)], trans, blank)
-             for i in range(n_utts)]
+def _tasks(inp, n_utts):
+    em, _, asg_t, ctc_t, _, trans, blank = inp
+    return [(em[i % len(em)], asg_t[i % len(em)], ctc_t[i % len(em)], trans, blank)
+            for i in range(n_utts)]
+
+
+def cpu_rates(pool, cores, inp, steps, warmup):
+    """Frames/s of the CPU implementation on this host: the process pool
+    (one utterance per task, all cores: the strongest honest CPU baseline),
+    warmed and timed exactly like the reference arm; plus the single-core
+    rate and the reference trainer's as-shipped thread pool
+    (trainer.py:424-437, GIL-bound)."""
+    n_utts = max(16, min(cores, 64))
+    tasks = _tasks(inp, n_utts)
+    for _ in range(warmup):
+        sum(pool.map(_cpu_worker, tasks))
+    frames, t0 = 0, time.perf_counter()
+    for _ in range(steps):
+        frames += sum(pool.map(_cpu_worker, tasks))
+    proc_fps = frames / (time.perf_counter() - t0)
+    _cpu_worker(tasks[0])
     t0 = time.perf_counter()
-    frames = sum(pool.map(_cpu_worker, tasks))
-    return frames / (time.perf_counter() - t0)
+    single_fps = _cpu_worker(tasks[0]) / (time.perf_counter() - t0)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=cores) as tp:
+        t0 = time.perf_counter()
+        thread_fps = sum(tp.map(_cpu_worker, tasks[:cores])) / (time.perf_counter() - t0)
+    return proc_fps, single_fps, thread_fps, n_utts
 
 
 def cpu_cores():
@@ -124,7 +194,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -183,12 +253,34 @@ def algorithmic_work(n=N_TOK, l=L_LAB, ctc_targets=None):
 
 def _ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    --set full capture (profiles/), or None."""
+    --set full capture (profiles/traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f).get(kernel)
     except (OSError, ValueError):
         return None
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------- launcher --
+
+def _relaunch(args):
+    """--gpus N > 1 without torchrun: re-exec under torch.distributed.run,
+    one process per GPU (the driver launches torchrun itself)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------------- main --
@@ -199,11 +291,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling: this many utterances split over the ranks "
+                         "(default: weak scaling, 64 per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-sub", action="store_true", help="skip per-criterion sub-benchmarks")
+    ap.add_argument("--no-sub", action="store_true", help="skip the sub-benchmarks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -211,10 +308,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
-    # CPU baseline pool forked before CUDA initialises (rank 0, single GPU)
+    # CPU baseline pool forked before CUDA initialises (rank 0 at N=1 only)
+    cores = cpu_cores()
     pool = None
     if world == 1 and not args.no_cpu_baseline:
-        pool = _pool(cpu_cores())
+        pool = _pool(cores)
 
     import torch
     import torch.distributed as dist
@@ -224,10 +322,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_1812_07625_b200 import _native, criterion as C
-    from paper_1812_07625_b200.distributed import allreduce_grad_transitions
+    from paper_1812_07625_b200.distributed import NcclComm, shard_bounds
 
-    em, em_len, asg_t, ctc_t, tgt_len, trans, blank = make_inputs(rank)
+    strong = args.global_batch is not None
+    g_batch = args.global_batch if strong else world * B_PER_GPU
+    lo, hi = shard_bounds(g_batch, world, rank)
+    em, em_len, asg_t, ctc_t, tgt_len, trans, blank = shard_inputs(lo, hi)
     B, T, N = em.shape
+    comm = NcclComm() if world > 1 else None
     em_d = torch.from_numpy(em).to(dev)
     el_d = torch.from_numpy(em_len).to(dev)
     ta_d = torch.from_numpy(asg_t).to(dev)
@@ -253,17 +355,15 @@ def main():
     def both(em_, el_, ta_, tc_, tl_, outs=None):
         oa_, oc_ = outs if outs is not None else (out_a, out_c)
         # the two criteria run concurrently on two streams (chain CTAs of both
-        # are co-resident: maximum shared-memory carveout).  The split-phase
-        # schedule (all recursions, then all gradient phases; phase="chain" /
-        # "grad") measured slower: co-resident lattice warps contend for issue
-        # slots while the gradient kernels would otherwise fill idle SMs.
+        # are co-resident: maximum shared-memory carveout)
         side.wait_stream(main_s)
         with torch.cuda.stream(side):
             oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False, workspace=ws_c,
                                          out=oc_)
         oa = C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
                                      out=oa_)
-        allreduce_grad_transitions(oa.grad_transitions)
+        if comm is not None:      # the one exchange: sum of grad_A over ranks
+            comm.allreduce_grad_transitions(oa.grad_transitions)
         main_s.wait_stream(side)
         return oa, oc
 
@@ -292,11 +392,12 @@ def main():
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
-    frames_step = world * B * T
+    frames_step = g_batch * T
     value = frames_step * args.steps / (total_ms / 1e3)
 
     # ---- end to end through the public API: pinned host inputs -> device ->
-    # both criteria -> losses back to the host, every step
+    # both criteria -> losses back to the host, every step (and a variant that
+    # also returns both gradients to the host, as the reference API does)
     em_h = torch.from_numpy(em).pin_memory()
     ta_h = torch.from_numpy(asg_t).pin_memory()
     tc_h = torch.from_numpy(ctc_t).pin_memory()
@@ -304,24 +405,25 @@ def main():
     tl_h = torch.from_numpy(tgt_len).pin_memory()
     loss_a_h = torch.empty(B, dtype=torch.float64).pin_memory()
     loss_c_h = torch.empty(B, dtype=torch.float64).pin_memory()
+    ge_a_h = torch.empty((B, T, N), dtype=torch.float32).pin_memory()
+    ge_c_h = torch.empty((B, T, N), dtype=torch.float32).pin_memory()
+    ga_h = torch.empty((N, N), dtype=torch.float32).pin_memory()
     # double-buffered device inputs: a copy stream brings step i+1's inputs in
     # while step i computes (each step still copies its own inputs and reads
-    # its losses back; only the overlap is new)
+    # its results back; only the overlap is new)
     bufs = [dict(em=torch.empty_like(em_d), ta=torch.empty_like(ta_d), tc=torch.empty_like(tc_d),
                  el=torch.empty_like(el_d), tl=torch.empty_like(tl_d)) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
-    d2h_s = torch.cuda.Stream(device=dev)   # loss read-back off the compute stream
+    d2h_s = torch.cuda.Stream(device=dev)   # read-back off the compute stream
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
     read_back = [torch.cuda.Event() for _ in range(2)]
-    # outputs double-buffered like the inputs: step i+2 reuses step i's
-    # outputs only after step i's losses reached the host
     outs = [(out_a, out_c),
             (C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a),
              C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank, check=False,
                                      workspace=ws_c))]
 
-    def e2e_step(i):
+    def e2e_step(i, grads):
         bi = bufs[i & 1]
         with torch.cuda.stream(copy_s):
             if i >= 2:
@@ -337,48 +439,54 @@ def main():
             main_s.wait_event(read_back[i & 1])       # outputs free again
         oa, oc = both(bi["em"], bi["el"], bi["ta"], bi["tc"], bi["tl"], outs[i & 1])
         consumed[i & 1].record(main_s)
-        # the losses go back on their own stream, so the next step's kernels
-        # do not queue behind the copy
         with torch.cuda.stream(d2h_s):
             d2h_s.wait_event(consumed[i & 1])
             loss_a_h.copy_(oa.loss, non_blocking=True)
             loss_c_h.copy_(oc.loss, non_blocking=True)
+            if grads:
+                ge_a_h.copy_(oa.grad_emissions, non_blocking=True)
+                ge_c_h.copy_(oc.grad_emissions, non_blocking=True)
+                ga_h.copy_(oa.grad_transitions, non_blocking=True)
             read_back[i & 1].record(d2h_s)
 
-    for i in range(args.warmup):
-        e2e_step(i)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    # steps are queued back to back (the host enqueues step i+1 while the
-    # device runs step i); the clock starts before the first input copy and
-    # stops after the last loss reached the host
-    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    flush.zero_()
-    torch.cuda.synchronize(dev)
-    e_s.record(main_s)
-    copy_s.wait_stream(main_s)
-    for i in range(args.steps):
-        e2e_step(i)
-    main_s.wait_stream(d2h_s)                  # the last losses are on the host
-    e_e.record(main_s)
-    e_e.synchronize()
-    e2e_ms = e_s.elapsed_time(e_e)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = frames_step * args.steps / (float(e2e_t.item()) / 1e3)
+    def e2e_run(grads):
+        for i in range(args.warmup):
+            e2e_step(i, grads)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        # steps are queued back to back; the clock starts before the first
+        # input copy and stops after the last results reached the host
+        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        e_s.record(main_s)
+        copy_s.wait_stream(main_s)
+        for i in range(args.steps):
+            e2e_step(i, grads)
+        main_s.wait_stream(d2h_s)
+        e_e.record(main_s)
+        e_e.synchronize()
+        t = torch.tensor([e_s.elapsed_time(e_e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return frames_step * args.steps / (float(t.item()) / 1e3)
+
+    e2e_value = e2e_run(False)
+    e2e_grads_value = e2e_run(True)
     h2d = em.nbytes + asg_t.nbytes + ctc_t.nbytes + em_len.nbytes + tgt_len.nbytes
     d2h = 2 * B * 8
+    d2h_grads = d2h + 2 * em.nbytes + N * N * 4
 
     if world > 1:
         dist.barrier()
     if rank != 0:
+        comm.close()
         dist.destroy_process_group()
         return
 
     # ---- per-stage device times (traced calls) and the roofline of the
-    # dominant kernel; sub-benchmarks per criterion and Viterbi
+    # dominant kernel; sub-benchmarks per criterion, Viterbi and peaky inputs
     torch.cuda.synchronize(dev)
     ta_run = C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a,
                                      trace=True)
@@ -402,11 +510,7 @@ def main():
         "kernel_ms": dom_ms,
         "peak_source": "w2l_probe_peaks: MUFU ex2 throughput measured on this GPU",
     }
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            hbm_peak, hbm_src = float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
-    except (OSError, KeyError, ValueError):
-        hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    hbm_peak, hbm_src = _hbm_peak()
     step_s = total_ms / args.steps / 1e3
     step_bytes = (work["bytes_asg"] + work["bytes_ctc"]) * frames
     step_ops = (work["asg_chain"] + work["asg_grad"] + work["ctc_chain"] + work["ctc_grad"]) * frames
@@ -426,9 +530,9 @@ def main():
         "kernel_ms": dom_ms,
         "peak_source": hbm_src,
         "note": ("serial T-step recursion: latency-bound; the SFU-equivalent view is in "
-                 "roofline_sfu") if stage == "chain" else
+                 "roofline_sfu, the latency view in roofline_latency") if stage == "chain" else
                 ("posterior/gradient kernels: achieved counts only the algorithmic bytes "
-                 "(emissions in, gradient out); traffic adds the workspace rows they read"),
+                 "(emissions in, gradient out); traffic adds the workspace it reads"),
         "step": {
             "sfu_ops_per_step": step_ops,
             "sfu_achieved_gops": step_ops / step_s / 1e9,
@@ -439,11 +543,19 @@ def main():
             "hbm_frac": step_bytes / step_s / 1e9 / hbm_peak,
         },
     }
+    # latency roofline of the serial recursions: T dependent steps, each at
+    # least the measured one-warp step floor (fcc ~174 cycles,
+    # lattice ~30 cycles of recursion arithmetic), at the sampled SM clock
+    clk_sum = clk.summary()
+    mhz = clk_sum.get("sm_mhz") or 1965.0
+    chain_ms = {c: stages.get((c, "chain")) for c in ("asg", "ctc")}
+    floor_cycles = {"asg": 174, "ctc": 30}
+    roof_lat = {c: {"kernel_ms": chain_ms[c], "floor_cycles_per_step": floor_cycles[c],
+                    "floor_ms": T * floor_cycles[c] / (mhz * 1e3),
+                    "cycles_per_step": (chain_ms[c] * mhz * 1e3 / T) if chain_ms[c] else None,
+                    "frac": (T * floor_cycles[c] / (mhz * 1e3) / chain_ms[c]) if chain_ms[c] else None}
+                for c in ("asg", "ctc")}
 
-    # the HBM-bound gradient stages: their measured DRAM traffic per launch
-    # (committed ncu --set full capture, profiles/traffic.json) over the stage
-    # time measured here -- how close the workspace-row streaming runs to the
-    # HBM peak (the contract roofline above counts algorithmic bytes only)
     roof_dram = {}
     for crit_, stages_ in (("asg", ta_run.stage_ms), ("ctc", tc_run.stage_ms)):
         traffic = _ncu_traffic(f"{crit_}_grad")
@@ -457,6 +569,7 @@ def main():
 
     sub = {"asg_stage_ms": ta_run.stage_ms, "ctc_stage_ms": tc_run.stage_ms,
            "peaks": peaks, "fp32_guard_fallbacks": fallbacks}
+    roof_vit = None
     if not args.no_sub:
         def timeit(fn, reps=5):
             fn()
@@ -476,7 +589,6 @@ def main():
         ms_c = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
                                                       check=False, workspace=ws_c, out=out_c))
         ms_v = timeit(lambda: C.viterbi_batched(em_d, el_d, A_d, check=False))
-        # SURVEY f3 (evaluation: loss only) and f1 (CTC on logits, log_softmax fused)
         ms_al = timeit(lambda: C.asg_loss_grad_batched(em_d, el_d, ta_d, tl_d, A_d, check=False,
                                                        workspace=ws_a, out=out_a, loss_only=True))
         ms_cl = timeit(lambda: C.ctc_loss_grad_batched(em_d, el_d, tc_d, tl_d, blank,
@@ -490,70 +602,116 @@ def main():
                     "viterbi_frames_per_s": frames / (ms_v / 1e3), "viterbi_ms": ms_v,
                     "asg_loss_only_ms": ms_al, "ctc_loss_only_ms": ms_cl,
                     "ctc_logits_fused_ms": ms_cx})
+        # Viterbi against its own bound: 2N^2 + N float64 add/compare ops per
+        # frame over the measured DADD rate
+        vit_ops = (2 * N * N + N) * frames
+        roof_vit = {"kernel": "viterbi", "bound": "fp64", "unit": "Gop/s",
+                    "achieved": vit_ops / (ms_v / 1e3) / 1e9,
+                    "peak": peaks["dadd_per_s"] / 1e9,
+                    "frac": vit_ops / (ms_v / 1e3) / peaks["dadd_per_s"], "kernel_ms": ms_v,
+                    "peak_source": "w2l_probe_peaks: DADD throughput measured on this GPU"}
+        # peaky emissions (trained models): fp32-guard fallbacks and step time
+        peaky = {}
+        for scale in (2.0, 5.0, 10.0, 20.0):
+            pe = peaky_inputs(scale, b=B)
+            pem = torch.from_numpy(pe[0]).to(dev)
+            pa = C.asg_loss_grad_batched(pem, el_d, ta_d, tl_d, A_d, check=False,
+                                         workspace=ws_a, fallback=False)
+            pc = C.ctc_loss_grad_batched(pem, el_d, tc_d, tl_d, blank, check=False,
+                                         workspace=ws_c, fallback=False)
+            fa, fc = int((pa.status != 0).sum().item()), int((pc.status != 0).sum().item())
+            ms_pa = timeit(lambda: C.asg_loss_grad_batched(pem, el_d, ta_d, tl_d, A_d,
+                                                           check=False, workspace=ws_a),
+                           reps=2)
+            ms_pc = timeit(lambda: C.ctc_loss_grad_batched(pem, el_d, tc_d, tl_d, blank,
+                                                           check=False, workspace=ws_c),
+                           reps=2)
+            peaky[f"s={scale:g}"] = {"asg_fallbacks": fa, "ctc_fallbacks": fc,
+                                     "asg_ms": ms_pa, "ctc_ms": ms_pc}
+        sub["peaky_emissions"] = peaky
 
     cpu = None
     if pool is not None:
-        cores = cpu_cores()
-        n_utts = max(16, min(cores, 64))
+        inp = (em, em_len, asg_t, ctc_t, tgt_len, trans, blank)
         with pool:
-            list(pool.map(_cpu_worker, [(em[0][:8], asg_t[0][:4], ctc_t[0][:4], trans, blank)] * cores))
-            fps = cpu_sample(pool, em, asg_t, ctc_t, trans, blank, n_utts)
-        cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
+            proc_fps, single_fps, thread_fps, n_utts = cpu_rates(pool, cores, inp, 3, 2)
+        kind = "reference" if _ref_available() else "port"
+        cpu = {"value": proc_fps, "unit": "frames/s", "cores": cores, "kind": kind,
                "cpu": cpu_model(),
+               "single_core_frames_per_s": single_fps,
+               "thread_pool_frames_per_s": thread_fps,
                "sample": f"{n_utts} utterances (T={T}, N={N}, L={L_LAB}) ASG+CTC loss+grad, "
-                         f"oracle port (float64 numpy), one utterance per task, process pool "
-                         f"of {cores}"}
+                         + ("asrkit.criterion (the reference, baseline/_ref)" if kind == "reference"
+                            else "oracle port (float64 numpy)")
+                         + f", one utterance per task, process pool of {cores} (warmed); "
+                           "single core: 1 utterance; thread pool (trainer.py:424-437): "
+                           f"{cores} utterances on {cores} threads"}
 
-    # our kernels per step: ASG em_check, prep, chain, grad (fac + fcc CTAs in
-    # one launch), final, exact (fallback, early exit), reduce; CTC em_check,
-    # prep, chain, grad, final, exact
+    # our kernels per step: ASG em_check, prep, chain, grad, final, exact
+    # (fallback, early exit), reduce; CTC em_check, prep, chain, grad, final,
+    # exact (+ the NCCL all-reduce at N > 1)
     launches_per_step = 7 + 6
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic seeded: log_softmax(2*N(0,1)) emissions, N(0,1) transitions, "
                 "uniform targets",
         "config": {"workload": f"ASG+CTC loss+grad, B={B}/GPU T={T} N={N} L={L_LAB} "
-                               "(C3 shape per GPU; C5 B=512 at 8 GPUs)",
-                   "global_batch": world * B, "frames_per_step": frames_step,
+                               + ("(strong scaling)" if strong else
+                                  "(C3 shape per GPU; C5 B=512 at 8 GPUs)"),
+                   "global_batch": g_batch, "frames_per_step": frames_step,
                    "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between steps"},
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "boundary": "pinned host inputs in, per-utterance losses out (on-GPU training "
+                            "keeps the gradients on the device)"},
+        "e2e_grads_to_host": {"value": e2e_grads_value, "unit": "frames/s",
+                              "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_grads,
+                              "boundary": "as e2e, plus both emission gradients and grad_A "
+                                          "back to pinned host memory (the reference API's "
+                                          "return values)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
         "roofline_sfu": roof_sfu,
+        "roofline_latency": roof_lat,
+        "roofline_viterbi": roof_vit,
         "roofline_dram_grad": roof_dram,
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clk_sum,
         "sub": sub,
         "library": lib.w2l_version().decode(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
+        comm.close()
         dist.destroy_process_group()
 
 
 def run_reference(args, world, rank):
-    """The reference algorithm (oracle port, float64 numpy, one utterance per
-    task on all host cores) on this arm's config and metric; rank 0 only."""
+    """The reference's CPU implementation of the path on this host's cores:
+    asrkit.criterion's asg_loss_grad + ctc_loss_grad (installed unmodified in
+    baseline/_ref) when present, else the oracle port; one utterance per task
+    in a process pool over every core; rank 0 only."""
     if rank != 0:
         return
-    em, em_len, asg_t, ctc_t, tgt_len, trans, blank = make_inputs(0)
+    inp = make_inputs(0)
     cores = cpu_cores()
-    n_utts = max(16, min(cores, 64))
-    total = 0.0
+    kind = "reference" if _ref_available() else "port"
     with _pool(cores) as pool:
+        n_utts = max(16, min(cores, 64))
+        tasks = _tasks(inp, n_utts)
         for _ in range(args.warmup):
-            cpu_sample(pool, em, asg_t, ctc_t, trans, blank, cores)
+            sum(pool.map(_cpu_worker, tasks))
         frames = 0
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            tasks = [(em[i % len(em)], asg_t[i % len(em)], ctc_t[i % len(em)], trans, blank)
-                     for i in range(n_utts)]
             frames += sum(pool.map(_cpu_worker, tasks))
         total = time.perf_counter() - t0
     value = frames / total
+    impl = ("asrkit.criterion.asg_loss_grad + ctc_loss_grad (the reference, baseline/_ref)"
+            if kind == "reference" else "oracle port (float64 numpy)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -563,8 +721,8 @@ def run_reference(args, world, rank):
         "config": {"workload": f"ASG+CTC loss+grad, T={T_FR} N={N_TOK} L={L_LAB}; each step a "
                                f"{n_utts}-utterance sample of the B={B_PER_GPU} shard",
                    "global_batch": n_utts, "parallelism": f"process pool x{cores}"},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
-                         "cpu": cpu_model(),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": kind,
+                         "cpu": cpu_model(), "impl": impl,
                          "sample": f"{n_utts} utterances per step, one per task"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

@@ -75,6 +75,10 @@ enum {
  * is that of log_softmax(x) (autodiff.py:394-411) and grad_em is the gradient
  * with respect to x; the |row logsumexp| <= 1e-2 contract does not apply. */
 #define W2L_FLAG_CTC_LOGITS 16u
+/* Skip the fp32 fast path: every valid utterance is computed by the float64
+ * log-domain kernel (the guard's fallback path, forced; tests and
+ * diagnostics). */
+#define W2L_FLAG_FORCE_EXACT 32u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */
@@ -143,6 +147,21 @@ W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const doubl
 W2L_API int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_sum, int N,
                                      int batch_size, float lr, float momentum,
                                      w2l_stream_t stream);
+
+/* ------------------------------------------------------- multi-GPU --
+ * The data-parallel exchange (trainer.py:433-447): each rank runs
+ * the batched criterion on its contiguous shard, then ONE sum all-reduce of
+ * the N x N transition gradient over NCCL (NVLink/NVSwitch), enqueued on the
+ * same stream right after w2l_asg_loss_grad.  The /B stays with the caller.
+ * NCCL is loaded at run time (libnccl.so.2); w2l_comm_available() reports
+ * whether it could be.  Communicators: rank 0 creates a 128-byte unique id,
+ * the host side distributes it (any channel), every rank calls
+ * w2l_comm_init with its CUDA device current.  Failures: W2L_ERR_COMM. */
+W2L_API int w2l_comm_available(void);
+W2L_API int w2l_comm_unique_id(void *id_out /* 128 bytes */);
+W2L_API int w2l_comm_init(const void *id, int world, int rank, void **comm);
+W2L_API int w2l_comm_destroy(void *comm);
+W2L_API int w2l_allreduce_grad_A(float *grad_A, int N, void *comm, w2l_stream_t stream);
 
 /* ------------------------------------------------------------- tracing --
  * Same computation as w2l_asg_loss_grad / w2l_ctc_loss_grad, with a CUDA

@@ -11,6 +11,5 @@ from .criterion import (AsgCriterion, BatchLossOutput, CtcCriterion, LossOutput,
                         viterbi, viterbi_batched)
 from .errors import (AsrkitError, ContractError, InfeasibleTargetError, NumericError,
                      TargetError, TokenError)
-from .tokens import TokenTable, load_tokens
 
 __version__ = "0.1.0"

@@ -26,7 +26,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompil
 # debug-only extra flags (e.g. -DW2L_PROF for the chain cycle profile)
 FLAGS += os.environ.get("W2L_EXTRA_NVCC_FLAGS", "").split()
 SOURCES = ["validate.cu", "viterbi.cu", "exact.cu", "asg_fast.cu", "ctc_fast.cu", "probe.cu",
-           "capi.cu"]
+           "comm.cu", "capi.cu"]
 
 
 def nvcc() -> str:
@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with cf.ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
             list(ex.map(lambda s: _compile(s, verbose), todo))
     if force or todo or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs]
+        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs, "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

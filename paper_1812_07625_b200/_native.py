@@ -55,6 +55,11 @@ SIGNATURES = {
     "w2l_probe_peaks": (c_i, [c_d_p, c_d_p, c_d_p]),
     "w2l_transitions_sgd_step": (c_i, [c_p, c_p, c_p, c_i, c_i, ctypes.c_float, ctypes.c_float,
                                        c_p]),
+    "w2l_comm_available": (c_i, []),
+    "w2l_comm_unique_id": (c_i, [c_p]),
+    "w2l_comm_init": (c_i, [c_p, c_i, c_i, ctypes.POINTER(c_p)]),
+    "w2l_comm_destroy": (c_i, [c_p]),
+    "w2l_allreduce_grad_A": (c_i, [c_p, c_i, c_p, c_p]),
 }
 
 # C-ABI status codes (include/w2l_criterion.h)
@@ -65,6 +70,7 @@ FLAG_PHASE_CHAIN = 2
 FLAG_PHASE_GRAD = 4
 FLAG_LOSS_ONLY = 8
 FLAG_CTC_LOGITS = 16
+FLAG_FORCE_EXACT = 32
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511
@@ -81,7 +87,7 @@ def header_symbols() -> list[str]:
     """Function names declared in include/w2l_criterion.h."""
     with open(HEADER) as f:
         text = f.read()
-    return sorted(set(re.findall(r"\b(w2l_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(w2l_[A-Za-z0-9_]+)\s*\(", text)))
 
 
 def lib() -> ctypes.CDLL:

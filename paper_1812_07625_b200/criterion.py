@@ -35,13 +35,17 @@ import torch
 from . import _native as nat
 from .errors import (ContractError, DeviceError, InfeasibleTargetError, NumericError,
                      TargetError, raise_for_status)
-from .tokens import REPETITION_SYMBOL, TokenTable
+
+# the ASG repetition token's symbol (lexicon.py:51-54); token tables are duck
+# typed: the criterion path needs only len(table), table.rep_id and
+# table.symbol(id), which the reference's TokenTable provides
+REPETITION_SYMBOL = "<2>"
 
 __all__ = [
     "LossOutput", "BatchLossOutput", "validate_target", "ctc_loss_grad", "asg_loss_grad",
     "viterbi", "collapse_path", "CtcCriterion", "AsgCriterion", "make_criterion",
     "asg_loss_grad_batched", "ctc_loss_grad_batched", "viterbi_batched", "asg_loss",
-    "ctc_loss",
+    "ctc_loss", "check_status",
 ]
 
 
@@ -137,7 +141,7 @@ def _target_ids(target) -> np.ndarray:
     return y
 
 
-def validate_target(tokens, criterion_kind: str, table: TokenTable):
+def validate_target(tokens, criterion_kind: str, table):
     """Canonicalise a target for the criterion (criterion.py:51-79): CTC passes
     through; ASG replaces the second of each consecutive duplicate with the
     repetition token, left to right ("a a a" -> "a <2> a")."""
@@ -353,8 +357,11 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
     return em, el, tg, tl
 
 
-def _flags(fallback: bool, phase: str, loss_only: bool = False, logits: bool = False) -> int:
+def _flags(fallback: bool, phase: str, loss_only: bool = False, logits: bool = False,
+           force_exact: bool = False) -> int:
     f = 0 if fallback else nat.FLAG_NO_FALLBACK
+    if force_exact:
+        f |= nat.FLAG_FORCE_EXACT
     if loss_only:
         f |= nat.FLAG_LOSS_ONLY
     if logits:
@@ -381,7 +388,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
                           per_utterance_grad_transitions=False, workspace=None,
                           out: Optional[BatchLossOutput] = None,
                           fallback: bool = True, trace: bool = False,
-                          phase: str = "all", loss_only: bool = False) -> BatchLossOutput:
+                          phase: str = "all", loss_only: bool = False,
+                          force_exact: bool = False) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -395,9 +403,10 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     phase="chain" | "grad" splits the call (W2L_FLAG_PHASE_*): "chain" runs
     the recursions into the workspace, a later "grad" call with the same
     inputs, workspace and out on the same stream order finishes it.
-    loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the forward
-    recursion and the loss only: grad_emissions / grad_transitions are not
-    computed."""
+    loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the recursions
+    and the loss only: grad_emissions / grad_transitions are not computed.
+    force_exact=True (W2L_FLAG_FORCE_EXACT) computes every utterance with
+    the float64 log-domain kernel (the guard's fallback path)."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -419,7 +428,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
-            _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase, loss_only), _stream())
+            _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase, loss_only,
+                                                       force_exact=force_exact), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_asg_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -436,7 +446,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
                           workspace=None, out: Optional[BatchLossOutput] = None,
                           fallback: bool = True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
-                          logits: bool = False) -> BatchLossOutput:
+                          logits: bool = False, force_exact: bool = False) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
     log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase and
     loss_only: as for asg_loss_grad_batched.  logits=True
@@ -459,7 +469,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
-            _flags(fallback, phase, loss_only, logits), _stream())
+            _flags(fallback, phase, loss_only, logits, force_exact), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -499,44 +509,75 @@ def viterbi_batched(emissions, em_len, transitions=None, *, check=True, workspac
 
 # ------------------------------------------------------------- autograd --
 
+# The autograd functions do not synchronise with the host (check=False): an
+# utterance whose inputs fail validation gets a NaN loss and a zero gradient,
+# and its status code stays readable from the returned loss tensor's
+# ``w2l_status`` attribute (raise it when convenient with check_status()).
+
+def _mask_failed(loss: torch.Tensor, status: torch.Tensor) -> torch.Tensor:
+    return torch.where(status == 0, loss, torch.full_like(loss, float("nan")))
+
+
+def check_status(loss: torch.Tensor, what: str = "criterion") -> None:
+    """Raise the reference exception for the first failing utterance of a
+    loss returned by asg_loss / ctc_loss (synchronises with the device)."""
+    st = getattr(loss, "w2l_status", None)
+    if st is not None:
+        _raise_batch(st, what)
+
+
 class _AsgLossFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, emissions, transitions, em_len, targets, tgt_len):
+    def forward(ctx, emissions, transitions, em_len, targets, tgt_len, check, holder):
         out = asg_loss_grad_batched(emissions.detach(), em_len, targets, tgt_len,
-                                    transitions.detach(), per_utterance_grad_transitions=True)
+                                    transitions.detach(), per_utterance_grad_transitions=True,
+                                    check=check)
         ctx.save_for_backward(out.grad_emissions, out.grad_transitions_per_utt)
-        return out.loss.to(emissions.dtype)
+        ctx.status = holder["status"] = out.status
+        return _mask_failed(out.loss, out.status).to(emissions.dtype)
 
     @staticmethod
     def backward(ctx, g):
         ge, ga = ctx.saved_tensors
-        g = g.to(torch.float32)
-        return (ge * g[:, None, None], torch.einsum("b,bij->ij", g, ga), None, None, None)
+        g = torch.where(ctx.status == 0, g, torch.zeros_like(g)).to(torch.float32)
+        return (ge * g[:, None, None], torch.einsum("b,bij->ij", g, ga), None, None, None, None,
+                None)
 
 
 class _CtcLossFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, logp, em_len, targets, tgt_len, blank_id, logits=False):
+    def forward(ctx, logp, em_len, targets, tgt_len, blank_id, logits, check, holder):
         out = ctc_loss_grad_batched(logp.detach(), em_len, targets, tgt_len, blank_id,
-                                    logits=logits)
+                                    logits=logits, check=check)
         ctx.save_for_backward(out.grad_emissions)
-        return out.loss.to(logp.dtype)
+        ctx.status = holder["status"] = out.status
+        return _mask_failed(out.loss, out.status).to(logp.dtype)
 
     @staticmethod
     def backward(ctx, g):
         (ge,) = ctx.saved_tensors
-        return (ge * g.to(torch.float32)[:, None, None], None, None, None, None, None)
+        g = torch.where(ctx.status == 0, g, torch.zeros_like(g)).to(torch.float32)
+        return (ge * g[:, None, None], None, None, None, None, None, None, None)
 
 
-def asg_loss(emissions, transitions, em_len, targets, tgt_len) -> torch.Tensor:
-    """Differentiable per-utterance ASG losses [B] (PyTorch training)."""
-    return _AsgLossFn.apply(emissions, transitions, em_len, targets, tgt_len)
+def asg_loss(emissions, transitions, em_len, targets, tgt_len, check: bool = False) -> torch.Tensor:
+    """Differentiable per-utterance ASG losses [B] (PyTorch training).  No
+    host synchronisation unless check=True (see check_status)."""
+    holder: dict = {}
+    loss = _AsgLossFn.apply(emissions, transitions, em_len, targets, tgt_len, check, holder)
+    loss.w2l_status = holder["status"]
+    return loss
 
 
-def ctc_loss(logp, em_len, targets, tgt_len, blank_id: int, logits: bool = False) -> torch.Tensor:
+def ctc_loss(logp, em_len, targets, tgt_len, blank_id: int, logits: bool = False,
+             check: bool = False) -> torch.Tensor:
     """Differentiable per-utterance CTC losses [B] on log-probabilities, or on
-    unnormalised logits with log_softmax fused in (logits=True)."""
-    return _CtcLossFn.apply(logp, em_len, targets, tgt_len, blank_id, logits)
+    unnormalised logits with log_softmax fused in (logits=True).  No host
+    synchronisation unless check=True (see check_status)."""
+    holder: dict = {}
+    loss = _CtcLossFn.apply(logp, em_len, targets, tgt_len, blank_id, logits, check, holder)
+    loss.w2l_status = holder["status"]
+    return loss
 
 
 # ------------------------------------------------------ trainer adapters --
@@ -546,7 +587,7 @@ class CtcCriterion:
 
     kind = "ctc"
 
-    def __init__(self, table: TokenTable):
+    def __init__(self, table):
         self.table = table
         self.blank_id = len(table)
         self.n_outputs = len(table) + 1
@@ -567,21 +608,94 @@ class CtcCriterion:
         return collapse_path(path, "ctc", blank_id=self.blank_id)
 
 
+class _HostTensor:
+    """Read-only float32 host view with the reference Tensor's surface
+    (autodiff.py:20-45: ``.data``, ``.shape``, ``.item()``)."""
+
+    __slots__ = ("_data",)
+
+    def __init__(self, arr):
+        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        arr.setflags(write=False)
+        self._data = arr
+
+    @property
+    def data(self) -> np.ndarray:
+        return self._data
+
+    @property
+    def shape(self) -> tuple:
+        return self._data.shape
+
+    def item(self) -> float:
+        return float(self._data.item())
+
+
+class TransitionsVariable:
+    """The reference Variable protocol (autodiff.py:75-116) over the device
+    transition parameter, so reference-side code that uses
+    ``criterion.params()`` works unchanged: ``.value`` reads the parameter
+    (a host snapshot) and assigning it writes the parameter (the optimizer's
+    ``p.value = ...``, autodiff.py:433); ``accumulate_grad`` / ``grad`` /
+    ``zero_grad`` keep a host gradient like the reference trainer expects
+    (trainer.py:442-449)."""
+
+    def __init__(self, param: torch.Tensor):
+        self._param = param
+        self._grad = None
+        self.requires_grad = True
+        self.node = None
+
+    @property
+    def value(self) -> _HostTensor:
+        return _HostTensor(self._param.detach().cpu().numpy())
+
+    @value.setter
+    def value(self, v) -> None:
+        data = np.asarray(getattr(v, "data", v), dtype=np.float32)
+        if data.shape != tuple(self._param.shape):
+            raise ContractError(f"transitions must be {tuple(self._param.shape)}, got {data.shape}")
+        with torch.no_grad():
+            self._param.copy_(torch.from_numpy(np.ascontiguousarray(data)))
+
+    @property
+    def shape(self) -> tuple:
+        return tuple(self._param.shape)
+
+    @property
+    def grad(self) -> _HostTensor:
+        return _HostTensor(np.zeros(self.shape, np.float32) if self._grad is None else self._grad)
+
+    def zero_grad(self) -> None:
+        self._grad = None
+
+    def accumulate_grad(self, contribution) -> None:
+        c = np.asarray(contribution, dtype=np.float32)
+        if c.shape != self.shape:
+            raise ContractError(f"gradient shape {c.shape} != value shape {self.shape}")
+        self._grad = c.copy() if self._grad is None else self._grad + c
+
+    def item(self) -> float:
+        return self.value.item()
+
+
 class AsgCriterion:
     """ASG with a learnable N x N transition matrix (criterion.py:342-369).
 
     ``transitions`` is a torch Parameter (zeros, as in the reference) living on
-    the current CUDA device; ``params()`` keeps the reference key."""
+    the current CUDA device; ``params()`` keeps the reference key and returns
+    a Variable-protocol view of it (``.value``, ``.grad``, ...)."""
 
     kind = "asg"
 
-    def __init__(self, table: TokenTable):
+    def __init__(self, table):
         self.table = table
         self.n_outputs = len(table)
         dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
             else torch.device("cpu")
         self.transitions = torch.nn.Parameter(
             torch.zeros((self.n_outputs, self.n_outputs), dtype=torch.float32, device=dev))
+        self._var = TransitionsVariable(self.transitions)
 
     def prepare_target(self, token_ids):
         return validate_target(token_ids, "asg", self.table)
@@ -590,7 +704,7 @@ class AsgCriterion:
         return asg_loss_grad(emissions, target, self.transitions.detach())
 
     def params(self) -> dict:
-        return {"criterion.transitions": self.transitions}
+        return {"criterion.transitions": self._var}
 
     def viterbi_path(self, emissions):
         return viterbi(emissions, self.transitions.detach())[0]
@@ -599,7 +713,7 @@ class AsgCriterion:
         return collapse_path(path, "asg", rep_id=self.table.rep_id)
 
 
-def make_criterion(kind: str, table: TokenTable):
+def make_criterion(kind: str, table):
     """criterion.py:372-377."""
     if kind == "ctc":
         return CtcCriterion(table)

@@ -272,6 +272,7 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
   if (FWD) {
     z = warp_sum(lane < N ? f.v : 0.f);
   } else {
+    wait_ge(&sm.prod, T);   // frame 0's Et (the last step only waited for T - 1)
     const float e0 = sm.ering[ring_slot(false, T - 1)][lane];   // frame 0
     z = warp_sum(e0 * f.v);
   }
@@ -282,12 +283,14 @@ template <bool FWD>
 __device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, int W,
                                                const float *em, int T, int L,
                                                const int64_t *y, const float *trans, Dims d,
-                                               const AsgFastWs &w, int b) {
+                                               const AsgFastWs &w, int b, int32_t *status) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float amax = trans_max(trans, d.N);
   const int weff = lat_warps(L);
   if (warp == 0) {
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W, 0};
+    // the fcc uses every token
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W, 0,
+               d.N >= 32 ? 0xffffffffu : (1u << d.N) - 1u};
     producer_run(sm, pc, lane, nullptr);
   } else if (warp == 1) {
     FccCtx fc;
@@ -318,7 +321,10 @@ __device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, 
     lattice_run<kFac, FWD>(sm, c, f);
   }
   __syncthreads();
-  if (threadIdx.x == 0) w.scal[b * 4 + (FWD ? 2 : 3)] = lattice_total(sm, weff);
+  if (threadIdx.x == 0) {
+    w.scal[b * 4 + (FWD ? 2 : 3)] = lattice_total(sm, weff);
+    if (sm.flush) status[b] = kNeedsExact;
+  }
 }
 
 // grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
-                     const int32_t *__restrict__ status) {
+                     int32_t *__restrict__ status) {
   extern __shared__ __align__(128) unsigned char dsm[];
   const int W = w.W;
   ChainSm &sm = *reinterpret_cast<ChainSm *>(
@@ -335,15 +341,15 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
   if (status[b] != W2L_OK) return;
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(L);
-  if (threadIdx.x == 0) sm.prod = 0;
+  if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0;
   // counters: 0 = fcc, 1 + w = lattice warp w (absent warps are done)
   if (threadIdx.x < kCounters) sm.cons[threadIdx.x] = threadIdx.x <= weff ? 0 : kDone;
   __syncthreads();
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (blockIdx.y == 0)
-    asg_chain_body<true>(sm, dsm, W, em, T, L, y, trans, d, w, b);
+    asg_chain_body<true>(sm, dsm, W, em, T, L, y, trans, d, w, b, status);
   else
-    asg_chain_body<false>(sm, dsm, W, em, T, L, y, trans, d, w, b);
+    asg_chain_body<false>(sm, dsm, W, em, T, L, y, trans, d, w, b, status);
 }
 
 size_t asg_chain_smem(int W) {
@@ -822,12 +828,19 @@ __global__ void __launch_bounds__(1024)
 }
 
 // loss only: fcc minus fac forward totals; non-finite -> float64
-__global__ void asg_loss_only_kernel(Dims d, AsgFastWs w, double *loss, int32_t *status) {
+// Both directions ran: their totals must agree (the per-frame guard of the
+// gradient path needs the posteriors, which loss-only mode does not form).
+__global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, AsgFastWs w,
+                                     double *loss, int32_t *status) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B || status[b] != W2L_OK) return;
-  const double zF = w.scal[b * 4 + 0], zC = w.scal[b * 4 + 2];
+  const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
+  const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
+  const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));
   loss[b] = zF - zC;                                         // criterion.py:244
-  if (!isfinite(zF - zC)) status[b] = kNeedsExact;
+  if (!(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb)) ||
+      !(fabs(zF - zFb) <= tol && fabs(zC - zCb) <= tol))
+    status[b] = kNeedsExact;
 }
 
 // One launch for both gradient kernels; they are independent, so their CTAs
@@ -923,15 +936,15 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
     err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
-    // loss only: the forward CTA alone (blockIdx.y == 0)
-    asg_chain_kernel<<<dim3(d.B, (phases & 4u) ? 1 : 2), 32 * (2 + w.W), smem, s>>>(
+    // (loss only runs both directions too: their totals are its guard)
+    asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(
         em, em_len, tgt, tgt_len, trans, d, w, status);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
   if (phases & 4u) {
-    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(d, w, loss, status);
+    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
     return cudaGetLastError();
   }
   if (!(phases & 2u)) return cudaSuccess;
@@ -971,11 +984,11 @@ __global__ void reduce_grad_trans_kernel(const float *ga_utt, const int32_t *sta
 
 // SGD with classical momentum on the transitions (autodiff.py:429-433) after
 // the /B of trainer.py:447; float32 arithmetic without contraction, as numpy
-__global__ void transitions_sgd_kernel(float *w, float *v, const float *gsum, int nn, double inv_b,
+__global__ void transitions_sgd_kernel(float *w, float *v, const float *gsum, int nn, double batch,
                                        float lr, float momentum) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= nn) return;
-  const float g = (float)((double)gsum[p] * inv_b);
+  const float g = (float)((double)gsum[p] / batch);   // (total / batch.size).astype(f32)
   const float vv = __fadd_rn(__fmul_rn(v[p], momentum), g);
   v[p] = vv;
   w[p] = __fsub_rn(w[p], __fmul_rn(lr, vv));
@@ -984,7 +997,7 @@ __global__ void transitions_sgd_kernel(float *w, float *v, const float *gsum, in
 cudaError_t launch_transitions_sgd(float *w, float *v, const float *gsum, int N, int batch,
                                    float lr, float momentum, cudaStream_t s) {
   const int nn = N * N;
-  transitions_sgd_kernel<<<(nn + 255) / 256, 256, 0, s>>>(w, v, gsum, nn, 1.0 / batch, lr,
+  transitions_sgd_kernel<<<(nn + 255) / 256, 256, 0, s>>>(w, v, gsum, nn, (double)batch, lr,
                                                           momentum);
   return cudaGetLastError();
 }

@@ -11,7 +11,9 @@ using namespace w2l;
 
 namespace {
 
-constexpr int kMaxExactSlotsFallback = 8;
+// float64 fallback: one CTA per flagged utterance up to this many (each slot
+// holds one utterance's float64 alpha/beta rows)
+constexpr int kMaxExactSlotsFallback = 64;
 constexpr int kMaxExactSlotsF64 = 32;
 
 thread_local cudaError_t g_last_cuda = cudaSuccess;  // per calling thread, like cudaGetLastError
@@ -49,7 +51,7 @@ int asg_slots_f64(int B) { return B < kMaxExactSlotsF64 ? B : kMaxExactSlotsF64;
 
 extern "C" {
 
-const char *w2l_version(void) { return "w2l-criterion sm_100a r1 (scaled-linear fp32 + f64 exact)"; }
+const char *w2l_version(void) { return "w2l-criterion sm_100a r2 (scaled-linear fp32 + f64 exact)"; }
 
 const char *w2l_stage_name(int kind, int i) {
   static const char *asg[] = {"validate", "chain", "grad", "final", "exact_fallback", "reduce"};
@@ -133,12 +135,19 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
                    int32_t *status, void *ws, size_t ws_bytes, unsigned flags,
                    cudaStream_t s, Tracer *tr) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
-  if (B == 0) return W2L_OK;
+  if (B == 0) {
+    // an empty shard contributes a zero transition gradient (trainer.py:433
+    // skips empty shards), so a following all-reduce sums well-defined data
+    if (grad_trans && !(flags & W2L_FLAG_PHASE_CHAIN))
+      return from_cuda(cudaMemsetAsync(grad_trans, 0, sizeof(float) * N * N, s));
+    return W2L_OK;
+  }
   if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
       !status || !ws)
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_asg_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
   const bool fallback = !(flags & W2L_FLAG_NO_FALLBACK);
+  const bool force = flags & W2L_FLAG_FORCE_EXACT;
   Dims d{B, Tmax, N, Lmax};
   AsgFastWs w;
   float *ga_ws;
@@ -149,9 +158,22 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
   trace(tr, s);
   int rc = W2L_OK;
+  if (force) {
+    // every valid utterance through the float64 kernel; the outputs of
+    // utterances failing validation are zero
+    rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
+                                              w.tok_start, status, s, kPrepForceExact));
+    if (!rc) rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+    if (!rc) rc = from_cuda(cudaMemsetAsync(ga, 0, sizeof(float) * (size_t)B * N * N, s));
+    if (!rc)
+      rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
+                                             slots, loss, grad_em, ga, status, s));
+    if (!rc && !loss_only) rc = from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
+    return rc;
+  }
   if (phases & 1u) {
     rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
-                                              w.tok_start, status, s));
+                                              w.tok_start, status, s, kPrepFast));
     if (rc) return rc;
   }
   trace(tr, s);  // validate
@@ -231,12 +253,14 @@ int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t
                           float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
                           w2l_stream_t stream) {
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
-  if (B == 0) return W2L_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0)
+    return grad_trans ? from_cuda(cudaMemsetAsync(grad_trans, 0, sizeof(float) * N * N, s))
+                      : W2L_OK;
   if (!em || !em_len || !tgt || !tgt_len || !trans || !loss || !grad_em || !grad_trans ||
       !status || !ws)
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_asg_workspace_bytes_f64(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
-  cudaStream_t s = (cudaStream_t)stream;
   Dims d{B, Tmax, N, Lmax};
   Carver c{(char *)ws};
   float *ga_ws = (float *)c.take((size_t)B * N * N * sizeof(float));
@@ -294,11 +318,23 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
   trace(tr, s);
   int rc = W2L_OK;
+  if (flags & W2L_FLAG_FORCE_EXACT) {
+    rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
+                                              w.perm, w.tok_start, status, s, !logits,
+                                              kPrepForceExact));
+    if (!rc) rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+    if (!rc)
+      rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
+                                             asg_slots(B), slots, loss, grad_em, status, s,
+                                             logits));
+    return rc;
+  }
   if (phases & 1u) {
     // logits: the |row logsumexp| <= 1e-2 contract (criterion.py:96-101) does
     // not apply to unnormalised inputs
     rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
-                                              w.perm, w.tok_start, status, s, !logits));
+                                              w.perm, w.tok_start, status, s, !logits,
+                                              kPrepFast));
     if (rc) return rc;
   }
   trace(tr, s);  // validate

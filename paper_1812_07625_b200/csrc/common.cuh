@@ -12,6 +12,13 @@ namespace w2l {
 // Internal per-utterance status: the fp32 guard asks for the float64 kernel.
 constexpr int kNeedsExact = 100;
 
+// exp(x) of an fp32 weight flushes to zero below about -87.3 nats; the fast
+// path sends any input whose weights (emissions relative to their frame
+// maximum, transitions relative to their maximum) fall below -kFlushNats to
+// the float64 kernel, since a flush applied identically to both directions
+// would be invisible to the forward/backward consistency guard
+constexpr float kFlushNats = 80.f;
+
 constexpr int kWarp = 32;
 constexpr int kChunk = 32;            // frames per staged emission chunk
 constexpr int kNegExp = -(1 << 24);   // exponent of an all-zero lane block

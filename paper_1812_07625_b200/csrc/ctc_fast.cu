@@ -27,12 +27,13 @@ template <bool FWD>
 __device__ __forceinline__ void ctc_chain_body(ChainSm &sm, unsigned char *dsm, int W,
                                                const float *em, int T, int L,
                                                const int64_t *y, int blank, Dims d,
-                                               const CtcFastWs &w, int b) {
+                                               const CtcFastWs &w, int b, unsigned tokmask,
+                                               int32_t *status) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = 2 * L + 1;
   const int weff = lat_warps(S);
   if (warp == 0) {
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, W, w.logits};
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, W, w.logits, tokmask};
     producer_run(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
   } else if (warp - 1 < weff) {
     LatCtx c;
@@ -52,14 +53,17 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm &sm, unsigned char *dsm, 
     lattice_run<kCtc, FWD>(sm, c, f);
   }
   __syncthreads();
-  if (threadIdx.x == 0) w.scal[b * 4 + (FWD ? 0 : 1)] = lattice_total(sm, weff);
+  if (threadIdx.x == 0) {
+    w.scal[b * 4 + (FWD ? 0 : 1)] = lattice_total(sm, weff);
+    if (sm.flush) status[b] = kNeedsExact;
+  }
 }
 
 // grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
 __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
-                     int blank, Dims d, CtcFastWs w, const int32_t *__restrict__ status) {
+                     int blank, Dims d, CtcFastWs w, int32_t *__restrict__ status) {
   extern __shared__ __align__(128) unsigned char dsm[];
   const int W = w.W;
   ChainSm &sm = *reinterpret_cast<ChainSm *>(dsm);
@@ -67,14 +71,18 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
   if (status[b] != W2L_OK) return;
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(2 * L + 1);
-  if (threadIdx.x == 0) sm.prod = 0;
+  __shared__ unsigned s_mask;
+  if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0, s_mask = 1u << blank;
   if (threadIdx.x < kCounters) sm.cons[threadIdx.x] = threadIdx.x < weff ? 0 : kDone;
   __syncthreads();
   const int64_t *y = tgt + (size_t)b * d.Lmax;
+  // tokens on the lattice: the blank and the target's labels
+  for (int l = threadIdx.x; l < L; l += blockDim.x) atomicOr(&s_mask, 1u << (int)y[l]);
+  __syncthreads();
   if (blockIdx.y == 0)
-    ctc_chain_body<true>(sm, dsm, W, em, T, L, y, blank, d, w, b);
+    ctc_chain_body<true>(sm, dsm, W, em, T, L, y, blank, d, w, b, s_mask, status);
   else
-    ctc_chain_body<false>(sm, dsm, W, em, T, L, y, blank, d, w, b);
+    ctc_chain_body<false>(sm, dsm, W, em, T, L, y, blank, d, w, b, s_mask, status);
 }
 
 size_t ctc_chain_smem(int W) { (void)W; return sizeof(ChainSm); }
@@ -218,13 +226,16 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
   }
 }
 
-// loss only: forward total and shifts; non-finite -> float64
-__global__ void ctc_loss_only_kernel(Dims d, CtcFastWs w, double *loss, int32_t *status) {
+// loss only: both directions ran, their totals must agree
+__global__ void ctc_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
+                                     double *loss, int32_t *status) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B || status[b] != W2L_OK) return;
-  const double zA = w.scal[b * 4 + 0], shifts = w.scal[b * 4 + 2];
+  const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
+  const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));
   loss[b] = -(zA + shifts);                                  // criterion.py:162
-  if (!isfinite(zA + shifts)) status[b] = kNeedsExact;
+  if (!(isfinite(zA + shifts) && isfinite(zB)) || !(fabs(zA - zB) <= tol))
+    status[b] = kNeedsExact;
 }
 
 }  // namespace
@@ -283,15 +294,15 @@ cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_
     err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
-    // loss only: the forward CTA alone (blockIdx.y == 0)
-    ctc_chain_kernel<<<dim3(d.B, (phases & 4u) ? 1 : 2), 32 * (1 + w.W), smem, s>>>(
+    // (loss only runs both directions too: their totals are its guard)
+    ctc_chain_kernel<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(
         em, em_len, tgt, tgt_len, blank, d, w, status);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
   if (phases & 4u) {
-    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(d, w, loss, status);
+    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
     return cudaGetLastError();
   }
   if (!(phases & 2u)) return cudaSuccess;

@@ -25,16 +25,21 @@ inline void trace(Tracer *t, cudaStream_t s) {
 }
 
 // ---- validation (reference check order; criterion.py:23-41,92-111,174-190)
-// perm/tok_start (nullable): token CSR of valid utterances for the fast path
+// perm/tok_start (nullable): token CSR of valid utterances for the fast path.
+// mode: kPrepExact (float64 API: valid utterances stay W2L_OK), kPrepFast
+// (fp32 path: inputs outside its range are marked kNeedsExact), or
+// kPrepForceExact (W2L_FLAG_FORCE_EXACT: every valid utterance kNeedsExact).
+enum { kPrepExact = 0, kPrepFast = 1, kPrepForceExact = 2 };
 template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
-                                int *perm, int *tok_start, int32_t *status, cudaStream_t s);
+                                int *perm, int *tok_start, int32_t *status, cudaStream_t s,
+                                int mode = kPrepExact);
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
                                 int *tok_start, int32_t *status, cudaStream_t s,
-                                int check_lse = 1);
+                                int check_lse = 1, int mode = kPrepExact);
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s);

@@ -90,6 +90,7 @@ struct ChainSm {
   double fin[kMaxLatWarps + 1];
   int prod;
   int cons[kCounters];
+  int flush;   // a lattice token's Et fell below exp(-kFlushNats) (set by the producer)
 };
 
 
@@ -138,6 +139,7 @@ struct ProdCtx {
   bool fwd;
   int nconsumers;  // counters cons[0 .. nconsumers) gate ring reuse
   int logits;      // shift term: 0 = max_i e (log-probs), 1 = -log sum_i Et (logits)
+  unsigned tokmask;  // tokens whose Et enter the recursions (flush check)
 };
 
 // frame of processing index p
@@ -172,6 +174,7 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
                                              double *shift_sum) {
   PROF_T0();
   double shifts = 0.0;
+  bool flush = false;
   const int nch = (c.T + kChunk - 1) / kChunk;
   // kProdStages - 1 chunks in flight ahead of the one being converted (an
   // empty commit group keeps the wait count uniform past the end)
@@ -193,12 +196,16 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
     float x[32];
     const int rlin = c.fwd ? lane : rows - 1 - lane;   // ascending-frame row of this lane
     const float *r = sm.raw[ch % kProdStages] + max(rlin, 0) * c.N;
-    float m = -CUDART_INF_F;
+    float m = -CUDART_INF_F, mn = CUDART_INF_F;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       x[i] = (i < c.N && lane < rows) ? r[i] : -CUDART_INF_F;
       m = fmaxf(m, x[i]);
+      if ((c.tokmask >> i) & 1u) mn = fminf(mn, x[i]);
     }
+    // Et = exp(e - m) of a token the recursions use must not flush to zero
+    // (the same flush in both directions would pass the consistency guard)
+    flush |= lane < rows && mn - m < -kFlushNats;
     // ring slots [p0, p0+rows) previously held p - kRing: every consumer must
     // be past the step that read them (a step j reads index <= j)
     const int need = p0 + rows + 1 - kRing;
@@ -227,6 +234,7 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
 #endif
   }
   if (lane == 0) PROF_ADD(0, clock64() - _pt0);
+  if (__any_sync(0xffffffffu, flush) && lane == 0) sm.flush = 1;
   if (shift_sum) {
     shifts = warp_sum(shifts);
     if (lane == 0) *shift_sum = shifts;
@@ -563,6 +571,7 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
       if (s == S - 1 || (KIND == kCtc && s == S - 2)) part += (double)f.v[k];
     }
   } else {
+    wait_ge(&sm.prod, T);   // frame 0's Et (the last step only waited for T - 1)
     const float *er = sm.ering[ring_slot(false, T - 1)];   // frame 0
     if (base == 0) {
       part = (double)er[f.tok[0]] * f.v[0];

@@ -52,18 +52,29 @@ __global__ void __launch_bounds__(128)
       m = fmaxf(m, (float)v);
     }
     if (check_lse && !bits) {
-      // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101)
-      float sum = 0.f;
-      for (int i = 0; i < N; ++i) sum += __expf((float)r[i] - m);
-      const float dev = fabsf(__logf(sum) + m);
-      if (dev > 0.0099f) {
-        if (dev > 0.0101f) {
-          bits |= kBitRowLse;
-        } else {
-          double md = -CUDART_INF, sd = 0.0;
-          for (int i = 0; i < N; ++i) md = fmax(md, (double)r[i]);
-          for (int i = 0; i < N; ++i) sd += exp((double)r[i] - md);
-          if (fabs(log(sd) + md) > 1e-2) bits |= kBitRowLse;
+      // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101).
+      // float inputs: an fp32 pre-check, re-checked in float64 (the
+      // reference's arithmetic) near the threshold; double inputs are checked
+      // in double throughout (a finite double beyond FLT_MAX must not turn
+      // into inf/NaN and slip through).  NaN deviations fail the check.
+      if (sizeof(TE) == sizeof(double)) {
+        double md = -CUDART_INF, sd = 0.0;
+        for (int i = 0; i < N; ++i) md = fmax(md, (double)r[i]);
+        for (int i = 0; i < N; ++i) sd += exp((double)r[i] - md);
+        if (!(fabs(log(sd) + md) <= 1e-2)) bits |= kBitRowLse;
+      } else {
+        float sum = 0.f;
+        for (int i = 0; i < N; ++i) sum += __expf((float)r[i] - m);
+        const float dev = fabsf(__logf(sum) + m);
+        if (!(dev <= 0.0099f)) {
+          if (!(dev <= 0.0101f)) {
+            bits |= kBitRowLse;
+          } else {
+            double md = -CUDART_INF, sd = 0.0;
+            for (int i = 0; i < N; ++i) md = fmax(md, (double)r[i]);
+            for (int i = 0; i < N; ++i) sd += exp((double)r[i] - md);
+            if (!(fabs(log(sd) + md) <= 1e-2)) bits |= kBitRowLse;
+          }
         }
       }
     }
@@ -119,7 +130,8 @@ template <class TE>
 __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int64_t *__restrict__ tgt,
                                 const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans,
-                                Dims d, int lpad, int *perm, int *tok_start, int32_t *status) {
+                                Dims d, int lpad, int *perm, int *tok_start, int32_t *status,
+                                int mode) {
   const int b = blockIdx.x;
   const int T = em_len[b], L = tgt_len[b];
   const int bits = status[b];
@@ -131,7 +143,29 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
     code = W2L_ERR_NUMERIC;                         // :27-28
   } else {
     int bad = 0;
-    for (int i = threadIdx.x; i < d.N * d.N; i += blockDim.x) bad |= !isfinite((double)trans[i]);
+    double amax = -CUDART_INF, amin = CUDART_INF;
+    for (int i = threadIdx.x; i < d.N * d.N; i += blockDim.x) {
+      const double a = (double)trans[i];
+      bad |= !isfinite(a);
+      amax = fmax(amax, a);
+      amin = fmin(amin, a);
+    }
+    // fp32 fast path: a transition weight exp(A - max A) below ~e^-80 would
+    // be flushed to zero in BOTH directions (invisible to the consistency
+    // guard), so such transitions send the utterance to the float64 kernel
+    __shared__ double s_mx[4], s_mn[4];   // 128 threads
+    amax = warp_max(amax);
+    amin = -warp_max(-amin);
+    if ((threadIdx.x & 31) == 0) {
+      s_mx[threadIdx.x >> 5] = amax;
+      s_mn[threadIdx.x >> 5] = amin;
+    }
+    __syncthreads();
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      amax = fmax(amax, s_mx[q]);
+      amin = fmin(amin, s_mn[q]);
+    }
+    const int range = mode == kPrepFast && amin - amax < -(double)kFlushNats;
     if (block_any(bad)) {
       code = W2L_ERR_NUMERIC;                       // :179-180
     } else if (L < 0 || L > d.Lmax) {
@@ -151,6 +185,7 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
       else if (T < L) code = W2L_ERR_INFEASIBLE;    // :187-190
       if (code == W2L_OK && perm)
         build_token_csr(y, L, d.N, 1, 0, perm + (size_t)b * lpad, tok_start + b * 33);
+      if (code == W2L_OK && (mode == kPrepForceExact || range)) code = kNeedsExact;
     }
   }
   __syncthreads();
@@ -160,7 +195,7 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
 __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int64_t *__restrict__ tgt,
                                 const int32_t *__restrict__ tgt_len, int blank, Dims d,
-                                int lpad, int *perm, int *tok_start, int32_t *status) {
+                                int lpad, int *perm, int *tok_start, int32_t *status, int mode) {
   const int b = blockIdx.x;
   const int T = em_len[b], L = tgt_len[b];
   const int bits = status[b];
@@ -196,6 +231,7 @@ __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
     else if (T < L + s_reps) code = W2L_ERR_INFEASIBLE;       // :105-111
     if (code == W2L_OK && perm)
       build_token_csr(y, L, d.N, 2, 1, perm + (size_t)b * lpad, tok_start + b * 33);
+    if (code == W2L_OK && mode == kPrepForceExact) code = kNeedsExact;
   }
   __syncthreads();
   if (threadIdx.x == 0) status[b] = code;
@@ -227,21 +263,23 @@ cudaError_t em_check(const TE *em, const int32_t *em_len, Dims d, int check_lse,
 template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
-                                int *perm, int *tok_start, int32_t *status, cudaStream_t s) {
+                                int *perm, int *tok_start, int32_t *status, cudaStream_t s,
+                                int mode) {
   cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s);
   if (err != cudaSuccess) return err;
   asg_prep_kernel<TE><<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, trans, d, lpad, perm,
-                                          tok_start, status);
+                                          tok_start, status, mode);
   return cudaGetLastError();
 }
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
-                                int *tok_start, int32_t *status, cudaStream_t s, int check_lse) {
+                                int *tok_start, int32_t *status, cudaStream_t s, int check_lse,
+                                int mode) {
   cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s);
   if (err != cudaSuccess) return err;
   ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
-                                      status);
+                                      status, mode);
   return cudaGetLastError();
 }
 template <class TE>
@@ -256,10 +294,10 @@ cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
 #define INST(TE)                                                                           \
   template cudaError_t launch_asg_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, const TE *, Dims, int, int *, \
-                                               int *, int32_t *, cudaStream_t);               \
+                                               int *, int32_t *, cudaStream_t, int);          \
   template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, int, Dims, int, int *, int *, \
-                                               int32_t *, cudaStream_t, int);                 \
+                                               int32_t *, cudaStream_t, int, int);            \
   template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,         \
                                                    int32_t *, cudaStream_t);
 INST(float)

@@ -13,6 +13,8 @@ CTC has no parameters and needs no exchange.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -24,6 +26,58 @@ def shard_bounds(batch_size: int, world: int, rank: int) -> tuple[int, int]:
     base, extra = divmod(batch_size, world)
     lo = rank * base + min(rank, extra)
     return lo, lo + base + (1 if rank < extra else 0)
+
+
+class NcclComm:
+    """The library's own NCCL communicator (C-ABI w2l_comm_*,
+    include/w2l_criterion.h): the transition-gradient all-reduce is enqueued
+    by ``w2l_allreduce_grad_A`` on the compute stream, the same entry a
+    non-Python host uses.  The 128-byte unique id travels over the default
+    torch.distributed group (any channel would do)."""
+
+    def __init__(self, group=None):
+        from . import _native as nat
+        self._nat = nat
+        lib = nat.lib()
+        if not lib.w2l_comm_available():
+            raise nat.NativeLibraryError("libnccl.so.2 could not be loaded")
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            self._check(lib.w2l_comm_unique_id(uid), "w2l_comm_unique_id")
+        if world > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        self._comm = ctypes.c_void_p()
+        self._check(lib.w2l_comm_init(uid, world, rank, ctypes.byref(self._comm)), "w2l_comm_init")
+        self.world, self.rank = world, rank
+
+    def _check(self, rc, what):
+        if rc != self._nat.OK:
+            from .errors import raise_for_status
+            raise_for_status(rc, f"{what} failed ({self._nat.lib().w2l_status_string(rc).decode()})")
+
+    def allreduce_grad_transitions(self, grad: torch.Tensor) -> torch.Tensor:
+        if not (grad.is_cuda and grad.dtype == torch.float32 and grad.is_contiguous()):
+            raise ValueError("grad_transitions must be a contiguous CUDA f32 tensor")
+        stream = ctypes.c_void_p(torch.cuda.current_stream(grad.device).cuda_stream)
+        self._check(self._nat.lib().w2l_allreduce_grad_A(grad.data_ptr(), grad.shape[0],
+                                                         self._comm, stream),
+                    "w2l_allreduce_grad_A")
+        return grad
+
+    def close(self):
+        if self._comm:
+            self._nat.lib().w2l_comm_destroy(self._comm)
+            self._comm = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def allreduce_grad_transitions(grad: torch.Tensor, group=None) -> torch.Tensor:

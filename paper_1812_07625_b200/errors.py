@@ -5,6 +5,9 @@ The C-ABI status codes (include/w2l_criterion.h) map onto them 1:1 through
 ``raise_for_status``.
 """
 
+import importlib
+import os
+
 
 class AsrkitError(Exception):
     """Base class for all toolkit errors (errors.py:4)."""
@@ -37,6 +40,24 @@ class EmissionsFormatError(AsrkitError):
 class DeviceError(AsrkitError):
     """CUDA launch/runtime failure or collective failure in the native layer."""
 
+
+# Drop-in mode: with W2L_REFERENCE_ERRORS naming the reference's errors
+# module (e.g. "asrkit.errors"), the shim raises the reference's own classes,
+# so existing ``except``/``pytest.raises`` clauses written against the
+# reference catch them (tools/ref_suite.py runs the reference tests so).
+_REF = os.environ.get("W2L_REFERENCE_ERRORS")
+if _REF:
+    _ref = importlib.import_module(_REF)
+    AsrkitError = _ref.AsrkitError
+    ContractError = _ref.ContractError
+    NumericError = _ref.NumericError
+    TokenError = _ref.TokenError
+    TargetError = _ref.TargetError
+    InfeasibleTargetError = _ref.InfeasibleTargetError
+    EmissionsFormatError = _ref.EmissionsFormatError
+
+    class DeviceError(AsrkitError):  # noqa: F811  (not in the reference)
+        """CUDA launch/runtime failure or collective failure in the native layer."""
 
 # C-ABI status code -> exception class
 STATUS_CLASSES = {

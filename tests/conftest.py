@@ -45,3 +45,23 @@ def cuda():
         pytest.skip("no CUDA device")
     import torch
     return torch.device("cuda:0")
+
+
+class TokenTable:
+    """Minimal token table for the tests (the criterion path duck-types the
+    table: len(), rep_id and symbol(); the reference's TokenTable,
+    lexicon.py:20-59, provides the same)."""
+
+    def __init__(self, symbols):
+        self.symbols = list(symbols)
+        self.ids = {s: i for i, s in enumerate(self.symbols)}
+
+    def __len__(self):
+        return len(self.symbols)
+
+    def symbol(self, i):
+        return self.symbols[i]
+
+    @property
+    def rep_id(self):
+        return self.ids.get("<2>")

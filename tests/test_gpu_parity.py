@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 C = pytest.importorskip("paper_1812_07625_b200.criterion")
 from paper_1812_07625_b200.errors import (ContractError, InfeasibleTargetError,  # noqa: E402
                                           NumericError, TargetError)
-from paper_1812_07625_b200.tokens import TokenTable  # noqa: E402
+from conftest import TokenTable  # noqa: E402
 
 REL = 1e-4
 

@@ -12,7 +12,7 @@ import torch
 from paper_1812_07625_b200 import _native as nat
 from paper_1812_07625_b200 import criterion as C
 from paper_1812_07625_b200.errors import ContractError, TargetError
-from paper_1812_07625_b200.tokens import TokenTable
+from conftest import TokenTable  # noqa: E402
 
 
 def test_library_exports_every_header_symbol():
