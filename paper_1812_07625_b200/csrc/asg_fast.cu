@@ -1,5 +1,5 @@
-// fp32 batched ASG loss + gradient (replaces criterion.py:167-247 for the
-// batched hot path).
+// Batched ASG loss + gradient (replaces criterion.py:167-247 for the batched
+// hot path), in two precision tiers of one algorithm.
 //
 // Algorithm: the four ASG recursions are run in the SCALED LINEAR domain,
 // the standard exact reformulation of log-space forward-backward
@@ -9,21 +9,27 @@
 // rounding in the scale factors).  The fcc (fully connected, N x N) graph is
 // a 32-lane mat-vec per frame with the previous vector broadcast through
 // shared memory; the fac (forced alignment, L-state chain) graph is a
-// multi-warp wavefront lattice (lattice.cuh): 4 states per lane in fp64 with
-// one power-of-two exponent per lane.  No transcendental sits on the
-// recursion's critical path.
+// multi-warp wavefront lattice (lattice.cuh): 4 states per lane with one
+// power-of-two exponent per lane.  No transcendental sits on the recursion's
+// critical path.  V (the lane type) is float for the fast tier and double
+// for the wide-range tier that takes the utterances failing the fp32 guard.
 //
 // Kernels (one stream, in order):
 //   asg_chain    grid (B, 2 directions), one CTA per (utterance, direction):
 //                producer warp (Et ring), fcc warp, W fac lattice warps;
 //                rows of alpha/beta and exponents to the workspace.
-//   asg_grad     grid (frame blocks, B): 8 warps, one frame per warp at a time:
-//                posteriors (per-frame normaliser Z_t), grad_e, partial
-//                transition gradients, and the consistency guard G_t.
-//   asg_final    per utterance: loss, grad_A_b, guard verdict -> either OK or
-//                kNeedsExact (then the float64 kernel recomputes it).
+//   asg_grad     two CTA bodies in one launch, 128 frames each:
+//                fac   per-frame fac posteriors (normaliser Z_t), the whole
+//                      gradient row (fcc node posteriors minus the fac node
+//                      posteriors gathered by token), state occupancies and
+//                      the fac guard;
+//                fcc   fcc edge outer products and the fcc guard.
+//   asg_final    per utterance: loss, grad_A_b, guard verdict -> OK, or the
+//                next tier.
 // Reference correspondence: fac alpha/beta = criterion.py:193-212, fac
 // posteriors = :214-224, fcc = :227-241, combine = :243-247.
+
+#include <algorithm>
 
 #include "laneblock.cuh"
 #include "lattice.cuh"
@@ -33,7 +39,8 @@
 namespace w2l {
 namespace {
 
-constexpr int kGradFramesPerBlock = 128;
+constexpr int kGradFramesPerBlock = 128;   // frames per gradient CTA (both bodies)
+constexpr int kFccFrames = kGradFramesPerBlock;
 constexpr int kGradWarps = 8;
 
 __device__ __forceinline__ float trans_max(const float *trans, int N) {
@@ -69,19 +76,11 @@ struct LaggedScale {
   }
 };
 
-// ---- fcc: one frame of the 32-lane mat-vec recursion.  `vin` is the vector
-// of the previous step (alpha_{t-1}, or w_u = Et_u * beta'_u), m the lane's
-// row (alpha) or column (beta) of M; returns the unscaled product.
-// packed fp32x2 arithmetic (FFMA2 / FADD2): two lanes of a 64-bit register
+// packed fp32x2 arithmetic (FFMA2): two lanes of a 64-bit register
 __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
                                                     unsigned long long c) {
   unsigned long long d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
 __device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
@@ -94,39 +93,40 @@ __device__ __forceinline__ float f2_hi(unsigned long long x) {
 }
 
 // m: the lane's row of M (alpha) or column (beta); vin: the 32-vector (16B
-// aligned); 8 independent accumulators of depth 4 (scalar FFMA measured
+// aligned); 8 independent accumulators of depth 4 (scalar FMA measured
 // faster than FFMA2 on this latency-bound chain).  SUM: also return the
 // exponent of the vector's sum (lane N's row of ones, or a direct sum).
-template <bool SUM>
-__device__ __forceinline__ float fcc_matvec(const float (&m)[32], const float *vin, bool spare,
-                                            int N, int &e_sum) {
-  const float4 *pv = reinterpret_cast<const float4 *>(vin);
-  float acc[8];
+template <bool SUM, class V>
+__device__ __forceinline__ V fcc_matvec(const V (&m)[32], const V *vin, bool spare, int N,
+                                        int &e_sum) {
+  V acc[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const float4 x = pv[q];
-    acc[q] = m[4 * q] * x.x;
-    acc[q] = fmaf(m[4 * q + 1], x.y, acc[q]);
-    acc[q] = fmaf(m[4 * q + 2], x.z, acc[q]);
-    acc[q] = fmaf(m[4 * q + 3], x.w, acc[q]);
+    V x[4];
+    ld4(vin + 4 * q, x);
+    acc[q] = m[4 * q] * x[0];
+    acc[q] = fma(m[4 * q + 1], x[1], acc[q]);
+    acc[q] = fma(m[4 * q + 2], x[2], acc[q]);
+    acc[q] = fma(m[4 * q + 3], x[3], acc[q]);
   }
-  const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  const V s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   if (SUM) {
     if (spare) {
-      e_sum = exponent_of(__shfl_sync(0xffffffffu, s, N));   // lane N: row of ones
+      e_sum = Pow2<V>::expo(__shfl_sync(0xffffffffu, s, N));   // lane N: row of ones
     } else {
-      float tot = 0.f;
+      V tot = (V)0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) tot += (pv[q].x + pv[q].y) + (pv[q].z + pv[q].w);
-      e_sum = exponent_of(tot);
+      for (int q = 0; q < 32; ++q) tot += vin[q];
+      e_sum = Pow2<V>::expo(tot);
     }
   }
   return s;
 }
 
+template <class V>
 struct FccState {
-  float m[32];
-  float v;       // this lane's current alpha_t / beta'_t
+  V m[32];
+  V v;           // this lane's current alpha_t / beta'_t
   int K;
   int knext;     // scale exponent of the next step (chosen one step ahead)
   LaggedScale sc;
@@ -135,21 +135,20 @@ struct FccState {
 
 // The power-of-two rescaling runs on every kFccRescale-th step only (RS):
 // between rescales the vector's magnitude moves by at most a few steps of
-// growth, far inside fp32's range.  The scale bookkeeping (the sum's exponent
-// arrives through a shuffle) runs after the step's vector is stored, so the
-// next step's mat-vec does not wait behind it.
+// growth, far inside the type's range.  The scale bookkeeping (the sum's
+// exponent arrives through a shuffle) runs after the step's vector is stored,
+// so the next step's mat-vec does not wait behind it.
 constexpr int kFccRescale = 4;
 
 // fcc alpha step t (criterion.py:230): alpha_t = Et (.) (M alpha_{t-1}) 2^-k
-template <bool RS>
-__device__ __forceinline__ void fcc_alpha_step(FccState &f, float et, float (*vec)[32],
-                                               int par, float *out_row, int *outk_t, int lane,
-                                               int N) {
+template <bool RS, class V>
+__device__ __forceinline__ void fcc_alpha_step(FccState<V> &f, V et, V (*vec)[32], int par,
+                                               V *out_row, int *outk_t, int lane, int N) {
   const int k = RS ? f.knext : 0;
-  const float sc = RS ? et * pow2f_fast(-k) : et;   // |k| <= 120: exact
+  const V sc = RS ? et * Pow2<V>::p2(-k) : et;   // |k| <= 120: exact
   __syncwarp();
   int e1 = 0;
-  const float s = fcc_matvec<RS>(f.m, vec[par ^ 1], f.spare, N, e1);
+  const V s = fcc_matvec<RS, V>(f.m, vec[par ^ 1], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
   vec[par][lane] = f.v;
@@ -162,16 +161,15 @@ __device__ __forceinline__ void fcc_alpha_step(FccState &f, float et, float (*ve
 }
 
 // fcc beta' step consuming frame u (criterion.py:236): beta'_{u-1} = M^T (Et_u beta'_u) 2^-k
-template <bool RS>
-__device__ __forceinline__ void fcc_beta_step(FccState &f, float et, float (*vec)[32],
-                                              int par, float *out_row, int *outk_t, int lane,
-                                              int N) {
+template <bool RS, class V>
+__device__ __forceinline__ void fcc_beta_step(FccState<V> &f, V et, V (*vec)[32], int par,
+                                              V *out_row, int *outk_t, int lane, int N) {
   const int k = RS ? f.knext : 0;
-  const float sc = lane < N ? (RS ? pow2f_fast(-k) : 1.f) : 0.f;
+  const V sc = lane < N ? (RS ? Pow2<V>::p2(-k) : (V)1) : (V)0;
   vec[par][lane] = et * f.v;
   __syncwarp();
   int e1 = 0;
-  const float s = fcc_matvec<RS>(f.m, vec[par], f.spare, N, e1);
+  const V s = fcc_matvec<RS, V>(f.m, vec[par], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
   out_row[lane] = f.v;
@@ -182,56 +180,54 @@ __device__ __forceinline__ void fcc_beta_step(FccState &f, float et, float (*vec
   }
 }
 
+template <class V>
 struct FccCtx {
   const float *trans;
   float amax;
   int N, T, lane, cons_idx;
-  float *rows;  // [Tmax][32] this utterance
+  V *rows;      // [Tmax][32] this utterance
   int *ks;      // cumulative exponents, indexed by frame
 };
 
 // fcc recursion over the shared Et ring (criterion.py:227-236); the same
 // step schedule as the lattice warps (lattice.cuh)
-template <bool FWD>
-__device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
-  PROF_T0();
+template <bool FWD, class V>
+__device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
+  constexpr int kRing = Ring<V>::n;
   const int lane = c.lane, N = c.N, T = c.T;
-  FccState f;
+  FccState<V> f;
   f.spare = N < 32;
-  float mrow[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     // forward: row `lane` of M; backward: column `lane`; lane N of a spare
     // lane is a row of ones (its product is the sum of the vector)
     const int p = FWD ? lane * N + j : j * N + lane;
-    mrow[j] = (lane < N && j < N) ? expf(c.trans[p] - c.amax)
-                                  : ((f.spare && lane == N && j < N) ? 1.f : 0.f);
+    f.m[j] = (lane < N && j < N) ? Pow2<V>::ex((V)c.trans[p] - (V)c.amax)
+                                 : ((f.spare && lane == N && j < N) ? (V)1 : (V)0);
   }
-#pragma unroll
-  for (int j = 0; j < 32; ++j) f.m[j] = mrow[j];
   f.K = 0;
   f.knext = f.sc.next();
   int *mycons = &sm.cons[c.cons_idx];
   if (FWD) {
     wait_ge(&sm.prod, 1);
-    f.v = sm.ering[ring_slot(true, 0)][lane];   // alpha_0 = Et_0 (criterion.py:228)
+    f.v = sm.ering[ring_slot<V>(true, 0)][lane];   // alpha_0 = Et_0 (criterion.py:228)
     sm.vec[0][lane] = f.v;
     c.rows[lane] = f.v;
     if (lane == 0) c.ks[0] = 0;
   } else {
-    f.v = lane < N ? 1.f : 0.f;
+    f.v = lane < N ? (V)1 : (V)0;
     c.rows[(size_t)(T - 1) * 32 + lane] = f.v;
     if (lane == 0) c.ks[T - 1] = 0;
   }
   publish(mycons, 1, lane);
   auto generic = [&](int j) {
     wait_ge(&sm.prod, eidx_of(FWD, j) + 1);
-    const float et = sm.ering[j & (kRing - 1)][lane];
+    const V et = sm.ering[j & (kRing - 1)][lane];
     const int t = frame_of(FWD, T, j);
     if (FWD)
-      fcc_alpha_step<true>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+      fcc_alpha_step<true, V>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
     else
-      fcc_beta_step<true>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
+      fcc_beta_step<true, V>(f, et, sm.vec, j & 1, c.rows + (size_t)t * 32, c.ks + t, lane, N);
     publish(mycons, j + 1, lane);
   };
   const int pro_end = min(T, kBlk);
@@ -240,12 +236,11 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
-    PROF_STEADY(m >= 40 && m < 160);
-    PROF_WAIT(1, wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, &sm.prod, 0, &sm.prod, 0));
-    const float *eb = sm.ering[j0 & (kRing - 1)];
+    wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, &sm.prod, 0, &sm.prod, 0);
+    const V *eb = sm.ering[j0 & (kRing - 1)];
     const int tb = frame_of(FWD, T, j0);
-    float *sv = c.rows + (size_t)tb * 32;
-    float etq[kBlk];
+    V *sv = c.rows + (size_t)tb * 32;
+    V etq[kBlk];
 #pragma unroll
     for (int q = 0; q < kBlk; ++q) etq[q] = eb[q * kStride + lane];
 #pragma unroll
@@ -253,56 +248,57 @@ __device__ void fcc_run(ChainSm &sm, const FccCtx &c, double *lnz) {
       const int dq = FWD ? q : -q;
       if ((q % kFccRescale) == kFccRescale - 1) {
         if (FWD)
-          fcc_alpha_step<true>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+          fcc_alpha_step<true, V>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
         else
-          fcc_beta_step<true>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+          fcc_beta_step<true, V>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
       } else {
         if (FWD)
-          fcc_alpha_step<false>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+          fcc_alpha_step<false, V>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane,
+                                   N);
         else
-          fcc_beta_step<false>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane, N);
+          fcc_beta_step<false, V>(f, etq[q], sm.vec, q & 1, sv + dq * 32, c.ks + tb + dq, lane,
+                                  N);
       }
     }
     publish(mycons, j0 + kBlk, lane);
   }
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
   publish(mycons, kDone, lane);
-  if (lane == 0) PROF_ADD(0, clock64() - _pt0);
-  float z;
+  V z;
   if (FWD) {
-    z = warp_sum(lane < N ? f.v : 0.f);
+    z = warp_sum(lane < N ? f.v : (V)0);
   } else {
     wait_ge(&sm.prod, T);   // frame 0's Et (the last step only waited for T - 1)
-    const float e0 = sm.ering[ring_slot(false, T - 1)][lane];   // frame 0
+    const V e0 = sm.ering[ring_slot<V>(false, T - 1)][lane];   // frame 0
     z = warp_sum(e0 * f.v);
   }
   if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
-template <bool FWD>
-__device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, int W,
-                                               const float *em, int T, int L,
+template <bool FWD, class V>
+__device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, int T, int L,
                                                const int64_t *y, const float *trans, Dims d,
-                                               const AsgFastWs &w, int b, int32_t *status) {
+                                               const AsgFastWs &w, int b, int32_t *status,
+                                               int fail) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float amax = trans_max(trans, d.N);
   const int weff = lat_warps(L);
   if (warp == 0) {
     // the fcc uses every token
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + W, 0,
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + weff, 0,
                d.N >= 32 ? 0xffffffffu : (1u << d.N) - 1u};
-    producer_run(sm, pc, lane, nullptr);
+    producer_run<V>(sm, pc, lane, nullptr);
   } else if (warp == 1) {
-    FccCtx fc;
+    FccCtx<V> fc;
     fc.trans = trans;
     fc.amax = amax;
     fc.N = d.N;
     fc.T = T;
     fc.lane = lane;
     fc.cons_idx = 0;
-    fc.rows = (FWD ? w.fcc_a : w.fcc_b) + (size_t)b * d.Tmax * 32;
+    fc.rows = reinterpret_cast<V *>(FWD ? w.fcc_a : w.fcc_b) + (size_t)b * d.Tmax * 32;
     fc.ks = FWD ? w.fcc_ka + (size_t)b * w.tpad : w.fcc_kb + (size_t)b * w.tpad + 1;
-    fcc_run<FWD>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
+    fcc_run<FWD, V>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
   } else if (warp - 2 < weff) {
     LatCtx c;
     c.w = warp - 2;
@@ -314,31 +310,30 @@ __device__ __forceinline__ void asg_chain_body(ChainSm &sm, unsigned char *dsm, 
     c.cons_idx = 1;
     c.Tmax = d.Tmax;
     const size_t ub = (size_t)b * w.W * d.Tmax;
-    c.rows = (FWD ? w.fac_a : w.fac_b) + ub * kLatStates;
+    c.rows = reinterpret_cast<V *>(FWD ? w.fac_a : w.fac_b) + ub * kLatStates;
     c.exps = (FWD ? w.fac_ea : w.fac_eb) + ub * 32;
-    LatState f;
-    lat_init_weights<kFac, FWD>(f, c, y, L, trans, amax, 0);
-    lattice_run<kFac, FWD>(sm, c, f);
+    LatState<V> f;
+    lat_init_weights<kFac, FWD, V>(f, c.w, lane, d.N, L, y, L, trans, amax, 0);
+    lattice_run<kFac, FWD, V>(sm, c, f);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     w.scal[b * 4 + (FWD ? 2 : 3)] = lattice_total(sm, weff);
-    if (sm.flush) status[b] = kNeedsExact;
+    if (sm.flush) status[b] = fail;
   }
 }
 
 // grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
+template <class V>
 __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const float *__restrict__ trans, Dims d, AsgFastWs w,
-                     int32_t *__restrict__ status) {
+                     int32_t *__restrict__ status, int want, int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  const int W = w.W;
-  ChainSm &sm = *reinterpret_cast<ChainSm *>(
-      dsm);
+  ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
   const int b = blockIdx.x;
-  if (status[b] != W2L_OK) return;
+  if (status[b] != want) return;
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(L);
   if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0;
@@ -347,17 +342,157 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
   __syncthreads();
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (blockIdx.y == 0)
-    asg_chain_body<true>(sm, dsm, W, em, T, L, y, trans, d, w, b, status);
+    asg_chain_body<true, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
   else
-    asg_chain_body<false>(sm, dsm, W, em, T, L, y, trans, d, w, b, status);
-}
-
-size_t asg_chain_smem(int W) {
-  (void)W;
-  return sizeof(ChainSm);
+    asg_chain_body<false, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
 }
 
 // ----------------------------------------------------------- grad kernel --
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Per-warp staging area of the fcc body: the warp's frames' fcc rows (alpha
+// including frame ta-1, beta), exponents and emission rows come in with one
+// cp.async batch.  Reused for the block reduction.
+constexpr int kFccFpw = kFccFrames / kGradWarps;            // 16 frames per warp
+template <class V>
+__host__ __device__ constexpr size_t fcc_stage_bytes() {
+  return (((size_t)(kFccFpw + 1) * 32 + (size_t)kFccFpw * 32) * sizeof(V) +
+          (size_t)kFccFpw * 32 * 4 + (size_t)(2 * kFccFpw + 1) * 4 + 15) & ~(size_t)15;
+}
+static_assert(fcc_stage_bytes<float>() >= 4096, "the staging area doubles as the reduction buffer");
+
+// fcc edge posteriors and the fcc guard (the fcc node posteriors are formed
+// by the fac body, which writes the whole gradient row)
+template <class V>
+__device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
+                                                  const int32_t *__restrict__ em_len, Dims d,
+                                                  const AsgFastWs &w,
+                                                  const int32_t *__restrict__ status, int want,
+                                                  int blk, unsigned char *smem) {
+  __shared__ float gwarp[kGradWarps][2];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = d.N;
+  const int T = em_len[b];
+  const int t0 = blk * kFccFrames;
+  if (status[b] != want || t0 >= T) return;
+  const int ta = t0 + warp * kFccFpw, tb = min(ta + kFccFpw, d.Tmax);
+  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
+  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
+  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
+  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
+  const int tend = min(tb, T);
+
+  // ---- stage this warp's frames: row r of sfa/ska is frame ta-1+r, row r of
+  // sfb/skb/se is frame ta+r
+  unsigned char *st = smem + warp * fcc_stage_bytes<V>();
+  V *sfa = reinterpret_cast<V *>(st);                // [kFccFpw+1][32]
+  V *sfb = sfa + (kFccFpw + 1) * 32;                 // [kFccFpw][32]
+  float *se = reinterpret_cast<float *>(sfb + kFccFpw * 32);   // [kFccFpw][N] (flat)
+  int *ska = reinterpret_cast<int *>(se + kFccFpw * 32);       // [kFccFpw+1]
+  int *skb = ska + kFccFpw + 1;                      // [kFccFpw]
+  constexpr int kRowChunks = 32 * sizeof(V) / 16;    // 16-byte chunks per row
+  if (ta < tend) {
+    const int f0 = max(ta - 1, 0), nf = tend - ta;
+    const V *fa_g = reinterpret_cast<const V *>(w.fcc_a) + (size_t)b * d.Tmax * 32;
+    const V *fb_g = reinterpret_cast<const V *>(w.fcc_b) + (size_t)b * d.Tmax * 32;
+    const int nfa = (tend - f0) * kRowChunks;
+    V *dfa = sfa + (f0 - (ta - 1)) * 32;
+    for (int i = lane; i < nfa; i += 32)
+      cp_async16(reinterpret_cast<char *>(dfa) + 16 * i,
+                 reinterpret_cast<const char *>(fa_g + (size_t)f0 * 32) + 16 * i);
+    for (int i = lane; i < nf * kRowChunks; i += 32)
+      cp_async16(reinterpret_cast<char *>(sfb) + 16 * i,
+                 reinterpret_cast<const char *>(fb_g + (size_t)ta * 32) + 16 * i);
+    const float *e_g = em + ((size_t)b * d.Tmax + ta) * N;
+    for (int i = lane; i < nf * N; i += 32) cp_async4(se + i, e_g + i);
+    const int *ka_g = w.fcc_ka + (size_t)b * w.tpad;
+    const int *kb_g = w.fcc_kb + (size_t)b * w.tpad + 1;
+    if (lane < tend - f0) cp_async4(ska + (f0 - (ta - 1)) + lane, ka_g + f0 + lane);
+    if (lane < nf) cp_async4(skb + lane, kb_g + ta + lane);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncwarp();
+
+  // edge accumulators: acc[lane][j] = sum_t u_t[lane] alpha_{t-1}[j]
+  unsigned long long accA[16];   // float: (row lane, columns 2jj, 2jj+1) packed
+  double accD[sizeof(V) == 8 ? 32 : 1];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) accA[j] = 0ull;
+#pragma unroll
+  for (int j = 0; j < (int)(sizeof(accD) / sizeof(double)); ++j) accD[j] = 0.0;
+#pragma unroll 2
+  for (int t = ta; t < tend; ++t) {
+    const int r = t - ta;
+    const float e = lane < N ? se[r * N + lane] : -CUDART_INF_F;
+    const V fa = sfa[(r + 1) * 32 + lane], fb = sfb[r * 32 + lane];
+    const int ka = ska[r + 1], kb = skb[r];
+    const float m = warp_max(e);
+    const V et = lane < N ? et_of<V>(e, m) : (V)0;
+    // the frame's fcc normaliser (the node posteriors themselves, :238, are
+    // formed in the fac body)
+    const V zf = warp_sum(fa * fb);
+    const V izf = (V)1 / zf;
+    float lz;
+    if constexpr (sizeof(V) == 4) lz = __log2f(zf);
+    else lz = (float)log2(zf);
+    const float g = lz + (float)(ka + kb - refFi) - refFf;
+    gmin = fminf(gmin, g);
+    gmax = fmaxf(gmax, g);
+    if (t >= 1) {
+      // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
+      const V u = et * fb * Pow2<V>::p2(ska[r] - ka) * izf;
+      if constexpr (sizeof(V) == 4) {
+        const unsigned long long u2 = f2_dup((float)u);
+        const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(sfa + r * 32);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          const ulonglong2 x = pv[qq];
+          accA[2 * qq] = ffma2(u2, x.x, accA[2 * qq]);
+          accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) accD[j] = fma((double)u, (double)sfa[r * 32 + j], accD[j]);
+      }
+    }
+  }
+  __syncwarp();
+  float *red = reinterpret_cast<float *>(st);   // this warp's partial [32][32]
+  if constexpr (sizeof(V) == 4) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      red[lane * 32 + 2 * j] = f2_lo(accA[j]);
+      red[lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) red[lane * 32 + j] = (float)accD[j];
+  }
+  if (lane == 0) {
+    gwarp[warp][0] = gmin;
+    gwarp[warp][1] = gmax;
+  }
+  __syncthreads();
+  float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < kGradWarps; ++q)
+      s += reinterpret_cast<const float *>(smem + q * fcc_stage_bytes<V>())[i];
+    dstA[i] = s;
+  }
+  if (threadIdx.x < 2) {
+    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    for (int q = 0; q < kGradWarps; ++q)
+      g = threadIdx.x ? fmaxf(g, gwarp[q][1]) : fminf(g, gwarp[q][0]);
+    w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
+  }
+}
+
 // sum of the shared-memory floats at addresses addr[q0 .. q1) (4 independent
 // chains; addresses are absolute shared-window addresses)
 __device__ __forceinline__ float lds_f32(unsigned a) {
@@ -384,151 +519,31 @@ __device__ __forceinline__ float gather_shared(const unsigned *addr, int q0, int
   return (c0 + c1) + (c2 + c3);
 }
 
-// 2^x as a float for integer x clamped to [-127, 127] (0 below)
-__device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
-
-// The gradient is split in two kernels with small register footprints (so
-// that enough warps are resident to hide the row loads):
-//   asg_fcc_grad  fcc node posteriors -> grad_e row (full part), fcc edge
-//                 outer products u_t alpha_{t-1}^T, fcc guard;
-//   asg_fac_grad  fac node posteriors gathered by token (subtracted from the
-//                 row), fac stay/step edge sums, fac guard.
-// A warp handles consecutive frames (alpha_{t-1} carried in registers).
-// Posteriors are normalised per frame by their own sums z_t; lattice values
-// are scaled into range by the lane exponents against the utterance's
-// reference exponent.  Edge sums are accumulated without their constant
-// transition weights (M, S, P), which are applied once in the epilogues.
-
-// Per-warp staging area of asg_fcc_grad (floats): the warp's frames' fcc
-// rows (alpha including frame ta-1, beta), exponents and emission rows come
-// in with one cp.async batch -- with a one-frame register prefetch every
-// frame paid most of a DRAM round trip.  Reused for the block reduction.
-constexpr int kFccFpw = kGradFramesPerBlock / kGradWarps;            // 16 frames per warp
-constexpr int kFccStage = ((kFccFpw + 1) * 32 + 2 * kFccFpw * 32 + 2 * (kFccFpw + 1) + 3) & ~3;
-static_assert(kFccStage >= 1024, "the staging area doubles as the reduction buffer");
-constexpr size_t kFccGradSmem = sizeof(float) * kGradWarps * kFccStage;
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-
-// fcc edge posteriors and the fcc guard (the fcc node posteriors are formed
-// by asg_fac_grad_body, which writes the whole gradient row)
-__device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
-                                                  const int32_t *__restrict__ em_len, Dims d,
-                                                  const AsgFastWs &w,
-                                                  const int32_t *__restrict__ status, int blk) {
-  extern __shared__ __align__(16) float fsm[];
-  __shared__ float gwarp[kGradWarps][2];
-  const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int N = d.N;
-  const int T = em_len[b];
-  const int t0 = blk * kGradFramesPerBlock;
-  if (status[b] != W2L_OK) return;
-  const int ta = t0 + warp * kFccFpw, tb = min(ta + kFccFpw, d.Tmax);
-  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
-  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
-  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
-  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
-  const int tend = min(tb, T);
-
-  // ---- stage this warp's frames: row r of sfa/ska is frame ta-1+r, row r of
-  // sfb/skb/se is frame ta+r
-  float *st = fsm + warp * kFccStage;
-  float *sfa = st;                                   // [kFccFpw+1][32]
-  float *sfb = sfa + (kFccFpw + 1) * 32;             // [kFccFpw][32]
-  float *se = sfb + kFccFpw * 32;                    // [kFccFpw][N] (flat)
-  int *ska = reinterpret_cast<int *>(se + kFccFpw * 32);   // [kFccFpw+1]
-  int *skb = ska + kFccFpw + 1;                      // [kFccFpw]
-  if (ta < tend) {
-    const int f0 = max(ta - 1, 0), nf = tend - ta;
-    const float *fa_g = w.fcc_a + (size_t)b * d.Tmax * 32;
-    const float *fb_g = w.fcc_b + (size_t)b * d.Tmax * 32;
-    const int nfa = (tend - f0) * 8;   // 16-byte chunks
-    float *dfa = sfa + (f0 - (ta - 1)) * 32;
-    for (int i = lane; i < nfa; i += 32) cp_async16(dfa + 4 * i, fa_g + (size_t)f0 * 32 + 4 * i);
-    for (int i = lane; i < nf * 8; i += 32) cp_async16(sfb + 4 * i, fb_g + (size_t)ta * 32 + 4 * i);
-    const float *e_g = em + ((size_t)b * d.Tmax + ta) * N;
-    for (int i = lane; i < nf * N; i += 32) cp_async4(se + i, e_g + i);
-    const int *ka_g = w.fcc_ka + (size_t)b * w.tpad;
-    const int *kb_g = w.fcc_kb + (size_t)b * w.tpad + 1;
-    if (lane < tend - f0) cp_async4(ska + (f0 - (ta - 1)) + lane, ka_g + f0 + lane);
-    if (lane < nf) cp_async4(skb + lane, kb_g + ta + lane);
-    cp_async_commit();
-    cp_async_wait<0>();
-  }
-  __syncwarp();
-
-  unsigned long long accA[16];   // accA[jj] = (row lane, columns 2jj, 2jj+1)
-#pragma unroll
-  for (int j = 0; j < 16; ++j) accA[j] = 0ull;
-#pragma unroll 2
-  for (int t = ta; t < tend; ++t) {
-    const int r = t - ta;
-    const float e = lane < N ? se[r * N + lane] : -CUDART_INF_F;
-    const float fa = sfa[(r + 1) * 32 + lane], fb = sfb[r * 32 + lane];
-    const int ka = ska[r + 1], kb = skb[r];
-    const float m = warp_max(e);
-    const float et = lane < N ? et_of(e, m) : 0.f;
-    // the frame's fcc normaliser (the node posteriors themselves, :238, are
-    // formed in asg_fac_grad_body)
-    const float zf = warp_sum(fa * fb);
-    const float izf = 1.f / zf;
-    const float g = __log2f(zf) + (float)(ka + kb - refFi) - refFf;
-    gmin = fminf(gmin, g);
-    gmax = fmaxf(gmax, g);
-    if (t >= 1) {
-      // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
-      const unsigned long long u2 = f2_dup(et * fb * pow2f_fast(ska[r] - ka) * izf);
-      const ulonglong2 *pv = reinterpret_cast<const ulonglong2 *>(sfa + r * 32);
-#pragma unroll
-      for (int qq = 0; qq < 8; ++qq) {
-        const ulonglong2 x = pv[qq];
-        accA[2 * qq] = ffma2(u2, x.x, accA[2 * qq]);
-        accA[2 * qq + 1] = ffma2(u2, x.y, accA[2 * qq + 1]);
-      }
-    }
-  }
-  __syncwarp();
-  float *red = st;   // this warp's partial [32][32]
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    red[lane * 32 + 2 * j] = f2_lo(accA[j]);
-    red[lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
-  }
-  if (lane == 0) {
-    gwarp[warp][0] = gmin;
-    gwarp[warp][1] = gmax;
-  }
-  __syncthreads();
-  float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < kGradWarps; ++q) s += fsm[q * kFccStage + i];
-    dstA[i] = s;
-  }
-  if (threadIdx.x < 2) {
-    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
-    for (int q = 0; q < kGradWarps; ++q)
-      g = threadIdx.x ? fmaxf(g, gwarp[q][1]) : fminf(g, gwarp[q][0]);
-    w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
-  }
+template <int W>
+constexpr size_t fac_grad_smem() {
+  return sizeof(float) * (kGradWarps * ((size_t)W * kLatStates + 2 + 2 + 2 * (size_t)W * kLatStates));
 }
 
 // The whole gradient row: fcc node posteriors (full part, :238) minus the
 // fac node posteriors gathered by token (:214-217), plus the fac occupancy.
-template <int W>
+// A warp handles consecutive frames; each frame's rows are loaded one frame
+// ahead.  Lanes past the lattice's last state were never stored: zeros.
+//
+// Fac edge sums need no edge products: a forced alignment enters every state
+// l >= 1 exactly once and stays in state l (n_l - 1) times, n_l its frame
+// count, so the summed posteriors of the stay and step edges (:218-224) are
+// occ(l) - 1 and 1, occ(l) = sum_t of the node posterior.  Only occ is
+// accumulated here; asg_final applies the identity.
+template <int W, class V>
 __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em_len,
                                                   const int32_t *__restrict__ tgt_len, Dims d,
                                                   const AsgFastWs &w, float *__restrict__ grad_em,
-                                                  const int32_t *__restrict__ status, int blk) {
+                                                  const int32_t *__restrict__ status, int want,
+                                                  int blk, unsigned char *smem) {
   constexpr int LP = W * kLatStates;
-  extern __shared__ __align__(16) float gsm[];
   // [kGradWarps][LP] posterior row; after its frame loop each warp reuses
   // its own row for the occupancy partials (redE)
-  float *prow = gsm;
+  float *prow = reinterpret_cast<float *>(smem);
   float *redE = prow;
   float *zcell = prow + kGradWarps * LP;         // [kGradWarps][2] zero cells
   float *gwarp = zcell + kGradWarps * 2;         // [kGradWarps][2] guard
@@ -544,24 +559,17 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
-  const bool ok = status[b] == W2L_OK;
-  // rows outside the utterance (or of a failed utterance) get zero gradient
-  for (int t = max(ta, ok ? T : 0); t < tb; ++t)
-    if (lane < N) ge[(size_t)t * N + lane] = 0.f;
-  if (!ok) return;
-  if (t0 >= T) {
-    // keep the partial buffers well-defined for the final reduction (the
-    // fcc part and its guard half come from asg_fcc_grad_body)
-    for (int i = threadIdx.x; i < LP; i += blockDim.x)
-      w.part_edge[((size_t)b * w.nblk + blk) * LP + i] = 0.f;
-    if (threadIdx.x < 2)
-      w.part_guard[((size_t)b * w.nblk + blk) * 4 + 2 + threadIdx.x] =
-          (threadIdx.x & 1) ? -CUDART_INF_F : CUDART_INF_F;
-    return;
+  const int st = status[b];
+  if (want == W2L_OK) {
+    // the first tier owns the zeros: padding frames and utterances it does
+    // not compute (a later tier rewrites the rows of the ones it takes)
+    for (int t = st == W2L_OK ? max(ta, T) : ta; t < tb; ++t)
+      if (lane < N) ge[(size_t)t * N + lane] = 0.f;
   }
+  if (st != want || t0 >= T) return;
 
   const int L = tgt_len[b];
-  // segments the chain wrote for this utterance (the batch's W may be wider)
+  // lattice warps the chain wrote for this utterance (the batch's W may be wider)
   const int weff = min(lat_warps(L), W);
   float *myp = prow + warp * LP;
   unsigned *myaddr = saddr + warp * 2 * LP;
@@ -592,18 +600,13 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
 
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  const float4 *A4 = reinterpret_cast<const float4 *>(w.fac_a + seg0 * kLatStates) + lane;
-  const float4 *B4 = reinterpret_cast<const float4 *>(w.fac_b + seg0 * kLatStates) + lane;
+  const V *A = reinterpret_cast<const V *>(w.fac_a) + seg0 * kLatStates + lane * kSpl;
+  const V *Bv = reinterpret_cast<const V *>(w.fac_b) + seg0 * kLatStates + lane * kSpl;
   const int *EA = w.fac_ea + seg0 * 32 + lane;
   const int *EB = w.fac_eb + seg0 * 32 + lane;
-  const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);   // float4 per segment
-  const unsigned sege = (unsigned)d.Tmax * 32;
+  const size_t segv = (size_t)d.Tmax * kLatStates;
+  const size_t sege = (size_t)d.Tmax * 32;
 
-  // Fac edge sums need no edge products: a forced alignment enters every
-  // state l >= 1 exactly once and stays in state l (n_l - 1) times, n_l its
-  // frame count, so the summed posteriors of the stay and step edges
-  // (:218-224) are occ(l) - 1 and 1, occ(l) = sum_t of the node posterior.
-  // Only occ is accumulated here; asg_final applies the identity.
   float accO[W][kSpl];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw)
@@ -612,60 +615,66 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   const int tend = min(tb, T);
   // the fcc rows of the next frame (full-part node posteriors) are loaded one
   // frame ahead
-  const float *fca = w.fcc_a + (size_t)b * d.Tmax * 32 + lane;
-  const float *fcb = w.fcc_b + (size_t)b * d.Tmax * 32 + lane;
-  float ca_nx = 0.f, cb_nx = 0.f;
+  const V *fca = reinterpret_cast<const V *>(w.fcc_a) + (size_t)b * d.Tmax * 32 + lane;
+  const V *fcb = reinterpret_cast<const V *>(w.fcc_b) + (size_t)b * d.Tmax * 32 + lane;
+  V ca_nx = (V)0, cb_nx = (V)0;
   if (ta < tend) {
-    ca_nx = fca[(unsigned)ta * 32];
-    cb_nx = fcb[(unsigned)ta * 32];
+    ca_nx = fca[(size_t)ta * 32];
+    cb_nx = fcb[(size_t)ta * 32];
   }
-  // the rows are loaded one frame ahead too (segments >= weff read zeros)
-  float4 na[W], nb[W];
+  // the rows are loaded one frame ahead too (lanes past the lattice read zeros)
+  V na[W][kSpl], nb[W][kSpl];
   int nea[W], neb[W];
+  bool live[W];
 #pragma unroll
   for (int sw = 0; sw < W; ++sw) {
-    na[sw] = nb[sw] = make_float4(0.f, 0.f, 0.f, 0.f);
+    live[sw] = sw < weff && sw * kLatStates + lane * kSpl < L;
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) na[sw][k] = nb[sw][k] = (V)0;
     nea[sw] = neb[sw] = kNegExp;
-    if (sw < weff && ta < tend) {
-      const unsigned tq = (unsigned)ta * 32;
-      na[sw] = A4[sw * segq + tq];
-      nb[sw] = B4[sw * segq + tq];
-      nea[sw] = EA[sw * sege + tq];
-      neb[sw] = EB[sw * sege + tq];
+    if (live[sw] && ta < tend) {
+      const size_t tq = (size_t)ta * kLatStates;
+      ld4(A + sw * segv + tq, na[sw]);
+      ld4(Bv + sw * segv + tq, nb[sw]);
+      nea[sw] = EA[sw * sege + (size_t)ta * 32];
+      neb[sw] = EB[sw * sege + (size_t)ta * 32];
     }
   }
   for (int t = ta; t < tend; ++t) {
-    const unsigned tq = (unsigned)t * 32;
-    float4 va[W], vb[W];
+    V va[W][kSpl], vb[W][kSpl];
     int ea[W], eb[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      va[sw] = na[sw];
-      vb[sw] = nb[sw];
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) {
+        va[sw][k] = na[sw][k];
+        vb[sw][k] = nb[sw][k];
+      }
       ea[sw] = nea[sw];
       eb[sw] = neb[sw];
-      if (sw < weff && t + 1 < tend) {
-        na[sw] = A4[sw * segq + tq + 32];
-        nb[sw] = B4[sw * segq + tq + 32];
-        nea[sw] = EA[sw * sege + tq + 32];
-        neb[sw] = EB[sw * sege + tq + 32];
+      if (live[sw] && t + 1 < tend) {
+        const size_t tq = (size_t)(t + 1) * kLatStates;
+        ld4(A + sw * segv + tq, na[sw]);
+        ld4(Bv + sw * segv + tq, nb[sw]);
+        nea[sw] = EA[sw * sege + (size_t)(t + 1) * 32];
+        neb[sw] = EB[sw * sege + (size_t)(t + 1) * 32];
       }
     }
-    const float gam = ca_nx * cb_nx;   // fcc node posterior, unnormalised
+    const float gam = (float)(ca_nx * cb_nx);   // fcc node posterior, unnormalised
     if (t + 1 < tend) {
-      ca_nx = fca[(unsigned)(t + 1) * 32];
-      cb_nx = fcb[(unsigned)(t + 1) * 32];
+      ca_nx = fca[(size_t)(t + 1) * 32];
+      cb_nx = fcb[(size_t)(t + 1) * 32];
     }
     // fac node posteriors (:214-217)
     float zl = 0.f;
     float4 p[W];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      const float sc = pow2_clamped(ea[sw] + eb[sw] - refCi);
-      p[sw].x = va[sw].x * vb[sw].x * sc;
-      p[sw].y = va[sw].y * vb[sw].y * sc;
-      p[sw].z = va[sw].z * vb[sw].z * sc;
-      p[sw].w = va[sw].w * vb[sw].w * sc;
+      const V sc = pow2_clamped<V>(ea[sw] + eb[sw] - refCi);
+      p[sw].x = (float)(va[sw][0] * vb[sw][0] * sc);
+      p[sw].y = (float)(va[sw][1] * vb[sw][1] * sc);
+      p[sw].z = (float)(va[sw][2] * vb[sw][2] * sc);
+      p[sw].w = (float)(va[sw][3] * vb[sw][3] * sc);
       reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p[sw];
       zl += (p[sw].x + p[sw].y) + (p[sw].z + p[sw].w);
     }
@@ -699,7 +708,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     } else {
       con = gather_shared(myaddr, ts0, ts1);
     }
-    if (lane < N) ge[tq / 32 * N + lane] = gam * izf - con * izc;
+    if (lane < N) ge[(size_t)t * N + lane] = gam * izf - con * izc;
     __syncwarp();
   }
 
@@ -737,9 +746,10 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 __global__ void __launch_bounds__(1024)
     asg_final_kernel(const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
-                     AsgFastWs w, double *loss, float *ga_utt, int32_t *status) {
+                     AsgFastWs w, double *loss, float *ga_utt, int32_t *status, int want,
+                     int fail) {
   const int b = blockIdx.x;
-  __shared__ float sEdge[1024];
+  __shared__ float sEdge[kMaxLatWarps * kLatStates];
   __shared__ float sA[1024];
   __shared__ float s_red[32];
   __shared__ int s_bad;
@@ -747,8 +757,11 @@ __global__ void __launch_bounds__(1024)
   __shared__ int sperm[W2L_MAX_ASG_LABELS];   // token CSR
   __shared__ int sts[33];
   const int N = d.N, NN = N * N;
-  if (status[b] != W2L_OK) {
-    for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
+  const int st = status[b];
+  if (st != want) {
+    // the first tier owns the zeros of the utterances it does not compute
+    if (want == W2L_OK)
+      for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
     return;
   }
   const int L = tgt_len[b], T = em_len[b], LP = w.lpad;
@@ -764,17 +777,14 @@ __global__ void __launch_bounds__(1024)
     sperm[l] = w.perm[(size_t)b * w.lpad + l];
   }
   if (threadIdx.x <= N) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];   // N+1 written
-  // fixed-order sums of the per-frame-block partials; 4 independent
-  // accumulators keep several loads in flight per thread
-  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
-  // (16 partials are loaded at once -- one memory latency per 16 blocks --
-  // then added in a fixed order)
-  auto sum_parts = [&](const float *base, size_t stride) {
+  // fixed-order sums of the per-frame-block partials (16 loaded at once --
+  // one memory latency per 16 blocks -- then added in a fixed order)
+  auto sum_parts = [&](const float *base, size_t stride, int nb) {
     float acc = 0.f;
-    for (int q0 = 0; q0 < nb_used; q0 += 16) {
+    for (int q0 = 0; q0 < nb; q0 += 16) {
       float v[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = q0 + k < nb_used ? base[(size_t)(q0 + k) * stride] : 0.f;
+      for (int k = 0; k < 16; ++k) v[k] = q0 + k < nb ? base[(size_t)(q0 + k) * stride] : 0.f;
 #pragma unroll
       for (int k = 0; k < 16; k += 2) v[k] += v[k + 1];
 #pragma unroll
@@ -783,23 +793,22 @@ __global__ void __launch_bounds__(1024)
     }
     return acc;
   };
+  const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
   for (int i = threadIdx.x; i < LP; i += blockDim.x)
-    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * LP + i, LP);
+    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * LP + i, LP, nb_used);
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
-    sA[i] = sum_parts(w.part_fullA + (size_t)b * w.nblk * 1024 + i, 1024);
+    sA[i] = sum_parts(w.part_fullA + (size_t)b * w.nblk * 1024 + i, 1024, nb_used);
   __syncthreads();
   float amax = s_red[0];
   for (int q = 1; q < (int)(blockDim.x >> 5); ++q) amax = fmaxf(amax, s_red[q]);
-  const int *perm = sperm;
-  const int *ts = sts;
   for (int p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = p / N, j = p % N;
     const float full = sA[i * 32 + j] * expf(trans[p] - amax);
     // states labelled i: stay edges (i,i) sum to occ(l) - 1, step edges
-    // (i, y_{l-1}) to 1 (see asg_fac_grad_kernel)
+    // (i, y_{l-1}) to 1 (see asg_fac_grad_body)
     float con = 0.f;
-    for (int q = ts[i]; q < ts[i + 1]; ++q) {
-      const int l = perm[q];
+    for (int q = sts[i]; q < sts[i + 1]; ++q) {
+      const int l = sperm[q];
       if (i == j) con += sEdge[l] - 1.f;
       if (l > 0 && sy[l - 1] == j) con += 1.f;
     }
@@ -812,72 +821,118 @@ __global__ void __launch_bounds__(1024)
   const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)T / 1600.0));
   int bad = !(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb));
-  bad |= fabs(zF - zFb) > tol || fabs(zC - zCb) > tol;
+  bad |= !(fabs(zF - zFb) <= tol) || !(fabs(zC - zCb) <= tol);
   for (int q = threadIdx.x; q < nb_used; q += blockDim.x) {
     const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 4;
     bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
     bad |= !(fabs((double)g[2]) * ln2 <= tol && fabs((double)g[3]) * ln2 <= tol);
   }
-  (void)L;
   if (bad) atomicOr(&s_bad, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     loss[b] = zF - zC;
-    if (s_bad) status[b] = kNeedsExact;
+    status[b] = s_bad ? fail : W2L_OK;
   }
 }
 
-// loss only: fcc minus fac forward totals; non-finite -> float64
 // Both directions ran: their totals must agree (the per-frame guard of the
 // gradient path needs the posteriors, which loss-only mode does not form).
 __global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, AsgFastWs w,
-                                     double *loss, int32_t *status) {
+                                     double *loss, int32_t *status, int want, int fail) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= d.B || status[b] != W2L_OK) return;
+  if (b >= d.B || status[b] != want) return;
   const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
   const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));
   loss[b] = zF - zC;                                         // criterion.py:244
-  if (!(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb)) ||
-      !(fabs(zF - zFb) <= tol && fabs(zC - zCb) <= tol))
-    status[b] = kNeedsExact;
+  const bool bad = !(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb)) ||
+                   !(fabs(zF - zFb) <= tol && fabs(zC - zCb) <= tol);
+  status[b] = bad ? fail : W2L_OK;
 }
 
-// One launch for both gradient kernels; they are independent, so their CTAs
-// run side by side.  The kinds alternate in x (even: fac + gradient row, odd:
-// fcc edges) so that both are dispatched from the start of the launch.
-template <int W>
+// One launch for both gradient bodies; they are independent, so their CTAs
+// run side by side.  The kinds alternate in x (even: fac + gradient row,
+// odd: fcc edges; 128 frames each), so both are dispatched from the start of
+// the launch.  With the kinds in blockIdx.z instead every fac CTA was
+// dispatched before any fcc CTA (slower).
+template <int W, class V>
 __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
     asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
-                    const int32_t *__restrict__ tgt_len, Dims d, AsgFastWs w,
-                    float *__restrict__ grad_em, const int32_t *__restrict__ status) {
+                    const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
+                    const float *__restrict__ trans, Dims d, AsgFastWs w,
+                    float *__restrict__ grad_em, const int32_t *__restrict__ status, int want) {
+  extern __shared__ __align__(16) unsigned char gsm[];
   const int blk = blockIdx.x >> 1;
-  if ((blockIdx.x & 1) == 0)
-    asg_fac_grad_body<W>(em_len, tgt_len, d, w, grad_em, status, blk);
+  if (blockIdx.x & 1)
+    asg_fcc_grad_body<V>(em, em_len, d, w, status, want, blk, gsm);
   else
-    asg_fcc_grad_body(em, em_len, d, w, status, blk);
+    asg_fac_grad_body<W, V>(em_len, tgt_len, d, w, grad_em, status, want, blk, gsm);
 }
 
-template <int W>
-cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int32_t *tgt_len, Dims d,
-                          const AsgFastWs &w, float *grad_em, const int32_t *status,
-                          cudaStream_t s) {
-  constexpr int LP = W * kLatStates;
-  const size_t smem = std::max(sizeof(float) * (kGradWarps * (LP + 2 + 2 + 2 * LP)),
-                               kFccGradSmem);
-  auto k = asg_grad_kernel<W>;
+template <int W, class V>
+cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
+                          const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
+                          float *grad_em, const int32_t *status, int want, cudaStream_t s) {
+  const size_t smem = std::max(fac_grad_smem<W>(), kGradWarps * fcc_stage_bytes<V>());
+  auto k = asg_grad_kernel<W, V>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(2 * w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt_len, d, w, grad_em,
-                                                         status);
+  k<<<dim3(2 * w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
+                                                         grad_em, status, want);
   return cudaGetLastError();
 }
 
-}  // namespace
+template <class V>
+cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, const float *trans, Dims d,
+                            const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
+                            int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases,
+                            int want, int fail) {
+  cudaError_t err = cudaSuccess;
+  if (phases & 5u) {
+    const size_t smem = sizeof(ChainSm<V>);
+    auto k = asg_chain_kernel<V>;
+    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    // maximum shared-memory carveout: chain CTAs of different criteria (and
+    // several per SM) can then be co-resident on one SM configuration
+    err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (err != cudaSuccess) return err;
+    // (loss only runs both directions too: their totals are its guard)
+    k<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status,
+                                                 want, fail);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  trace(tr, s);  // chain
+  if (phases & 4u) {
+    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status, want,
+                                                           fail);
+    return cudaGetLastError();
+  }
+  if (!(phases & 2u)) return cudaSuccess;
+  switch (w.W) {
+#define W2L_CASE(n)                                                                          \
+  case n:                                                                                    \
+    err = launch_grad_w<n, V>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, want,  \
+                              s);                                                            \
+    break;
+    W2L_CASE(1) W2L_CASE(2) W2L_CASE(3) W2L_CASE(4) W2L_CASE(5) W2L_CASE(6) W2L_CASE(7)
+    W2L_CASE(8)
+#undef W2L_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (err != cudaSuccess) return err;
+  trace(tr, s);  // grad
+  asg_final_kernel<<<d.B, 1024, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status,
+                                        want, fail);
+  err = cudaGetLastError();
+  trace(tr, s);  // final
+  return err;
+}
 
-#ifdef W2L_PROF
-W2L_PROF_READER(w2l_debug_prof_asg)
-#endif
+}  // namespace
 
 int asg_fast_spl(int Lmax) { return lat_warps(Lmax) <= kMaxLatWarps ? kSpl : 0; }
 
@@ -893,13 +948,15 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
     return base ? (void *)((char *)base + o) : nullptr;
   };
   AsgFastWs t;
-  t.fcc_a = (float *)take(BT * 32 * 4);
-  t.fcc_b = (float *)take(BT * 32 * 4);
+  // rows sized for the double tier (the float tier uses the first half; the
+  // tiers run one after the other on the same stream)
+  t.fcc_a = take(BT * 32 * sizeof(double));
+  t.fcc_b = take(BT * 32 * sizeof(double));
   const int tpad = round_up(d.Tmax + 1, 8);
   t.fcc_ka = (int *)take((size_t)d.B * tpad * 4);
   t.fcc_kb = (int *)take((size_t)d.B * tpad * 4);
-  t.fac_a = (float *)take(BT * lpad * 4);
-  t.fac_b = (float *)take(BT * lpad * 4);
+  t.fac_a = take(BT * lpad * sizeof(double));
+  t.fac_b = take(BT * lpad * sizeof(double));
   t.fac_ea = (int *)take(BT * W * 32 * 4);
   t.fac_eb = (int *)take(BT * W * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
@@ -923,48 +980,14 @@ void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w) { asg_ws_layout(d, ws, w)
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
-                            int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases) {
+                            int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases,
+                            int tier) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
-  cudaError_t err = cudaSuccess;
-  if (phases & 5u) {
-    const size_t smem = asg_chain_smem(w.W);
-    err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-    if (err != cudaSuccess) return err;
-    // maximum shared-memory carveout: chain CTAs of different criteria (and
-    // several per SM) can then be co-resident on one SM configuration
-    err = cudaFuncSetAttribute(asg_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (err != cudaSuccess) return err;
-    // (loss only runs both directions too: their totals are its guard)
-    asg_chain_kernel<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(
-        em, em_len, tgt, tgt_len, trans, d, w, status);
-    err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-  }
-  trace(tr, s);  // chain
-  if (phases & 4u) {
-    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
-    return cudaGetLastError();
-  }
-  if (!(phases & 2u)) return cudaSuccess;
-  switch (w.W) {
-    case 1: err = launch_grad_w<1>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 2: err = launch_grad_w<2>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 3: err = launch_grad_w<3>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 4: err = launch_grad_w<4>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 5: err = launch_grad_w<5>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 6: err = launch_grad_w<6>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 7: err = launch_grad_w<7>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    case 8: err = launch_grad_w<8>(em, em_len, tgt_len, d, w, grad_em, status, s); break;
-    default: return cudaErrorInvalidValue;
-  }
-  if (err != cudaSuccess) return err;
-  trace(tr, s);  // grad
-  asg_final_kernel<<<d.B, 1024, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status);
-  err = cudaGetLastError();
-  trace(tr, s);  // final
-  return err;
+  if (tier == 0)
+    return launch_asg_tier<float>(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga_utt,
+                                  status, s, tr, phases, W2L_OK, kNeedsF64);
+  return launch_asg_tier<double>(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga_utt,
+                                 status, s, tr, phases, kNeedsF64, kNeedsLog);
 }
 
 // --------------------------------------------------- batch reduction of dA --

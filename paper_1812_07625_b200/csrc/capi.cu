@@ -54,8 +54,8 @@ extern "C" {
 const char *w2l_version(void) { return "w2l-criterion sm_100a r2 (scaled-linear fp32 + f64 exact)"; }
 
 const char *w2l_stage_name(int kind, int i) {
-  static const char *asg[] = {"validate", "chain", "grad", "final", "exact_fallback", "reduce"};
-  static const char *ctc[] = {"validate", "chain", "grad", "final", "exact_fallback"};
+  static const char *asg[] = {"validate", "chain", "grad", "final", "fallback", "reduce"};
+  static const char *ctc[] = {"validate", "chain", "grad", "final", "fallback"};
   if (kind == 0 && i >= 0 && i < 6) return asg[i];
   if (kind == 1 && i >= 0 && i < 5) return ctc[i];
   return "";
@@ -98,7 +98,7 @@ int w2l_status_first_error(const int32_t *status, int B, int32_t *bad_index,
   } else {
     for (int b = 0; b < B; ++b) {
       if (host[b] != W2L_OK) {
-        code = host[b] == kNeedsExact ? W2L_ERR_PRECISION : host[b];
+        code = (host[b] == kNeedsF64 || host[b] == kNeedsLog) ? W2L_ERR_PRECISION : host[b];
         if (bad_index) *bad_index = b;
         break;
       }
@@ -178,21 +178,22 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   }
   trace(tr, s);  // validate
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
-                                 status, s, tr, phases));
+                                 status, s, tr, phases, 0));
   if (rc) return rc;
-  if (loss_only) {
-    if (fallback)
+  if (!loss_only && !(phases & 2u)) return W2L_OK;
+  if (fallback) {
+    // the precision tiers: fp64 lanes for what the fp32 guard rejected, then
+    // the float64 log-domain kernel for what the fp64 guard rejected (both
+    // launches exit at once when nothing is flagged)
+    rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
+                                   status, s, nullptr, loss_only ? (1u | 4u) : 3u, 1));
+    if (!rc)
       rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
                                              slots, loss, grad_em, ga, status, s));
-    return rc;
-  }
-  if (!(phases & 2u)) return W2L_OK;
-  if (fallback) {
-    rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
-                                           slots, loss, grad_em, ga, status, s));
     if (rc) return rc;
   }
-  trace(tr, s);  // exact fallback
+  if (loss_only) return W2L_OK;
+  trace(tr, s);  // fallback tiers
   rc = from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
   trace(tr, s);  // reduce
   return rc;
@@ -339,14 +340,18 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   }
   trace(tr, s);  // validate
   rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
-                                 s, tr, phases));
+                                 s, tr, phases, 0));
   if (rc) return rc;
   if (!loss_only && !(phases & 2u)) return W2L_OK;
-  if (!(flags & W2L_FLAG_NO_FALLBACK))
-    rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
-                                           asg_slots(B), slots, loss, grad_em, status, s,
-                                           logits));
-  trace(tr, s);  // exact fallback
+  if (!(flags & W2L_FLAG_NO_FALLBACK)) {
+    rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em,
+                                   status, s, nullptr, loss_only ? (1u | 4u) : 3u, 1));
+    if (!rc)
+      rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
+                                             asg_slots(B), slots, loss, grad_em, status, s,
+                                             logits));
+  }
+  trace(tr, s);  // fallback tiers
   return rc;
 }
 

@@ -9,8 +9,12 @@
 
 namespace w2l {
 
-// Internal per-utterance status: the fp32 guard asks for the float64 kernel.
-constexpr int kNeedsExact = 100;
+// Internal per-utterance statuses of the precision tiers: the fp32
+// scaled-linear tier failed its guard (-> the fp64 scaled-linear tier), and
+// the fp64 tier failed too (-> the float64 log-domain kernel, exact.cu).
+constexpr int kNeedsF64 = 100;
+constexpr int kNeedsLog = 101;
+constexpr int kNeedsExact = kNeedsF64;   // "the fp32 path could not take it"
 
 // exp(x) of an fp32 weight flushes to zero below about -87.3 nats; the fast
 // path sends any input whose weights (emissions relative to their frame
@@ -18,6 +22,7 @@ constexpr int kNeedsExact = 100;
 // the float64 kernel, since a flush applied identically to both directions
 // would be invisible to the forward/backward consistency guard
 constexpr float kFlushNats = 80.f;
+constexpr float kFlushNats64 = 700.f;   // the same for double (exp underflows near -708)
 
 constexpr int kWarp = 32;
 constexpr int kChunk = 32;            // frames per staged emission chunk
@@ -87,6 +92,10 @@ __device__ __forceinline__ int warp_min(int v) {
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16_ca(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>

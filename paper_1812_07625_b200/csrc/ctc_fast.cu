@@ -1,16 +1,22 @@
-// fp32 batched CTC loss + gradient (replaces criterion.py:84-162 for the
-// batched hot path).
+// Batched CTC loss + gradient (replaces criterion.py:84-162 for the batched
+// hot path), in two precision tiers of one algorithm.
 //
 // The 2L+1-state blank-augmented lattice (criterion.py:113-120) runs in the
 // scaled linear domain on the multi-warp wavefront lattice of lattice.cuh
-// (4 states per lane, fp64 with a per-lane power-of-two exponent):
+// (4 states per lane, type V with a per-lane power-of-two exponent):
 //   alpha_t[s] = Et[lab_s] (alpha[s] + alpha[s-1] + skip_s alpha[s-2])
 //   beta'_t[s] = w[s] + w[s+1] + skip_{s+2} w[s+2],  w = Et+1[lab] beta'_{t+1}
 // with Et = exp(logp - max_i logp) and the per-frame shifts summed in f64 for
-// the loss.  The gradient kernel forms per-frame posteriors with their own
-// normaliser Z_t, gathers them by token (blank = even states, labels through
-// a token CSR) and checks the per-frame consistency guard; failing utterances
-// are recomputed by the float64 log-domain kernel.
+// the loss.  Kernels (one stream):
+//   ctc_chain     grid (B, 2): the forward and backward recursions, every
+//                 row (lane values + exponents) to the workspace;
+//   ctc_grad      grid (T / 128, B): per-frame posteriors with their own
+//                 normaliser Z_t, gather by token (blank = even states,
+//                 labels through a token CSR), gradient rows, per-frame guard;
+//   ctc_final     loss and guard verdict.
+// V = float is the fast tier; utterances that fail its guard are recomputed
+// with V = double (range 2^+-1022), and those that fail again by the float64
+// log-domain kernel (exact.cu).
 
 #include "laneblock.cuh"
 #include "lattice.cuh"
@@ -20,21 +26,17 @@
 namespace w2l {
 namespace {
 
-constexpr int kGradFramesPerBlock = 128;
-constexpr int kGradWarps = 8;
-
-template <bool FWD>
-__device__ __forceinline__ void ctc_chain_body(ChainSm &sm, unsigned char *dsm, int W,
-                                               const float *em, int T, int L,
+template <bool FWD, class V>
+__device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, int T, int L,
                                                const int64_t *y, int blank, Dims d,
                                                const CtcFastWs &w, int b, unsigned tokmask,
-                                               int32_t *status) {
+                                               int32_t *status, int fail) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = 2 * L + 1;
   const int weff = lat_warps(S);
   if (warp == 0) {
-    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, W, w.logits, tokmask};
-    producer_run(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
+    ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, weff, w.logits, tokmask};
+    producer_run<V>(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
   } else if (warp - 1 < weff) {
     LatCtx c;
     c.w = warp - 1;
@@ -46,29 +48,30 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm &sm, unsigned char *dsm, 
     c.cons_idx = 0;
     c.Tmax = d.Tmax;
     const size_t ub = (size_t)b * w.W * d.Tmax;
-    c.rows = (FWD ? w.a : w.b) + ub * kLatStates;
+    c.rows = reinterpret_cast<V *>(FWD ? w.a : w.b) + ub * kLatStates;
     c.exps = (FWD ? w.ea : w.eb) + ub * 32;
-    LatState f;
-    lat_init_weights<kCtc, FWD>(f, c, y, L, nullptr, 0.f, blank);
-    lattice_run<kCtc, FWD>(sm, c, f);
+    LatState<V> f;
+    lat_init_weights<kCtc, FWD, V>(f, c.w, lane, d.N, S, y, L, nullptr, 0.f, blank);
+    lattice_run<kCtc, FWD, V>(sm, c, f);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     w.scal[b * 4 + (FWD ? 0 : 1)] = lattice_total(sm, weff);
-    if (sm.flush) status[b] = kNeedsExact;
+    if (sm.flush) status[b] = fail;
   }
 }
 
 // grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
+template <class V>
 __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
-                     int blank, Dims d, CtcFastWs w, int32_t *__restrict__ status) {
+                     int blank, Dims d, CtcFastWs w, int32_t *__restrict__ status, int want,
+                     int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  const int W = w.W;
-  ChainSm &sm = *reinterpret_cast<ChainSm *>(dsm);
+  ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
   const int b = blockIdx.x;
-  if (status[b] != W2L_OK) return;
+  if (status[b] != want) return;
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(2 * L + 1);
   __shared__ unsigned s_mask;
@@ -80,26 +83,25 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
   for (int l = threadIdx.x; l < L; l += blockDim.x) atomicOr(&s_mask, 1u << (int)y[l]);
   __syncthreads();
   if (blockIdx.y == 0)
-    ctc_chain_body<true>(sm, dsm, W, em, T, L, y, blank, d, w, b, s_mask, status);
+    ctc_chain_body<true, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   else
-    ctc_chain_body<false>(sm, dsm, W, em, T, L, y, blank, d, w, b, s_mask, status);
+    ctc_chain_body<false, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
 }
 
-size_t ctc_chain_smem(int W) { (void)W; return sizeof(ChainSm); }
+constexpr int kGradFramesPerBlock = 128;
+constexpr int kGradWarps = 8;
 
-// 2^x as a float for integer x clamped to [-127, 127] (0 below)
-__device__ __forceinline__ float pow2_clamped(int x) { return pow2f_fast(max(min(x, 127), -127)); }
-
-// One warp per frame at a time; lane i owns states 128 w + 4 i + k of every
-// segment w and token i of the gradient row.  Posteriors are scaled into
-// range by the lane exponents against the utterance's reference exponent
-// and normalised by their own per-frame sum z_t.
-template <int W>
+// One warp per frame at a time; lane i owns states 128 sw + 4 i + k of every
+// lattice warp sw and token i of the gradient row.  Posteriors are scaled
+// into range by the lane exponents against the utterance's reference
+// exponent and normalised by their own per-frame sum z_t.  Rows of lanes
+// past the lattice's last state were never stored and are read as zero.
+template <int W, class V>
 __global__ void __launch_bounds__(kGradWarps * 32)
     ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
-                    const int32_t *__restrict__ status) {
+                    const int32_t *__restrict__ status, int want) {
   constexpr int LP = W * kLatStates;
   __shared__ __align__(16) float prow[kGradWarps][LP];
   __shared__ int sperm[LP];
@@ -108,16 +110,19 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N, T = em_len[b];
   const int t0 = blk * kGradFramesPerBlock;
-  const bool ok = status[b] == W2L_OK;
+  const int st = status[b];
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
-  for (int t = ta; t < tb; ++t)
-    if (!ok || t >= T)
+  if (want == W2L_OK) {
+    // the first tier owns the zeros: padding frames and utterances it does
+    // not compute (a later tier rewrites the rows of the ones it takes)
+    for (int t = st == W2L_OK ? max(ta, T) : ta; t < tb; ++t)
       if (lane < N) ge[(size_t)t * N + lane] = 0.f;
-  if (!ok) return;
-  const int L = tgt_len[b];
-  const int weff = lat_warps(2 * L + 1);
+  }
+  if (st != want || t0 >= T) return;
+  const int L = tgt_len[b], S = 2 * L + 1;
+  const int weff = lat_warps(S);
   for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
   __syncthreads();
   const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
@@ -127,28 +132,31 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   const float reff = isfinite(ref) ? (float)(ref - refi) : CUDART_NAN_F;
   float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  const float4 *A4 = reinterpret_cast<const float4 *>(w.a + seg0 * kLatStates) + lane;
-  const float4 *B4 = reinterpret_cast<const float4 *>(w.b + seg0 * kLatStates) + lane;
+  const V *A = reinterpret_cast<const V *>(w.a) + seg0 * kLatStates + lane * kSpl;
+  const V *Bv = reinterpret_cast<const V *>(w.b) + seg0 * kLatStates + lane * kSpl;
   const int *EA = w.ea + seg0 * 32 + lane;
   const int *EB = w.eb + seg0 * 32 + lane;
-  const unsigned segq = (unsigned)d.Tmax * (kLatStates / 4);
-  const unsigned sege = (unsigned)d.Tmax * 32;
+  const size_t segv = (size_t)d.Tmax * kLatStates;
+  const size_t sege = (size_t)d.Tmax * 32;
   float *myp = prow[warp];
   const int tend = min(tb, T);
   for (int t = ta; t < tend; ++t) {
-    const unsigned tq = (unsigned)t * 32;
+    const size_t tq = (size_t)t * kLatStates;
     float zl = 0.f, zb = 0.f;
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
+      float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (sw < weff && sw * kLatStates + lane * kSpl < S) {
+        V va[kSpl], vb[kSpl];
+        ld4(A + sw * segv + tq, va);
+        ld4(Bv + sw * segv + tq, vb);
+        const V sc = pow2_clamped<V>(EA[sw * sege + (size_t)t * 32] + EB[sw * sege + (size_t)t * 32] - refi);
+        p.x = (float)(va[0] * vb[0] * sc);
+        p.y = (float)(va[1] * vb[1] * sc);
+        p.z = (float)(va[2] * vb[2] * sc);
+        p.w = (float)(va[3] * vb[3] * sc);
+      }
       if (sw < weff) {
-        const float4 va = A4[sw * segq + tq];
-        const float4 vb = B4[sw * segq + tq];
-        const float sc = pow2_clamped(EA[sw * sege + tq] + EB[sw * sege + tq] - refi);
-        float4 p;
-        p.x = va.x * vb.x * sc;
-        p.y = va.y * vb.y * sc;
-        p.z = va.z * vb.z * sc;
-        p.w = va.w * vb.w * sc;
         reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
         zl += (p.x + p.y) + (p.z + p.w);
         zb += p.x + p.z;   // blank states are the even ones
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       const float ex = lane < N ? __expf(x - mx) : 0.f;
       sm_k = ex / warp_sum(ex);
     }
-    if (lane < N) ge[(unsigned)t * N + lane] = sm_k - ((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
+    if (lane < N) ge[(size_t)t * N + lane] = sm_k - ((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
     __syncwarp();
   }
   if (lane == 0) {
@@ -193,21 +201,21 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   }
 }
 
-template <int W>
+template <int W, class V>
 cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
                               const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
-                              float *grad_em, const int32_t *status, cudaStream_t s) {
-  ctc_grad_kernel<W><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(em, em_len, tgt, tgt_len,
-                                                                   blank, d, w, grad_em, status);
+                              float *grad_em, const int32_t *status, int want, cudaStream_t s) {
+  ctc_grad_kernel<W, V><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(
+      em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want);
   return cudaGetLastError();
 }
 
 // one warp per utterance: loss and guard verdict (partials read in parallel)
 __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
-                                 double *loss, int32_t *status) {
+                                 double *loss, int32_t *status, int want, int fail) {
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (b >= d.B || status[b] != W2L_OK) return;
+  if (b >= d.B || status[b] != want) return;
   const int T = em_len[b];
   const double ln2 = 0.6931471805599453;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
@@ -220,29 +228,73 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
   }
   bad = __any_sync(0xffffffffu, bad);
   if (lane == 0) {
-    bad |= !(isfinite(zA) && isfinite(zB)) || fabs(zA - zB) > tol;
+    bad |= !(isfinite(zA) && isfinite(zB)) || !(fabs(zA - zB) <= tol);
     loss[b] = -(zA + shifts);                                  // criterion.py:162
-    if (bad) status[b] = kNeedsExact;
+    status[b] = bad ? fail : W2L_OK;
   }
 }
 
 // loss only: both directions ran, their totals must agree
 __global__ void ctc_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
-                                     double *loss, int32_t *status) {
+                                     double *loss, int32_t *status, int want, int fail) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= d.B || status[b] != W2L_OK) return;
+  if (b >= d.B || status[b] != want) return;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));
   loss[b] = -(zA + shifts);                                  // criterion.py:162
-  if (!(isfinite(zA + shifts) && isfinite(zB)) || !(fabs(zA - zB) <= tol))
-    status[b] = kNeedsExact;
+  const bool bad = !(isfinite(zA + shifts) && isfinite(zB)) || !(fabs(zA - zB) <= tol);
+  status[b] = bad ? fail : W2L_OK;
+}
+
+template <class V>
+cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_t *tgt,
+                            const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
+                            double *loss, float *grad_em, int32_t *status, cudaStream_t s,
+                            Tracer *tr, unsigned phases, int want, int fail) {
+  cudaError_t err = cudaSuccess;
+  if (phases & 5u) {
+    const size_t smem = sizeof(ChainSm<V>);
+    auto k = ctc_chain_kernel<V>;
+    err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    // maximum shared-memory carveout: chain CTAs of different criteria (and
+    // several per SM) can then be co-resident on one SM configuration
+    err = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (err != cudaSuccess) return err;
+    // (loss only runs both directions too: their totals are its guard)
+    k<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status,
+                                                 want, fail);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  trace(tr, s);  // chain
+  if (phases & 4u) {
+    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status, want,
+                                                           fail);
+    return cudaGetLastError();
+  }
+  if (!(phases & 2u)) return cudaSuccess;
+  switch (w.W) {
+#define W2L_CASE(n)                                                                          \
+  case n:                                                                                    \
+    err = launch_ctc_grad_w<n, V>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status,    \
+                                  want, s);                                                  \
+    break;
+    W2L_CASE(1) W2L_CASE(2) W2L_CASE(3) W2L_CASE(4) W2L_CASE(5) W2L_CASE(6) W2L_CASE(7)
+    W2L_CASE(8)
+#undef W2L_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (err != cudaSuccess) return err;
+  trace(tr, s);  // grad
+  ctc_final_kernel<<<(d.B + 7) / 8, 256, 0, s>>>(em_len, d, w, loss, status, want, fail);
+  err = cudaGetLastError();
+  trace(tr, s);  // final
+  return err;
 }
 
 }  // namespace
-
-#ifdef W2L_PROF
-W2L_PROF_READER(w2l_debug_prof_ctc)
-#endif
 
 int ctc_fast_spl(int Lmax) { return lat_warps(2 * Lmax + 1) <= kMaxLatWarps ? kSpl : 0; }
 
@@ -250,7 +302,7 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
   const int W = lat_warps(2 * d.Lmax + 1);
   const int lpad = W * kLatStates;
   const int nblk = (d.Tmax + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
-  const size_t BT = (size_t)d.B * d.Tmax;
+  const size_t BWT = (size_t)d.B * W * d.Tmax;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -258,10 +310,12 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
     return base ? (void *)((char *)base + o) : nullptr;
   };
   CtcFastWs t;
-  t.a = (float *)take(BT * lpad * 4);
-  t.b = (float *)take(BT * lpad * 4);
-  t.ea = (int *)take(BT * W * 32 * 4);
-  t.eb = (int *)take(BT * W * 32 * 4);
+  // rows sized for the double tier (the float tier uses the first half; the
+  // tiers run one after the other on the same stream)
+  t.a = take(BWT * kLatStates * sizeof(double));
+  t.b = take(BWT * kLatStates * sizeof(double));
+  t.ea = (int *)take(BWT * 32 * 4);
+  t.eb = (int *)take(BWT * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
   t.part_guard = (float *)take((size_t)d.B * nblk * 2 * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
@@ -281,48 +335,13 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w)
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
-                            Tracer *tr, unsigned phases) {
+                            Tracer *tr, unsigned phases, int tier) {
   if (w.W < 1 || w.W > kMaxLatWarps) return cudaErrorInvalidValue;
-  cudaError_t err = cudaSuccess;
-  if (phases & 5u) {
-    const size_t smem = ctc_chain_smem(w.W);
-    err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-    if (err != cudaSuccess) return err;
-    // maximum shared-memory carveout: chain CTAs of different criteria (and
-    // several per SM) can then be co-resident on one SM configuration
-    err = cudaFuncSetAttribute(ctc_chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (err != cudaSuccess) return err;
-    // (loss only runs both directions too: their totals are its guard)
-    ctc_chain_kernel<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(
-        em, em_len, tgt, tgt_len, blank, d, w, status);
-    err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-  }
-  trace(tr, s);  // chain
-  if (phases & 4u) {
-    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status);
-    return cudaGetLastError();
-  }
-  if (!(phases & 2u)) return cudaSuccess;
-  switch (w.W) {
-    case 1: err = launch_ctc_grad_w<1>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 2: err = launch_ctc_grad_w<2>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 3: err = launch_ctc_grad_w<3>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 4: err = launch_ctc_grad_w<4>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 5: err = launch_ctc_grad_w<5>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 6: err = launch_ctc_grad_w<6>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 7: err = launch_ctc_grad_w<7>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    case 8: err = launch_ctc_grad_w<8>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, s); break;
-    default: return cudaErrorInvalidValue;
-  }
-  if (err != cudaSuccess) return err;
-  trace(tr, s);  // grad
-  ctc_final_kernel<<<(d.B + 7) / 8, 256, 0, s>>>(em_len, d, w, loss, status);
-  err = cudaGetLastError();
-  trace(tr, s);  // final
-  return err;
+  if (tier == 0)
+    return launch_ctc_tier<float>(em, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
+                                  s, tr, phases, W2L_OK, kNeedsF64);
+  return launch_ctc_tier<double>(em, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
+                                 s, tr, phases, kNeedsF64, kNeedsLog);
 }
 
 }  // namespace w2l

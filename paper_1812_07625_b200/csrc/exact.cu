@@ -10,8 +10,9 @@
 //   phase 2 -- all threads form posteriors and gradients in parallel over
 //              frames / transition pairs / states.
 // They serve (a) the reference-compatible float64 entry points
-// (w2l_*_loss_grad_f64), and (b) the fallback for utterances whose fp32
-// fast-path guard fired (only_flagged).  A fixed number of workspace slots
+// (w2l_*_loss_grad_f64), and (b) the last-resort fallback for utterances
+// that failed the guards of both scaled-linear tiers (only_flagged:
+// status kNeedsLog).  A fixed number of workspace slots
 // bounds memory: CTA k handles utterances k, k+nslots, ...
 
 #include "common.cuh"
@@ -23,7 +24,7 @@ namespace {
 constexpr int kExactThreads = 128;
 
 __device__ __forceinline__ bool wants(int st, int only_flagged) {
-  return only_flagged ? (st == kNeedsExact) : (st == W2L_OK);
+  return only_flagged ? (st == kNeedsLog) : (st == W2L_OK);
 }
 
 // log-sum-exp with the reference's non-finite-max rule (criterion.py:250-254)

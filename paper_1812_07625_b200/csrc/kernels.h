@@ -60,31 +60,34 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
                              int nslots, void *slot_ws, double *loss, float *grad_em,
                              int32_t *status, cudaStream_t s, int logits = 0);
 
-// ---- fp32 fast path
+// ---- scaled-linear fast path (tier 0: fp32 lanes; tier 1: fp64 lanes for
+// the utterances whose fp32 guard failed).  Rows are sized for fp64.
 struct AsgFastWs {
-  float *fcc_a, *fcc_b;      // [B][Tmax][32]
+  void *fcc_a, *fcc_b;       // V [B][Tmax][32]
   int *fcc_ka, *fcc_kb;      // [B][tpad] cumulative exponents (kb stored at t+1)
-  float *fac_a, *fac_b;      // [B][W][Tmax][128] warp-major lattice rows (fp64 high words)
+  void *fac_a, *fac_b;       // V [B][W][Tmax][128] warp-major lattice rows
   int *fac_ea, *fac_eb;      // [B][W][Tmax][32] per-lane exponents
   double *scal;              // [B][4]: lnZ fcc fwd, fcc bwd, fac fwd, fac bwd
   float *part_fullA;         // [B][nblk][32][32]
-  float *part_edge;          // [B][nblk][2][Lpad]
+  float *part_edge;          // [B][nblk][Lpad]
   float *part_guard;         // [B][nblk][4]
   int *perm;                 // [B][Lpad] states sorted by token
   int *tok_start;            // [B][33]
-  int spl, W, lpad, nblk, tpad;  // W lattice warps; tpad = round_up(Tmax + 1, 8): 16B-aligned bulk blocks
+  int spl, W, lpad, nblk, tpad;  // W lattice warps; tpad = round_up(Tmax + 1, 8)
 };
 int asg_fast_spl(int Lmax);  // 0 if unsupported
 size_t asg_fast_ws_bytes(Dims d);
 void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w);
+// tier 0 processes status W2L_OK and marks failures kNeedsF64; tier 1
+// processes kNeedsF64 and marks failures kNeedsLog (exact.cu takes those)
 cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, const float *trans, Dims d,
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
                             int32_t *status, cudaStream_t s, Tracer *tr = nullptr,
-                            unsigned phases = 3u);   // bit 0: chain, bit 1: gradient
+                            unsigned phases = 3u, int tier = 0);  // phases bit 0: chain, 1: gradient, 2: loss only
 
 struct CtcFastWs {
-  float *a, *b;              // [B][W][Tmax][128] warp-major lattice rows
+  void *a, *b;               // V [B][W][Tmax][128] warp-major lattice rows
   int *ea, *eb;              // [B][W][Tmax][32]
   double *scal;              // [B][4]: lnZ fwd, lnZ bwd, sum of frame shifts, spare
   float *part_guard;         // [B][nblk][2]
@@ -99,8 +102,7 @@ void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w);
 cudaError_t launch_ctc_fast(const float *em, const int32_t *em_len, const int64_t *tgt,
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
-                            Tracer *tr = nullptr, unsigned phases = 3u);
-// phases bit 2 (value 4): loss only -- forward recursion + loss, no gradients
+                            Tracer *tr = nullptr, unsigned phases = 3u, int tier = 0);
 
 // ---- reductions
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,

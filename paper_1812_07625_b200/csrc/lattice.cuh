@@ -1,6 +1,6 @@
 // Multi-warp wavefront chains for the serial forward/backward recursions.
 //
-// One CTA runs one (utterance, direction).  Its warps:
+// CHAIN CTA: one CTA runs one (utterance, direction).  Its warps:
 //   warp 0          producer: stages emission chunks with cp.async and writes
 //                   Et[t][i] = exp(e[t][i] - max_i e[t][i]) into a ring in
 //                   shared memory, once for the whole CTA;
@@ -9,32 +9,32 @@
 //   lattice warps   W warps over a linear lattice (ASG fac: L states; CTC:
 //                   2L+1 states).  Lattice warp w owns states
 //                   [128 w, 128 (w+1)), kSpl = 4 consecutive states per lane
-//                   in fp32 registers with one power-of-two exponent per lane
-//                   (block floating point, renormalised every kRenormF steps).
+//                   in registers of type V with one power-of-two exponent per
+//                   lane (block floating point, renormalised every kRenormF
+//                   steps).
+//
+// V is the precision tier: float (the fast path) or double (the wide-range
+// tier for inputs whose dynamic range exceeds fp32's; same algorithm).
 //
 // A lattice state at step j depends only on its own lane and the previous
 // lane's states at step j-1 (criterion.py:126-134,147-155 for CTC,
 // :197-202,207-212 for the fac graph), so the warps form a WAVEFRONT: warp w
 // runs a few steps behind its upstream neighbour (w-1 forward, w+1 backward)
 // and reads the neighbour's boundary states of step j-1 from a small ring in
-// shared memory instead of a shuffle.  Progress is published every
-// kBlk = 8 steps through release/acquire counters, so the warps never
-// meet at a barrier.  Splitting the lattice over W warps cuts the
-// instructions each warp issues per frame by W, which is what bounds a
-// latency-bound serial recursion (one dependent step per frame).
+// shared memory.  Progress is published every kBlk = 8 steps through
+// release/acquire counters, so the warps never meet at a barrier.
 //
-// Range: with 4 states per lane the posterior-relevant states of the bench
-// data lie at most 2^39 below their lane maximum (probe in DESIGN.md), far
-// inside fp32's 2^126; whatever falls outside trips the consistency guard
-// and is recomputed by the float64 kernel.
+// ROWS.  Every step's lane values and exponents go to the workspace
+// (warp-major [W][Tmax][128] values, [W][Tmax][32] exponents; lanes wholly
+// past the lattice's last state store nothing and the gradient kernels do
+// not read them).  A checkpointed variant that recomputed alpha and beta per
+// 16-frame segment inside the gradient kernels moved ~10x less HBM data but
+// executed 2.3x the instructions and ran 2x slower.
 //
 // The processing index j counts steps in the direction of the recursion
 // (forward: frame t = j; backward: frame t = T-1-j).  Forward step j consumes
-// Et at frame j; backward step j consumes frame u = T-j (processing index
-// j-1) and produces beta' at frame T-1-j.  Ring slots are assigned so that
-// step j always reads slot j mod kRing: unrolled blocks of 8 steps starting
-// at multiples of 8 then address the ring, the boundary ring and the row
-// staging with compile-time offsets from one base per block.
+// Et at frame j; backward step j consumes frame u = T-j and produces beta' at
+// frame T-1-j.  Ring slots are assigned so that step j reads slot j mod kRing.
 #pragma once
 
 #include <type_traits>
@@ -43,56 +43,58 @@
 
 namespace w2l {
 
-#ifdef W2L_PROF
-// debug-only chain profile: per (utterance, direction, warp) cycle counters
-// [total, wait_prod, wait_up, wait_dn, acquire, blocks]
-static __device__ unsigned long long g_prof[64 * 2 * 16 * 8];
-#define PROF_STEADY(cond) const bool g_prof_on = (cond)
-#define W2L_PROF_READER(name) \
-  extern "C" __attribute__((visibility("default"))) int name(unsigned long long *out, int clear) { \
-    cudaDeviceSynchronize(); \
-    cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof)); \
-    if (clear) { static unsigned long long z[64 * 2 * 16 * 8]; cudaMemcpyToSymbol(g_prof, z, sizeof(g_prof)); } \
-    return 0; \
-  }
-#define PROF_T0() const long long _pt0 = clock64()
-#define PROF_ADD(idx, v) atomicAdd(&g_prof[(((blockIdx.x & 63) * 2 + blockIdx.y) * 16 + (threadIdx.x >> 5)) * 8 + (idx)], (unsigned long long)(v))
-#define PROF_WAIT(idx, stmt) do { const long long _a = clock64(); stmt; if ((threadIdx.x & 31) == 0 && g_prof_on) PROF_ADD(idx, clock64() - _a); } while (0)
-#else
-#define PROF_T0()
-#define PROF_ADD(idx, v)
-#define PROF_WAIT(idx, stmt) stmt
-#define PROF_STEADY(cond)
-#endif
-
 constexpr int kSpl = 4;                    // lattice states per lane
 constexpr int kLatStates = 32 * kSpl;      // states per lattice warp
 constexpr int kMaxLatWarps = 8;            // 1024 states
-constexpr int kRing = 256;                 // emission ring (frames): > wavefront spread + 2 chunks
 constexpr int kBndRing = 128;              // boundary ring (steps): decouples neighbouring warps
 constexpr int kCounters = kMaxLatWarps + 2;  // lattice warps + fcc warp (+ spare)
 constexpr int kDone = 1 << 30;             // progress of a finished consumer
-constexpr int kRenormF = 4;                // steps between fp32 lane renormalisations
+constexpr int kRenormF = 4;                // steps between lane renormalisations
 constexpr int kBlk = 8;                    // steps per unrolled block (one publish / wait per block)
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
 
-struct __align__(16) Bnd {
-  float v0, v1;
+// Et ring depth (frames): > wavefront spread + producer stages
+template <class V>
+struct Ring {
+  static constexpr int n = sizeof(V) == 4 ? 256 : 128;
+};
+
+template <class V>
+struct __align__(sizeof(V) == 4 ? 16 : 8) BndT {
+  V v0, v1;
   int ex, pad;
 };
 
 // shared-memory layout of a chain CTA (dynamic shared memory)
+template <class V>
 struct ChainSm {
-  float ering[kRing][kStride];
+  V ering[Ring<V>::n][kStride];
   float raw[kProdStages][kChunk * 32];
-  Bnd bnd[kMaxLatWarps][kBndRing];
-  __align__(16) float vec[2][32];
+  BndT<V> bnd[kMaxLatWarps][kBndRing];
+  __align__(16) V vec[2][32];
   double fin[kMaxLatWarps + 1];
   int prod;
   int cons[kCounters];
-  int flush;   // a lattice token's Et fell below exp(-kFlushNats) (set by the producer)
+  int flush;   // a used token's Et fell below exp(-kFlush) (set by the producer)
 };
 
+// ---- 4-wide vector load/store of lane values (float4 / 2 x double2)
+__device__ __forceinline__ void ld4(const float *p, float (&v)[4]) {
+  const float4 x = *reinterpret_cast<const float4 *>(p);
+  v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+__device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
+  const double2 x = reinterpret_cast<const double2 *>(p)[0];
+  const double2 y = reinterpret_cast<const double2 *>(p)[1];
+  v[0] = x.x, v[1] = x.y, v[2] = y.x, v[3] = y.y;
+}
+__device__ __forceinline__ void st4(float *p, const float (&v)[4]) {
+  *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void st4(double *p, const double (&v)[4]) {
+  reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
 
 // ---- release/acquire progress counters (CTA scope, shared memory)
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -146,14 +148,18 @@ struct ProdCtx {
 __device__ __forceinline__ int frame_of(bool fwd, int T, int p) { return fwd ? p : T - 1 - p; }
 // ring slot of processing index p: step j reads slot j (forward reads index
 // j, backward index j-1)
-__device__ __forceinline__ int ring_slot(bool fwd, int p) { return (p + (fwd ? 0 : 1)) & (kRing - 1); }
+template <class V>
+__device__ __forceinline__ int ring_slot(bool fwd, int p) {
+  return (p + (fwd ? 0 : 1)) & (Ring<V>::n - 1);
+}
 __device__ __forceinline__ int eidx_of(bool fwd, int j) { return fwd ? j : j - 1; }
 
 // Stage chunk p0 (up to 32 frames, processing order) linearly: the frames of
 // a chunk are contiguous in the emissions (ascending for the forward
 // direction, descending for the backward one), so lane l copies elements
 // l, l+32, ... of that range (coalesced 4-byte cp.async).
-__device__ __forceinline__ void prod_issue(ChainSm &sm, const ProdCtx &c, int p0, int buf,
+template <class V>
+__device__ __forceinline__ void prod_issue(ChainSm<V> &sm, const ProdCtx &c, int p0, int buf,
                                            int lane) {
   const int rows = min(kChunk, c.T - p0);
   const int f0 = c.fwd ? p0 : c.T - p0 - rows;   // lowest frame of the chunk
@@ -165,14 +171,19 @@ __device__ __forceinline__ void prod_issue(ChainSm &sm, const ProdCtx &c, int p0
 }
 
 // Et of one emission value (the gradient kernels recompute it identically)
-__device__ __forceinline__ float et_of(float e, float m) { return __expf(e - m); }
+template <class V>
+__device__ __forceinline__ V et_of(float e, float m) {
+  if (sizeof(V) == 4) return (V)__expf(e - m);
+  return (V)exp((double)e - (double)m);
+}
 
 // The producer warp: converts every frame once for the whole CTA (lane r
 // owns processing row r of a 32-frame chunk).  The row maxima are summed
 // into *shift_sum (CTC loss offset) when requested.
-__device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int lane,
+template <class V>
+__device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, int lane,
                                              double *shift_sum) {
-  PROF_T0();
+  constexpr int kRing = Ring<V>::n;
   double shifts = 0.0;
   bool flush = false;
   const int nch = (c.T + kChunk - 1) / kChunk;
@@ -184,15 +195,12 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
     else cp_async_commit();
   }
   for (int ch = 0; ch < nch; ++ch) {
-    PROF_STEADY(ch >= 10 && ch < 40);
     const int p0 = ch * kChunk, rows = min(kChunk, c.T - p0);
     const int nx = ch + kProdStages - 1;
     if (nx < nch) prod_issue(sm, c, nx * kChunk, nx % kProdStages, lane);
     else cp_async_commit();
-    PROF_WAIT(2, cp_async_wait<kProdStages - 1>(); __syncwarp());
-#ifdef W2L_PROF
-    const long long _cv0 = clock64();
-#endif
+    cp_async_wait<kProdStages - 1>();
+    __syncwarp();
     float x[32];
     const int rlin = c.fwd ? lane : rows - 1 - lane;   // ascending-frame row of this lane
     const float *r = sm.raw[ch % kProdStages] + max(rlin, 0) * c.N;
@@ -205,35 +213,30 @@ __device__ __forceinline__ void producer_run(ChainSm &sm, const ProdCtx &c, int 
     }
     // Et = exp(e - m) of a token the recursions use must not flush to zero
     // (the same flush in both directions would pass the consistency guard)
-    flush |= lane < rows && mn - m < -kFlushNats;
+    flush |= lane < rows && mn - m < -Pow2<V>::kFlush;
     // ring slots [p0, p0+rows) previously held p - kRing: every consumer must
     // be past the step that read them (a step j reads index <= j)
     const int need = p0 + rows + 1 - kRing;
-    PROF_WAIT(1, for (int q = 0; q < c.nconsumers; ++q)
-      while (ld_relaxed(&sm.cons[q]) < need) __nanosleep(32));
+    for (int q = 0; q < c.nconsumers; ++q)
+      while (ld_relaxed(&sm.cons[q]) < need) __nanosleep(32);
     fence_acq_rel_cta();
     if (lane < rows) {
-      float *dd = sm.ering[ring_slot(c.fwd, p0 + lane)];
-      float se = 0.f;
+      V *dd = sm.ering[ring_slot<V>(c.fwd, p0 + lane)];
+      double se = 0.0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float v = i < c.N ? et_of(x[i], m) : 0.f;
+        const V v = i < c.N ? et_of<V>(x[i], m) : (V)0;
         dd[i] = v;
-        se += v;
+        se += (double)v;
       }
-      dd[32] = 0.f;
+      dd[32] = (V)0;
       // log-probs: the frame's shift is its max; logits (log-softmax fused):
       // max logp = -log sum_i exp(x_i - max x)
-      shifts += c.logits ? -log((double)se) : (double)m;
+      shifts += c.logits ? -log(se) : (double)m;
     }
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
-#ifdef W2L_PROF
-    if (lane == 0 && g_prof_on) PROF_ADD(3, clock64() - _cv0);
-    if (lane == 0 && ch == 25) g_prof[(((blockIdx.x & 63) * 2 + blockIdx.y) * 16 + (threadIdx.x >> 5)) * 8 + 4] = clock64();
-#endif
   }
-  if (lane == 0) PROF_ADD(0, clock64() - _pt0);
   if (__any_sync(0xffffffffu, flush) && lane == 0) sm.flush = 1;
   if (shift_sum) {
     shifts = warp_sum(shifts);
@@ -249,29 +252,29 @@ struct LatCtx {
   int lane, T, N;
   int nstates;       // L (fac) or 2L+1 (CTC)
   int cons_idx;      // counter index of lattice warp 0
-  float *rows;       // [W][Tmax][128] this utterance (warp-major)
-  int *exps;         // [W][Tmax][32]
+  void *rows;        // rows of this utterance: V [W][Tmax][128]
+  int *exps;         //                         int [W][Tmax][32]
   int Tmax;
 };
 
+template <class V>
 struct LatState {
-  float v[kSpl];
-  float S[kSpl], P[kSpl];   // fac weights (stay, step); CTC: skip flags in P
+  V v[kSpl];
+  V S[kSpl], P[kSpl];       // fac weights (stay, step); CTC: skip flags in P
   int tok[kSpl];            // tokens (E column) of this lane's states
   int nbtok1, nbtok2;       // tokens of the two states after this lane (backward)
   int ex;
-  float asc;                // alignment factor of the neighbour's values
+  V asc;                    // alignment factor of the neighbour's values
 };
 
 // lattice state weights.  fac: tok = y_l, S = M[y_l][y_l], P = M[y_l][y_{l-1}]
 // (forward) or M[y_{l+1}][y_l] (backward), M = exp(A - max A).  CTC: tok =
 // blank (even s) or y_{s/2}; P = skip flag (forward: edge s-2 -> s; backward:
 // edge s+2 -> s).  Padding states read the zero column N.
-template <int KIND, bool FWD>
-__device__ __forceinline__ void lat_init_weights(LatState &f, const LatCtx &c, const int64_t *y,
-                                                 int L, const float *trans, float amax,
-                                                 int blank) {
-  const int N = c.N, S = c.nstates;
+template <int KIND, bool FWD, class V>
+__device__ __forceinline__ void lat_init_weights(LatState<V> &f, int w, int lane, int N, int S,
+                                                 const int64_t *y, int L, const float *trans,
+                                                 float amax, int blank) {
   auto tok_of = [&](int s) -> int {
     if (s >= S) return N;
     if (KIND == kFac) return (int)y[s];
@@ -280,7 +283,8 @@ __device__ __forceinline__ void lat_init_weights(LatState &f, const LatCtx &c, c
   auto ctc_skip = [&](int s) -> bool {   // edge s-2 -> s exists
     return (s & 1) && s >= 3 && s < S && y[s >> 1] != y[(s >> 1) - 1];
   };
-  const int base = (c.w * 32 + c.lane) * kSpl;
+  auto mexp = [&](float a) -> V { return Pow2<V>::ex((V)a - (V)amax); };
+  const int base = (w * 32 + lane) * kSpl;
 #pragma unroll
   for (int k = 0; k < kSpl; ++k) {
     const int s = base + k;
@@ -288,18 +292,18 @@ __device__ __forceinline__ void lat_init_weights(LatState &f, const LatCtx &c, c
     if (KIND == kFac) {
       if (s < L) {
         const int yl = (int)y[s];
-        f.S[k] = expf(trans[yl * N + yl] - amax);
+        f.S[k] = mexp(trans[yl * N + yl]);
         if (FWD)
-          f.P[k] = s > 0 ? expf(trans[yl * N + (int)y[s - 1]] - amax) : 0.f;
+          f.P[k] = s > 0 ? mexp(trans[yl * N + (int)y[s - 1]]) : (V)0;
         else
-          f.P[k] = s + 1 < L ? expf(trans[(int)y[s + 1] * N + yl] - amax) : 0.f;
+          f.P[k] = s + 1 < L ? mexp(trans[(int)y[s + 1] * N + yl]) : (V)0;
       } else {
-        f.S[k] = 0.f;
-        f.P[k] = 0.f;
+        f.S[k] = (V)0;
+        f.P[k] = (V)0;
       }
     } else {
-      f.S[k] = 1.f;
-      f.P[k] = FWD ? (ctc_skip(s) ? 1.f : 0.f) : (ctc_skip(s + 2) ? 1.f : 0.f);
+      f.S[k] = (V)1;
+      f.P[k] = FWD ? (ctc_skip(s) ? (V)1 : (V)0) : (ctc_skip(s + 2) ? (V)1 : (V)0);
     }
   }
   f.nbtok1 = tok_of(base + kSpl);
@@ -308,16 +312,17 @@ __device__ __forceinline__ void lat_init_weights(LatState &f, const LatCtx &c, c
 
 // Inputs of one step, loaded ahead of the recursion (shared-memory loads
 // cannot be hoisted by the compiler across the previous steps' stores).
+template <class V>
 struct StepIn {
-  float E[kSpl];     // Et of this lane's states
-  float En1, En2;    // Et of the two states after this lane (backward edge lane)
-  float b0, b1;      // upstream boundary states after the previous step
-  int bex;           // their lane exponent
+  V E[kSpl];     // Et of this lane's states
+  V En1, En2;    // Et of the two states after this lane (backward edge lane)
+  V b0, b1;      // upstream boundary states after the previous step
+  int bex;       // their lane exponent
 };
 
-template <int KIND, bool FWD>
-__device__ __forceinline__ void load_step_in(StepIn &in, const LatState &f, const float *er,
-                                             const Bnd *bi, int lane) {
+template <int KIND, bool FWD, class V>
+__device__ __forceinline__ void load_step_in(StepIn<V> &in, const LatState<V> &f, const V *er,
+                                             const BndT<V> *bi, int lane) {
   if (KIND == kCtc) {   // even states are blanks: one shared Et
     in.E[0] = in.E[2] = er[f.tok[0]];
     in.E[1] = er[f.tok[1]];
@@ -328,15 +333,15 @@ __device__ __forceinline__ void load_step_in(StepIn &in, const LatState &f, cons
   }
   if (!FWD) {
     in.En1 = er[f.nbtok1];
-    in.En2 = KIND == kCtc ? er[f.nbtok2] : 0.f;
+    in.En2 = KIND == kCtc ? er[f.nbtok2] : (V)0;
   }
   if (bi) {
-    const Bnd x = *bi;
+    const BndT<V> x = *bi;
     in.b0 = x.v0;
     in.b1 = x.v1;
     in.bex = x.ex;
   } else {
-    in.b0 = in.b1 = 0.f;
+    in.b0 = in.b1 = (V)0;
     in.bex = kNegExp;
   }
 }
@@ -348,41 +353,41 @@ __device__ __forceinline__ void load_step_in(StepIn &in, const LatState &f, cons
 // the neighbour's alignment factor f.asc is recomputed on the step after
 // each renormalisation (`check`) and a step is one shuffle plus the
 // recursion's arithmetic.
-template <int KIND, bool FWD, bool FAST>
-__device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo, int lane,
-                                         bool renorm, bool check) {
+template <int KIND, bool FWD, bool FAST, class V>
+__device__ __forceinline__ void lat_step(LatState<V> &f, const StepIn<V> &in, BndT<V> *bo,
+                                         int lane, bool renorm, bool check) {
   const bool edge_in = FWD ? lane == 0 : lane == 31;
   if (FWD) {
-    float nb = __shfl_up_sync(0xffffffffu, f.v[kSpl - 1], 1);
+    V nb = __shfl_up_sync(0xffffffffu, f.v[kSpl - 1], 1);
     if (edge_in) nb = in.b0;
     if (!FAST || check) {
       int nbe = __shfl_up_sync(0xffffffffu, f.ex, 1);
       if (edge_in) nbe = in.bex;
-      f.asc = align_factor<kSpl>(nbe, f.v, f.ex, check);
+      f.asc = align_factor<kSpl, V>(nbe, f.v, f.ex, check);
     }
-    const float n1 = nb * f.asc;
+    const V n1 = nb * f.asc;
     if (KIND == kFac) {
 #pragma unroll
       for (int k = kSpl - 1; k >= 1; --k)
-        f.v[k] = in.E[k] * fmaf(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
-      f.v[0] = in.E[0] * fmaf(f.S[0], f.v[0], f.P[0] * n1);
+        f.v[k] = in.E[k] * fma(f.S[k], f.v[k], f.P[k] * f.v[k - 1]);
+      f.v[0] = in.E[0] * fma(f.S[0], f.v[0], f.P[0] * n1);
     } else {
       // even states are blanks (no skip edge); odd state k skips from k-2,
       // which for k = 1 is the previous lane's last state
 #pragma unroll
       for (int k = kSpl - 1; k >= 2; --k)
-        f.v[k] = (k & 1) ? in.E[k] * fmaf(f.P[k], f.v[k - 2], f.v[k] + f.v[k - 1])
+        f.v[k] = (k & 1) ? in.E[k] * fma(f.P[k], f.v[k - 2], f.v[k] + f.v[k - 1])
                          : in.E[k] * (f.v[k] + f.v[k - 1]);
-      const float v1 = in.E[1] * fmaf(f.P[1], n1, f.v[1] + f.v[0]);
+      const V v1 = in.E[1] * fma(f.P[1], n1, f.v[1] + f.v[0]);
       f.v[0] = in.E[0] * (f.v[0] + n1);
       f.v[1] = v1;
     }
   } else {
-    float wv[kSpl];
+    V wv[kSpl];
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) wv[k] = in.E[k] * f.v[k];
-    float nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-    float nb2 = KIND == kCtc ? __shfl_down_sync(0xffffffffu, wv[1], 1) : 0.f;
+    V nb1 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+    V nb2 = KIND == kCtc ? __shfl_down_sync(0xffffffffu, wv[1], 1) : (V)0;
     if (edge_in) {
       nb1 = in.En1 * in.b0;
       nb2 = in.En2 * in.b1;
@@ -390,27 +395,27 @@ __device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo,
     if (!FAST || check) {
       int nbe = __shfl_down_sync(0xffffffffu, f.ex, 1);
       if (edge_in) nbe = in.bex;
-      f.asc = align_factor<kSpl>(nbe, wv, f.ex, check);
+      f.asc = align_factor<kSpl, V>(nbe, wv, f.ex, check);
     }
-    const float n1 = nb1 * f.asc;
+    const V n1 = nb1 * f.asc;
     if (KIND == kFac) {
 #pragma unroll
-      for (int k = 0; k < kSpl - 1; ++k) f.v[k] = fmaf(f.S[k], wv[k], f.P[k] * wv[k + 1]);
-      f.v[kSpl - 1] = fmaf(f.S[kSpl - 1], wv[kSpl - 1], f.P[kSpl - 1] * n1);
+      for (int k = 0; k < kSpl - 1; ++k) f.v[k] = fma(f.S[k], wv[k], f.P[k] * wv[k + 1]);
+      f.v[kSpl - 1] = fma(f.S[kSpl - 1], wv[kSpl - 1], f.P[kSpl - 1] * n1);
     } else {
-      const float n2 = nb2 * f.asc;
+      const V n2 = nb2 * f.asc;
       // P[k] holds the skip flag of the edge k+2 -> k
 #pragma unroll
       for (int k = 0; k < kSpl - 2; ++k)
-        f.v[k] = (k & 1) ? fmaf(f.P[k], wv[k + 2], wv[k] + wv[k + 1]) : wv[k] + wv[k + 1];
+        f.v[k] = (k & 1) ? fma(f.P[k], wv[k + 2], wv[k] + wv[k + 1]) : wv[k] + wv[k + 1];
       f.v[kSpl - 2] = wv[kSpl - 2] + wv[kSpl - 1];
-      f.v[kSpl - 1] = fmaf(f.P[kSpl - 1], n2, wv[kSpl - 1] + n1);
+      f.v[kSpl - 1] = fma(f.P[kSpl - 1], n2, wv[kSpl - 1] + n1);
     }
   }
-  if (renorm) lane_renorm<kSpl>(f.v, f.ex);
+  if (renorm) lane_renorm<kSpl, V>(f.v, f.ex);
   const bool edge = FWD ? lane == 31 : lane == 0;
   if (bo && edge) {
-    Bnd o;
+    BndT<V> o;
     o.v0 = FWD ? f.v[kSpl - 1] : f.v[0];
     o.v1 = FWD ? f.v[kSpl - 2] : f.v[1];
     o.ex = f.ex;
@@ -419,39 +424,43 @@ __device__ __forceinline__ void lat_step(LatState &f, const StepIn &in, Bnd *bo,
   }
 }
 
-__device__ __forceinline__ void lat_store_row(const float (&v)[kSpl], int ex, float *row,
-                                              int *erow, int lane) {
-  reinterpret_cast<float4 *>(row)[lane] = make_float4(v[0], v[1], v[2], v[3]);
-  erow[lane] = ex;
+template <class V>
+__device__ __forceinline__ void lat_store_row(const LatState<V> &f, V *row, int *erow, int lane,
+                                              bool live) {
+  if (live) {
+    st4(row + lane * kSpl, f.v);
+    erow[lane] = f.ex;
+  }
 }
 
 // Run a lattice warp over the whole utterance; its share of the recursion's
-// total goes to sm.fin[w] (log domain) for the CTA epilogue.
-template <int KIND, bool FWD>
-__device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
-  PROF_T0();
+// total goes to sm.fin[w] (log domain) for the CTA epilogue.  Every step's
+// lane values and exponents are stored (padding lanes excepted).
+template <int KIND, bool FWD, class V>
+__device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
+  constexpr int kRing = Ring<V>::n;
   const int T = c.T, lane = c.lane;
   int *mycons = &sm.cons[c.cons_idx + c.w];
   const int up = FWD ? c.w - 1 : c.w + 1, dn = FWD ? c.w + 1 : c.w - 1;
   const bool has_up = up >= 0 && up < c.W, has_dn = dn >= 0 && dn < c.W;
   const int *upcons = &sm.cons[c.cons_idx + (has_up ? up : c.w)];
   const int *dncons = &sm.cons[c.cons_idx + (has_dn ? dn : c.w)];
-  const Bnd *ubnd = has_up ? sm.bnd[up] : nullptr;
-  Bnd *mybnd = sm.bnd[c.w];
-  float *rows = c.rows + (size_t)c.w * c.Tmax * kLatStates;
+  const BndT<V> *ubnd = has_up ? sm.bnd[up] : nullptr;
+  BndT<V> *mybnd = sm.bnd[c.w];
+  V *rows = reinterpret_cast<V *>(c.rows) + (size_t)c.w * c.Tmax * kLatStates;
   int *exps = c.exps + (size_t)c.w * c.Tmax * 32;
   auto row_of = [&](int t) { return rows + (size_t)t * kLatStates; };
   auto exp_of = [&](int t) { return exps + (size_t)t * 32; };
 
   // ---- step 0: initial values (criterion.py:123-125 / :194, :143-146 / :205-206)
 #pragma unroll
-  for (int k = 0; k < kSpl; ++k) f.v[k] = 0.f;
+  for (int k = 0; k < kSpl; ++k) f.v[k] = (V)0;
   f.ex = 0;
   const int base = (c.w * 32 + lane) * kSpl;
-  const bool pad_lane = base >= c.nstates;   // padding states stay 0
+  const bool pad_lane = base >= c.nstates;   // padding states stay 0 (and are not stored)
   if (FWD) {
     wait_ge(&sm.prod, 1);
-    const float *er = sm.ering[ring_slot(true, 0)];
+    const V *er = sm.ering[ring_slot<V>(true, 0)];
     if (base == 0) {
       f.v[0] = er[f.tok[0]];
       if (KIND == kCtc && c.nstates > 1) f.v[1] = er[f.tok[1]];
@@ -461,16 +470,16 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) {
       const int s = base + k;
-      f.v[k] = (s == S - 1 || (KIND == kCtc && s == S - 2)) ? 1.f : 0.f;
+      f.v[k] = (s == S - 1 || (KIND == kCtc && s == S - 2)) ? (V)1 : (V)0;
     }
   }
-  lane_renorm<kSpl>(f.v, f.ex);
-  f.asc = 0.f;
+  lane_renorm<kSpl, V>(f.v, f.ex);
+  f.asc = (V)0;
   {
     const int t = frame_of(FWD, T, 0);
-    lat_store_row(f.v, f.ex, row_of(t), exp_of(t), lane);
+    lat_store_row(f, row_of(t), exp_of(t), lane, !pad_lane);
     if (FWD ? lane == 31 : lane == 0) {
-      Bnd o;
+      BndT<V> o;
       o.v0 = FWD ? f.v[kSpl - 1] : f.v[0];
       o.v1 = FWD ? f.v[kSpl - 2] : f.v[1];
       o.ex = f.ex;
@@ -485,13 +494,13 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     wait_ge(&sm.prod, eidx_of(FWD, j) + 1);
     if (has_up) wait_ge(upcons, j);
     if (has_dn) wait_ge(dncons, j + 2 - kBndRing);
-    StepIn in;
-    load_step_in<KIND, FWD>(in, f, sm.ering[j & (kRing - 1)],
-                            has_up ? &ubnd[(j - 1) & (kBndRing - 1)] : nullptr, lane);
-    lat_step<KIND, FWD, false>(f, in, &mybnd[j & (kBndRing - 1)], lane,
-                               (j % kRenormF) == 0 || j == T - 1, true);
+    StepIn<V> in;
+    load_step_in<KIND, FWD, V>(in, f, sm.ering[j & (kRing - 1)],
+                               has_up ? &ubnd[(j - 1) & (kBndRing - 1)] : nullptr, lane);
+    lat_step<KIND, FWD, false, V>(f, in, &mybnd[j & (kBndRing - 1)], lane,
+                                  (j % kRenormF) == 0 || j == T - 1, true);
     const int t = frame_of(FWD, T, j);
-    lat_store_row(f.v, f.ex, row_of(t), exp_of(t), lane);
+    lat_store_row(f, row_of(t), exp_of(t), lane, !pad_lane);
     publish(mycons, j + 1, lane);
   };
   const int pro_end = min(T, kBlk);
@@ -502,28 +511,21 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
-    PROF_STEADY(m >= 40 && m < 160);
-#ifdef W2L_PROF
-    PROF_WAIT(1, while (ld_relaxed(&sm.prod) < eidx_of(FWD, j0 + kBlk - 1) + 1) {});
-    PROF_WAIT(2, while (has_up && ld_relaxed(upcons) < j0 + kBlk - 1) {});
-    PROF_WAIT(3, while (has_dn && ld_relaxed(dncons) < j0 + kBlk + 1 - kBndRing) {});
-#endif
-    PROF_WAIT(6, wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, upcons,
-                       has_up ? j0 + kBlk - 1 : 0, dncons,
-                       has_dn ? j0 + kBlk + 1 - kBndRing : -kDone));
-    const float *eb = sm.ering[j0 & (kRing - 1)];
-    const Bnd *ub0 = has_up ? &ubnd[(j0 - 1) & (kBndRing - 1)] : nullptr;
-    const Bnd *ub1 = has_up ? &ubnd[j0 & (kBndRing - 1)] : nullptr;   // q >= 1: ub1[q-1]
-    Bnd *ob = has_dn ? &mybnd[j0 & (kBndRing - 1)] : nullptr;   // no reader: no store
+    wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, upcons, has_up ? j0 + kBlk - 1 : 0, dncons,
+          has_dn ? j0 + kBlk + 1 - kBndRing : -kDone);
+    const V *eb = sm.ering[j0 & (kRing - 1)];
+    const BndT<V> *ub0 = has_up ? &ubnd[(j0 - 1) & (kBndRing - 1)] : nullptr;
+    const BndT<V> *ub1 = has_up ? &ubnd[j0 & (kBndRing - 1)] : nullptr;   // q >= 1: ub1[q-1]
+    BndT<V> *ob = has_dn ? &mybnd[j0 & (kBndRing - 1)] : nullptr;   // no reader: no store
     // rows go straight to global memory (fire-and-forget vector stores)
     const int tb = frame_of(FWD, T, j0);
-    float *sv = row_of(tb);
+    V *sv = row_of(tb);
     int *se = exp_of(tb);
-    StepIn in[kBlk];
+    StepIn<V> in[kBlk];
 #pragma unroll
     for (int q = 0; q < kBlk; ++q)
-      load_step_in<KIND, FWD>(in[q], f, eb + q * kStride,
-                              q == 0 ? ub0 : (ub1 ? ub1 + (q - 1) : nullptr), lane);
+      load_step_in<KIND, FWD, V>(in[q], f, eb + q * kStride,
+                                 q == 0 ? ub0 : (ub1 ? ub1 + (q - 1) : nullptr), lane);
     // every lane live (and the incoming boundary lane): exponents only move at
     // renormalisations from here on
     const bool fast = __all_sync(0xffffffffu, (f.ex != kNegExp || pad_lane) &&
@@ -533,31 +535,21 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
       constexpr bool FAST = decltype(fast_tag)::value;
 #pragma unroll
       for (int q = 0; q < kBlk; ++q) {
-        lat_step<KIND, FWD, FAST>(f, in[q], ob ? ob + q : nullptr, lane, (q % kRenormF) == 0,
-                                  (q % kRenormF) == 1);
+        lat_step<KIND, FWD, FAST, V>(f, in[q], ob ? ob + q : nullptr, lane, (q % kRenormF) == 0,
+                                     (q % kRenormF) == 1);
         const int dq = FWD ? q : -q;
-        lat_store_row(f.v, f.ex, sv + dq * kLatStates, se + dq * 32, lane);
+        lat_store_row(f, sv + dq * kLatStates, se + dq * 32, lane, !pad_lane);
       }
     };
-#ifdef W2L_PROF
-    const long long _c0 = clock64();
-#endif
     if (fast)
       run_block(std::true_type{});
     else
       run_block(std::false_type{});
-#ifdef W2L_PROF
-    if (lane == 0 && g_prof_on) { PROF_ADD(7, clock64() - _c0); }
-    if (lane == 0 && m == 40) PROF_ADD(5, clock64());
-    if (lane == 0 && m == 100) PROF_ADD(4, 0), g_prof[(((blockIdx.x & 63) * 2 + blockIdx.y) * 16 + (threadIdx.x >> 5)) * 8 + 4] = clock64();
-    if (lane == 0 && m == 159) PROF_ADD(5, -clock64());
-#endif
     publish(mycons, j0 + kBlk, lane);
   }
   // ---- tail steps
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
   publish(mycons, kDone, lane);
-  if (lane == 0) { PROF_ADD(0, clock64() - _pt0); PROF_ADD(5, nfull); }
 
   // ---- totals (criterion.py:136-141 CTC, :203 fac forward; backward: the
   // frame-0 emissions times beta'_0)
@@ -572,10 +564,10 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
     }
   } else {
     wait_ge(&sm.prod, T);   // frame 0's Et (the last step only waited for T - 1)
-    const float *er = sm.ering[ring_slot(false, T - 1)];   // frame 0
+    const V *er = sm.ering[ring_slot<V>(false, T - 1)];   // frame 0
     if (base == 0) {
-      part = (double)er[f.tok[0]] * f.v[0];
-      if (KIND == kCtc && c.nstates > 1) part += (double)er[f.tok[1]] * f.v[1];
+      part = (double)er[f.tok[0]] * (double)f.v[0];
+      if (KIND == kCtc && c.nstates > 1) part += (double)er[f.tok[1]] * (double)f.v[1];
     }
   }
   const double lp = part > 0.0 ? log(part) + (double)f.ex * ln2 : -CUDART_INF;
@@ -585,7 +577,8 @@ __device__ void lattice_run(ChainSm &sm, const LatCtx &c, LatState &f) {
 }
 
 // combine the per-warp totals (log domain) after a CTA barrier
-__device__ __forceinline__ double lattice_total(const ChainSm &sm, int W) {
+template <class V>
+__device__ __forceinline__ double lattice_total(const ChainSm<V> &sm, int W) {
   double m = -CUDART_INF;
   for (int w = 0; w < W; ++w) m = fmax(m, sm.fin[w]);
   if (!isfinite(m)) return -CUDART_INF;
@@ -598,20 +591,10 @@ __host__ __device__ inline int lat_warps(int nstates) {
   return nstates <= 0 ? 1 : (nstates + kLatStates - 1) / kLatStates;
 }
 
-// Posterior of one state from stored alpha and beta lane values:
-// a * b * 2^xs with xs = lane exponents minus the utterance's reference
-// exponent, split over both factors so that neither the product of two small
-// mantissas underflows nor a scaled factor overflows (both factors are
-// < 2^8 after renormalisation, the split is clamped to 2^119).
-struct PostScale {
-  float sa, sb;
-};
-__device__ __forceinline__ PostScale post_scale(int ea, int eb, int ref) {
-  int xs = ea + eb - ref;
-  xs = max(min(xs, 238), -300);
-  const int xa = xs >> 1, xb = xs - xa;
-  return PostScale{pow2f_fast(xa), pow2f_fast(xb)};
+// 2^x for an integer x, clamped to the type's range (0 below)
+template <class V>
+__device__ __forceinline__ V pow2_clamped(int x) {
+  return Pow2<V>::p2(max(min(x, Pow2<V>::kMaxExp), -Pow2<V>::kMaxExp));
 }
-__device__ __forceinline__ float post_of(float a, float b, PostScale s) { return (a * s.sa) * (b * s.sb); }
 
 }  // namespace w2l

@@ -165,7 +165,10 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
       amax = fmax(amax, s_mx[q]);
       amin = fmin(amin, s_mn[q]);
     }
-    const int range = mode == kPrepFast && amin - amax < -(double)kFlushNats;
+    // 0: fp32 range; 1: fp64 range (kNeedsF64); 2: beyond it (kNeedsLog)
+    const int range = mode != kPrepFast ? 0
+                      : amin - amax < -(double)kFlushNats64 ? 2
+                      : amin - amax < -(double)kFlushNats ? 1 : 0;
     if (block_any(bad)) {
       code = W2L_ERR_NUMERIC;                       // :179-180
     } else if (L < 0 || L > d.Lmax) {
@@ -185,7 +188,8 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
       else if (T < L) code = W2L_ERR_INFEASIBLE;    // :187-190
       if (code == W2L_OK && perm)
         build_token_csr(y, L, d.N, 1, 0, perm + (size_t)b * lpad, tok_start + b * 33);
-      if (code == W2L_OK && (mode == kPrepForceExact || range)) code = kNeedsExact;
+      if (code == W2L_OK && (mode == kPrepForceExact || range == 2)) code = kNeedsLog;
+      else if (code == W2L_OK && range == 1) code = kNeedsF64;
     }
   }
   __syncthreads();
@@ -231,7 +235,7 @@ __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
     else if (T < L + s_reps) code = W2L_ERR_INFEASIBLE;       // :105-111
     if (code == W2L_OK && perm)
       build_token_csr(y, L, d.N, 2, 1, perm + (size_t)b * lpad, tok_start + b * 33);
-    if (code == W2L_OK && mode == kPrepForceExact) code = kNeedsExact;
+    if (code == W2L_OK && mode == kPrepForceExact) code = kNeedsLog;
   }
   __syncthreads();
   if (threadIdx.x == 0) status[b] = code;
