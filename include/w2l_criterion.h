@@ -57,7 +57,7 @@ enum {
 };
 
 /* flags for the fp32 batched entry points */
-#define W2L_FLAG_NO_FALLBACK 1u  /* report guard failures instead of recomputing in f64 */
+#define W2L_FLAG_NO_FALLBACK 1u  /* report fp32 guard failures instead of recomputing them */
 /* Split-phase calls (both bits clear = the whole call).  PHASE_CHAIN runs the
  * validation and the forward/backward recursions, leaving their rows in the
  * workspace; PHASE_GRAD then runs the posterior/gradient kernels, the loss,
@@ -79,6 +79,11 @@ enum {
  * log-domain kernel (the guard's fallback path, forced; tests and
  * diagnostics). */
 #define W2L_FLAG_FORCE_EXACT 32u
+/* Precision tiers of the fp32 batched entry points: an utterance whose fp32
+ * guard fails is recomputed with fp64 lanes (same kernels, range 2^+-1022);
+ * one that fails that guard too by the float64 log-domain kernel.  This flag
+ * stops after the fp64 tier (diagnostics: which tier resolved an input). */
+#define W2L_FLAG_NO_LOG_FALLBACK 64u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

@@ -71,6 +71,7 @@ FLAG_PHASE_GRAD = 4
 FLAG_LOSS_ONLY = 8
 FLAG_CTC_LOGITS = 16
 FLAG_FORCE_EXACT = 32
+FLAG_NO_LOG_FALLBACK = 64
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

@@ -357,9 +357,13 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
     return em, el, tg, tl
 
 
-def _flags(fallback: bool, phase: str, loss_only: bool = False, logits: bool = False,
+def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
            force_exact: bool = False) -> int:
+    # fallback: True (every precision tier), False (fp32 only) or "f64" (the
+    # fp32 and fp64 scaled-linear tiers, no log-domain kernel)
     f = 0 if fallback else nat.FLAG_NO_FALLBACK
+    if fallback == "f64":
+        f = nat.FLAG_NO_LOG_FALLBACK
     if force_exact:
         f |= nat.FLAG_FORCE_EXACT
     if loss_only:
@@ -387,7 +391,7 @@ def _raise_batch(status: torch.Tensor, what: str) -> None:
 def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, check=True,
                           per_utterance_grad_transitions=False, workspace=None,
                           out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True, trace: bool = False,
+                          fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
                           force_exact: bool = False) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
@@ -397,9 +401,11 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     tgt_len int [B]; transitions f32 [N,N] (A[to][from]).  Returns loss f64 [B],
     grad_emissions f32 [B,Tmax,N], grad_transitions f32 [N,N] summed over the
     batch and (optionally) per utterance.  check=True synchronises and raises
-    the reference exception for the first failing utterance.  fallback=False
-    disables the float64 recompute of utterances failing the fp32 guard (they
-    report W2L_ERR_PRECISION instead) -- a diagnostic for the fast path.
+    the reference exception for the first failing utterance.  Precision
+    tiers: an utterance failing the fp32 guard is recomputed with fp64 lanes,
+    one failing that guard too by the float64 log-domain kernel;
+    fallback=False stops after the fp32 tier and fallback="f64" after the
+    fp64 tier (the rest report W2L_ERR_PRECISION) -- diagnostics.
     phase="chain" | "grad" splits the call (W2L_FLAG_PHASE_*): "chain" runs
     the recursions into the workspace, a later "grad" call with the same
     inputs, workspace and out on the same stream order finishes it.
@@ -444,7 +450,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
 
 def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *, check=True,
                           workspace=None, out: Optional[BatchLossOutput] = None,
-                          fallback: bool = True, trace: bool = False,
+                          fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
                           logits: bool = False, force_exact: bool = False) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are

@@ -187,7 +187,7 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
     // launches exit at once when nothing is flagged)
     rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
                                    status, s, nullptr, loss_only ? (1u | 4u) : 3u, 1));
-    if (!rc)
+    if (!rc && !(flags & W2L_FLAG_NO_LOG_FALLBACK))
       rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
                                              slots, loss, grad_em, ga, status, s));
     if (rc) return rc;
@@ -346,7 +346,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   if (!(flags & W2L_FLAG_NO_FALLBACK)) {
     rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em,
                                    status, s, nullptr, loss_only ? (1u | 4u) : 3u, 1));
-    if (!rc)
+    if (!rc && !(flags & W2L_FLAG_NO_LOG_FALLBACK))
       rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
                                              asg_slots(B), slots, loss, grad_em, status, s,
                                              logits));

@@ -230,3 +230,22 @@ def test_library_nccl_allreduce_single_rank():
     comm.close()
     # contract violations and a missing communicator are reported, not run
     assert nat.lib().w2l_allreduce_grad_A(g.data_ptr(), 40, None, None) == nat.ERR_CONTRACT
+
+
+@pytest.mark.parametrize("scale", [10.0, 20.0])
+def test_peaky_emissions_resolved_by_fp64_tier(scale):
+    # trained acoustic models are peaky: log_softmax(s N(0,1)) with s = 10, 20
+    # leaves the fp32 range (every utterance fails its guard or its flush
+    # check) and must be resolved by the fp64 scaled-linear tier alone (the
+    # log-domain kernel disabled), matching the oracle at 1e-4
+    import bench
+    em, el, ta, tc, tl, a, blank = bench.peaky_inputs(scale, b=12)
+    x = torch.from_numpy(em).cuda()
+    fast = C.asg_loss_grad_batched(x, el, ta, tl, a, fallback=False, check=False)
+    assert (fast.status.cpu().numpy() != 0).any()
+    out = C.asg_loss_grad_batched(x, el, ta, tl, a, fallback="f64", check=False)
+    assert (out.status.cpu().numpy() == 0).all()
+    _check_asg(out, *pool.asg_batch(em, el, ta, tl, a), el)
+    outc = C.ctc_loss_grad_batched(x, el, tc, tl, blank, fallback="f64", check=False)
+    assert (outc.status.cpu().numpy() == 0).all()
+    _check_ctc(outc, *pool.ctc_batch(em, el, tc, tl, blank), el)
