@@ -610,7 +610,10 @@ def main():
                     "peak": peaks["dadd_per_s"] / 1e9,
                     "frac": vit_ops / (ms_v / 1e3) / peaks["dadd_per_s"], "kernel_ms": ms_v,
                     "peak_source": "w2l_probe_peaks: DADD throughput measured on this GPU"}
-        # peaky emissions (trained models): fp32-guard fallbacks and step time
+        # peaky emissions (trained models): fp32-guard failures, and the step
+        # time with the precision routing (default: a batch the fp32 tier
+        # would fail goes straight to the fp64 tier) and without it (fp32
+        # pass, then the fp64 tier for its failures)
         peaky = {}
         for scale in (2.0, 5.0, 10.0, 20.0):
             pe = peaky_inputs(scale, b=B)
@@ -620,14 +623,16 @@ def main():
             pc = C.ctc_loss_grad_batched(pem, el_d, tc_d, tl_d, blank, check=False,
                                          workspace=ws_c, fallback=False)
             fa, fc = int((pa.status != 0).sum().item()), int((pc.status != 0).sum().item())
-            ms_pa = timeit(lambda: C.asg_loss_grad_batched(pem, el_d, ta_d, tl_d, A_d,
-                                                           check=False, workspace=ws_a),
-                           reps=2)
-            ms_pc = timeit(lambda: C.ctc_loss_grad_batched(pem, el_d, tc_d, tl_d, blank,
-                                                           check=False, workspace=ws_c),
-                           reps=2)
-            peaky[f"s={scale:g}"] = {"asg_fallbacks": fa, "ctc_fallbacks": fc,
-                                     "asg_ms": ms_pa, "ctc_ms": ms_pc}
+            row = {"asg_fallbacks": fa, "ctc_fallbacks": fc}
+            for tag, rt in (("", True), ("_unrouted", False)):
+                row["asg_ms" + tag] = timeit(lambda: C.asg_loss_grad_batched(
+                    pem, el_d, ta_d, tl_d, A_d, check=False, workspace=ws_a, route=rt), reps=2)
+                row["ctc_ms" + tag] = timeit(lambda: C.ctc_loss_grad_batched(
+                    pem, el_d, tc_d, tl_d, blank, check=False, workspace=ws_c, route=rt),
+                    reps=2)
+            row["asg_vs_fast"] = row["asg_ms"] / ms_a
+            row["ctc_vs_fast"] = row["ctc_ms"] / ms_c
+            peaky[f"s={scale:g}"] = row
         sub["peaky_emissions"] = peaky
 
     cpu = None

@@ -84,6 +84,15 @@ enum {
  * one that fails that guard too by the float64 log-domain kernel.  This flag
  * stops after the fp64 tier (diagnostics: which tier resolved an input). */
 #define W2L_FLAG_NO_LOG_FALLBACK 64u
+/* Precision routing (on by default with the fallback tiers): when the
+ * emissions are so peaky that the fp32 tier would fail its guard (any frame
+ * row spread max - min beyond the fp32 flush limit, or more than a quarter
+ * of the rows wider than a criterion-specific spread: 16 nats ASG, 32 CTC),
+ * the whole batch goes straight to the fp64 tier, skipping an fp32 pass whose
+ * results would be discarded (the chains are latency-bound: two passes cost
+ * two passes, whatever the number of failures).  Results are the same either
+ * way; this flag disables the routing (diagnostics, A/B timing). */
+#define W2L_FLAG_NO_ROUTE 128u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

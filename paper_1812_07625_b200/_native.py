@@ -16,6 +16,8 @@ from ._build import LIB as _BUILT_LIB
 
 # W2L_LIB selects another build of the same library (A/B timing in tools/ab.sh)
 LIB = os.environ.get("W2L_LIB", _BUILT_LIB)
+if not os.path.isabs(LIB):   # relative to the repo root (subprocesses change directory)
+    LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), LIB)
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                       "include", "w2l_criterion.h")
@@ -72,6 +74,7 @@ FLAG_LOSS_ONLY = 8
 FLAG_CTC_LOGITS = 16
 FLAG_FORCE_EXACT = 32
 FLAG_NO_LOG_FALLBACK = 64
+FLAG_NO_ROUTE = 128
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

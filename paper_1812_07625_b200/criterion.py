@@ -358,7 +358,7 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
 
 
 def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
-           force_exact: bool = False) -> int:
+           force_exact: bool = False, route: bool = True) -> int:
     # fallback: True (every precision tier), False (fp32 only) or "f64" (the
     # fp32 and fp64 scaled-linear tiers, no log-domain kernel)
     f = 0 if fallback else nat.FLAG_NO_FALLBACK
@@ -366,6 +366,8 @@ def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
         f = nat.FLAG_NO_LOG_FALLBACK
     if force_exact:
         f |= nat.FLAG_FORCE_EXACT
+    if not route:
+        f |= nat.FLAG_NO_ROUTE
     if loss_only:
         f |= nat.FLAG_LOSS_ONLY
     if logits:
@@ -393,7 +395,7 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
                           out: Optional[BatchLossOutput] = None,
                           fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
-                          force_exact: bool = False) -> BatchLossOutput:
+                          force_exact: bool = False, route: bool = True) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -412,7 +414,10 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the recursions
     and the loss only: grad_emissions / grad_transitions are not computed.
     force_exact=True (W2L_FLAG_FORCE_EXACT) computes every utterance with
-    the float64 log-domain kernel (the guard's fallback path)."""
+    the float64 log-domain kernel (the guard's fallback path).  route=False
+    (W2L_FLAG_NO_ROUTE) disables the precision routing that sends a batch of
+    very peaky emissions straight to the fp64 tier (the results are the same
+    either way; see include/w2l_criterion.h)."""
     dev = _device()
     em, el, tg, tl = _batch_inputs(emissions, em_len, targets, tgt_len, dev)
     b, t_max, n = em.shape
@@ -435,7 +440,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
             _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase, loss_only,
-                                                       force_exact=force_exact), _stream())
+                                                       force_exact=force_exact, route=route),
+            _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_asg_loss_grad_traced(*args, ms, ctypes.byref(cnt))
@@ -452,7 +458,8 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
                           workspace=None, out: Optional[BatchLossOutput] = None,
                           fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
-                          logits: bool = False, force_exact: bool = False) -> BatchLossOutput:
+                          logits: bool = False, force_exact: bool = False,
+                          route: bool = True) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
     log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase and
     loss_only: as for asg_loss_grad_batched.  logits=True
@@ -475,7 +482,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
-            _flags(fallback, phase, loss_only, logits, force_exact), _stream())
+            _flags(fallback, phase, loss_only, logits, force_exact, route), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))

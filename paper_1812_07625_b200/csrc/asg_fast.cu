@@ -334,6 +334,10 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
   const int b = blockIdx.x;
   if (status[b] != want) return;
+  if (want == W2L_OK && route_to_f64(w.route)) {   // the batch goes to the fp64 tier
+    if (threadIdx.x == 0 && blockIdx.y == 0) status[b] = kNeedsF64;
+    return;
+  }
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(L);
   if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0;
@@ -634,8 +638,8 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     nea[sw] = neb[sw] = kNegExp;
     if (live[sw] && ta < tend) {
       const size_t tq = (size_t)ta * kLatStates;
-      ld4(A + sw * segv + tq, na[sw]);
-      ld4(Bv + sw * segv + tq, nb[sw]);
+      ldv(A + sw * segv + tq, na[sw]);
+      ldv(Bv + sw * segv + tq, nb[sw]);
       nea[sw] = EA[sw * sege + (size_t)ta * 32];
       neb[sw] = EB[sw * sege + (size_t)ta * 32];
     }
@@ -654,8 +658,8 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
       eb[sw] = neb[sw];
       if (live[sw] && t + 1 < tend) {
         const size_t tq = (size_t)(t + 1) * kLatStates;
-        ld4(A + sw * segv + tq, na[sw]);
-        ld4(Bv + sw * segv + tq, nb[sw]);
+        ldv(A + sw * segv + tq, na[sw]);
+        ldv(Bv + sw * segv + tq, nb[sw]);
         nea[sw] = EA[sw * sege + (size_t)(t + 1) * 32];
         neb[sw] = EB[sw * sege + (size_t)(t + 1) * 32];
       }
@@ -667,16 +671,15 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     }
     // fac node posteriors (:214-217)
     float zl = 0.f;
-    float4 p[W];
+    float p[W][kSpl];
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
       const V sc = pow2_clamped<V>(ea[sw] + eb[sw] - refCi);
-      p[sw].x = (float)(va[sw][0] * vb[sw][0] * sc);
-      p[sw].y = (float)(va[sw][1] * vb[sw][1] * sc);
-      p[sw].z = (float)(va[sw][2] * vb[sw][2] * sc);
-      p[sw].w = (float)(va[sw][3] * vb[sw][3] * sc);
-      reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p[sw];
-      zl += (p[sw].x + p[sw].y) + (p[sw].z + p[sw].w);
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) p[sw][k] = (float)(va[sw][k] * vb[sw][k] * sc);
+      stv(myp + sw * kLatStates + lane * kSpl, p[sw]);
+#pragma unroll
+      for (int k = 0; k < kSpl; k += 2) zl += p[sw][k] + p[sw][k + 1];
     }
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
@@ -685,12 +688,9 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     gmin = fminf(gmin, g);
     gmax = fmaxf(gmax, g);
 #pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-      accO[sw][0] = fmaf(p[sw].x, izc, accO[sw][0]);
-      accO[sw][1] = fmaf(p[sw].y, izc, accO[sw][1]);
-      accO[sw][2] = fmaf(p[sw].z, izc, accO[sw][2]);
-      accO[sw][3] = fmaf(p[sw].w, izc, accO[sw][3]);
-    }
+    for (int sw = 0; sw < W; ++sw)
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) accO[sw][k] = fmaf(p[sw][k], izc, accO[sw][k]);
     __syncwarp();
     // token gather: lane k sums the posteriors of the states labelled k
     float con;
@@ -915,8 +915,12 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   switch (w.W) {
 #define W2L_CASE(n)                                                                          \
   case n:                                                                                    \
+    if constexpr (n <= kMaxLatWarps) {                                                       \
     err = launch_grad_w<n, V>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, want,  \
                               s);                                                            \
+    } else {                                                                                 \
+      return cudaErrorInvalidValue;                                                          \
+    }                                                                                        \
     break;
     W2L_CASE(1) W2L_CASE(2) W2L_CASE(3) W2L_CASE(4) W2L_CASE(5) W2L_CASE(6) W2L_CASE(7)
     W2L_CASE(8)
@@ -963,6 +967,7 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   t.part_fullA = (float *)take((size_t)d.B * nblk * 1024 * 4);
   t.part_edge = (float *)take((size_t)d.B * nblk * lpad * 4);
   t.part_guard = (float *)take((size_t)d.B * nblk * 4 * 4);
+  t.route = (int *)take(kRouteWords * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
   t.spl = kSpl;

@@ -147,12 +147,15 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
     return W2L_ERR_CONTRACT;
   if (ws_bytes < w2l_asg_workspace_bytes(B, Tmax, N, Lmax)) return W2L_ERR_CONTRACT;
   const bool fallback = !(flags & W2L_FLAG_NO_FALLBACK);
+  // precision routing needs the fp64 tier behind the fp32 one
+  const bool route = fallback && !(flags & W2L_FLAG_NO_ROUTE);
   const bool force = flags & W2L_FLAG_FORCE_EXACT;
   Dims d{B, Tmax, N, Lmax};
   AsgFastWs w;
   float *ga_ws;
   void *slots;
   asg_ws(B, Tmax, N, Lmax, ws, &w, &ga_ws, &slots);
+  if (!route) w.route = nullptr;
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
   const bool loss_only = flags & W2L_FLAG_LOSS_ONLY;
   const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
@@ -173,7 +176,8 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   }
   if (phases & 1u) {
     rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
-                                              w.tok_start, status, s, kPrepFast));
+                                              w.tok_start, status, s, kPrepFast,
+                                              route ? w.route : nullptr));
     if (rc) return rc;
   }
   trace(tr, s);  // validate
@@ -315,6 +319,8 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   ctc_ws(B, Tmax, N, Lmax, ws, &w, &slots);
   const bool loss_only = flags & W2L_FLAG_LOSS_ONLY;
   const int logits = (flags & W2L_FLAG_CTC_LOGITS) ? 1 : 0;
+  const bool route = !(flags & (W2L_FLAG_NO_FALLBACK | W2L_FLAG_NO_ROUTE));
+  if (!route) w.route = nullptr;
   w.logits = logits;
   const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
   trace(tr, s);
@@ -335,7 +341,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
     // not apply to unnormalised inputs
     rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
                                               w.perm, w.tok_start, status, s, !logits,
-                                              kPrepFast));
+                                              kPrepFast, route ? w.route : nullptr));
     if (rc) return rc;
   }
   trace(tr, s);  // validate

@@ -24,6 +24,25 @@ constexpr int kNeedsExact = kNeedsF64;   // "the fp32 path could not take it"
 constexpr float kFlushNats = 80.f;
 constexpr float kFlushNats64 = 700.f;   // the same for double (exp underflows near -708)
 
+// Precision routing.  The fp32 tier fails its guard on peaky emissions
+// (relevant lattice states more than 2^126 apart inside a 4-state lane
+// block), and the chains are latency-bound: a batch run through fp32 and
+// then (for its failures) through fp64 costs both passes, whatever the
+// number of failures.  em_check counts the frame rows whose spread
+// max - min exceeds kRouteNats* (and kFlushNats: an fp32 weight that would
+// flush), and the fp32 chain sends the WHOLE batch straight to the fp64
+// tier when any row would flush or more than a quarter of the rows are that
+// wide.  Calibrated on log_softmax(s N(0,1)) emissions (N = 30): ASG fails
+// most utterances from s = 5 (spread ~20 nats), CTC from s = 10 (~41 nats).
+// Results do not depend on the routing (both tiers are guarded).
+constexpr int kRouteWords = 4;
+constexpr float kRouteNatsAsg = 16.f;
+constexpr float kRouteNatsCtc = 32.f;
+__device__ __forceinline__ bool route_to_f64(const int *route) {
+  if (!route) return false;
+  const int rows = route[0], wide = route[1], hard = route[2];
+  return hard > 0 || 4 * wide > rows;
+}
 constexpr int kWarp = 32;
 constexpr int kChunk = 32;            // frames per staged emission chunk
 constexpr int kNegExp = -(1 << 24);   // exponent of an all-zero lane block

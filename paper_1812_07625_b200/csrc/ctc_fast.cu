@@ -72,6 +72,10 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
   const int b = blockIdx.x;
   if (status[b] != want) return;
+  if (want == W2L_OK && route_to_f64(w.route)) {   // the batch goes to the fp64 tier
+    if (threadIdx.x == 0 && blockIdx.y == 0) status[b] = kNeedsF64;
+    return;
+  }
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(2 * L + 1);
   __shared__ unsigned s_mask;
@@ -145,21 +149,24 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     float zl = 0.f, zb = 0.f;
 #pragma unroll
     for (int sw = 0; sw < W; ++sw) {
-      float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+      float p[kSpl];
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) p[k] = 0.f;
       if (sw < weff && sw * kLatStates + lane * kSpl < S) {
         V va[kSpl], vb[kSpl];
-        ld4(A + sw * segv + tq, va);
-        ld4(Bv + sw * segv + tq, vb);
+        ldv(A + sw * segv + tq, va);
+        ldv(Bv + sw * segv + tq, vb);
         const V sc = pow2_clamped<V>(EA[sw * sege + (size_t)t * 32] + EB[sw * sege + (size_t)t * 32] - refi);
-        p.x = (float)(va[0] * vb[0] * sc);
-        p.y = (float)(va[1] * vb[1] * sc);
-        p.z = (float)(va[2] * vb[2] * sc);
-        p.w = (float)(va[3] * vb[3] * sc);
+#pragma unroll
+        for (int k = 0; k < kSpl; ++k) p[k] = (float)(va[k] * vb[k] * sc);
       }
       if (sw < weff) {
-        reinterpret_cast<float4 *>(myp + sw * kLatStates)[lane] = p;
-        zl += (p.x + p.y) + (p.z + p.w);
-        zb += p.x + p.z;   // blank states are the even ones
+        stv(myp + sw * kLatStates + lane * kSpl, p);
+#pragma unroll
+        for (int k = 0; k < kSpl; k += 2) {
+          zl += p[k] + p[k + 1];
+          zb += p[k];   // blank states are the even ones
+        }
       }
     }
     const float z = warp_sum(zl);
@@ -278,8 +285,12 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
   switch (w.W) {
 #define W2L_CASE(n)                                                                          \
   case n:                                                                                    \
+    if constexpr (n <= kMaxLatWarps) {                                                       \
     err = launch_ctc_grad_w<n, V>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status,    \
                                   want, s);                                                  \
+    } else {                                                                                 \
+      return cudaErrorInvalidValue;                                                          \
+    }                                                                                        \
     break;
     W2L_CASE(1) W2L_CASE(2) W2L_CASE(3) W2L_CASE(4) W2L_CASE(5) W2L_CASE(6) W2L_CASE(7)
     W2L_CASE(8)
@@ -318,6 +329,7 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
   t.eb = (int *)take(BWT * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
   t.part_guard = (float *)take((size_t)d.B * nblk * 2 * 4);
+  t.route = (int *)take(kRouteWords * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
   t.spl = kSpl;

@@ -34,12 +34,12 @@ template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
                                 int *perm, int *tok_start, int32_t *status, cudaStream_t s,
-                                int mode = kPrepExact);
+                                int mode = kPrepExact, int *route = nullptr);
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
                                 int *tok_start, int32_t *status, cudaStream_t s,
-                                int check_lse = 1, int mode = kPrepExact);
+                                int check_lse = 1, int mode = kPrepExact, int *route = nullptr);
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s);
@@ -71,6 +71,7 @@ struct AsgFastWs {
   float *part_fullA;         // [B][nblk][32][32]
   float *part_edge;          // [B][nblk][Lpad]
   float *part_guard;         // [B][nblk][4]
+  int *route;                // [kRouteWords] precision routing counters (em_check)
   int *perm;                 // [B][Lpad] states sorted by token
   int *tok_start;            // [B][33]
   int spl, W, lpad, nblk, tpad;  // W lattice warps; tpad = round_up(Tmax + 1, 8)
@@ -91,6 +92,7 @@ struct CtcFastWs {
   int *ea, *eb;              // [B][W][Tmax][32]
   double *scal;              // [B][4]: lnZ fwd, lnZ bwd, sum of frame shifts, spare
   float *part_guard;         // [B][nblk][2]
+  int *route;                // [kRouteWords] precision routing counters (em_check)
   int *perm;                 // [B][Lpad] label positions sorted by token
   int *tok_start;            // [B][33]
   int spl, W, lpad, nblk;

@@ -43,9 +43,13 @@
 
 namespace w2l {
 
-constexpr int kSpl = 4;                    // lattice states per lane
+#ifndef W2L_SPL
+#define W2L_SPL 4
+#endif
+constexpr int kSpl = W2L_SPL;              // lattice states per lane (even, multiple of 4)
+static_assert(kSpl % 4 == 0, "lane blocks are moved as 4-wide vectors");
 constexpr int kLatStates = 32 * kSpl;      // states per lattice warp
-constexpr int kMaxLatWarps = 8;            // 1024 states
+constexpr int kMaxLatWarps = 32 / kSpl;    // 1024 states
 constexpr int kBndRing = 128;              // boundary ring (steps): decouples neighbouring warps
 constexpr int kCounters = kMaxLatWarps + 2;  // lattice warps + fcc warp (+ spare)
 constexpr int kDone = 1 << 30;             // progress of a finished consumer
@@ -94,6 +98,17 @@ __device__ __forceinline__ void st4(float *p, const float (&v)[4]) {
 __device__ __forceinline__ void st4(double *p, const double (&v)[4]) {
   reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
   reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
+// a whole lane block (kSpl values) as 4-wide vectors
+template <class V, int K>
+__device__ __forceinline__ void ldv(const V *p, V (&v)[K]) {
+#pragma unroll
+  for (int q = 0; q < K; q += 4) ld4(p + q, *reinterpret_cast<V(*)[4]>(v + q));
+}
+template <class V, int K>
+__device__ __forceinline__ void stv(V *p, const V (&v)[K]) {
+#pragma unroll
+  for (int q = 0; q < K; q += 4) st4(p + q, *reinterpret_cast<const V(*)[4]>(v + q));
 }
 
 // ---- release/acquire progress counters (CTA scope, shared memory)
@@ -324,9 +339,9 @@ template <int KIND, bool FWD, class V>
 __device__ __forceinline__ void load_step_in(StepIn<V> &in, const LatState<V> &f, const V *er,
                                              const BndT<V> *bi, int lane) {
   if (KIND == kCtc) {   // even states are blanks: one shared Et
-    in.E[0] = in.E[2] = er[f.tok[0]];
-    in.E[1] = er[f.tok[1]];
-    in.E[3] = er[f.tok[3]];
+    const V eblank = er[f.tok[0]];
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) in.E[k] = (k & 1) ? er[f.tok[k]] : eblank;
   } else {
 #pragma unroll
     for (int k = 0; k < kSpl; ++k) in.E[k] = er[f.tok[k]];
@@ -428,7 +443,7 @@ template <class V>
 __device__ __forceinline__ void lat_store_row(const LatState<V> &f, V *row, int *erow, int lane,
                                               bool live) {
   if (live) {
-    st4(row + lane * kSpl, f.v);
+    stv(row + lane * kSpl, f.v);
     erow[lane] = f.ex;
   }
 }

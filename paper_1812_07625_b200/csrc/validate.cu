@@ -27,10 +27,13 @@ constexpr int kBitRowLse = 1 << 9;
 // contiguous range, loaded coalesced into shared memory, then lane r checks
 // row r.  The CTC row normalisation is checked in fp32 and re-checked in
 // float64 (the reference's arithmetic) only near the 1e-2 threshold.
+// route (nullable, zeroed beforehand): precision routing counters of the
+// batch, [0] rows checked, [1] rows whose spread max - min exceeds
+// route_nats, [2] rows whose spread exceeds kFlushNats (see route_to_f64).
 template <class TE>
 __global__ void __launch_bounds__(128)
     em_check_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len, Dims d,
-                    int check_lse, int32_t *status) {
+                    int check_lse, int32_t *status, int *route, float route_nats) {
   __shared__ TE rows[4][32 * 32];
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -43,14 +46,17 @@ __global__ void __launch_bounds__(128)
   for (int e = lane; e < nrows * N; e += 32) buf[e] = src[e];
   __syncwarp();
   int bits = 0;
+  float spread = 0.f;
   if (lane < nrows) {
     const TE *r = buf + lane * N;
-    float m = -CUDART_INF_F;
+    float m = -CUDART_INF_F, mn = CUDART_INF_F;
     for (int i = 0; i < N; ++i) {
       const double v = (double)r[i];
       if (!isfinite(v)) bits = kBitNonFinite;
       m = fmaxf(m, (float)v);
+      mn = fminf(mn, (float)v);
     }
+    spread = m - mn;
     if (check_lse && !bits) {
       // rows must be log-normalised: |logsumexp| <= 1e-2 (criterion.py:96-101).
       // float inputs: an fp32 pre-check, re-checked in float64 (the
@@ -81,6 +87,15 @@ __global__ void __launch_bounds__(128)
   }
   bits = __reduce_or_sync(0xffffffffu, bits);
   if (lane == 0 && bits) atomicOr(&status[b], bits);
+  if (route) {
+    const unsigned wide = __ballot_sync(0xffffffffu, lane < nrows && spread > route_nats);
+    const unsigned hard = __ballot_sync(0xffffffffu, lane < nrows && spread > kFlushNats);
+    if (lane == 0) {
+      atomicAdd(&route[0], nrows);
+      if (wide) atomicAdd(&route[1], __popc(wide));
+      if (hard) atomicAdd(&route[2], __popc(hard));
+    }
+  }
 }
 
 __device__ bool block_any(int v) { return __syncthreads_or(v); }
@@ -254,11 +269,16 @@ __global__ void viterbi_prep_kernel(const int32_t *__restrict__ em_len, Dims d,
 
 template <class TE>
 cudaError_t em_check(const TE *em, const int32_t *em_len, Dims d, int check_lse,
-                     int32_t *status, cudaStream_t s) {
+                     int32_t *status, cudaStream_t s, int *route = nullptr,
+                     float route_nats = 0.f) {
   cudaError_t err = cudaMemsetAsync(status, 0, sizeof(int32_t) * d.B, s);
   if (err != cudaSuccess) return err;
+  if (route) {
+    err = cudaMemsetAsync(route, 0, sizeof(int) * kRouteWords, s);
+    if (err != cudaSuccess) return err;
+  }
   dim3 grid((d.Tmax + 127) / 128, d.B);
-  em_check_kernel<TE><<<grid, 128, 0, s>>>(em, em_len, d, check_lse, status);
+  em_check_kernel<TE><<<grid, 128, 0, s>>>(em, em_len, d, check_lse, status, route, route_nats);
   return cudaGetLastError();
 }
 
@@ -268,8 +288,8 @@ template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
                                 int *perm, int *tok_start, int32_t *status, cudaStream_t s,
-                                int mode) {
-  cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s);
+                                int mode, int *route) {
+  cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s, route, kRouteNatsAsg);
   if (err != cudaSuccess) return err;
   asg_prep_kernel<TE><<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, trans, d, lpad, perm,
                                           tok_start, status, mode);
@@ -279,8 +299,8 @@ template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
                                 int *tok_start, int32_t *status, cudaStream_t s, int check_lse,
-                                int mode) {
-  cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s);
+                                int mode, int *route) {
+  cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s, route, kRouteNatsCtc);
   if (err != cudaSuccess) return err;
   ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
                                       status, mode);
@@ -298,10 +318,10 @@ cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
 #define INST(TE)                                                                           \
   template cudaError_t launch_asg_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, const TE *, Dims, int, int *, \
-                                               int *, int32_t *, cudaStream_t, int);          \
+                                               int *, int32_t *, cudaStream_t, int, int *);   \
   template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, int, Dims, int, int *, int *, \
-                                               int32_t *, cudaStream_t, int, int);            \
+                                               int32_t *, cudaStream_t, int, int, int *);     \
   template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,         \
                                                    int32_t *, cudaStream_t);
 INST(float)

@@ -249,3 +249,20 @@ def test_peaky_emissions_resolved_by_fp64_tier(scale):
     outc = C.ctc_loss_grad_batched(x, el, tc, tl, blank, fallback="f64", check=False)
     assert (outc.status.cpu().numpy() == 0).all()
     _check_ctc(outc, *pool.ctc_batch(em, el, tc, tl, blank), el)
+
+
+@pytest.mark.parametrize("scale", [2.0, 5.0, 10.0, 20.0])
+def test_precision_routing_keeps_results(scale):
+    # W2L_FLAG_NO_ROUTE: the routing (peaky batches straight to the fp64
+    # tier) changes which tier computes, never the results: routed and
+    # unrouted calls both match the oracle at 1e-4 and each other
+    import bench
+    em, el, ta, tc, tl, a, blank = bench.peaky_inputs(scale, b=12)
+    x = torch.from_numpy(em).cuda()
+    want_a = pool.asg_batch(em, el, ta, tl, a)
+    want_c = pool.ctc_batch(em, el, tc, tl, blank)
+    for rt in (True, False):
+        out = C.asg_loss_grad_batched(x, el, ta, tl, a, route=rt, per_utterance_grad_transitions=True)
+        _check_asg(out, *want_a, el)
+        outc = C.ctc_loss_grad_batched(x, el, tc, tl, blank, route=rt)
+        _check_ctc(outc, *want_c, el)
