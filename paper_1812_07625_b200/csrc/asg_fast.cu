@@ -31,6 +31,7 @@
 
 #include <algorithm>
 
+#include "band.cuh"
 #include "laneblock.cuh"
 #include "lattice.cuh"
 #include "common.cuh"
@@ -287,6 +288,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     // the fcc uses every token
     ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + weff, 0,
                d.N >= 32 ? 0xffffffffu : (1u << d.N) - 1u};
+    pc.gprog = w.prog ? w.prog + 2 * b + (FWD ? 0 : 1) : nullptr;
     producer_run<V>(sm, pc, lane, nullptr);
   } else if (warp == 1) {
     FccCtx<V> fc;
@@ -320,6 +322,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
   if (threadIdx.x == 0) {
     w.scal[b * 4 + (FWD ? 2 : 3)] = lattice_total(sm, weff);
     if (sm.flush) status[b] = fail;
+    if (w.prog) st_release_gpu(w.prog + 2 * b + (FWD ? 0 : 1), T);   // last write of the CTA
   }
 }
 
@@ -332,10 +335,19 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
                      int32_t *__restrict__ status, int want, int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
+  pdl_launch_dependents();
+  W2L_TL(const unsigned long long tl0 = gtimer());
   const int b = blockIdx.x;
-  if (status[b] != want) return;
+  int *gprog = w.prog ? w.prog + 2 * b + blockIdx.y : nullptr;
+  if (status[b] != want) {
+    if (gprog && threadIdx.x == 0) st_release_gpu(gprog, kProgIdle);
+    return;
+  }
   if (want == W2L_OK && route_to_f64(w.route)) {   // the batch goes to the fp64 tier
-    if (threadIdx.x == 0 && blockIdx.y == 0) status[b] = kNeedsF64;
+    if (threadIdx.x == 0) {
+      if (blockIdx.y == 0) status[b] = kNeedsF64;
+      if (gprog) st_release_gpu(gprog, kProgIdle);
+    }
     return;
   }
   const int T = em_len[b], L = tgt_len[b];
@@ -349,6 +361,7 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_body<true, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
   else
     asg_chain_body<false, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
+  W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), 0));
 }
 
 // ----------------------------------------------------------- grad kernel --
@@ -373,21 +386,16 @@ static_assert(fcc_stage_bytes<float>() >= 4096, "the staging area doubles as the
 template <class V>
 __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
                                                   const int32_t *__restrict__ em_len, Dims d,
-                                                  const AsgFastWs &w,
-                                                  const int32_t *__restrict__ status, int want,
+                                                  const AsgFastWs &w, int ust, int want, int b,
                                                   int blk, unsigned char *smem) {
-  __shared__ float gwarp[kGradWarps][2];
-  const int b = blockIdx.y;
+  __shared__ double gwarp[kGradWarps][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
   const int T = em_len[b];
   const int t0 = blk * kFccFrames;
-  if (status[b] != want || t0 >= T) return;
+  if (ust != want || t0 >= T) return;
   const int ta = t0 + warp * kFccFpw, tb = min(ta + kFccFpw, d.Tmax);
-  const double refF = w.scal[b * 4 + 0] * 1.4426950408889634;
-  const int refFi = isfinite(refF) ? (int)floor(refF) : 0;
-  const float refFf = isfinite(refF) ? (float)(refF - refFi) : CUDART_NAN_F;
-  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
+  double gmin = CUDART_INF, gmax = -CUDART_INF;
   const int tend = min(tb, T);
 
   // ---- stage this warp's frames: row r of sfa/ska is frame ta-1+r, row r of
@@ -415,8 +423,10 @@ __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
     for (int i = lane; i < nf * N; i += 32) cp_async4(se + i, e_g + i);
     const int *ka_g = w.fcc_ka + (size_t)b * w.tpad;
     const int *kb_g = w.fcc_kb + (size_t)b * w.tpad + 1;
-    if (lane < tend - f0) cp_async4(ska + (f0 - (ta - 1)) + lane, ka_g + f0 + lane);
-    if (lane < nf) cp_async4(skb + lane, kb_g + ta + lane);
+    // (L2 loads: these words share cache lines with frames a concurrently
+    // running chain may not have written yet)
+    if (lane < tend - f0) ska[(f0 - (ta - 1)) + lane] = __ldcg(ka_g + f0 + lane);
+    if (lane < nf) skb[lane] = __ldcg(kb_g + ta + lane);
     cp_async_commit();
     cp_async_wait<0>();
   }
@@ -444,9 +454,10 @@ __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
     float lz;
     if constexpr (sizeof(V) == 4) lz = __log2f(zf);
     else lz = (float)log2(zf);
-    const float g = lz + (float)(ka + kb - refFi) - refFf;
-    gmin = fminf(gmin, g);
-    gmax = fmaxf(gmax, g);
+    // the frame's log2-normaliser
+    const double g = (double)lz + (double)(ka + kb);
+    gmin = fmin(gmin, g);
+    gmax = fmax(gmax, g);
     if (t >= 1) {
       // fcc edge posteriors (:240-241): u_t[i] alpha_{t-1}[j] (times M later)
       const V u = et * fb * Pow2<V>::p2(ska[r] - ka) * izf;
@@ -490,72 +501,52 @@ __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
     dstA[i] = s;
   }
   if (threadIdx.x < 2) {
-    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    double g = threadIdx.x ? -CUDART_INF : CUDART_INF;
     for (int q = 0; q < kGradWarps; ++q)
-      g = threadIdx.x ? fmaxf(g, gwarp[q][1]) : fminf(g, gwarp[q][0]);
+      g = threadIdx.x ? fmax(g, gwarp[q][1]) : fmin(g, gwarp[q][0]);
     w.part_guard[((size_t)b * w.nblk + blk) * 4 + threadIdx.x] = g;
   }
 }
 
-// sum of the shared-memory floats at addresses addr[q0 .. q1) (4 independent
-// chains; addresses are absolute shared-window addresses)
+// one shared-memory float at an absolute shared-window address
 __device__ __forceinline__ float lds_f32(unsigned a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ float gather_shared(const unsigned *addr, int q0, int q1) {
-  float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-  int q = q0;
-  for (; q + 4 <= q1; q += 4) {
-    const unsigned a0 = addr[q], a1 = addr[q + 1], a2 = addr[q + 2], a3 = addr[q + 3];
-    c0 += lds_f32(a0);
-    c1 += lds_f32(a1);
-    c2 += lds_f32(a2);
-    c3 += lds_f32(a3);
-  }
-  // tail of up to 3 (independent loads, predicated)
-  const int r = q1 - q;
-  const unsigned a0 = r > 0 ? addr[q] : 0u, a1 = r > 1 ? addr[q + 1] : 0u, a2 = r > 2 ? addr[q + 2] : 0u;
-  if (r > 0) c0 += lds_f32(a0);
-  if (r > 1) c1 += lds_f32(a1);
-  if (r > 2) c2 += lds_f32(a2);
-  return (c0 + c1) + (c2 + c3);
-}
-
 template <int W>
 constexpr size_t fac_grad_smem() {
-  return sizeof(float) * (kGradWarps * ((size_t)W * kLatStates + 2 + 2 + 2 * (size_t)W * kLatStates));
+  // per warp: posterior row + occupancy row (floats), guard (2 doubles),
+  // token bins; the CTA's lane-block tokens
+  return sizeof(float) * (kGradWarps * (2 * (size_t)W * kLatStates + 4 + 32) +
+                          (size_t)W * kLatStates / kSpl);
 }
 
 // The whole gradient row: fcc node posteriors (full part, :238) minus the
 // fac node posteriors gathered by token (:214-217), plus the fac occupancy.
-// A warp handles consecutive frames; each frame's rows are loaded one frame
-// ahead.  Lanes past the lattice's last state were never stored: zeros.
+// A warp walks consecutive frames with the band-limited reads of band.cuh
+// (fac posterior mass moves by 0 or 1 state per frame).
 //
 // Fac edge sums need no edge products: a forced alignment enters every state
 // l >= 1 exactly once and stays in state l (n_l - 1) times, n_l its frame
 // count, so the summed posteriors of the stay and step edges (:218-224) are
 // occ(l) - 1 and 1, occ(l) = sum_t of the node posterior.  Only occ is
-// accumulated here; asg_final applies the identity.
+// accumulated here (per warp, in shared memory: a lane's blocks move with
+// the window); asg_final applies the identity.
 template <int W, class V>
 __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em_len,
+                                                  const int64_t *__restrict__ tgt,
                                                   const int32_t *__restrict__ tgt_len, Dims d,
                                                   const AsgFastWs &w, float *__restrict__ grad_em,
-                                                  const int32_t *__restrict__ status, int want,
-                                                  int blk, unsigned char *smem) {
+                                                  int st, int want, int b, int blk,
+                                                  unsigned char *smem) {
   constexpr int LP = W * kLatStates;
-  // [kGradWarps][LP] posterior row; after its frame loop each warp reuses
-  // its own row for the occupancy partials (redE)
-  float *prow = reinterpret_cast<float *>(smem);
-  float *redE = prow;
-  float *zcell = prow + kGradWarps * LP;         // [kGradWarps][2] zero cells
-  float *gwarp = zcell + kGradWarps * 2;         // [kGradWarps][2] guard
-  // per-warp token CSR as absolute shared addresses into that warp's
-  // posterior row (the gather is then load-address, load-value, add)
-  unsigned *saddr = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][2 LP]
+  float *prow = reinterpret_cast<float *>(smem);       // [kGradWarps][LP] wide-window posteriors
+  float *occ = prow + kGradWarps * LP;                 // [kGradWarps][LP] occupancy
+  double *gwarp = reinterpret_cast<double *>(occ + kGradWarps * LP);   // [kGradWarps][2]
+  unsigned *bins = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][32]
+  unsigned *stok = bins + kGradWarps * 32;             // [LP / kSpl] tokens per lane block
 
-  const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
   const int T = em_len[b];
@@ -563,7 +554,6 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
-  const int st = status[b];
   if (want == W2L_OK) {
     // the first tier owns the zeros: padding frames and utterances it does
     // not compute (a later tier rewrites the rows of the ones it takes)
@@ -573,152 +563,132 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   if (st != want || t0 >= T) return;
 
   const int L = tgt_len[b];
-  // lattice warps the chain wrote for this utterance (the batch's W may be wider)
-  const int weff = min(lat_warps(L), W);
   float *myp = prow + warp * LP;
-  unsigned *myaddr = saddr + warp * 2 * LP;
-  if (lane == 0) zcell[warp * 2] = 0.f;   // padding entries of the gather table
-  const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
-  const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
-  // Token gather table: column `lane` lists the shared addresses (in this
-  // warp's posterior row) of the states labelled `lane`, padded with a zero
-  // cell to a uniform depth G4 -- every lane then runs the same unrolled loop
-  // (no divergence, no tail).  Falls back to the CSR walk if too deep.
-  const int g4 = (warp_max(ts1 - ts0) + 3) & ~3;
-  const bool uniform = g4 * 32 <= 2 * LP;
-  {
-    const unsigned base = (unsigned)__cvta_generic_to_shared(myp);
-    const unsigned zero = (unsigned)__cvta_generic_to_shared(zcell + warp * 2);
-    const int *perm = w.perm + (size_t)b * w.lpad;
-    if (uniform) {
-      for (int q = 0; q < g4; ++q)
-        myaddr[q * 32 + lane] = ts0 + q < ts1 ? base + 4u * (unsigned)perm[ts0 + q] : zero;
-    } else {
-      for (int i = lane; i < L; i += 32) myaddr[i] = base + 4u * (unsigned)perm[i];
-    }
+  float *myo = occ + warp * LP;
+  unsigned *mybins = bins + warp * 32;
+  for (int i = lane; i < LP; i += 32) myo[i] = 0.f;
+  mybins[lane] = 0u;
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  for (int m = threadIdx.x; m < (L + kSpl - 1) / kSpl; m += blockDim.x) {
+    unsigned v = 0;
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k)
+      v |= (m * kSpl + k < L ? (unsigned)y[m * kSpl + k] : 0xffu) << (8 * k);
+    stok[m] = v;
   }
   __syncthreads();
-  const double refC = w.scal[b * 4 + 2] * 1.4426950408889634;
-  const int refCi = isfinite(refC) ? (int)floor(refC) : 0;
-  const float refCf = isfinite(refC) ? (float)(refC - refCi) : CUDART_NAN_F;
-  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
-
+  double gmin = CUDART_INF, gmax = -CUDART_INF;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  const V *A = reinterpret_cast<const V *>(w.fac_a) + seg0 * kLatStates + lane * kSpl;
-  const V *Bv = reinterpret_cast<const V *>(w.fac_b) + seg0 * kLatStates + lane * kSpl;
-  const int *EA = w.fac_ea + seg0 * 32 + lane;
-  const int *EB = w.fac_eb + seg0 * 32 + lane;
-  const size_t segv = (size_t)d.Tmax * kLatStates;
-  const size_t sege = (size_t)d.Tmax * 32;
-
-  float accO[W][kSpl];
-#pragma unroll
-  for (int sw = 0; sw < W; ++sw)
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) accO[sw][k] = 0.f;
   const int tend = min(tb, T);
+
   // the fcc rows of the next frame (full-part node posteriors) are loaded one
   // frame ahead
   const V *fca = reinterpret_cast<const V *>(w.fcc_a) + (size_t)b * d.Tmax * 32 + lane;
   const V *fcb = reinterpret_cast<const V *>(w.fcc_b) + (size_t)b * d.Tmax * 32 + lane;
   V ca_nx = (V)0, cb_nx = (V)0;
   if (ta < tend) {
-    ca_nx = fca[(size_t)ta * 32];
-    cb_nx = fcb[(size_t)ta * 32];
+    ca_nx = __ldcg(fca + (size_t)ta * 32);
+    cb_nx = __ldcg(fcb + (size_t)ta * 32);
   }
-  // the rows are loaded one frame ahead too (lanes past the lattice read zeros)
-  V na[W][kSpl], nb[W][kSpl];
-  int nea[W], neb[W];
-  bool live[W];
+  BandRows<V> br;
+  br.A = reinterpret_cast<const V *>(w.fac_a) + seg0 * kLatStates;
+  br.B = reinterpret_cast<const V *>(w.fac_b) + seg0 * kLatStates;
+  br.EA = w.fac_ea + seg0 * 32;
+  br.EB = w.fac_eb + seg0 * 32;
+  br.segv = (size_t)d.Tmax * kLatStates;
+  br.sege = (size_t)d.Tmax * 32;
+  br.S = L;
+  br.nblk = (L + kSpl - 1) / kSpl;
+  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window
+  const int ref = ta < tend ? br.reference(ta, lane) : 0;
+  V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
+  int pe[kBandRounds];
 #pragma unroll
-  for (int sw = 0; sw < W; ++sw) {
-    live[sw] = sw < weff && sw * kLatStates + lane * kSpl < L;
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) na[sw][k] = nb[sw][k] = (V)0;
-    nea[sw] = neb[sw] = kNegExp;
-    if (live[sw] && ta < tend) {
-      const size_t tq = (size_t)ta * kLatStates;
-      ldv(A + sw * segv + tq, na[sw]);
-      ldv(Bv + sw * segv + tq, nb[sw]);
-      nea[sw] = EA[sw * sege + (size_t)ta * 32];
-      neb[sw] = EB[sw * sege + (size_t)ta * 32];
-    }
-  }
+  for (int r = 0; r < kBandRounds; ++r)
+    br.load(mlo + lane + 32 * r, ta, ta < tend && mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
   for (int t = ta; t < tend; ++t) {
-    V va[W][kSpl], vb[W][kSpl];
-    int ea[W], eb[W];
-#pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-#pragma unroll
-      for (int k = 0; k < kSpl; ++k) {
-        va[sw][k] = na[sw][k];
-        vb[sw][k] = nb[sw][k];
-      }
-      ea[sw] = nea[sw];
-      eb[sw] = neb[sw];
-      if (live[sw] && t + 1 < tend) {
-        const size_t tq = (size_t)(t + 1) * kLatStates;
-        ldv(A + sw * segv + tq, na[sw]);
-        ldv(Bv + sw * segv + tq, nb[sw]);
-        nea[sw] = EA[sw * sege + (size_t)(t + 1) * 32];
-        neb[sw] = EB[sw * sege + (size_t)(t + 1) * 32];
-      }
-    }
     const float gam = (float)(ca_nx * cb_nx);   // fcc node posterior, unnormalised
     if (t + 1 < tend) {
-      ca_nx = fca[(size_t)(t + 1) * 32];
-      cb_nx = fcb[(size_t)(t + 1) * 32];
+      ca_nx = __ldcg(fca + (size_t)(t + 1) * 32);
+      cb_nx = __ldcg(fcb + (size_t)(t + 1) * 32);
     }
     // fac node posteriors (:214-217)
     float zl = 0.f;
-    float p[W][kSpl];
+    int lo = INT_MAX, hi = -1;
+    float qr[kBandRounds][kSpl];
+    auto take = [&](const V (&va)[kSpl], const V (&vb)[kSpl], int e, int m, float (&q)[kSpl],
+                    bool keep) {
 #pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-      const V sc = pow2_clamped<V>(ea[sw] + eb[sw] - refCi);
+      for (int k = 0; k < kSpl; ++k) q[k] = 0.f;
+      if (e == INT_MIN) return;
+      band_block<V>(va, vb, e, ref, m, q, lo, hi);
+      if (keep) stv(myp + m * kSpl, q);
 #pragma unroll
-      for (int k = 0; k < kSpl; ++k) p[sw][k] = (float)(va[sw][k] * vb[sw][k] * sc);
-      stv(myp + sw * kLatStates + lane * kSpl, p[sw]);
+      for (int k = 0; k < kSpl; ++k) zl += q[k];
+    };
 #pragma unroll
-      for (int k = 0; k < kSpl; k += 2) zl += p[sw][k] + p[sw][k + 1];
+    for (int r = 0; r < kBandRounds; ++r)
+      take(pa[r], pb[r], pe[r], mlo + lane + 32 * r, qr[r], false);
+    for (int m = mlo + lane + 32 * kBandRounds; m <= mhi; m += 32) {   // wide windows
+      V va[kSpl], vb[kSpl];
+      float q[kSpl];
+      int e;
+      br.load(m, t, true, va, vb, e);
+      take(va, vb, e, m, q, true);
+    }
+    const int cmlo = mlo, cmhi = mhi;
+    // the next frame's window (fac mass moves by 0 or 1 state per frame)
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi >= lo) {
+      mlo = lo / kSpl;
+      mhi = min(hi + 1, L - 1) / kSpl;
+    } else {   // nothing above the threshold (cannot happen for a finite loss): read all
+      mlo = 0;
+      mhi = br.nblk - 1;
+    }
+    if (t + 1 < tend) {
+#pragma unroll
+      for (int r = 0; r < kBandRounds; ++r)
+        br.load(mlo + lane + 32 * r, t + 1, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
     }
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
     const float izf = 1.f / warp_sum(gam);
-    const float g = __log2f(zc) - refCf;
-    gmin = fminf(gmin, g);
-    gmax = fmaxf(gmax, g);
+    const double g = (double)ref + (double)__log2f(zc);   // the frame's log2-normaliser
+    gmin = fmin(gmin, g);
+    gmax = fmax(gmax, g);
+    // token bins and state occupancies of this frame's window (a lane owns
+    // its blocks: plain shared read-modify-write for the occupancy)
+    auto settle = [&](const float (&q)[kSpl], int m) {
+      band_scatter(q, izc, stok[m], mybins);
+      float o[kSpl];
+      ldv(myo + m * kSpl, o);
 #pragma unroll
-    for (int sw = 0; sw < W; ++sw)
+      for (int k = 0; k < kSpl; ++k) o[k] = fmaf(q[k], izc, o[k]);
+      stv(myo + m * kSpl, o);
+    };
 #pragma unroll
-      for (int k = 0; k < kSpl; ++k) accO[sw][k] = fmaf(p[sw][k], izc, accO[sw][k]);
-    __syncwarp();
-    // token gather: lane k sums the posteriors of the states labelled k
-    float con;
-    if (uniform) {
-      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-      for (int q = 0; q < g4; q += 4) {
-        const unsigned a0 = myaddr[q * 32 + lane], a1 = myaddr[(q + 1) * 32 + lane];
-        const unsigned a2 = myaddr[(q + 2) * 32 + lane], a3 = myaddr[(q + 3) * 32 + lane];
-        c0 += lds_f32(a0);
-        c1 += lds_f32(a1);
-        c2 += lds_f32(a2);
-        c3 += lds_f32(a3);
-      }
-      con = (c0 + c1) + (c2 + c3);
-    } else {
-      con = gather_shared(myaddr, ts0, ts1);
+    for (int r = 0; r < kBandRounds; ++r) {
+      const int m = cmlo + lane + 32 * r;
+      if (m <= cmhi && m < br.nblk) settle(qr[r], m);
     }
-    if (lane < N) ge[(size_t)t * N + lane] = gam * izf - con * izc;
+    for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+      if (m < br.nblk) {
+        float q[kSpl];
+        ldv(myp + m * kSpl, q);
+        settle(q, m);
+      }
+    }
+    __syncwarp();
+    const float con = (float)mybins[lane] * kFixInv;
+    mybins[lane] = 0u;
+    if (lane < N) ge[(size_t)t * N + lane] = gam * izf - con;
     __syncwarp();
   }
 
   // ---- block reduction of the occupancy partials in fixed warp order
   // (deterministic)
-  float *rE = redE + warp * LP;
-#pragma unroll
-  for (int sw = 0; sw < W; ++sw)
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) rE[sw * kLatStates + lane * kSpl + k] = accO[sw][k];
   if (lane == 0) {
     gwarp[warp * 2 + 0] = gmin;
     gwarp[warp * 2 + 1] = gmax;
@@ -727,14 +697,14 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   float *dstE = w.part_edge + ((size_t)b * w.nblk + blk) * LP;
   for (int i = threadIdx.x; i < LP; i += blockDim.x) {
     float s = 0.f;
-    for (int q = 0; q < kGradWarps; ++q) s += redE[q * LP + i];
+    for (int q = 0; q < kGradWarps; ++q) s += occ[q * LP + i];
     dstE[i] = s;
   }
   if (threadIdx.x < 2) {
-    float g2 = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    double g2 = threadIdx.x ? -CUDART_INF : CUDART_INF;
     for (int q = 0; q < kGradWarps; ++q) {
-      const float v = gwarp[q * 2 + threadIdx.x];
-      g2 = threadIdx.x ? fmaxf(g2, v) : fminf(g2, v);
+      const double v = gwarp[q * 2 + threadIdx.x];
+      g2 = threadIdx.x ? fmax(g2, v) : fmin(g2, v);
     }
     w.part_guard[((size_t)b * w.nblk + blk) * 4 + 2 + threadIdx.x] = g2;
   }
@@ -757,6 +727,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ int sperm[W2L_MAX_ASG_LABELS];   // token CSR
   __shared__ int sts[33];
   const int N = d.N, NN = N * N;
+  if (threadIdx.x < 2 && w.prog) w.prog[2 * b + threadIdx.x] = 0;   // next tier / call
   const int st = status[b];
   if (st != want) {
     // the first tier owns the zeros of the utterances it does not compute
@@ -823,9 +794,10 @@ __global__ void __launch_bounds__(1024)
   int bad = !(isfinite(zF) && isfinite(zFb) && isfinite(zC) && isfinite(zCb));
   bad |= !(fabs(zF - zFb) <= tol) || !(fabs(zC - zCb) <= tol);
   for (int q = threadIdx.x; q < nb_used; q += blockDim.x) {
-    const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 4;
-    bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
-    bad |= !(fabs((double)g[2]) * ln2 <= tol && fabs((double)g[3]) * ln2 <= tol);
+    // every frame's log-normaliser (log2 units) must reproduce the totals
+    const double *g = w.part_guard + ((size_t)b * w.nblk + q) * 4;
+    bad |= !(fabs(g[0] * ln2 - zF) <= tol && fabs(g[1] * ln2 - zF) <= tol);
+    bad |= !(fabs(g[2] * ln2 - zC) <= tol && fabs(g[3] * ln2 - zC) <= tol);
   }
   if (bad) atomicOr(&s_bad, 1);
   __syncthreads();
@@ -854,32 +826,43 @@ __global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d,
 // run side by side.  The kinds alternate in x (even: fac + gradient row,
 // odd: fcc edges; 128 frames each), so both are dispatched from the start of
 // the launch.  With the kinds in blockIdx.z instead every fac CTA was
-// dispatched before any fcc CTA (slower).
+// dispatched before any fcc CTA (slower).  Grid (2B, nblk): y is the frame
+// block's completion rank (block_of_rank), so with PDL the CTAs run in the
+// order the two chains complete their frames; prog (null: the chains have
+// finished) gates them.
 template <int W, class V>
-__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? 2 : 1)
+__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? (sizeof(V) == 4 ? 3 : 2) : 1)
     asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     const float *__restrict__ trans, Dims d, AsgFastWs w,
-                    float *__restrict__ grad_em, const int32_t *__restrict__ status, int want) {
+                    float *__restrict__ grad_em, const int32_t *__restrict__ status, int want,
+                    const int *prog) {
   extern __shared__ __align__(16) unsigned char gsm[];
-  const int blk = blockIdx.x >> 1;
+  const int b = blockIdx.x >> 1, blk = block_of_rank(blockIdx.y, w.nblk);
+  const int T = em_len[b], t0 = blk * kGradFramesPerBlock;
+  W2L_TL(const unsigned long long tl0 = gtimer());
+  if (t0 < T) wait_chain_progress(prog, b, min(t0 + kGradFramesPerBlock, T), T - t0);
+  W2L_TL(const unsigned long long tl1 = gtimer());
+  const int st = *(volatile const int32_t *)(status + b);
   if (blockIdx.x & 1)
-    asg_fcc_grad_body<V>(em, em_len, d, w, status, want, blk, gsm);
+    asg_fcc_grad_body<V>(em, em_len, d, w, st, want, b, blk, gsm);
   else
-    asg_fac_grad_body<W, V>(em_len, tgt_len, d, w, grad_em, status, want, blk, gsm);
+    asg_fac_grad_body<W, V>(em_len, tgt, tgt_len, d, w, grad_em, st, want, b, blk, gsm);
+  W2L_TL(if (threadIdx.x == 0 && t0 < T) tl_rec(4000000ull + (blockIdx.x & 1) * 500000ull + b * 1000 + blk, tl0, tl1, gtimer()));
 }
 
 template <int W, class V>
 cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
-                          float *grad_em, const int32_t *status, int want, cudaStream_t s) {
+                          float *grad_em, const int32_t *status, int want, cudaStream_t s,
+                          bool stream) {
   const size_t smem = std::max(fac_grad_smem<W>(), kGradWarps * fcc_stage_bytes<V>());
   auto k = asg_grad_kernel<W, V>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<dim3(2 * w.nblk, d.B), kGradWarps * 32, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w,
-                                                         grad_em, status, want);
-  return cudaGetLastError();
+  return launch_maybe_pdl(k, dim3(2 * d.B, w.nblk), dim3(kGradWarps * 32), smem, s, stream, em,
+                          em_len, tgt, tgt_len, trans, d, w, grad_em, status, want,
+                          (const int *)(stream ? w.prog : nullptr));
 }
 
 template <class V>
@@ -888,6 +871,12 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
                             const AsgFastWs &w, double *loss, float *grad_em, float *ga_utt,
                             int32_t *status, cudaStream_t s, Tracer *tr, unsigned phases,
                             int want, int fail) {
+  // stream the gradient behind the chains (PDL) when both run in this call
+  // and no stage trace separates them; otherwise the chains publish no
+  // progress and the gradient CTAs do not wait
+  const bool stream = (phases & 1u) && (phases & 2u) && !(phases & 4u) && !tr && pdl_enabled();
+  AsgFastWs wc = w;
+  if (!stream) wc.prog = nullptr;
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
     const size_t smem = sizeof(ChainSm<V>);
@@ -900,7 +889,7 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
     // (loss only runs both directions too: their totals are its guard)
-    k<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d, w, status,
+    k<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d, wc, status,
                                                  want, fail);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
@@ -917,7 +906,7 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   case n:                                                                                    \
     if constexpr (n <= kMaxLatWarps) {                                                       \
     err = launch_grad_w<n, V>(em, em_len, tgt, tgt_len, trans, d, w, grad_em, status, want,  \
-                              s);                                                            \
+                              s, stream);                                                    \
     } else {                                                                                 \
       return cudaErrorInvalidValue;                                                          \
     }                                                                                        \
@@ -966,7 +955,8 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   t.scal = (double *)take((size_t)d.B * 4 * 8);
   t.part_fullA = (float *)take((size_t)d.B * nblk * 1024 * 4);
   t.part_edge = (float *)take((size_t)d.B * nblk * lpad * 4);
-  t.part_guard = (float *)take((size_t)d.B * nblk * 4 * 4);
+  t.part_guard = (double *)take((size_t)d.B * nblk * 4 * 8);
+  t.prog = (int *)take((size_t)d.B * 2 * 4);
   t.route = (int *)take(kRouteWords * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
@@ -978,6 +968,19 @@ static size_t asg_ws_layout(Dims d, void *base, AsgFastWs *w) {
   if (w) *w = t;
   return off;
 }
+
+#ifdef W2L_TIMELINE
+int tl_read_asg(unsigned long long *host, int maxn) {
+  unsigned n = 0;
+  cudaMemcpyFromSymbol(&n, g_tl_n, sizeof(n));
+  n = n < (unsigned)maxn ? n : (unsigned)maxn;
+  n = n < (unsigned)kTlMax ? n : (unsigned)kTlMax;
+  cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 4 * n);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(g_tl_n, &z, sizeof(z));
+  return (int)n;
+}
+#endif
 
 size_t asg_fast_ws_bytes(Dims d) { return asg_ws_layout(d, nullptr, nullptr); }
 void asg_fast_ws_carve(Dims d, void *ws, AsgFastWs *w) { asg_ws_layout(d, ws, w); }

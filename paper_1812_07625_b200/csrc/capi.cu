@@ -177,7 +177,7 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   if (phases & 1u) {
     rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
                                               w.tok_start, status, s, kPrepFast,
-                                              route ? w.route : nullptr));
+                                              route ? w.route : nullptr, w.prog));
     if (rc) return rc;
   }
   trace(tr, s);  // validate
@@ -341,7 +341,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
     // not apply to unnormalised inputs
     rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
                                               w.perm, w.tok_start, status, s, !logits,
-                                              kPrepFast, route ? w.route : nullptr));
+                                              kPrepFast, route ? w.route : nullptr, w.prog));
     if (rc) return rc;
   }
   trace(tr, s);  // validate
@@ -452,6 +452,13 @@ int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_su
   return from_cuda(launch_transitions_sgd(trans, velocity, grad_sum, N, batch_size, lr, momentum,
                                           (cudaStream_t)stream));
 }
+
+#ifdef W2L_TIMELINE
+// debug builds: CTA timeline records of the last calls (kind 0: CTC TU, 1: ASG TU)
+__attribute__((visibility("default"))) int w2l_timeline_read(int kind, unsigned long long *host, int maxn) {
+  return kind ? tl_read_asg(host, maxn) : tl_read_ctc(host, maxn);
+}
+#endif
 
 int w2l_probe_peaks(double *mufu_ops_per_s, double *dadd_ops_per_s, double *ffma_ops_per_s) {
   return probe_peaks(mufu_ops_per_s, dadd_ops_per_s, ffma_ops_per_s);

@@ -4,6 +4,10 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <climits>
+#include <utility>
 
 #include "../../include/w2l_criterion.h"
 
@@ -120,6 +124,112 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ------------------------------------------- chain -> gradient streaming --
+// The gradient kernels are launched with programmatic dependent launch (PDL)
+// right behind the chain kernel and run while the chains are still going:
+// the frames of the middle of an utterance have both their alpha and beta
+// rows once the two directions have crossed, and more frames complete with
+// every step after that.  Each chain CTA publishes its progress (steps whose
+// rows are complete) in a per-(utterance, direction) word with gpu-scope
+// release; a gradient CTA acquires the two words of its utterance before it
+// reads rows.  A chain CTA that does not run (status, routing) publishes
+// kProgIdle.  Every chain CTA executes griddepcontrol.launch_dependents on
+// entry, so the gradient grid is only scheduled once every chain CTA is
+// resident: gradient CTAs spinning on progress can never keep a chain CTA
+// from running.
+constexpr int kProgIdle = 0x7fffffff;
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// PDL: let the dependent grid launch (primary side) / no-op without PDL
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// Gradient-CTA side: wait until both directions of utterance b have
+// published at least need_f / need_b steps.  Thread 0 polls (acquire), the
+// CTA barrier then orders every thread's row loads after it.  A bound turns
+// a protocol bug into a launch error instead of a hung GPU.
+__device__ __forceinline__ void wait_chain_progress(const int *prog, int b, int need_f,
+                                                    int need_b) {
+  if (threadIdx.x == 0 && prog) {
+    unsigned spins = 0;
+    while (ld_acquire_gpu(prog + 2 * b) < need_f || ld_acquire_gpu(prog + 2 * b + 1) < need_b) {
+      __nanosleep(256);
+      if (++spins > (1u << 25)) __trap();   // ~10 s
+    }
+  }
+  __syncthreads();
+}
+
+// Gradient CTAs are scheduled in the order their frames complete: frame
+// blocks from the middle of the utterance outwards (rank 0 is the middle
+// block), all utterances of one rank next to each other.
+__host__ __device__ inline int block_of_rank(int r, int nblk) {
+  const int c = (nblk - 1) / 2;
+  const int d = (r + 1) / 2;
+  return (r & 1) ? c + d : c - d;
+}
+
+// ---- optional CTA timeline (debug builds with -DW2L_TIMELINE only): each
+// instrumented CTA appends {tag, t0, t1, t2} (globaltimer ns) to a per-
+// translation-unit buffer read back by w2l_timeline_read (tools/timeline_pdl.py)
+#ifdef W2L_TIMELINE
+constexpr int kTlMax = 1 << 16;
+static __device__ unsigned long long g_tl[kTlMax][4];
+static __device__ unsigned g_tl_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_rec(unsigned long long tag, unsigned long long t0,
+                                       unsigned long long t1, unsigned long long t2) {
+  const unsigned i = atomicAdd(&g_tl_n, 1u);
+  if (i < kTlMax) {
+    g_tl[i][0] = tag;
+    g_tl[i][1] = t0;
+    g_tl[i][2] = t1;
+    g_tl[i][3] = t2;
+  }
+}
+#define W2L_TL(x) x
+#else
+#define W2L_TL(x)
+#endif
+
+// Streamed gradients (PDL) only with W2L_PDL=1: measured slower in the
+// two-criteria step, where one criterion's gradient CTAs take the SMs the
+// other criterion's chain CTAs need.
+inline bool pdl_enabled() {
+  static const bool on = getenv("W2L_PDL") != nullptr && getenv("W2L_PDL")[0] == '1';
+  return on;
+}
+
+// Launch k, optionally as a programmatic dependent of the previous kernel
+// in the stream.
+template <class... KArgs, class... Args>
+cudaError_t launch_maybe_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, bool pdl, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 }  // namespace w2l

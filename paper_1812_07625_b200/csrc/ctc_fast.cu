@@ -18,6 +18,7 @@
 // with V = double (range 2^+-1022), and those that fail again by the float64
 // log-domain kernel (exact.cu).
 
+#include "band.cuh"
 #include "laneblock.cuh"
 #include "lattice.cuh"
 #include "common.cuh"
@@ -36,6 +37,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
   const int weff = lat_warps(S);
   if (warp == 0) {
     ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, weff, w.logits, tokmask};
+    pc.gprog = w.prog ? w.prog + 2 * b + (FWD ? 0 : 1) : nullptr;
     producer_run<V>(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
   } else if (warp - 1 < weff) {
     LatCtx c;
@@ -58,6 +60,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
   if (threadIdx.x == 0) {
     w.scal[b * 4 + (FWD ? 0 : 1)] = lattice_total(sm, weff);
     if (sm.flush) status[b] = fail;
+    if (w.prog) st_release_gpu(w.prog + 2 * b + (FWD ? 0 : 1), T);   // last write of the CTA
   }
 }
 
@@ -70,10 +73,19 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
                      int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
+  pdl_launch_dependents();
+  W2L_TL(const unsigned long long tl0 = gtimer());
   const int b = blockIdx.x;
-  if (status[b] != want) return;
+  int *gprog = w.prog ? w.prog + 2 * b + blockIdx.y : nullptr;
+  if (status[b] != want) {
+    if (gprog && threadIdx.x == 0) st_release_gpu(gprog, kProgIdle);
+    return;
+  }
   if (want == W2L_OK && route_to_f64(w.route)) {   // the batch goes to the fp64 tier
-    if (threadIdx.x == 0 && blockIdx.y == 0) status[b] = kNeedsF64;
+    if (threadIdx.x == 0) {
+      if (blockIdx.y == 0) status[b] = kNeedsF64;
+      if (gprog) st_release_gpu(gprog, kProgIdle);
+    }
     return;
   }
   const int T = em_len[b], L = tgt_len[b];
@@ -90,6 +102,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_body<true, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   else
     ctc_chain_body<false, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
+  W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), 0));
 }
 
 constexpr int kGradFramesPerBlock = 128;
@@ -97,94 +110,152 @@ constexpr int kGradWarps = 8;
 
 // One warp per frame at a time; lane i owns states 128 sw + 4 i + k of every
 // lattice warp sw and token i of the gradient row.  Posteriors are scaled
-// into range by the lane exponents against the utterance's reference
-// exponent and normalised by their own per-frame sum z_t.  Rows of lanes
-// past the lattice's last state were never stored and are read as zero.
+// into range by the lane exponents against the frame's largest exponent sum
+// and normalised by their own per-frame sum z_t; log2 z_t plus that
+// reference is the frame's log-normaliser, which the guard compares with the
+// totals.  Rows of lanes past the lattice's last state were never stored
+// and are read as zero.  Grid (B, nblk): y is the block's completion rank
+// (block_of_rank), so with PDL the CTAs run in the order the two chains
+// complete their frames; prog (null: the chains have finished) gates them.
 template <int W, class V>
 __global__ void __launch_bounds__(kGradWarps * 32)
     ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
-                    const int32_t *__restrict__ status, int want) {
+                    const int32_t *__restrict__ status, int want, const int *prog) {
   constexpr int LP = W * kLatStates;
-  __shared__ __align__(16) float prow[kGradWarps][LP];
-  __shared__ int sperm[LP];
-  __shared__ float gw[kGradWarps][2];
-  const int b = blockIdx.y, blk = blockIdx.x;
+  __shared__ __align__(16) float prow[kGradWarps][LP];   // wide-window posteriors
+  __shared__ unsigned stok[LP / kSpl];                    // label tokens per lane block (band.cuh)
+  __shared__ unsigned bins[kGradWarps][32];               // per-warp token sums (fixed point)
+  __shared__ double gw[kGradWarps][2];
+  const int b = blockIdx.x, blk = block_of_rank(blockIdx.y, w.nblk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N, T = em_len[b];
   const int t0 = blk * kGradFramesPerBlock;
-  const int st = status[b];
   float *ge = grad_em + (size_t)b * d.Tmax * N;
   const int fpw = kGradFramesPerBlock / kGradWarps;
   const int ta = t0 + warp * fpw, tb = min(ta + fpw, d.Tmax);
+  if (t0 >= T) {   // padding frames only: the first tier owns their zeros
+    if (want == W2L_OK)
+      for (int t = ta; t < tb; ++t)
+        if (lane < N) ge[(size_t)t * N + lane] = 0.f;
+    return;
+  }
+  W2L_TL(const unsigned long long tl0 = gtimer());
+  wait_chain_progress(prog, b, min(t0 + kGradFramesPerBlock, T), T - t0);
+  W2L_TL(const unsigned long long tl1 = gtimer());
+  const int st = *(volatile const int32_t *)(status + b);
   if (want == W2L_OK) {
     // the first tier owns the zeros: padding frames and utterances it does
     // not compute (a later tier rewrites the rows of the ones it takes)
     for (int t = st == W2L_OK ? max(ta, T) : ta; t < tb; ++t)
       if (lane < N) ge[(size_t)t * N + lane] = 0.f;
   }
-  if (st != want || t0 >= T) return;
+  if (st != want) return;
   const int L = tgt_len[b], S = 2 * L + 1;
-  const int weff = lat_warps(S);
-  for (int i = threadIdx.x; i < L; i += blockDim.x) sperm[i] = w.perm[(size_t)b * w.lpad + i];
+  // tokens of each lane block's label states (odd states 2l+1 carry y_l;
+  // blanks are summed apart)
+  const int64_t *y = tgt + (size_t)b * d.Lmax;
+  for (int m = threadIdx.x; m < (S + kSpl - 1) / kSpl; m += blockDim.x) {
+    unsigned v = 0;
+#pragma unroll
+    for (int k = 0; k < kSpl; ++k) {
+      const int st4 = m * kSpl + k;
+      const unsigned tk = ((st4 & 1) && st4 < S) ? (unsigned)y[st4 >> 1] : 0xffu;
+      v |= tk << (8 * k);
+    }
+    stok[m] = v;
+  }
+  bins[warp][lane] = 0u;
   __syncthreads();
-  const int ts0 = lane < N ? w.tok_start[b * 33 + lane] : 0;
-  const int ts1 = lane < N ? w.tok_start[b * 33 + lane + 1] : 0;
-  const double ref = w.scal[b * 4 + 0] * 1.4426950408889634;
-  const int refi = isfinite(ref) ? (int)floor(ref) : 0;
-  const float reff = isfinite(ref) ? (float)(ref - refi) : CUDART_NAN_F;
-  float gmin = CUDART_INF_F, gmax = -CUDART_INF_F;
+  double gmin = CUDART_INF, gmax = -CUDART_INF;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  const V *A = reinterpret_cast<const V *>(w.a) + seg0 * kLatStates + lane * kSpl;
-  const V *Bv = reinterpret_cast<const V *>(w.b) + seg0 * kLatStates + lane * kSpl;
-  const int *EA = w.ea + seg0 * 32 + lane;
-  const int *EB = w.eb + seg0 * 32 + lane;
   const size_t segv = (size_t)d.Tmax * kLatStates;
   const size_t sege = (size_t)d.Tmax * 32;
   float *myp = prow[warp];
   const int tend = min(tb, T);
+  // band-limited walk over the warp's frames (band.cuh); CTC posterior mass
+  // moves by up to 2 states per frame
+  BandRows<V> br;
+  br.A = reinterpret_cast<const V *>(w.a) + seg0 * kLatStates;
+  br.B = reinterpret_cast<const V *>(w.b) + seg0 * kLatStates;
+  br.EA = w.ea + seg0 * 32;
+  br.EB = w.eb + seg0 * 32;
+  br.segv = segv;
+  br.sege = sege;
+  br.S = S;
+  br.nblk = (S + kSpl - 1) / kSpl;
+  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window
+  unsigned *mybins = bins[warp];
+  const int ref = ta < tend ? br.reference(ta, lane) : 0;
+  V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
+  int pe[kBandRounds];
+#pragma unroll
+  for (int r = 0; r < kBandRounds; ++r)
+    br.load(mlo + lane + 32 * r, ta, ta < tend && mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
   for (int t = ta; t < tend; ++t) {
-    const size_t tq = (size_t)t * kLatStates;
     float zl = 0.f, zb = 0.f;
+    int lo = INT_MAX, hi = -1;
+    float qr[kBandRounds][kSpl];
+    auto take = [&](const V (&va)[kSpl], const V (&vb)[kSpl], int e, int m, float (&q)[kSpl],
+                    bool keep) {
 #pragma unroll
-    for (int sw = 0; sw < W; ++sw) {
-      float p[kSpl];
+      for (int k = 0; k < kSpl; ++k) q[k] = 0.f;
+      if (e == INT_MIN) return;
+      band_block<V>(va, vb, e, ref, m, q, lo, hi);
+      if (keep) stv(myp + m * kSpl, q);
 #pragma unroll
-      for (int k = 0; k < kSpl; ++k) p[k] = 0.f;
-      if (sw < weff && sw * kLatStates + lane * kSpl < S) {
-        V va[kSpl], vb[kSpl];
-        ldv(A + sw * segv + tq, va);
-        ldv(Bv + sw * segv + tq, vb);
-        const V sc = pow2_clamped<V>(EA[sw * sege + (size_t)t * 32] + EB[sw * sege + (size_t)t * 32] - refi);
-#pragma unroll
-        for (int k = 0; k < kSpl; ++k) p[k] = (float)(va[k] * vb[k] * sc);
+      for (int k = 0; k < kSpl; k += 2) {
+        zl += q[k] + q[k + 1];
+        zb += q[k];   // blank states are the even ones
       }
-      if (sw < weff) {
-        stv(myp + sw * kLatStates + lane * kSpl, p);
+    };
 #pragma unroll
-        for (int k = 0; k < kSpl; k += 2) {
-          zl += p[k] + p[k + 1];
-          zb += p[k];   // blank states are the even ones
-        }
-      }
+    for (int r = 0; r < kBandRounds; ++r)
+      take(pa[r], pb[r], pe[r], mlo + lane + 32 * r, qr[r], false);
+    const int wide0 = mlo + lane + 32 * kBandRounds;
+    for (int m = wide0; m <= mhi; m += 32) {   // wide windows (first frame, flat posteriors)
+      V va[kSpl], vb[kSpl];
+      float q[kSpl];
+      int e;
+      br.load(m, t, true, va, vb, e);
+      take(va, vb, e, m, q, true);
+    }
+    const int cmlo = mlo, cmhi = mhi;
+    // the next frame's window (CTC mass moves by up to 2 states per frame)
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi >= lo) {
+      mlo = lo / kSpl;
+      mhi = min(hi + 2, S - 1) / kSpl;
+    } else {   // nothing above the threshold (cannot happen for a finite loss): read all
+      mlo = 0;
+      mhi = br.nblk - 1;
+    }
+    if (t + 1 < tend) {
+#pragma unroll
+      for (int r = 0; r < kBandRounds; ++r)
+        br.load(mlo + lane + 32 * r, t + 1, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
     }
     const float z = warp_sum(zl);
     const float zblank = warp_sum(zb);
     const float inv = 1.f / z;
-    const float g = __log2f(z) - reff;
-    gmin = fminf(gmin, g);
-    gmax = fmaxf(gmax, g);
-    __syncwarp();
-    float c0 = lane == blank ? zblank : 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-    int q = ts0;
-    for (; q + 4 <= ts1; q += 4) {
-      c0 += myp[sperm[q]];
-      c1 += myp[sperm[q + 1]];
-      c2 += myp[sperm[q + 2]];
-      c3 += myp[sperm[q + 3]];
+    const double g = (double)ref + (double)__log2f(z);
+    gmin = fmin(gmin, g);
+    gmax = fmax(gmax, g);
+    // label posteriors into the token bins
+#pragma unroll
+    for (int r = 0; r < kBandRounds; ++r) {
+      const int m = cmlo + lane + 32 * r;
+      if (m <= cmhi && m < br.nblk) band_scatter(qr[r], inv, stok[m], mybins);
     }
-    for (; q < ts1; ++q) c0 += myp[sperm[q]];
+    for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+      if (m < br.nblk) {
+        float q[kSpl];
+        ldv(myp + m * kSpl, q);
+        band_scatter(q, inv, stok[m], mybins);
+      }
+    }
     float sm_k = 0.f;
     if (w.logits) {   // gradient w.r.t. logits: softmax - posterior
       const float x = lane < N ? em[((size_t)b * d.Tmax + t) * N + lane] : -CUDART_INF_F;
@@ -192,7 +263,10 @@ __global__ void __launch_bounds__(kGradWarps * 32)
       const float ex = lane < N ? __expf(x - mx) : 0.f;
       sm_k = ex / warp_sum(ex);
     }
-    if (lane < N) ge[(size_t)t * N + lane] = sm_k - ((c0 + c1) + (c2 + c3)) * inv;   // criterion.py:159-161
+    __syncwarp();
+    const float c = lane == blank ? zblank * inv : (float)mybins[lane] * kFixInv;
+    mybins[lane] = 0u;
+    if (lane < N) ge[(size_t)t * N + lane] = sm_k - c;   // criterion.py:159-161
     __syncwarp();
   }
   if (lane == 0) {
@@ -201,28 +275,33 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   }
   __syncthreads();
   if (threadIdx.x < 2) {
-    float g = threadIdx.x ? -CUDART_INF_F : CUDART_INF_F;
+    double g = threadIdx.x ? -CUDART_INF : CUDART_INF;
     for (int q = 0; q < kGradWarps; ++q)
-      g = threadIdx.x ? fmaxf(g, gw[q][1]) : fminf(g, gw[q][0]);
+      g = threadIdx.x ? fmax(g, gw[q][1]) : fmin(g, gw[q][0]);
     w.part_guard[((size_t)b * w.nblk + blk) * 2 + threadIdx.x] = g;
   }
+  W2L_TL(if (threadIdx.x == 0) tl_rec(2000000ull + b * 1000 + blk, tl0, tl1, gtimer()));
 }
 
 template <int W, class V>
 cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int64_t *tgt,
                               const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
-                              float *grad_em, const int32_t *status, int want, cudaStream_t s) {
-  ctc_grad_kernel<W, V><<<dim3(w.nblk, d.B), kGradWarps * 32, 0, s>>>(
-      em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want);
-  return cudaGetLastError();
+                              float *grad_em, const int32_t *status, int want, cudaStream_t s,
+                              bool stream) {
+  return launch_maybe_pdl(ctc_grad_kernel<W, V>, dim3(d.B, w.nblk), dim3(kGradWarps * 32), 0, s,
+                          stream, em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want,
+                          (const int *)(stream ? w.prog : nullptr));
 }
 
-// one warp per utterance: loss and guard verdict (partials read in parallel)
+// one warp per utterance: loss and guard verdict (partials read in parallel);
+// resets the utterance's progress words for the next tier / call
 __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
                                  double *loss, int32_t *status, int want, int fail) {
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (b >= d.B || status[b] != want) return;
+  if (b >= d.B) return;
+  if (lane < 2 && w.prog) w.prog[2 * b + lane] = 0;
+  if (status[b] != want) return;
   const int T = em_len[b];
   const double ln2 = 0.6931471805599453;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
@@ -230,8 +309,9 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
   int bad = 0;
   for (int q = lane; q < nb_used; q += 32) {
-    const float *g = w.part_guard + ((size_t)b * w.nblk + q) * 2;
-    bad |= !(fabs((double)g[0]) * ln2 <= tol && fabs((double)g[1]) * ln2 <= tol);
+    // every frame's log-normaliser (log2 units) must reproduce the total
+    const double *g = w.part_guard + ((size_t)b * w.nblk + q) * 2;
+    bad |= !(fabs(g[0] * ln2 - zA) <= tol && fabs(g[1] * ln2 - zA) <= tol);
   }
   bad = __any_sync(0xffffffffu, bad);
   if (lane == 0) {
@@ -258,6 +338,12 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
                             const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                             double *loss, float *grad_em, int32_t *status, cudaStream_t s,
                             Tracer *tr, unsigned phases, int want, int fail) {
+  // stream the gradient behind the chains (PDL) when both run in this call
+  // and no stage trace separates them; otherwise the chains publish no
+  // progress and the gradient CTAs do not wait
+  const bool stream = (phases & 1u) && (phases & 2u) && !(phases & 4u) && !tr && pdl_enabled();
+  CtcFastWs wc = w;
+  if (!stream) wc.prog = nullptr;
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
     const size_t smem = sizeof(ChainSm<V>);
@@ -270,7 +356,7 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
     // (loss only runs both directions too: their totals are its guard)
-    k<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank, d, w, status,
+    k<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank, d, wc, status,
                                                  want, fail);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
@@ -287,7 +373,7 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
   case n:                                                                                    \
     if constexpr (n <= kMaxLatWarps) {                                                       \
     err = launch_ctc_grad_w<n, V>(em, em_len, tgt, tgt_len, blank, d, w, grad_em, status,    \
-                                  want, s);                                                  \
+                                  want, s, stream);                                          \
     } else {                                                                                 \
       return cudaErrorInvalidValue;                                                          \
     }                                                                                        \
@@ -328,7 +414,8 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
   t.ea = (int *)take(BWT * 32 * 4);
   t.eb = (int *)take(BWT * 32 * 4);
   t.scal = (double *)take((size_t)d.B * 4 * 8);
-  t.part_guard = (float *)take((size_t)d.B * nblk * 2 * 4);
+  t.part_guard = (double *)take((size_t)d.B * nblk * 2 * 8);
+  t.prog = (int *)take((size_t)d.B * 2 * 4);
   t.route = (int *)take(kRouteWords * 4);
   t.perm = (int *)take((size_t)d.B * lpad * 4);
   t.tok_start = (int *)take((size_t)d.B * 33 * 4);
@@ -340,6 +427,19 @@ static size_t ctc_ws_layout(Dims d, void *base, CtcFastWs *w) {
   if (w) *w = t;
   return off;
 }
+
+#ifdef W2L_TIMELINE
+int tl_read_ctc(unsigned long long *host, int maxn) {
+  unsigned n = 0;
+  cudaMemcpyFromSymbol(&n, g_tl_n, sizeof(n));
+  n = n < (unsigned)maxn ? n : (unsigned)maxn;
+  n = n < (unsigned)kTlMax ? n : (unsigned)kTlMax;
+  cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 4 * n);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(g_tl_n, &z, sizeof(z));
+  return (int)n;
+}
+#endif
 
 size_t ctc_fast_ws_bytes(Dims d) { return ctc_ws_layout(d, nullptr, nullptr); }
 void ctc_fast_ws_carve(Dims d, void *ws, CtcFastWs *w) { ctc_ws_layout(d, ws, w); }

@@ -34,12 +34,14 @@ template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
                                 int *perm, int *tok_start, int32_t *status, cudaStream_t s,
-                                int mode = kPrepExact, int *route = nullptr);
+                                int mode = kPrepExact, int *route = nullptr,
+                                int *prog = nullptr);
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
                                 int *tok_start, int32_t *status, cudaStream_t s,
-                                int check_lse = 1, int mode = kPrepExact, int *route = nullptr);
+                                int check_lse = 1, int mode = kPrepExact, int *route = nullptr,
+                                int *prog = nullptr);
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s);
@@ -70,7 +72,8 @@ struct AsgFastWs {
   double *scal;              // [B][4]: lnZ fcc fwd, fcc bwd, fac fwd, fac bwd
   float *part_fullA;         // [B][nblk][32][32]
   float *part_edge;          // [B][nblk][Lpad]
-  float *part_guard;         // [B][nblk][4]
+  double *part_guard;        // [B][nblk][4] min / max frame log2-normalisers (fcc, fac)
+  int *prog;                 // [B][2] chain progress (streamed gradient; common.cuh)
   int *route;                // [kRouteWords] precision routing counters (em_check)
   int *perm;                 // [B][Lpad] states sorted by token
   int *tok_start;            // [B][33]
@@ -91,7 +94,8 @@ struct CtcFastWs {
   void *a, *b;               // V [B][W][Tmax][128] warp-major lattice rows
   int *ea, *eb;              // [B][W][Tmax][32]
   double *scal;              // [B][4]: lnZ fwd, lnZ bwd, sum of frame shifts, spare
-  float *part_guard;         // [B][nblk][2]
+  double *part_guard;        // [B][nblk][2] min / max frame log2-normaliser
+  int *prog;                 // [B][2] chain progress (streamed gradient; common.cuh)
   int *route;                // [kRouteWords] precision routing counters (em_check)
   int *perm;                 // [B][Lpad] label positions sorted by token
   int *tok_start;            // [B][33]
@@ -119,6 +123,11 @@ template <class TE, class TA>
 cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans, Dims d,
                            int64_t *path, double *score, const int32_t *status, void *ws,
                            cudaStream_t s);
+
+#ifdef W2L_TIMELINE
+int tl_read_ctc(unsigned long long *host, int maxn);
+int tl_read_asg(unsigned long long *host, int maxn);
+#endif
 
 // ---- microbenchmarks
 int probe_peaks(double *mufu, double *dadd, double *ffma);

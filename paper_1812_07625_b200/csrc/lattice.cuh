@@ -99,6 +99,21 @@ __device__ __forceinline__ void st4(double *p, const double (&v)[4]) {
   reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
   reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
 }
+// L2-only loads (rows written by a concurrently running chain grid)
+__device__ __forceinline__ void ld4_cg(const float *p, float (&v)[4]) {
+  const float4 x = __ldcg(reinterpret_cast<const float4 *>(p));
+  v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+__device__ __forceinline__ void ld4_cg(const double *p, double (&v)[4]) {
+  const double2 x = __ldcg(reinterpret_cast<const double2 *>(p));
+  const double2 y = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
+  v[0] = x.x, v[1] = x.y, v[2] = y.x, v[3] = y.y;
+}
+template <class V, int K>
+__device__ __forceinline__ void ldv_cg(const V *p, V (&v)[K]) {
+#pragma unroll
+  for (int q = 0; q < K; q += 4) ld4_cg(p + q, *reinterpret_cast<V(*)[4]>(v + q));
+}
 // a whole lane block (kSpl values) as 4-wide vectors
 template <class V, int K>
 __device__ __forceinline__ void ldv(const V *p, V (&v)[K]) {
@@ -157,7 +172,24 @@ struct ProdCtx {
   int nconsumers;  // counters cons[0 .. nconsumers) gate ring reuse
   int logits;      // shift term: 0 = max_i e (log-probs), 1 = -log sum_i Et (logits)
   unsigned tokmask;  // tokens whose Et enter the recursions (flush check)
+  int *gprog = nullptr;  // global progress word of this (utterance, direction), or null
 };
+
+// Publish the CTA's progress (steps whose rows every row-writing warp has
+// stored) to the global word, capped at T - 1: the final value T is
+// published by the CTA epilogue after the totals are written.  The
+// acquire of the warps' CTA-scope counters followed by the gpu-scope
+// release makes their row stores visible to a gradient CTA that acquires
+// the word (release is cumulative).  Lane 0 only.
+template <class V>
+__device__ __forceinline__ void prod_publish(ChainSm<V> &sm, const ProdCtx &c, int &last) {
+  int mn = c.T - 1;
+  for (int q = 0; q < c.nconsumers; ++q) mn = min(mn, ld_acquire(&sm.cons[q]));
+  if (mn > last) {
+    st_release_gpu(c.gprog, mn);
+    last = mn;
+  }
+}
 
 // frame of processing index p
 __device__ __forceinline__ int frame_of(bool fwd, int T, int p) { return fwd ? p : T - 1 - p; }
@@ -201,6 +233,7 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
   constexpr int kRing = Ring<V>::n;
   double shifts = 0.0;
   bool flush = false;
+  int published = 0;
   const int nch = (c.T + kChunk - 1) / kChunk;
   // kProdStages - 1 chunks in flight ahead of the one being converted (an
   // empty commit group keeps the wait count uniform past the end)
@@ -251,7 +284,17 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
     }
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
+    if (c.gprog && lane == 0) prod_publish(sm, c, published);
   }
+  // the recursions trail the producer by up to the ring depth: keep
+  // publishing until they are done (T - 1: see prod_publish)
+  if (c.gprog && lane == 0) {
+    while (published < c.T - 1) {
+      __nanosleep(512);
+      prod_publish(sm, c, published);
+    }
+  }
+  __syncwarp();
   if (__any_sync(0xffffffffu, flush) && lane == 0) sm.flush = 1;
   if (shift_sum) {
     shifts = warp_sum(shifts);

@@ -146,8 +146,9 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int64_t *__restrict__ tgt,
                                 const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans,
                                 Dims d, int lpad, int *perm, int *tok_start, int32_t *status,
-                                int mode) {
+                                int mode, int *prog) {
   const int b = blockIdx.x;
+  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int T = em_len[b], L = tgt_len[b];
   const int bits = status[b];
   __syncthreads();
@@ -214,8 +215,10 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
 __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int64_t *__restrict__ tgt,
                                 const int32_t *__restrict__ tgt_len, int blank, Dims d,
-                                int lpad, int *perm, int *tok_start, int32_t *status, int mode) {
+                                int lpad, int *perm, int *tok_start, int32_t *status, int mode,
+                                int *prog) {
   const int b = blockIdx.x;
+  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int T = em_len[b], L = tgt_len[b];
   const int bits = status[b];
   __syncthreads();
@@ -288,22 +291,22 @@ template <class TE>
 cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, const TE *trans, Dims d, int lpad,
                                 int *perm, int *tok_start, int32_t *status, cudaStream_t s,
-                                int mode, int *route) {
+                                int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s, route, kRouteNatsAsg);
   if (err != cudaSuccess) return err;
   asg_prep_kernel<TE><<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, trans, d, lpad, perm,
-                                          tok_start, status, mode);
+                                          tok_start, status, mode, prog);
   return cudaGetLastError();
 }
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
                                 const int32_t *tgt_len, int blank, Dims d, int lpad, int *perm,
                                 int *tok_start, int32_t *status, cudaStream_t s, int check_lse,
-                                int mode, int *route) {
+                                int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s, route, kRouteNatsCtc);
   if (err != cudaSuccess) return err;
   ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
-                                      status, mode);
+                                      status, mode, prog);
   return cudaGetLastError();
 }
 template <class TE>
@@ -318,10 +321,12 @@ cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
 #define INST(TE)                                                                           \
   template cudaError_t launch_asg_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, const TE *, Dims, int, int *, \
-                                               int *, int32_t *, cudaStream_t, int, int *);   \
+                                               int *, int32_t *, cudaStream_t, int, int *,    \
+                                               int *);                                        \
   template cudaError_t launch_ctc_validate<TE>(const TE *, const int32_t *, const int64_t *,  \
                                                const int32_t *, int, Dims, int, int *, int *, \
-                                               int32_t *, cudaStream_t, int, int, int *);     \
+                                               int32_t *, cudaStream_t, int, int, int *,      \
+                                               int *);                                        \
   template cudaError_t launch_viterbi_validate<TE>(const TE *, const int32_t *, Dims,         \
                                                    int32_t *, cudaStream_t);
 INST(float)

@@ -1,0 +1,81 @@
+"""CTA timeline of one streamed (PDL) call: when the chain CTAs run and when
+the gradient CTAs are dispatched, released by the chains' progress words and
+finish.  Needs a -DW2L_TIMELINE build:
+    bash tools/ab_flags.sh tl -DW2L_TIMELINE
+    W2L_LIB=abl/tl.so python tools/timeline_pdl.py [ctc|asg|both]
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_1812_07625_b200 import _native, criterion as C  # noqa: E402
+
+lib = _native.lib()
+fn = lib.w2l_timeline_read if hasattr(lib, "w2l_timeline_read") else None
+if fn is None:
+    fn = ctypes.CDLL(_native.LIB).w2l_timeline_read
+fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+fn.restype = ctypes.c_int
+buf = np.zeros((1 << 16, 4), dtype=np.uint64)
+
+
+def read(kind):
+    n = fn(kind, buf.ctypes.data, 1 << 16)
+    return buf[:n].copy()
+
+
+em, el, ta, tc, tl, A, blank = bench.make_inputs(0)
+d = torch.from_numpy(em).cuda()
+el_d, ta_d, tc_d, tl_d, A_d = (torch.from_numpy(x).cuda() for x in (el, ta, tc, tl, A))
+side = torch.cuda.Stream()
+main = torch.cuda.current_stream()
+which = sys.argv[1] if len(sys.argv) > 1 else "both"
+
+
+def call():
+    if which in ("ctc", "both"):
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False)
+    if which in ("asg", "both"):
+        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False)
+    main.wait_stream(side)
+
+
+for _ in range(5):
+    call()
+torch.cuda.synchronize()
+read(0), read(1)
+call()
+torch.cuda.synchronize()
+recs = np.concatenate([read(0), read(1)])
+tag = recs[:, 0].astype(np.int64)
+kind = tag // 1000000
+t = recs[:, 1:].astype(np.int64)
+t0 = t[kind % 2 == 1, 0].min()   # first chain CTA start
+us = lambda x: (x - t0) / 1e3
+for k, name in [(1, "ctc_chain"), (3, "asg_chain")]:
+    m = kind == k
+    if m.any():
+        print(f"{name:10s} n={m.sum():4d} start {us(t[m,0].min()):7.1f}..{us(t[m,0].max()):7.1f}"
+              f"  end {us(t[m,1].min()):7.1f}..{us(t[m,1].max()):7.1f} us")
+for k, name in [(2, "ctc_grad"), (4, "asg_grad")]:
+    m = kind == k
+    if not m.any():
+        continue
+    cend = us(t[kind == k - 1, 1].max())
+    s, w, e = us(t[m, 0]), us(t[m, 1]), us(t[m, 2])
+    busy = e - w
+    print(f"{name:10s} n={m.sum():4d} dispatch {s.min():7.1f}/{np.median(s):7.1f}/{s.max():7.1f}"
+          f"  released {w.min():7.1f}/{np.median(w):7.1f}/{w.max():7.1f}"
+          f"  end {e.min():7.1f}/{np.median(e):7.1f}/{e.max():7.1f} us (min/med/max)")
+    before = np.clip(np.minimum(e, cend) - w, 0, None).sum() / busy.sum()
+    print(f"{'':10s} CTA busy {busy.mean():6.1f} us mean; {before*100:4.1f}% of gradient CTA time"
+          f" before its chain ended ({cend:.1f} us); waited {np.mean(w - s):6.1f} us mean")
+    hist = np.histogram(e, bins=12)
+    print(f"{'':10s} end histogram: " + " ".join(f"{int(c)}@{b:.0f}" for c, b in zip(hist[0], hist[1])))
