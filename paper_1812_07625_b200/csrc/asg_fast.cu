@@ -43,6 +43,10 @@ namespace {
 constexpr int kGradFramesPerBlock = 128;   // frames per gradient CTA (both bodies)
 constexpr int kFccFrames = kGradFramesPerBlock;
 constexpr int kGradWarps = 8;
+// asg_final: one CTA per utterance; small, so that its CTAs -- launched as
+// programmatic dependents during the gradient grid's last wave -- do not
+// hold SM resources the other criterion's stream needs
+constexpr int kFinalThreads = 256;
 
 __device__ __forceinline__ float trans_max(const float *trans, int N) {
   float m = -CUDART_INF_F;
@@ -153,7 +157,9 @@ __device__ __forceinline__ void fcc_alpha_step(FccState<V> &f, V et, V (*vec)[32
   f.K += k;
   f.v = s * sc;
   vec[par][lane] = f.v;
+#ifndef W2L_NO_ROW_STORES
   out_row[lane] = f.v;
+#endif
   if (lane == 0) *outk_t = f.K;
   if (RS) {
     f.sc.observe(e1);
@@ -173,7 +179,9 @@ __device__ __forceinline__ void fcc_beta_step(FccState<V> &f, V et, V (*vec)[32]
   const V s = fcc_matvec<RS, V>(f.m, vec[par], f.spare, N, e1);
   f.K += k;
   f.v = s * sc;
+#ifndef W2L_NO_ROW_STORES
   out_row[lane] = f.v;
+#endif
   if (lane == 0) *outk_t = f.K;
   if (RS) {
     f.sc.observe(e1);
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
                      int32_t *__restrict__ status, int want, int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
-  pdl_launch_dependents();
+  pdl_wait();   // launched as a programmatic dependent of the prep / previous tier
   W2L_TL(const unsigned long long tl0 = gtimer());
   const int b = blockIdx.x;
   int *gprog = w.prog ? w.prog + 2 * b + blockIdx.y : nullptr;
@@ -350,6 +358,10 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     }
     return;
   }
+  // streamed gradient: its CTAs may launch now (they wait on the progress
+  // words); otherwise a CTA with work triggers nothing before it completes,
+  // so the gradient grid only takes SMs once the chains are done
+  if (gprog) pdl_launch_dependents();
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(L);
   if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0;
@@ -361,7 +373,7 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_body<true, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
   else
     asg_chain_body<false, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
-  W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), 0));
+  W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid()));
 }
 
 // ----------------------------------------------------------- grad kernel --
@@ -713,11 +725,12 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 // ---------------------------------------------------------- final kernel --
 // per utterance: dA_b = M (.) sum_blocks(fullA partials) - scatter(fac edge
 // sums) (criterion.py:239-246), the loss (:244) and the guard verdict.
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kFinalThreads)
     asg_final_kernel(const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
                      AsgFastWs w, double *loss, float *ga_utt, int32_t *status, int want,
                      int fail) {
+  pdl_enter();
   const int b = blockIdx.x;
   __shared__ float sEdge[kMaxLatWarps * kLatStates];
   __shared__ float sA[1024];
@@ -811,6 +824,7 @@ __global__ void __launch_bounds__(1024)
 // gradient path needs the posteriors, which loss-only mode does not form).
 __global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, AsgFastWs w,
                                      double *loss, int32_t *status, int want, int fail) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B || status[b] != want) return;
   const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
@@ -838,6 +852,8 @@ __global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? (sizeof(V) == 4 ? 3 
                     float *__restrict__ grad_em, const int32_t *__restrict__ status, int want,
                     const int *prog) {
   extern __shared__ __align__(16) unsigned char gsm[];
+  pdl_launch_dependents();
+  if (!prog) pdl_wait();   // not streamed: the chain grid must have completed
   const int b = blockIdx.x >> 1, blk = block_of_rank(blockIdx.y, w.nblk);
   const int T = em_len[b], t0 = blk * kGradFramesPerBlock;
   W2L_TL(const unsigned long long tl0 = gtimer());
@@ -860,7 +876,7 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
   auto k = asg_grad_kernel<W, V>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  return launch_maybe_pdl(k, dim3(2 * d.B, w.nblk), dim3(kGradWarps * 32), smem, s, stream, em,
+  return launch_maybe_pdl(k, dim3(2 * d.B, w.nblk), dim3(kGradWarps * 32), smem, s, true, em,
                           em_len, tgt, tgt_len, trans, d, w, grad_em, status, want,
                           (const int *)(stream ? w.prog : nullptr));
 }
@@ -879,7 +895,7 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   if (!stream) wc.prog = nullptr;
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
-    const size_t smem = sizeof(ChainSm<V>);
+    const size_t smem = chain_smem_bytes<V>();
     auto k = asg_chain_kernel<V>;
     err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
@@ -889,16 +905,16 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
     // (loss only runs both directions too: their totals are its guard)
-    k<<<dim3(d.B, 2), 32 * (2 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, trans, d, wc, status,
-                                                 want, fail);
-    err = cudaGetLastError();
+    // (a plain launch: launched early, the waiting chain CTAs would hold the
+    // shared memory the other stream's kernels need)
+    err = launch_maybe_pdl(k, dim3(d.B, 2), dim3(32 * (2 + w.W)), smem, s, false, em, em_len, tgt,
+                           tgt_len, trans, d, wc, status, want, fail);
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
   if (phases & 4u) {
-    asg_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status, want,
-                                                           fail);
-    return cudaGetLastError();
+    return launch_maybe_pdl(asg_loss_only_kernel, dim3((d.B + 127) / 128), dim3(128), 0, s, true,
+                            em_len, d, w, loss, status, want, fail);
   }
   if (!(phases & 2u)) return cudaSuccess;
   switch (w.W) {
@@ -918,9 +934,8 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   }
   if (err != cudaSuccess) return err;
   trace(tr, s);  // grad
-  asg_final_kernel<<<d.B, 1024, 0, s>>>(tgt, tgt_len, em_len, trans, d, w, loss, ga_utt, status,
-                                        want, fail);
-  err = cudaGetLastError();
+  err = launch_maybe_pdl(asg_final_kernel, dim3(d.B), dim3(kFinalThreads), 0, s, true, tgt, tgt_len, em_len,
+                         trans, d, w, loss, ga_utt, status, want, fail);
   trace(tr, s);  // final
   return err;
 }
@@ -1003,6 +1018,7 @@ cudaError_t launch_asg_fast(const float *em, const int32_t *em_len, const int64_
 // (trainer.py:442-447 sums in float64), deterministic run to run
 __global__ void reduce_grad_trans_kernel(const float *ga_utt, const int32_t *status, Dims d,
                                          float *grad_trans) {
+  pdl_enter();
   const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= d.N * d.N) return;
@@ -1036,8 +1052,8 @@ cudaError_t launch_transitions_sgd(float *w, float *v, const float *gsum, int N,
 cudaError_t launch_reduce_grad_trans(const float *ga_utt, const int32_t *status, Dims d,
                                      float *grad_trans, cudaStream_t s) {
   const int n = d.N * d.N;
-  reduce_grad_trans_kernel<<<(n + 7) / 8, 256, 0, s>>>(ga_utt, status, d, grad_trans);
-  return cudaGetLastError();
+  return launch_maybe_pdl(reduce_grad_trans_kernel, dim3((n + 7) / 8), dim3(256), 0, s, true, ga_utt,
+                          status, d, grad_trans);
 }
 
 }  // namespace w2l

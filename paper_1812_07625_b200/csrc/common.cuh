@@ -153,6 +153,19 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v) {
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
+// PDL: wait until the prerequisite grid has completed and its writes are
+// visible (no-op for a kernel launched without PDL).  Every kernel that may
+// be launched as a programmatic dependent calls it before touching data the
+// previous kernel writes; the launch sequences chain the short kernels of a
+// call this way (final, fallback tiers, reduction: their launch latency
+// overlaps the previous kernel), each kernel waiting for its predecessor,
+// which waited for its own.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// the short kernels of a launch sequence: let the next one launch, then wait
+__device__ __forceinline__ void pdl_enter() {
+  pdl_launch_dependents();
+  pdl_wait();
+}
 
 // Gradient-CTA side: wait until both directions of utterance b have
 // published at least need_f / need_b steps.  Thread 0 polls (acquire), the
@@ -190,6 +203,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
 }
 __device__ __forceinline__ void tl_rec(unsigned long long tag, unsigned long long t0,
                                        unsigned long long t1, unsigned long long t2) {

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
                      int fail) {
   extern __shared__ __align__(128) unsigned char dsm[];
   ChainSm<V> &sm = *reinterpret_cast<ChainSm<V> *>(dsm);
-  pdl_launch_dependents();
+  pdl_wait();   // launched as a programmatic dependent of the prep / previous tier
   W2L_TL(const unsigned long long tl0 = gtimer());
   const int b = blockIdx.x;
   int *gprog = w.prog ? w.prog + 2 * b + blockIdx.y : nullptr;
@@ -88,6 +88,10 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     }
     return;
   }
+  // streamed gradient: its CTAs may launch now (they wait on the progress
+  // words); otherwise a CTA with work triggers nothing before it completes,
+  // so the gradient grid only takes SMs once the chains are done
+  if (gprog) pdl_launch_dependents();
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(2 * L + 1);
   __shared__ unsigned s_mask;
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_body<true, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   else
     ctc_chain_body<false, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
-  W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), 0));
+  W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid()));
 }
 
 constexpr int kGradFramesPerBlock = 128;
@@ -128,6 +132,8 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   __shared__ unsigned stok[LP / kSpl];                    // label tokens per lane block (band.cuh)
   __shared__ unsigned bins[kGradWarps][32];               // per-warp token sums (fixed point)
   __shared__ double gw[kGradWarps][2];
+  pdl_launch_dependents();
+  if (!prog) pdl_wait();   // not streamed: the chain grid must have completed
   const int b = blockIdx.x, blk = block_of_rank(blockIdx.y, w.nblk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N, T = em_len[b];
@@ -289,7 +295,7 @@ cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int6
                               float *grad_em, const int32_t *status, int want, cudaStream_t s,
                               bool stream) {
   return launch_maybe_pdl(ctc_grad_kernel<W, V>, dim3(d.B, w.nblk), dim3(kGradWarps * 32), 0, s,
-                          stream, em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want,
+                          true, em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want,
                           (const int *)(stream ? w.prog : nullptr));
 }
 
@@ -297,6 +303,7 @@ cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int6
 // resets the utterance's progress words for the next tier / call
 __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
                                  double *loss, int32_t *status, int want, int fail) {
+  pdl_enter();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= d.B) return;
@@ -324,6 +331,7 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
 // loss only: both directions ran, their totals must agree
 __global__ void ctc_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d, CtcFastWs w,
                                      double *loss, int32_t *status, int want, int fail) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B || status[b] != want) return;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
@@ -346,7 +354,7 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
   if (!stream) wc.prog = nullptr;
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
-    const size_t smem = sizeof(ChainSm<V>);
+    const size_t smem = chain_smem_bytes<V>();
     auto k = ctc_chain_kernel<V>;
     err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
@@ -356,16 +364,16 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
                                cudaSharedmemCarveoutMaxShared);
     if (err != cudaSuccess) return err;
     // (loss only runs both directions too: their totals are its guard)
-    k<<<dim3(d.B, 2), 32 * (1 + w.W), smem, s>>>(em, em_len, tgt, tgt_len, blank, d, wc, status,
-                                                 want, fail);
-    err = cudaGetLastError();
+    // (a plain launch: launched early, the waiting chain CTAs would hold the
+    // shared memory the other stream's kernels need)
+    err = launch_maybe_pdl(k, dim3(d.B, 2), dim3(32 * (1 + w.W)), smem, s, false, em, em_len, tgt,
+                           tgt_len, blank, d, wc, status, want, fail);
     if (err != cudaSuccess) return err;
   }
   trace(tr, s);  // chain
   if (phases & 4u) {
-    ctc_loss_only_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, w, loss, status, want,
-                                                           fail);
-    return cudaGetLastError();
+    return launch_maybe_pdl(ctc_loss_only_kernel, dim3((d.B + 127) / 128), dim3(128), 0, s, true,
+                            em_len, d, w, loss, status, want, fail);
   }
   if (!(phases & 2u)) return cudaSuccess;
   switch (w.W) {
@@ -385,8 +393,8 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
   }
   if (err != cudaSuccess) return err;
   trace(tr, s);  // grad
-  ctc_final_kernel<<<(d.B + 7) / 8, 256, 0, s>>>(em_len, d, w, loss, status, want, fail);
-  err = cudaGetLastError();
+  err = launch_maybe_pdl(ctc_final_kernel, dim3((d.B + 7) / 8), dim3(256), 0, s, true, em_len, d, w,
+                         loss, status, want, fail);
   trace(tr, s);  // final
   return err;
 }

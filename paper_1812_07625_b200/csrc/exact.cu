@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kExactThreads)
                      const TE *__restrict__ trans, Dims d, int only_flagged, int nslots,
                      uint8_t *slot_ws, double *loss, float *grad_em, float *ga_utt,
                      int32_t *status) {
+  pdl_enter();
   extern __shared__ __align__(16) double sm[];
   const int N = d.N, Lmax = d.Lmax;
   double *A = sm;                       // [N][N]
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kExactThreads)
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                      int blank, Dims d, int only_flagged, int nslots, uint8_t *slot_ws,
                      double *loss, float *grad_em, int32_t *status, int logits) {
+  pdl_enter();
   extern __shared__ __align__(16) double sm[];
   const int N = d.N, Smax = 2 * d.Lmax + 1;
   double *rows = sm;                         // 2 chains x 2 buffers x Smax
@@ -407,10 +409,9 @@ cudaError_t launch_asg_exact(const TE *em, const int32_t *em_len, const int64_t 
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<nslots, kExactThreads, smem, s>>>(em, em_len, tgt, tgt_len, trans, d, only_flagged,
-                                         nslots, (uint8_t *)slot_ws, loss, grad_em, ga_utt,
-                                         status);
-  return cudaGetLastError();
+  return launch_maybe_pdl(k, dim3(nslots), dim3(kExactThreads), smem, s, true, em, em_len, tgt,
+                          tgt_len, trans, d, only_flagged, nslots, (uint8_t *)slot_ws, loss,
+                          grad_em, ga_utt, status);
 }
 
 template <class TE>
@@ -424,10 +425,9 @@ cudaError_t launch_ctc_exact(const TE *em, const int32_t *em_len, const int64_t 
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
   if (err != cudaSuccess) return err;
-  k<<<nslots, kExactThreads, smem, s>>>(em, em_len, tgt, tgt_len, blank, d, only_flagged,
-                                         nslots, (uint8_t *)slot_ws, loss, grad_em, status,
-                                         logits);
-  return cudaGetLastError();
+  return launch_maybe_pdl(k, dim3(nslots), dim3(kExactThreads), smem, s, true, em, em_len, tgt,
+                          tgt_len, blank, d, only_flagged, nslots, (uint8_t *)slot_ws, loss,
+                          grad_em, status, logits);
 }
 
 #define INST(TE)                                                                           \

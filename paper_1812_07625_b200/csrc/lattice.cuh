@@ -56,6 +56,12 @@ constexpr int kDone = 1 << 30;             // progress of a finished consumer
 constexpr int kRenormF = 4;                // steps between lane renormalisations
 constexpr int kBlk = 8;                    // steps per unrolled block (one publish / wait per block)
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
+// The producer runs up to a ring ahead of the recursions and then polls for
+// free slots; each poll takes issue slots from the recursion warps of the
+// (up to two) chain CTAs on the SM, so it sleeps between polls.
+#ifndef W2L_PROD_SLEEP_NS
+#define W2L_PROD_SLEEP_NS 256
+#endif
 
 // Et ring depth (frames): > wavefront spread + producer stages
 template <class V>
@@ -81,6 +87,22 @@ struct ChainSm {
   int cons[kCounters];
   int flush;   // a used token's Et fell below exp(-kFlush) (set by the producer)
 };
+
+// Dynamic shared memory of a chain CTA.  Requested above a third of the SM's
+// shared memory so that at most TWO chain CTAs (of either criterion) are
+// resident per SM: with the default placement a third chain CTA on an SM
+// ran its three recursions at about half speed, and the slowest chain of
+// the batch gates the gradient phase (two-stream timeline: chains ending
+// between 153 and 330 us instead of ~180).  W2L_CHAIN_SMEM_KB overrides
+// (A/B measurements).
+template <class V>
+inline size_t chain_smem_bytes() {
+  static const size_t kb = [] {
+    const char *e = getenv("W2L_CHAIN_SMEM_KB");
+    return e ? (size_t)atoi(e) : (size_t)80;
+  }();
+  return sizeof(ChainSm<V>) > kb * 1024 ? sizeof(ChainSm<V>) : kb * 1024;
+}
 
 // ---- 4-wide vector load/store of lane values (float4 / 2 x double2)
 __device__ __forceinline__ void ld4(const float *p, float (&v)[4]) {
@@ -266,7 +288,7 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
     // be past the step that read them (a step j reads index <= j)
     const int need = p0 + rows + 1 - kRing;
     for (int q = 0; q < c.nconsumers; ++q)
-      while (ld_relaxed(&sm.cons[q]) < need) __nanosleep(32);
+      while (ld_relaxed(&sm.cons[q]) < need) __nanosleep(W2L_PROD_SLEEP_NS);
     fence_acq_rel_cta();
     if (lane < rows) {
       V *dd = sm.ering[ring_slot<V>(c.fwd, p0 + lane)];
@@ -485,6 +507,9 @@ __device__ __forceinline__ void lat_step(LatState<V> &f, const StepIn<V> &in, Bn
 template <class V>
 __device__ __forceinline__ void lat_store_row(const LatState<V> &f, V *row, int *erow, int lane,
                                               bool live) {
+#ifdef W2L_NO_ROW_STORES   // timing experiments only: results are wrong
+  live = false;
+#endif
   if (live) {
     stv(row + lane * kSpl, f.v);
     erow[lane] = f.ex;

@@ -34,6 +34,7 @@ template <class TE>
 __global__ void __launch_bounds__(128)
     em_check_kernel(const TE *__restrict__ em, const int32_t *__restrict__ em_len, Dims d,
                     int check_lse, int32_t *status, int *route, float route_nats) {
+  pdl_launch_dependents();   // the prep kernel may launch (it waits for this grid)
   __shared__ TE rows[4][32 * 32];
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -147,6 +148,7 @@ __global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans,
                                 Dims d, int lpad, int *perm, int *tok_start, int32_t *status,
                                 int mode, int *prog) {
+  pdl_enter();
   const int b = blockIdx.x;
   if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int T = em_len[b], L = tgt_len[b];
@@ -217,6 +219,7 @@ __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
                                 const int32_t *__restrict__ tgt_len, int blank, Dims d,
                                 int lpad, int *perm, int *tok_start, int32_t *status, int mode,
                                 int *prog) {
+  pdl_enter();
   const int b = blockIdx.x;
   if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int T = em_len[b], L = tgt_len[b];
@@ -261,6 +264,7 @@ __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
 
 __global__ void viterbi_prep_kernel(const int32_t *__restrict__ em_len, Dims d,
                                     int32_t *status) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= d.B) return;
   const int T = em_len[b];
@@ -294,9 +298,8 @@ cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64
                                 int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s, route, kRouteNatsAsg);
   if (err != cudaSuccess) return err;
-  asg_prep_kernel<TE><<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, trans, d, lpad, perm,
-                                          tok_start, status, mode, prog);
-  return cudaGetLastError();
+  return launch_maybe_pdl(asg_prep_kernel<TE>, dim3(d.B), dim3(128), 0, s, true, em_len, tgt,
+                          tgt_len, trans, d, lpad, perm, tok_start, status, mode, prog);
 }
 template <class TE>
 cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64_t *tgt,
@@ -305,17 +308,16 @@ cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64
                                 int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s, route, kRouteNatsCtc);
   if (err != cudaSuccess) return err;
-  ctc_prep_kernel<<<d.B, 128, 0, s>>>(em_len, tgt, tgt_len, blank, d, lpad, perm, tok_start,
-                                      status, mode, prog);
-  return cudaGetLastError();
+  return launch_maybe_pdl(ctc_prep_kernel, dim3(d.B), dim3(128), 0, s, true, em_len, tgt, tgt_len,
+                          blank, d, lpad, perm, tok_start, status, mode, prog);
 }
 template <class TE>
 cudaError_t launch_viterbi_validate(const TE *em, const int32_t *em_len, Dims d,
                                     int32_t *status, cudaStream_t s) {
   cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s);
   if (err != cudaSuccess) return err;
-  viterbi_prep_kernel<<<(d.B + 127) / 128, 128, 0, s>>>(em_len, d, status);
-  return cudaGetLastError();
+  return launch_maybe_pdl(viterbi_prep_kernel, dim3((d.B + 127) / 128), dim3(128), 0, s, true,
+                          em_len, d, status);
 }
 
 #define INST(TE)                                                                           \

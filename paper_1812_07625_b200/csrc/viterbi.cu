@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) double dp_buf[2][32];
   __shared__ __align__(16) TE ebuf[2 * kVitChunk * 32];
+  pdl_wait();   // a programmatic dependent of the validation kernels
   const int b = blockIdx.x, N = d.N;
   int64_t *pb = path + (size_t)b * d.Tmax;
   if (status[b] != W2L_OK) {
@@ -221,12 +222,11 @@ cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans,
     cudaError_t err =
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBackMax);
     if (err != cudaSuccess) return err;
-    k<<<d.B, 128, back_bytes, s>>>(em, em_len, trans, d, path, score, status, nullptr);
-  } else {
-    viterbi4_kernel<TE, TA, false><<<d.B, 128, 0, s>>>(em, em_len, trans, d, path, score, status,
-                                                       (uint8_t *)ws);
+    return launch_maybe_pdl(k, dim3(d.B), dim3(128), back_bytes, s, true, em, em_len, trans, d, path,
+                            score, status, (uint8_t *)nullptr);
   }
-  return cudaGetLastError();
+  return launch_maybe_pdl(viterbi4_kernel<TE, TA, false>, dim3(d.B), dim3(128), 0, s, true, em,
+                          em_len, trans, d, path, score, status, (uint8_t *)ws);
 }
 
 template cudaError_t launch_viterbi<float, float>(const float *, const int32_t *, const float *,

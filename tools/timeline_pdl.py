@@ -35,15 +35,16 @@ el_d, ta_d, tc_d, tl_d, A_d = (torch.from_numpy(x).cuda() for x in (el, ta, tc, 
 side = torch.cuda.Stream()
 main = torch.cuda.current_stream()
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
+FB = os.environ.get("TL_NOFB") != "1"   # TL_NOFB=1: no fallback tiers (timing-only builds)
 
 
 def call():
     if which in ("ctc", "both"):
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False)
+            C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB)
     if which in ("asg", "both"):
-        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False)
+        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB)
     main.wait_stream(side)
 
 
@@ -51,8 +52,16 @@ for _ in range(5):
     call()
 torch.cuda.synchronize()
 read(0), read(1)
+# a ~1 ms sleep ahead of the call, so every launch is queued before the GPU
+# reaches it (otherwise the host's enqueue latency shows up as gaps)
+torch.cuda._sleep(2_000_000)
+g0 = torch.cuda.Event(enable_timing=True)
+g1 = torch.cuda.Event(enable_timing=True)
+g0.record()
 call()
+g1.record()
 torch.cuda.synchronize()
+print(f"call (events, after the sleep): {g0.elapsed_time(g1)*1e3:.1f} us")
 recs = np.concatenate([read(0), read(1)])
 tag = recs[:, 0].astype(np.int64)
 kind = tag // 1000000
@@ -64,6 +73,24 @@ for k, name in [(1, "ctc_chain"), (3, "asg_chain")]:
     if m.any():
         print(f"{name:10s} n={m.sum():4d} start {us(t[m,0].min()):7.1f}..{us(t[m,0].max()):7.1f}"
               f"  end {us(t[m,1].min()):7.1f}..{us(t[m,1].max()):7.1f} us")
+# chain CTAs per SM (t2 of a chain record is its SM id) vs their end times
+ch = (kind == 1) | (kind == 3)
+if ch.any():
+    sm = t[ch, 2]
+    cnt = {s: int((sm == s).sum()) for s in np.unique(sm)}
+    for c in sorted(set(cnt.values())):
+        m = np.array([cnt[s] == c for s in sm])
+        e = us(t[ch, 1][m])
+        print(f"chains on SMs hosting {c}: n={m.sum():4d} end {e.min():7.1f}/{np.median(e):7.1f}/{e.max():7.1f} us")
+    k2 = kind[ch]
+    for kk, nm in [(1, "ctc"), (3, "asg")]:
+        mm = k2 == kk
+        if mm.any():
+            e = us(t[ch, 1][mm]); d = (tag[ch][mm] % 10)
+            print(f"  {nm}: fwd end med {np.median(e[d == 0]):7.1f} bwd end med {np.median(e[d == 1]):7.1f};"
+                  f" slowest 5 (b,dir,sm,end): " + ", ".join(
+                      f"({int(tag[ch][mm][i] % 1000000 // 10)},{int(d[i])},{int(sm[mm][i])},{e[i]:.0f})"
+                      for i in np.argsort(-e)[:5]))
 for k, name in [(2, "ctc_grad"), (4, "asg_grad")]:
     m = kind == k
     if not m.any():
@@ -77,5 +104,14 @@ for k, name in [(2, "ctc_grad"), (4, "asg_grad")]:
     before = np.clip(np.minimum(e, cend) - w, 0, None).sum() / busy.sum()
     print(f"{'':10s} CTA busy {busy.mean():6.1f} us mean; {before*100:4.1f}% of gradient CTA time"
           f" before its chain ended ({cend:.1f} us); waited {np.mean(w - s):6.1f} us mean")
+    if k == 4:   # fac (x even) vs fcc (x odd) CTA bodies
+        body = (tag[m] % 1000000) // 500000
+        for bb, nm in [(0, "fac"), (1, "fcc")]:
+            mm = body == bb
+            print(f"{'':10s} {nm}: n={mm.sum()} busy {busy[mm].mean():6.1f} us mean, end max {e[mm].max():7.1f}")
+    # CTAs of this launch running at once (sampled every 2 us)
+    grid_t = np.arange(w.min(), e.max(), 2.0)
+    conc = [int(((w <= x) & (e > x)).sum()) for x in grid_t]
+    print(f"{'':10s} concurrent CTAs: max {max(conc)}, median {int(np.median(conc))}")
     hist = np.histogram(e, bins=12)
     print(f"{'':10s} end histogram: " + " ".join(f"{int(c)}@{b:.0f}" for c, b in zip(hist[0], hist[1])))
