@@ -531,7 +531,7 @@ constexpr size_t fac_grad_smem() {
   // per warp: posterior row + occupancy row (floats), guard (2 doubles),
   // token bins; the CTA's lane-block tokens
   return sizeof(float) * (kGradWarps * (2 * (size_t)W * kLatStates + 4 + 32) +
-                          (size_t)W * kLatStates / kSpl);
+                          (size_t)W * kLatStates / 4);
 }
 
 // The whole gradient row: fcc node posteriors (full part, :238) minus the
@@ -557,7 +557,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   float *occ = prow + kGradWarps * LP;                 // [kGradWarps][LP] occupancy
   double *gwarp = reinterpret_cast<double *>(occ + kGradWarps * LP);   // [kGradWarps][2]
   unsigned *bins = reinterpret_cast<unsigned *>(gwarp + kGradWarps * 2);   // [kGradWarps][32]
-  unsigned *stok = bins + kGradWarps * 32;             // [LP / kSpl] tokens per lane block
+  unsigned *stok = bins + kGradWarps * 32;             // [LP / 4] tokens, 4 states per word
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = d.N;
@@ -581,11 +581,10 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   for (int i = lane; i < LP; i += 32) myo[i] = 0.f;
   mybins[lane] = 0u;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  for (int m = threadIdx.x; m < (L + kSpl - 1) / kSpl; m += blockDim.x) {
+  for (int m = threadIdx.x; m < (L + 3) / 4; m += blockDim.x) {
     unsigned v = 0;
 #pragma unroll
-    for (int k = 0; k < kSpl; ++k)
-      v |= (m * kSpl + k < L ? (unsigned)y[m * kSpl + k] : 0xffu) << (8 * k);
+    for (int k = 0; k < 4; ++k) v |= (m * 4 + k < L ? (unsigned)y[m * 4 + k] : 0xffu) << (8 * k);
     stok[m] = v;
   }
   __syncthreads();
@@ -673,7 +672,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     // token bins and state occupancies of this frame's window (a lane owns
     // its blocks: plain shared read-modify-write for the occupancy)
     auto settle = [&](const float (&q)[kSpl], int m) {
-      band_scatter(q, izc, stok[m], mybins);
+      band_scatter(q, izc, stok + m * kTokWords, mybins);
       float o[kSpl];
       ldv(myo + m * kSpl, o);
 #pragma unroll

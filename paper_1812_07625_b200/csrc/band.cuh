@@ -108,12 +108,12 @@ __device__ __forceinline__ void band_block(const V (&va)[kSpl], const V (&vb)[kS
 // byte each, 0xff for none (CTC blanks are summed separately, as a float).
 constexpr float kFixScale = 0x1p30f;
 constexpr float kFixInv = 0x1p-30f;
-__device__ __forceinline__ void band_scatter(const float (&q)[kSpl], float inv, unsigned tok4,
+constexpr int kTokWords = kSpl / 4;   // token words per lane block (4 bytes each)
+__device__ __forceinline__ void band_scatter(const float (&q)[kSpl], float inv, const unsigned *tok,
                                              unsigned *bins) {
-  static_assert(kSpl == 4, "one token byte per state of a 4-state block");
 #pragma unroll
   for (int k = 0; k < kSpl; ++k) {
-    const unsigned tk = (tok4 >> (8 * k)) & 0xffu;
+    const unsigned tk = (tok[k >> 2] >> (8 * (k & 3))) & 0xffu;
     if (tk != 0xffu && q[k] > 0.f) atomicAdd(bins + tk, __float2uint_rn(q[k] * inv * kFixScale));
   }
 }

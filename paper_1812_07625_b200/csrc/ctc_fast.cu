@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
                     const int32_t *__restrict__ status, int want, const int *prog) {
   constexpr int LP = W * kLatStates;
   __shared__ __align__(16) float prow[kGradWarps][LP];   // wide-window posteriors
-  __shared__ unsigned stok[LP / kSpl];                    // label tokens per lane block (band.cuh)
+  __shared__ unsigned stok[LP / 4];                        // label tokens per lane block (band.cuh)
   __shared__ unsigned bins[kGradWarps][32];               // per-warp token sums (fixed point)
   __shared__ double gw[kGradWarps][2];
   pdl_launch_dependents();
@@ -162,11 +162,11 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   // tokens of each lane block's label states (odd states 2l+1 carry y_l;
   // blanks are summed apart)
   const int64_t *y = tgt + (size_t)b * d.Lmax;
-  for (int m = threadIdx.x; m < (S + kSpl - 1) / kSpl; m += blockDim.x) {
+  for (int m = threadIdx.x; m < (S + 3) / 4; m += blockDim.x) {
     unsigned v = 0;
 #pragma unroll
-    for (int k = 0; k < kSpl; ++k) {
-      const int st4 = m * kSpl + k;
+    for (int k = 0; k < 4; ++k) {
+      const int st4 = m * 4 + k;
       const unsigned tk = ((st4 & 1) && st4 < S) ? (unsigned)y[st4 >> 1] : 0xffu;
       v |= tk << (8 * k);
     }
@@ -253,13 +253,13 @@ __global__ void __launch_bounds__(kGradWarps * 32)
 #pragma unroll
     for (int r = 0; r < kBandRounds; ++r) {
       const int m = cmlo + lane + 32 * r;
-      if (m <= cmhi && m < br.nblk) band_scatter(qr[r], inv, stok[m], mybins);
+      if (m <= cmhi && m < br.nblk) band_scatter(qr[r], inv, stok + m * kTokWords, mybins);
     }
     for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);
-        band_scatter(q, inv, stok[m], mybins);
+        band_scatter(q, inv, stok + m * kTokWords, mybins);
       }
     }
     float sm_k = 0.f;

@@ -165,10 +165,17 @@ __device__ __forceinline__ int ld_relaxed(const int *p) {
 __device__ __forceinline__ void fence_acq_rel_cta() {
   asm volatile("fence.acq_rel.cta;\n" ::: "memory");
 }
+// Polls of the recursion warps.  W2L_SPIN_NS > 0 sleeps between polls (a
+// poll takes issue slots from the other chain CTA on the SM).
+#ifndef W2L_SPIN_NS
+#define W2L_SPIN_NS 32
+#endif
+__device__ __forceinline__ void spin_pause() {
+  if (W2L_SPIN_NS > 0) __nanosleep(W2L_SPIN_NS);
+}
 // every lane spins on the same word (a broadcast load, no divergence)
 __device__ __forceinline__ void wait_ge(const int *p, int need) {
-  while (ld_acquire(p) < need) {
-  }
+  while (ld_acquire(p) < need) spin_pause();
 }
 // wait for up to three counters with relaxed polls issued together, then one
 // acquire fence (cheaper than three acquire loads when they are satisfied)
@@ -177,6 +184,7 @@ __device__ __forceinline__ void wait3(const int *p0, int n0, const int *p1, int 
   while (true) {
     const int a = ld_relaxed(p0), b = ld_relaxed(p1), c = ld_relaxed(p2);
     if (a >= n0 && b >= n1 && c >= n2) break;
+    spin_pause();
   }
   fence_acq_rel_cta();
 }
