@@ -530,7 +530,7 @@ template <int W>
 constexpr size_t fac_grad_smem() {
   // per warp: posterior row + occupancy row (floats), guard (2 doubles),
   // token bins; the CTA's lane-block tokens
-  return sizeof(float) * (kGradWarps * (2 * (size_t)W * kLatStates + 4 + 32) +
+  return sizeof(float) * (kGradWarps * (2 * (size_t)W * kLatStates + 4 + 32 + 1) +
                           (size_t)W * kLatStates / 4);
 }
 
@@ -588,7 +588,6 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     stok[m] = v;
   }
   __syncthreads();
-  double gmin = CUDART_INF, gmax = -CUDART_INF;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
   const int tend = min(tb, T);
 
@@ -606,17 +605,35 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   br.B = reinterpret_cast<const V *>(w.fac_b) + seg0 * kLatStates;
   br.EA = w.fac_ea + seg0 * 32;
   br.EB = w.fac_eb + seg0 * 32;
-  br.segv = (size_t)d.Tmax * kLatStates;
-  br.sege = (size_t)d.Tmax * 32;
+  br.segv = (uint32_t)d.Tmax * kLatStates;
+  br.sege = (uint32_t)d.Tmax * 32;
   br.S = L;
   br.nblk = (L + kSpl - 1) / kSpl;
-  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window
-  const int ref = ta < tend ? br.reference(ta, lane) : 0;
+  // the CTA's reference exponent (frame t0, every warp a share of the blocks)
+  int *sref = reinterpret_cast<int *>(stok + LP / 4);   // [kGradWarps]
+  {
+    const int part = br.magnitude_part(t0, warp, kGradWarps, lane);
+    if (lane == 0) sref[warp] = part;
+  }
+  __syncthreads();
+  int ref = INT_MIN;
+#pragma unroll
+  for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
+  if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
+  float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
+  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window (first: all)
   V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
   int pe[kBandRounds];
+  auto prefetch = [&](int t) {   // the window's first kBandRounds rounds of frame t
+    const typename BandRows<V>::Frame f = br.frame(t);
 #pragma unroll
-  for (int r = 0; r < kBandRounds; ++r)
-    br.load(mlo + lane + 32 * r, ta, ta < tend && mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    for (int r = 0; r < kBandRounds; ++r) {
+      pe[r] = INT_MIN;
+      if (mlo + 32 * r <= mhi)   // warp-uniform: skip empty rounds
+        br.load(f, mlo + lane + 32 * r, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    }
+  };
+  if (ta < tend) prefetch(ta);
   for (int t = ta; t < tend; ++t) {
     const float gam = (float)(ca_nx * cb_nx);   // fcc node posterior, unnormalised
     if (t + 1 < tend) {
@@ -637,38 +654,32 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 #pragma unroll
       for (int k = 0; k < kSpl; ++k) zl += q[k];
     };
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r)
-      take(pa[r], pb[r], pe[r], mlo + lane + 32 * r, qr[r], false);
-    for (int m = mlo + lane + 32 * kBandRounds; m <= mhi; m += 32) {   // wide windows
-      V va[kSpl], vb[kSpl];
-      float q[kSpl];
-      int e;
-      br.load(m, t, true, va, vb, e);
-      take(va, vb, e, m, q, true);
-    }
     const int cmlo = mlo, cmhi = mhi;
-    // the next frame's window (fac mass moves by 0 or 1 state per frame)
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    if (hi >= lo) {
-      mlo = lo / kSpl;
-      mhi = min(hi + 1, L - 1) / kSpl;
-    } else {   // nothing above the threshold (cannot happen for a finite loss): read all
-      mlo = 0;
-      mhi = br.nblk - 1;
-    }
-    if (t + 1 < tend) {
 #pragma unroll
-      for (int r = 0; r < kBandRounds; ++r)
-        br.load(mlo + lane + 32 * r, t + 1, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    for (int r = 0; r < kBandRounds; ++r) {
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) qr[r][k] = 0.f;
+      if (cmlo + 32 * r <= cmhi) take(pa[r], pb[r], pe[r], cmlo + lane + 32 * r, qr[r], false);
     }
+    if (cmlo + 32 * kBandRounds <= cmhi) {   // wide windows (first frame, flat posteriors)
+      const typename BandRows<V>::Frame f = br.frame(t);
+      for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+        V va[kSpl], vb[kSpl];
+        float q[kSpl];
+        int e;
+        br.load(f, m, true, va, vb, e);
+        take(va, vb, e, m, q, true);
+      }
+    }
+    // the next frame's window (fac mass moves by 0 or 1 state per frame)
+    br.next_window(lo, hi, 1, mlo, mhi);
+    if (t + 1 < tend) prefetch(t + 1);
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
     const float izf = 1.f / warp_sum(gam);
-    const double g = (double)ref + (double)__log2f(zc);   // the frame's log2-normaliser
-    gmin = fmin(gmin, g);
-    gmax = fmax(gmax, g);
+    const float l2 = __log2f(zc);
+    l2min = fminf(l2min, l2);
+    l2max = fmaxf(l2max, l2);
     // token bins and state occupancies of this frame's window (a lane owns
     // its blocks: plain shared read-modify-write for the occupancy)
     auto settle = [&](const float (&q)[kSpl], int m) {
@@ -682,7 +693,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 #pragma unroll
     for (int r = 0; r < kBandRounds; ++r) {
       const int m = cmlo + lane + 32 * r;
-      if (m <= cmhi && m < br.nblk) settle(qr[r], m);
+      if (cmlo + 32 * r <= cmhi && m <= cmhi && m < br.nblk) settle(qr[r], m);
     }
     for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
       if (m < br.nblk) {
@@ -697,6 +708,8 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     if (lane < N) ge[(size_t)t * N + lane] = gam * izf - con;
     __syncwarp();
   }
+  // the frames' log2-normalisers (ref + log2 z_t) for the guard
+  const double gmin = (double)ref + (double)l2min, gmax = (double)ref + (double)l2max;
 
   // ---- block reduction of the occupancy partials in fixed warp order
   // (deterministic)

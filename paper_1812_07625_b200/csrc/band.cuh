@@ -18,14 +18,17 @@
 //
 // LANES.  Each frame, lane l takes the window's lane blocks mlo + l + 32 r
 // (rounds r = 0, 1, ...): two rounds cover 64 blocks (256 states), and those
-// two are prefetched one frame ahead in registers; wider windows (the first
-// frame, flat posteriors) load their extra rounds in the frame itself.
+// two are prefetched one frame ahead in registers; wider windows (a warp's
+// first frame, flat posteriors) load their extra rounds in the frame itself.
 //
 // SCALE.  sum_s alpha_t beta'_t = Z for every frame, so one reference
-// exponent -- the magnitude of the warp's first frame, from its largest
+// exponent -- the magnitude of the CTA's first frame, from its largest
 // block (block exponent sum plus the exponent of the block's largest
-// product; all-zero blocks ignored) -- scales all the warp's frames into
-// fp32 range.  Each frame's posteriors are normalised by their own sum z_t,
+// product; all-zero blocks ignored), found by the CTA's warps together --
+// scales all the CTA's frames into fp32 range.  (A block's exponent alone
+// does not bound its values: between renormalisations a block may carry a
+// dominant neighbour's mass scaled onto its exponent by up to 2^kLaneGap, so
+// a warp's first frame is read whole.)  Each frame's posteriors are normalised by their own sum z_t,
 // and ref + log2 z_t is the frame's log2-normaliser the guard checks.
 #pragma once
 
@@ -42,61 +45,80 @@ template <class V>
 struct BandRows {
   const V *A, *B;       // this utterance's alpha / beta' rows (lattice warp 0)
   const int *EA, *EB;   // their block exponents
-  size_t segv, sege;    // per lattice warp: Tmax * kLatStates values, Tmax * 32 exponents
+  uint32_t segv, sege;  // per lattice warp: Tmax * kLatStates values, Tmax * 32 exponents
   int S;                // lattice states
   int nblk;             // lane blocks holding states: ceil(S / kSpl)
 
-  __device__ __forceinline__ size_t voff(int m, int t) const {
-    return (size_t)(m >> 5) * segv + (size_t)t * kLatStates + (size_t)(m & 31) * kSpl;
+  // one frame's rows; blocks are addressed by 32-bit offsets from them
+  struct Frame {
+    const V *a, *b;
+    const int *ea, *eb;
+  };
+  __device__ __forceinline__ Frame frame(int t) const {
+    return {A + (size_t)t * kLatStates, B + (size_t)t * kLatStates, EA + (size_t)t * 32,
+            EB + (size_t)t * 32};
   }
-  __device__ __forceinline__ size_t eoff(int m, int t) const {
-    return (size_t)(m >> 5) * sege + (size_t)t * 32 + (m & 31);
+  __device__ __forceinline__ uint32_t voff(int m) const {
+    return (uint32_t)(m >> 5) * segv + (uint32_t)(m & 31) * kSpl;
   }
-  // block m of frame t: values and exponent sum (INT_MIN: outside the lattice)
-  __device__ __forceinline__ void load(int m, int t, bool want, V (&va)[kSpl], V (&vb)[kSpl],
-                                       int &e) const {
+  __device__ __forceinline__ uint32_t eoff(int m) const {
+    return (uint32_t)(m >> 5) * sege + (uint32_t)(m & 31);
+  }
+  // block m of a frame: values and exponent sum (INT_MIN: not loaded)
+  __device__ __forceinline__ void load(const Frame &f, int m, bool want, V (&va)[kSpl],
+                                       V (&vb)[kSpl], int &e) const {
     e = INT_MIN;
     if (want && m < nblk) {
-      ldv_cg(A + voff(m, t), va);
-      ldv_cg(B + voff(m, t), vb);
-      e = __ldcg(EA + eoff(m, t)) + __ldcg(EB + eoff(m, t));
+      const uint32_t vo = voff(m), eo = eoff(m);
+      ldv_cg(f.a + vo, va);
+      ldv_cg(f.b + vo, vb);
+      e = __ldcg(f.ea + eo) + __ldcg(f.eb + eo);
     }
   }
-  // the warp's reference exponent from frame t (all blocks)
-  __device__ __forceinline__ int reference(int t, int lane) const {
-    int ref = INT_MIN;
-    for (int m = lane; m < nblk; m += 32) {
+  // this warp's share (blocks warp*32 + lane + 32*nwarps*k) of the largest
+  // block magnitude of frame t: block exponent sum plus the exponent of the
+  // block's largest product (all-zero blocks ignored)
+  __device__ __forceinline__ int magnitude_part(int t, int warp, int nwarps, int lane) const {
+    const Frame f = frame(t);
+    int mag = INT_MIN;
+    for (int m = warp * 32 + lane; m < nblk; m += 32 * nwarps) {
       V va[kSpl], vb[kSpl], pp[kSpl];
       int e;
-      load(m, t, true, va, vb, e);
+      load(f, m, true, va, vb, e);
 #pragma unroll
       for (int k = 0; k < kSpl; ++k) pp[k] = va[k] * vb[k];
       const V pm = tree_max<kSpl, V>(pp);
-      if (pm > (V)0) ref = max(ref, e + Pow2<V>::expo(pm));
+      if (pm > (V)0) mag = max(mag, e + Pow2<V>::expo(pm));
     }
-    ref = __reduce_max_sync(0xffffffffu, ref);
-    return ref == INT_MIN ? 0 : ref;   // no mass: the guard rejects the utterance
+    return __reduce_max_sync(0xffffffffu, mag);
+  }
+  // next frame's window (lane blocks) from this frame's band (blocks lo..hi
+  // holding a scaled posterior above kBandEps); mass moves by <= step states
+  __device__ __forceinline__ void next_window(int lo, int hi, int step, int &mlo,
+                                              int &mhi) const {
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi >= lo) {
+      mlo = lo;
+      mhi = min(hi * kSpl + kSpl - 1 + step, S - 1) / kSpl;
+    } else {   // nothing above the threshold (cannot happen for a finite loss): read all
+      mlo = 0;
+      mhi = nblk - 1;
+    }
   }
 };
 
-// Scaled posteriors of one lane block into q (float) and their band edges
-// into lo / hi.
+// Scaled posteriors of one lane block into q (float); a block above the band
+// threshold widens the band [lo, hi] (lane blocks).
 template <class V>
 __device__ __forceinline__ void band_block(const V (&va)[kSpl], const V (&vb)[kSpl], int e,
                                            int ref, int m, float (&q)[kSpl], int &lo, int &hi) {
   const V sc = e == INT_MIN ? (V)0 : pow2_clamped<V>(e - ref);
 #pragma unroll
   for (int k = 0; k < kSpl; ++k) q[k] = (float)(va[k] * vb[k] * sc);
-  int first = kSpl, last = -1;
-#pragma unroll
-  for (int k = kSpl - 1; k >= 0; --k)
-    if (q[k] > kBandEps) first = k;
-#pragma unroll
-  for (int k = 0; k < kSpl; ++k)
-    if (q[k] > kBandEps) last = k;
-  if (last >= 0) {
-    lo = min(lo, m * kSpl + first);
-    hi = max(hi, m * kSpl + last);
+  if (tree_max<kSpl, float>(q) > kBandEps) {
+    lo = min(lo, m);
+    hi = max(hi, m);
   }
 }
 

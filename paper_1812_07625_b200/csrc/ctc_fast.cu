@@ -122,7 +122,7 @@ constexpr int kGradWarps = 8;
 // (block_of_rank), so with PDL the CTAs run in the order the two chains
 // complete their frames; prog (null: the chains have finished) gates them.
 template <int W, class V>
-__global__ void __launch_bounds__(kGradWarps * 32)
+__global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
     ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
@@ -174,10 +174,7 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   }
   bins[warp][lane] = 0u;
   __syncthreads();
-  double gmin = CUDART_INF, gmax = -CUDART_INF;
   const size_t seg0 = (size_t)b * w.W * d.Tmax;
-  const size_t segv = (size_t)d.Tmax * kLatStates;
-  const size_t sege = (size_t)d.Tmax * 32;
   float *myp = prow[warp];
   const int tend = min(tb, T);
   // band-limited walk over the warp's frames (band.cuh); CTC posterior mass
@@ -187,18 +184,36 @@ __global__ void __launch_bounds__(kGradWarps * 32)
   br.B = reinterpret_cast<const V *>(w.b) + seg0 * kLatStates;
   br.EA = w.ea + seg0 * 32;
   br.EB = w.eb + seg0 * 32;
-  br.segv = segv;
-  br.sege = sege;
+  br.segv = (uint32_t)d.Tmax * kLatStates;
+  br.sege = (uint32_t)d.Tmax * 32;
   br.S = S;
   br.nblk = (S + kSpl - 1) / kSpl;
-  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window
   unsigned *mybins = bins[warp];
-  const int ref = ta < tend ? br.reference(ta, lane) : 0;
+  // the CTA's reference exponent (frame t0, every warp a share of the blocks)
+  __shared__ int sref[kGradWarps];
+  {
+    const int part = br.magnitude_part(t0, warp, kGradWarps, lane);
+    if (lane == 0) sref[warp] = part;
+  }
+  __syncthreads();
+  int ref = INT_MIN;
+#pragma unroll
+  for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
+  if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
+  float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
+  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window (first: all)
   V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
   int pe[kBandRounds];
+  auto prefetch = [&](int t) {   // the window's first kBandRounds rounds of frame t
+    const typename BandRows<V>::Frame f = br.frame(t);
 #pragma unroll
-  for (int r = 0; r < kBandRounds; ++r)
-    br.load(mlo + lane + 32 * r, ta, ta < tend && mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    for (int r = 0; r < kBandRounds; ++r) {
+      pe[r] = INT_MIN;
+      if (mlo + 32 * r <= mhi)   // warp-uniform: skip empty rounds
+        br.load(f, mlo + lane + 32 * r, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    }
+  };
+  if (ta < tend) prefetch(ta);
   for (int t = ta; t < tend; ++t) {
     float zl = 0.f, zb = 0.f;
     int lo = INT_MAX, hi = -1;
@@ -216,44 +231,38 @@ __global__ void __launch_bounds__(kGradWarps * 32)
         zb += q[k];   // blank states are the even ones
       }
     };
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r)
-      take(pa[r], pb[r], pe[r], mlo + lane + 32 * r, qr[r], false);
-    const int wide0 = mlo + lane + 32 * kBandRounds;
-    for (int m = wide0; m <= mhi; m += 32) {   // wide windows (first frame, flat posteriors)
-      V va[kSpl], vb[kSpl];
-      float q[kSpl];
-      int e;
-      br.load(m, t, true, va, vb, e);
-      take(va, vb, e, m, q, true);
-    }
     const int cmlo = mlo, cmhi = mhi;
-    // the next frame's window (CTC mass moves by up to 2 states per frame)
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    if (hi >= lo) {
-      mlo = lo / kSpl;
-      mhi = min(hi + 2, S - 1) / kSpl;
-    } else {   // nothing above the threshold (cannot happen for a finite loss): read all
-      mlo = 0;
-      mhi = br.nblk - 1;
-    }
-    if (t + 1 < tend) {
 #pragma unroll
-      for (int r = 0; r < kBandRounds; ++r)
-        br.load(mlo + lane + 32 * r, t + 1, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
+    for (int r = 0; r < kBandRounds; ++r) {
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) qr[r][k] = 0.f;
+      if (cmlo + 32 * r <= cmhi) take(pa[r], pb[r], pe[r], cmlo + lane + 32 * r, qr[r], false);
     }
+    if (cmlo + 32 * kBandRounds <= cmhi) {   // wide windows (first frame, flat posteriors)
+      const typename BandRows<V>::Frame f = br.frame(t);
+      for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+        V va[kSpl], vb[kSpl];
+        float q[kSpl];
+        int e;
+        br.load(f, m, true, va, vb, e);
+        take(va, vb, e, m, q, true);
+      }
+    }
+    // the next frame's window (CTC mass moves by up to 2 states per frame)
+    br.next_window(lo, hi, 2, mlo, mhi);
+    if (t + 1 < tend) prefetch(t + 1);
     const float z = warp_sum(zl);
     const float zblank = warp_sum(zb);
     const float inv = 1.f / z;
-    const double g = (double)ref + (double)__log2f(z);
-    gmin = fmin(gmin, g);
-    gmax = fmax(gmax, g);
+    const float l2 = __log2f(z);
+    l2min = fminf(l2min, l2);
+    l2max = fmaxf(l2max, l2);
     // label posteriors into the token bins
 #pragma unroll
     for (int r = 0; r < kBandRounds; ++r) {
       const int m = cmlo + lane + 32 * r;
-      if (m <= cmhi && m < br.nblk) band_scatter(qr[r], inv, stok + m * kTokWords, mybins);
+      if (cmlo + 32 * r <= cmhi && m <= cmhi && m < br.nblk)
+        band_scatter(qr[r], inv, stok + m * kTokWords, mybins);
     }
     for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
       if (m < br.nblk) {
@@ -275,6 +284,8 @@ __global__ void __launch_bounds__(kGradWarps * 32)
     if (lane < N) ge[(size_t)t * N + lane] = sm_k - c;   // criterion.py:159-161
     __syncwarp();
   }
+  // the frames' log2-normalisers (ref + log2 z_t) for the guard
+  const double gmin = (double)ref + (double)l2min, gmax = (double)ref + (double)l2max;
   if (lane == 0) {
     gw[warp][0] = gmin;
     gw[warp][1] = gmax;

@@ -44,7 +44,14 @@ __global__ void __launch_bounds__(128)
   const int nrows = min(32, T - t0), N = d.N;
   const TE *src = em + ((size_t)b * d.Tmax + t0) * N;
   TE *buf = rows[warp];
-  for (int e = lane; e < nrows * N; e += 32) buf[e] = src[e];
+  // every load in flight before the first store (N <= 32: at most 32 each)
+  TE v[32];
+  const int n = nrows * N;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = lane + 32 * k < n ? src[lane + 32 * k] : (TE)0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (lane + 32 * k < n) buf[lane + 32 * k] = v[k];
   __syncwarp();
   int bits = 0;
   float spread = 0.f;
