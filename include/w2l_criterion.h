@@ -101,7 +101,8 @@ enum {
 
 /* ------------------------------------------------------------------ ASG --
  * Replaces asg_loss_grad (criterion.py:167-247), batched.
- *   loss[B]            f64  per-utterance loss  (fcc score - fac score)
+ *   loss[B]            f64  per-utterance loss  (fcc score - fac score); NaN for an
+ *                           utterance whose status is an error
  *   grad_em[B,Tmax,N]  f32  d loss_b / d emissions_b
  *   grad_trans[N,N]    f32  sum over utterances of d loss_b / d A
  *                           (trainer.py:417-418; the /B stays with the caller)

@@ -755,9 +755,12 @@ __global__ void __launch_bounds__(kFinalThreads)
   if (threadIdx.x < 2 && w.prog) w.prog[2 * b + threadIdx.x] = 0;   // next tier / call
   const int st = status[b];
   if (st != want) {
-    // the first tier owns the zeros of the utterances it does not compute
-    if (want == W2L_OK)
+    // the first tier owns the zeros (NaN loss) of the utterances it does not
+    // compute; a later tier overwrites those it takes
+    if (want == W2L_OK) {
       for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
+      if (threadIdx.x == 0) loss[b] = CUDART_NAN;
+    }
     return;
   }
   const int L = tgt_len[b], T = em_len[b], LP = w.lpad;
@@ -838,7 +841,11 @@ __global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d,
                                      double *loss, int32_t *status, int want, int fail) {
   pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= d.B || status[b] != want) return;
+  if (b >= d.B) return;
+  if (status[b] != want) {
+    if (want == W2L_OK) loss[b] = CUDART_NAN;   // (a later tier overwrites those it takes)
+    return;
+  }
   const double zF = w.scal[b * 4 + 0], zFb = w.scal[b * 4 + 1];
   const double zC = w.scal[b * 4 + 2], zCb = w.scal[b * 4 + 3];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));

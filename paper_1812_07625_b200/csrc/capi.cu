@@ -168,6 +168,7 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
                                               w.tok_start, status, s, kPrepForceExact));
     if (!rc) rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
     if (!rc) rc = from_cuda(cudaMemsetAsync(ga, 0, sizeof(float) * (size_t)B * N * N, s));
+    if (!rc) rc = from_cuda(cudaMemsetAsync(loss, 0xff, sizeof(double) * B, s));   // NaN
     if (!rc)
       rc = from_cuda(launch_asg_exact<float>(em, em_len, tgt, tgt_len, trans, d, 1, asg_slots(B),
                                              slots, loss, grad_em, ga, status, s));
@@ -279,6 +280,8 @@ int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t
   if (rc) return rc;
   rc = from_cuda(cudaMemsetAsync(ga, 0, sizeof(float) * (size_t)B * N * N, s));
   if (rc) return rc;
+  rc = from_cuda(cudaMemsetAsync(loss, 0xff, sizeof(double) * B, s));   // NaN: failed utterances
+  if (rc) return rc;
   rc = from_cuda(launch_asg_exact<double>(em, em_len, tgt, tgt_len, trans, d, 0,
                                           asg_slots_f64(B), slots, loss, grad_em, ga, status,
                                           s));
@@ -330,6 +333,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
                                               w.perm, w.tok_start, status, s, !logits,
                                               kPrepForceExact));
     if (!rc) rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+    if (!rc) rc = from_cuda(cudaMemsetAsync(loss, 0xff, sizeof(double) * B, s));   // NaN
     if (!rc)
       rc = from_cuda(launch_ctc_exact<float>(logp, em_len, tgt, tgt_len, blank, d, 1,
                                              asg_slots(B), slots, loss, grad_em, status, s,
@@ -402,6 +406,8 @@ int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64
                                             nullptr, status, s));
   if (rc) return rc;
   rc = from_cuda(cudaMemsetAsync(grad_em, 0, sizeof(float) * (size_t)B * Tmax * N, s));
+  if (rc) return rc;
+  rc = from_cuda(cudaMemsetAsync(loss, 0xff, sizeof(double) * B, s));   // NaN: failed utterances
   if (rc) return rc;
   return from_cuda(launch_ctc_exact<double>(logp, em_len, tgt, tgt_len, blank, d, 0,
                                             asg_slots_f64(B), ws, loss, grad_em, status, s));

@@ -319,7 +319,12 @@ __global__ void ctc_final_kernel(const int32_t *__restrict__ em_len, Dims d, Ctc
   const int lane = threadIdx.x & 31;
   if (b >= d.B) return;
   if (lane < 2 && w.prog) w.prog[2 * b + lane] = 0;
-  if (status[b] != want) return;
+  if (status[b] != want) {
+    // the first tier owns the NaN loss of the utterances it does not
+    // compute; a later tier overwrites those it takes
+    if (want == W2L_OK && lane == 0) loss[b] = CUDART_NAN;
+    return;
+  }
   const int T = em_len[b];
   const double ln2 = 0.6931471805599453;
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
@@ -344,7 +349,11 @@ __global__ void ctc_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d,
                                      double *loss, int32_t *status, int want, int fail) {
   pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= d.B || status[b] != want) return;
+  if (b >= d.B) return;
+  if (status[b] != want) {
+    if (want == W2L_OK) loss[b] = CUDART_NAN;   // (a later tier overwrites those it takes)
+    return;
+  }
   const double zA = w.scal[b * 4 + 0], zB = w.scal[b * 4 + 1], shifts = w.scal[b * 4 + 2];
   const double tol = 1e-4 * fmax(1.0, sqrt((double)em_len[b] / 1600.0));
   loss[b] = -(zA + shifts);                                  // criterion.py:162
