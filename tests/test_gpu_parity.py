@@ -486,11 +486,13 @@ def test_loss_only_mode_matches_full_call():
     np.testing.assert_allclose(lo.loss.cpu().numpy(), loss, rtol=REL)
 
 
-def test_transitions_sgd_step_matches_reference_optimizer():
-    # /B + momentum + SGD (trainer.py:442-449, autodiff.py:429-433)
+@pytest.mark.parametrize("bsz", [64, 6, 17])
+def test_transitions_sgd_step_matches_reference_optimizer(bsz):
+    # /B + momentum + SGD (trainer.py:442-449, autodiff.py:429-433);
+    # B = 6, 17: the /B is a true division (x * (1/B) differs from x / B there)
     from paper_1812_07625_b200.distributed import sgd_step_transitions
     rng = np.random.default_rng(46)
-    n, bsz, lr, mom = 30, 64, 0.05, 0.9
+    n, lr, mom = 30, 0.05, 0.9
     a = rng.standard_normal((n, n)).astype(np.float32)
     v = rng.standard_normal((n, n)).astype(np.float32)
     gsum = (rng.standard_normal((n, n)) * 7).astype(np.float32)
