@@ -222,10 +222,13 @@ cudaError_t launch_viterbi(const TE *em, const int32_t *em_len, const TA *trans,
     cudaError_t err =
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBackMax);
     if (err != cudaSuccess) return err;
-    return launch_maybe_pdl(k, dim3(d.B), dim3(128), back_bytes, s, true, em, em_len, trans, d, path,
-                            score, status, (uint8_t *)nullptr);
+    return launch_maybe_pdl(k, dim3(d.B), dim3(128), back_bytes, s, false, em, em_len, trans, d,
+                            path, score, status, (uint8_t *)nullptr);
   }
-  return launch_maybe_pdl(viterbi4_kernel<TE, TA, false>, dim3(d.B), dim3(128), 0, s, true, em,
+  // (plain launches: launched early as programmatic dependents, the
+  // latency-bound CTAs were packed two to an SM while the validation kernels
+  // held the others -- 0.69 vs 0.37 ms at B=64 T=1600)
+  return launch_maybe_pdl(viterbi4_kernel<TE, TA, false>, dim3(d.B), dim3(128), 0, s, false, em,
                           em_len, trans, d, path, score, status, (uint8_t *)ws);
 }
 

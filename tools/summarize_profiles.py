@@ -20,7 +20,8 @@ shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(dst, "launches_bench
 
 
 def short(name):
-    n = name.split("(")[0].replace("void ", "").replace("w2l::", "")
+    n = name.replace("(int)", "")   # demangled template arguments (ncu --kernel-name-base demangled)
+    n = n.split("(")[0].replace("void ", "").replace("w2l::", "")
     return n.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("::")[-1]
 
 
@@ -61,8 +62,9 @@ def to_mb(v, u):
 keymap = {"asg_chain_kernel": "asg_chain", "ctc_chain_kernel": "ctc_chain",
           "asg_fcc_grad_kernel": "asg_grad_fcc"}
 traffic = {}
-out = ["# ncu --set full --clock-control none --import-source on -k regex:'_chain_kernel|_grad_kernel' -s 4 -c 4 "
-       "(tools/prof_chain.py all; bench shape B=64 T=1600 N=30 L=300)",
+out = ["# ncu --set full --clock-control none --import-source on --kernel-name-base demangled "
+       "-k regex:'(chain|grad)_kernel<.*float>' -s 4 -c 4 "
+       "(tools/prof_chain.py all; bench shape B=64 T=1600 N=30 L=300; the fp32 tier)",
        f"{'kernel':30s}{'dur_us':>9s}{'dram_rd_MB':>11s}{'dram_wr_MB':>11s}{'occ%':>7s}"
        f"{'inst/frame':>11s}{'IPC':>6s}{'regs':>6s}"]
 for r in data:
@@ -72,9 +74,10 @@ for r in data:
         dur /= 1e3
     rd = to_mb(r[ix["dram__bytes_read.sum"]], units[ix["dram__bytes_read.sum"]])
     wr = to_mb(r[ix["dram__bytes_write.sum"]], units[ix["dram__bytes_write.sum"]])
-    key = keymap.get(name, "asg_grad" if name.startswith("asg_grad") else
-                     ("asg_grad_fac" if name.startswith("asg_fac_grad") else
-                      ("ctc_grad" if name.startswith("ctc_grad") else name)))
+    key = next((v for k, v in keymap.items() if name.startswith(k)),
+               "asg_grad" if name.startswith("asg_grad") else
+               ("asg_grad_fac" if name.startswith("asg_fac_grad") else
+                ("ctc_grad" if name.startswith("ctc_grad") else name)))
     traffic[key] = int((rd + wr) * 1e6)
     inst = float(r[ix["smsp__inst_executed.sum"]].replace(",", "")) / 102400
     out.append(f"{name:30s}{dur:9.1f}{rd:11.1f}{wr:11.1f}"
