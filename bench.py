@@ -40,6 +40,8 @@ METRIC = "ASG/CTC loss+grad frames/sec (B×T) at 1/2/4/8 B200; % of HBM/SFU roof
 B_PER_GPU, T_FR, N_TOK, L_LAB = 64, 1600, 30, 300
 SEED = 20260004  # 20260000 + config index (C5)
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+# staggered start of the two criteria (W2L_BENCH_STAGGER=0 starts them together; A/B)
+STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
 
 
 # ---------------------------------------------------------------- inputs --
@@ -350,6 +352,7 @@ def main():
 
     side = torch.cuda.Stream(device=dev)
     main_s = torch.cuda.current_stream(dev)
+    validated = torch.cuda.Event()   # CTC's validation done (the staggered start)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def both(em_, el_, ta_, tc_, tl_, outs=None):
@@ -357,9 +360,23 @@ def main():
         # the two criteria run concurrently on two streams (chain CTAs of both
         # are co-resident: maximum shared-memory carveout)
         side.wait_stream(main_s)
+        # Staggered start: ASG begins its validation when CTC's has finished,
+        # so its recursions start ~25 us after CTC's.  Started together, the
+        # two chains sharing each SM fall into a slow mode on about two thirds
+        # of the steps (per-step device times 0.49 vs 0.53-0.58 ms,
+        # tools/step_times.py); staggered, every step runs in the fast mode.
         with torch.cuda.stream(side):
-            oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False, workspace=ws_c,
-                                         out=oc_)
+            if STAGGER:
+                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
+                                             workspace=ws_c, out=oc_, phase="validate")
+                validated.record(side)
+                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
+                                             workspace=ws_c, out=oc_, phase="rest")
+            else:
+                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
+                                             workspace=ws_c, out=oc_)
+        if STAGGER:
+            main_s.wait_event(validated)
         oa = C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
                                      out=oa_)
         if comm is not None:      # the one exchange: sum of grad_A over ranks
@@ -437,6 +454,9 @@ def main():
         main_s.wait_event(copied[i & 1])
         if i >= 2:
             main_s.wait_event(read_back[i & 1])       # outputs free again
+        # (the CTC stream waits for everything on main: letting a step's CTC
+        # chain start under the previous step's ASG gradient measured slower,
+        # 1.80-1.87e8 vs 1.89-1.91e8 frames/s)
         oa, oc = both(bi["em"], bi["el"], bi["ta"], bi["tc"], bi["tl"], outs[i & 1])
         consumed[i & 1].record(main_s)
         with torch.cuda.stream(d2h_s):

@@ -93,6 +93,16 @@ enum {
  * two passes, whatever the number of failures).  Results are the same either
  * way; this flag disables the routing (diagnostics, A/B timing). */
 #define W2L_FLAG_NO_ROUTE 128u
+/* Validation as its own phase.  PHASE_VALIDATE runs only the input checks
+ * (status, token CSR, routing counters) into status and the workspace;
+ * VALIDATED then runs the compute phases (chain and gradient, or those named
+ * by PHASE_CHAIN / PHASE_GRAD) without repeating them.  Lets a caller stagger
+ * two criteria on two streams: the second starts its validation when the
+ * first's has finished, so its recursions start that much later -- measured
+ * on the two-criteria step, the chains then share the SMs without the
+ * simultaneous-start slow mode. */
+#define W2L_FLAG_PHASE_VALIDATE 256u
+#define W2L_FLAG_VALIDATED 512u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

@@ -75,6 +75,8 @@ FLAG_CTC_LOGITS = 16
 FLAG_FORCE_EXACT = 32
 FLAG_NO_LOG_FALLBACK = 64
 FLAG_NO_ROUTE = 128
+FLAG_PHASE_VALIDATE = 256
+FLAG_VALIDATED = 512
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

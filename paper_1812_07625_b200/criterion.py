@@ -376,8 +376,13 @@ def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
         f |= nat.FLAG_PHASE_CHAIN
     elif phase == "grad":
         f |= nat.FLAG_PHASE_GRAD
+    elif phase == "validate":
+        f |= nat.FLAG_PHASE_VALIDATE
+    elif phase == "rest":
+        f |= nat.FLAG_VALIDATED
     elif phase != "all":
-        raise ContractError(f"phase must be 'all', 'chain' or 'grad', got {phase!r}")
+        raise ContractError("phase must be 'all', 'chain', 'grad', 'validate' or 'rest', "
+                            f"got {phase!r}")
     return f
 
 
@@ -411,6 +416,9 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     phase="chain" | "grad" splits the call (W2L_FLAG_PHASE_*): "chain" runs
     the recursions into the workspace, a later "grad" call with the same
     inputs, workspace and out on the same stream order finishes it.
+    phase="validate" runs only the input checks; a later phase="rest" call
+    (same inputs, workspace, out) runs everything after them
+    (W2L_FLAG_PHASE_VALIDATE / W2L_FLAG_VALIDATED: staggering two criteria).
     loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the recursions
     and the loss only: grad_emissions / grad_transitions are not computed.
     force_exact=True (W2L_FLAG_FORCE_EXACT) computes every utterance with

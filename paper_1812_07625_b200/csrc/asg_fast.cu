@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_body<true, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
   else
     asg_chain_body<false, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
-  W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid()));
+  W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid() | (hw_warpid() << 16)));
 }
 
 // ----------------------------------------------------------- grad kernel --

@@ -175,12 +175,13 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
     if (!rc && !loss_only) rc = from_cuda(launch_reduce_grad_trans(ga, status, d, grad_trans, s));
     return rc;
   }
-  if (phases & 1u) {
+  if ((phases & 1u) && !(flags & W2L_FLAG_VALIDATED)) {
     rc = from_cuda(launch_asg_validate<float>(em, em_len, tgt, tgt_len, trans, d, w.lpad, w.perm,
                                               w.tok_start, status, s, kPrepFast,
                                               route ? w.route : nullptr, w.prog));
     if (rc) return rc;
   }
+  if (flags & W2L_FLAG_PHASE_VALIDATE) return W2L_OK;
   trace(tr, s);  // validate
   rc = from_cuda(launch_asg_fast(em, em_len, tgt, tgt_len, trans, d, w, loss, grad_em, ga,
                                  status, s, tr, phases, 0));
@@ -340,7 +341,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
                                              logits));
     return rc;
   }
-  if (phases & 1u) {
+  if ((phases & 1u) && !(flags & W2L_FLAG_VALIDATED)) {
     // logits: the |row logsumexp| <= 1e-2 contract (criterion.py:96-101) does
     // not apply to unnormalised inputs
     rc = from_cuda(launch_ctc_validate<float>(logp, em_len, tgt, tgt_len, blank, d, w.lpad,
@@ -348,6 +349,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
                                               kPrepFast, route ? w.route : nullptr, w.prog));
     if (rc) return rc;
   }
+  if (flags & W2L_FLAG_PHASE_VALIDATE) return W2L_OK;
   trace(tr, s);  // validate
   rc = from_cuda(launch_ctc_fast(logp, em_len, tgt, tgt_len, blank, d, w, loss, grad_em, status,
                                  s, tr, phases, 0));

@@ -209,6 +209,11 @@ __device__ __forceinline__ unsigned smid() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
+__device__ __forceinline__ unsigned hw_warpid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tl_rec(unsigned long long tag, unsigned long long t0,
                                        unsigned long long t1, unsigned long long t2) {
   const unsigned i = atomicAdd(&g_tl_n, 1u);

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_body<true, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   else
     ctc_chain_body<false, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
-  W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid()));
+  W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid() | (hw_warpid() << 16)));
 }
 
 constexpr int kGradFramesPerBlock = 128;

@@ -109,26 +109,31 @@ __global__ void __launch_bounds__(128)
 __device__ bool block_any(int v) { return __syncthreads_or(v); }
 
 // grouped-by-token chain states: perm[tok_start[k] .. tok_start[k+1]) lists
-// the states (ASG: l, CTC: 2l+1) whose label is k, in ascending order.  The
-// targets are staged in shared memory; thread k < N appends the positions of
-// token k in one ordered scan.
-__device__ void build_token_csr(const int64_t *y, int L, int N, int state_mul, int state_off,
-                                int *perm, int *tok_start) {
-  __shared__ unsigned char ys[W2L_MAX_ASG_LABELS];
+// the states (ASG: l, CTC: 2l+1) whose label is k, in ascending order, from
+// the targets staged in shared memory (ys, valid tokens < N).
+__device__ void build_token_csr(const unsigned char *ys, int L, int N, int state_mul,
+                                int state_off, int *perm, int *tok_start) {
   __shared__ int cnt[33];
-  for (int l = threadIdx.x; l < L; l += blockDim.x) ys[l] = (unsigned char)y[l];
   if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
   __syncthreads();
   for (int l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&cnt[ys[l]], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k <= N; ++k) {
-      const int c = k < N ? cnt[k] : 0;
-      tok_start[k] = acc;
-      cnt[k] = acc;
-      acc += c;
+  // exclusive prefix over the N+1 counts by warp 0 (shuffle scan)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int c = lane < N ? cnt[lane] : 0;
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += v;
     }
+    const int excl = x - c;
+    const int total = __shfl_sync(0xffffffffu, x, 31);
+    if (lane < N) tok_start[lane] = excl;
+    if (lane == 0) tok_start[N] = total;
+    __syncwarp();
+    if (lane < N) cnt[lane] = excl;
   }
   __syncthreads();
   // warp 0 walks the targets 32 at a time: lanes holding the same token
@@ -149,88 +154,140 @@ __device__ void build_token_csr(const int64_t *y, int L, int N, int state_mul, i
   __syncthreads();
 }
 
+// Targets of utterance b into shared memory (one byte per label; tokens
+// outside [0, N) flagged in *oor), every thread's loads issued at once.
+// Inputs only: a prep kernel stages them before its PDL wait.
+constexpr int kPrepThreads = 128;
+template <int MAXL>
+__device__ __forceinline__ void stage_targets(const int64_t *y, int L, int N,
+                                              unsigned char *ys, int &oor) {
+  constexpr int K = (MAXL + kPrepThreads - 1) / kPrepThreads;
+  int64_t v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int l = threadIdx.x + kPrepThreads * k;
+    v[k] = l < L ? y[l] : 0;
+  }
+  oor = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int l = threadIdx.x + kPrepThreads * k;
+    if (l < L) {
+      oor |= (v[k] < 0 || v[k] >= N);
+      ys[l] = (unsigned char)(v[k] < 0 || v[k] >= N ? 0 : v[k]);
+    }
+  }
+}
+
 template <class TE>
-__global__ void asg_prep_kernel(const int32_t *__restrict__ em_len,
-                                const int64_t *__restrict__ tgt,
-                                const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans,
-                                Dims d, int lpad, int *perm, int *tok_start, int32_t *status,
-                                int mode, int *prog) {
-  pdl_enter();
+__global__ void __launch_bounds__(kPrepThreads)
+    asg_prep_kernel(const int32_t *__restrict__ em_len, const int64_t *__restrict__ tgt,
+                    const int32_t *__restrict__ tgt_len, const TE *__restrict__ trans, Dims d,
+                    int lpad, int *perm, int *tok_start, int32_t *status, int mode, int *prog) {
+  __shared__ unsigned char ys[W2L_MAX_ASG_LABELS];
+  pdl_launch_dependents();
   const int b = blockIdx.x;
-  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
+  // ---- inputs first (not written by em_check: they load under its tail)
   const int T = em_len[b], L = tgt_len[b];
+  const int Lc = min(max(L, 0), d.Lmax);
+  constexpr int KA = (W2L_MAX_TOKENS * W2L_MAX_TOKENS) / kPrepThreads;
+  TE av[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    const int i = threadIdx.x + kPrepThreads * k;
+    av[k] = i < d.N * d.N ? trans[i] : (TE)0;
+  }
+  int oor;
+  stage_targets<W2L_MAX_ASG_LABELS>(tgt + (size_t)b * d.Lmax, Lc, d.N, ys, oor);
+  // ---- then em_check's verdict
+  pdl_wait();
+  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int bits = status[b];
-  __syncthreads();
+  int bad = 0;
+  double amax = -CUDART_INF, amin = CUDART_INF;
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    if (threadIdx.x + kPrepThreads * k < d.N * d.N) {
+      const double a = (double)av[k];
+      bad |= !isfinite(a);
+      amax = fmax(amax, a);
+      amin = fmin(amin, a);
+    }
+  }
+  // fp32 fast path: a transition weight exp(A - max A) below ~e^-80 would
+  // be flushed to zero in BOTH directions (invisible to the consistency
+  // guard), so such transitions send the utterance to the float64 kernel
+  __shared__ double s_mx[kPrepThreads / 32], s_mn[kPrepThreads / 32];
+  amax = warp_max(amax);
+  amin = -warp_max(-amin);
+  if ((threadIdx.x & 31) == 0) {
+    s_mx[threadIdx.x >> 5] = amax;
+    s_mn[threadIdx.x >> 5] = amin;
+  }
+  __syncthreads();   // (also: the staged targets)
+  for (int q = 0; q < kPrepThreads / 32; ++q) {
+    amax = fmax(amax, s_mx[q]);
+    amin = fmin(amin, s_mn[q]);
+  }
+  int dup = 0;
+  for (int l = threadIdx.x + 1; l < Lc; l += kPrepThreads) dup |= ys[l] == ys[l - 1];
+  bad = block_any(bad);
+  oor = block_any(oor);
+  dup = block_any(dup);
   int code = W2L_OK;
   if (T < 1 || T > d.Tmax) {
     code = W2L_ERR_CONTRACT;                        // criterion.py:25-26
   } else if (bits & kBitNonFinite) {
     code = W2L_ERR_NUMERIC;                         // :27-28
+  } else if (bad) {
+    code = W2L_ERR_NUMERIC;                         // :179-180
+  } else if (L < 0 || L > d.Lmax) {
+    code = W2L_ERR_CONTRACT;
   } else {
-    int bad = 0;
-    double amax = -CUDART_INF, amin = CUDART_INF;
-    for (int i = threadIdx.x; i < d.N * d.N; i += blockDim.x) {
-      const double a = (double)trans[i];
-      bad |= !isfinite(a);
-      amax = fmax(amax, a);
-      amin = fmin(amin, a);
-    }
-    // fp32 fast path: a transition weight exp(A - max A) below ~e^-80 would
-    // be flushed to zero in BOTH directions (invisible to the consistency
-    // guard), so such transitions send the utterance to the float64 kernel
-    __shared__ double s_mx[4], s_mn[4];   // 128 threads
-    amax = warp_max(amax);
-    amin = -warp_max(-amin);
-    if ((threadIdx.x & 31) == 0) {
-      s_mx[threadIdx.x >> 5] = amax;
-      s_mn[threadIdx.x >> 5] = amin;
-    }
-    __syncthreads();
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-      amax = fmax(amax, s_mx[q]);
-      amin = fmin(amin, s_mn[q]);
-    }
     // 0: fp32 range; 1: fp64 range (kNeedsF64); 2: beyond it (kNeedsLog)
     const int range = mode != kPrepFast ? 0
                       : amin - amax < -(double)kFlushNats64 ? 2
                       : amin - amax < -(double)kFlushNats ? 1 : 0;
-    if (block_any(bad)) {
-      code = W2L_ERR_NUMERIC;                       // :179-180
-    } else if (L < 0 || L > d.Lmax) {
-      code = W2L_ERR_CONTRACT;
-    } else {
-      const int64_t *y = tgt + (size_t)b * d.Lmax;
-      int oor = 0, dup = 0;
-      for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        oor |= (y[i] < 0 || y[i] >= d.N);
-        dup |= (i > 0 && y[i] == y[i - 1]);
-      }
-      oor = block_any(oor);
-      dup = block_any(dup);
-      if (oor) code = W2L_ERR_TARGET;               // :36-40
-      else if (L == 0) code = W2L_ERR_TARGET;       // :183-184
-      else if (dup) code = W2L_ERR_CONTRACT;        // :185-186
-      else if (T < L) code = W2L_ERR_INFEASIBLE;    // :187-190
-      if (code == W2L_OK && perm)
-        build_token_csr(y, L, d.N, 1, 0, perm + (size_t)b * lpad, tok_start + b * 33);
-      if (code == W2L_OK && (mode == kPrepForceExact || range == 2)) code = kNeedsLog;
-      else if (code == W2L_OK && range == 1) code = kNeedsF64;
-    }
+    if (oor) code = W2L_ERR_TARGET;                 // :36-40
+    else if (L == 0) code = W2L_ERR_TARGET;         // :183-184
+    else if (dup) code = W2L_ERR_CONTRACT;          // :185-186
+    else if (T < L) code = W2L_ERR_INFEASIBLE;      // :187-190
+    if (code == W2L_OK && perm)
+      build_token_csr(ys, L, d.N, 1, 0, perm + (size_t)b * lpad, tok_start + b * 33);
+    if (code == W2L_OK && (mode == kPrepForceExact || range == 2)) code = kNeedsLog;
+    else if (code == W2L_OK && range == 1) code = kNeedsF64;
   }
   __syncthreads();
   if (threadIdx.x == 0) status[b] = code;
 }
 
-__global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
-                                const int64_t *__restrict__ tgt,
-                                const int32_t *__restrict__ tgt_len, int blank, Dims d,
-                                int lpad, int *perm, int *tok_start, int32_t *status, int mode,
-                                int *prog) {
-  pdl_enter();
+__global__ void __launch_bounds__(kPrepThreads)
+    ctc_prep_kernel(const int32_t *__restrict__ em_len, const int64_t *__restrict__ tgt,
+                    const int32_t *__restrict__ tgt_len, int blank, Dims d, int lpad, int *perm,
+                    int *tok_start, int32_t *status, int mode, int *prog) {
+  __shared__ unsigned char ys[W2L_MAX_CTC_LABELS + 1];
+  __shared__ int s_reps;
+  pdl_launch_dependents();
   const int b = blockIdx.x;
-  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
+  // ---- inputs first (not written by em_check: they load under its tail)
   const int T = em_len[b], L = tgt_len[b];
+  const int Lc = min(max(L, 0), d.Lmax);
+  int oor;
+  stage_targets<W2L_MAX_CTC_LABELS + 1>(tgt + (size_t)b * d.Lmax, Lc, d.N, ys, oor);
+  if (threadIdx.x == 0) s_reps = 0;
+  // ---- then em_check's verdict
+  pdl_wait();
+  if (prog && threadIdx.x < 2) prog[2 * b + threadIdx.x] = 0;   // streamed-gradient progress
   const int bits = status[b];
+  __syncthreads();   // the staged targets
+  int has_blank = 0, reps = 0;
+  for (int l = threadIdx.x; l < Lc; l += kPrepThreads) {
+    has_blank |= ys[l] == blank;
+    reps += (l > 0 && ys[l] == ys[l - 1]);
+  }
+  oor = block_any(oor);
+  has_blank = block_any(has_blank);
+  atomicAdd(&s_reps, reps);
   __syncthreads();
   int code = W2L_OK;
   if (T < 1 || T > d.Tmax) {
@@ -244,25 +301,11 @@ __global__ void ctc_prep_kernel(const int32_t *__restrict__ em_len,
   } else if (L < 0 || L > d.Lmax) {
     code = W2L_ERR_CONTRACT;
   } else {
-    const int64_t *y = tgt + (size_t)b * d.Lmax;
-    int oor = 0, has_blank = 0, reps = 0;
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-      oor |= (y[i] < 0 || y[i] >= d.N);
-      has_blank |= (y[i] == blank);
-      reps += (i > 0 && y[i] == y[i - 1]);
-    }
-    oor = block_any(oor);
-    has_blank = block_any(has_blank);
-    __shared__ int s_reps;
-    if (threadIdx.x == 0) s_reps = 0;
-    __syncthreads();
-    atomicAdd(&s_reps, reps);
-    __syncthreads();
     if (oor) code = W2L_ERR_TARGET;                           // :102
     else if (has_blank) code = W2L_ERR_TARGET;                // :103-104
     else if (T < L + s_reps) code = W2L_ERR_INFEASIBLE;       // :105-111
     if (code == W2L_OK && perm)
-      build_token_csr(y, L, d.N, 2, 1, perm + (size_t)b * lpad, tok_start + b * 33);
+      build_token_csr(ys, L, d.N, 2, 1, perm + (size_t)b * lpad, tok_start + b * 33);
     if (code == W2L_OK && mode == kPrepForceExact) code = kNeedsLog;
   }
   __syncthreads();
@@ -305,7 +348,7 @@ cudaError_t launch_asg_validate(const TE *em, const int32_t *em_len, const int64
                                 int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, 0, status, s, route, kRouteNatsAsg);
   if (err != cudaSuccess) return err;
-  return launch_maybe_pdl(asg_prep_kernel<TE>, dim3(d.B), dim3(128), 0, s, true, em_len, tgt,
+  return launch_maybe_pdl(asg_prep_kernel<TE>, dim3(d.B), dim3(kPrepThreads), 0, s, true, em_len, tgt,
                           tgt_len, trans, d, lpad, perm, tok_start, status, mode, prog);
 }
 template <class TE>
@@ -315,7 +358,7 @@ cudaError_t launch_ctc_validate(const TE *em, const int32_t *em_len, const int64
                                 int mode, int *route, int *prog) {
   cudaError_t err = em_check<TE>(em, em_len, d, check_lse, status, s, route, kRouteNatsCtc);
   if (err != cudaSuccess) return err;
-  return launch_maybe_pdl(ctc_prep_kernel, dim3(d.B), dim3(128), 0, s, true, em_len, tgt, tgt_len,
+  return launch_maybe_pdl(ctc_prep_kernel, dim3(d.B), dim3(kPrepThreads), 0, s, true, em_len, tgt, tgt_len,
                           blank, d, lpad, perm, tok_start, status, mode, prog);
 }
 template <class TE>

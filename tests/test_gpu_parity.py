@@ -397,6 +397,25 @@ def test_split_phase_calls_match_whole_calls():
                                    phase="grad")
     assert torch.equal(whole.loss, part.loss)
     assert torch.equal(whole.grad_emissions, part.grad_emissions)
+    # W2L_FLAG_PHASE_VALIDATE then W2L_FLAG_VALIDATED == one whole call, also
+    # with a failing utterance (its status comes from the validation call)
+    emc[1, 3, :] = 0.5   # a row that is not log-normalised: ContractError for utterance 1
+    xc = torch.from_numpy(emc).cuda()
+    whole = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, check=False)
+    part = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, workspace=wsc, check=False,
+                                   phase="validate")
+    part = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, workspace=wsc, out=part,
+                                   check=False, phase="rest")
+    assert whole.status.cpu().tolist()[1] != 0
+    assert torch.equal(whole.status, part.status)
+    assert torch.equal(whole.loss.nan_to_num(), part.loss.nan_to_num())
+    assert torch.equal(whole.grad_emissions, part.grad_emissions)
+    part = C.asg_loss_grad_batched(x, el, tg, tl, a, workspace=ws, phase="validate")
+    part = C.asg_loss_grad_batched(x, el, tg, tl, a, workspace=ws, out=part, phase="rest")
+    whole = C.asg_loss_grad_batched(x, el, tg, tl, a)
+    assert torch.equal(whole.loss, part.loss)
+    assert torch.equal(whole.grad_emissions, part.grad_emissions)
+    assert torch.equal(whole.grad_transitions, part.grad_transitions)
 
 
 def _ctc_logits_oracle(x, el, tg, tl, blank):

@@ -38,12 +38,17 @@ which = sys.argv[1] if len(sys.argv) > 1 else "both"
 FB = os.environ.get("TL_NOFB") != "1"   # TL_NOFB=1: no fallback tiers (timing-only builds)
 
 
+ASG_DELAY = int(os.environ.get("TL_ASG_DELAY", "0"))   # cycles the ASG stream is held back
+
+
 def call():
     if which in ("ctc", "both"):
         side.wait_stream(main)
         with torch.cuda.stream(side):
             C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB)
     if which in ("asg", "both"):
+        if ASG_DELAY:
+            torch.cuda._sleep(ASG_DELAY)
         C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB)
     main.wait_stream(side)
 
@@ -52,17 +57,34 @@ for _ in range(5):
     call()
 torch.cuda.synchronize()
 read(0), read(1)
-# a ~1 ms sleep ahead of the call, so every launch is queued before the GPU
-# reaches it (otherwise the host's enqueue latency shows up as gaps)
+# LOOP=n: n bench-like steps back to back (L2 flush + call), the last one
+# analysed; otherwise one call behind a ~1 ms sleep, so every launch is
+# queued before the GPU reaches it (the host's enqueue latency would show up
+# as gaps)
+loops = int(os.environ.get("LOOP", "0"))
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if loops else None
 torch.cuda._sleep(2_000_000)
 g0 = torch.cuda.Event(enable_timing=True)
 g1 = torch.cuda.Event(enable_timing=True)
-g0.record()
-call()
+if loops:
+    for i in range(loops):
+        flush.zero_()
+        if i == loops - 1:
+            g0.record()
+        call()
+else:
+    g0.record()
+    call()
 g1.record()
 torch.cuda.synchronize()
 print(f"call (events, after the sleep): {g0.elapsed_time(g1)*1e3:.1f} us")
 recs = np.concatenate([read(0), read(1)])
+if loops:   # keep the last step: records after its first chain start
+    kk = recs[:, 0].astype(np.int64) // 1000000
+    cs = np.sort(recs[(kk == 1) | (kk == 3), 1].astype(np.int64))
+    gaps = np.nonzero(np.diff(cs) > 150000)[0]   # steps are > 150 us apart
+    t_last = cs[gaps[-1] + 1] if len(gaps) else cs[0]
+    recs = recs[recs[:, 1].astype(np.int64) >= t_last - 20000]
 tag = recs[:, 0].astype(np.int64)
 kind = tag // 1000000
 t = recs[:, 1:].astype(np.int64)
@@ -76,12 +98,41 @@ for k, name in [(1, "ctc_chain"), (3, "asg_chain")]:
 # chain CTAs per SM (t2 of a chain record is its SM id) vs their end times
 ch = (kind == 1) | (kind == 3)
 if ch.any():
+    slot0 = t[ch, 2] >> 16        # hardware warp slot of the CTA's warp 0
+    t[ch, 2] &= 0xffff
     sm = t[ch, 2]
+    # ASG CTAs sharing an SM with a CTC CTA: who took the lower warp slots
+    kinds_ = kind[ch]
+    first, second = [], []
+    for smv in np.unique(sm):
+        idx = np.nonzero(sm == smv)[0]
+        if len(idx) == 2 and set(kinds_[idx]) == {1, 3}:
+            ia = idx[kinds_[idx] == 3][0]
+            ic = idx[kinds_[idx] == 1][0]
+            (first if slot0[ia] < slot0[ic] else second).append(ia)
+    for nm, lst in [("ASG below CTC (ASG slots first)", first), ("ASG above CTC", second)]:
+        if lst:
+            e = us(t[ch, 1][np.array(lst)])
+            sl = slot0[np.array(lst)]
+            print(f"  {nm}: n={len(lst)} end {e.min():7.1f}/{np.median(e):7.1f}/{e.max():7.1f} us;"
+                  f" ASG warp-0 slot mod 4: {np.bincount(sl % 4, minlength=4).tolist()}")
     cnt = {s: int((sm == s).sum()) for s in np.unique(sm)}
     for c in sorted(set(cnt.values())):
         m = np.array([cnt[s] == c for s in sm])
         e = us(t[ch, 1][m])
         print(f"chains on SMs hosting {c}: n={m.sum():4d} end {e.min():7.1f}/{np.median(e):7.1f}/{e.max():7.1f} us")
+    # SMs hosting two chain CTAs: which kinds share them
+    kinds = kind[ch]
+    pair = {}
+    for smv in np.unique(sm):
+        idx = np.nonzero(sm == smv)[0]
+        if len(idx) == 2:
+            pair[smv] = "+".join(sorted("asg" if kinds[i] == 3 else "ctc" for i in idx))
+    for pt in sorted(set(pair.values())):
+        m = np.array([pair.get(s_) == pt for s_ in sm])
+        e = us(t[ch, 1][m])
+        print(f"  pair {pt}: {m.sum() // 2:3d} SMs, chain end {e.min():7.1f}/{np.median(e):7.1f}/{e.max():7.1f} us;"
+              f" chain start spread {us(t[ch, 0][m]).min():.1f}..{us(t[ch, 0][m]).max():.1f}")
     k2 = kind[ch]
     for kk, nm in [(1, "ctc"), (3, "asg")]:
         mm = k2 == kk
