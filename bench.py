@@ -42,6 +42,8 @@ SEED = 20260004  # 20260000 + config index (C5)
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 # staggered start of the two criteria (W2L_BENCH_STAGGER=0 starts them together; A/B)
 STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
+# the later criterion's gradient streamed behind its chains (W2L_FLAG_STREAM_GRAD)
+STREAM_ASG = os.environ.get("W2L_BENCH_STREAM_ASG", "1") != "0"
 
 
 # ---------------------------------------------------------------- inputs --
@@ -378,7 +380,7 @@ def main():
         if STAGGER:
             main_s.wait_event(validated)
         oa = C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
-                                     out=oa_)
+                                     out=oa_, stream_grad=STREAM_ASG)
         if comm is not None:      # the one exchange: sum of grad_A over ranks
             comm.allreduce_grad_transitions(oa.grad_transitions)
         main_s.wait_stream(side)

@@ -103,6 +103,13 @@ enum {
  * simultaneous-start slow mode. */
 #define W2L_FLAG_PHASE_VALIDATE 256u
 #define W2L_FLAG_VALIDATED 512u
+/* Streamed gradient: the gradient kernels are launched as programmatic
+ * dependents of the chains and start on the middle frames of an utterance
+ * once its two directions have crossed, gated by per-utterance progress
+ * words.  Correct in every setting (the gradient grid only launches once
+ * every chain CTA is resident); faster when no other criterion's chains still
+ * need SMs, e.g. the later of two staggered criteria. */
+#define W2L_FLAG_STREAM_GRAD 1024u
 
 /* Library limits of the sm_100a kernels. */
 #define W2L_MAX_TOKENS 32        /* N: one lane per token in the N x N graph   */

@@ -77,6 +77,7 @@ FLAG_NO_LOG_FALLBACK = 64
 FLAG_NO_ROUTE = 128
 FLAG_PHASE_VALIDATE = 256
 FLAG_VALIDATED = 512
+FLAG_STREAM_GRAD = 1024
 MAX_TOKENS = 32
 MAX_ASG_LABELS = 1024
 MAX_CTC_LABELS = 511

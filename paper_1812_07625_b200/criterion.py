@@ -358,7 +358,7 @@ def _batch_inputs(emissions, em_len, targets, tgt_len, dev):
 
 
 def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
-           force_exact: bool = False, route: bool = True) -> int:
+           force_exact: bool = False, route: bool = True, stream_grad: bool = False) -> int:
     # fallback: True (every precision tier), False (fp32 only) or "f64" (the
     # fp32 and fp64 scaled-linear tiers, no log-domain kernel)
     f = 0 if fallback else nat.FLAG_NO_FALLBACK
@@ -372,6 +372,8 @@ def _flags(fallback, phase: str, loss_only: bool = False, logits: bool = False,
         f |= nat.FLAG_LOSS_ONLY
     if logits:
         f |= nat.FLAG_CTC_LOGITS
+    if stream_grad:
+        f |= nat.FLAG_STREAM_GRAD
     if phase == "chain":
         f |= nat.FLAG_PHASE_CHAIN
     elif phase == "grad":
@@ -400,7 +402,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
                           out: Optional[BatchLossOutput] = None,
                           fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
-                          force_exact: bool = False, route: bool = True) -> BatchLossOutput:
+                          force_exact: bool = False, route: bool = True,
+                          stream_grad: bool = False) -> BatchLossOutput:
     """Batched ASG loss + gradients on the device (fp32 path).
 
     emissions f32 [B,Tmax,N]; em_len int [B]; targets int64 [B,Lmax] padded
@@ -419,6 +422,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     phase="validate" runs only the input checks; a later phase="rest" call
     (same inputs, workspace, out) runs everything after them
     (W2L_FLAG_PHASE_VALIDATE / W2L_FLAG_VALIDATED: staggering two criteria).
+    stream_grad=True (W2L_FLAG_STREAM_GRAD) starts the gradient kernels on
+    the middle frames while the recursions are still running.
     loss_only=True (evaluation, W2L_FLAG_LOSS_ONLY) runs the recursions
     and the loss only: grad_emissions / grad_transitions are not computed.
     force_exact=True (W2L_FLAG_FORCE_EXACT) computes every utterance with
@@ -448,7 +453,8 @@ def asg_loss_grad_batched(emissions, em_len, targets, tgt_len, transitions, *, c
     args = (_p(em), _p(el), _p(tg), _p(tl), _p(a), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.grad_transitions), _p(out.grad_transitions_per_utt),
             _p(out.status), _p(ws), ws.numel(), _flags(fallback, phase, loss_only,
-                                                       force_exact=force_exact, route=route),
+                                                       force_exact=force_exact, route=route,
+                                                       stream_grad=stream_grad),
             _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
@@ -467,7 +473,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
                           fallback=True, trace: bool = False,
                           phase: str = "all", loss_only: bool = False,
                           logits: bool = False, force_exact: bool = False,
-                          route: bool = True) -> BatchLossOutput:
+                          route: bool = True, stream_grad: bool = False) -> BatchLossOutput:
     """Batched CTC loss + gradient on the device (fp32 path); emissions are
     log-probabilities f32 [B,Tmax,N] with |row logsumexp| <= 1e-2.  phase and
     loss_only: as for asg_loss_grad_batched.  logits=True
@@ -490,7 +496,7 @@ def ctc_loss_grad_batched(emissions, em_len, targets, tgt_len, blank_id: int, *,
             status=torch.empty(b, dtype=torch.int32, device=dev))
     args = (_p(em), _p(el), _p(tg), _p(tl), int(blank_id), b, t_max, n, lmax, _p(out.loss),
             _p(out.grad_emissions), _p(out.status), _p(ws), ws.numel(),
-            _flags(fallback, phase, loss_only, logits, force_exact, route), _stream())
+            _flags(fallback, phase, loss_only, logits, force_exact, route, stream_grad), _stream())
     if trace:
         ms, cnt = (ctypes.c_float * 16)(), ctypes.c_int(0)
         rc = lib.w2l_ctc_loss_grad_traced(*args, ms, ctypes.byref(cnt))

@@ -909,7 +909,8 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   // stream the gradient behind the chains (PDL) when both run in this call
   // and no stage trace separates them; otherwise the chains publish no
   // progress and the gradient CTAs do not wait
-  const bool stream = (phases & 1u) && (phases & 2u) && !(phases & 4u) && !tr && pdl_enabled();
+  const bool stream = (phases & 1u) && (phases & 2u) && !(phases & 4u) && !tr &&
+                      ((phases & 8u) || pdl_enabled());
   AsgFastWs wc = w;
   if (!stream) wc.prog = nullptr;
   cudaError_t err = cudaSuccess;

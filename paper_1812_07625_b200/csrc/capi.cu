@@ -158,7 +158,9 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
   if (!route) w.route = nullptr;
   float *ga = grad_trans_utt ? grad_trans_utt : ga_ws;
   const bool loss_only = flags & W2L_FLAG_LOSS_ONLY;
-  const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
+  // phases: bit 0 chain, 1 gradient, 2 loss only, 3 streamed gradient
+  const unsigned phases = (loss_only ? (1u | 4u) : phase_mask(flags)) |
+                          ((flags & W2L_FLAG_STREAM_GRAD) ? 8u : 0u);
   trace(tr, s);
   int rc = W2L_OK;
   if (force) {
@@ -326,7 +328,9 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
   const bool route = !(flags & (W2L_FLAG_NO_FALLBACK | W2L_FLAG_NO_ROUTE));
   if (!route) w.route = nullptr;
   w.logits = logits;
-  const unsigned phases = loss_only ? (1u | 4u) : phase_mask(flags);
+  // phases: bit 0 chain, 1 gradient, 2 loss only, 3 streamed gradient
+  const unsigned phases = (loss_only ? (1u | 4u) : phase_mask(flags)) |
+                          ((flags & W2L_FLAG_STREAM_GRAD) ? 8u : 0u);
   trace(tr, s);
   int rc = W2L_OK;
   if (flags & W2L_FLAG_FORCE_EXACT) {

@@ -140,3 +140,33 @@ def test_gradients_are_deterministic():
     c2 = C.ctc_loss_grad_batched(xc, elc, tgc, tlc, blank, check=False)
     assert torch.equal(c1.grad_emissions, c2.grad_emissions)
     assert torch.equal(c1.loss, c2.loss)
+
+
+@pytest.mark.parametrize("kind", ["asg", "ctc"])
+def test_streamed_gradient_matches_plain_call(kind):
+    # W2L_FLAG_STREAM_GRAD: the gradient CTAs run behind the chains, gated by
+    # the chains' progress words; the same kernels, so the results must be
+    # bitwise identical -- ragged lengths, a failing utterance, and a batch
+    # routed to the fp64 tier (peaky emissions)
+    if kind == "asg":
+        em, el, tg, tl, a = orc.synth_asg(56, 12, 1600, 30, 300, ragged=True)
+        em[3, 7, 2] = np.nan
+        x = torch.from_numpy(em).cuda()
+        run = lambda x_, **kw: C.asg_loss_grad_batched(x_, el, tg, tl, a, check=False, **kw)
+    else:
+        em, el, tg, tl, blank = orc.synth_ctc(57, 12, 1600, 30, 300, ragged=True)
+        em[3, 7, :] = 0.5
+        x = torch.from_numpy(em).cuda()
+        run = lambda x_, **kw: C.ctc_loss_grad_batched(x_, el, tg, tl, blank, check=False, **kw)
+    peaky = x * 10.0 if kind == "asg" else torch.log_softmax(x * 10.0, dim=-1)
+    if kind == "ctc":
+        peaky[3, 7, :] = 0.5   # keep utterance 3 failing
+    for inp in (x, peaky):
+        plain = run(inp)
+        streamed = run(inp, stream_grad=True)
+        assert torch.equal(plain.status, streamed.status)
+        assert plain.status.cpu().numpy()[3] != 0
+        assert torch.equal(plain.loss.nan_to_num(), streamed.loss.nan_to_num())
+        assert torch.equal(plain.grad_emissions, streamed.grad_emissions)
+        if kind == "asg":
+            assert torch.equal(plain.grad_transitions, streamed.grad_transitions)
