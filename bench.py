@@ -677,7 +677,11 @@ def main():
     # our kernels per step: ASG em_check, prep, chain, grad, final, exact
     # (fallback, early exit), reduce; CTC em_check, prep, chain, grad, final,
     # exact (+ the NCCL all-reduce at N > 1)
-    launches_per_step = 7 + 6
+    # library kernels per step (the ncu launch list, profiles/r2): ASG em_check,
+    # prep, chain, grad, final, fp64 chain / grad / final, log-domain, reduce
+    # (10); CTC the same without the reduction (9).  The status and routing
+    # memsets are not counted.
+    launches_per_step = 10 + 9
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
