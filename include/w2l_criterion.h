@@ -169,6 +169,25 @@ W2L_API int w2l_viterbi_f64(const double *em, const int32_t *em_len, const doubl
                     int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
                     size_t ws_bytes, w2l_stream_t stream);
 
+/* ---------------------------------------------- greedy evaluation --
+ * the reference's evaluate loop per utterance (trainer.py:465-514)
+ * on the device, for a batch of Viterbi paths (w2l_viterbi):
+ *   collapse the path (criterion.py:287-310): kind 0 = ASG (drop repeats,
+ *     the repetition token `special` -- or -1 -- becomes its predecessor),
+ *     kind 1 = CTC (drop repeats, then the blank `special`);
+ *   tok_dist[b]  Levenshtein distance of the collapsed path to ref[b];
+ *   word_dist[b] the same over silence-delimited token groups
+ *     (lexicon.py:182-195; silence < 0: the whole sequence is one group);
+ *   ref_words[b] the reference's group count;
+ *   hyp[B,Tmax]  the collapsed tokens (-1 padded), hyp_len[b] their count.
+ * status[b]: 0, or W2L_ERR_CONTRACT for a length out of range or an ASG path
+ * starting with the repetition token.  Tmax <= ~11000 (shared memory). */
+W2L_API int w2l_greedy_eval(const int64_t *path, const int32_t *path_len, int B, int Tmax,
+                    int kind, int special, const int64_t *ref, const int32_t *ref_len,
+                    int Lmax, int silence, int64_t *hyp, int32_t *hyp_len, int32_t *tok_dist,
+                    int32_t *word_dist, int32_t *ref_words, int32_t *status,
+                    w2l_stream_t stream);
+
 /* ------------------------------------------------- transition update --
  * the step after the transition-gradient all-reduce
  * (trainer.py:442-449, autodiff.py:429-433) in one N x N kernel:

@@ -288,6 +288,51 @@ def collapse(path, kind, blank_id=None, rep_id=None):
     return out
 
 
+# ------------------------------------------------- greedy evaluation --
+# (trainer.py:465-514, lexicon.py:182-195)
+
+def edit_distance(ref, hyp):
+    """Levenshtein distance, unit costs (trainer.py:465-476)."""
+    ref, hyp = list(ref), list(hyp)
+    if not ref:
+        return len(hyp)
+    prev = list(range(len(hyp) + 1))
+    for i, r in enumerate(ref, start=1):
+        cur = [i] + [0] * len(hyp)
+        for j, h in enumerate(hyp, start=1):
+            cur[j] = min(prev[j] + 1, cur[j - 1] + 1, prev[j - 1] + (r != h))
+        prev = cur
+    return prev[-1]
+
+
+def split_on_silence(ids, silence):
+    """Silence-free groups, empty groups dropped (lexicon.py:182-195)."""
+    groups, cur = [], []
+    for t in ids:
+        if t == silence:
+            if cur:
+                groups.append(cur)
+            cur = []
+        else:
+            cur.append(int(t))
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def greedy_metrics(path, ref, kind, blank_id=None, rep_id=None, silence=None):
+    """One utterance of trainer.evaluate (trainer.py:496-510): the collapsed
+    path's token edit distance, word edit distance and reference word count."""
+    hyp = collapse(path, kind, blank_id, rep_id)
+    ref = [int(t) for t in ref]
+    if silence is not None:
+        rw = [tuple(g) for g in split_on_silence(ref, silence)]
+        hw = [tuple(g) for g in split_on_silence(hyp, silence)]
+    else:
+        rw, hw = [tuple(ref)], [tuple(hyp)]
+    return hyp, edit_distance(ref, hyp), edit_distance(rw, hw), len(rw)
+
+
 # ------------------------------------------------ brute-force enumeration --
 # (restated from tests/oracles.py:87-144; exponential, toy sizes only)
 

@@ -26,7 +26,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompil
 # debug-only extra flags (e.g. -DW2L_PROF for the chain cycle profile)
 FLAGS += os.environ.get("W2L_EXTRA_NVCC_FLAGS", "").split()
 SOURCES = ["validate.cu", "viterbi.cu", "exact.cu", "asg_fast.cu", "ctc_fast.cu", "probe.cu",
-           "comm.cu", "capi.cu"]
+           "comm.cu", "evaluate.cu", "capi.cu"]
 
 
 def nvcc() -> str:

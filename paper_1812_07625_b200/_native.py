@@ -45,6 +45,8 @@ SIGNATURES = {
     "w2l_viterbi_workspace_bytes": (c_sz, [c_i, c_i, c_i]),
     "w2l_viterbi": (c_i, [c_p, c_p, c_p, c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "w2l_viterbi_f64": (c_i, [c_p, c_p, c_p, c_i, c_i, c_i, c_p, c_p, c_p, c_p, c_sz, c_p]),
+    "w2l_greedy_eval": (c_i, [c_p, c_p, c_i, c_i, c_i, c_i, c_p, c_p, c_i, c_i, c_p, c_p, c_p, c_p,
+                              c_p, c_p, c_p]),
     "w2l_asg_loss_grad_traced": (c_i, [c_p, c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_p, c_p,
                                        c_p, c_p, c_p, c_p, c_sz, ctypes.c_uint, c_p, c_p, c_p]),
     "w2l_ctc_loss_grad_traced": (c_i, [c_p, c_p, c_p, c_p, c_i, c_i, c_i, c_i, c_i, c_p, c_p,

@@ -45,7 +45,7 @@ __all__ = [
     "LossOutput", "BatchLossOutput", "validate_target", "ctc_loss_grad", "asg_loss_grad",
     "viterbi", "collapse_path", "CtcCriterion", "AsgCriterion", "make_criterion",
     "asg_loss_grad_batched", "ctc_loss_grad_batched", "viterbi_batched", "asg_loss",
-    "ctc_loss", "check_status",
+    "ctc_loss", "check_status", "GreedyEval", "greedy_eval_batched", "evaluate_batch",
 ]
 
 
@@ -532,6 +532,84 @@ def viterbi_batched(emissions, em_len, transitions=None, *, check=True, workspac
     if check:
         _raise_batch(st, "viterbi_batched")
     return path, score
+
+
+# ---------------------------------------------------- greedy evaluation --
+
+@dataclass
+class GreedyEval:
+    """Per-utterance greedy metrics of a batch (trainer.py:465-514):
+    the collapsed hypotheses (-1 padded), their lengths, the token and word
+    edit distances to the references and the references' word counts."""
+    hyp: torch.Tensor
+    hyp_len: torch.Tensor
+    tok_dist: torch.Tensor
+    word_dist: torch.Tensor
+    ref_words: torch.Tensor
+    status: torch.Tensor
+
+
+def greedy_eval_batched(paths, path_len, targets, tgt_len, kind: str, *, blank_id=None,
+                        rep_id=None, silence_id=None, check=True) -> GreedyEval:
+    """Collapse a batch of framewise paths (collapse_path, criterion.py:287-310)
+    and score them against the targets (edit_distance and split_on_silence,
+    trainer.py:465-510) on the device.  kind "ctc" needs blank_id; "asg"
+    takes the repetition token rep_id (or None)."""
+    dev = _device()
+    pa = _dev_tensor(paths, torch.int64, dev)
+    if pa.dim() != 2:
+        raise ContractError(f"paths must be B x Tmax, got {tuple(pa.shape)}")
+    b, t_max = pa.shape
+    pl = _dev_tensor(path_len, torch.int32, dev).reshape(-1)
+    tg = _dev_tensor(targets, torch.int64, dev)
+    if tg.dim() == 1:
+        tg = tg.reshape(b, -1)
+    tl = _dev_tensor(tgt_len, torch.int32, dev).reshape(-1)
+    if kind not in ("asg", "ctc"):
+        raise ContractError(f"unknown criterion kind {kind!r}")
+    if kind == "ctc" and blank_id is None:
+        raise ContractError("CTC collapse needs blank_id")
+    special = int(blank_id) if kind == "ctc" else (-1 if rep_id is None else int(rep_id))
+    out = GreedyEval(hyp=torch.empty((b, t_max), dtype=torch.int64, device=dev),
+                     hyp_len=torch.empty(b, dtype=torch.int32, device=dev),
+                     tok_dist=torch.empty(b, dtype=torch.int32, device=dev),
+                     word_dist=torch.empty(b, dtype=torch.int32, device=dev),
+                     ref_words=torch.empty(b, dtype=torch.int32, device=dev),
+                     status=torch.empty(b, dtype=torch.int32, device=dev))
+    rc = nat.lib().w2l_greedy_eval(_p(pa), _p(pl), b, t_max, 0 if kind == "asg" else 1, special,
+                                   _p(tg), _p(tl), int(tg.shape[1]),
+                                   -1 if silence_id is None else int(silence_id), _p(out.hyp),
+                                   _p(out.hyp_len), _p(out.tok_dist), _p(out.word_dist),
+                                   _p(out.ref_words), _p(out.status), _stream())
+    _check_call(rc, "w2l_greedy_eval")
+    if check:
+        _raise_batch(out.status, "greedy_eval_batched")
+    return out
+
+
+def evaluate_batch(emissions, em_len, targets, tgt_len, kind: str, *, transitions=None,
+                   blank_id=None, rep_id=None, silence_id=None) -> dict:
+    """One batch of the reference's evaluate loop (trainer.py:478-514) on the
+    device: loss-only criterion, Viterbi paths (with the transitions for ASG,
+    argmax paths for CTC: criterion.py:334-336, 364-366), collapse, token and
+    word edit distances.  Utterances with an empty reference are skipped, as
+    the reference does.  Returns the sums the reference accumulates."""
+    dev = _device()
+    em = _dev_tensor(emissions, torch.float32, dev)
+    el = _dev_tensor(em_len, torch.int32, dev).reshape(-1)
+    tl = _dev_tensor(tgt_len, torch.int32, dev).reshape(-1)
+    if kind == "asg":
+        out = asg_loss_grad_batched(em, el, targets, tl, transitions, loss_only=True)
+        paths, _ = viterbi_batched(em, el, transitions)
+    else:
+        out = ctc_loss_grad_batched(em, el, targets, tl, blank_id, loss_only=True)
+        paths, _ = viterbi_batched(em, el, None)
+    g = greedy_eval_batched(paths, el, targets, tl, kind, blank_id=blank_id, rep_id=rep_id,
+                            silence_id=silence_id)
+    keep = tl > 0
+    return {"loss_sum": float(out.loss[keep].sum()), "utterances": int(keep.sum()),
+            "tok_dist": int(g.tok_dist[keep].sum()), "tok_len": int(tl[keep].sum()),
+            "word_dist": int(g.word_dist[keep].sum()), "word_len": int(g.ref_words[keep].sum())}
 
 
 # ------------------------------------------------------------- autograd --

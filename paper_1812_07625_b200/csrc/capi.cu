@@ -457,6 +457,23 @@ int w2l_viterbi_f64(const double *em, const int32_t *em_len, const double *trans
       launch_viterbi<double, double>(em, em_len, trans, d, path, score, status, ws, s));
 }
 
+int w2l_greedy_eval(const int64_t *path, const int32_t *path_len, int B, int Tmax, int kind,
+                    int special, const int64_t *ref, const int32_t *ref_len, int Lmax,
+                    int silence, int64_t *hyp, int32_t *hyp_len, int32_t *tok_dist,
+                    int32_t *word_dist, int32_t *ref_words, int32_t *status,
+                    w2l_stream_t stream) {
+  if (B < 0 || Tmax < 1 || Lmax < 0 || (kind != 0 && kind != 1) || (kind == 1 && special < 0))
+    return W2L_ERR_CONTRACT;
+  if (greedy_eval_smem_bytes(Tmax, Lmax) > 227 * 1024) return W2L_ERR_CONTRACT;
+  if (B == 0) return W2L_OK;
+  if (!path || !path_len || !ref || !ref_len || !hyp || !hyp_len || !tok_dist || !word_dist ||
+      !ref_words || !status)
+    return W2L_ERR_CONTRACT;
+  return from_cuda(launch_greedy_eval(path, path_len, B, Tmax, kind, special, ref, ref_len,
+                                      max(Lmax, 1), silence, hyp, hyp_len, tok_dist, word_dist,
+                                      ref_words, status, (cudaStream_t)stream));
+}
+
 int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_sum, int N,
                              int batch_size, float lr, float momentum, w2l_stream_t stream) {
   if (N < 1 || N > W2L_MAX_TOKENS || batch_size < 1 || !trans || !velocity || !grad_sum)

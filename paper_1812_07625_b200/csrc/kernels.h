@@ -129,6 +129,14 @@ int tl_read_ctc(unsigned long long *host, int maxn);
 int tl_read_asg(unsigned long long *host, int maxn);
 #endif
 
+// ---- greedy evaluation (evaluate.cu)
+size_t greedy_eval_smem_bytes(int Tmax, int Lmax);
+cudaError_t launch_greedy_eval(const int64_t *path, const int32_t *path_len, int B, int Tmax,
+                               int kind, int special, const int64_t *ref, const int32_t *ref_len,
+                               int Lmax, int silence, int64_t *hyp, int32_t *hyp_len,
+                               int32_t *tok_dist, int32_t *word_dist, int32_t *ref_words,
+                               int32_t *status, cudaStream_t s);
+
 // ---- microbenchmarks
 int probe_peaks(double *mufu, double *dadd, double *ffma);
 
