@@ -112,3 +112,30 @@ def test_evaluate_batch_matches_reference_loop():
     assert (r["tok_dist"], r["tok_len"], r["word_dist"], r["word_len"]) == (tok, tok_len, word,
                                                                             word_len)
     assert abs(r["loss_sum"] - loss_sum) <= 1e-4 * abs(loss_sum)
+
+
+def test_reference_golden_cases():
+    # the reference's own collapse_path / edit_distance / split_on_silence
+    # outputs (tests/golden/make_eval_golden.py), batched through the kernel
+    import json
+    import os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "eval_golden.json")))
+    for kind in ("ctc", "asg"):
+        for sil in sorted({c["silence"] for c in cases if c["kind"] == kind}):
+            cs = [c for c in cases if c["kind"] == kind and c["silence"] == sil]
+            t_max = max(len(c["path"]) for c in cs)
+            l_max = max(1, max(len(c["ref"]) for c in cs))
+            paths = np.zeros((len(cs), t_max), np.int64)
+            tg = np.full((len(cs), l_max), -1, np.int64)
+            for i, c in enumerate(cs):
+                paths[i, :len(c["path"])] = c["path"]
+                tg[i, :len(c["ref"])] = c["ref"]
+            plen = np.array([len(c["path"]) for c in cs], np.int32)
+            tl = np.array([len(c["ref"]) for c in cs], np.int32)
+            g = C.greedy_eval_batched(paths, plen, tg, tl, kind, blank_id=cs[0]["blank"],
+                                      rep_id=cs[0]["rep"], silence_id=None if sil < 0 else sil)
+            hyp, hl = g.hyp.cpu().numpy(), g.hyp_len.cpu().numpy()
+            for i, c in enumerate(cs):
+                assert list(hyp[i, :hl[i]]) == c["hyp"]
+                assert (int(g.tok_dist[i]), int(g.word_dist[i]), int(g.ref_words[i])) == \
+                    (c["tok_dist"], c["word_dist"], c["ref_words"])

@@ -114,3 +114,18 @@ def test_validation_order():
     e = orc.log_softmax_rows(np.zeros((2, 3)))
     assert orc.ctc_validate(e, [0, 0], 2)[0] == "InfeasibleTargetError"
     assert orc.ctc_validate(e, [2], 2)[0] == "TargetError"
+
+
+def test_greedy_evaluation_restatement_matches_reference_goldens():
+    # tests/golden/eval_golden.json: collapse_path, edit_distance and
+    # split_on_silence run by the reference itself (make_eval_golden.py)
+    import json
+    import os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "eval_golden.json")))
+    assert len(cases) == 120
+    for c in cases:
+        sil = None if c["silence"] < 0 else c["silence"]
+        hyp, td, wd, rw = orc.greedy_metrics(c["path"], c["ref"], c["kind"], blank_id=c["blank"],
+                                             rep_id=c["rep"], silence=sil)
+        assert hyp == c["hyp"]
+        assert (td, wd, rw) == (c["tok_dist"], c["word_dist"], c["ref_words"])
