@@ -196,6 +196,7 @@ struct FccCtx {
   int N, T, lane, cons_idx;
   V *rows;      // [Tmax][32] this utterance
   int *ks;      // cumulative exponents, indexed by frame
+  bool stream = false;   // streamed gradient: trigger the dependent launch mid-utterance
 };
 
 // fcc recursion over the shared Et ring (criterion.py:227-236); the same
@@ -242,9 +243,11 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
   const int pro_end = min(T, kBlk);
   for (int j = 1; j < pro_end; ++j) generic(j);
   const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
+  const int mtrig = c.stream ? stream_trigger_block(T) : -1;   // (see lattice_run)
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
+    if (m == mtrig) pdl_launch_dependents();
     wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, &sm.prod, 0, &sm.prod, 0);
     const V *eb = sm.ering[j0 & (kRing - 1)];
     const int tb = frame_of(FWD, T, j0);
@@ -272,6 +275,7 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
     publish(mycons, j0 + kBlk, lane);
   }
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
+  if (c.stream && mtrig > nfull) pdl_launch_dependents();
   publish(mycons, kDone, lane);
   V z;
   if (FWD) {
@@ -308,6 +312,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     fc.cons_idx = 0;
     fc.rows = reinterpret_cast<V *>(FWD ? w.fcc_a : w.fcc_b) + (size_t)b * d.Tmax * 32;
     fc.ks = FWD ? w.fcc_ka + (size_t)b * w.tpad : w.fcc_kb + (size_t)b * w.tpad + 1;
+    fc.stream = w.prog != nullptr;
     fcc_run<FWD, V>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
   } else if (warp - 2 < weff) {
     LatCtx c;
@@ -322,9 +327,13 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     const size_t ub = (size_t)b * w.W * d.Tmax;
     c.rows = reinterpret_cast<V *>(FWD ? w.fac_a : w.fac_b) + ub * kLatStates;
     c.exps = (FWD ? w.fac_ea : w.fac_eb) + ub * 32;
+    c.stream = w.prog != nullptr;
     LatState<V> f;
     lat_init_weights<kFac, FWD, V>(f, c.w, lane, d.N, L, y, L, trans, amax, 0);
     lattice_run<kFac, FWD, V>(sm, c, f);
+  } else if (w.prog) {   // a warp without a role: its share of the trigger, at
+    wait_ge(&sm.cons[1], (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV);   // lattice warp 0's midpoint
+    pdl_launch_dependents();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -358,10 +367,10 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     }
     return;
   }
-  // streamed gradient: its CTAs may launch now (they wait on the progress
-  // words); otherwise a CTA with work triggers nothing before it completes,
-  // so the gradient grid only takes SMs once the chains are done
-  if (gprog) pdl_launch_dependents();
+  // streamed gradient: every warp triggers the dependent launch once its own
+  // progress passes the middle of the utterance (lattice_run, producer_run),
+  // so the gradient CTAs take SMs only when their first frames are ready;
+  // otherwise a CTA with work triggers nothing before it completes
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(L);
   if (threadIdx.x == 0) sm.prod = 0, sm.flush = 0;

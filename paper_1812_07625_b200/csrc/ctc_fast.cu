@@ -52,9 +52,13 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
     const size_t ub = (size_t)b * w.W * d.Tmax;
     c.rows = reinterpret_cast<V *>(FWD ? w.a : w.b) + ub * kLatStates;
     c.exps = (FWD ? w.ea : w.eb) + ub * 32;
+    c.stream = w.prog != nullptr;
     LatState<V> f;
     lat_init_weights<kCtc, FWD, V>(f, c.w, lane, d.N, S, y, L, nullptr, 0.f, blank);
     lattice_run<kCtc, FWD, V>(sm, c, f);
+  } else if (w.prog) {   // a warp without a role: its share of the trigger, at
+    wait_ge(&sm.cons[0], (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV);   // lattice warp 0's midpoint
+    pdl_launch_dependents();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -88,10 +92,10 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     }
     return;
   }
-  // streamed gradient: its CTAs may launch now (they wait on the progress
-  // words); otherwise a CTA with work triggers nothing before it completes,
-  // so the gradient grid only takes SMs once the chains are done
-  if (gprog) pdl_launch_dependents();
+  // streamed gradient: every warp triggers the dependent launch once its own
+  // progress passes the middle of the utterance (lattice_run, producer_run),
+  // so the gradient CTAs take SMs only when their first frames are ready;
+  // otherwise a CTA with work triggers nothing before it completes
   const int T = em_len[b], L = tgt_len[b];
   const int weff = lat_warps(2 * L + 1);
   __shared__ unsigned s_mask;

@@ -53,8 +53,20 @@ constexpr int kMaxLatWarps = 32 / kSpl;    // 1024 states
 constexpr int kBndRing = 128;              // boundary ring (steps): decouples neighbouring warps
 constexpr int kCounters = kMaxLatWarps + 2;  // lattice warps + fcc warp (+ spare)
 constexpr int kDone = 1 << 30;             // progress of a finished consumer
+
 constexpr int kRenormF = 4;                // steps between lane renormalisations
 constexpr int kBlk = 8;                    // steps per unrolled block (one publish / wait per block)
+
+// Streamed gradient: the block of kBlk steps after which a chain warp
+// triggers the dependent launch (its steps then reach T / W2L_TRIG_DIV)
+#ifndef W2L_TRIG_DIV
+#define W2L_TRIG_DIV 2
+#endif
+__device__ __forceinline__ int stream_trigger_block(int T) {
+  const int need = (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV;
+  return max(1, (need + kBlk - 1) / kBlk - 1);
+}
+
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
 // The producer runs up to a ring ahead of the recursions and then polls for
 // free slots; each poll takes issue slots from the recursion warps of the
@@ -264,6 +276,7 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
   double shifts = 0.0;
   bool flush = false;
   int published = 0;
+  bool trig = false;   // streamed gradient: this warp's share of the dependent launch
   const int nch = (c.T + kChunk - 1) / kChunk;
   // kProdStages - 1 chunks in flight ahead of the one being converted (an
   // empty commit group keeps the wait count uniform past the end)
@@ -315,7 +328,12 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
     if (c.gprog && lane == 0) prod_publish(sm, c, published);
+    if (c.gprog && !trig && W2L_TRIG_DIV * (p0 + rows) >= c.T) {
+      pdl_launch_dependents();   // (see lattice_run)
+      trig = true;
+    }
   }
+  if (c.gprog && !trig) pdl_launch_dependents();
   // the recursions trail the producer by up to the ring depth: keep
   // publishing until they are done (T - 1: see prod_publish)
   if (c.gprog && lane == 0) {
@@ -343,6 +361,7 @@ struct LatCtx {
   void *rows;        // rows of this utterance: V [W][Tmax][128]
   int *exps;         //                         int [W][Tmax][32]
   int Tmax;
+  bool stream = false;   // streamed gradient (W2L_FLAG_STREAM_GRAD)
 };
 
 template <class V>
@@ -599,6 +618,11 @@ __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
 
   // ---- full blocks of kBlk steps at j0 = 8 m
   const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
+  // Streamed gradient: the dependent gradient grid launches once every
+  // warp of every chain CTA has passed the middle of its utterance, when
+  // the first frames have both their rows -- its CTAs then do not hold SMs
+  // while there is nothing to do (another criterion's kernels need them).
+  const int mtrig = c.stream ? stream_trigger_block(T) : -1;
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
@@ -637,9 +661,11 @@ __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
     else
       run_block(std::false_type{});
     publish(mycons, j0 + kBlk, lane);
+    if (m == mtrig) pdl_launch_dependents();
   }
   // ---- tail steps
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
+  if (c.stream && mtrig > nfull) pdl_launch_dependents();
   publish(mycons, kDone, lane);
 
   // ---- totals (criterion.py:136-141 CTC, :203 fac forward; backward: the

@@ -41,15 +41,30 @@ FB = os.environ.get("TL_NOFB") != "1"   # TL_NOFB=1: no fallback tiers (timing-o
 ASG_DELAY = int(os.environ.get("TL_ASG_DELAY", "0"))   # cycles the ASG stream is held back
 
 
+SCHED = os.environ.get("TL_SCHED", "bench")   # "bench": bench.py's schedule; "plain"
+validated = torch.cuda.Event()
+
+
 def call():
+    bench_sched = SCHED == "bench" and which == "both"
     if which in ("ctc", "both"):
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB)
+            if bench_sched:   # staggered: ASG starts when CTC's validation is done
+                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB,
+                                        phase="validate")
+                validated.record(side)
+                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB,
+                                        phase="rest")
+            else:
+                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB)
     if which in ("asg", "both"):
         if ASG_DELAY:
             torch.cuda._sleep(ASG_DELAY)
-        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB)
+        if bench_sched:
+            main.wait_event(validated)
+        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB,
+                                stream_grad=bench_sched)
     main.wait_stream(side)
 
 
