@@ -40,10 +40,14 @@ METRIC = "ASG/CTC loss+grad frames/sec (B×T) at 1/2/4/8 B200; % of HBM/SFU roof
 B_PER_GPU, T_FR, N_TOK, L_LAB = 64, 1600, 30, 300
 SEED = 20260004  # 20260000 + config index (C5)
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")
-# staggered start of the two criteria (W2L_BENCH_STAGGER=0 starts them together; A/B)
+# The two-criteria step's schedule (A/B knobs):
+# staggered start (W2L_BENCH_STAGGER=0 starts both criteria together), which
+# criterion starts first (W2L_BENCH_FIRST=asg|ctc), and which criteria stream
+# their gradient behind their chains (W2L_FLAG_STREAM_GRAD)
 STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
-# the later criterion's gradient streamed behind its chains (W2L_FLAG_STREAM_GRAD)
+FIRST = os.environ.get("W2L_BENCH_FIRST", "asg")
 STREAM_ASG = os.environ.get("W2L_BENCH_STREAM_ASG", "1") != "0"
+STREAM_CTC = os.environ.get("W2L_BENCH_STREAM_CTC", "0") == "1"
 
 
 # ---------------------------------------------------------------- inputs --
@@ -354,33 +358,40 @@ def main():
 
     side = torch.cuda.Stream(device=dev)
     main_s = torch.cuda.current_stream(dev)
-    validated = torch.cuda.Event()   # CTC's validation done (the staggered start)
+    validated = torch.cuda.Event()   # the first criterion's validation done (staggered start)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def both(em_, el_, ta_, tc_, tl_, outs=None):
         oa_, oc_ = outs if outs is not None else (out_a, out_c)
-        # the two criteria run concurrently on two streams (chain CTAs of both
-        # are co-resident: maximum shared-memory carveout)
+
+        def asg(**kw):
+            return C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
+                                           out=oa_, stream_grad=STREAM_ASG, **kw)
+
+        def ctc(**kw):
+            return C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False, workspace=ws_c,
+                                           out=oc_, stream_grad=STREAM_CTC, **kw)
+
+        # The two criteria run concurrently on two streams (the chain CTAs of
+        # both are co-resident: maximum shared-memory carveout).  Staggered
+        # start: the second criterion begins its validation when the first's
+        # has finished, so its recursions start ~20 us later.  Started
+        # together, the two chains sharing each SM fall into a slow mode on
+        # about two thirds of the steps (per-step device times 0.49 vs
+        # 0.53-0.58 ms, tools/step_times.py).  ASG (the longer chains) goes
+        # first, and streams its gradient behind its chains.
+        first, second = (asg, ctc) if FIRST == "asg" else (ctc, asg)
         side.wait_stream(main_s)
-        # Staggered start: ASG begins its validation when CTC's has finished,
-        # so its recursions start ~25 us after CTC's.  Started together, the
-        # two chains sharing each SM fall into a slow mode on about two thirds
-        # of the steps (per-step device times 0.49 vs 0.53-0.58 ms,
-        # tools/step_times.py); staggered, every step runs in the fast mode.
-        with torch.cuda.stream(side):
-            if STAGGER:
-                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
-                                             workspace=ws_c, out=oc_, phase="validate")
-                validated.record(side)
-                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
-                                             workspace=ws_c, out=oc_, phase="rest")
-            else:
-                oc = C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False,
-                                             workspace=ws_c, out=oc_)
         if STAGGER:
-            main_s.wait_event(validated)
-        oa = C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
-                                     out=oa_, stream_grad=STREAM_ASG)
+            o1 = first(phase="validate")
+            validated.record(main_s)
+            o1 = first(phase="rest")
+            side.wait_event(validated)
+        else:
+            o1 = first()
+        with torch.cuda.stream(side):
+            o2 = second()
+        oa, oc = (o1, o2) if FIRST == "asg" else (o2, o1)
         if comm is not None:      # the one exchange: sum of grad_A over ranks
             comm.allreduce_grad_transitions(oa.grad_transitions)
         main_s.wait_stream(side)
@@ -484,8 +495,10 @@ def main():
         torch.cuda.synchronize(dev)
         e_s.record(main_s)
         copy_s.wait_stream(main_s)
+        h0 = time.perf_counter()
         for i in range(args.steps):
             e2e_step(i, grads)
+        host_ms.append((time.perf_counter() - h0) * 1e3 / args.steps)
         main_s.wait_stream(d2h_s)
         e_e.record(main_s)
         e_e.synchronize()
@@ -494,6 +507,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return frames_step * args.steps / (float(t.item()) / 1e3)
 
+    host_ms = []   # host enqueue time per e2e step (is the e2e host-bound?)
     e2e_value = e2e_run(False)
     e2e_grads_value = e2e_run(True)
     h2d = em.nbytes + asg_t.nbytes + ctc_t.nbytes + em_len.nbytes + tgt_len.nbytes
@@ -693,16 +707,24 @@ def main():
                                + ("(strong scaling)" if strong else
                                   "(C3 shape per GPU; C5 B=512 at 8 GPUs)"),
                    "global_batch": g_batch, "frames_per_step": frames_step,
-                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between steps"},
+                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between steps",
+                   "schedule": (f"two streams, {FIRST} first"
+                                + (", staggered" if STAGGER else ", together")
+                                + "; streamed gradient: "
+                                + ("+".join([k for k, v in (("asg", STREAM_ASG),
+                                                            ("ctc", STREAM_CTC)) if v])
+                                   or "none"))},
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "boundary": "pinned host inputs in, per-utterance losses out (on-GPU training "
-                            "keeps the gradients on the device)"},
+                            "keeps the gradients on the device)",
+                "host_enqueue_ms_per_step": round(host_ms[0], 4)},
         "e2e_grads_to_host": {"value": e2e_grads_value, "unit": "frames/s",
                               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_grads,
                               "boundary": "as e2e, plus both emission gradients and grad_A "
                                           "back to pinned host memory (the reference API's "
-                                          "return values)"},
+                                          "return values)",
+                              "host_enqueue_ms_per_step": round(host_ms[1], 4)},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
         "roofline_sfu": roof_sfu,

@@ -38,7 +38,7 @@ which = sys.argv[1] if len(sys.argv) > 1 else "both"
 FB = os.environ.get("TL_NOFB") != "1"   # TL_NOFB=1: no fallback tiers (timing-only builds)
 
 
-ASG_DELAY = int(os.environ.get("TL_ASG_DELAY", "0"))   # cycles the ASG stream is held back
+ASG_DELAY = int(os.environ.get("TL_ASG_DELAY", "0"))   # cycles the second stream is held back
 
 
 SCHED = os.environ.get("TL_SCHED", "bench")   # "bench": bench.py's schedule; "plain"
@@ -47,24 +47,28 @@ validated = torch.cuda.Event()
 
 def call():
     bench_sched = SCHED == "bench" and which == "both"
-    if which in ("ctc", "both"):
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            if bench_sched:   # staggered: ASG starts when CTC's validation is done
-                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB,
-                                        phase="validate")
-                validated.record(side)
-                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB,
-                                        phase="rest")
-            else:
-                C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False, fallback=FB)
-    if which in ("asg", "both"):
+    asg = lambda **kw: C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB,
+                                               stream_grad=bench_sched and bench.STREAM_ASG, **kw)
+    ctc = lambda **kw: C.ctc_loss_grad_batched(d, el_d, tc_d, tl_d, blank, check=False,
+                                               fallback=FB,
+                                               stream_grad=bench_sched and bench.STREAM_CTC, **kw)
+    if which != "both":
+        (asg if which == "asg" else ctc)()
+        return
+    # bench.py's schedule (first criterion, stagger) or both started together
+    first, second = (asg, ctc) if bench.FIRST == "asg" else (ctc, asg)
+    side.wait_stream(main)
+    if bench_sched and bench.STAGGER:
+        first(phase="validate")
+        validated.record(main)
+        first(phase="rest")
+        side.wait_event(validated)
+    else:
+        first()
+    with torch.cuda.stream(side):
         if ASG_DELAY:
             torch.cuda._sleep(ASG_DELAY)
-        if bench_sched:
-            main.wait_event(validated)
-        C.asg_loss_grad_batched(d, el_d, ta_d, tl_d, A_d, check=False, fallback=FB,
-                                stream_grad=bench_sched)
+        second()
     main.wait_stream(side)
 
 
