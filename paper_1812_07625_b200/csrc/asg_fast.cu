@@ -332,7 +332,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     lat_init_weights<kFac, FWD, V>(f, c.w, lane, d.N, L, y, L, trans, amax, 0);
     lattice_run<kFac, FWD, V>(sm, c, f);
   } else if (w.prog) {   // a warp without a role: its share of the trigger, at
-    wait_ge(&sm.cons[1], (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV);   // lattice warp 0's midpoint
+    wait_ge(&sm.cons[1], stream_trigger_step(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
   __syncthreads();

@@ -57,7 +57,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
     lat_init_weights<kCtc, FWD, V>(f, c.w, lane, d.N, S, y, L, nullptr, 0.f, blank);
     lattice_run<kCtc, FWD, V>(sm, c, f);
   } else if (w.prog) {   // a warp without a role: its share of the trigger, at
-    wait_ge(&sm.cons[0], (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV);   // lattice warp 0's midpoint
+    wait_ge(&sm.cons[0], stream_trigger_step(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
   __syncthreads();

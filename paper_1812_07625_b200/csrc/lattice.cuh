@@ -57,14 +57,20 @@ constexpr int kDone = 1 << 30;             // progress of a finished consumer
 constexpr int kRenormF = 4;                // steps between lane renormalisations
 constexpr int kBlk = 8;                    // steps per unrolled block (one publish / wait per block)
 
-// Streamed gradient: the block of kBlk steps after which a chain warp
-// triggers the dependent launch (its steps then reach T / W2L_TRIG_DIV)
+// Streamed gradient: a chain warp triggers the dependent launch once its
+// steps reach stream_trigger_step(T) = ceil(T NUM / DIV) (the midpoint), i.e.
+// after the block of kBlk steps stream_trigger_block(T)
+#ifndef W2L_TRIG_NUM
+#define W2L_TRIG_NUM 1
+#endif
 #ifndef W2L_TRIG_DIV
 #define W2L_TRIG_DIV 2
 #endif
+__host__ __device__ __forceinline__ int stream_trigger_step(int T) {
+  return (T * W2L_TRIG_NUM + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV;
+}
 __device__ __forceinline__ int stream_trigger_block(int T) {
-  const int need = (T + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV;
-  return max(1, (need + kBlk - 1) / kBlk - 1);
+  return max(1, (stream_trigger_step(T) + kBlk - 1) / kBlk - 1);
 }
 
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
@@ -328,7 +334,7 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
     if (c.gprog && lane == 0) prod_publish(sm, c, published);
-    if (c.gprog && !trig && W2L_TRIG_DIV * (p0 + rows) >= c.T) {
+    if (c.gprog && !trig && p0 + rows >= stream_trigger_step(c.T)) {
       pdl_launch_dependents();   // (see lattice_run)
       trig = true;
     }

@@ -1,0 +1,5 @@
+# streamed-gradient trigger point: T/2 (cur) vs 2T/5, 3T/5, 2T/3, 3T/4
+W2L_LIB=abl/t23.so timeout 600 python -m pytest tests/test_gpu_band.py -x -q -p no:cacheprovider 2>&1 | tail -1
+for r in 1 2 3; do for v in cur t25 t35 t23 t34; do W2L_LIB=abl/$v.so timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/ab_$v.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/ab_$v.json')); s=d['sub']
+print('$v', round(d['ms_per_step'],4), '%.3e'%d['e2e']['value'], 'asg', round(s['asg_only_ms'],4), 'ctc', round(s['ctc_only_ms'],4))"; done; done
