@@ -108,6 +108,61 @@ struct BandRows {
   }
 };
 
+// PREFETCH.  A warp's frames go through a pipeline two frames deep: while
+// it works on frame t, the first round (32 lane blocks) of the windows of
+// frames t + 1 and t + 2 is on its way into a per-warp shared-memory ring
+// (cp.async; no registers held).  The window of frame t + 2 is frame t's
+// band widened by two steps, which contains frame t + 1's band widened by
+// one.  Each lane copies and later reads only its own block, so the
+// per-thread cp.async groups need no warp barrier: group g holds frame g's
+// copies (one group committed per frame, empty ones included), and
+// wait_group 1 at frame t leaves only frame t + 1's group in flight.
+constexpr int kPfSlots = 3;
+template <class V>
+__host__ __device__ constexpr size_t band_pf_bytes() {   // per warp
+  return (size_t)kPfSlots * 32 * (2 * kSpl * sizeof(V) + 2 * sizeof(int));
+}
+template <class V>
+struct BandPf {
+  V *a, *b;      // [kPfSlots][32][kSpl]
+  int *ea, *eb;  // [kPfSlots][32]
+  __device__ __forceinline__ void init(unsigned char *base) {
+    a = reinterpret_cast<V *>(base);
+    b = a + kPfSlots * 32 * kSpl;
+    ea = reinterpret_cast<int *>(b + kPfSlots * 32 * kSpl);
+    eb = ea + kPfSlots * 32;
+  }
+  // block m of frame f into this lane's entry of slot s (nothing outside
+  // the window or the lattice)
+  __device__ __forceinline__ void issue(const BandRows<V> &br,
+                                        const typename BandRows<V>::Frame &f, int m, bool want,
+                                        int s, int lane) const {
+    if (want && m < br.nblk) {
+      const uint32_t vo = br.voff(m), eo = br.eoff(m);
+      const int i = s * 32 + lane;
+      constexpr int kV = 16 / (int)sizeof(V);   // values per 16-byte copy
+#pragma unroll
+      for (int k = 0; k < kSpl; k += kV) {
+        cp_async16_ca(a + i * kSpl + k, f.a + vo + k);
+        cp_async16_ca(b + i * kSpl + k, f.b + vo + k);
+      }
+      cp_async4(ea + i, f.ea + eo);
+      cp_async4(eb + i, f.eb + eo);
+    }
+  }
+  // this lane's block of slot s (e = INT_MIN: none)
+  __device__ __forceinline__ void take(int s, int lane, bool want, V (&va)[kSpl], V (&vb)[kSpl],
+                                       int &e) const {
+    e = INT_MIN;
+    if (want) {
+      const int i = s * 32 + lane;
+      ldv(a + i * kSpl, va);
+      ldv(b + i * kSpl, vb);
+      e = ea[i] + eb[i];
+    }
+  }
+};
+
 // Scaled posteriors of one lane block into q (float); a block above the band
 // threshold widens the band [lo, hi] (lane blocks).
 template <class V>

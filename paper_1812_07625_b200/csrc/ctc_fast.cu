@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
   __shared__ unsigned stok[LP / 4];                        // label tokens per lane block (band.cuh)
   __shared__ unsigned bins[kGradWarps][32];               // per-warp token sums (fixed point)
   __shared__ double gw[kGradWarps][2];
+  extern __shared__ __align__(16) unsigned char gsm[];   // [kGradWarps] prefetch rings
   pdl_launch_dependents();
   if (!prog) pdl_wait();   // not streamed: the chain grid must have completed
   const int b = blockIdx.x, blk = block_of_rank(blockIdx.y, w.nblk);
@@ -205,23 +206,16 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
   for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
   if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
   float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
-  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window (first: all)
-  V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
-  int pe[kBandRounds];
-  auto prefetch = [&](int t) {   // the window's first kBandRounds rounds of frame t
-    const typename BandRows<V>::Frame f = br.frame(t);
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-      pe[r] = INT_MIN;
-      if (mlo + 32 * r <= mhi)   // warp-uniform: skip empty rounds
-        br.load(f, mlo + lane + 32 * r, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
-    }
-  };
-  if (ta < tend) prefetch(ta);
+  BandPf<V> pf;   // the two-frame prefetch ring (band.cuh)
+  pf.init(gsm + warp * band_pf_bytes<V>());
+  int clo = 0, chi = br.nblk - 1;   // lane-block window of frame t (the first: all)
+  int nlo = 0, nhi = -1;            // ... of frame t + 1
+  int slot = 0;                     // ring slot of frame t
   for (int t = ta; t < tend; ++t) {
+    const bool pfd = t > ta;   // the window's first round was prefetched
     float zl = 0.f, zb = 0.f;
     int lo = INT_MAX, hi = -1;
-    float qr[kBandRounds][kSpl];
+    float q0[kSpl];
     auto take = [&](const V (&va)[kSpl], const V (&vb)[kSpl], int e, int m, float (&q)[kSpl],
                     bool keep) {
 #pragma unroll
@@ -235,16 +229,18 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
         zb += q[k];   // blank states are the even ones
       }
     };
-    const int cmlo = mlo, cmhi = mhi;
 #pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-#pragma unroll
-      for (int k = 0; k < kSpl; ++k) qr[r][k] = 0.f;
-      if (cmlo + 32 * r <= cmhi) take(pa[r], pb[r], pe[r], cmlo + lane + 32 * r, qr[r], false);
+    for (int k = 0; k < kSpl; ++k) q0[k] = 0.f;
+    if (pfd) {
+      cp_async_wait<1>();
+      V va[kSpl], vb[kSpl];
+      int e;
+      pf.take(slot, lane, clo + lane <= chi && clo + lane < br.nblk, va, vb, e);
+      take(va, vb, e, clo + lane, q0, false);
     }
-    if (cmlo + 32 * kBandRounds <= cmhi) {   // wide windows (first frame, flat posteriors)
+    {   // the rest of the window directly (the first frame, windows wider than a round)
       const typename BandRows<V>::Frame f = br.frame(t);
-      for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+      for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
         V va[kSpl], vb[kSpl];
         float q[kSpl];
         int e;
@@ -252,9 +248,21 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
         take(va, vb, e, m, q, true);
       }
     }
-    // the next frame's window (CTC mass moves by up to 2 states per frame)
-    br.next_window(lo, hi, 2, mlo, mhi);
-    if (t + 1 < tend) prefetch(t + 1);
+    // the window of frame t + 2 (CTC mass moves by up to 2 states per frame)
+    // and, after the first frame, of frame t + 1
+    int lo2, hi2;
+    br.next_window(lo, hi, 4, lo2, hi2);
+    if (!pfd) {
+      br.next_window(lo, hi, 2, nlo, nhi);
+      if (t + 1 < tend)
+        pf.issue(br, br.frame(t + 1), nlo + lane, nlo + lane <= nhi, slot == 2 ? 0 : slot + 1,
+                 lane);
+      cp_async_commit();
+    }
+    if (t + 2 < tend)
+      pf.issue(br, br.frame(t + 2), lo2 + lane, lo2 + lane <= hi2, slot == 0 ? 2 : slot - 1,
+               lane);
+    cp_async_commit();
     const float z = warp_sum(zl);
     const float zblank = warp_sum(zb);
     const float inv = 1.f / z;
@@ -262,13 +270,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
     l2min = fminf(l2min, l2);
     l2max = fmaxf(l2max, l2);
     // label posteriors into the token bins
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-      const int m = cmlo + lane + 32 * r;
-      if (cmlo + 32 * r <= cmhi && m <= cmhi && m < br.nblk)
-        band_scatter(qr[r], inv, stok + m * kTokWords, mybins);
-    }
-    for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+    if (pfd && clo + lane <= chi && clo + lane < br.nblk)
+      band_scatter(q0, inv, stok + (clo + lane) * kTokWords, mybins);
+    for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);
@@ -287,7 +291,13 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
     mybins[lane] = 0u;
     if (lane < N) ge[(size_t)t * N + lane] = sm_k - c;   // criterion.py:159-161
     __syncwarp();
+    clo = nlo;
+    chi = nhi;
+    nlo = lo2;
+    nhi = hi2;
+    slot = slot == 2 ? 0 : slot + 1;
   }
+  cp_async_wait<0>();
   // the frames' log2-normalisers (ref + log2 z_t) for the guard
   const double gmin = (double)ref + (double)l2min, gmax = (double)ref + (double)l2max;
   if (lane == 0) {
@@ -309,8 +319,11 @@ cudaError_t launch_ctc_grad_w(const float *em, const int32_t *em_len, const int6
                               const int32_t *tgt_len, int blank, Dims d, const CtcFastWs &w,
                               float *grad_em, const int32_t *status, int want, cudaStream_t s,
                               bool stream) {
-  return launch_maybe_pdl(ctc_grad_kernel<W, V>, dim3(d.B, w.nblk), dim3(kGradWarps * 32), 0, s,
-                          true, em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want,
+  const size_t smem = kGradWarps * band_pf_bytes<V>();
+  auto k = ctc_grad_kernel<W, V>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  return launch_maybe_pdl(k, dim3(d.B, w.nblk), dim3(kGradWarps * 32), smem, s, true, em, em_len, tgt, tgt_len, blank, d, w, grad_em, status, want,
                           (const int *)(stream ? w.prog : nullptr));
 }
 
