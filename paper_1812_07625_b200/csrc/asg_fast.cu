@@ -630,20 +630,13 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
   if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
   float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
-  int mlo = 0, mhi = br.nblk - 1;   // lane blocks of this frame's window (first: all)
-  V pa[kBandRounds][kSpl], pb[kBandRounds][kSpl];
-  int pe[kBandRounds];
-  auto prefetch = [&](int t) {   // the window's first kBandRounds rounds of frame t
-    const typename BandRows<V>::Frame f = br.frame(t);
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-      pe[r] = INT_MIN;
-      if (mlo + 32 * r <= mhi)   // warp-uniform: skip empty rounds
-        br.load(f, mlo + lane + 32 * r, mlo + lane + 32 * r <= mhi, pa[r], pb[r], pe[r]);
-    }
-  };
-  if (ta < tend) prefetch(ta);
+  BandPf<V> pf;   // the two-frame prefetch ring (band.cuh)
+  pf.init(smem + align_up(fac_grad_smem<W>(), 16) + warp * band_pf_bytes<V>());
+  int clo = 0, chi = br.nblk - 1;   // lane-block window of frame t (the first: all)
+  int nlo = 0, nhi = -1;            // ... of frame t + 1
+  int slot = 0;                     // ring slot of frame t
   for (int t = ta; t < tend; ++t) {
+    const bool pfd = t > ta;   // the window's first round was prefetched
     const float gam = (float)(ca_nx * cb_nx);   // fcc node posterior, unnormalised
     if (t + 1 < tend) {
       ca_nx = __ldcg(fca + (size_t)(t + 1) * 32);
@@ -652,7 +645,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     // fac node posteriors (:214-217)
     float zl = 0.f;
     int lo = INT_MAX, hi = -1;
-    float qr[kBandRounds][kSpl];
+    float q0[kSpl];
     auto take = [&](const V (&va)[kSpl], const V (&vb)[kSpl], int e, int m, float (&q)[kSpl],
                     bool keep) {
 #pragma unroll
@@ -663,16 +656,18 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 #pragma unroll
       for (int k = 0; k < kSpl; ++k) zl += q[k];
     };
-    const int cmlo = mlo, cmhi = mhi;
 #pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-#pragma unroll
-      for (int k = 0; k < kSpl; ++k) qr[r][k] = 0.f;
-      if (cmlo + 32 * r <= cmhi) take(pa[r], pb[r], pe[r], cmlo + lane + 32 * r, qr[r], false);
+    for (int k = 0; k < kSpl; ++k) q0[k] = 0.f;
+    if (pfd) {
+      cp_async_wait<1>();
+      V va[kSpl], vb[kSpl];
+      int e;
+      pf.take(slot, lane, clo + lane <= chi && clo + lane < br.nblk, va, vb, e);
+      take(va, vb, e, clo + lane, q0, false);
     }
-    if (cmlo + 32 * kBandRounds <= cmhi) {   // wide windows (first frame, flat posteriors)
+    {   // the rest of the window directly (the first frame, windows wider than a round)
       const typename BandRows<V>::Frame f = br.frame(t);
-      for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+      for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
         V va[kSpl], vb[kSpl];
         float q[kSpl];
         int e;
@@ -680,9 +675,21 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
         take(va, vb, e, m, q, true);
       }
     }
-    // the next frame's window (fac mass moves by 0 or 1 state per frame)
-    br.next_window(lo, hi, 1, mlo, mhi);
-    if (t + 1 < tend) prefetch(t + 1);
+    // the window of frame t + 2 (fac mass moves by 0 or 1 state per frame)
+    // and, after the first frame, of frame t + 1
+    int lo2, hi2;
+    br.next_window(lo, hi, 2, lo2, hi2);
+    if (!pfd) {
+      br.next_window(lo, hi, 1, nlo, nhi);
+      if (t + 1 < tend)
+        pf.issue(br, br.frame(t + 1), nlo + lane, nlo + lane <= nhi, slot == 2 ? 0 : slot + 1,
+                 lane);
+      cp_async_commit();
+    }
+    if (t + 2 < tend)
+      pf.issue(br, br.frame(t + 2), lo2 + lane, lo2 + lane <= hi2, slot == 0 ? 2 : slot - 1,
+               lane);
+    cp_async_commit();
     const float zc = warp_sum(zl);
     const float izc = 1.f / zc;
     const float izf = 1.f / warp_sum(gam);
@@ -699,12 +706,8 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
       for (int k = 0; k < kSpl; ++k) o[k] = fmaf(q[k], izc, o[k]);
       stv(myo + m * kSpl, o);
     };
-#pragma unroll
-    for (int r = 0; r < kBandRounds; ++r) {
-      const int m = cmlo + lane + 32 * r;
-      if (cmlo + 32 * r <= cmhi && m <= cmhi && m < br.nblk) settle(qr[r], m);
-    }
-    for (int m = cmlo + lane + 32 * kBandRounds; m <= cmhi; m += 32) {
+    if (pfd && clo + lane <= chi && clo + lane < br.nblk) settle(q0, clo + lane);
+    for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);
@@ -716,7 +719,13 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
     mybins[lane] = 0u;
     if (lane < N) ge[(size_t)t * N + lane] = gam * izf - con;
     __syncwarp();
+    clo = nlo;
+    chi = nhi;
+    nlo = lo2;
+    nhi = hi2;
+    slot = slot == 2 ? 0 : slot + 1;
   }
+  cp_async_wait<0>();
   // the frames' log2-normalisers (ref + log2 z_t) for the guard
   const double gmin = (double)ref + (double)l2min, gmax = (double)ref + (double)l2max;
 
@@ -900,7 +909,8 @@ cudaError_t launch_grad_w(const float *em, const int32_t *em_len, const int64_t 
                           const int32_t *tgt_len, const float *trans, Dims d, const AsgFastWs &w,
                           float *grad_em, const int32_t *status, int want, cudaStream_t s,
                           bool stream) {
-  const size_t smem = std::max(fac_grad_smem<W>(), kGradWarps * fcc_stage_bytes<V>());
+  const size_t smem = std::max(align_up(fac_grad_smem<W>(), 16) + kGradWarps * band_pf_bytes<V>(),
+                               kGradWarps * fcc_stage_bytes<V>());
   auto k = asg_grad_kernel<W, V>;
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
