@@ -538,9 +538,9 @@ __device__ __forceinline__ float lds_f32(unsigned a) {
 template <int W>
 constexpr size_t fac_grad_smem() {
   // per warp: posterior row + occupancy row (floats), guard (2 doubles),
-  // token bins; the CTA's lane-block tokens
+  // token bins, a band word; the CTA's lane-block tokens, 2 band words
   return sizeof(float) * (kGradWarps * (2 * (size_t)W * kLatStates + 4 + 32 + 1) +
-                          (size_t)W * kLatStates / 4);
+                          (size_t)W * kLatStates / 4 + 2);
 }
 
 // The whole gradient row: fcc node posteriors (full part, :238) minus the
@@ -562,6 +562,7 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
                                                   int st, int want, int b, int blk,
                                                   unsigned char *smem) {
   constexpr int LP = W * kLatStates;
+  static_assert(W <= kGradWarps, "cta_first_band: one lane block per thread");
   float *prow = reinterpret_cast<float *>(smem);       // [kGradWarps][LP] wide-window posteriors
   float *occ = prow + kGradWarps * LP;                 // [kGradWarps][LP] occupancy
   double *gwarp = reinterpret_cast<double *>(occ + kGradWarps * LP);   // [kGradWarps][2]
@@ -618,25 +619,25 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
   br.sege = (uint32_t)d.Tmax * 32;
   br.S = L;
   br.nblk = (L + kSpl - 1) / kSpl;
-  // the CTA's reference exponent (frame t0, every warp a share of the blocks)
-  int *sref = reinterpret_cast<int *>(stok + LP / 4);   // [kGradWarps]
-  {
-    const int part = br.magnitude_part(t0, warp, kGradWarps, lane);
-    if (lane == 0) sref[warp] = part;
-  }
-  __syncthreads();
-  int ref = INT_MIN;
-#pragma unroll
-  for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
-  if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
+  // the CTA's reference exponent and the band of its first frame t0
+  int *sband = reinterpret_cast<int *>(stok + LP / 4);   // [kGradWarps + 2]
+  int ref, blo, bhi;
+  br.cta_first_band(t0, kGradWarps, sband, ref, blo, bhi);
   float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
-  BandPf<V> pf;   // the two-frame prefetch ring (band.cuh)
+  // the two-frame prefetch ring (band.cuh): this warp's first two frames from
+  // the CTA's band, widened by the frames in between (fac mass moves by at
+  // most one state per frame)
+  BandPf<V> pf;
   pf.init(smem + align_up(fac_grad_smem<W>(), 16) + warp * band_pf_bytes<V>());
-  int clo = 0, chi = br.nblk - 1;   // lane-block window of frame t (the first: all)
-  int nlo = 0, nhi = -1;            // ... of frame t + 1
-  int slot = 0;                     // ring slot of frame t
+  int clo, chi, nlo, nhi;   // lane-block windows of frames t and t + 1
+  br.window(blo, bhi, ta - t0, clo, chi);
+  br.window(blo, bhi, ta + 1 - t0, nlo, nhi);
+  if (ta < tend) pf.issue(br, br.frame(ta), clo + lane, clo + lane <= chi, 0, lane);
+  cp_async_commit();
+  if (ta + 1 < tend) pf.issue(br, br.frame(ta + 1), nlo + lane, nlo + lane <= nhi, 1, lane);
+  cp_async_commit();
+  int slot = 0;   // ring slot of frame t
   for (int t = ta; t < tend; ++t) {
-    const bool pfd = t > ta;   // the window's first round was prefetched
     const float gam = (float)(ca_nx * cb_nx);   // fcc node posterior, unnormalised
     if (t + 1 < tend) {
       ca_nx = __ldcg(fca + (size_t)(t + 1) * 32);
@@ -656,18 +657,16 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
 #pragma unroll
       for (int k = 0; k < kSpl; ++k) zl += q[k];
     };
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) q0[k] = 0.f;
-    if (pfd) {
+    {   // the window's first round from the ring
       cp_async_wait<1>();
       V va[kSpl], vb[kSpl];
       int e;
       pf.take(slot, lane, clo + lane <= chi && clo + lane < br.nblk, va, vb, e);
       take(va, vb, e, clo + lane, q0, false);
     }
-    {   // the rest of the window directly (the first frame, windows wider than a round)
+    {   // the rest of a window wider than a round directly
       const typename BandRows<V>::Frame f = br.frame(t);
-      for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
+      for (int m = clo + lane + 32; m <= chi; m += 32) {
         V va[kSpl], vb[kSpl];
         float q[kSpl];
         int e;
@@ -675,17 +674,9 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
         take(va, vb, e, m, q, true);
       }
     }
-    // the window of frame t + 2 (fac mass moves by 0 or 1 state per frame)
-    // and, after the first frame, of frame t + 1
+    // the window of frame t + 2: this frame's band widened by two frames
     int lo2, hi2;
     br.next_window(lo, hi, 2, lo2, hi2);
-    if (!pfd) {
-      br.next_window(lo, hi, 1, nlo, nhi);
-      if (t + 1 < tend)
-        pf.issue(br, br.frame(t + 1), nlo + lane, nlo + lane <= nhi, slot == 2 ? 0 : slot + 1,
-                 lane);
-      cp_async_commit();
-    }
     if (t + 2 < tend)
       pf.issue(br, br.frame(t + 2), lo2 + lane, lo2 + lane <= hi2, slot == 0 ? 2 : slot - 1,
                lane);
@@ -706,8 +697,8 @@ __device__ __forceinline__ void asg_fac_grad_body(const int32_t *__restrict__ em
       for (int k = 0; k < kSpl; ++k) o[k] = fmaf(q[k], izc, o[k]);
       stv(myo + m * kSpl, o);
     };
-    if (pfd && clo + lane <= chi && clo + lane < br.nblk) settle(q0, clo + lane);
-    for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
+    if (clo + lane <= chi && clo + lane < br.nblk) settle(q0, clo + lane);
+    for (int m = clo + lane + 32; m <= chi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);

@@ -9,27 +9,31 @@
 // BAND.  Posterior mass only moves forward along a left-to-right lattice: a
 // path in state s at frame t is in s .. s + kMaxStep at t + 1 (CTC: 2, fac:
 // 1).  So if [lo_t, hi_t] holds every state of frame t whose scaled posterior
-// exceeds kBandEps, the states carrying mass at t + 1 lie in
-// [lo_t, hi_t + kMaxStep]: a warp that walks consecutive frames reads its
-// first frame whole and afterwards only that window -- about 100 of the
-// 601 CTC states at the bench shape.  The mass outside the window stays
-// below S kBandEps per frame (~1e-11 of the frame's mass), far inside the
-// 1e-4 tolerance.
+// exceeds kBandEps, the states carrying mass at t + k lie in
+// [lo_t, hi_t + k kMaxStep], up to the mass outside [lo_t, hi_t] at t, which
+// stays below S kBandEps (~1e-11 of a frame's mass; the window's own mass
+// flows within the widened window), far inside the 1e-4 tolerance.  About
+// 100 of the 601 CTC states at the bench shape are read per frame.
+//
+// FIRST FRAMES.  The CTA reads its first frame t0 whole, one lane block per
+// thread: the largest block magnitude gives the reference exponent and the
+// blocks above kBandEps the band of t0.  The window of a warp's first frame
+// ta is that band widened by ta - t0 frames of movement.
 //
 // LANES.  Each frame, lane l takes the window's lane blocks mlo + l + 32 r
-// (rounds r = 0, 1, ...): two rounds cover 64 blocks (256 states), and those
-// two are prefetched one frame ahead in registers; wider windows (a warp's
-// first frame, flat posteriors) load their extra rounds in the frame itself.
+// (rounds r = 0, 1, ...).  Round 0 arrives through the prefetch ring below;
+// wider windows (flat posteriors, a late warp's first frame) load their
+// extra rounds in the frame itself.
 //
 // SCALE.  sum_s alpha_t beta'_t = Z for every frame, so one reference
 // exponent -- the magnitude of the CTA's first frame, from its largest
 // block (block exponent sum plus the exponent of the block's largest
-// product; all-zero blocks ignored), found by the CTA's warps together --
-// scales all the CTA's frames into fp32 range.  (A block's exponent alone
-// does not bound its values: between renormalisations a block may carry a
-// dominant neighbour's mass scaled onto its exponent by up to 2^kLaneGap, so
-// a warp's first frame is read whole.)  Each frame's posteriors are normalised by their own sum z_t,
-// and ref + log2 z_t is the frame's log2-normaliser the guard checks.
+// product; all-zero blocks ignored) -- scales all the CTA's frames into fp32
+// range.  (A block's exponent alone does not bound its values: between
+// renormalisations a block may carry a dominant neighbour's mass scaled onto
+// its exponent by up to 2^kLaneGap, so the first frame is read whole.)  Each
+// frame's posteriors are normalised by their own sum z_t, and ref + log2 z_t
+// is the frame's log2-normaliser the guard checks.
 #pragma once
 
 #include <climits>
@@ -39,7 +43,20 @@
 namespace w2l {
 
 constexpr float kBandEps = 0x1p-44f;   // band threshold (scaled posterior units)
-constexpr int kBandRounds = 2;         // prefetched lane-block rounds (64 blocks)
+
+// Scaled posteriors of one lane block into q (float); a block above the band
+// threshold widens the band [lo, hi] (lane blocks).
+template <class V>
+__device__ __forceinline__ void band_block(const V (&va)[kSpl], const V (&vb)[kSpl], int e,
+                                           int ref, int m, float (&q)[kSpl], int &lo, int &hi) {
+  const V sc = e == INT_MIN ? (V)0 : pow2_clamped<V>(e - ref);
+#pragma unroll
+  for (int k = 0; k < kSpl; ++k) q[k] = (float)(va[k] * vb[k] * sc);
+  if (tree_max<kSpl, float>(q) > kBandEps) {
+    lo = min(lo, m);
+    hi = max(hi, m);
+  }
+}
 
 template <class V>
 struct BandRows {
@@ -75,36 +92,65 @@ struct BandRows {
       e = __ldcg(f.ea + eo) + __ldcg(f.eb + eo);
     }
   }
-  // this warp's share (blocks warp*32 + lane + 32*nwarps*k) of the largest
-  // block magnitude of frame t: block exponent sum plus the exponent of the
-  // block's largest product (all-zero blocks ignored)
-  __device__ __forceinline__ int magnitude_part(int t, int warp, int nwarps, int lane) const {
-    const Frame f = frame(t);
-    int mag = INT_MIN;
-    for (int m = warp * 32 + lane; m < nblk; m += 32 * nwarps) {
-      V va[kSpl], vb[kSpl], pp[kSpl];
-      int e;
-      load(f, m, true, va, vb, e);
-#pragma unroll
-      for (int k = 0; k < kSpl; ++k) pp[k] = va[k] * vb[k];
-      const V pm = tree_max<kSpl, V>(pp);
-      if (pm > (V)0) mag = max(mag, e + Pow2<V>::expo(pm));
-    }
-    return __reduce_max_sync(0xffffffffu, mag);
-  }
-  // next frame's window (lane blocks) from this frame's band (blocks lo..hi
-  // holding a scaled posterior above kBandEps); mass moves by <= step states
-  __device__ __forceinline__ void next_window(int lo, int hi, int step, int &mlo,
-                                              int &mhi) const {
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
+  // the window (lane blocks) of a frame `ext` states of mass movement after
+  // a frame whose band (blocks lo..hi holding a scaled posterior above
+  // kBandEps) is known
+  __device__ __forceinline__ void window(int lo, int hi, int ext, int &mlo, int &mhi) const {
     if (hi >= lo) {
       mlo = lo;
-      mhi = min(hi * kSpl + kSpl - 1 + step, S - 1) / kSpl;
+      mhi = min(hi * kSpl + kSpl - 1 + ext, S - 1) / kSpl;
     } else {   // nothing above the threshold (cannot happen for a finite loss): read all
       mlo = 0;
       mhi = nblk - 1;
     }
+  }
+  // the same from a warp's per-lane band edges
+  __device__ __forceinline__ void next_window(int lo, int hi, int ext, int &mlo,
+                                              int &mhi) const {
+    window(__reduce_min_sync(0xffffffffu, lo), __reduce_max_sync(0xffffffffu, hi), ext, mlo, mhi);
+  }
+  // The CTA's first frame t0, one lane block per thread (nblk <= blockDim.x):
+  // the reference exponent and the band of blocks above kBandEps, from which
+  // every warp's first windows follow (frame t0 + k: the band widened by k
+  // steps of mass movement).  sh: nwarps + 2 ints of shared memory.
+  __device__ __forceinline__ void cta_first_band(int t0, int nwarps, int *sh, int &ref, int &blo,
+                                                 int &bhi) const {
+    const int m = threadIdx.x, lane = m & 31, warp = m >> 5;
+    V va[kSpl], vb[kSpl];
+    int e;
+    load(frame(t0), m, true, va, vb, e);
+    int mag = INT_MIN;
+    if (e != INT_MIN) {
+      V pp[kSpl];
+#pragma unroll
+      for (int k = 0; k < kSpl; ++k) pp[k] = va[k] * vb[k];
+      const V pm = tree_max<kSpl, V>(pp);
+      if (pm > (V)0) mag = e + Pow2<V>::expo(pm);
+    }
+    mag = __reduce_max_sync(0xffffffffu, mag);
+    if (lane == 0) sh[warp] = mag;
+    if (threadIdx.x == 0) {
+      sh[nwarps] = INT_MAX;
+      sh[nwarps + 1] = -1;
+    }
+    __syncthreads();
+    ref = INT_MIN;
+    for (int q = 0; q < nwarps; ++q) ref = max(ref, sh[q]);
+    if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
+    int lo = INT_MAX, hi = -1;
+    if (e != INT_MIN) {
+      float q[kSpl];
+      band_block<V>(va, vb, e, ref, m, q, lo, hi);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0 && hi >= lo) {
+      atomicMin(&sh[nwarps], lo);
+      atomicMax(&sh[nwarps + 1], hi);
+    }
+    __syncthreads();
+    blo = sh[nwarps];
+    bhi = sh[nwarps + 1];
   }
 };
 
@@ -163,19 +209,6 @@ struct BandPf {
   }
 };
 
-// Scaled posteriors of one lane block into q (float); a block above the band
-// threshold widens the band [lo, hi] (lane blocks).
-template <class V>
-__device__ __forceinline__ void band_block(const V (&va)[kSpl], const V (&vb)[kSpl], int e,
-                                           int ref, int m, float (&q)[kSpl], int &lo, int &hi) {
-  const V sc = e == INT_MIN ? (V)0 : pow2_clamped<V>(e - ref);
-#pragma unroll
-  for (int k = 0; k < kSpl; ++k) q[k] = (float)(va[k] * vb[k] * sc);
-  if (tree_max<kSpl, float>(q) > kBandEps) {
-    lo = min(lo, m);
-    hi = max(hi, m);
-  }
-}
 
 // Token sums of a frame's posteriors, deterministic: each state's normalised
 // posterior (in [0, 1]) is added to its token's bin as a 2^-30 fixed-point

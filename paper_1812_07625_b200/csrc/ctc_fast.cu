@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
                     const int32_t *__restrict__ status, int want, const int *prog) {
   constexpr int LP = W * kLatStates;
+  static_assert(W <= kGradWarps, "cta_first_band: one lane block per thread");
   __shared__ __align__(16) float prow[kGradWarps][LP];   // wide-window posteriors
   __shared__ unsigned stok[LP / 4];                        // label tokens per lane block (band.cuh)
   __shared__ unsigned bins[kGradWarps][32];               // per-warp token sums (fixed point)
@@ -194,25 +195,25 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
   br.S = S;
   br.nblk = (S + kSpl - 1) / kSpl;
   unsigned *mybins = bins[warp];
-  // the CTA's reference exponent (frame t0, every warp a share of the blocks)
-  __shared__ int sref[kGradWarps];
-  {
-    const int part = br.magnitude_part(t0, warp, kGradWarps, lane);
-    if (lane == 0) sref[warp] = part;
-  }
-  __syncthreads();
-  int ref = INT_MIN;
-#pragma unroll
-  for (int q = 0; q < kGradWarps; ++q) ref = max(ref, sref[q]);
-  if (ref == INT_MIN) ref = 0;   // no mass: the guard rejects the utterance
+  // the CTA's reference exponent and the band of its first frame t0
+  __shared__ int sband[kGradWarps + 2];
+  int ref, blo, bhi;
+  br.cta_first_band(t0, kGradWarps, sband, ref, blo, bhi);
   float l2min = CUDART_INF_F, l2max = -CUDART_INF_F;   // log2 z_t (the guard adds ref)
-  BandPf<V> pf;   // the two-frame prefetch ring (band.cuh)
+  // the two-frame prefetch ring (band.cuh): this warp's first two frames from
+  // the CTA's band, widened by the frames in between (CTC mass moves by up
+  // to 2 states per frame)
+  BandPf<V> pf;
   pf.init(gsm + warp * band_pf_bytes<V>());
-  int clo = 0, chi = br.nblk - 1;   // lane-block window of frame t (the first: all)
-  int nlo = 0, nhi = -1;            // ... of frame t + 1
-  int slot = 0;                     // ring slot of frame t
+  int clo, chi, nlo, nhi;   // lane-block windows of frames t and t + 1
+  br.window(blo, bhi, 2 * (ta - t0), clo, chi);
+  br.window(blo, bhi, 2 * (ta + 1 - t0), nlo, nhi);
+  if (ta < tend) pf.issue(br, br.frame(ta), clo + lane, clo + lane <= chi, 0, lane);
+  cp_async_commit();
+  if (ta + 1 < tend) pf.issue(br, br.frame(ta + 1), nlo + lane, nlo + lane <= nhi, 1, lane);
+  cp_async_commit();
+  int slot = 0;   // ring slot of frame t
   for (int t = ta; t < tend; ++t) {
-    const bool pfd = t > ta;   // the window's first round was prefetched
     float zl = 0.f, zb = 0.f;
     int lo = INT_MAX, hi = -1;
     float q0[kSpl];
@@ -229,18 +230,16 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
         zb += q[k];   // blank states are the even ones
       }
     };
-#pragma unroll
-    for (int k = 0; k < kSpl; ++k) q0[k] = 0.f;
-    if (pfd) {
+    {   // the window's first round from the ring
       cp_async_wait<1>();
       V va[kSpl], vb[kSpl];
       int e;
       pf.take(slot, lane, clo + lane <= chi && clo + lane < br.nblk, va, vb, e);
       take(va, vb, e, clo + lane, q0, false);
     }
-    {   // the rest of the window directly (the first frame, windows wider than a round)
+    {   // the rest of a window wider than a round directly
       const typename BandRows<V>::Frame f = br.frame(t);
-      for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
+      for (int m = clo + lane + 32; m <= chi; m += 32) {
         V va[kSpl], vb[kSpl];
         float q[kSpl];
         int e;
@@ -248,17 +247,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
         take(va, vb, e, m, q, true);
       }
     }
-    // the window of frame t + 2 (CTC mass moves by up to 2 states per frame)
-    // and, after the first frame, of frame t + 1
+    // the window of frame t + 2: this frame's band widened by two frames
     int lo2, hi2;
     br.next_window(lo, hi, 4, lo2, hi2);
-    if (!pfd) {
-      br.next_window(lo, hi, 2, nlo, nhi);
-      if (t + 1 < tend)
-        pf.issue(br, br.frame(t + 1), nlo + lane, nlo + lane <= nhi, slot == 2 ? 0 : slot + 1,
-                 lane);
-      cp_async_commit();
-    }
     if (t + 2 < tend)
       pf.issue(br, br.frame(t + 2), lo2 + lane, lo2 + lane <= hi2, slot == 0 ? 2 : slot - 1,
                lane);
@@ -270,9 +261,9 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
     l2min = fminf(l2min, l2);
     l2max = fmaxf(l2max, l2);
     // label posteriors into the token bins
-    if (pfd && clo + lane <= chi && clo + lane < br.nblk)
+    if (clo + lane <= chi && clo + lane < br.nblk)
       band_scatter(q0, inv, stok + (clo + lane) * kTokWords, mybins);
-    for (int m = clo + lane + (pfd ? 32 : 0); m <= chi; m += 32) {
+    for (int m = clo + lane + 32; m <= chi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);
