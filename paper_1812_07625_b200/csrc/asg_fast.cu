@@ -43,10 +43,19 @@ namespace {
 constexpr int kGradFramesPerBlock = 128;   // frames per gradient CTA (both bodies)
 constexpr int kFccFrames = kGradFramesPerBlock;
 constexpr int kGradWarps = 8;
-// asg_final: one CTA per utterance; small, so that its CTAs -- launched as
-// programmatic dependents during the gradient grid's last wave -- do not
-// hold SM resources the other criterion's stream needs
-constexpr int kFinalThreads = 256;
+// asg_final: one CTA per utterance (launched as a programmatic dependent
+// during the gradient grid's last wave, it stages its inputs before the
+// gradient completes); 512 threads, each with the partials of up to 4
+// entries in flight (kFinalChunk frame blocks each): ASG alone 0.327 ->
+// 0.321 ms.  16 blocks per entry (111 registers) was no better in the
+// two-criteria step, where the early-launched CTAs hold their registers.
+constexpr int kFinalThreads = 512;
+#ifndef W2L_FINAL_CHUNK
+#define W2L_FINAL_CHUNK 4
+#endif
+constexpr int kFinalChunk = W2L_FINAL_CHUNK;   // frame-block partials in flight per entry
+constexpr int kFinalEnt =   // entries (L occupancies + N^2 edge sums) per thread
+    (W2L_MAX_ASG_LABELS + W2L_MAX_TOKENS * W2L_MAX_TOKENS + kFinalThreads - 1) / kFinalThreads;
 
 __device__ __forceinline__ float trans_max(const float *trans, int N) {
   float m = -CUDART_INF_F;
@@ -751,9 +760,9 @@ __global__ void __launch_bounds__(kFinalThreads)
                      const int32_t *__restrict__ em_len, const float *__restrict__ trans, Dims d,
                      AsgFastWs w, double *loss, float *ga_utt, int32_t *status, int want,
                      int fail) {
-  pdl_enter();
+  pdl_launch_dependents();
   const int b = blockIdx.x;
-  __shared__ float sEdge[kMaxLatWarps * kLatStates];
+  __shared__ float sEdge[W2L_MAX_ASG_LABELS];
   __shared__ float sA[1024];
   __shared__ float s_red[32];
   __shared__ int s_bad;
@@ -761,17 +770,8 @@ __global__ void __launch_bounds__(kFinalThreads)
   __shared__ int sperm[W2L_MAX_ASG_LABELS];   // token CSR
   __shared__ int sts[33];
   const int N = d.N, NN = N * N;
-  if (threadIdx.x < 2 && w.prog) w.prog[2 * b + threadIdx.x] = 0;   // next tier / call
-  const int st = status[b];
-  if (st != want) {
-    // the first tier owns the zeros (NaN loss) of the utterances it does not
-    // compute; a later tier overwrites those it takes
-    if (want == W2L_OK) {
-      for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
-      if (threadIdx.x == 0) loss[b] = CUDART_NAN;
-    }
-    return;
-  }
+  // ---- inputs and the prep kernel's token CSR first (the gradient writes
+  // none of them: they load while the gradient grid finishes)
   const int L = tgt_len[b], T = em_len[b], LP = w.lpad;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -785,27 +785,70 @@ __global__ void __launch_bounds__(kFinalThreads)
     sperm[l] = w.perm[(size_t)b * w.lpad + l];
   }
   if (threadIdx.x <= N) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];   // N+1 written
-  // fixed-order sums of the per-frame-block partials (16 loaded at once --
-  // one memory latency per 16 blocks -- then added in a fixed order)
-  auto sum_parts = [&](const float *base, size_t stride, int nb) {
-    float acc = 0.f;
-    for (int q0 = 0; q0 < nb; q0 += 16) {
-      float v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = q0 + k < nb ? base[(size_t)(q0 + k) * stride] : 0.f;
-#pragma unroll
-      for (int k = 0; k < 16; k += 2) v[k] += v[k + 1];
-#pragma unroll
-      for (int k = 0; k < 16; k += 4) v[k] += v[k + 2];
-      acc += (v[0] + v[4]) + (v[8] + v[12]);
+  pdl_wait();
+  if (threadIdx.x < 2 && w.prog) w.prog[2 * b + threadIdx.x] = 0;   // next tier / call
+  const int st = status[b];
+  if (st != want) {
+    // the first tier owns the zeros (NaN loss) of the utterances it does not
+    // compute; a later tier overwrites those it takes
+    if (want == W2L_OK) {
+      for (int p = threadIdx.x; p < NN; p += blockDim.x) ga_utt[(size_t)b * NN + p] = 0.f;
+      if (threadIdx.x == 0) loss[b] = CUDART_NAN;
     }
-    return acc;
-  };
+    return;
+  }
+  // ---- fixed-order sums of the per-frame-block partials: the fac
+  // occupancies of the L states and the fcc edge sums of the N x N
+  // transitions; each thread owns up to kFinalEnt of these entries and has
+  // every partial of a 16-block chunk in flight at once
   const int nb_used = (T + kGradFramesPerBlock - 1) / kGradFramesPerBlock;
-  for (int i = threadIdx.x; i < LP; i += blockDim.x)
-    sEdge[i] = sum_parts(w.part_edge + (size_t)b * w.nblk * LP + i, LP, nb_used);
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x)
-    sA[i] = sum_parts(w.part_fullA + (size_t)b * w.nblk * 1024 + i, 1024, nb_used);
+  const int nent = L + NN;
+  const float *pe = w.part_edge + (size_t)b * w.nblk * LP;
+  const float *pa = w.part_fullA + (size_t)b * w.nblk * 1024;
+  float acc[kFinalEnt];
+  const float *src[kFinalEnt];
+  size_t stride[kFinalEnt];
+#pragma unroll
+  for (int k = 0; k < kFinalEnt; ++k) {
+    const int e = threadIdx.x + k * kFinalThreads;
+    acc[k] = 0.f;
+    if (e < L) {
+      src[k] = pe + e;
+      stride[k] = LP;
+    } else {
+      const int p = min(e - L, NN - 1);
+      src[k] = pa + (p / N) * 32 + p % N;
+      stride[k] = 1024;
+    }
+  }
+  for (int q0 = 0; q0 < nb_used; q0 += kFinalChunk) {
+    float v[kFinalEnt][kFinalChunk];
+#pragma unroll
+    for (int k = 0; k < kFinalEnt; ++k) {
+      const bool on = threadIdx.x + k * kFinalThreads < nent;
+#pragma unroll
+      for (int q = 0; q < kFinalChunk; ++q)
+        v[k][q] = on && q0 + q < nb_used ? src[k][(size_t)(q0 + q) * stride[k]] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kFinalEnt; ++k) {   // fixed pairwise order
+#pragma unroll
+      for (int h = 1; h < kFinalChunk; h *= 2)
+#pragma unroll
+        for (int q = 0; q < kFinalChunk; q += 2 * h) v[k][q] += v[k][q + h];
+      acc[k] += v[k][0];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFinalEnt; ++k) {
+    const int e = threadIdx.x + k * kFinalThreads;
+    if (e < L) {
+      sEdge[e] = acc[k];
+    } else if (e < nent) {
+      const int p = e - L;
+      sA[(p / N) * 32 + p % N] = acc[k];
+    }
+  }
   __syncthreads();
   float amax = s_red[0];
   for (int q = 1; q < (int)(blockDim.x >> 5); ++q) amax = fmaxf(amax, s_red[q]);
