@@ -205,12 +205,11 @@ struct FccCtx {
   int N, T, lane, cons_idx;
   V *rows;      // [Tmax][32] this utterance
   int *ks;      // cumulative exponents, indexed by frame
-  bool stream = false;   // streamed gradient: trigger the dependent launch mid-utterance
 };
 
 // fcc recursion over the shared Et ring (criterion.py:227-236); the same
 // step schedule as the lattice warps (lattice.cuh)
-template <bool FWD, class V>
+template <bool FWD, class V, bool STREAM>
 __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
   constexpr int kRing = Ring<V>::n;
   const int lane = c.lane, N = c.N, T = c.T;
@@ -252,11 +251,11 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
   const int pro_end = min(T, kBlk);
   for (int j = 1; j < pro_end; ++j) generic(j);
   const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
-  const int mtrig = c.stream ? stream_trigger_block(T) : -1;   // (see lattice_run)
+  const int mtrig = STREAM ? stream_trigger_block(T) : -1;   // (see lattice_run)
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
-    if (m == mtrig) pdl_launch_dependents();
+    if (STREAM && m == mtrig) pdl_launch_dependents();
     wait3(&sm.prod, eidx_of(FWD, j0 + kBlk - 1) + 1, &sm.prod, 0, &sm.prod, 0);
     const V *eb = sm.ering[j0 & (kRing - 1)];
     const int tb = frame_of(FWD, T, j0);
@@ -284,7 +283,7 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
     publish(mycons, j0 + kBlk, lane);
   }
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
-  if (c.stream && mtrig > nfull) pdl_launch_dependents();
+  if (STREAM && mtrig > nfull) pdl_launch_dependents();
   publish(mycons, kDone, lane);
   V z;
   if (FWD) {
@@ -297,7 +296,7 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
   if (lane == 0) *lnz = log((double)z) + (double)f.K * 0.6931471805599453;
 }
 
-template <bool FWD, class V>
+template <bool FWD, class V, bool STREAM>
 __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, int T, int L,
                                                const int64_t *y, const float *trans, Dims d,
                                                const AsgFastWs &w, int b, int32_t *status,
@@ -321,8 +320,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     fc.cons_idx = 0;
     fc.rows = reinterpret_cast<V *>(FWD ? w.fcc_a : w.fcc_b) + (size_t)b * d.Tmax * 32;
     fc.ks = FWD ? w.fcc_ka + (size_t)b * w.tpad : w.fcc_kb + (size_t)b * w.tpad + 1;
-    fc.stream = w.prog != nullptr;
-    fcc_run<FWD, V>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
+    fcc_run<FWD, V, STREAM>(sm, fc, w.scal + b * 4 + (FWD ? 0 : 1));
   } else if (warp - 2 < weff) {
     LatCtx c;
     c.w = warp - 2;
@@ -336,11 +334,10 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     const size_t ub = (size_t)b * w.W * d.Tmax;
     c.rows = reinterpret_cast<V *>(FWD ? w.fac_a : w.fac_b) + ub * kLatStates;
     c.exps = (FWD ? w.fac_ea : w.fac_eb) + ub * 32;
-    c.stream = w.prog != nullptr;
     LatState<V> f;
     lat_init_weights<kFac, FWD, V>(f, c.w, lane, d.N, L, y, L, trans, amax, 0);
-    lattice_run<kFac, FWD, V>(sm, c, f);
-  } else if (w.prog) {   // a warp without a role: its share of the trigger, at
+    lattice_run<kFac, FWD, V, STREAM>(sm, c, f);
+  } else if (STREAM) {   // a warp without a role: its share of the trigger, at
     wait_ge(&sm.cons[1], stream_trigger_step(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
@@ -352,8 +349,9 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
   }
 }
 
-// grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
-template <class V>
+// grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta);
+// STREAM: publish progress and trigger the streamed gradient (w.prog set)
+template <class V, bool STREAM>
 __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
     asg_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
@@ -388,9 +386,9 @@ __global__ void __launch_bounds__(32 * (2 + kMaxLatWarps))
   __syncthreads();
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   if (blockIdx.y == 0)
-    asg_chain_body<true, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
+    asg_chain_body<true, V, STREAM>(sm, em, T, L, y, trans, d, w, b, status, fail);
   else
-    asg_chain_body<false, V>(sm, em, T, L, y, trans, d, w, b, status, fail);
+    asg_chain_body<false, V, STREAM>(sm, em, T, L, y, trans, d, w, b, status, fail);
   W2L_TL(if (threadIdx.x == 0) tl_rec(3000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid() | (hw_warpid() << 16)));
 }
 
@@ -969,7 +967,9 @@ cudaError_t launch_asg_tier(const float *em, const int32_t *em_len, const int64_
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
     const size_t smem = chain_smem_bytes<V>();
-    auto k = asg_chain_kernel<V>;
+    // (the streamed-gradient trigger is compiled only into the streaming
+    // variant: its checks cost the recursion loops ~2.5%)
+    auto k = wc.prog ? asg_chain_kernel<V, true> : asg_chain_kernel<V, false>;
     err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     // maximum shared-memory carveout: chain CTAs of different criteria (and

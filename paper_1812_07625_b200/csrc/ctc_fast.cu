@@ -27,7 +27,7 @@
 namespace w2l {
 namespace {
 
-template <bool FWD, class V>
+template <bool FWD, class V, bool STREAM>
 __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, int T, int L,
                                                const int64_t *y, int blank, Dims d,
                                                const CtcFastWs &w, int b, unsigned tokmask,
@@ -52,11 +52,10 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
     const size_t ub = (size_t)b * w.W * d.Tmax;
     c.rows = reinterpret_cast<V *>(FWD ? w.a : w.b) + ub * kLatStates;
     c.exps = (FWD ? w.ea : w.eb) + ub * 32;
-    c.stream = w.prog != nullptr;
     LatState<V> f;
     lat_init_weights<kCtc, FWD, V>(f, c.w, lane, d.N, S, y, L, nullptr, 0.f, blank);
-    lattice_run<kCtc, FWD, V>(sm, c, f);
-  } else if (w.prog) {   // a warp without a role: its share of the trigger, at
+    lattice_run<kCtc, FWD, V, STREAM>(sm, c, f);
+  } else if (STREAM) {   // a warp without a role: its share of the trigger, at
     wait_ge(&sm.cons[0], stream_trigger_step(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
@@ -68,8 +67,9 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
   }
 }
 
-// grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta)
-template <class V>
+// grid (B, 2): blockIdx.y 0 = forward (alpha), 1 = backward (beta);
+// STREAM: publish progress and trigger the streamed gradient (w.prog set)
+template <class V, bool STREAM>
 __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
     ctc_chain_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                      const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
@@ -107,9 +107,9 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
   for (int l = threadIdx.x; l < L; l += blockDim.x) atomicOr(&s_mask, 1u << (int)y[l]);
   __syncthreads();
   if (blockIdx.y == 0)
-    ctc_chain_body<true, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
+    ctc_chain_body<true, V, STREAM>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   else
-    ctc_chain_body<false, V>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
+    ctc_chain_body<false, V, STREAM>(sm, em, T, L, y, blank, d, w, b, s_mask, status, fail);
   W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid() | (hw_warpid() << 16)));
 }
 
@@ -384,7 +384,9 @@ cudaError_t launch_ctc_tier(const float *em, const int32_t *em_len, const int64_
   cudaError_t err = cudaSuccess;
   if (phases & 5u) {
     const size_t smem = chain_smem_bytes<V>();
-    auto k = ctc_chain_kernel<V>;
+    // (the streamed-gradient trigger is compiled only into the streaming
+    // variant: its checks cost the recursion loops ~2.5%)
+    auto k = wc.prog ? ctc_chain_kernel<V, true> : ctc_chain_kernel<V, false>;
     err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     // maximum shared-memory carveout: chain CTAs of different criteria (and

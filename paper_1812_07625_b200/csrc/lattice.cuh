@@ -367,7 +367,6 @@ struct LatCtx {
   void *rows;        // rows of this utterance: V [W][Tmax][128]
   int *exps;         //                         int [W][Tmax][32]
   int Tmax;
-  bool stream = false;   // streamed gradient (W2L_FLAG_STREAM_GRAD)
 };
 
 template <class V>
@@ -552,7 +551,7 @@ __device__ __forceinline__ void lat_store_row(const LatState<V> &f, V *row, int 
 // Run a lattice warp over the whole utterance; its share of the recursion's
 // total goes to sm.fin[w] (log domain) for the CTA epilogue.  Every step's
 // lane values and exponents are stored (padding lanes excepted).
-template <int KIND, bool FWD, class V>
+template <int KIND, bool FWD, class V, bool STREAM>
 __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
   constexpr int kRing = Ring<V>::n;
   const int T = c.T, lane = c.lane;
@@ -628,7 +627,7 @@ __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
   // warp of every chain CTA has passed the middle of its utterance, when
   // the first frames have both their rows -- its CTAs then do not hold SMs
   // while there is nothing to do (another criterion's kernels need them).
-  const int mtrig = c.stream ? stream_trigger_block(T) : -1;
+  const int mtrig = STREAM ? stream_trigger_block(T) : -1;
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
@@ -667,11 +666,11 @@ __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
     else
       run_block(std::false_type{});
     publish(mycons, j0 + kBlk, lane);
-    if (m == mtrig) pdl_launch_dependents();
+    if (STREAM && m == mtrig) pdl_launch_dependents();
   }
   // ---- tail steps
   for (int j = max(pro_end, (nfull + 1) * kBlk); j < T; ++j) generic(j);
-  if (c.stream && mtrig > nfull) pdl_launch_dependents();
+  if (STREAM && mtrig > nfull) pdl_launch_dependents();
   publish(mycons, kDone, lane);
 
   // ---- totals (criterion.py:136-141 CTC, :203 fac forward; backward: the
