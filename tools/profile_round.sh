@@ -8,5 +8,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sub > gpurun_out/launches.csv 2> gpurun_out/launches.err
 timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-  -k regex:"(chain|grad)_kernel<.*float>" -s 4 -c 4 -o gpurun_out/full python tools/prof_chain.py all > gpurun_out/full.log 2>&1
+  -k regex:"(chain_kernel<float|grad_kernel<[^>]*, float)" -s 4 -c 4 -o gpurun_out/full python tools/prof_chain.py all > gpurun_out/full.log 2>&1
 tail -2 gpurun_out/full.log

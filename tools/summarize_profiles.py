@@ -63,7 +63,7 @@ keymap = {"asg_chain_kernel": "asg_chain", "ctc_chain_kernel": "ctc_chain",
           "asg_fcc_grad_kernel": "asg_grad_fcc"}
 traffic = {}
 out = ["# ncu --set full --clock-control none --import-source on --kernel-name-base demangled "
-       "-k regex:'(chain|grad)_kernel<.*float>' -s 4 -c 4 "
+       "-k regex:'(chain_kernel<float|grad_kernel<[^>]*, float)' -s 4 -c 4 "
        "(tools/prof_chain.py all; bench shape B=64 T=1600 N=30 L=300; the fp32 tier)",
        f"{'kernel':30s}{'dur_us':>9s}{'dram_rd_MB':>11s}{'dram_wr_MB':>11s}{'occ%':>7s}"
        f"{'inst/frame':>11s}{'IPC':>6s}{'regs':>6s}"]

@@ -178,7 +178,8 @@ for k, name in [(2, "ctc_grad"), (4, "asg_grad")]:
         body = (tag[m] % 1000000) // 500000
         for bb, nm in [(0, "fac"), (1, "fcc")]:
             mm = body == bb
-            print(f"{'':10s} {nm}: n={mm.sum()} busy {busy[mm].mean():6.1f} us mean, end max {e[mm].max():7.1f}")
+            print(f"{'':10s} {nm}: n={mm.sum()} busy {busy[mm].mean():6.1f} us mean, dispatch med "
+                  f"{np.median(s[mm]):7.1f}, end med {np.median(e[mm]):7.1f} max {e[mm].max():7.1f}")
     # CTAs of this launch running at once (sampled every 2 us)
     grid_t = np.arange(w.min(), e.max(), 2.0)
     conc = [int(((w <= x) & (e > x)).sum()) for x in grid_t]
