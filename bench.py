@@ -48,6 +48,7 @@ STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
 FIRST = os.environ.get("W2L_BENCH_FIRST", "asg")
 STREAM_ASG = os.environ.get("W2L_BENCH_STREAM_ASG", "1") != "0"
 STREAM_CTC = os.environ.get("W2L_BENCH_STREAM_CTC", "0") == "1"
+SIDE_PRIO = int(os.environ.get("W2L_BENCH_SIDE_PRIO", "0"))   # second stream's priority (A/B)
 
 
 # ---------------------------------------------------------------- inputs --
@@ -356,7 +357,7 @@ def main():
                                     fallback=False)
     fallbacks = int((chk_a.status != 0).sum().item() + (chk_c.status != 0).sum().item())
 
-    side = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev, priority=SIDE_PRIO)
     main_s = torch.cuda.current_stream(dev)
     validated = torch.cuda.Event()   # the first criterion's validation done (staggered start)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
