@@ -48,6 +48,10 @@ STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
 FIRST = os.environ.get("W2L_BENCH_FIRST", "asg")
 STREAM_ASG = os.environ.get("W2L_BENCH_STREAM_ASG", "1") != "0"
 STREAM_CTC = os.environ.get("W2L_BENCH_STREAM_CTC", "0") == "1"
+# diagnostics only (the bound on what skipping the empty fallback tiers would
+# save; a bench line taken with it is not valid: the precision tiers are part
+# of the contract)
+FB_KW = {"fallback": False} if os.environ.get("W2L_BENCH_NOFB") == "1" else {}
 SIDE_PRIO = int(os.environ.get("W2L_BENCH_SIDE_PRIO", "0"))   # second stream's priority (A/B)
 
 
@@ -367,11 +371,11 @@ def main():
 
         def asg(**kw):
             return C.asg_loss_grad_batched(em_, el_, ta_, tl_, A_d, check=False, workspace=ws_a,
-                                           out=oa_, stream_grad=STREAM_ASG, **kw)
+                                           out=oa_, stream_grad=STREAM_ASG, **kw, **FB_KW)
 
         def ctc(**kw):
             return C.ctc_loss_grad_batched(em_, el_, tc_, tl_, blank, check=False, workspace=ws_c,
-                                           out=oc_, stream_grad=STREAM_CTC, **kw)
+                                           out=oc_, stream_grad=STREAM_CTC, **kw, **FB_KW)
 
         # The two criteria run concurrently on two streams (the chain CTAs of
         # both are co-resident: maximum shared-memory carveout).  Staggered

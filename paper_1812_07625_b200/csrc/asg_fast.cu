@@ -768,9 +768,9 @@ __global__ void __launch_bounds__(kFinalThreads)
   __shared__ int sperm[W2L_MAX_ASG_LABELS];   // token CSR
   __shared__ int sts[33];
   const int N = d.N, NN = N * N;
-  // ---- inputs and the prep kernel's token CSR first (the gradient writes
-  // none of them: they load while the gradient grid finishes)
-  const int L = tgt_len[b], T = em_len[b], LP = w.lpad;
+  // ---- inputs first (the gradient writes none of them: they load while the
+  // gradient grid finishes); the token CSR only exists for valid utterances
+  const int L = min(max(tgt_len[b], 0), d.Lmax), T = em_len[b], LP = w.lpad;
   const int64_t *y = tgt + (size_t)b * d.Lmax;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float am = -CUDART_INF_F;
@@ -778,11 +778,7 @@ __global__ void __launch_bounds__(kFinalThreads)
   am = warp_max(am);
   if (lane == 0) s_red[warp] = am;
   if (threadIdx.x == 0) s_bad = 0;
-  for (int l = threadIdx.x; l < L; l += blockDim.x) {
-    sy[l] = (int)y[l];
-    sperm[l] = w.perm[(size_t)b * w.lpad + l];
-  }
-  if (threadIdx.x <= N) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];   // N+1 written
+  for (int l = threadIdx.x; l < L; l += blockDim.x) sy[l] = (int)y[l];
   pdl_wait();
   if (threadIdx.x < 2 && w.prog) w.prog[2 * b + threadIdx.x] = 0;   // next tier / call
   const int st = status[b];
@@ -795,6 +791,8 @@ __global__ void __launch_bounds__(kFinalThreads)
     }
     return;
   }
+  for (int l = threadIdx.x; l < L; l += blockDim.x) sperm[l] = w.perm[(size_t)b * w.lpad + l];
+  if (threadIdx.x <= N) sts[threadIdx.x] = w.tok_start[b * 33 + threadIdx.x];   // N+1 written
   // ---- fixed-order sums of the per-frame-block partials: the fac
   // occupancies of the L states and the fcc edge sums of the N x N
   // transitions; each thread owns up to kFinalEnt of these entries and has
