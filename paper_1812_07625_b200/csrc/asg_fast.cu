@@ -251,7 +251,7 @@ __device__ void fcc_run(ChainSm<V> &sm, const FccCtx<V> &c, double *lnz) {
   const int pro_end = min(T, kBlk);
   for (int j = 1; j < pro_end; ++j) generic(j);
   const int nfull = T > kBlk ? (T - kBlk) / kBlk : 0;
-  const int mtrig = STREAM ? stream_trigger_block(T) : -1;   // (see lattice_run)
+  const int mtrig = STREAM ? stream_trigger_block<kFac>(T) : -1;   // (see lattice_run)
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
@@ -309,6 +309,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, 1 + weff, 0,
                d.N >= 32 ? 0xffffffffu : (1u << d.N) - 1u};
     pc.gprog = w.prog ? w.prog + 2 * b + (FWD ? 0 : 1) : nullptr;
+    pc.trig = stream_trigger_step<kFac>(T);
     producer_run<V>(sm, pc, lane, nullptr);
   } else if (warp == 1) {
     FccCtx<V> fc;
@@ -338,7 +339,7 @@ __device__ __forceinline__ void asg_chain_body(ChainSm<V> &sm, const float *em, 
     lat_init_weights<kFac, FWD, V>(f, c.w, lane, d.N, L, y, L, trans, amax, 0);
     lattice_run<kFac, FWD, V, STREAM>(sm, c, f);
   } else if (STREAM) {   // a warp without a role: its share of the trigger, at
-    wait_ge(&sm.cons[1], stream_trigger_step(T));   // lattice warp 0's midpoint
+    wait_ge(&sm.cons[1], stream_trigger_step<kFac>(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
   __syncthreads();

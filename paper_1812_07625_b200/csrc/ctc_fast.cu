@@ -38,6 +38,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
   if (warp == 0) {
     ProdCtx pc{em + (size_t)b * d.Tmax * d.N, d.N, T, FWD, weff, w.logits, tokmask};
     pc.gprog = w.prog ? w.prog + 2 * b + (FWD ? 0 : 1) : nullptr;
+    pc.trig = stream_trigger_step<kCtc>(T);
     producer_run<V>(sm, pc, lane, FWD ? w.scal + b * 4 + 2 : nullptr);
   } else if (warp - 1 < weff) {
     LatCtx c;
@@ -56,7 +57,7 @@ __device__ __forceinline__ void ctc_chain_body(ChainSm<V> &sm, const float *em, 
     lat_init_weights<kCtc, FWD, V>(f, c.w, lane, d.N, S, y, L, nullptr, 0.f, blank);
     lattice_run<kCtc, FWD, V, STREAM>(sm, c, f);
   } else if (STREAM) {   // a warp without a role: its share of the trigger, at
-    wait_ge(&sm.cons[0], stream_trigger_step(T));   // lattice warp 0's midpoint
+    wait_ge(&sm.cons[0], stream_trigger_step<kCtc>(T));   // lattice warp 0's midpoint
     pdl_launch_dependents();
   }
   __syncthreads();

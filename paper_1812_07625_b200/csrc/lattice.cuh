@@ -59,18 +59,29 @@ constexpr int kBlk = 8;                    // steps per unrolled block (one publ
 
 // Streamed gradient: a chain warp triggers the dependent launch once its
 // steps reach stream_trigger_step(T) = ceil(T NUM / DIV) (the midpoint), i.e.
-// after the block of kBlk steps stream_trigger_block(T)
-#ifndef W2L_TRIG_NUM
-#define W2L_TRIG_NUM 1
+// after the block of kBlk steps stream_trigger_block(T).  Per lattice kind
+// (A/B builds: W2L_TRIG_{FAC,CTC}_{NUM,DIV}; the fac fraction also serves
+// ASG's fcc warp).
+#ifndef W2L_TRIG_FAC_NUM
+#define W2L_TRIG_FAC_NUM 1
 #endif
-#ifndef W2L_TRIG_DIV
-#define W2L_TRIG_DIV 2
+#ifndef W2L_TRIG_FAC_DIV
+#define W2L_TRIG_FAC_DIV 2
 #endif
+#ifndef W2L_TRIG_CTC_NUM
+#define W2L_TRIG_CTC_NUM 1
+#endif
+#ifndef W2L_TRIG_CTC_DIV
+#define W2L_TRIG_CTC_DIV 2
+#endif
+template <int KIND>   // 0: fac (ASG), 1: CTC
 __host__ __device__ __forceinline__ int stream_trigger_step(int T) {
-  return (T * W2L_TRIG_NUM + W2L_TRIG_DIV - 1) / W2L_TRIG_DIV;
+  return KIND == 0 ? (T * W2L_TRIG_FAC_NUM + W2L_TRIG_FAC_DIV - 1) / W2L_TRIG_FAC_DIV
+                   : (T * W2L_TRIG_CTC_NUM + W2L_TRIG_CTC_DIV - 1) / W2L_TRIG_CTC_DIV;
 }
+template <int KIND>
 __device__ __forceinline__ int stream_trigger_block(int T) {
-  return max(1, (stream_trigger_step(T) + kBlk - 1) / kBlk - 1);
+  return max(1, (stream_trigger_step<KIND>(T) + kBlk - 1) / kBlk - 1);
 }
 
 constexpr int kProdStages = 4;             // emission chunks in flight (hides HBM latency)
@@ -221,6 +232,7 @@ struct ProdCtx {
   int logits;      // shift term: 0 = max_i e (log-probs), 1 = -log sum_i Et (logits)
   unsigned tokmask;  // tokens whose Et enter the recursions (flush check)
   int *gprog = nullptr;  // global progress word of this (utterance, direction), or null
+  int trig = 0;          // streamed gradient: the step at which to trigger the launch
 };
 
 // Publish the CTA's progress (steps whose rows every row-writing warp has
@@ -334,7 +346,7 @@ __device__ __forceinline__ void producer_run(ChainSm<V> &sm, const ProdCtx &c, i
     __syncwarp();   // raw[ch % kProdStages] is refilled by a later issue
     publish(&sm.prod, p0 + rows, lane);
     if (c.gprog && lane == 0) prod_publish(sm, c, published);
-    if (c.gprog && !trig && p0 + rows >= stream_trigger_step(c.T)) {
+    if (c.gprog && !trig && p0 + rows >= c.trig) {
       pdl_launch_dependents();   // (see lattice_run)
       trig = true;
     }
@@ -627,7 +639,7 @@ __device__ void lattice_run(ChainSm<V> &sm, const LatCtx &c, LatState<V> &f) {
   // warp of every chain CTA has passed the middle of its utterance, when
   // the first frames have both their rows -- its CTAs then do not hold SMs
   // while there is nothing to do (another criterion's kernels need them).
-  const int mtrig = STREAM ? stream_trigger_block(T) : -1;
+  const int mtrig = STREAM ? stream_trigger_block<KIND>(T) : -1;
 #pragma unroll 1
   for (int m = 1; m <= nfull; ++m) {
     const int j0 = m * kBlk;
