@@ -9,8 +9,8 @@
 // lane's 8 sources, 2 across lanes by shuffles); emissions are staged in
 // shared memory 32 frames at a time (cp.async, double buffered); the previous frame's dp vector is broadcast through shared
 // memory (double buffered, one CTA barrier per frame); backpointers are
-// uint8 in shared memory when T*N fits, else in the workspace; thread 0
-// traces back.
+// uint8 in shared memory when T*N fits, else in the workspace; the traceback
+// runs in chunks on all threads.
 
 #include "common.cuh"
 #include "kernels.h"
@@ -70,11 +70,19 @@ __device__ __forceinline__ void vit_issue_chunk(const TE *__restrict__ e, int T,
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
+// traceback chunk length: 32 frames, longer for long utterances so that the
+// chunk maps ((T / lc) * N bytes) stay within kTraceMapMax
+constexpr int kTraceMapMax = 8192;
+__host__ __device__ inline int vit_trace_chunk(int T) {
+  return max(32, (T * 32 + kTraceMapMax - 1) / kTraceMapMax);
+}
+
 template <class TE, bool kSmemBack, bool kNanAware>
 __device__ __forceinline__ void viterbi4_body(const TE *__restrict__ e, int T, int N,
                                               const double (&arow)[8], double (*dp_buf)[32],
                                               TE *ebuf, uint8_t *back, double *score_out,
-                                              int64_t *path_out) {
+                                              int64_t *path_out, uint8_t *tmap,
+                                              uint8_t *tend_state) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = warp * 8 + (lane >> 2), q = lane & 3;
   const bool owner = q == 0 && d < N;   // writes dp'[d] and back[t][d]
@@ -145,6 +153,40 @@ __device__ __forceinline__ void viterbi4_body(const TE *__restrict__ e, int T, i
       __syncthreads();
     }
   }
+  // ---- traceback in chunks of lc frames (vit_trace_chunk), all threads:
+  // (1) for every chunk c >= 1 and every state s at its last frame, the state
+  //     one frame before the chunk (map[c][s]); 4 walks interleaved per
+  //     thread, so 4 dependent backpointer loads are in flight at a time
+  // (2) thread 0 picks the best final state (first maximum, NaN wins) and
+  //     chains the maps from the last chunk down: the end state of each chunk
+  // (3) each chunk walks back from its end state writing its path frames
+  // Serially, thread 0 spent ~35 cycles per frame on the dependent loads.
+  const int lc = vit_trace_chunk(T);
+  const int ntc = (T + lc - 1) / lc;
+  const int nw = (ntc - 1) * N;   // walks of phase 1
+  auto bk = [&](int t, int st) -> int {
+    return (int)back[(size_t)t * N + st];   // (written by this CTA: no read-only path)
+  };
+  for (int w0 = threadIdx.x * 4; w0 < nw; w0 += blockDim.x * 4) {
+    int cur[4], lo[4], hi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int w = min(w0 + k, nw - 1);
+      const int c = 1 + w / N;
+      cur[k] = w % N;
+      lo[k] = c * lc;
+      hi[k] = min(T, (c + 1) * lc) - 1;
+    }
+    for (int j = 0; j < lc; ++j) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (hi[k] - j >= lo[k]) cur[k] = bk(hi[k] - j, cur[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (w0 + k < nw) tmap[w0 + k] = (uint8_t)cur[k];   // map[c][s] at (c - 1) * N + s
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     const double *fin = dp_buf[(T - 1) & 1];
     int best_i = 0;
@@ -156,9 +198,19 @@ __device__ __forceinline__ void viterbi4_body(const TE *__restrict__ e, int T, i
       }
     *score_out = bv;
     int cur = best_i;
-    path_out[T - 1] = cur;
-    for (int t = T - 1; t > 0; --t) {
-      cur = back[(size_t)t * N + cur];
+    for (int c = ntc - 1; c >= 1; --c) {
+      tend_state[c] = (uint8_t)cur;
+      cur = tmap[(c - 1) * N + cur];
+    }
+    tend_state[0] = (uint8_t)cur;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ntc; c += blockDim.x) {
+    const int lo = c * lc, hi = min(T, (c + 1) * lc) - 1;
+    int cur = tend_state[c];
+    path_out[hi] = cur;
+    for (int t = hi; t > lo; --t) {
+      cur = bk(t, cur);
       path_out[t - 1] = cur;
     }
   }
@@ -175,6 +227,8 @@ __global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(16) double dp_buf[2][32];
   __shared__ __align__(16) TE ebuf[2 * kVitChunk * 32];
+  __shared__ uint8_t tmap[kTraceMapMax];        // traceback chunk maps (viterbi4_body)
+  __shared__ uint8_t tend_state[kTraceMapMax / 32 + 1];
   pdl_wait();   // a programmatic dependent of the validation kernels
   const int b = blockIdx.x, N = d.N;
   int64_t *pb = path + (size_t)b * d.Tmax;
@@ -199,9 +253,11 @@ __global__ void __launch_bounds__(128) viterbi4_kernel(const TE *__restrict__ em
   // sources j >= N: dp = -inf makes them lose; A may hold inf/NaN (not
   // validated by the reference, :270-272) -- only then the NaN-aware compare
   if (__syncthreads_and(finite))
-    viterbi4_body<TE, kSmemBack, false>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb);
+    viterbi4_body<TE, kSmemBack, false>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb, tmap,
+                                        tend_state);
   else
-    viterbi4_body<TE, kSmemBack, true>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb);
+    viterbi4_body<TE, kSmemBack, true>(e, T, N, arow, dp_buf, ebuf, back, score + b, pb, tmap,
+                                       tend_state);
   for (int t = T + threadIdx.x; t < d.Tmax; t += blockDim.x) pb[t] = 0;
 }
 
