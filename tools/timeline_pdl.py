@@ -104,6 +104,8 @@ if loops:   # keep the last step: records after its first chain start
     gaps = np.nonzero(np.diff(cs) > 150000)[0]   # steps are > 150 us apart
     t_last = cs[gaps[-1] + 1] if len(gaps) else cs[0]
     recs = recs[recs[:, 1].astype(np.int64) >= t_last - 20000]
+if os.environ.get("TL_DUMP"):   # raw records for offline analysis
+    np.save(os.environ["TL_DUMP"], recs)
 tag = recs[:, 0].astype(np.int64)
 kind = tag // 1000000
 t = recs[:, 1:].astype(np.int64)
