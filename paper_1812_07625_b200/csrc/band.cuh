@@ -219,10 +219,13 @@ struct BandPf {
 constexpr float kFixScale = 0x1p30f;
 constexpr float kFixInv = 0x1p-30f;
 constexpr int kTokWords = kSpl / 4;   // token words per lane block (4 bytes each)
+// kOddOnly: only the odd states of a block carry labels (CTC: the even ones
+// are blanks), so only they are scattered.
+template <bool kOddOnly = false>
 __device__ __forceinline__ void band_scatter(const float (&q)[kSpl], float inv, const unsigned *tok,
                                              unsigned *bins) {
 #pragma unroll
-  for (int k = 0; k < kSpl; ++k) {
+  for (int k = kOddOnly ? 1 : 0; k < kSpl; k += kOddOnly ? 2 : 1) {
     const unsigned tk = (tok[k >> 2] >> (8 * (k & 3))) & 0xffu;
     if (tk != 0xffu && q[k] > 0.f) atomicAdd(bins + tk, __float2uint_rn(q[k] * inv * kFixScale));
   }

@@ -263,12 +263,12 @@ __global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
     l2max = fmaxf(l2max, l2);
     // label posteriors into the token bins
     if (clo + lane <= chi && clo + lane < br.nblk)
-      band_scatter(q0, inv, stok + (clo + lane) * kTokWords, mybins);
+      band_scatter<true>(q0, inv, stok + (clo + lane) * kTokWords, mybins);
     for (int m = clo + lane + 32; m <= chi; m += 32) {
       if (m < br.nblk) {
         float q[kSpl];
         ldv(myp + m * kSpl, q);
-        band_scatter(q, inv, stok + m * kTokWords, mybins);
+        band_scatter<true>(q, inv, stok + m * kTokWords, mybins);
       }
     }
     float sm_k = 0.f;
