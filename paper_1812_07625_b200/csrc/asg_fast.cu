@@ -408,7 +408,9 @@ __host__ __device__ constexpr size_t fcc_stage_bytes() {
   return (((size_t)(kFccFpw + 1) * 32 + (size_t)kFccFpw * 32) * sizeof(V) +
           (size_t)kFccFpw * 32 * 4 + (size_t)(2 * kFccFpw + 1) * 4 + 15) & ~(size_t)15;
 }
-static_assert(fcc_stage_bytes<float>() >= 4096, "the staging area doubles as the reduction buffer");
+constexpr int kRedStride = 33;   // padded row of the fcc body's per-warp [32][32] partial
+static_assert(fcc_stage_bytes<float>() >= 32 * kRedStride * sizeof(float),
+              "the staging area doubles as the reduction buffer");
 
 // fcc edge posteriors and the fcc guard (the fcc node posteriors are formed
 // by the fac body, which writes the whole gradient row)
@@ -506,16 +508,19 @@ __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
     }
   }
   __syncwarp();
-  float *red = reinterpret_cast<float *>(st);   // this warp's partial [32][32]
+  // this warp's partial [32][32], rows padded to kRedStride floats so that the
+  // 32 lanes' stores of one column hit 32 different banks (an unpadded row of
+  // 32 floats put every lane on the same bank)
+  float *red = reinterpret_cast<float *>(st);
   if constexpr (sizeof(V) == 4) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      red[lane * 32 + 2 * j] = f2_lo(accA[j]);
-      red[lane * 32 + 2 * j + 1] = f2_hi(accA[j]);
+      red[lane * kRedStride + 2 * j] = f2_lo(accA[j]);
+      red[lane * kRedStride + 2 * j + 1] = f2_hi(accA[j]);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) red[lane * 32 + j] = (float)accD[j];
+    for (int j = 0; j < 32; ++j) red[lane * kRedStride + j] = (float)accD[j];
   }
   if (lane == 0) {
     gwarp[warp][0] = gmin;
@@ -525,8 +530,9 @@ __device__ __forceinline__ void asg_fcc_grad_body(const float *__restrict__ em,
   float *dstA = w.part_fullA + ((size_t)b * w.nblk + blk) * 1024;
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
     float s = 0.f;
+    const int ri = (i >> 5) * kRedStride + (i & 31);
     for (int q = 0; q < kGradWarps; ++q)
-      s += reinterpret_cast<const float *>(smem + q * fcc_stage_bytes<V>())[i];
+      s += reinterpret_cast<const float *>(smem + q * fcc_stage_bytes<V>())[ri];
     dstA[i] = s;
   }
   if (threadIdx.x < 2) {
