@@ -40,7 +40,10 @@
 namespace w2l {
 namespace {
 
-constexpr int kGradFramesPerBlock = 128;   // frames per gradient CTA (both bodies)
+#ifndef W2L_ASG_GRAD_FRAMES
+#define W2L_ASG_GRAD_FRAMES 128
+#endif
+constexpr int kGradFramesPerBlock = W2L_ASG_GRAD_FRAMES;   // frames per gradient CTA (both bodies)
 constexpr int kFccFrames = kGradFramesPerBlock;
 constexpr int kGradWarps = 8;
 // asg_final: one CTA per utterance (launched as a programmatic dependent
@@ -403,12 +406,15 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 // including frame ta-1, beta), exponents and emission rows come in with one
 // cp.async batch.  Reused for the block reduction.
 constexpr int kFccFpw = kFccFrames / kGradWarps;            // 16 frames per warp
+constexpr int kRedStride = 33;   // padded row of the fcc body's per-warp [32][32] partial
 template <class V>
 __host__ __device__ constexpr size_t fcc_stage_bytes() {
-  return (((size_t)(kFccFpw + 1) * 32 + (size_t)kFccFpw * 32) * sizeof(V) +
-          (size_t)kFccFpw * 32 * 4 + (size_t)(2 * kFccFpw + 1) * 4 + 15) & ~(size_t)15;
+  const size_t stage = (((size_t)(kFccFpw + 1) * 32 + (size_t)kFccFpw * 32) * sizeof(V) +
+                        (size_t)kFccFpw * 32 * 4 + (size_t)(2 * kFccFpw + 1) * 4 + 15) &
+                       ~(size_t)15;
+  const size_t red = (32 * kRedStride * sizeof(float) + 15) & ~(size_t)15;
+  return stage > red ? stage : red;
 }
-constexpr int kRedStride = 33;   // padded row of the fcc body's per-warp [32][32] partial
 static_assert(fcc_stage_bytes<float>() >= 32 * kRedStride * sizeof(float),
               "the staging area doubles as the reduction buffer");
 

@@ -114,7 +114,10 @@ __global__ void __launch_bounds__(32 * (1 + kMaxLatWarps))
   W2L_TL(if (threadIdx.x == 0) tl_rec(1000000ull + b * 10 + blockIdx.y, tl0, gtimer(), smid() | (hw_warpid() << 16)));
 }
 
-constexpr int kGradFramesPerBlock = 128;
+#ifndef W2L_CTC_GRAD_FRAMES
+#define W2L_CTC_GRAD_FRAMES 128
+#endif
+constexpr int kGradFramesPerBlock = W2L_CTC_GRAD_FRAMES;   // frames per gradient CTA
 constexpr int kGradWarps = 8;
 
 // One warp per frame at a time; lane i owns states 128 sw + 4 i + k of every
