@@ -4,6 +4,8 @@
 
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,6 +25,14 @@ inline int from_cuda(cudaError_t e) {
   g_last_cuda = e;
   return W2L_ERR_CUDA;
 }
+
+// An NVTX range around each entry point's launch sequence (the enqueue, on
+// the host timeline; ncu --nvtx-include / nsys group the kernels by it).
+// Header-only NVTX3: without an attached tool a push/pop is a null check.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 bool dims_ok(int B, int Tmax, int N, int Lmax, int max_l) {
   return B >= 0 && Tmax >= 1 && N >= 1 && N <= W2L_MAX_TOKENS && Lmax >= 0 && Lmax <= max_l;
@@ -134,6 +144,7 @@ static int asg_run(const float *em, const int32_t *em_len, const int64_t *tgt,
                    double *loss, float *grad_em, float *grad_trans, float *grad_trans_utt,
                    int32_t *status, void *ws, size_t ws_bytes, unsigned flags,
                    cudaStream_t s, Tracer *tr) {
+  NvtxRange nv("w2l_asg_loss_grad");
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) {
     // an empty shard contributes a zero transition gradient (trainer.py:433
@@ -261,6 +272,7 @@ int w2l_asg_loss_grad_f64(const double *em, const int32_t *em_len, const int64_t
                           int N, int Lmax, double *loss, float *grad_em, float *grad_trans,
                           float *grad_trans_utt, int32_t *status, void *ws, size_t ws_bytes,
                           w2l_stream_t stream) {
+  NvtxRange nv("w2l_asg_loss_grad_f64");
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_ASG_LABELS)) return W2L_ERR_CONTRACT;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0)
@@ -314,6 +326,7 @@ static int ctc_run(const float *logp, const int32_t *em_len, const int64_t *tgt,
                    const int32_t *tgt_len, int blank, int B, int Tmax, int N, int Lmax,
                    double *loss, float *grad_em, int32_t *status, void *ws, size_t ws_bytes,
                    unsigned flags, cudaStream_t s, Tracer *tr) {
+  NvtxRange nv("w2l_ctc_loss_grad");
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
@@ -400,6 +413,7 @@ int w2l_ctc_loss_grad_f64(const double *logp, const int32_t *em_len, const int64
                           const int32_t *tgt_len, int blank, int B, int Tmax, int N,
                           int Lmax, double *loss, float *grad_em, int32_t *status, void *ws,
                           size_t ws_bytes, w2l_stream_t stream) {
+  NvtxRange nv("w2l_ctc_loss_grad_f64");
   if (!dims_ok(B, Tmax, N, Lmax, W2L_MAX_CTC_LABELS)) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!logp || !em_len || !tgt || !tgt_len || !loss || !grad_em || !status || !ws)
@@ -429,6 +443,7 @@ size_t w2l_viterbi_workspace_bytes(int B, int Tmax, int N) {
 int w2l_viterbi(const float *em, const int32_t *em_len, const float *trans, int B, int Tmax,
                 int N, int64_t *path, double *score, int32_t *status, void *ws,
                 size_t ws_bytes, w2l_stream_t stream) {
+  NvtxRange nv("w2l_viterbi");
   if (B < 0 || Tmax < 1 || N < 1 || N > W2L_MAX_TOKENS) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!em || !em_len || !path || !score || !status) return W2L_ERR_CONTRACT;
@@ -444,6 +459,7 @@ int w2l_viterbi(const float *em, const int32_t *em_len, const float *trans, int 
 int w2l_viterbi_f64(const double *em, const int32_t *em_len, const double *trans, int B,
                     int Tmax, int N, int64_t *path, double *score, int32_t *status, void *ws,
                     size_t ws_bytes, w2l_stream_t stream) {
+  NvtxRange nv("w2l_viterbi_f64");
   if (B < 0 || Tmax < 1 || N < 1 || N > W2L_MAX_TOKENS) return W2L_ERR_CONTRACT;
   if (B == 0) return W2L_OK;
   if (!em || !em_len || !path || !score || !status) return W2L_ERR_CONTRACT;
@@ -462,6 +478,7 @@ int w2l_greedy_eval(const int64_t *path, const int32_t *path_len, int B, int Tma
                     int silence, int64_t *hyp, int32_t *hyp_len, int32_t *tok_dist,
                     int32_t *word_dist, int32_t *ref_words, int32_t *status,
                     w2l_stream_t stream) {
+  NvtxRange nv("w2l_greedy_eval");
   if (B < 0 || Tmax < 1 || Lmax < 0 || (kind != 0 && kind != 1) || (kind == 1 && special < 0))
     return W2L_ERR_CONTRACT;
   if (greedy_eval_smem_bytes(Tmax, Lmax) > 227 * 1024) return W2L_ERR_CONTRACT;
@@ -476,6 +493,7 @@ int w2l_greedy_eval(const int64_t *path, const int32_t *path_len, int B, int Tma
 
 int w2l_transitions_sgd_step(float *trans, float *velocity, const float *grad_sum, int N,
                              int batch_size, float lr, float momentum, w2l_stream_t stream) {
+  NvtxRange nv("w2l_transitions_sgd_step");
   if (N < 1 || N > W2L_MAX_TOKENS || batch_size < 1 || !trans || !velocity || !grad_sum)
     return W2L_ERR_CONTRACT;
   return from_cuda(launch_transitions_sgd(trans, velocity, grad_sum, N, batch_size, lr, momentum,

@@ -10,3 +10,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
   -k regex:"(chain_kernel<float|grad_kernel<[^>]*, float)" -s 4 -c 4 -o gpurun_out/full python tools/prof_chain.py all > gpurun_out/full.log 2>&1
 tail -2 gpurun_out/full.log
+# the kernels one criterion call enqueues, grouped by the C-ABI's NVTX range
+timeout 600 ncu --nvtx --nvtx-include "w2l_ctc_loss_grad/" --metrics gpu__time_duration.sum \
+  --clock-control none --csv python tools/prof_chain.py ctc > gpurun_out/nvtx_ctc.csv 2> gpurun_out/nvtx_ctc.err
