@@ -1,10 +1,10 @@
 """Chain-stage time vs lattice width (lattice warps W = ceil((2L+1)/128)) at B=64 T=1600."""
 import sys, torch
 sys.path.insert(0, ".")
-from oracle import criterion_oracle as orc
+import bench
 from paper_1812_07625_b200 import criterion as C
 for L in (20, 60, 120, 180, 240, 300):
-    em, el, tg, tl, blank = orc.synth_ctc(20260004, 64, 1600, 30, L)
+    em, el, _, tg, tl, _, blank = bench.make_inputs(0, l=L)
     d = torch.from_numpy(em).cuda()
     best = 1e9
     for _ in range(4):
