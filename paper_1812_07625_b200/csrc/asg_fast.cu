@@ -924,8 +924,15 @@ __global__ void asg_loss_only_kernel(const int32_t *__restrict__ em_len, Dims d,
 // block's completion rank (block_of_rank), so with PDL the CTAs run in the
 // order the two chains complete their frames; prog (null: the chains have
 // finished) gates them.
+// fp32 gradient CTAs per SM the registers must allow (W <= 3): 4 (64
+// registers, no spills) against 3 (79): asg grad 100 -> 96 us, two-criteria
+// step 0.426 -> 0.418 ms (5 of 5 A/B pairs)
+#ifndef W2L_ASG_GRAD_MINB
+#define W2L_ASG_GRAD_MINB 4
+#endif
 template <int W, class V>
-__global__ void __launch_bounds__(kGradWarps * 32, W <= 3 ? (sizeof(V) == 4 ? 3 : 2) : 1)
+__global__ void __launch_bounds__(kGradWarps * 32,
+                                  W <= 3 ? (sizeof(V) == 4 ? W2L_ASG_GRAD_MINB : 2) : 1)
     asg_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     const float *__restrict__ trans, Dims d, AsgFastWs w,

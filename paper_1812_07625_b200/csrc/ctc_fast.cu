@@ -129,8 +129,13 @@ constexpr int kGradWarps = 8;
 // and are read as zero.  Grid (B, nblk): y is the block's completion rank
 // (block_of_rank), so with PDL the CTAs run in the order the two chains
 // complete their frames; prog (null: the chains have finished) gates them.
+// fp32 gradient CTAs per SM the registers must allow; shared memory (~52 KB
+// per CTA) caps residency at 4 anyway (5: 48 registers, step 0.431 vs 0.424 ms)
+#ifndef W2L_CTC_GRAD_MINB
+#define W2L_CTC_GRAD_MINB 4
+#endif
 template <int W, class V>
-__global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? 4 : 1)
+__global__ void __launch_bounds__(kGradWarps * 32, sizeof(V) == 4 ? W2L_CTC_GRAD_MINB : 1)
     ctc_grad_kernel(const float *__restrict__ em, const int32_t *__restrict__ em_len,
                     const int64_t *__restrict__ tgt, const int32_t *__restrict__ tgt_len,
                     int blank, Dims d, CtcFastWs w, float *__restrict__ grad_em,
