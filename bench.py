@@ -47,7 +47,7 @@ REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 STAGGER = os.environ.get("W2L_BENCH_STAGGER", "1") != "0"
 FIRST = os.environ.get("W2L_BENCH_FIRST", "asg")
 STREAM_ASG = os.environ.get("W2L_BENCH_STREAM_ASG", "1") != "0"
-STREAM_CTC = os.environ.get("W2L_BENCH_STREAM_CTC", "0") == "1"
+STREAM_CTC = os.environ.get("W2L_BENCH_STREAM_CTC", "1") != "0"
 # diagnostics only (the bound on what skipping the empty fallback tiers would
 # save; a bench line taken with it is not valid: the precision tiers are part
 # of the contract)
@@ -390,7 +390,9 @@ def main():
         # together, the two chains sharing each SM fall into a slow mode on
         # about two thirds of the steps (per-step device times 0.49 vs
         # 0.53-0.58 ms, tools/step_times.py).  ASG (the longer chains) goes
-        # first, and streams its gradient behind its chains.
+        # first.  Both stream their gradients behind their chains (CTC's too
+        # since the ASG gradient runs 4 CTAs per SM: device step -2..-4%,
+        # e2e equal, 8 A/B pairs on two boxes).
         first, second = (asg, ctc) if FIRST == "asg" else (ctc, asg)
         side.wait_stream(main_s)
         if STAGGER:
